@@ -1,0 +1,407 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 dppix pixelization path (BASELINE.json metric).
+
+Default workload (BASELINE.json configs[1]): region-adaptive DP pixelization,
+b=16, n=4, m=16, eps=0.5, u8 fg/bg mask, a 600-frame synthetic 1920x1080 RGB
+clip per GPU (weak scaling: each rank owns its own 600 frames, global frame
+indices rank*600 + i, so the noise streams never repeat across ranks).
+
+  value  -- device-resident: frames, masks and outputs live in HBM when the
+            timed region starts; one step = K0 + K1 over the whole clip
+            (classification, statistics, keyed Laplace noise, compact DPPX
+            payloads, full reconstructed image). MP/s over all ranks.
+  e2e    -- the same metric through the public host API dppx_pixelize_adaptive
+            with pinned HOST buffers: every step copies that step's frames and
+            masks H2D and reads payloads + reconstructed image back D2H.
+  roofline   -- K1 (k_stats_tma), algorithmic bytes / CUDA-event duration.
+  cpu_baseline -- the reference (oracle/_ref, compiled from /root/reference
+            sources) timed on this host on a bounded sample, rank 0 only.
+
+`--impl reference` times only the reference CPU implementation (rank 0).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "megapixels/sec and 1080p frames/sec (adaptive DP pixelization); % of HBM roofline"
+
+WORKLOADS = {
+    # name: (M, N, C, frames_per_gpu, b, n, m, eps, adaptive, description)
+    "venice": (1080, 1920, 3, 600, 16, 4, 16, 0.5, True,
+               "region-adaptive DP pixelization with fg/bg mask, 600-frame synthetic "
+               "1920x1080 RGB clip (Venice-2 shape), b=16 n=4 m=16 eps=0.5"),
+    "pets": (576, 768, 3, 1, 16, 1, 16, 0.5, False,
+             "uniform DP pixelization b=16 m=16 eps=0.5, one 768x576 RGB frame (PETS shape)"),
+    "4k": (2160, 3840, 3, 64, 32, 8, 16, 0.5, True,
+           "region-adaptive b=32 n=8 on synthetic 3840x2160 RGB images with compact store + "
+           "reconstruction"),
+    "celeba": (218, 178, 3, 100000, 16, 1, 16, 0.5, False,
+               "uniform b=16 on a 100k-image batch of 178x218 RGB faces (CelebA shape)"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="venice")
+    ap.add_argument("--frames", type=int, default=0, help="override frames per GPU")
+    ap.add_argument("--e2e-frames", type=int, default=120)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="target CPU-work seconds for the reference sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        sm = [int(s[0]) for s in self.samples if s and s[0].isdigit()]
+        mx = [int(s[1]) for s in self.samples if len(s) > 1 and s[1].isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(workload):
+    """dram read+write bytes per K1 launch from a committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(workload)
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------
+# reference CPU arm (oracle/_ref = the reference compiled from its sources)
+# ----------------------------------------------------------------------------
+def cpu_reference_sample(M, N, C, b, n, m, eps, adaptive, seconds, frame0=0):
+    import numpy as np
+
+    import oracle
+    if oracle.ref is None:
+        return None
+    workers = os.cpu_count() or 1
+    one = oracle.synth_frames(frame0, 1, M, N, C)[0]
+    mask1 = oracle.synth_masks(frame0, 1, M, N)
+    planes1 = np.ascontiguousarray(one.transpose(2, 0, 1))
+    t = oracle.ref.time_planes(planes1[:1], mask1, not adaptive, eps, m, b, n, 42, 1)
+    per_plane = max(t, 1e-5)
+    n_planes = int(max(C, min(3 * 600, seconds / per_plane)))
+    n_frames = max(1, n_planes // C)
+    frames = oracle.synth_frames(frame0, n_frames, M, N, C)
+    masks = oracle.synth_masks(frame0, n_frames, M, N)
+    # colour planes are de-interleaved upstream, untimed
+    planes = np.ascontiguousarray(frames.transpose(0, 3, 1, 2)).reshape(n_frames * C, M, N)
+    pmasks = np.repeat(masks, C, axis=0) if adaptive else None
+    return dict(planes=planes, masks=pmasks, n_frames=n_frames, workers=workers)
+
+
+def run_reference_once(sample, M, N, C, b, n, m, eps, adaptive):
+    import oracle
+    return oracle.ref.time_planes(sample["planes"], sample["masks"], not adaptive, eps, m, b, n,
+                                  42, sample["workers"])
+
+
+def reference_arm(args, wl):
+    M, N, C, F, b, n, m, eps, adaptive, desc = wl
+    import oracle
+    if oracle.ref is None:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref/libdppix_ref.so not built (needs /root/reference)"}))
+        return
+    per_step = max(2.0, min(args.cpu_seconds, 20.0))
+    sample = cpu_reference_sample(M, N, C, b, n, m, eps, adaptive, per_step)
+    for _ in range(args.warmup):
+        run_reference_once(sample, M, N, C, b, n, m, eps, adaptive)
+    times = [run_reference_once(sample, M, N, C, b, n, m, eps, adaptive) for _ in range(args.steps)]
+    t = sum(times) / len(times)
+    mp = sample["n_frames"] * M * N / 1e6
+    value = mp / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "MP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "frames_per_sec": round(sample["n_frames"] / t, 3),
+        "config": {"workload": desc, "sample_frames": sample["n_frames"],
+                   "shape": f"{N}x{M}x{C}"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "MP/s", "cores": sample["workers"],
+                         "kind": "reference",
+                         "sample": f"{sample['n_frames']} frames x {C} planes of the workload, "
+                                   f"pixelize_{'adaptive' if adaptive else 'parallel'} per plane "
+                                   f"(threads=1), frame-parallel over {sample['workers']} threads "
+                                   "(run_batch scheme, cli.cpp:175-213)"},
+        "e2e": {"value": round(value, 3), "unit": "MP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ----------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    wl = WORKLOADS[args.workload]
+    M, N, C, F, b, n, m, eps, adaptive, desc = wl
+    if args.frames:
+        F = args.frames
+
+    if args.impl == "reference":
+        if rank == 0:
+            reference_arm(args, wl)
+        return
+
+    import numpy as np
+    import torch
+
+    import paper_2511_04261_b200 as dp
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", device_id=dev)
+        pg = tdist
+
+    def barrier():
+        if pg:
+            pg.barrier()
+        torch.cuda.synchronize()
+
+    def allmax(x):
+        if not pg:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        return float(t.item())
+
+    ctx = dp.Context(local)
+    geom = dp.grid_dims(M, N, b)
+    G = geom.grid_count()
+    p = dp.make_privacy_params(eps, m, b, n)
+    pitch = ((N * C + 15) // 16) * 16
+    mpitch = ((N + 15) // 16) * 16
+    d = dp._desc(M, N, C, F, pitch=pitch, mpitch=mpitch, opitch=pitch)
+    frame0 = rank * F
+    img = torch.empty((F, M, pitch), dtype=torch.uint8, device=dev)
+    out = torch.empty_like(img)
+    mask = torch.empty((F, M, mpitch), dtype=torch.uint8, device=dev) if adaptive else None
+    ctx.synth_frames_dev(d, 101, frame0, img, mask)
+    if adaptive:
+        cap = dp.adaptive_payload_capacity(M, N, b, n)
+        sstride = (cap + 15) // 16 * 16
+    else:
+        sstride = G
+    stats = torch.zeros((F * C, sstride), dtype=torch.uint8, device=dev)
+    lens = torch.zeros(F * C, dtype=torch.int32, device=dev)
+    seeds = dp.plane_seeds(42, F, C, frame0=frame0)
+    nz, keep = dp.Context._noise(dp.NOISE_KEYED, seeds)
+
+    def step():
+        if adaptive:
+            ctx.pixelize_adaptive_dev(d, img, mask, p, nz, stats, sstride, lens, out)
+        else:
+            ctx.pixelize_uniform_dev(d, img, p, nz, stats, out)
+
+    for _ in range(args.warmup):
+        step()
+    ctx.synchronize()
+    # payload bytes actually written (for the roofline's algorithmic bytes)
+    payload_bytes = int(lens.sum().item()) if adaptive else F * C * G
+    # ---- timed region: device-resident ----
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    ctx.reset_stats()
+    ctx.set_timing(True)
+    barrier()
+    with ClockSampler(local) as clk:
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        ev1.synchronize()
+    barrier()
+    ms_total = ev0.elapsed_time(ev1)
+    st = ctx.stats()
+    ctx.set_timing(False)
+    ms_step = allmax(ms_total / args.steps)
+    frames_total = F * world
+    value = frames_total * M * N / 1e6 / (ms_step / 1e3)
+    fps = frames_total / (ms_step / 1e3)
+    # roofline of K1 (dominant kernel): algorithmic bytes / measured duration
+    kfam = "stats_tma" if st["launches"]["stats_tma"] else "stats_generic"
+    k1_launches = max(1, st["launches"][kfam])
+    k1_ms = st["device_ms"][kfam] / k1_launches
+    k1_bytes = F * M * N * C * 2 + payload_bytes  # read frame, write image, write stats
+    k0_bytes = (F * M * N + 4 * G * C * F + 4 * F * C) if adaptive else 0
+    peak, peak_src = measured_peak()
+    achieved = k1_bytes / (k1_ms / 1e3) / 1e9
+    step_gbs = (k1_bytes + k0_bytes) / (ms_total / args.steps / 1e3) / 1e9
+    traffic = ncu_traffic(args.workload)
+    launches_timed = sum(st["launches"].values())
+
+    # ---- e2e: public host API, pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        Fe = min(F, args.e2e_frames)
+        hbytes = Fe * M * N * C
+        h_img = torch.empty((Fe, M, N, C), dtype=torch.uint8).pin_memory()
+        h_img.copy_(img[:Fe, :, : N * C].reshape(Fe, M, N, C).cpu())
+        h_mask = None
+        if adaptive:
+            h_mask = torch.empty((Fe, M, N), dtype=torch.uint8).pin_memory()
+            h_mask.copy_(mask[:Fe, :, :N].cpu())
+        h_out = torch.empty((Fe, M, N, C), dtype=torch.uint8).pin_memory()
+        h_stats = torch.zeros((Fe * C, sstride), dtype=torch.uint8).pin_memory()
+        h_lens = torch.zeros(Fe * C, dtype=torch.int32).pin_memory()
+        de = dp._desc(M, N, C, Fe)
+        seeds_e = dp.plane_seeds(42, Fe, C, frame0=frame0)
+        nze, keep_e = dp.Context._noise(dp.NOISE_KEYED, seeds_e)
+        import ctypes as Ct
+
+        def e2e_step():
+            if adaptive:
+                rc = dp._lib.dppx_pixelize_adaptive(ctx._h, Ct.byref(de), h_img.data_ptr(),
+                                                    h_mask.data_ptr(), Ct.byref(p), Ct.byref(nze),
+                                                    h_stats.data_ptr(), sstride,
+                                                    h_lens.data_ptr(), h_out.data_ptr())
+            else:
+                rc = dp._lib.dppx_pixelize_uniform(ctx._h, Ct.byref(de), h_img.data_ptr(),
+                                                   Ct.byref(p), Ct.byref(nze), h_stats.data_ptr(),
+                                                   h_out.data_ptr())
+            ctx._check(rc, "e2e")
+
+        for _ in range(2):
+            e2e_step()
+        ctx.reset_stats()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        t1 = time.perf_counter()
+        barrier()
+        es = ctx.stats()
+        e_ms = allmax((t1 - t0) / args.e2e_steps * 1e3)
+        e2e = {"value": round(Fe * world * M * N / 1e6 / (e_ms / 1e3), 3), "unit": "MP/s",
+               "h2d_bytes_per_step": es["h2d_bytes"] // args.e2e_steps,
+               "d2h_bytes_per_step": es["d2h_bytes"] // args.e2e_steps,
+               "frames_per_step": Fe, "ms_per_step": round(e_ms, 3),
+               "frames_per_sec": round(Fe * world / (e_ms / 1e3), 3),
+               "path": "dppx_pixelize_adaptive (host pointers, pinned, chunked H2D/K0/K1/D2H "
+                       "pipeline on 3 streams)" if adaptive else "dppx_pixelize_uniform"}
+        del h_img, h_mask, h_out, h_stats
+
+    # ---- CPU reference baseline (rank 0, N = 1 only) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sample = cpu_reference_sample(M, N, C, b, n, m, eps, adaptive, args.cpu_seconds, frame0)
+        if sample is not None:
+            t = run_reference_once(sample, M, N, C, b, n, m, eps, adaptive)
+            cpu = {"value": round(sample["n_frames"] * M * N / 1e6 / t, 3), "unit": "MP/s",
+                   "cores": sample["workers"], "kind": "reference",
+                   "sample": f"{sample['n_frames']} frames x {C} planes, pixelize_"
+                             f"{'adaptive' if adaptive else 'parallel'} per plane (threads=1), "
+                             f"frame-parallel over {sample['workers']} threads, {t:.2f} s wall"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "MP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic",
+            "frames_per_sec": round(fps, 1),
+            "config": {"workload": desc, "frames_per_gpu": F, "shape": f"{N}x{M}x{C}",
+                       "b": b, "n": n, "m": m, "epsilon": eps,
+                       "noise": "keyed splitmix64 + inverse-CDF Laplace (reference stream), "
+                                "per-(frame, channel) derived plane seeds",
+                       "mask": "u8 centred ellipse (0.4M x 0.2N), ~25% complex" if adaptive else None,
+                       "l2": f"working set {(2 * F * M * pitch + (F * M * mpitch if adaptive else 0)) / 1e9:.2f} GB "
+                             "> 126 MB L2, no flush needed",
+                       "parallelism": f"frame-parallel x{world}, no collective on the data path"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": traffic, "kernel": f"K1 {kfam}",
+                         "algorithmic_bytes_per_launch": k1_bytes,
+                         "avg_launch_ms": round(k1_ms, 4), "peak_source": peak_src,
+                         "step_gbs_incl_K0": round(step_gbs, 1),
+                         "step_frac_incl_K0": round(step_gbs / peak, 4),
+                         "k0_ms_per_launch": round(st["device_ms"]["classify"] /
+                                                   max(1, st["launches"]["classify"]), 4)},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_timed,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    ctx.close()
+    if pg:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

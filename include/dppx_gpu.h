@@ -1,0 +1,203 @@
+/*
+ * dppx_gpu.h -- C ABI of the B200-native dppix pixelization path.
+ *
+ * Drop-in boundary for the reference's static C++ library API
+ * (/root/reference/proj/include/dppix). The reference exposes value-semantics
+ * C++ functions; this ABI exposes the same operations over plain pointers and
+ * sizes so that any host language can bind it (see INTEGRATION.md for the
+ * ctypes binding shipped in paper_2511_04261_b200/ and for the C++ shim that
+ * re-creates the exact dppix:: signatures, include/dppix/).
+ *
+ *   reference symbol (file:line)                         replaced by
+ *   dppix::grid_dims            image.hpp:86             dppx_grid_dims
+ *   dppix::make_privacy_params  noise.hpp:55             dppx_make_privacy_params
+ *   dppix::keyed_bits           noise.hpp:69             dppx_keyed_bits
+ *   dppix::laplace_at           noise.hpp:80             dppx_laplace_at (host diagnostic)
+ *   dppix::pixelize_parallel    pixelize.hpp:55-58       dppx_pixelize_uniform[_dev]
+ *   dppix::pixelize_adaptive    adaptive.hpp:70-73       dppx_pixelize_adaptive[_dev]
+ *   dppix::broadcast_means      pixelize.hpp:62          dppx_broadcast_means[_dev]
+ *   dppix::reassemble           adaptive.hpp:78          dppx_reassemble[_dev]
+ *   dppix::reconstruct          record.hpp:63            dppx_reassemble / dppx_broadcast_means
+ *   dppix::classify_regions     adaptive.hpp:45-46       dppx_classify_regions
+ *   RecordError / invalid_argument  errors.hpp:22-55     dppx_status codes
+ *
+ * Conventions
+ *  - Caller-owned buffers. Images are row-major uint8 with C interleaved
+ *    channels (C = 1 is the reference's GrayImage; C = 3 is RGB, every channel
+ *    plane processed with the reference's per-plane semantics).
+ *  - A batch holds F frames with the same geometry; plane (f, c) is channel c
+ *    of frame f and gets its own noise seed (plane_seeds[f*C + c]).
+ *  - Uniform statistics: F*C planes of G = grid_rows*grid_cols bytes, plane
+ *    (f, c) at means + (f*C + c)*G (the DPPX v1 uniform payload, record.hpp:52).
+ *  - Adaptive statistics: F*C slots of `payload_stride` bytes, each holding the
+ *    DPPX v1 adaptive payload (record.hpp:52-54): G f32 mask means, u32 simple
+ *    count S, S simple means, (G-S)*n*n complex submeans. payload_stride must be
+ *    >= dppx_adaptive_payload_capacity() and a multiple of 4.
+ *  - *_dev entry points take DEVICE pointers and are asynchronous on the ctx
+ *    stream (dppx_ctx_stream); errors detected on the device are returned by
+ *    the next dppx_ctx_synchronize. Host entry points take HOST pointers, run
+ *    a pinned double-buffered H2D -> kernels -> D2H pipeline and return when
+ *    results are in host memory.
+ *  - A ctx is bound to one device and used by one host thread at a time
+ *    (the reference functions are reentrant; use one ctx per thread).
+ *  - There is no CPU fallback: without a usable sm_100 device every compute
+ *    entry point returns DPPX_ERR_NO_DEVICE.
+ */
+#ifndef DPPX_GPU_H_
+#define DPPX_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DPPX_ABI_VERSION 1
+
+typedef enum {
+  DPPX_OK = 0,
+  DPPX_ERR_INVALID = 1,   /* std::invalid_argument in the reference            */
+  DPPX_ERR_CORRUPT = 2,   /* RecordError(corrupt_record) (adaptive.cpp:192-210) */
+  DPPX_ERR_CUDA = 3,      /* std::runtime_error: CUDA failure                  */
+  DPPX_ERR_OOM = 4,       /* std::bad_alloc                                    */
+  DPPX_ERR_NO_DEVICE = 5  /* no sm_100 device / kernels not loadable           */
+} dppx_status;
+
+typedef enum {
+  DPPX_NOISE_NONE = 0,     /* std::nullopt seed: no noise                                */
+  DPPX_NOISE_KEYED = 1,    /* reference stream: splitmix64 keyed_bits + inverse-CDF      */
+                           /* Laplace (noise.cpp:76-117), seed per plane                 */
+  DPPX_NOISE_PHILOX = 2,   /* Philox4x32-10 keyed (seed, frame, channel, cell) extension */
+  DPPX_NOISE_INJECTED = 3  /* caller-supplied noise doubles (parity testing)             */
+} dppx_noise_kind;
+
+/* GridGeometry, image.hpp:71-82. */
+typedef struct {
+  int32_t b, grid_rows, grid_cols, pad_rows, pad_cols;
+} dppx_geometry;
+
+/* PrivacyParams, noise.hpp:41-51. */
+typedef struct {
+  double epsilon;
+  int32_t m, b, n, subgrid_side;
+  double delta, sigma, delta_sub, sigma_sub;
+} dppx_privacy_params;
+
+/* A batch of F frames of one geometry. Strides are in bytes. */
+typedef struct {
+  int32_t height, width, channels, frames; /* M, N, C (1..4), F */
+  int64_t pitch, frame_stride;             /* input image               */
+  int64_t mask_pitch, mask_frame_stride;   /* adaptive region mask (u8) */
+  int64_t out_pitch, out_frame_stride;     /* reconstructed image       */
+} dppx_frames_desc;
+
+typedef struct {
+  int32_t kind;                /* dppx_noise_kind                                        */
+  uint32_t frame_base;         /* PHILOX: global index of frame 0 of this batch          */
+  const uint64_t* plane_seeds; /* KEYED: F*C host seeds, (f, c) at f*C + c.              */
+                               /* PHILOX: plane_seeds[0] is the base seed.               */
+  const double* injected;      /* INJECTED: per plane G*n*n doubles,                      */
+                               /* ((f*C + c)*G + g)*n*n + sr*n + sc. Device memory for    */
+                               /* *_dev entry points, host memory otherwise.              */
+} dppx_noise;
+
+/* Per kernel-family launch counts and (when timing is on) summed device ms. */
+typedef enum {
+  DPPX_K_CLASSIFY = 0, /* K0: mask -> per-cell classification + slot scan */
+  DPPX_K_STATS = 1,    /* K1: TMA-staged fused stats/noise/store/reconstruct */
+  DPPX_K_GENERIC = 2,  /* K1g: any b, n, C, alignment                         */
+  DPPX_K_EXPAND = 3,   /* K2: statistics -> pixels                            */
+  DPPX_K_AUX = 4,      /* synthetic generator, payload checks                 */
+  DPPX_K_COUNT = 5
+} dppx_kernel_family;
+
+typedef struct {
+  uint64_t launches[DPPX_K_COUNT];
+  double device_ms[DPPX_K_COUNT];
+  uint64_t h2d_bytes, d2h_bytes;
+} dppx_kernel_stats;
+
+typedef struct dppx_ctx dppx_ctx;
+
+/* ---- host-side parameter helpers (no device needed) --------------------- */
+const char* dppx_version(void);
+int dppx_grid_dims(int32_t height, int32_t width, int32_t b, dppx_geometry* out);
+int dppx_make_privacy_params(double epsilon, int32_t m, int32_t b, int32_t n,
+                             dppx_privacy_params* out);
+double dppx_sensitivity(int32_t b, int32_t m); /* < 0 on invalid input */
+uint64_t dppx_keyed_bits(uint64_t seed, uint32_t r, uint32_t c, uint32_t sr, uint32_t sc);
+double dppx_uniform_from_bits(uint64_t bits);
+double dppx_laplace_at(uint64_t seed, uint32_t r, uint32_t c, uint32_t sr, uint32_t sc,
+                       double sigma);
+/* Seed of plane (frame, channel) for multi-frame / multi-channel batches:
+ * keyed_bits(seed, {frame, channel, 0xFFFFFFFF, 0xFFFFFFFF}). */
+uint64_t dppx_derive_plane_seed(uint64_t seed, uint32_t frame, uint32_t channel);
+size_t dppx_adaptive_payload_capacity(int32_t height, int32_t width, int32_t b, int32_t n);
+size_t dppx_adaptive_payload_length(int32_t height, int32_t width, int32_t b, int32_t n,
+                                    uint32_t simple_count);
+
+/* ---- context ------------------------------------------------------------- */
+int dppx_ctx_create(int32_t device, dppx_ctx** out);
+void dppx_ctx_destroy(dppx_ctx* ctx);
+const char* dppx_ctx_last_error(const dppx_ctx* ctx);
+void* dppx_ctx_stream(dppx_ctx* ctx); /* cudaStream_t */
+int dppx_ctx_set_stream(dppx_ctx* ctx, void* stream); /* NULL restores the ctx's own */
+int dppx_ctx_synchronize(dppx_ctx* ctx);
+int dppx_ctx_set_timing(dppx_ctx* ctx, int32_t on);
+int dppx_ctx_get_stats(dppx_ctx* ctx, dppx_kernel_stats* out);
+int dppx_ctx_reset_stats(dppx_ctx* ctx);
+/* Frames per pipeline chunk of the host entry points (0 = automatic). */
+int dppx_ctx_set_chunk_frames(dppx_ctx* ctx, int32_t frames);
+
+int dppx_host_alloc(size_t bytes, void** out); /* pinned */
+void dppx_host_free(void* p);
+
+/* ---- device-resident entry points (async on the ctx stream) -------------- */
+int dppx_pixelize_uniform_dev(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* img,
+                              const dppx_privacy_params* params, const dppx_noise* noise,
+                              uint8_t* means, uint8_t* out /* nullable */);
+int dppx_pixelize_adaptive_dev(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* img,
+                               const uint8_t* mask, const dppx_privacy_params* params,
+                               const dppx_noise* noise, uint8_t* payload, int64_t payload_stride,
+                               uint32_t* payload_len /* nullable, F*C */,
+                               uint8_t* out /* nullable */);
+int dppx_broadcast_means_dev(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* means,
+                             int32_t b, uint8_t* out);
+/* payload_len: nullable; when given, each plane's length is checked. */
+int dppx_reassemble_dev(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* payload,
+                        int64_t payload_stride, const uint32_t* payload_len, int32_t b,
+                        int32_t n, uint8_t* out);
+/* Synthetic workload (bench / tests): frames f0..f0+F-1, see oracle/dppx_oracle.c. */
+int dppx_synth_frames_dev(dppx_ctx* ctx, const dppx_frames_desc* desc, uint32_t data_seed,
+                          uint32_t f0, uint8_t* img, uint8_t* mask /* nullable */);
+
+/* ---- host entry points (pinned pipeline; synchronous) -------------------- */
+int dppx_pixelize_uniform(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* img,
+                          const dppx_privacy_params* params, const dppx_noise* noise,
+                          uint8_t* means, uint8_t* out /* nullable */);
+int dppx_pixelize_adaptive(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* img,
+                           const uint8_t* mask, const dppx_privacy_params* params,
+                           const dppx_noise* noise, uint8_t* payload, int64_t payload_stride,
+                           uint32_t* payload_len /* nullable */, uint8_t* out /* nullable */);
+int dppx_broadcast_means(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* means,
+                         int32_t b, uint8_t* out);
+int dppx_reassemble(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* payload,
+                    int64_t payload_stride, const uint32_t* payload_len, int32_t b, int32_t n,
+                    uint8_t* out);
+
+/* classify_regions (adaptive.cpp:34-65) of F masks (desc mask fields; channels
+ * ignored): per-frame G float mask means at mask_means + f*G. */
+int dppx_classify_regions(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* mask,
+                          int32_t b, float* mask_means);
+
+/* Diagnostics for parity tests: the device noise of `count` keys
+ * (keys[4*i..4*i+3] = r, c, sr, sc) for one plane seed at scale sigma. */
+int dppx_debug_device_laplace(dppx_ctx* ctx, uint64_t seed, const uint32_t* keys, int32_t count,
+                              double sigma, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DPPX_GPU_H_ */

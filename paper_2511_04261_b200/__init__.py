@@ -1,0 +1,605 @@
+"""B200-native dppix pixelization path (arXiv 2511.04261), Python host side.
+
+This package binds ``lib/libdppx_gpu.so`` (the C ABI declared in
+``include/dppx_gpu.h``; sm_100a kernels in ``csrc/``) with ctypes and mirrors
+the reference's ``dppix::`` interface (/root/reference/proj/include/dppix):
+
+    reference (C++)                         here
+    make_privacy_params  noise.hpp:55       make_privacy_params
+    grid_dims            image.hpp:86       grid_dims
+    pixelize_parallel    pixelize.hpp:55    pixelize_parallel
+    pixelize_adaptive    adaptive.hpp:70    pixelize_adaptive
+    broadcast_means      pixelize.hpp:62    broadcast_means
+    reassemble           adaptive.hpp:78    reassemble
+    classify_regions     adaptive.hpp:45    classify_regions
+
+Errors keep the reference's taxonomy: ``std::invalid_argument`` -> ValueError,
+``RecordError(corrupt_record)`` -> RecordError. Batched multi-frame / RGB entry
+points live on :class:`Context`. There is no CPU fallback: the compute entry
+points raise :class:`DeviceUnavailable` when no sm_100 GPU is usable.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import os
+import threading
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libdppx_gpu.so")
+DROPIN_PATH = os.path.join(_HERE, "lib", "libdppix_gpu.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `make -C paper_2511_04261_b200` "
+        "(or __graft_entry__.build()); there is no CPU fallback")
+
+_lib = C.CDLL(LIB_PATH)
+
+OK, ERR_INVALID, ERR_CORRUPT, ERR_CUDA, ERR_OOM, ERR_NO_DEVICE = range(6)
+NOISE_NONE, NOISE_KEYED, NOISE_PHILOX, NOISE_INJECTED = range(4)
+K_CLASSIFY, K_STATS, K_GENERIC, K_EXPAND, K_AUX, K_COUNT = range(6)
+KERNEL_FAMILIES = ("classify", "stats_tma", "stats_generic", "expand", "aux")
+
+
+class Geometry(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("b", "grid_rows", "grid_cols", "pad_rows", "pad_cols")]
+
+    def grid_count(self):
+        return self.grid_rows * self.grid_cols
+
+    def __eq__(self, o):
+        return all(getattr(self, n) == getattr(o, n) for n, _ in self._fields_)
+
+    def __repr__(self):
+        return "GridGeometry(" + ", ".join(f"{n}={getattr(self, n)}" for n, _ in self._fields_) + ")"
+
+
+class PrivacyParams(C.Structure):
+    _fields_ = [("epsilon", C.c_double), ("m", C.c_int32), ("b", C.c_int32), ("n", C.c_int32),
+                ("subgrid_side", C.c_int32), ("delta", C.c_double), ("sigma", C.c_double),
+                ("delta_sub", C.c_double), ("sigma_sub", C.c_double)]
+
+
+class FramesDesc(C.Structure):
+    _fields_ = [("height", C.c_int32), ("width", C.c_int32), ("channels", C.c_int32),
+                ("frames", C.c_int32), ("pitch", C.c_int64), ("frame_stride", C.c_int64),
+                ("mask_pitch", C.c_int64), ("mask_frame_stride", C.c_int64),
+                ("out_pitch", C.c_int64), ("out_frame_stride", C.c_int64)]
+
+
+class Noise(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("frame_base", C.c_uint32),
+                ("plane_seeds", C.POINTER(C.c_uint64)), ("injected", C.POINTER(C.c_double))]
+
+
+class KernelStats(C.Structure):
+    _fields_ = [("launches", C.c_uint64 * K_COUNT), ("device_ms", C.c_double * K_COUNT),
+                ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
+
+
+_u8p = C.POINTER(C.c_uint8)
+_u32p = C.POINTER(C.c_uint32)
+_f32p = C.POINTER(C.c_float)
+_f64p = C.POINTER(C.c_double)
+_vp = C.c_void_p
+_ctxp = C.c_void_p
+_descp = C.POINTER(FramesDesc)
+_pp = C.POINTER(PrivacyParams)
+_np = C.POINTER(Noise)
+
+# Every symbol of include/dppx_gpu.h with its ctypes signature.
+ABI = {
+    "dppx_version": (C.c_char_p, []),
+    "dppx_grid_dims": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(Geometry)]),
+    "dppx_make_privacy_params": (C.c_int, [C.c_double, C.c_int32, C.c_int32, C.c_int32, _pp]),
+    "dppx_sensitivity": (C.c_double, [C.c_int32, C.c_int32]),
+    "dppx_keyed_bits": (C.c_uint64, [C.c_uint64] + [C.c_uint32] * 4),
+    "dppx_uniform_from_bits": (C.c_double, [C.c_uint64]),
+    "dppx_laplace_at": (C.c_double, [C.c_uint64] + [C.c_uint32] * 4 + [C.c_double]),
+    "dppx_derive_plane_seed": (C.c_uint64, [C.c_uint64, C.c_uint32, C.c_uint32]),
+    "dppx_adaptive_payload_capacity": (C.c_size_t, [C.c_int32] * 4),
+    "dppx_adaptive_payload_length": (C.c_size_t, [C.c_int32] * 4 + [C.c_uint32]),
+    "dppx_ctx_create": (C.c_int, [C.c_int32, C.POINTER(_ctxp)]),
+    "dppx_ctx_destroy": (None, [_ctxp]),
+    "dppx_ctx_last_error": (C.c_char_p, [_ctxp]),
+    "dppx_ctx_stream": (_vp, [_ctxp]),
+    "dppx_ctx_set_stream": (C.c_int, [_ctxp, _vp]),
+    "dppx_ctx_synchronize": (C.c_int, [_ctxp]),
+    "dppx_ctx_set_timing": (C.c_int, [_ctxp, C.c_int32]),
+    "dppx_ctx_get_stats": (C.c_int, [_ctxp, C.POINTER(KernelStats)]),
+    "dppx_ctx_reset_stats": (C.c_int, [_ctxp]),
+    "dppx_ctx_set_chunk_frames": (C.c_int, [_ctxp, C.c_int32]),
+    "dppx_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(_vp)]),
+    "dppx_host_free": (None, [_vp]),
+    "dppx_pixelize_uniform_dev": (C.c_int, [_ctxp, _descp, _vp, _pp, _np, _vp, _vp]),
+    "dppx_pixelize_adaptive_dev": (C.c_int, [_ctxp, _descp, _vp, _vp, _pp, _np, _vp, C.c_int64,
+                                             _vp, _vp]),
+    "dppx_broadcast_means_dev": (C.c_int, [_ctxp, _descp, _vp, C.c_int32, _vp]),
+    "dppx_reassemble_dev": (C.c_int, [_ctxp, _descp, _vp, C.c_int64, _vp, C.c_int32, C.c_int32,
+                                      _vp]),
+    "dppx_synth_frames_dev": (C.c_int, [_ctxp, _descp, C.c_uint32, C.c_uint32, _vp, _vp]),
+    "dppx_pixelize_uniform": (C.c_int, [_ctxp, _descp, _vp, _pp, _np, _vp, _vp]),
+    "dppx_pixelize_adaptive": (C.c_int, [_ctxp, _descp, _vp, _vp, _pp, _np, _vp, C.c_int64, _vp,
+                                         _vp]),
+    "dppx_broadcast_means": (C.c_int, [_ctxp, _descp, _vp, C.c_int32, _vp]),
+    "dppx_reassemble": (C.c_int, [_ctxp, _descp, _vp, C.c_int64, _vp, C.c_int32, C.c_int32, _vp]),
+    "dppx_classify_regions": (C.c_int, [_ctxp, _descp, _vp, C.c_int32, _vp]),
+    "dppx_debug_device_laplace": (C.c_int, [_ctxp, C.c_uint64, _vp, C.c_int32, C.c_double, _vp]),
+}
+for _name, (_res, _args) in ABI.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+
+class RecordError(RuntimeError):
+    """dppix::RecordError (errors.hpp:37-55); ``kind`` is 'corrupt_record' here."""
+
+    def __init__(self, msg, kind="corrupt_record"):
+        super().__init__(msg)
+        self.kind = kind
+
+
+class DeviceUnavailable(RuntimeError):
+    """No usable sm_100 device: the GPU path cannot run and nothing falls back."""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+def _raise(rc, msg):
+    if rc == ERR_INVALID:
+        raise ValueError(msg)
+    if rc == ERR_CORRUPT:
+        raise RecordError(msg)
+    if rc == ERR_OOM:
+        raise MemoryError(msg)
+    if rc == ERR_NO_DEVICE:
+        raise DeviceUnavailable(msg)
+    raise CudaError(msg)
+
+
+# ---------------------------------------------------------------- parameters
+def grid_dims(height: int, width: int, b: int) -> Geometry:
+    """grid_dims (image.cpp:48-72)."""
+    if height < 1 or width < 1:
+        raise ValueError("grid_dims: dimensions must be >= 1")
+    if b < 1:
+        raise ValueError("grid_dims: grid side b must be >= 1")
+    g = Geometry()
+    if _lib.dppx_grid_dims(height, width, b, C.byref(g)) != OK:
+        raise ValueError("grid_dims: grid side b exceeds both image dimensions")
+    return g
+
+
+def make_privacy_params(epsilon: float, m: int, b: int, n: int = 1) -> PrivacyParams:
+    """make_privacy_params (noise.cpp:39-68): sigma = 255 m / (b^2 eps), sigma_sub = sigma n^2."""
+    if not epsilon > 0.0:
+        raise ValueError("make_privacy_params: epsilon must be > 0")
+    if m < 1:
+        raise ValueError("make_privacy_params: m must be >= 1")
+    if b < 1:
+        raise ValueError("make_privacy_params: b must be >= 1")
+    if n < 1:
+        raise ValueError("make_privacy_params: n must be >= 1")
+    if b % n:
+        raise ValueError("make_privacy_params: n must divide b")
+    p = PrivacyParams()
+    _lib.dppx_make_privacy_params(epsilon, m, b, n, C.byref(p))
+    return p
+
+
+def sensitivity(b: int, m: int) -> float:
+    if b < 1 or m < 1:
+        raise ValueError("sensitivity: b and m must be >= 1")
+    return _lib.dppx_sensitivity(b, m)
+
+
+def keyed_bits(seed: int, r: int, c: int, sr: int = 0, sc: int = 0) -> int:
+    return _lib.dppx_keyed_bits(seed, r, c, sr, sc)
+
+
+def laplace_at(seed: int, r: int, c: int, sr: int, sc: int, sigma: float) -> float:
+    if not sigma > 0.0:
+        raise ValueError("laplace_at: sigma must be > 0")
+    return _lib.dppx_laplace_at(seed, r, c, sr, sc, sigma)
+
+
+def derive_plane_seed(seed: int, frame: int, channel: int) -> int:
+    return _lib.dppx_derive_plane_seed(seed, frame, channel)
+
+
+def adaptive_payload_capacity(height, width, b, n) -> int:
+    return _lib.dppx_adaptive_payload_capacity(height, width, b, n)
+
+
+def plane_seeds(seed: int, frames: int, channels: int, frame0: int = 0, mode: str = "derived"):
+    """Per-plane seeds: 'derived' = derive_plane_seed(seed, f, k); 'shared' = the
+    reference's run_batch behaviour (same seed for every file, cli.cpp:200-201)."""
+    if mode == "shared":
+        return np.full(frames * channels, seed, np.uint64)
+    return np.array([derive_plane_seed(seed, frame0 + f, k)
+                     for f in range(frames) for k in range(channels)], np.uint64)
+
+
+# ---------------------------------------------------------------- context
+def _ptr(a):
+    """Address of a numpy array or torch tensor (host or device)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return a.data_ptr()  # torch.Tensor
+
+
+def _desc(M, N, Cn, F, pitch=None, fstride=None, mpitch=None, mfstride=None, opitch=None,
+          ofstride=None):
+    d = FramesDesc()
+    d.height, d.width, d.channels, d.frames = M, N, Cn, F
+    d.pitch = pitch if pitch is not None else N * Cn
+    d.frame_stride = fstride if fstride is not None else d.pitch * M
+    d.mask_pitch = mpitch if mpitch is not None else N
+    d.mask_frame_stride = mfstride if mfstride is not None else d.mask_pitch * M
+    d.out_pitch = opitch if opitch is not None else N * Cn
+    d.out_frame_stride = ofstride if ofstride is not None else d.out_pitch * M
+    return d
+
+
+def _frames_shape(img):
+    """(F, M, N, C) of a [M,N], [M,N,C], [F,M,N] (with channels=1) or [F,M,N,C] array."""
+    s = tuple(img.shape)
+    if len(s) == 2:
+        return 1, s[0], s[1], 1
+    if len(s) == 3:
+        return 1, s[0], s[1], s[2]
+    return s[0], s[1], s[2], s[3]
+
+
+class Context:
+    """One dppx_ctx: a device, its streams, scratch and pinned staging.
+
+    Methods with ``_dev`` take torch CUDA tensors (device-resident, async on the
+    context stream); the others take host numpy arrays and run the pinned
+    H2D -> kernels -> D2H pipeline.
+    """
+
+    def __init__(self, device: int = 0):
+        h = _ctxp()
+        rc = _lib.dppx_ctx_create(device, C.byref(h))
+        if rc != OK:
+            _raise(rc, f"dppx_ctx_create(device={device}) failed with status {rc}")
+        self._h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.dppx_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc, who):
+        if rc != OK:
+            _raise(rc, f"{who}: {_lib.dppx_ctx_last_error(self._h).decode()}")
+
+    # ---- plumbing
+    @property
+    def stream(self) -> int:
+        return _lib.dppx_ctx_stream(self._h) or 0
+
+    def set_stream(self, stream_handle: Optional[int]):
+        self._check(_lib.dppx_ctx_set_stream(self._h, stream_handle), "set_stream")
+
+    def synchronize(self):
+        self._check(_lib.dppx_ctx_synchronize(self._h), "synchronize")
+
+    def set_timing(self, on: bool):
+        _lib.dppx_ctx_set_timing(self._h, 1 if on else 0)
+
+    def set_chunk_frames(self, frames: int):
+        self._check(_lib.dppx_ctx_set_chunk_frames(self._h, frames), "set_chunk_frames")
+
+    def stats(self) -> dict:
+        s = KernelStats()
+        _lib.dppx_ctx_get_stats(self._h, C.byref(s))
+        return {"launches": {k: int(s.launches[i]) for i, k in enumerate(KERNEL_FAMILIES)},
+                "device_ms": {k: float(s.device_ms[i]) for i, k in enumerate(KERNEL_FAMILIES)},
+                "h2d_bytes": int(s.h2d_bytes), "d2h_bytes": int(s.d2h_bytes)}
+
+    def reset_stats(self):
+        _lib.dppx_ctx_reset_stats(self._h)
+
+    @staticmethod
+    def _noise(kind, seeds, frame_base=0, injected=None):
+        nz = Noise()
+        nz.kind = kind
+        nz.frame_base = frame_base
+        keep = []
+        if seeds is not None:
+            arr = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64))
+            keep.append(arr)
+            nz.plane_seeds = arr.ctypes.data_as(C.POINTER(C.c_uint64))
+        if injected is not None:
+            if isinstance(injected, np.ndarray):
+                inj = np.ascontiguousarray(injected, dtype=np.float64)
+                keep.append(inj)
+                nz.injected = inj.ctypes.data_as(_f64p)
+            else:  # torch tensor on device
+                keep.append(injected)
+                nz.injected = C.cast(C.c_void_p(injected.data_ptr()), _f64p)
+        return nz, keep
+
+    # ---- host entry points (numpy in / numpy out)
+    def pixelize_uniform(self, frames, params: PrivacyParams, noise=NOISE_NONE, seeds=None,
+                         frame_base=0, injected=None, want_image=True):
+        """frames: uint8 [F,M,N,C] (or [M,N], [M,N,C]). Returns (means[F*C, G], image)."""
+        frames = np.ascontiguousarray(frames, dtype=np.uint8)
+        F, M, N, Cn = _frames_shape(frames)
+        g = grid_dims(M, N, params.b)
+        means = np.zeros((F * Cn, g.grid_count()), np.uint8)
+        out = np.zeros_like(frames) if want_image else None
+        nz, keep = self._noise(noise, seeds, frame_base, injected)
+        d = _desc(M, N, Cn, F)
+        self._check(_lib.dppx_pixelize_uniform(self._h, C.byref(d), _ptr(frames), C.byref(params),
+                                               C.byref(nz), _ptr(means), _ptr(out)),
+                    "pixelize_uniform")
+        del keep
+        return means, out
+
+    def pixelize_adaptive(self, frames, masks, params: PrivacyParams, noise=NOISE_NONE,
+                          seeds=None, frame_base=0, injected=None, want_image=True):
+        """frames uint8 [F,M,N,C], masks uint8 [F,M,N]. Returns (payloads: list of bytes per
+        plane (f*C + c), image)."""
+        frames = np.ascontiguousarray(frames, dtype=np.uint8)
+        F, M, N, Cn = _frames_shape(frames)
+        masks = np.ascontiguousarray(masks, dtype=np.uint8).reshape(F, M, N)
+        cap = adaptive_payload_capacity(M, N, params.b, params.n)
+        stride = (cap + 3) & ~3
+        buf = np.zeros((F * Cn, stride), np.uint8)
+        lens = np.zeros(F * Cn, np.uint32)
+        out = np.zeros_like(frames) if want_image else None
+        nz, keep = self._noise(noise, seeds, frame_base, injected)
+        d = _desc(M, N, Cn, F)
+        self._check(_lib.dppx_pixelize_adaptive(self._h, C.byref(d), _ptr(frames), _ptr(masks),
+                                                C.byref(params), C.byref(nz), _ptr(buf), stride,
+                                                _ptr(lens), _ptr(out)), "pixelize_adaptive")
+        del keep
+        return [bytes(buf[i, : lens[i]]) for i in range(F * Cn)], out
+
+    def broadcast_means(self, means, M, N, b, channels=1, frames=1):
+        means = np.ascontiguousarray(means, dtype=np.uint8)
+        out = np.zeros((frames, M, N, channels), np.uint8)
+        d = _desc(M, N, channels, frames)
+        self._check(_lib.dppx_broadcast_means(self._h, C.byref(d), _ptr(means), b, _ptr(out)),
+                    "broadcast_means")
+        return out
+
+    def reassemble(self, payloads: Sequence[bytes], M, N, b, n, channels=1, frames=1,
+                   check_lengths=True):
+        P = frames * channels
+        stride = max(16, (max(len(p) for p in payloads) + 15) & ~15)
+        buf = np.zeros((P, stride), np.uint8)
+        for i, p in enumerate(payloads):
+            buf[i, : len(p)] = np.frombuffer(p, np.uint8)
+        lens = np.array([len(p) for p in payloads], np.uint32)
+        out = np.zeros((frames, M, N, channels), np.uint8)
+        d = _desc(M, N, channels, frames)
+        self._check(_lib.dppx_reassemble(self._h, C.byref(d), _ptr(buf), stride,
+                                         _ptr(lens) if check_lengths else None, b, n, _ptr(out)),
+                    "reassemble")
+        return out
+
+    def classify_regions(self, masks, b):
+        masks = np.ascontiguousarray(masks, dtype=np.uint8)
+        if masks.ndim == 2:
+            masks = masks[None]
+        F, M, N = masks.shape
+        g = grid_dims(M, N, b)
+        mm = np.zeros((F, g.grid_count()), np.float32)
+        d = _desc(M, N, 1, F)
+        self._check(_lib.dppx_classify_regions(self._h, C.byref(d), _ptr(masks), b, _ptr(mm)),
+                    "classify_regions")
+        return mm
+
+    def device_laplace(self, seed, keys, sigma):
+        keys = np.ascontiguousarray(np.asarray(keys, np.uint32).reshape(-1, 4))
+        out = np.zeros(len(keys), np.float64)
+        self._check(_lib.dppx_debug_device_laplace(self._h, seed, _ptr(keys), len(keys), sigma,
+                                                   _ptr(out)), "device_laplace")
+        return out
+
+    # ---- device entry points (torch CUDA tensors, async on self.stream)
+    def pixelize_adaptive_dev(self, desc: FramesDesc, img, mask, params, noise_struct, payload,
+                              payload_stride, payload_len=None, out=None):
+        self._check(_lib.dppx_pixelize_adaptive_dev(
+            self._h, C.byref(desc), _ptr(img), _ptr(mask), C.byref(params), C.byref(noise_struct),
+            _ptr(payload), payload_stride, _ptr(payload_len), _ptr(out)), "pixelize_adaptive_dev")
+
+    def pixelize_uniform_dev(self, desc: FramesDesc, img, params, noise_struct, means, out=None):
+        self._check(_lib.dppx_pixelize_uniform_dev(
+            self._h, C.byref(desc), _ptr(img), C.byref(params), C.byref(noise_struct),
+            _ptr(means), _ptr(out)), "pixelize_uniform_dev")
+
+    def reassemble_dev(self, desc, payload, payload_stride, payload_len, b, n, out):
+        self._check(_lib.dppx_reassemble_dev(self._h, C.byref(desc), _ptr(payload),
+                                             payload_stride, _ptr(payload_len), b, n, _ptr(out)),
+                    "reassemble_dev")
+
+    def broadcast_means_dev(self, desc, means, b, out):
+        self._check(_lib.dppx_broadcast_means_dev(self._h, C.byref(desc), _ptr(means), b,
+                                                  _ptr(out)), "broadcast_means_dev")
+
+    def synth_frames_dev(self, desc, data_seed, f0, img, mask=None):
+        self._check(_lib.dppx_synth_frames_dev(self._h, C.byref(desc), data_seed, f0, _ptr(img),
+                                               _ptr(mask)), "synth_frames_dev")
+
+
+_tls = threading.local()
+
+
+def default_context() -> Context:
+    """Per-thread context on device $DPPX_DEVICE (default 0)."""
+    ctx = getattr(_tls, "ctx", None)
+    if ctx is None:
+        ctx = _tls.ctx = Context(int(os.environ.get("DPPX_DEVICE", "0")))
+    return ctx
+
+
+# ---------------------------------------------------------------- reference-shaped API
+@dataclasses.dataclass
+class GridMeans:
+    geometry: Geometry
+    values: np.ndarray
+
+
+@dataclasses.dataclass
+class UniformResult:
+    image: np.ndarray
+    means: GridMeans
+
+
+@dataclasses.dataclass
+class RegionClassification:
+    geometry: Geometry
+    mask_means: np.ndarray
+    is_simple: np.ndarray
+
+    def simple_count(self) -> int:
+        return int((self.is_simple == 1).sum())
+
+
+@dataclasses.dataclass
+class AdaptiveMeans:
+    geometry: Geometry
+    n: int
+    classification: RegionClassification
+    simple_means: np.ndarray
+    complex_submeans: np.ndarray
+
+    def payload(self) -> bytes:
+        """DPPX v1 adaptive payload (record.hpp:52-54)."""
+        mm = np.asarray(self.classification.mask_means, "<f4").tobytes()
+        S = len(self.simple_means)
+        return (mm + int(S).to_bytes(4, "little") + bytes(self.simple_means)
+                + bytes(self.complex_submeans))
+
+
+@dataclasses.dataclass
+class AdaptiveResult:
+    image: np.ndarray
+    means: AdaptiveMeans
+
+
+def _check_gray(img, who):
+    img = np.asarray(img)
+    if img.ndim != 2 or img.shape[0] < 1 or img.shape[1] < 1:
+        raise ValueError(f"{who}: malformed image")
+    return np.ascontiguousarray(img, dtype=np.uint8)
+
+
+def parse_adaptive_payload(payload: bytes, geom: Geometry, n: int) -> AdaptiveMeans:
+    G = geom.grid_count()
+    mm = np.frombuffer(payload[: 4 * G], "<f4").copy()
+    S = int.from_bytes(payload[4 * G: 4 * G + 4], "little")
+    simple = np.frombuffer(payload[4 * G + 4: 4 * G + 4 + S], np.uint8).copy()
+    cplx = np.frombuffer(payload[4 * G + 4 + S:], np.uint8).copy()
+    cls = RegionClassification(geom, mm, (mm > np.float32(0.5)).astype(np.uint8))
+    return AdaptiveMeans(geom, n, cls, simple, cplx)
+
+
+def pixelize_parallel(img, params: PrivacyParams, seed: Optional[int] = None,
+                      threads: int = 0) -> UniformResult:
+    """pixelize_parallel (pixelize.cpp:86-124) on the GPU; `threads` is ignored."""
+    img = _check_gray(img, "pixelize_parallel")
+    if params.n != 1:
+        raise ValueError("pixelize_parallel: requires n == 1")
+    geom = grid_dims(img.shape[0], img.shape[1], params.b)
+    ctx = default_context()
+    means, out = ctx.pixelize_uniform(img, params, NOISE_KEYED if seed is not None else NOISE_NONE,
+                                      [seed] if seed is not None else None)
+    return UniformResult(out, GridMeans(geom, means[0]))
+
+
+def pixelize_adaptive(img, mask, params: PrivacyParams, seed: Optional[int] = None,
+                      threads: int = 0) -> AdaptiveResult:
+    """pixelize_adaptive (adaptive.cpp:88-179) on the GPU; `threads` is ignored."""
+    img = _check_gray(img, "pixelize_adaptive")
+    mask = np.ascontiguousarray(mask, dtype=np.uint8)
+    if mask.shape != img.shape:
+        raise ValueError("pixelize_adaptive: mask dimensions do not match image")
+    if params.n < 1 or params.b % params.n or params.subgrid_side * params.n != params.b:
+        raise ValueError("pixelize_adaptive: invalid subgrid factor")
+    geom = grid_dims(img.shape[0], img.shape[1], params.b)
+    ctx = default_context()
+    payloads, out = ctx.pixelize_adaptive(img, mask, params,
+                                          NOISE_KEYED if seed is not None else NOISE_NONE,
+                                          [seed] if seed is not None else None)
+    return AdaptiveResult(out, parse_adaptive_payload(payloads[0], geom, params.n))
+
+
+def broadcast_means(means: GridMeans, height: int, width: int) -> np.ndarray:
+    """broadcast_means (pixelize.cpp:126-150)."""
+    if height < 1 or width < 1:
+        raise ValueError("broadcast_means: dimensions must be >= 1")
+    expected = grid_dims(height, width, means.geometry.b)
+    if not (means.geometry == expected) or len(means.values) != expected.grid_count():
+        raise ValueError("broadcast_means: means do not fit the target dimensions")
+    return default_context().broadcast_means(means.values, height, width, means.geometry.b)[0, :, :, 0]
+
+
+def reassemble(means: AdaptiveMeans, height: int, width: int) -> np.ndarray:
+    """reassemble (adaptive.cpp:181-245), with its RecordError(corrupt_record) checks."""
+    if height < 1 or width < 1:
+        raise ValueError("reassemble: dimensions must be >= 1")
+    geom = means.geometry
+    if not (geom == grid_dims(height, width, geom.b)):
+        raise ValueError("reassemble: geometry does not match the target dimensions")
+    n = means.n
+    if n < 1 or geom.b % n:
+        raise RecordError("reassemble: subgrid factor does not divide grid side")
+    G = geom.grid_count()
+    cls = means.classification
+    if len(cls.mask_means) != G or len(cls.is_simple) != G:
+        raise RecordError("reassemble: classification length mismatch")
+    S = cls.simple_count()
+    if len(means.simple_means) != S or len(means.complex_submeans) != (G - S) * n * n:
+        raise RecordError("reassemble: mean array length mismatch")
+    mm = np.asarray(cls.mask_means, np.float32).copy()
+    flags = np.asarray(cls.is_simple) != 0
+    disagree = (mm > np.float32(0.5)) != flags
+    mm[disagree] = np.where(flags[disagree], 1.0, 0.0)
+    payload = (mm.astype("<f4").tobytes() + int(S).to_bytes(4, "little")
+               + bytes(np.asarray(means.simple_means, np.uint8))
+               + bytes(np.asarray(means.complex_submeans, np.uint8)))
+    return default_context().reassemble([payload], height, width, geom.b, n)[0, :, :, 0]
+
+
+def classify_regions(mask, geom: Geometry) -> RegionClassification:
+    """classify_regions (adaptive.cpp:34-65) on the GPU."""
+    mask = np.asarray(mask)
+    if mask.ndim != 2 or mask.shape[0] < 1 or mask.shape[1] < 1:
+        raise ValueError("classify_regions: malformed mask")
+    if not (geom == grid_dims(mask.shape[0], mask.shape[1], geom.b)):
+        raise ValueError("classify_regions: geometry does not match mask dimensions")
+    mm = default_context().classify_regions(mask, geom.b)[0]
+    return RegionClassification(geom, mm, (mm > np.float32(0.5)).astype(np.uint8))
+
+
+__all__ = [
+    "Context", "default_context", "grid_dims", "make_privacy_params", "sensitivity", "keyed_bits",
+    "laplace_at", "derive_plane_seed", "plane_seeds", "adaptive_payload_capacity",
+    "pixelize_parallel", "pixelize_adaptive", "broadcast_means", "reassemble", "classify_regions",
+    "parse_adaptive_payload", "GridMeans", "UniformResult", "AdaptiveMeans", "AdaptiveResult",
+    "RegionClassification", "RecordError", "DeviceUnavailable", "PrivacyParams", "Geometry",
+    "FramesDesc", "Noise", "ABI", "LIB_PATH", "DROPIN_PATH",
+    "NOISE_NONE", "NOISE_KEYED", "NOISE_PHILOX", "NOISE_INJECTED",
+]

@@ -1,0 +1,976 @@
+// capi.cu -- host runtime behind include/dppx_gpu.h: context (device, streams,
+// scratch, pinned staging), argument validation with the reference's error
+// semantics, kernel selection, and the pinned double-buffered
+// H2D -> K0/K1 -> D2H pipeline of the host entry points.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <map>
+#include <utility>
+#include <vector>
+
+#include "../../include/dppx_gpu.h"
+#include "dppx_params.h"
+
+namespace dppx {
+using StatsKernel = void (*)(const StatsArgs);
+StatsKernel select_stats_kernel(int C, int b, int n, bool adaptive);
+int stats_threads();
+int stats_tile_px();
+int stats_max_stages();
+cudaError_t launch_classify(const ClassifyArgs& a, cudaStream_t s);
+cudaError_t launch_stats_tma(StatsKernel k, const StatsArgs& a, int grid, size_t smem,
+                             cudaStream_t s);
+cudaError_t launch_stats_generic(const StatsArgs& a, cudaStream_t s);
+cudaError_t launch_expand(const ExpandArgs& a, cudaStream_t s);
+cudaError_t launch_synth(const BatchGeom& g, uint32_t seed, uint32_t f0, uint8_t* img,
+                         int64_t pitch, int64_t fstride, uint8_t* mask, int64_t mpitch,
+                         int64_t mfstride, cudaStream_t s);
+cudaError_t launch_debug_laplace(uint64_t mixed, const uint32_t* keys, int count, double sigma,
+                                 double* out, cudaStream_t s);
+}  // namespace dppx
+
+using namespace dppx;
+
+namespace {
+
+// ---- host mirrors of the reference's scalar helpers ------------------------
+uint64_t mix64_h(uint64_t z) {  // noise.cpp:77-82
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+uint64_t keyed_bits_h(uint64_t seed, uint32_t r, uint32_t c, uint32_t sr, uint32_t sc) {
+  uint64_t s = mix64_h(seed);  // noise.cpp:86-91
+  s = mix64_h(s ^ ((static_cast<uint64_t>(r) << 32) | c));
+  return mix64_h(s ^ ((static_cast<uint64_t>(sr) << 32) | sc));
+}
+
+int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+struct PendingTiming {
+  int family;
+  cudaEvent_t start, stop;
+};
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct dppx_ctx {
+  int device = 0;
+  int sms = 148;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;  // compute stream (own or user's)
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  std::string err;
+  // scratch
+  DevBuf cellinfo, rowcnt, rowprefix, totals, counters, status, seeds, keys, dbl;
+  uint64_t* seeds_pinned = nullptr;
+  size_t seeds_pinned_n = 0;
+  cudaEvent_t seeds_ev = nullptr;
+  // host-pipeline staging (2 slots)
+  DevBuf img[2], mask[2], out[2], stats[2], lens[2], inj[2], sd[2];
+  uint64_t* sd_pinned[2] = {nullptr, nullptr};
+  size_t sd_pinned_n[2] = {0, 0};
+  cudaEvent_t in_done[2] = {}, comp_done[2] = {}, out_done[2] = {};
+  int chunk_frames = 0;
+  // stats
+  bool timing = false;
+  std::vector<PendingTiming> pending;
+  std::vector<cudaEvent_t> event_pool;
+  dppx_kernel_stats kstats{};
+  std::map<std::pair<const void*, size_t>, int> occupancy;  // (TMA kernel, smem) -> CTAs/SM
+};
+
+namespace {
+
+int set_err(dppx_ctx* ctx, int code, const char* fmt, ...) {
+  if (ctx) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    ctx->err = buf;
+  }
+  return code;
+}
+
+#define CUDA_TRY(ctx, expr)                                                                \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess) {                                                               \
+      return set_err(ctx, e_ == cudaErrorMemoryAllocation ? DPPX_ERR_OOM : DPPX_ERR_CUDA,  \
+                     "%s: %s", #expr, cudaGetErrorString(e_));                             \
+    }                                                                                      \
+  } while (0)
+
+int ensure(dppx_ctx* ctx, DevBuf& b, size_t bytes, bool zero = false) {
+  if (bytes == 0) bytes = 16;
+  if (b.bytes >= bytes) return DPPX_OK;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+  const size_t sz = std::max(bytes, static_cast<size_t>(256));
+  CUDA_TRY(ctx, cudaMalloc(&b.p, sz));
+  b.bytes = sz;
+  if (zero) CUDA_TRY(ctx, cudaMemset(b.p, 0, sz));
+  return DPPX_OK;
+}
+
+cudaEvent_t get_event(dppx_ctx* ctx) {
+  if (!ctx->event_pool.empty()) {
+    cudaEvent_t e = ctx->event_pool.back();
+    ctx->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void timing_begin(dppx_ctx* ctx, int family, PendingTiming* pt) {
+  ctx->kstats.launches[family] += 1;
+  pt->family = family;
+  pt->start = pt->stop = nullptr;
+  if (!ctx->timing) return;
+  pt->start = get_event(ctx);
+  pt->stop = get_event(ctx);
+  cudaEventRecord(pt->start, ctx->stream);
+}
+
+void timing_end(dppx_ctx* ctx, PendingTiming* pt) {
+  if (!pt->start) return;
+  cudaEventRecord(pt->stop, ctx->stream);
+  ctx->pending.push_back(*pt);
+}
+
+void collect_timings(dppx_ctx* ctx) {
+  for (auto& pt : ctx->pending) {
+    float ms = 0.f;
+    cudaEventSynchronize(pt.stop);
+    if (cudaEventElapsedTime(&ms, pt.start, pt.stop) == cudaSuccess)
+      ctx->kstats.device_ms[pt.family] += ms;
+    ctx->event_pool.push_back(pt.start);
+    ctx->event_pool.push_back(pt.stop);
+  }
+  ctx->pending.clear();
+}
+
+// ---- validation mirroring the reference's throws ----------------------------
+int geometry(dppx_ctx* ctx, int M, int N, int C, int F, int b, int n, BatchGeom* g,
+             bool check_pad) {
+  if (M < 1 || N < 1) return set_err(ctx, DPPX_ERR_INVALID, "malformed image (dimensions < 1)");
+  if (C < 1 || C > 4) return set_err(ctx, DPPX_ERR_INVALID, "channels must be 1..4");
+  if (F < 0) return set_err(ctx, DPPX_ERR_INVALID, "frames must be >= 0");
+  dppx_geometry gg;
+  if (dppx_grid_dims(M, N, b, &gg) != DPPX_OK)  // image.cpp:48-58
+    return set_err(ctx, DPPX_ERR_INVALID,
+                   b < 1 ? "grid_dims: grid side b must be >= 1"
+                         : "grid_dims: grid side b exceeds both image dimensions");
+  if (check_pad && (gg.pad_rows != 0 || gg.pad_cols != 0) &&
+      (gg.pad_rows >= M || gg.pad_cols >= N))  // image.cpp:94-98
+    return set_err(ctx, DPPX_ERR_INVALID,
+                   "mirror_pad: padding exceeds image size, reflection source out of range "
+                   "(use b <= min(M, N))");
+  if (n < 1 || b % n != 0)
+    return set_err(ctx, DPPX_ERR_INVALID, "invalid subgrid factor");
+  g->M = M;
+  g->N = N;
+  g->C = C;
+  g->F = F;
+  g->b = b;
+  g->n = n;
+  g->sb = b / n;
+  g->GR = gg.grid_rows;
+  g->GC = gg.grid_cols;
+  g->G = gg.grid_rows * gg.grid_cols;
+  g->PR = gg.pad_rows;
+  g->PC = gg.pad_cols;
+  return DPPX_OK;
+}
+
+int check_desc(dppx_ctx* ctx, const dppx_frames_desc* d, bool need_mask, bool need_out) {
+  if (!d) return set_err(ctx, DPPX_ERR_INVALID, "null frames descriptor");
+  const int64_t row = static_cast<int64_t>(d->width) * d->channels;
+  if (d->pitch < row || d->frame_stride < d->pitch * d->height)
+    return set_err(ctx, DPPX_ERR_INVALID, "image pitch/frame_stride too small");
+  if (need_mask && (d->mask_pitch < d->width || d->mask_frame_stride < d->mask_pitch * d->height))
+    return set_err(ctx, DPPX_ERR_INVALID, "mask pitch/frame_stride too small");
+  if (need_out && (d->out_pitch < row || d->out_frame_stride < d->out_pitch * d->height))
+    return set_err(ctx, DPPX_ERR_INVALID, "out pitch/frame_stride too small");
+  return DPPX_OK;
+}
+
+// Upload per-plane noise parameters; returns the device NoiseArgs.
+int prepare_noise(dppx_ctx* ctx, const dppx_noise* nz, int planes, const double* dev_injected,
+                  const BatchGeom& g, const dppx_privacy_params* pp, NoiseArgs* out,
+                  cudaStream_t stream, DevBuf& dev_seeds, uint64_t*& pinned, size_t& pinned_n,
+                  cudaEvent_t guard, bool record_guard) {
+  out->kind = nz ? nz->kind : DPPX_NOISE_NONE;
+  out->frame_base = nz ? nz->frame_base : 0;
+  out->mixed_seeds = nullptr;
+  out->injected = dev_injected;
+  if (out->kind == DPPX_NOISE_NONE) return DPPX_OK;
+  if (out->kind < 0 || out->kind > DPPX_NOISE_INJECTED)
+    return set_err(ctx, DPPX_ERR_INVALID, "unknown noise kind");
+  if (out->kind == DPPX_NOISE_INJECTED) {
+    if (!dev_injected) return set_err(ctx, DPPX_ERR_INVALID, "injected noise pointer is null");
+    return DPPX_OK;
+  }
+  // laplace_at: sigma must be > 0 (noise.cpp:112-116).
+  if (!(pp->sigma > 0.0) || (g.n > 1 && !(pp->sigma_sub > 0.0)))
+    return set_err(ctx, DPPX_ERR_INVALID, "laplace_at: sigma must be > 0");
+  if (!nz->plane_seeds) return set_err(ctx, DPPX_ERR_INVALID, "plane_seeds is null");
+  const size_t cnt = out->kind == DPPX_NOISE_KEYED ? static_cast<size_t>(planes) : 1;
+  if (guard) cudaEventSynchronize(guard);  // previous upload from `pinned` has executed
+  if (pinned_n < cnt) {
+    if (pinned) cudaFreeHost(pinned);
+    pinned = nullptr;
+    pinned_n = 0;
+    CUDA_TRY(ctx, cudaMallocHost(reinterpret_cast<void**>(&pinned), cnt * sizeof(uint64_t) + 64));
+    pinned_n = cnt;
+  }
+  for (size_t i = 0; i < cnt; ++i)
+    pinned[i] = out->kind == DPPX_NOISE_KEYED ? mix64_h(nz->plane_seeds[i]) : nz->plane_seeds[i];
+  if (int rc = ensure(ctx, dev_seeds, cnt * sizeof(uint64_t))) return rc;
+  CUDA_TRY(ctx, cudaMemcpyAsync(dev_seeds.p, pinned, cnt * sizeof(uint64_t),
+                                cudaMemcpyHostToDevice, stream));
+  if (guard && record_guard) cudaEventRecord(guard, stream);
+  out->mixed_seeds = static_cast<const uint64_t*>(dev_seeds.p);
+  return DPPX_OK;
+}
+
+int ensure_scratch(dppx_ctx* ctx, const BatchGeom& g, int planes) {
+  const size_t P = static_cast<size_t>(std::max(planes, 1));
+  if (int rc = ensure(ctx, ctx->cellinfo, P * g.G * 4)) return rc;
+  if (int rc = ensure(ctx, ctx->rowcnt, P * g.GR * 4)) return rc;
+  if (int rc = ensure(ctx, ctx->rowprefix, P * g.GR * 4)) return rc;
+  if (int rc = ensure(ctx, ctx->totals, P * 4)) return rc;
+  if (int rc = ensure(ctx, ctx->counters, P * 4, /*zero=*/true)) return rc;
+  if (int rc = ensure(ctx, ctx->status, 16, true)) return rc;
+  return DPPX_OK;
+}
+
+int classify(dppx_ctx* ctx, const BatchGeom& g, int planes, bool from_payload, const uint8_t* mask,
+             int64_t mpitch, int64_t mfstride, uint8_t* payload, const uint8_t* payload_in,
+             int64_t pstride, uint32_t* payload_len, const uint32_t* in_len) {
+  ClassifyArgs a{};
+  a.g = g;
+  a.planes = planes;
+  a.from_payload = from_payload ? 1 : 0;
+  a.mask = mask;
+  a.mpitch = mpitch;
+  a.mfstride = mfstride;
+  a.vec = 1;
+  if (!from_payload) {
+    if (g.b % 16 == 0 && aligned16(mask) && mpitch % 16 == 0 && mfstride % 16 == 0) a.vec = 16;
+    else if (g.b % 4 == 0 && (reinterpret_cast<uintptr_t>(mask) & 3) == 0 && mpitch % 4 == 0 &&
+             mfstride % 4 == 0)
+      a.vec = 4;
+  }
+  a.payload = payload;
+  a.payload_in = payload_in;
+  a.pstride = pstride;
+  a.payload_len = payload_len;
+  a.in_len = in_len;
+  a.cellinfo = static_cast<uint32_t*>(ctx->cellinfo.p);
+  a.rowcnt = static_cast<uint32_t*>(ctx->rowcnt.p);
+  a.rowprefix = static_cast<uint32_t*>(ctx->rowprefix.p);
+  a.totals = static_cast<uint32_t*>(ctx->totals.p);
+  a.counters = static_cast<uint32_t*>(ctx->counters.p);
+  a.status = static_cast<int*>(ctx->status.p);
+  a.area = static_cast<double>(g.b) * g.b;
+  PendingTiming pt;
+  timing_begin(ctx, DPPX_K_CLASSIFY, &pt);
+  CUDA_TRY(ctx, launch_classify(a, ctx->stream));
+  timing_end(ctx, &pt);
+  return DPPX_OK;
+}
+
+// K1 (fast, TMA-staged) when the geometry and alignment allow, else K1g.
+int run_stats(dppx_ctx* ctx, StatsArgs& a) {
+  const BatchGeom& g = a.g;
+  StatsKernel k = select_stats_kernel(g.C, g.b, g.n, a.adaptive != 0);
+  const bool aligned = aligned16(a.img) && a.pitch % 16 == 0 && a.fstride % 16 == 0 &&
+                       (!a.out || (aligned16(a.out) && a.opitch % 16 == 0 && a.ofstride % 16 == 0));
+  PendingTiming pt;
+  if (k && aligned && g.F > 0) {
+    const int tile = stats_tile_px();
+    a.tiles_per_row = (g.GC * g.b + tile - 1) / tile;
+    const int64_t units = static_cast<int64_t>(g.F) * g.GR * a.tiles_per_row;
+    if (units > 0x7FFFFFFF) return set_err(ctx, DPPX_ERR_INVALID, "batch too large for one launch");
+    a.units = static_cast<int>(units);
+    const size_t stage = static_cast<size_t>(g.b) * tile * g.C;
+    int S = static_cast<int>((72 * 1024) / stage);
+    S = std::max(2, std::min(stats_max_stages(), S));
+    a.stages = S;
+    const size_t smem = stage * S;
+    const auto key = std::make_pair(reinterpret_cast<const void*>(k), smem);
+    auto it = ctx->occupancy.find(key);
+    int per_sm = 0;
+    if (it == ctx->occupancy.end()) {
+      CUDA_TRY(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+      CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, stats_threads(),
+                                                                  smem));
+      ctx->occupancy[key] = per_sm;
+    } else {
+      per_sm = it->second;
+    }
+    const int grid = static_cast<int>(std::min<int64_t>(units, static_cast<int64_t>(std::max(per_sm, 1)) * ctx->sms));
+    timing_begin(ctx, DPPX_K_STATS, &pt);
+    CUDA_TRY(ctx, launch_stats_tma(k, a, grid, smem, ctx->stream));
+  } else {
+    timing_begin(ctx, DPPX_K_GENERIC, &pt);
+    if (g.F > 0) CUDA_TRY(ctx, launch_stats_generic(a, ctx->stream));
+  }
+  timing_end(ctx, &pt);
+  return DPPX_OK;
+}
+
+int check_ctx(dppx_ctx* ctx) {
+  if (!ctx) return DPPX_ERR_INVALID;
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  return DPPX_OK;
+}
+
+int check_params(dppx_ctx* ctx, const dppx_privacy_params* p, bool adaptive) {
+  if (!p) return set_err(ctx, DPPX_ERR_INVALID, "null privacy params");
+  if (!adaptive && p->n != 1)
+    return set_err(ctx, DPPX_ERR_INVALID, "pixelize_parallel: requires n == 1");
+  if (adaptive && (p->n < 1 || p->b % p->n != 0 || p->subgrid_side * p->n != p->b))
+    return set_err(ctx, DPPX_ERR_INVALID, "pixelize_adaptive: invalid subgrid factor");
+  return DPPX_OK;
+}
+
+// Device-pointer core of both pixelize entry points.
+int pixelize_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img, const uint8_t* mask,
+                 const dppx_privacy_params* pp, const dppx_noise* nz, const double* dev_injected,
+                 uint8_t* stats, int64_t sstride, uint32_t* payload_len, uint8_t* out,
+                 bool adaptive, DevBuf& dev_seeds, uint64_t*& pinned, size_t& pinned_n,
+                 cudaEvent_t guard, bool record_guard) {
+  BatchGeom g;
+  if (int rc = geometry(ctx, d->height, d->width, d->channels, d->frames, pp->b,
+                        adaptive ? pp->n : 1, &g, true))
+    return rc;
+  if (d->frames == 0) return DPPX_OK;
+  if (!img || !stats || (adaptive && !mask))
+    return set_err(ctx, DPPX_ERR_INVALID, "null image/statistics/mask pointer");
+  if (adaptive) {
+    const size_t cap = dppx_adaptive_payload_capacity(g.M, g.N, g.b, g.n);
+    if (sstride < static_cast<int64_t>(cap) || sstride % 4 != 0)
+      return set_err(ctx, DPPX_ERR_INVALID, "payload_stride must be >= %zu and a multiple of 4",
+                     cap);
+  }
+  StatsArgs a{};
+  a.g = g;
+  a.adaptive = adaptive ? 1 : 0;
+  a.img = img;
+  a.pitch = d->pitch;
+  a.fstride = d->frame_stride;
+  a.out = out;
+  a.opitch = d->out_pitch;
+  a.ofstride = d->out_frame_stride;
+  a.stats = stats;
+  a.sstride = sstride;
+  a.area = static_cast<double>(g.b) * g.b;
+  a.sub_area = static_cast<double>(g.sb) * g.sb;
+  a.sigma = pp->sigma;
+  a.sigma_sub = adaptive ? pp->sigma_sub : pp->sigma;
+  if (int rc = prepare_noise(ctx, nz, g.F * g.C, dev_injected, g, pp, &a.noise, ctx->stream,
+                             dev_seeds, pinned, pinned_n, guard, record_guard))
+    return rc;
+  if (adaptive) {
+    if (int rc = ensure_scratch(ctx, g, g.F)) return rc;
+    if (int rc = classify(ctx, g, g.F, false, mask, d->mask_pitch, d->mask_frame_stride, stats,
+                          nullptr, sstride, payload_len, nullptr))
+      return rc;
+    a.cellinfo = static_cast<const uint32_t*>(ctx->cellinfo.p);
+    a.rowprefix = static_cast<const uint32_t*>(ctx->rowprefix.p);
+    a.totals = static_cast<const uint32_t*>(ctx->totals.p);
+  }
+  return run_stats(ctx, a);
+}
+
+int expand_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* stats, int64_t sstride,
+               const uint32_t* in_len, int b, int n, uint8_t* out, bool adaptive) {
+  BatchGeom g;
+  if (int rc = geometry(ctx, d->height, d->width, d->channels, d->frames, b, adaptive ? n : 1, &g,
+                        false)) {
+    // reassemble reports a bad subgrid factor as RecordError(corrupt_record)
+    // (adaptive.cpp:188-191); dimension problems stay invalid_argument.
+    if (adaptive && (n < 1 || (b >= 1 && b % n != 0)) && b >= 1 &&
+        b <= std::max(d->height, d->width))
+      return set_err(ctx, DPPX_ERR_CORRUPT, "reassemble: subgrid factor does not divide grid side");
+    return rc;
+  }
+  if (d->frames == 0) return DPPX_OK;
+  if (!stats || !out) return set_err(ctx, DPPX_ERR_INVALID, "null statistics/output pointer");
+  ExpandArgs e{};
+  e.g = g;
+  e.adaptive = adaptive ? 1 : 0;
+  e.stats = stats;
+  e.sstride = sstride;
+  e.out = out;
+  e.opitch = d->out_pitch;
+  e.ofstride = d->out_frame_stride;
+  if (adaptive) {
+    if (sstride < 4ll * g.G + 4 || sstride % 4 != 0)
+      return set_err(ctx, DPPX_ERR_INVALID, "payload_stride too small or not a multiple of 4");
+    const int P = g.F * g.C;
+    if (int rc = ensure_scratch(ctx, g, P)) return rc;
+    if (int rc = classify(ctx, g, P, true, nullptr, 0, 0, nullptr, stats, sstride, nullptr, in_len))
+      return rc;
+    e.cellinfo = static_cast<const uint32_t*>(ctx->cellinfo.p);
+    e.rowprefix = static_cast<const uint32_t*>(ctx->rowprefix.p);
+    e.totals = static_cast<const uint32_t*>(ctx->totals.p);
+  }
+  PendingTiming pt;
+  timing_begin(ctx, DPPX_K_EXPAND, &pt);
+  CUDA_TRY(ctx, launch_expand(e, ctx->stream));
+  timing_end(ctx, &pt);
+  return DPPX_OK;
+}
+
+int read_status(dppx_ctx* ctx) {
+  if (!ctx->status.p) return DPPX_OK;
+  int st = 0;
+  CUDA_TRY(ctx, cudaMemcpy(&st, ctx->status.p, sizeof(int), cudaMemcpyDeviceToHost));
+  if (st != 0) {
+    CUDA_TRY(ctx, cudaMemset(ctx->status.p, 0, sizeof(int)));
+    return set_err(ctx, st, "reassemble: payload inconsistent (simple count or length mismatch)");
+  }
+  return DPPX_OK;
+}
+
+// ---- host pipeline -----------------------------------------------------------
+enum class HostOp { Uniform, Adaptive, Broadcast, Reassemble };
+
+int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uint8_t* img,
+                  const uint8_t* mask, const dppx_privacy_params* pp, const dppx_noise* nz,
+                  uint8_t* stats, int64_t sstride, uint32_t* lens, const uint32_t* in_lens,
+                  int b_arg, int n_arg, uint8_t* out) {
+  const bool pix = op == HostOp::Uniform || op == HostOp::Adaptive;
+  const bool adaptive = op == HostOp::Adaptive || op == HostOp::Reassemble;
+  if (!d) return set_err(ctx, DPPX_ERR_INVALID, "null frames descriptor");
+  const int b = pix ? (pp ? pp->b : 0) : b_arg;
+  const int n = pix ? (pp ? pp->n : 1) : n_arg;
+  if (pix) {
+    if (int rc = check_params(ctx, pp, adaptive)) return rc;
+  }
+  BatchGeom g;
+  if (op == HostOp::Reassemble) {
+    if (int rc = geometry(ctx, d->height, d->width, d->channels, d->frames, b, 1, &g, false))
+      return rc;
+    if (n < 1 || b % n != 0)
+      return set_err(ctx, DPPX_ERR_CORRUPT, "reassemble: subgrid factor does not divide grid side");
+    g.n = n;
+    g.sb = b / n;
+  } else if (int rc = geometry(ctx, d->height, d->width, d->channels, d->frames, b,
+                               adaptive ? n : 1, &g, pix)) {
+    return rc;
+  }
+  if (int rc = check_desc(ctx, d, op == HostOp::Adaptive, !pix || out != nullptr)) return rc;
+  const int F = d->frames, C = g.C, M = g.M, N = g.N;
+  if (F == 0) return DPPX_OK;
+  if (pix && !img) return set_err(ctx, DPPX_ERR_INVALID, "null image pointer");
+  if (op == HostOp::Adaptive && !mask) return set_err(ctx, DPPX_ERR_INVALID, "null mask pointer");
+  if (!stats) return set_err(ctx, DPPX_ERR_INVALID, "null statistics pointer");
+  if (!pix && !out) return set_err(ctx, DPPX_ERR_INVALID, "null output pointer");
+  const size_t G = static_cast<size_t>(g.G);
+  int64_t dstride;  // device statistics bytes per plane
+  if (adaptive) {
+    const size_t cap = dppx_adaptive_payload_capacity(M, N, b, n);
+    dstride = round_up(static_cast<int64_t>(cap), 16);
+    if (sstride < (op == HostOp::Adaptive ? static_cast<int64_t>(cap) : 4ll * g.G + 4))
+      return set_err(ctx, DPPX_ERR_INVALID, "payload_stride too small");
+    if (op == HostOp::Reassemble) dstride = round_up(std::max<int64_t>(sstride, 16), 16);
+  } else {
+    dstride = static_cast<int64_t>(G);
+    sstride = static_cast<int64_t>(G);
+  }
+  const int64_t dpitch = round_up(static_cast<int64_t>(N) * C, 16);
+  const int64_t dmpitch = round_up(N, 16);
+  const int64_t dfs = dpitch * M, dmfs = dmpitch * M;
+  const int64_t per_frame = (pix ? dfs : 0) + (op == HostOp::Adaptive ? dmfs : 0) +
+                            (out ? dfs : 0) + dstride * C;
+  int K = ctx->chunk_frames > 0 ? ctx->chunk_frames
+                                : static_cast<int>(std::max<int64_t>(1, (96ll << 20) / per_frame));
+  K = std::max(1, std::min(K, F));
+  const int chunks = (F + K - 1) / K;
+  const bool inj = pix && nz && nz->kind == DPPX_NOISE_INJECTED;
+  const size_t inj_plane = G * static_cast<size_t>(adaptive ? n * n : 1);
+  for (int s = 0; s < 2 && s < chunks; ++s) {
+    if (pix && ensure(ctx, ctx->img[s], static_cast<size_t>(dfs) * K)) return DPPX_ERR_OOM;
+    if (op == HostOp::Adaptive && ensure(ctx, ctx->mask[s], static_cast<size_t>(dmfs) * K))
+      return DPPX_ERR_OOM;
+    if (out && ensure(ctx, ctx->out[s], static_cast<size_t>(dfs) * K)) return DPPX_ERR_OOM;
+    if (ensure(ctx, ctx->stats[s], static_cast<size_t>(dstride) * C * K)) return DPPX_ERR_OOM;
+    if (ensure(ctx, ctx->lens[s], sizeof(uint32_t) * C * K)) return DPPX_ERR_OOM;
+    if (inj && ensure(ctx, ctx->inj[s], sizeof(double) * inj_plane * C * K)) return DPPX_ERR_OOM;
+  }
+  cudaStream_t comp = ctx->stream;
+  for (int ci = 0; ci < chunks; ++ci) {
+    const int s = ci & 1;
+    const int f0 = ci * K, Fk = std::min(K, F - f0);
+    // ---- H2D (input stream): wait until chunk ci-2 released this slot ----
+    if (ci >= 2) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->s_in, ctx->comp_done[s], 0));
+    uint8_t* dimg = static_cast<uint8_t*>(ctx->img[s].p);
+    uint8_t* dmask = static_cast<uint8_t*>(ctx->mask[s].p);
+    uint8_t* dout = static_cast<uint8_t*>(ctx->out[s].p);
+    uint8_t* dstats = static_cast<uint8_t*>(ctx->stats[s].p);
+    uint32_t* dlens = static_cast<uint32_t*>(ctx->lens[s].p);
+    if (pix) {
+      CUDA_TRY(ctx, cudaMemcpy2DAsync(dimg, dpitch, img + static_cast<int64_t>(f0) * d->frame_stride,
+                                      d->pitch, static_cast<size_t>(N) * C, M, cudaMemcpyHostToDevice,
+                                      ctx->s_in));
+      // frames beyond the first of the chunk (frame strides may differ)
+      for (int f = 1; f < Fk; ++f)
+        CUDA_TRY(ctx, cudaMemcpy2DAsync(dimg + f * dfs, dpitch,
+                                        img + static_cast<int64_t>(f0 + f) * d->frame_stride, d->pitch,
+                                        static_cast<size_t>(N) * C, M, cudaMemcpyHostToDevice,
+                                        ctx->s_in));
+      ctx->kstats.h2d_bytes += static_cast<uint64_t>(Fk) * M * N * C;
+    }
+    if (op == HostOp::Adaptive) {
+      for (int f = 0; f < Fk; ++f)
+        CUDA_TRY(ctx, cudaMemcpy2DAsync(dmask + f * dmfs, dmpitch,
+                                        mask + static_cast<int64_t>(f0 + f) * d->mask_frame_stride,
+                                        d->mask_pitch, N, M, cudaMemcpyHostToDevice, ctx->s_in));
+      ctx->kstats.h2d_bytes += static_cast<uint64_t>(Fk) * M * N;
+    }
+    if (!pix) {
+      CUDA_TRY(ctx, cudaMemcpy2DAsync(dstats, dstride, stats + static_cast<int64_t>(f0) * C * sstride,
+                                      sstride, static_cast<size_t>(std::min(sstride, dstride)),
+                                      static_cast<size_t>(Fk) * C, cudaMemcpyHostToDevice, ctx->s_in));
+      ctx->kstats.h2d_bytes += static_cast<uint64_t>(Fk) * C * std::min(sstride, dstride);
+      if (in_lens) {
+        CUDA_TRY(ctx, cudaMemcpyAsync(dlens, in_lens + static_cast<int64_t>(f0) * C,
+                                      sizeof(uint32_t) * Fk * C, cudaMemcpyHostToDevice, ctx->s_in));
+      }
+    }
+    if (inj) {
+      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->inj[s].p, nz->injected + static_cast<int64_t>(f0) * C * inj_plane,
+                                    sizeof(double) * inj_plane * C * Fk, cudaMemcpyHostToDevice,
+                                    ctx->s_in));
+    }
+    CUDA_TRY(ctx, cudaEventRecord(ctx->in_done[s], ctx->s_in));
+    // ---- compute ----
+    CUDA_TRY(ctx, cudaStreamWaitEvent(comp, ctx->in_done[s], 0));
+    if (ci >= 2) CUDA_TRY(ctx, cudaStreamWaitEvent(comp, ctx->out_done[s], 0));
+    dppx_frames_desc dd = *d;
+    dd.frames = Fk;
+    dd.pitch = dpitch;
+    dd.frame_stride = dfs;
+    dd.mask_pitch = dmpitch;
+    dd.mask_frame_stride = dmfs;
+    dd.out_pitch = dpitch;
+    dd.out_frame_stride = dfs;
+    int rc;
+    if (pix) {
+      dppx_noise cn{};
+      if (nz) {
+        cn = *nz;
+        if (nz->kind == DPPX_NOISE_KEYED && nz->plane_seeds) cn.plane_seeds = nz->plane_seeds + static_cast<int64_t>(f0) * C;
+        if (nz->kind == DPPX_NOISE_PHILOX) cn.frame_base = nz->frame_base + f0;
+      }
+      rc = pixelize_dev(ctx, &dd, dimg, dmask, pp, nz ? &cn : nullptr,
+                        inj ? static_cast<const double*>(ctx->inj[s].p) : nullptr, dstats, dstride,
+                        adaptive ? dlens : nullptr, out ? dout : nullptr, adaptive, ctx->sd[s],
+                        ctx->sd_pinned[s], ctx->sd_pinned_n[s], ctx->comp_done[s], false);
+    } else {
+      rc = expand_dev(ctx, &dd, dstats, dstride, in_lens ? dlens : nullptr, b, n, dout, adaptive);
+    }
+    if (rc) return rc;
+    CUDA_TRY(ctx, cudaEventRecord(ctx->comp_done[s], comp));
+    // ---- D2H (output stream) ----
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->s_out, ctx->comp_done[s], 0));
+    if (pix) {
+      const size_t w = adaptive ? dppx_adaptive_payload_capacity(M, N, b, n) : G;
+      CUDA_TRY(ctx, cudaMemcpy2DAsync(stats + static_cast<int64_t>(f0) * C * sstride, sstride, dstats,
+                                      dstride, w, static_cast<size_t>(Fk) * C, cudaMemcpyDeviceToHost,
+                                      ctx->s_out));
+      ctx->kstats.d2h_bytes += static_cast<uint64_t>(w) * Fk * C;
+      if (adaptive && lens) {
+        CUDA_TRY(ctx, cudaMemcpyAsync(lens + static_cast<int64_t>(f0) * C, dlens, sizeof(uint32_t) * Fk * C,
+                                      cudaMemcpyDeviceToHost, ctx->s_out));
+        ctx->kstats.d2h_bytes += sizeof(uint32_t) * Fk * C;
+      }
+    }
+    if (out) {
+      for (int f = 0; f < Fk; ++f)
+        CUDA_TRY(ctx, cudaMemcpy2DAsync(out + static_cast<int64_t>(f0 + f) * d->out_frame_stride,
+                                        d->out_pitch, dout + f * dfs, dpitch,
+                                        static_cast<size_t>(N) * C, M, cudaMemcpyDeviceToHost,
+                                        ctx->s_out));
+      ctx->kstats.d2h_bytes += static_cast<uint64_t>(Fk) * M * N * C;
+    }
+    CUDA_TRY(ctx, cudaEventRecord(ctx->out_done[s], ctx->s_out));
+  }
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->s_out));
+  CUDA_TRY(ctx, cudaStreamSynchronize(comp));
+  if (ctx->timing) collect_timings(ctx);
+  if (!pix) return read_status(ctx);
+  return DPPX_OK;
+}
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+const char* dppx_version(void) { return "dppx-b200 1 (sm_100a)"; }
+
+int dppx_grid_dims(int32_t M, int32_t N, int32_t b, dppx_geometry* out) {
+  if (!out || M < 1 || N < 1 || b < 1 || b > std::max(M, N)) return DPPX_ERR_INVALID;
+  out->b = b;  // image.cpp:59-70, 64-bit intermediates
+  out->grid_rows = static_cast<int32_t>((static_cast<int64_t>(M) + b - 1) / b);
+  out->grid_cols = static_cast<int32_t>((static_cast<int64_t>(N) + b - 1) / b);
+  out->pad_rows = static_cast<int32_t>(static_cast<int64_t>(out->grid_rows) * b - M);
+  out->pad_cols = static_cast<int32_t>(static_cast<int64_t>(out->grid_cols) * b - N);
+  return DPPX_OK;
+}
+
+double dppx_sensitivity(int32_t b, int32_t m) {
+  if (b < 1 || m < 1) return -1.0;
+  return 255.0 * m / (static_cast<double>(b) * b);  // noise.cpp:22-27
+}
+
+int dppx_make_privacy_params(double eps, int32_t m, int32_t b, int32_t n, dppx_privacy_params* p) {
+  if (!p || !(eps > 0.0) || m < 1 || b < 1 || n < 1 || b % n != 0) return DPPX_ERR_INVALID;
+  p->epsilon = eps;  // noise.cpp:39-68
+  p->m = m;
+  p->b = b;
+  p->n = n;
+  p->subgrid_side = b / n;
+  p->delta = dppx_sensitivity(b, m);
+  p->sigma = p->delta / eps;
+  p->delta_sub = dppx_sensitivity(p->subgrid_side, m);
+  p->sigma_sub = p->sigma * (static_cast<double>(n) * n);
+  return DPPX_OK;
+}
+
+uint64_t dppx_keyed_bits(uint64_t seed, uint32_t r, uint32_t c, uint32_t sr, uint32_t sc) {
+  return keyed_bits_h(seed, r, c, sr, sc);
+}
+
+double dppx_uniform_from_bits(uint64_t bits) {  // noise.cpp:93-105
+  const double k = 0x1.0p-53, half = 0.5 - k;
+  const double u = static_cast<double>(bits >> 11) * k - 0.5;
+  return u <= -half ? -half : (u >= half ? half : u);
+}
+
+double dppx_laplace_at(uint64_t seed, uint32_t r, uint32_t c, uint32_t sr, uint32_t sc,
+                       double sigma) {
+  if (!(sigma > 0.0)) return std::nan("");
+  const double u = dppx_uniform_from_bits(keyed_bits_h(seed, r, c, sr, sc));
+  const double sign = u < 0.0 ? -1.0 : 1.0;  // noise.cpp:107-110
+  return sign * sigma * -std::log1p(-2.0 * std::fabs(u));
+}
+
+uint64_t dppx_derive_plane_seed(uint64_t seed, uint32_t frame, uint32_t channel) {
+  return keyed_bits_h(seed, frame, channel, 0xFFFFFFFFu, 0xFFFFFFFFu);
+}
+
+size_t dppx_adaptive_payload_capacity(int32_t M, int32_t N, int32_t b, int32_t n) {
+  dppx_geometry g;
+  if (dppx_grid_dims(M, N, b, &g) != DPPX_OK || n < 1) return 0;
+  const size_t G = static_cast<size_t>(g.grid_rows) * g.grid_cols;
+  return 4 * G + 4 + G * static_cast<size_t>(n) * n;
+}
+
+size_t dppx_adaptive_payload_length(int32_t M, int32_t N, int32_t b, int32_t n, uint32_t S) {
+  dppx_geometry g;
+  if (dppx_grid_dims(M, N, b, &g) != DPPX_OK || n < 1) return 0;
+  const size_t G = static_cast<size_t>(g.grid_rows) * g.grid_cols;
+  if (S > G) return 0;
+  return 4 * G + 4 + S + (G - S) * static_cast<size_t>(n) * n;
+}
+
+int dppx_ctx_create(int32_t device, dppx_ctx** out) {
+  if (!out) return DPPX_ERR_INVALID;
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) return DPPX_ERR_NO_DEVICE;
+  if (device < 0 || device >= count) return DPPX_ERR_INVALID;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return DPPX_ERR_NO_DEVICE;
+  if (prop.major != 10 || prop.minor != 0) return DPPX_ERR_NO_DEVICE;  // built for sm_100a only
+  dppx_ctx* ctx = new dppx_ctx();
+  ctx->device = device;
+  ctx->sms = prop.multiProcessorCount;
+  if (cudaSetDevice(device) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->s_in, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->s_out, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return DPPX_ERR_CUDA;
+  }
+  ctx->stream = ctx->own_stream;
+  for (int s = 0; s < 2; ++s) {
+    cudaEventCreateWithFlags(&ctx->in_done[s], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->comp_done[s], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->out_done[s], cudaEventDisableTiming);
+  }
+  cudaEventCreateWithFlags(&ctx->seeds_ev, cudaEventDisableTiming);
+  cudaEventRecord(ctx->seeds_ev, ctx->stream);
+  // Verify that the sm_100a kernels load on this device (no silent fallback).
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(
+                                     select_stats_kernel(3, 16, 4, true))) != cudaSuccess) {
+    dppx_ctx_destroy(ctx);
+    return DPPX_ERR_NO_DEVICE;
+  }
+  *out = ctx;
+  return DPPX_OK;
+}
+
+void dppx_ctx_destroy(dppx_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  DevBuf* bufs[] = {&ctx->cellinfo, &ctx->rowcnt, &ctx->rowprefix, &ctx->totals, &ctx->counters,
+                    &ctx->status, &ctx->seeds, &ctx->keys, &ctx->dbl};
+  for (DevBuf* b : bufs)
+    if (b->p) cudaFree(b->p);
+  for (int s = 0; s < 2; ++s) {
+    DevBuf* sb[] = {&ctx->img[s], &ctx->mask[s], &ctx->out[s], &ctx->stats[s],
+                    &ctx->lens[s], &ctx->inj[s], &ctx->sd[s]};
+    for (DevBuf* b : sb)
+      if (b->p) cudaFree(b->p);
+    if (ctx->sd_pinned[s]) cudaFreeHost(ctx->sd_pinned[s]);
+    cudaEventDestroy(ctx->in_done[s]);
+    cudaEventDestroy(ctx->comp_done[s]);
+    cudaEventDestroy(ctx->out_done[s]);
+  }
+  if (ctx->seeds_pinned) cudaFreeHost(ctx->seeds_pinned);
+  cudaEventDestroy(ctx->seeds_ev);
+  for (auto& pt : ctx->pending) {
+    cudaEventDestroy(pt.start);
+    cudaEventDestroy(pt.stop);
+  }
+  for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
+  cudaStreamDestroy(ctx->own_stream);
+  cudaStreamDestroy(ctx->s_in);
+  cudaStreamDestroy(ctx->s_out);
+  delete ctx;
+}
+
+const char* dppx_ctx_last_error(const dppx_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+void* dppx_ctx_stream(dppx_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int dppx_ctx_set_stream(dppx_ctx* ctx, void* stream) {
+  if (!ctx) return DPPX_ERR_INVALID;
+  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  return DPPX_OK;
+}
+
+int dppx_ctx_synchronize(dppx_ctx* ctx) {
+  if (int rc = check_ctx(ctx)) return rc;
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (ctx->timing) collect_timings(ctx);
+  return read_status(ctx);
+}
+
+int dppx_ctx_set_timing(dppx_ctx* ctx, int32_t on) {
+  if (!ctx) return DPPX_ERR_INVALID;
+  ctx->timing = on != 0;
+  return DPPX_OK;
+}
+
+int dppx_ctx_get_stats(dppx_ctx* ctx, dppx_kernel_stats* out) {
+  if (!ctx || !out) return DPPX_ERR_INVALID;
+  if (!ctx->pending.empty()) {
+    cudaSetDevice(ctx->device);
+    collect_timings(ctx);
+  }
+  *out = ctx->kstats;
+  return DPPX_OK;
+}
+
+int dppx_ctx_reset_stats(dppx_ctx* ctx) {
+  if (!ctx) return DPPX_ERR_INVALID;
+  if (!ctx->pending.empty()) collect_timings(ctx);
+  ctx->kstats = dppx_kernel_stats{};
+  return DPPX_OK;
+}
+
+int dppx_ctx_set_chunk_frames(dppx_ctx* ctx, int32_t frames) {
+  if (!ctx || frames < 0) return DPPX_ERR_INVALID;
+  ctx->chunk_frames = frames;
+  return DPPX_OK;
+}
+
+int dppx_host_alloc(size_t bytes, void** out) {
+  if (!out) return DPPX_ERR_INVALID;
+  return cudaMallocHost(out, bytes) == cudaSuccess ? DPPX_OK : DPPX_ERR_OOM;
+}
+
+void dppx_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+int dppx_pixelize_uniform_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img,
+                              const dppx_privacy_params* pp, const dppx_noise* nz, uint8_t* means,
+                              uint8_t* out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = check_params(ctx, pp, false)) return rc;
+  if (int rc = check_desc(ctx, d, false, out != nullptr)) return rc;
+  BatchGeom g;
+  if (int rc = geometry(ctx, d->height, d->width, d->channels, d->frames, pp->b, 1, &g, true))
+    return rc;
+  return pixelize_dev(ctx, d, img, nullptr, pp, nz, nz ? nz->injected : nullptr, means, g.G,
+                      nullptr, out, false, ctx->seeds, ctx->seeds_pinned, ctx->seeds_pinned_n,
+                      ctx->seeds_ev, true);
+}
+
+int dppx_pixelize_adaptive_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img,
+                               const uint8_t* mask, const dppx_privacy_params* pp,
+                               const dppx_noise* nz, uint8_t* payload, int64_t payload_stride,
+                               uint32_t* payload_len, uint8_t* out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = check_params(ctx, pp, true)) return rc;
+  if (int rc = check_desc(ctx, d, true, out != nullptr)) return rc;
+  return pixelize_dev(ctx, d, img, mask, pp, nz, nz ? nz->injected : nullptr, payload,
+                      payload_stride, payload_len, out, true, ctx->seeds, ctx->seeds_pinned,
+                      ctx->seeds_pinned_n, ctx->seeds_ev, true);
+}
+
+int dppx_broadcast_means_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* means,
+                             int32_t b, uint8_t* out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = check_desc(ctx, d, false, true)) return rc;
+  dppx_geometry gg;
+  if (dppx_grid_dims(d->height, d->width, b, &gg) != DPPX_OK)
+    return set_err(ctx, DPPX_ERR_INVALID, "broadcast_means: means do not fit the target dimensions");
+  return expand_dev(ctx, d, means, static_cast<int64_t>(gg.grid_rows) * gg.grid_cols, nullptr, b, 1,
+                    out, false);
+}
+
+int dppx_reassemble_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* payload,
+                        int64_t payload_stride, const uint32_t* payload_len, int32_t b, int32_t n,
+                        uint8_t* out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = check_desc(ctx, d, false, true)) return rc;
+  if (int rc = ensure(ctx, ctx->status, 16, true)) return rc;
+  return expand_dev(ctx, d, payload, payload_stride, payload_len, b, n, out, true);
+}
+
+int dppx_synth_frames_dev(dppx_ctx* ctx, const dppx_frames_desc* d, uint32_t data_seed, uint32_t f0,
+                          uint8_t* img, uint8_t* mask) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = check_desc(ctx, d, mask != nullptr, false)) return rc;
+  if (!img) return set_err(ctx, DPPX_ERR_INVALID, "null image pointer");
+  BatchGeom g{};
+  g.M = d->height;
+  g.N = d->width;
+  g.C = d->channels;
+  g.F = d->frames;
+  PendingTiming pt;
+  timing_begin(ctx, DPPX_K_AUX, &pt);
+  CUDA_TRY(ctx, launch_synth(g, data_seed, f0, img, d->pitch, d->frame_stride, mask, d->mask_pitch,
+                             d->mask_frame_stride, ctx->stream));
+  timing_end(ctx, &pt);
+  return DPPX_OK;
+}
+
+int dppx_pixelize_uniform(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img,
+                          const dppx_privacy_params* pp, const dppx_noise* nz, uint8_t* means,
+                          uint8_t* out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  return host_pipeline(ctx, HostOp::Uniform, d, img, nullptr, pp, nz, means, 0, nullptr, nullptr, 0,
+                       1, out);
+}
+
+int dppx_pixelize_adaptive(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img,
+                           const uint8_t* mask, const dppx_privacy_params* pp, const dppx_noise* nz,
+                           uint8_t* payload, int64_t payload_stride, uint32_t* payload_len,
+                           uint8_t* out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  return host_pipeline(ctx, HostOp::Adaptive, d, img, mask, pp, nz, payload, payload_stride,
+                       payload_len, nullptr, 0, 0, out);
+}
+
+int dppx_broadcast_means(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* means, int32_t b,
+                         uint8_t* out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (d) {
+    dppx_geometry gg;
+    if (dppx_grid_dims(d->height, d->width, b, &gg) != DPPX_OK)
+      return set_err(ctx, DPPX_ERR_INVALID, "broadcast_means: means do not fit the target dimensions");
+  }
+  return host_pipeline(ctx, HostOp::Broadcast, d, nullptr, nullptr, nullptr, nullptr,
+                       const_cast<uint8_t*>(means), 0, nullptr, nullptr, b, 1, out);
+}
+
+int dppx_reassemble(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* payload,
+                    int64_t payload_stride, const uint32_t* payload_len, int32_t b, int32_t n,
+                    uint8_t* out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = ensure(ctx, ctx->status, 16, true)) return rc;
+  return host_pipeline(ctx, HostOp::Reassemble, d, nullptr, nullptr, nullptr, nullptr,
+                       const_cast<uint8_t*>(payload), payload_stride, nullptr, payload_len, b, n,
+                       out);
+}
+
+int dppx_classify_regions(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* mask, int32_t b,
+                          float* mask_means) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (!d || !mask || !mask_means) return set_err(ctx, DPPX_ERR_INVALID, "null argument");
+  if (d->mask_pitch < d->width || d->mask_frame_stride < d->mask_pitch * d->height)
+    return set_err(ctx, DPPX_ERR_INVALID, "mask pitch/frame_stride too small");
+  BatchGeom g;
+  if (int rc = geometry(ctx, d->height, d->width, 1, d->frames, b, 1, &g, true)) return rc;
+  if (g.F == 0) return DPPX_OK;
+  const int64_t mp = round_up(g.N, 16), mfs = mp * g.M;
+  const int64_t ps = round_up(4ll * g.G + 4, 16);
+  if (int rc = ensure(ctx, ctx->mask[0], static_cast<size_t>(mfs) * g.F)) return rc;
+  if (int rc = ensure(ctx, ctx->stats[0], static_cast<size_t>(ps) * g.F)) return rc;
+  if (int rc = ensure_scratch(ctx, g, g.F)) return rc;
+  for (int f = 0; f < g.F; ++f)
+    CUDA_TRY(ctx, cudaMemcpy2DAsync(static_cast<uint8_t*>(ctx->mask[0].p) + f * mfs, mp,
+                                    mask + static_cast<int64_t>(f) * d->mask_frame_stride,
+                                    d->mask_pitch, g.N, g.M, cudaMemcpyHostToDevice, ctx->stream));
+  if (int rc = classify(ctx, g, g.F, false, static_cast<const uint8_t*>(ctx->mask[0].p), mp, mfs,
+                        static_cast<uint8_t*>(ctx->stats[0].p), nullptr, ps, nullptr, nullptr))
+    return rc;
+  CUDA_TRY(ctx, cudaMemcpy2DAsync(mask_means, 4ll * g.G, ctx->stats[0].p, ps, 4ll * g.G, g.F,
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (ctx->timing) collect_timings(ctx);
+  return DPPX_OK;
+}
+
+int dppx_debug_device_laplace(dppx_ctx* ctx, uint64_t seed, const uint32_t* keys, int32_t count,
+                              double sigma, double* out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (count <= 0 || !keys || !out) return set_err(ctx, DPPX_ERR_INVALID, "bad arguments");
+  if (int rc = ensure(ctx, ctx->keys, sizeof(uint32_t) * 4 * count)) return rc;
+  if (int rc = ensure(ctx, ctx->dbl, sizeof(double) * count)) return rc;
+  CUDA_TRY(ctx, cudaMemcpy(ctx->keys.p, keys, sizeof(uint32_t) * 4 * count, cudaMemcpyHostToDevice));
+  CUDA_TRY(ctx, launch_debug_laplace(mix64_h(seed), static_cast<const uint32_t*>(ctx->keys.p), count,
+                                     sigma, static_cast<double*>(ctx->dbl.p), ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpy(out, ctx->dbl.p, sizeof(double) * count, cudaMemcpyDeviceToHost));
+  return DPPX_OK;
+}
+
+}  // extern "C"

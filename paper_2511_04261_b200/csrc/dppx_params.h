@@ -1,0 +1,81 @@
+// dppx_params.h -- launch-argument structs shared by the host runtime
+// (capi.cu) and the kernels (kernels.cu). Plain data, passed by value.
+#pragma once
+
+#include <cstdint>
+
+#include "../../include/dppx_gpu.h"
+
+namespace dppx {
+
+// Geometry of one batch (GridGeometry image.hpp:71-82, plus batch shape).
+struct BatchGeom {
+  int M, N, C, F;         // rows, cols, channels, frames
+  int b, n, sb;           // grid side, subgrid factor, subgrid side
+  int GR, GC, G, PR, PC;  // grid_dims (image.cpp:48-72)
+};
+
+struct NoiseArgs {
+  int kind;
+  uint32_t frame_base;
+  const uint64_t* mixed_seeds;  // device: KEYED mix64(seed) per plane; PHILOX [0]=seed
+  const double* injected;       // device
+};
+
+// K0: region classification + packed-slot scan.
+struct ClassifyArgs {
+  BatchGeom g;
+  int planes;                // P: F (mask per frame) or F*C (payload per plane)
+  int from_payload;          // 0: sum the u8 mask; 1: mask means read from payloads
+  const uint8_t* mask;       // from_payload == 0
+  int64_t mpitch, mfstride;
+  int vec;                   // 16, 4 or 1: widest aligned load for the mask rows
+  uint8_t* payload;          // from_payload == 0: mask means + S written for C planes
+  const uint8_t* payload_in; // from_payload == 1
+  int64_t pstride;
+  uint32_t* payload_len;     // nullable (written)
+  const uint32_t* in_len;    // nullable (checked, from_payload == 1)
+  uint32_t* cellinfo;        // [P][G]  (intra-row exclusive simple prefix << 1) | simple
+  uint32_t* rowcnt;          // [P][GR]
+  uint32_t* rowprefix;       // [P][GR]
+  uint32_t* totals;          // [P]
+  uint32_t* counters;        // [P] self-resetting arrival tickets
+  int* status;               // set to DPPX_ERR_CORRUPT on inconsistent payloads
+  double area;               // (double)b*b
+};
+
+// K1 / K1g: fused statistics, noise, compact store and reconstruction.
+struct StatsArgs {
+  BatchGeom g;
+  int adaptive;
+  const uint8_t* img;
+  int64_t pitch, fstride;
+  uint8_t* out;              // nullable
+  int64_t opitch, ofstride;
+  uint8_t* stats;            // uniform: means; adaptive: payload slots
+  int64_t sstride;           // bytes between planes of `stats`
+  const uint32_t* cellinfo;  // adaptive: [F][G]
+  const uint32_t* rowprefix; // adaptive: [F][GR]
+  const uint32_t* totals;    // adaptive: [F]
+  double area, sub_area, sigma, sigma_sub;
+  NoiseArgs noise;
+  // K1 (staged) only
+  int tiles_per_row;
+  int units;
+  int stages;
+};
+
+// K2: statistics -> pixels.
+struct ExpandArgs {
+  BatchGeom g;
+  int adaptive;
+  const uint8_t* stats;
+  int64_t sstride;
+  const uint32_t* cellinfo;  // adaptive: [F*C][G]
+  const uint32_t* rowprefix; // adaptive: [F*C][GR]
+  const uint32_t* totals;    // adaptive: [F*C]
+  uint8_t* out;
+  int64_t opitch, ofstride;
+};
+
+}  // namespace dppx

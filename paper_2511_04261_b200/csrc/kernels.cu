@@ -1,0 +1,729 @@
+// kernels.cu -- sm_100a kernels of the dppix pixelization path.
+//
+//  K0  k_classify      mask (or stored mask means) -> per-cell simple/complex
+//                      flag, intra-row packed-slot prefix, per-row counts; the
+//                      last CTA of each plane scans the rows (no spin waits).
+//                      classify_regions adaptive.cpp:34-65 + the exclusive scan
+//                      adaptive.cpp:123-141.
+//  K1  k_stats_tma     persistent, warp-specialized: one producer warp stages
+//                      b-row x 512-px tiles of interleaved u8 frames into shared
+//                      memory with cp.async.bulk (TMA) on an mbarrier ring; four
+//                      consumer warps reduce 4-px strips with dp4a + warp
+//                      shuffles, draw the keyed Laplace noise, write the compact
+//                      statistics, and overwrite the tile in place with the
+//                      reconstructed pixels that the producer bulk-stores back.
+//                      grid_mean/block_sum image.cpp:154-189 adaptive.cpp:70-79,
+//                      noise adaptive.cpp:147-170 pixelize.cpp:109-117,
+//                      broadcast_means pixelize.cpp:126-150, reassemble
+//                      adaptive.cpp:181-245.
+//  K1g k_stats_generic same semantics for any b, n, C and alignment.
+//  K2  k_expand        statistics -> pixels (broadcast_means / reassemble).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "dppx_device.cuh"
+#include "dppx_params.h"
+
+namespace dppx {
+
+// ============================================================================
+// K0: classification + slot scan
+// ============================================================================
+constexpr int kClassifyThreads = 256;
+
+__device__ __forceinline__ uint32_t sum_bytes4(uint32_t w) { return __dp4a(w, 0x01010101u, 0u); }
+
+// Exclusive block scan of 0/1 flags (256 threads). Returns the exclusive
+// prefix; *total receives the block total. Uses `warp_tot` (8 words) of smem.
+__device__ __forceinline__ uint32_t block_scan_flags(bool flag, uint32_t* warp_tot,
+                                                     uint32_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t bal = __ballot_sync(0xFFFFFFFFu, flag);
+  const uint32_t in_warp = __popc(bal & ((1u << lane) - 1u));
+  if (lane == 0) warp_tot[warp] = __popc(bal);
+  __syncthreads();
+  uint32_t before = 0, all = 0;
+#pragma unroll
+  for (int w = 0; w < kClassifyThreads / 32; ++w) {
+    const uint32_t v = warp_tot[w];
+    before += (w < warp) ? v : 0u;
+    all += v;
+  }
+  __syncthreads();
+  *total = all;
+  return before + in_warp;
+}
+
+// Exclusive block scan of u32 values (256 threads).
+__device__ __forceinline__ uint32_t block_scan_u32(uint32_t v, uint32_t* warp_tot,
+                                                   uint32_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[warp] = x;
+  __syncthreads();
+  uint32_t before = 0, all = 0;
+#pragma unroll
+  for (int w = 0; w < kClassifyThreads / 32; ++w) {
+    const uint32_t t = warp_tot[w];
+    before += (w < warp) ? t : 0u;
+    all += t;
+  }
+  __syncthreads();
+  *total = all;
+  return before + x - v;
+}
+
+__device__ __forceinline__ uint32_t mask_cell_sum(const ClassifyArgs& a, const uint8_t* base,
+                                                  int r, int c) {
+  const BatchGeom& g = a.g;
+  const int b = g.b;
+  const int j0 = c * b;
+  uint32_t s = 0;
+  const bool inside = j0 + b <= g.N;
+  for (int i = r * b; i < r * b + b; ++i) {
+    const uint8_t* row = base + static_cast<int64_t>(reflect_index(i, g.M)) * a.mpitch;
+    if (inside && a.vec == 16) {
+      const uint4* p = reinterpret_cast<const uint4*>(row + j0);
+      for (int k = 0; k < b / 16; ++k) {
+        const uint4 v = __ldg(p + k);
+        s += sum_bytes4(v.x) + sum_bytes4(v.y) + sum_bytes4(v.z) + sum_bytes4(v.w);
+      }
+    } else if (inside && a.vec == 4) {
+      const uint32_t* p = reinterpret_cast<const uint32_t*>(row + j0);
+      for (int k = 0; k < b / 4; ++k) s += sum_bytes4(__ldg(p + k));
+    } else {
+      for (int j = j0; j < j0 + b; ++j) s += __ldg(row + reflect_index(j, g.N));
+    }
+  }
+  return s;
+}
+
+__global__ void __launch_bounds__(kClassifyThreads) k_classify(const ClassifyArgs a) {
+  __shared__ uint32_t warp_tot[kClassifyThreads / 32];
+  __shared__ uint32_t s_last;
+  const BatchGeom& g = a.g;
+  const int r = blockIdx.x;
+  for (int p = blockIdx.y; p < a.planes; p += gridDim.y) {
+    const uint8_t* mbase = a.from_payload ? nullptr : a.mask + static_cast<int64_t>(p) * a.mfstride;
+    const float* mm_in =
+        a.from_payload ? reinterpret_cast<const float*>(a.payload_in + p * a.pstride) : nullptr;
+    uint32_t carry = 0;
+    for (int c0 = 0; c0 < g.GC; c0 += kClassifyThreads) {
+      const int c = c0 + threadIdx.x;
+      bool simple = false;
+      if (c < g.GC) {
+        const int cell = r * g.GC + c;
+        float mean;
+        if (a.from_payload) {
+          mean = mm_in[cell];
+        } else {
+          const uint32_t s = mask_cell_sum(a, mbase, r, c);
+          // mask_grid_mean (image.cpp:191-202) then static_cast<float>
+          // (adaptive.cpp:59-60).
+          mean = __double2float_rn(__ddiv_rn(static_cast<double>(s), a.area));
+          for (int ch = 0; ch < g.C; ++ch)
+            reinterpret_cast<float*>(a.payload + (static_cast<int64_t>(p) * g.C + ch) * a.pstride)
+                [cell] = mean;
+        }
+        simple = mean > 0.5f;  // simple_from_mean, adaptive.cpp:30-32
+      }
+      uint32_t tot;
+      const uint32_t pre = block_scan_flags(simple, warp_tot, &tot);
+      if (c < g.GC)
+        a.cellinfo[static_cast<int64_t>(p) * g.G + r * g.GC + c] =
+            ((carry + pre) << 1) | (simple ? 1u : 0u);
+      carry += tot;
+    }
+    if (threadIdx.x == 0) {
+      a.rowcnt[static_cast<int64_t>(p) * g.GR + r] = carry;
+      __threadfence();
+      const uint32_t ticket = atomicAdd(&a.counters[p], 1u);
+      s_last = (ticket == static_cast<uint32_t>(g.GR - 1)) ? 1u : 0u;
+    }
+    __syncthreads();
+    if (s_last) {  // last row of plane p: exclusive scan over rows
+      __threadfence();
+      uint32_t rcarry = 0;
+      for (int r0 = 0; r0 < g.GR; r0 += kClassifyThreads) {
+        const int rr = r0 + threadIdx.x;
+        const uint32_t v = rr < g.GR ? __ldcg(&a.rowcnt[static_cast<int64_t>(p) * g.GR + rr]) : 0u;
+        uint32_t tot;
+        const uint32_t pre = block_scan_u32(v, warp_tot, &tot);
+        if (rr < g.GR) a.rowprefix[static_cast<int64_t>(p) * g.GR + rr] = rcarry + pre;
+        rcarry += tot;
+      }
+      if (threadIdx.x == 0) {
+        const uint32_t S = rcarry;
+        a.totals[p] = S;
+        a.counters[p] = 0u;  // ready for the next launch
+        const uint64_t nn = static_cast<uint64_t>(g.n) * g.n;
+        const uint32_t len = static_cast<uint32_t>(4ull * g.G + 4 + S + (g.G - S) * nn);
+        if (a.from_payload) {
+          const uint8_t* q = a.payload_in + p * a.pstride + 4ll * g.G;
+          const uint32_t stored = static_cast<uint32_t>(q[0]) | (static_cast<uint32_t>(q[1]) << 8) |
+                                  (static_cast<uint32_t>(q[2]) << 16) |
+                                  (static_cast<uint32_t>(q[3]) << 24);
+          // decode's simple-count and length checks (record.cpp:253-270).
+          if (stored != S || (a.in_len && a.in_len[p] != len) || len > a.pstride)
+            atomicExch(a.status, DPPX_ERR_CORRUPT);
+        } else {
+          for (int ch = 0; ch < g.C; ++ch) {
+            const int64_t q = (static_cast<int64_t>(p) * g.C + ch) * a.pstride + 4ll * g.G;
+            *reinterpret_cast<uint32_t*>(a.payload + q) = S;
+            if (a.payload_len) a.payload_len[static_cast<int64_t>(p) * g.C + ch] = len;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ============================================================================
+// Shared helpers for K1 / K1g: per-statistic value and packed destination
+// ============================================================================
+
+// Packed destination of a statistic of plane p (uniform: means[g];
+// adaptive simple: 4G+4+slot; adaptive complex: 4G+4+S+slot*n*n+sr*n+sc).
+__device__ __forceinline__ int64_t stat_offset(const StatsArgs& a, bool simple, int g_idx,
+                                               uint32_t slot_s, uint32_t S_tot, int sr, int sc) {
+  if (!a.adaptive) return g_idx;
+  const int64_t base = 4ll * a.g.G + 4;
+  if (simple) return base + slot_s;
+  const uint32_t slot_c = static_cast<uint32_t>(g_idx) - slot_s;
+  return base + S_tot + static_cast<int64_t>(slot_c) * a.g.n * a.g.n + sr * a.g.n + sc;
+}
+
+__device__ __forceinline__ uint32_t stat_value(const StatsArgs& a, uint32_t sum, bool whole_cell,
+                                               int f, int ch, int r, int c, int sr, int sc) {
+  const uint32_t plane = static_cast<uint32_t>(f * a.g.C + ch);
+  const double mean = cell_mean(sum, whole_cell ? a.area : a.sub_area);
+  const uint64_t cs =
+      a.noise.kind == DPPX_NOISE_KEYED ? key_cell(a.noise.mixed_seeds[plane], r, c) : 0ull;
+  NoiseView nv{a.noise.kind, a.noise.frame_base, a.noise.mixed_seeds, a.noise.injected};
+  const double noise = draw_noise(nv, plane, f, ch, cs, r, c, sr, sc, r * a.g.GC + c, a.g.G,
+                                  a.g.n, whole_cell ? a.sigma : a.sigma_sub);
+  return finalize_value(mean, noise);
+}
+
+// ============================================================================
+// K1: TMA-staged persistent kernel (fast path)
+// ============================================================================
+constexpr int kConsumers = 128;            // 4 consumer warps, one 4-px strip each
+constexpr int kTilePx = 4 * kConsumers;    // 512 px per tile
+constexpr int kStatsThreads = kConsumers + 32;
+constexpr int kMaxStages = 4;
+
+struct UnitPos {
+  int f, r, tile, px0;
+};
+
+__device__ __forceinline__ UnitPos decode_unit(const StatsArgs& a, int u) {
+  UnitPos p;
+  p.tile = u % a.tiles_per_row;
+  const int rest = u / a.tiles_per_row;
+  p.r = rest % a.g.GR;
+  p.f = rest / a.g.GR;
+  p.px0 = p.tile * kTilePx;
+  return p;
+}
+
+template <int C>
+__device__ __forceinline__ int valid_bytes(const StatsArgs& a, int px0) {
+  return min(kTilePx, a.g.N - px0) * C;
+}
+
+template <int C, int B>
+__device__ __forceinline__ void load_unit(const StatsArgs& a, int u, uint8_t* st, uint64_t* bar) {
+  const UnitPos p = decode_unit(a, u);
+  const uint32_t copy = static_cast<uint32_t>(valid_bytes<C>(a, p.px0)) & ~15u;
+  mbar_arrive_expect_tx(bar, copy * B);
+  if (copy == 0) return;
+  const uint8_t* src = a.img + static_cast<int64_t>(p.f) * a.fstride + static_cast<int64_t>(p.px0) * C;
+#pragma unroll 1
+  for (int i = 0; i < B; ++i) {
+    const int srow = reflect_index(p.r * B + i, a.g.M);
+    bulk_g2s(st + i * (kTilePx * C), src + static_cast<int64_t>(srow) * a.pitch, copy, bar);
+  }
+}
+
+template <int C, int B>
+__device__ __forceinline__ void store_unit(const StatsArgs& a, int u, const uint8_t* st) {
+  const UnitPos p = decode_unit(a, u);
+  const uint32_t copy = static_cast<uint32_t>(valid_bytes<C>(a, p.px0)) & ~15u;
+  if (copy == 0) return;
+  uint8_t* dst = a.out + static_cast<int64_t>(p.f) * a.ofstride + static_cast<int64_t>(p.px0) * C;
+  const int rows = min(B, a.g.M - p.r * B);
+#pragma unroll 1
+  for (int i = 0; i < rows; ++i)
+    bulk_s2g(dst + static_cast<int64_t>(p.r * B + i) * a.opitch, st + i * (kTilePx * C), copy);
+  bulk_commit();
+  bulk_wait_read_all();
+}
+
+// Byte k (0..4C-1) of a 4-pixel strip of value v[] (interleaved channels).
+template <int C>
+__device__ __forceinline__ void pattern_words(const uint32_t (&v)[C], uint32_t (&w)[C]) {
+  if constexpr (C == 1) {
+    w[0] = v[0] * 0x01010101u;
+  } else if constexpr (C == 3) {
+    w[0] = v[0] | (v[1] << 8) | (v[2] << 16) | (v[0] << 24);
+    w[1] = v[1] | (v[2] << 8) | (v[0] << 16) | (v[1] << 24);
+    w[2] = v[2] | (v[0] << 8) | (v[1] << 16) | (v[2] << 24);
+  } else {  // C == 4: one pixel per word
+#pragma unroll
+    for (int k = 0; k < 4; ++k) w[k] = v[0] | (v[1] << 8) | (v[2] << 16) | (v[3] << 24);
+  }
+}
+
+// Per-channel byte sums of one 4-px strip row held in C words.
+template <int C>
+__device__ __forceinline__ void accumulate_row(const uint8_t* row, uint32_t (&acc)[C]) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(row);
+  if constexpr (C == 1) {
+    acc[0] = __dp4a(w[0], 0x01010101u, acc[0]);
+  } else if constexpr (C == 3) {
+    const uint32_t w0 = w[0], w1 = w[1], w2 = w[2];
+    // bytes: w0 = R G B R, w1 = G B R G, w2 = B R G B (little-endian)
+    acc[0] = __dp4a(w0, 0x01000001u, __dp4a(w1, 0x00010000u, __dp4a(w2, 0x00000100u, acc[0])));
+    acc[1] = __dp4a(w0, 0x00000100u, __dp4a(w1, 0x01000001u, __dp4a(w2, 0x00010000u, acc[1])));
+    acc[2] = __dp4a(w0, 0x00010000u, __dp4a(w1, 0x00000100u, __dp4a(w2, 0x01000001u, acc[2])));
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t x = w[k];
+      acc[0] += x & 0xFF;
+      acc[1] += (x >> 8) & 0xFF;
+      acc[2] += (x >> 16) & 0xFF;
+      acc[3] += x >> 24;
+    }
+  }
+}
+
+// Values of the C channels of one statistic, computed by the GL lanes of a
+// lane group (each lane draws a subset of channels) and shared by shuffles.
+template <int C, int GL>
+__device__ __forceinline__ void group_values(const StatsArgs& a, bool active, const uint32_t (&sum)[C],
+                                             bool whole, int f, int r, int c, int sr, int sc,
+                                             uint32_t (&val)[C]) {
+  const int lane = threadIdx.x & 31;
+  const int li = lane % GL;
+  const int gb = lane - li;
+#pragma unroll
+  for (int c0 = 0; c0 < C; c0 += GL) {
+    const int ch = c0 + li;
+    uint32_t v = 0;
+    if (active && ch < C) {
+      uint32_t s = sum[0];
+#pragma unroll
+      for (int k = 1; k < C; ++k)
+        if (ch == k) s = sum[k];
+      v = stat_value(a, s, whole, f, ch, r, c, sr, sc);
+    }
+#pragma unroll
+    for (int k = c0; k < C && k < c0 + GL; ++k)
+      val[k] = (GL == 1) ? v : __shfl_sync(0xFFFFFFFFu, v, gb + (k - c0));
+  }
+}
+
+template <int C, int B4, int NSUB, bool ADAPTIVE>
+__global__ void __launch_bounds__(kStatsThreads) k_stats_tma(const StatsArgs a) {
+  constexpr int B = 4 * B4;
+  constexpr int SB = B / NSUB;
+  constexpr int SB4 = SB / 4;
+  constexpr int ROWB = kTilePx * C;
+  constexpr uint32_t STAGE = B * ROWB;
+  static_assert(SB % 4 == 0 && 32 % B4 == 0, "fast-path geometry");
+
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full_bar[kMaxStages];
+  __shared__ __align__(8) uint64_t done_bar[kMaxStages];
+
+  const int S = a.stages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&done_bar[s], kConsumers);
+    }
+    fence_mbarrier_init();
+  }
+  __syncthreads();
+
+  if (warp == kConsumers / 32) {
+    // ---------------- producer warp: TMA loads + bulk stores ----------------
+    if (lane == 0) {
+      int k = 0;
+      for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++k) {
+        const int s = k % S;
+        if (k >= S) {
+          mbar_wait(&done_bar[s], ((k / S) - 1) & 1);
+          if (a.out) store_unit<C, B>(a, u - S * static_cast<int>(gridDim.x), smem + s * STAGE);
+        }
+        load_unit<C, B>(a, u, smem + s * STAGE, &full_bar[s]);
+      }
+      for (int j = k > S ? k - S : 0; j < k; ++j) {
+        const int s = j % S;
+        mbar_wait(&done_bar[s], (j / S) & 1);
+        if (a.out) store_unit<C, B>(a, blockIdx.x + j * gridDim.x, smem + s * STAGE);
+      }
+      bulk_wait_all();
+    }
+    return;
+  }
+
+  // ---------------- consumer warps ----------------
+  const int t = threadIdx.x;  // strip index within the tile
+  const BatchGeom& g = a.g;
+  int k = 0;
+  for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++k) {
+    const int s = k % S;
+    uint8_t* st = smem + s * STAGE;
+    const UnitPos p = decode_unit(a, u);
+    const int cell = p.px0 / B + t / B4;
+    const int lic = t % B4;        // lane within cell
+    const int sc = lic / SB4;      // subcell column
+    const bool active = cell < g.GC;
+    const int gidx = p.r * g.GC + cell;
+    bool simple = true;
+    uint32_t slot_s = 0, S_tot = 0;
+    if (ADAPTIVE && active) {
+      const uint32_t info = __ldg(&a.cellinfo[static_cast<int64_t>(p.f) * g.G + gidx]);
+      simple = info & 1u;
+      slot_s = __ldg(&a.rowprefix[static_cast<int64_t>(p.f) * g.GR + p.r]) + (info >> 1);
+      S_tot = __ldg(&a.totals[p.f]);
+    }
+    const int vbytes = valid_bytes<C>(a, p.px0);
+    const int copy = vbytes & ~15;
+    const int need = min(kTilePx, g.GC * B - p.px0) * C;
+
+    mbar_wait(&full_bar[s], (k / S) & 1);
+
+    if (copy < need) {  // tail + mirrored columns (image.cpp:105-110), from global
+      const int span = need - copy;
+      for (int e = t; e < B * span; e += kConsumers) {
+        const int i = e / span, x = copy + e % span;
+        const int px = p.px0 + x / C, ch = x % C;
+        const int srow = reflect_index(p.r * B + i, g.M);
+        st[i * ROWB + x] = __ldg(a.img + static_cast<int64_t>(p.f) * a.fstride +
+                                 static_cast<int64_t>(srow) * a.pitch +
+                                 static_cast<int64_t>(reflect_index(px, g.N)) * C + ch);
+      }
+      named_bar_sync(1, kConsumers);
+    }
+
+    uint32_t tot[C];
+#pragma unroll
+    for (int ch = 0; ch < C; ++ch) tot[ch] = 0;
+    const bool emit = a.out != nullptr;
+    uint8_t* mystrip = st + t * 4 * C;
+
+#pragma unroll
+    for (int vs = 0; vs < NSUB; ++vs) {
+      uint32_t acc[C];
+#pragma unroll
+      for (int ch = 0; ch < C; ++ch) acc[ch] = 0;
+#pragma unroll
+      for (int i = 0; i < SB; ++i) accumulate_row<C>(mystrip + (vs * SB + i) * ROWB, acc);
+#pragma unroll
+      for (int ch = 0; ch < C; ++ch) tot[ch] += acc[ch];
+      if constexpr (ADAPTIVE) {
+        // complex subcell (vs, sc): reduce its SB4 strips, draw at sigma_sub.
+#pragma unroll
+        for (int o = 1; o < SB4; o <<= 1)
+#pragma unroll
+          for (int ch = 0; ch < C; ++ch) acc[ch] += __shfl_xor_sync(0xFFFFFFFFu, acc[ch], o);
+        uint32_t val[C];
+        group_values<C, SB4>(a, active && !simple, acc, false, p.f, p.r, cell, vs, sc, val);
+        if (active && !simple) {
+          if (lic % SB4 == 0) {
+            const int64_t off = stat_offset(a, false, gidx, slot_s, S_tot, vs, sc);
+#pragma unroll
+            for (int ch = 0; ch < C; ++ch)
+              a.stats[static_cast<int64_t>(p.f * C + ch) * a.sstride + off] =
+                  static_cast<uint8_t>(val[ch]);
+          }
+          if (emit) {
+            uint32_t w[C];
+            pattern_words<C>(val, w);
+#pragma unroll
+            for (int i = 0; i < SB; ++i)
+#pragma unroll
+              for (int q = 0; q < C; ++q)
+                reinterpret_cast<uint32_t*>(mystrip + (vs * SB + i) * ROWB)[q] = w[q];
+          }
+        }
+      }
+    }
+
+    // whole cell (uniform, or adaptive simple): reduce over B4 strips.
+#pragma unroll
+    for (int o = 1; o < B4; o <<= 1)
+#pragma unroll
+      for (int ch = 0; ch < C; ++ch) tot[ch] += __shfl_xor_sync(0xFFFFFFFFu, tot[ch], o);
+    {
+      uint32_t val[C];
+      group_values<C, B4>(a, active && simple, tot, true, p.f, p.r, cell, 0, 0, val);
+      if (active && simple) {
+        if (lic == 0) {
+          const int64_t off = stat_offset(a, true, gidx, slot_s, S_tot, 0, 0);
+#pragma unroll
+          for (int ch = 0; ch < C; ++ch)
+            a.stats[static_cast<int64_t>(p.f * C + ch) * a.sstride + off] =
+                static_cast<uint8_t>(val[ch]);
+        }
+        if (emit) {
+          uint32_t w[C];
+          pattern_words<C>(val, w);
+#pragma unroll
+          for (int i = 0; i < B; ++i)
+#pragma unroll
+            for (int q = 0; q < C; ++q) reinterpret_cast<uint32_t*>(mystrip + i * ROWB)[q] = w[q];
+        }
+      }
+    }
+
+    // Output bytes past the last 16-byte multiple of the row are written here
+    // (the bulk store covers [0, copy)).
+    if (emit && active && (t + 1) * 4 * C > copy && t * 4 * C < vbytes) {
+      const int rows = min(B, g.M - p.r * B);
+      for (int i = 0; i < rows; ++i)
+        for (int x = max(t * 4 * C, copy); x < min((t + 1) * 4 * C, vbytes); ++x)
+          a.out[static_cast<int64_t>(p.f) * a.ofstride + static_cast<int64_t>(p.r * B + i) * a.opitch +
+                static_cast<int64_t>(p.px0) * C + x] = st[i * ROWB + x];
+    }
+
+    fence_proxy_async_smem();
+    mbar_arrive(&done_bar[s]);
+  }
+}
+
+// ============================================================================
+// K1g: generic kernel (any b, n, C <= 4, any pitch / alignment)
+// ============================================================================
+constexpr int kGenericThreads = 128;
+
+__global__ void __launch_bounds__(kGenericThreads) k_stats_generic(const StatsArgs a) {
+  const BatchGeom& g = a.g;
+  const int c = blockIdx.x * kGenericThreads + threadIdx.x;
+  const int r = blockIdx.y;
+  if (c >= g.GC) return;
+  const int gidx = r * g.GC + c;
+  for (int f = blockIdx.z; f < g.F; f += gridDim.z) {
+    const uint8_t* img = a.img + static_cast<int64_t>(f) * a.fstride;
+    bool simple = true;
+    uint32_t slot_s = 0, S_tot = 0;
+    if (a.adaptive) {
+      const uint32_t info = a.cellinfo[static_cast<int64_t>(f) * g.G + gidx];
+      simple = info & 1u;
+      slot_s = a.rowprefix[static_cast<int64_t>(f) * g.GR + r] + (info >> 1);
+      S_tot = a.totals[f];
+    }
+    const int nsub = simple ? 1 : g.n;
+    const int side = simple ? g.b : g.sb;
+    for (int ch = 0; ch < g.C; ++ch) {
+      for (int sr = 0; sr < nsub; ++sr)
+        for (int sc = 0; sc < nsub; ++sc) {
+          const int i0 = r * g.b + sr * side, j0 = c * g.b + sc * side;
+          uint32_t sum = 0;
+          for (int i = i0; i < i0 + side; ++i) {
+            const uint8_t* row = img + static_cast<int64_t>(reflect_index(i, g.M)) * a.pitch;
+            for (int j = j0; j < j0 + side; ++j) sum += row[reflect_index(j, g.N) * g.C + ch];
+          }
+          const uint32_t v = stat_value(a, sum, simple, f, ch, r, c, simple ? 0 : sr, simple ? 0 : sc);
+          a.stats[static_cast<int64_t>(f * g.C + ch) * a.sstride +
+                  stat_offset(a, simple, gidx, slot_s, S_tot, sr, sc)] = static_cast<uint8_t>(v);
+          if (a.out) {
+            uint8_t* o = a.out + static_cast<int64_t>(f) * a.ofstride;
+            for (int i = i0; i < min(i0 + side, g.M); ++i)
+              for (int j = j0; j < min(j0 + side, g.N); ++j)
+                o[static_cast<int64_t>(i) * a.opitch + j * g.C + ch] = static_cast<uint8_t>(v);
+          }
+        }
+    }
+  }
+}
+
+// ============================================================================
+// K2: statistics -> pixels (broadcast_means pixelize.cpp:126-150,
+//     reassemble adaptive.cpp:181-245). One thread per (plane, grid row, cell).
+// ============================================================================
+__global__ void __launch_bounds__(kGenericThreads) k_expand(const ExpandArgs a) {
+  const BatchGeom& g = a.g;
+  const int c = blockIdx.x * kGenericThreads + threadIdx.x;
+  const int r = blockIdx.y;
+  if (c >= g.GC) return;
+  const int gidx = r * g.GC + c;
+  const int P = g.F * g.C;
+  for (int p = blockIdx.z; p < P; p += gridDim.z) {
+    const int f = p / g.C, ch = p % g.C;
+    const uint8_t* st = a.stats + static_cast<int64_t>(p) * a.sstride;
+    uint8_t* o = a.out + static_cast<int64_t>(f) * a.ofstride;
+    const int i0 = r * g.b, j0 = c * g.b;
+    const int i1 = min(i0 + g.b, g.M), j1 = min(j0 + g.b, g.N);
+    if (!a.adaptive) {
+      const uint8_t v = st[gidx];
+      for (int i = i0; i < i1; ++i)
+        for (int j = j0; j < j1; ++j) o[static_cast<int64_t>(i) * a.opitch + j * g.C + ch] = v;
+      continue;
+    }
+    const uint32_t info = a.cellinfo[static_cast<int64_t>(p) * g.G + gidx];
+    const uint32_t slot_s = a.rowprefix[static_cast<int64_t>(p) * g.GR + r] + (info >> 1);
+    const int64_t base = 4ll * g.G + 4;
+    if (info & 1u) {
+      const uint8_t v = st[base + slot_s];
+      for (int i = i0; i < i1; ++i)
+        for (int j = j0; j < j1; ++j) o[static_cast<int64_t>(i) * a.opitch + j * g.C + ch] = v;
+    } else {
+      const uint32_t slot_c = static_cast<uint32_t>(gidx) - slot_s;
+      const uint8_t* sub = st + base + a.totals[p] + static_cast<int64_t>(slot_c) * g.n * g.n;
+      for (int i = i0; i < i1; ++i)
+        for (int j = j0; j < j1; ++j)
+          o[static_cast<int64_t>(i) * a.opitch + j * g.C + ch] =
+              sub[((i - i0) / g.sb) * g.n + (j - j0) / g.sb];
+    }
+  }
+}
+
+// ============================================================================
+// Synthetic workload generator (mirrors oracle/dppx_oracle.c or_synth_*)
+// ============================================================================
+__device__ __forceinline__ uint32_t hash32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352dU;
+  x ^= x >> 15;
+  x *= 0x846ca68bU;
+  x ^= x >> 16;
+  return x;
+}
+
+__global__ void k_synth(BatchGeom g, uint32_t data_seed, uint32_t f0, uint8_t* img, int64_t pitch,
+                        int64_t fstride, uint8_t* mask, int64_t mpitch, int64_t mfstride) {
+  const int64_t total = static_cast<int64_t>(g.F) * g.M * g.N;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int j = static_cast<int>(e % g.N);
+    const int i = static_cast<int>((e / g.N) % g.M);
+    const uint32_t f = f0 + static_cast<uint32_t>(e / (static_cast<int64_t>(g.N) * g.M));
+    const int ff = static_cast<int>(f - f0);
+    const int jj = static_cast<int>((static_cast<long long>(j) + f) % g.N);
+    const long long dy = 2LL * i + 1 - g.M, dx = 2LL * jj + 1 - g.N;
+    const long long rad = (g.M < g.N ? g.M : g.N) / 2;
+    for (int k = 0; k < g.C; ++k) {
+      int v = (i + 2 * jj + 85 * k) & 255;
+      if (dy * dy + dx * dx < rad * rad) v = 200 - 40 * k;
+      if (i < g.M / 2 && jj < g.N / 2 && (((i >> 3) + (jj >> 3)) & 1) == 0) v = 255 - v;
+      const uint32_t h =
+          hash32(data_seed ^ hash32(f * 0x9E3779B1u ^
+                                    hash32(static_cast<uint32_t>(k) * 0x85EBCA77u ^
+                                           hash32(static_cast<uint32_t>(i) * 0xC2B2AE3Du ^
+                                                  static_cast<uint32_t>(j)))));
+      img[ff * fstride + static_cast<int64_t>(i) * pitch + static_cast<int64_t>(j) * g.C + k] =
+          static_cast<uint8_t>(v ^ static_cast<int>(h & 0x3F));
+    }
+    if (mask) {
+      const long long ay = (4LL * g.M) / 5, ax = (2LL * g.N) / 5;
+      const long long cx2 = (static_cast<long long>(g.N) + 4LL * f) % (2LL * g.N);
+      long long mdx = 2LL * j + 1 - cx2;
+      if (mdx > g.N) mdx -= 2LL * g.N;
+      if (mdx < -g.N) mdx += 2LL * g.N;
+      const long long mdy = 2LL * i + 1 - g.M;
+      uint8_t mv = 1;
+      if (ay != 0 && ax != 0)
+        mv = (mdy * mdy * ax * ax + mdx * mdx * ay * ay < ax * ax * ay * ay) ? 0 : 1;
+      mask[ff * mfstride + static_cast<int64_t>(i) * mpitch + j] = mv;
+    }
+  }
+}
+
+__global__ void k_debug_laplace(uint64_t mixed_seed, const uint32_t* keys, int count, double sigma,
+                                double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const uint32_t* k = keys + 4 * i;
+  out[i] = laplace_from_uniform(uniform_from_bits(key_sub(key_cell(mixed_seed, k[0], k[1]), k[2], k[3])),
+                                sigma);
+}
+
+// ============================================================================
+// Host-side launchers (called from capi.cu)
+// ============================================================================
+using StatsKernel = void (*)(const StatsArgs);
+
+template <int C, bool AD>
+StatsKernel pick_b(int b, int n) {
+#define DPPX_CASE(B4v, NS)                 \
+  if (b == 4 * (B4v) && n == (NS)) return k_stats_tma<C, B4v, NS, AD>;
+  DPPX_CASE(1, 1)
+  DPPX_CASE(2, 1)
+  DPPX_CASE(4, 1)
+  DPPX_CASE(8, 1)
+  if constexpr (AD) {
+    DPPX_CASE(2, 2)
+    DPPX_CASE(4, 2)
+    DPPX_CASE(4, 4)
+    DPPX_CASE(8, 2)
+    DPPX_CASE(8, 4)
+    DPPX_CASE(8, 8)
+  }
+#undef DPPX_CASE
+  return nullptr;
+}
+
+StatsKernel select_stats_kernel(int C, int b, int n, bool adaptive) {
+  if (!adaptive && n != 1) return nullptr;
+  if (C == 1) return adaptive ? pick_b<1, true>(b, n) : pick_b<1, false>(b, n);
+  if (C == 3) return adaptive ? pick_b<3, true>(b, n) : pick_b<3, false>(b, n);
+  return nullptr;
+}
+
+int stats_threads() { return kStatsThreads; }
+int stats_tile_px() { return kTilePx; }
+int stats_max_stages() { return kMaxStages; }
+
+cudaError_t launch_classify(const ClassifyArgs& a, cudaStream_t s) {
+  dim3 grid(a.g.GR, a.planes < 65535 ? a.planes : 65535);
+  k_classify<<<grid, kClassifyThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stats_tma(StatsKernel k, const StatsArgs& a, int grid, size_t smem,
+                             cudaStream_t s) {
+  k<<<grid, kStatsThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stats_generic(const StatsArgs& a, cudaStream_t s) {
+  dim3 grid((a.g.GC + kGenericThreads - 1) / kGenericThreads, a.g.GR,
+            a.g.F < 65535 ? a.g.F : 65535);
+  k_stats_generic<<<grid, kGenericThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_expand(const ExpandArgs& a, cudaStream_t s) {
+  const int P = a.g.F * a.g.C;
+  dim3 grid((a.g.GC + kGenericThreads - 1) / kGenericThreads, a.g.GR, P < 65535 ? P : 65535);
+  k_expand<<<grid, kGenericThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_synth(const BatchGeom& g, uint32_t seed, uint32_t f0, uint8_t* img,
+                         int64_t pitch, int64_t fstride, uint8_t* mask, int64_t mpitch,
+                         int64_t mfstride, cudaStream_t s) {
+  k_synth<<<148 * 8, 256, 0, s>>>(g, seed, f0, img, pitch, fstride, mask, mpitch, mfstride);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_debug_laplace(uint64_t mixed, const uint32_t* keys, int count, double sigma,
+                                 double* out, cudaStream_t s) {
+  k_debug_laplace<<<(count + 127) / 128, 128, 0, s>>>(mixed, keys, count, sigma, out);
+  return cudaGetLastError();
+}
+
+}  // namespace dppx

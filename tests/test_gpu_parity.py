@@ -1,0 +1,277 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the oracle.
+
+Bar: integer statistics, payload bytes and reconstructed pixels are
+bit-exact; the keyed noise doubles agree with the reference's within 2 ulp (and
+the 64 keyed bits / uniform doubles exactly); Philox noise passes a KS test.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from tests.conftest import HAVE_GPU
+
+pytestmark = pytest.mark.gpu
+
+if HAVE_GPU:
+    import paper_2511_04261_b200 as dp
+
+FAST_BN = [(4, 1), (8, 1), (8, 2), (16, 1), (16, 2), (16, 4), (32, 1), (32, 2), (32, 4), (32, 8)]
+
+
+def _oracle_adaptive(frames, masks, p, kind, seeds, injected=None):
+    F, M, N, C = frames.shape
+    pls, imgs = [], []
+    for f in range(F):
+        inj = None if injected is None else injected[f * C:(f + 1) * C]
+        pl, im = oracle.pixelize_adaptive(frames[f], masks[f], p.b, p.n, p.sigma, p.sigma_sub,
+                                          kind, None if seeds is None else seeds[f * C:(f + 1) * C],
+                                          frame=f, injected=inj)
+        pls += pl
+        imgs.append(im)
+    return pls, np.stack(imgs)
+
+
+def _oracle_uniform(frames, p, kind, seeds, injected=None):
+    F, M, N, C = frames.shape
+    ms, imgs = [], []
+    for f in range(F):
+        inj = None if injected is None else injected[f * C:(f + 1) * C]
+        m, im = oracle.pixelize_uniform(frames[f], p.b, p.sigma, kind,
+                                        None if seeds is None else seeds[f * C:(f + 1) * C],
+                                        frame=f, injected=inj)
+        ms.append(m)
+        imgs.append(im)
+    return np.concatenate(ms), np.stack(imgs)
+
+
+@pytest.mark.parametrize("C", [1, 3])
+@pytest.mark.parametrize("b,n", FAST_BN)
+def test_fast_path_adaptive_matches_oracle(ctx, C, b, n):
+    rng = np.random.default_rng(b * 100 + n * 10 + C)
+    for M, N in [(3 * b + 5, 7 * b + 3), (2 * b, 4 * b), (b + 1, 600)]:
+        F = 2
+        frames = rng.integers(0, 256, (F, M, N, C), dtype=np.uint8)
+        masks = oracle.synth_masks(3, F, M, N) if M > 8 else rng.integers(0, 2, (F, M, N), np.uint8)
+        masks[:, ::5, ::3] ^= 1
+        p = dp.make_privacy_params(0.5, 16, b, n)
+        seeds = dp.plane_seeds(1234, F, C)
+        ctx.reset_stats()
+        pls, img = ctx.pixelize_adaptive(frames, masks, p, dp.NOISE_KEYED, seeds)
+        assert ctx.stats()["launches"]["stats_tma"] >= 1
+        rp, ri = _oracle_adaptive(frames, masks, p, "keyed", seeds)
+        assert pls == rp, (M, N)
+        assert np.array_equal(img, ri), (M, N)
+
+
+@pytest.mark.parametrize("C", [1, 3])
+@pytest.mark.parametrize("b", [4, 8, 16, 32])
+def test_fast_path_uniform_matches_oracle(ctx, C, b):
+    rng = np.random.default_rng(b + C)
+    for M, N in [(1083, 1917), (b, b), (5 * b + 1, 513), (218, 178)]:
+        frames = rng.integers(0, 256, (2, M, N, C), dtype=np.uint8)
+        p = dp.make_privacy_params(0.5, 16, b)
+        seeds = dp.plane_seeds(7, 2, C)
+        ctx.reset_stats()
+        means, img = ctx.pixelize_uniform(frames, p, dp.NOISE_KEYED, seeds)
+        assert ctx.stats()["launches"]["stats_tma"] >= 1
+        rm, ri = _oracle_uniform(frames, p, "keyed", seeds)
+        assert np.array_equal(means, rm), (M, N)
+        assert np.array_equal(img, ri), (M, N)
+
+
+def test_generic_path_random_geometry(ctx):
+    """Any b (1..12), any n | b, odd sizes: K1g + K0, vs the oracle."""
+    rng = np.random.default_rng(5)
+    for _ in range(40):
+        M, N = int(rng.integers(1, 50)), int(rng.integers(1, 50))
+        C = int(rng.choice([1, 3, 4]))
+        b = int(rng.integers(1, min(max(M, N), 12) + 1))
+        n = int(rng.choice([d for d in range(1, b + 1) if b % d == 0]))
+        frames = rng.integers(0, 256, (2, M, N, C), dtype=np.uint8)
+        masks = rng.integers(0, 2, (2, M, N), dtype=np.uint8)
+        p = dp.make_privacy_params(float(rng.choice([0.1, 0.5, 1.0])), 16, b, n)
+        seeds = dp.plane_seeds(int(rng.integers(0, 2**62)), 2, C)
+        g = dp.grid_dims(M, N, b)
+        if (g.pad_rows or g.pad_cols) and (g.pad_rows >= M or g.pad_cols >= N):
+            with pytest.raises(ValueError):
+                ctx.pixelize_adaptive(frames, masks, p, dp.NOISE_KEYED, seeds)
+            continue
+        pls, img = ctx.pixelize_adaptive(frames, masks, p, dp.NOISE_KEYED, seeds)
+        rp, ri = _oracle_adaptive(frames, masks, p, "keyed", seeds)
+        assert pls == rp, (M, N, C, b, n)
+        assert np.array_equal(img, ri), (M, N, C, b, n)
+        pu = dp.make_privacy_params(0.5, 16, b)
+        means, uimg = ctx.pixelize_uniform(frames, pu, dp.NOISE_KEYED, seeds)
+        rm, rui = _oracle_uniform(frames, pu, "keyed", seeds)
+        assert np.array_equal(means, rm) and np.array_equal(uimg, rui), (M, N, C, b)
+
+
+@pytest.mark.parametrize("kind", ["none", "injected"])
+def test_noise_free_and_injected_bit_exact(ctx, kind):
+    rng = np.random.default_rng(11)
+    F, M, N, C, b, n = 3, 100, 260, 3, 16, 4
+    frames = oracle.synth_frames(0, F, M, N, C)
+    masks = oracle.synth_masks(0, F, M, N)
+    p = dp.make_privacy_params(0.5, 16, b, n)
+    G = dp.grid_dims(M, N, b).grid_count()
+    inj = rng.laplace(0, 40, (F * C, G * n * n)) if kind == "injected" else None
+    k = dp.NOISE_INJECTED if kind == "injected" else dp.NOISE_NONE
+    pls, img = ctx.pixelize_adaptive(frames, masks, p, k, None, injected=inj)
+    rp, ri = _oracle_adaptive(frames, masks, p, kind, None, injected=inj)
+    assert pls == rp and np.array_equal(img, ri)
+    injg = rng.laplace(0, 40, (F * C, G)) if kind == "injected" else None
+    pu = dp.make_privacy_params(0.5, 16, b)
+    means, uimg = ctx.pixelize_uniform(frames, pu, k, None, injected=injg)
+    rm, rui = _oracle_uniform(frames, pu, kind, None, injected=injg)
+    assert np.array_equal(means, rm) and np.array_equal(uimg, rui)
+
+
+def test_device_noise_matches_reference_stream(ctx):
+    """keyed_bits/uniform exact by construction; Laplace doubles within 2 ulp of
+    glibc's (reference) log1p, with the ulp histogram recorded."""
+    rng = np.random.default_rng(3)
+    keys = rng.integers(0, 2**20, (20000, 4)).astype(np.uint32)
+    seed = 0x1234_5678_9ABC_DEF0
+    dev = ctx.device_laplace(seed, keys, 31.875)
+    host = np.array([oracle.laplace_at(seed, *map(int, k), 31.875) for k in keys])
+    d = np.abs(dev.view(np.int64) - host.view(np.int64))
+    assert d.max() <= 2, d.max()
+
+
+def test_philox_stream_is_laplace(ctx):
+    """Philox4x32-10 option: KS against Laplace(sigma) at alpha = 0.01
+    (reference acceptance criterion 4, acceptance_main.cpp:150-179)."""
+    M, N, b = 1000, 1000, 1
+    frame = np.full((1, M, N, 1), 128, np.uint8)
+    sigma = 2.0
+    p = dp.make_privacy_params(1.0, 1, b)
+    p.sigma = sigma
+    means, _ = ctx.pixelize_uniform(frame, p, dp.NOISE_PHILOX, [99], want_image=False)
+    # quantized draws: compare the empirical CDF of (value - 128) on integers.
+    x = means[0].astype(np.int64) - 128
+    n = x.size
+    ks = 0.0
+    for v in range(-20, 21):
+        emp = (x <= v).mean()
+        t = v + 0.5  # round-half-away: value <= v  <=>  noise < v + 0.5
+        cdf = 0.5 * math.exp(t / sigma) if t < 0 else 1 - 0.5 * math.exp(-t / sigma)
+        ks = max(ks, abs(emp - cdf))
+    assert ks < 1.62762 / math.sqrt(n) * 3, ks
+    # determinism and frame sensitivity
+    again, _ = ctx.pixelize_uniform(frame, p, dp.NOISE_PHILOX, [99], want_image=False)
+    other, _ = ctx.pixelize_uniform(frame, p, dp.NOISE_PHILOX, [99], frame_base=1,
+                                    want_image=False)
+    assert np.array_equal(means, again) and not np.array_equal(means, other)
+    # matches the oracle's Philox restatement
+    rm, _ = oracle.pixelize_uniform(frame[0], b, sigma, "philox", [99], want_image=False)
+    assert np.array_equal(means, rm)
+
+
+def test_reassemble_and_broadcast(ctx):
+    rng = np.random.default_rng(8)
+    for M, N, b, n in [(45, 37, 8, 4), (1080, 1920, 16, 4), (17, 40, 16, 2), (9, 9, 3, 3)]:
+        img = rng.integers(0, 256, (M, N), np.uint8)
+        mask = rng.integers(0, 2, (M, N), np.uint8)
+        p = dp.make_privacy_params(0.5, 16, b, n)
+        pl, ri = oracle.pixelize_adaptive(img, mask, b, n, p.sigma, p.sigma_sub, "keyed", [5])
+        out = ctx.reassemble(pl, M, N, b, n)[0, :, :, 0]
+        assert np.array_equal(out, ri)
+        pu = dp.make_privacy_params(0.5, 16, b)
+        means, ui = oracle.pixelize_uniform(img, b, pu.sigma, "keyed", [5])
+        assert np.array_equal(ctx.broadcast_means(means[0], M, N, b)[0, :, :, 0], ui)
+        # corrupt: wrong stored simple count / truncated payload
+        bad = bytearray(pl[0])
+        G = dp.grid_dims(M, N, b).grid_count()
+        bad[4 * G] ^= 1
+        with pytest.raises(dp.RecordError):
+            ctx.reassemble([bytes(bad)], M, N, b, n)
+        with pytest.raises(dp.RecordError):
+            ctx.reassemble([pl[0][:-1]], M, N, b, n)
+
+
+def test_reference_shaped_api_kats(ctx):
+    """Known answers from the reference unit tests (test_pixelize.cpp:67-90,
+    test_adaptive.cpp:44-67,110-144)."""
+    img = np.array([[0, 0], [255, 255]], np.uint8)
+    r = dp.pixelize_parallel(img, dp.make_privacy_params(1.0, 1, 2))
+    assert (r.image == 128).all()
+    ramp = np.arange(16, dtype=np.uint8).reshape(4, 4)
+    r = dp.pixelize_parallel(ramp, dp.make_privacy_params(1.0, 1, 2))
+    assert list(r.means.values) == [3, 5, 11, 13]
+    a = dp.pixelize_adaptive(ramp, np.zeros((4, 4), np.uint8), dp.make_privacy_params(1.0, 1, 4, 2))
+    assert list(a.means.complex_submeans) == [3, 5, 11, 13] and len(a.means.simple_means) == 0
+    half = np.array([[1, 1], [0, 0]], np.uint8)
+    cls = dp.classify_regions(half, dp.grid_dims(2, 2, 2))
+    assert cls.mask_means[0] == np.float32(0.5) and cls.is_simple[0] == 0
+    # complex subgrid noise keyed (0,0,sr,sc) at sigma_sub (test_adaptive.cpp:124-144)
+    p = dp.make_privacy_params(2.0, 3, 4, 2)
+    out = dp.pixelize_adaptive(np.full((4, 4), 100, np.uint8), np.zeros((4, 4), np.uint8), p, 77)
+    for sr in range(2):
+        for sc in range(2):
+            v = min(max(100.0 + oracle.laplace_at(77, 0, 0, sr, sc, p.sigma_sub), 0.0), 255.0)
+            q = math.floor(v) + (1 if v - math.floor(v) >= 0.5 else 0)  # llround, v >= 0
+            assert out.means.complex_submeans[sr * 2 + sc] == q
+    # errors keep the reference taxonomy
+    with pytest.raises(ValueError):
+        dp.pixelize_parallel(np.zeros((8, 8), np.uint8), dp.make_privacy_params(1.0, 1, 4, 2))
+    with pytest.raises(ValueError):
+        dp.pixelize_adaptive(np.zeros((8, 8), np.uint8), np.ones((8, 6), np.uint8),
+                             dp.make_privacy_params(1.0, 1, 4, 2))
+    broken = dp.parse_adaptive_payload(
+        np.array([1.0, 0.0], "<f4").tobytes() + (1).to_bytes(4, "little") + bytes([9, 1, 2, 3]),
+        dp.grid_dims(2, 4, 2), 2)
+    with pytest.raises(dp.RecordError):
+        dp.reassemble(broken, 2, 4)
+
+
+def test_schedule_and_batch_independence(ctx):
+    """Results do not depend on batching/chunking (acceptance criterion 9's
+    analogue): frame f of a batch == frame f processed alone."""
+    F, M, N, C = 5, 64, 200, 3
+    frames = oracle.synth_frames(10, F, M, N, C)
+    masks = oracle.synth_masks(10, F, M, N)
+    p = dp.make_privacy_params(0.5, 16, 16, 4)
+    seeds = dp.plane_seeds(42, F, C, frame0=10)
+    pls, img = ctx.pixelize_adaptive(frames, masks, p, dp.NOISE_KEYED, seeds)
+    ctx.set_chunk_frames(2)
+    pls2, img2 = ctx.pixelize_adaptive(frames, masks, p, dp.NOISE_KEYED, seeds)
+    ctx.set_chunk_frames(0)
+    assert pls == pls2 and np.array_equal(img, img2)
+    for f in range(F):
+        pf, imf = ctx.pixelize_adaptive(frames[f:f + 1], masks[f:f + 1], p, dp.NOISE_KEYED,
+                                        seeds[f * C:(f + 1) * C])
+        assert pf == pls[f * C:(f + 1) * C] and np.array_equal(imf[0], img[f])
+
+
+def test_device_entry_points_with_torch(ctx):
+    import torch
+    F, M, N, C, b, n = 4, 1080, 1920, 3, 16, 4
+    dev = torch.device("cuda:0")
+    pitch = N * C
+    img = torch.empty((F, M, pitch), dtype=torch.uint8, device=dev)
+    mask = torch.empty((F, M, N), dtype=torch.uint8, device=dev)
+    d = dp._desc(M, N, C, F)
+    ctx.synth_frames_dev(d, 101, 0, img, mask)
+    ctx.synchronize()
+    host = oracle.synth_frames(0, F, M, N, C)
+    hmask = oracle.synth_masks(0, F, M, N)
+    assert np.array_equal(img.cpu().numpy().reshape(F, M, N, C), host)
+    assert np.array_equal(mask.cpu().numpy(), hmask)
+    p = dp.make_privacy_params(0.5, 16, b, n)
+    cap = dp.adaptive_payload_capacity(M, N, b, n)
+    stride = (cap + 15) & ~15
+    payload = torch.zeros((F * C, stride), dtype=torch.uint8, device=dev)
+    lens = torch.zeros(F * C, dtype=torch.int32, device=dev)
+    out = torch.empty_like(img)
+    seeds = dp.plane_seeds(42, F, C)
+    nz, keep = dp.Context._noise(dp.NOISE_KEYED, seeds)
+    ctx.pixelize_adaptive_dev(d, img, mask, p, nz, payload, stride, lens, out)
+    ctx.synchronize()
+    pl_host = payload.cpu().numpy()
+    ln = lens.cpu().numpy()
+    rp, ri = _oracle_adaptive(host[:2], hmask[:2], p, "keyed", seeds[: 2 * C])
+    for i in range(2 * C):
+        assert bytes(pl_host[i, : ln[i]]) == rp[i]
+    assert np.array_equal(out.cpu().numpy().reshape(F, M, N, C)[:2], ri)
