@@ -147,6 +147,9 @@ int dppx_ctx_synchronize(dppx_ctx* ctx);
 int dppx_ctx_set_timing(dppx_ctx* ctx, int32_t on);
 int dppx_ctx_get_stats(dppx_ctx* ctx, dppx_kernel_stats* out);
 int dppx_ctx_reset_stats(dppx_ctx* ctx);
+/* 1: evaluate every statistic with the reference's f64 arithmetic (no bounded
+ * f32 fast path); the bytes produced are identical either way. */
+int dppx_ctx_set_exact_noise(dppx_ctx* ctx, int32_t on);
 /* Frames per pipeline chunk of the host entry points (0 = automatic). */
 int dppx_ctx_set_chunk_frames(dppx_ctx* ctx, int32_t frames);
 
@@ -195,6 +198,8 @@ int dppx_classify_regions(dppx_ctx* ctx, const dppx_frames_desc* desc, const uin
  * (keys[4*i..4*i+3] = r, c, sr, sc) for one plane seed at scale sigma. */
 int dppx_debug_device_laplace(dppx_ctx* ctx, uint64_t seed, const uint32_t* keys, int32_t count,
                               double sigma, double* out);
+/* Max |lg2.approx(m) - log2(m)| over all f32 mantissas (fast-path error bound). */
+int dppx_debug_lg2_max_error(dppx_ctx* ctx, double* out);
 
 #ifdef __cplusplus
 }

@@ -113,6 +113,7 @@ ABI = {
     "dppx_ctx_get_stats": (C.c_int, [_ctxp, C.POINTER(KernelStats)]),
     "dppx_ctx_reset_stats": (C.c_int, [_ctxp]),
     "dppx_ctx_set_chunk_frames": (C.c_int, [_ctxp, C.c_int32]),
+    "dppx_ctx_set_exact_noise": (C.c_int, [_ctxp, C.c_int32]),
     "dppx_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(_vp)]),
     "dppx_host_free": (None, [_vp]),
     "dppx_pixelize_uniform_dev": (C.c_int, [_ctxp, _descp, _vp, _pp, _np, _vp, _vp]),
@@ -129,6 +130,7 @@ ABI = {
     "dppx_reassemble": (C.c_int, [_ctxp, _descp, _vp, C.c_int64, _vp, C.c_int32, C.c_int32, _vp]),
     "dppx_classify_regions": (C.c_int, [_ctxp, _descp, _vp, C.c_int32, _vp]),
     "dppx_debug_device_laplace": (C.c_int, [_ctxp, C.c_uint64, _vp, C.c_int32, C.c_double, _vp]),
+    "dppx_debug_lg2_max_error": (C.c_int, [_ctxp, C.POINTER(C.c_double)]),
 }
 for _name, (_res, _args) in ABI.items():
     _f = getattr(_lib, _name)
@@ -307,6 +309,15 @@ class Context:
 
     def set_chunk_frames(self, frames: int):
         self._check(_lib.dppx_ctx_set_chunk_frames(self._h, frames), "set_chunk_frames")
+
+    def set_exact_noise(self, on: bool):
+        """Force the f64 reference arithmetic for every statistic (testing)."""
+        self._check(_lib.dppx_ctx_set_exact_noise(self._h, 1 if on else 0), "set_exact_noise")
+
+    def lg2_max_error(self) -> float:
+        v = C.c_double()
+        self._check(_lib.dppx_debug_lg2_max_error(self._h, C.byref(v)), "lg2_max_error")
+        return v.value
 
     def stats(self) -> dict:
         s = KernelStats()

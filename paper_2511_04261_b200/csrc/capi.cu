@@ -32,6 +32,7 @@ cudaError_t launch_expand(const ExpandArgs& a, cudaStream_t s);
 cudaError_t launch_synth(const BatchGeom& g, uint32_t seed, uint32_t f0, uint8_t* img,
                          int64_t pitch, int64_t fstride, uint8_t* mask, int64_t mpitch,
                          int64_t mfstride, cudaStream_t s);
+cudaError_t launch_debug_lg2(unsigned int* out, cudaStream_t s);
 cudaError_t launch_debug_laplace(uint64_t mixed, const uint32_t* keys, int count, double sigma,
                                  double* out, cudaStream_t s);
 }  // namespace dppx
@@ -88,6 +89,7 @@ struct dppx_ctx {
   size_t sd_pinned_n[2] = {0, 0};
   cudaEvent_t in_done[2] = {}, comp_done[2] = {}, out_done[2] = {};
   int chunk_frames = 0;
+  bool exact_noise = false;
   // stats
   bool timing = false;
   std::vector<PendingTiming> pending;
@@ -392,6 +394,7 @@ int pixelize_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img, c
   a.sub_area = static_cast<double>(g.sb) * g.sb;
   a.sigma = pp->sigma;
   a.sigma_sub = adaptive ? pp->sigma_sub : pp->sigma;
+  a.exact_noise = ctx->exact_noise ? 1 : 0;
   if (int rc = prepare_noise(ctx, nz, g.F * g.C, dev_injected, g, pp, &a.noise, ctx->stream,
                              dev_seeds, pinned, pinned_n, guard, record_guard))
     return rc;
@@ -819,6 +822,12 @@ int dppx_ctx_set_chunk_frames(dppx_ctx* ctx, int32_t frames) {
   return DPPX_OK;
 }
 
+int dppx_ctx_set_exact_noise(dppx_ctx* ctx, int32_t on) {
+  if (!ctx) return DPPX_ERR_INVALID;
+  ctx->exact_noise = on != 0;
+  return DPPX_OK;
+}
+
 int dppx_host_alloc(size_t bytes, void** out) {
   if (!out) return DPPX_ERR_INVALID;
   return cudaMallocHost(out, bytes) == cudaSuccess ? DPPX_OK : DPPX_ERR_OOM;
@@ -970,6 +979,21 @@ int dppx_debug_device_laplace(dppx_ctx* ctx, uint64_t seed, const uint32_t* keys
                                      sigma, static_cast<double*>(ctx->dbl.p), ctx->stream));
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   CUDA_TRY(ctx, cudaMemcpy(out, ctx->dbl.p, sizeof(double) * count, cudaMemcpyDeviceToHost));
+  return DPPX_OK;
+}
+
+int dppx_debug_lg2_max_error(dppx_ctx* ctx, double* out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (!out) return set_err(ctx, DPPX_ERR_INVALID, "null output");
+  if (int rc = ensure(ctx, ctx->keys, 16)) return rc;
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->keys.p, 0, 4, ctx->stream));
+  CUDA_TRY(ctx, launch_debug_lg2(static_cast<unsigned int*>(ctx->keys.p), ctx->stream));
+  unsigned int bits = 0;
+  CUDA_TRY(ctx, cudaMemcpyAsync(&bits, ctx->keys.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  float f;
+  std::memcpy(&f, &bits, 4);
+  *out = f;
   return DPPX_OK;
 }
 

@@ -88,32 +88,94 @@ __device__ __forceinline__ double cell_mean(uint32_t sum, double area) {
   return __ddiv_rn(static_cast<double>(sum), area);
 }
 
-// Noise for one statistic of plane `plane` (= f*C + ch) at key (r, c, sr, sc).
-// cell_state is key_cell(mix64(seed), r, c) for the KEYED stream.
-struct NoiseView {
+// ---- quantized statistic: fast bounded path + exact fallback ---------------
+//
+// The reference computes q = llround(clip(mean + noise)) in f64 with
+// noise = (sign*sigma) * -log1p(-2|u|) (noise.cpp:107-110, pixelize.cpp:25-31).
+// q only depends on which interval [j - 0.5, j + 0.5) the f64 value falls in,
+// so a cheap f32 estimate v_est with a proven error bound decides q whenever
+// v_est is farther than `margin` from every rounding boundary (0.5 ... 254.5);
+// otherwise (a few per mille of draws) the exact f64 arithmetic runs. The
+// emitted bytes are therefore those of the exact evaluation. Error budget of
+// the estimate:
+//   log2 of w = 1 - 2|u| = W * 2^-52 (W an exact integer): exponent exact,
+//   mantissa truncated to 23 bits (<= 1.8e-7), lg2.approx (<= 2^-21,
+//   checked exhaustively on the device by tests/test_gpu_parity.py)
+//   => |d noise| <= sigma * ln2 * 6.6e-7 <= sigma * 4.6e-7;
+//   f32 rounding of mean, noise and the sum (< 8 ulp of 512) <= 2.5e-4.
+// margin = 2e-3 + sigma * 4e-6 keeps a factor >= 8 over that budget.
+__device__ __forceinline__ float fast_margin(double sigma) {
+  return 2e-3f + static_cast<float>(sigma) * 4e-6f;
+}
+
+// Returns the quantized value, or 0xFFFFFFFF when v_est is ambiguous.
+__device__ __forceinline__ uint32_t fast_quantize(uint32_t sum, float inv_area, uint64_t bits,
+                                                  float sigmaf, float margin) {
+  const uint64_t y = bits >> 11;  // 53-bit integer of uniform_from_bits
+  const uint64_t half = 1ull << 52;
+  const bool neg = y < half;      // u < 0
+  uint64_t d = neg ? half - y : y - half;
+  d = d < half - 1 ? d : half - 1;  // the +-(0.5 - 2^-53) clamp of noise.cpp:99-104
+  const uint64_t W = half - d;      // 1 - 2|u| = W * 2^-52, W in [1, 2^52]
+  const int lz = __clzll(W);
+  const int e = 63 - lz;            // floor(log2 W)
+  const uint32_t mant = static_cast<uint32_t>((W << lz) >> 40) & 0x7FFFFFu;
+  const float lg_m = __log2f(__uint_as_float(0x3F800000u | mant));  // log2 of [1,2)
+  const float L = (static_cast<float>(52 - e) - lg_m) * 0.693147180559945f;  // -ln(1-2|u|)
+  const float noise = neg ? -sigmaf * L : sigmaf * L;
+  const float t = static_cast<float>(sum) * inv_area + noise + 0.5f;
+  const float j = rintf(t);
+  if (fabsf(t - j) <= margin && j >= 1.0f && j <= 255.0f) return 0xFFFFFFFFu;
+  return static_cast<uint32_t>(fminf(fmaxf(floorf(t), 0.0f), 255.0f));
+}
+
+// The reference's f64 arithmetic, step for step (rare path).
+__device__ __noinline__ uint32_t exact_quantize(uint32_t sum, double area, int kind, uint64_t bits,
+                                                double sigma, double injected) {
+  const double mean = cell_mean(sum, area);
+  double noise = 0.0;
+  if (kind == DPPX_NOISE_KEYED || kind == DPPX_NOISE_PHILOX)
+    noise = laplace_from_uniform(uniform_from_bits(bits), sigma);
+  else if (kind == DPPX_NOISE_INJECTED)
+    noise = injected;
+  return finalize_value(mean, noise);
+}
+
+// Per-(unit, statistic kind) constants.
+struct DrawEnv {
   int kind;
-  uint32_t frame_base;
-  const uint64_t* mixed_seeds;  // KEYED: mix64(seed) per plane; PHILOX: [0] = base seed
-  const double* injected;       // INJECTED: ((plane*G + g)*n + sr)*n + sc
+  bool exact_only;  // test switch: always take the f64 path
+  bool pow2;        // area is a power of two: sum * inv_area is exact in f32
+  double area, sigma;
+  float inv_area, sigmaf, margin;
 };
 
-__device__ __forceinline__ double draw_noise(const NoiseView& nz, uint32_t plane, uint32_t frame,
-                                             uint32_t ch, uint64_t cell_state, uint32_t r,
-                                             uint32_t c, uint32_t sr, uint32_t sc, uint32_t g,
-                                             uint32_t G, uint32_t n, double sigma) {
-  switch (nz.kind) {
-    case DPPX_NOISE_KEYED:
-      return laplace_from_uniform(uniform_from_bits(key_sub(cell_state, sr, sc)), sigma);
-    case DPPX_NOISE_PHILOX:
-      return laplace_from_uniform(
-          uniform_from_bits(philox_bits(nz.mixed_seeds[0], nz.frame_base + frame, ch, r, c, sr,
-                                        sc)),
-          sigma);
-    case DPPX_NOISE_INJECTED:
-      return nz.injected[((static_cast<size_t>(plane) * G + g) * n + sr) * n + sc];
-    default:
-      return 0.0;
+__device__ __forceinline__ DrawEnv make_env(int kind, bool exact_only, double area, double sigma) {
+  DrawEnv e;
+  e.kind = kind;
+  e.exact_only = exact_only;
+  const uint32_t ia = static_cast<uint32_t>(area);
+  e.pow2 = (ia & (ia - 1)) == 0 && static_cast<double>(ia) == area;
+  e.area = area;
+  e.sigma = sigma;
+  e.inv_area = 1.0f / static_cast<float>(area);
+  e.sigmaf = static_cast<float>(sigma);
+  e.margin = fast_margin(sigma);
+  return e;
+}
+
+__device__ __forceinline__ uint32_t quantize_stat(const DrawEnv& e, uint32_t sum, uint64_t bits,
+                                                  double injected) {
+  if (!e.exact_only) {
+    if (e.kind == DPPX_NOISE_KEYED || e.kind == DPPX_NOISE_PHILOX) {
+      const uint32_t q = fast_quantize(sum, e.inv_area, bits, e.sigmaf, e.margin);
+      if (q != 0xFFFFFFFFu) return q;
+    } else if (e.kind == DPPX_NOISE_NONE && e.pow2) {
+      // sum * 2^-k + 0.5 is exact in f32 (< 24 significant bits).
+      return static_cast<uint32_t>(floorf(static_cast<float>(sum) * e.inv_area + 0.5f));
+    }
   }
+  return exact_quantize(sum, e.area, e.kind, bits, e.sigma, injected);
 }
 
 // ---- PTX wrappers: mbarrier + bulk async copies (sm_90+ / sm_100a) ---------
@@ -143,16 +205,19 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
                : "memory");
 }
 
+// Blocking wait for the phase with `parity`; the thread is suspended in
+// hardware (suspend-time hint) instead of spinning, so a waiting producer or
+// consumer does not steal issue slots from the warps doing the work.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   asm volatile(
       "{\n"
       ".reg .pred P;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%0], %1;\n"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%0], %1, %2;\n"
       "@!P bra WAIT_%=;\n"
       "}\n" ::"r"(addr),
-      "r"(parity)
+      "r"(parity), "r"(0x100000u)
       : "memory");
 }
 

@@ -59,6 +59,7 @@ struct StatsArgs {
   const uint32_t* totals;    // adaptive: [F]
   double area, sub_area, sigma, sigma_sub;
   NoiseArgs noise;
+  int exact_noise;           // 1: always evaluate the f64 reference arithmetic
   // K1 (staged) only
   int tiles_per_row;
   int units;

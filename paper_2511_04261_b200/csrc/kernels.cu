@@ -30,12 +30,12 @@ namespace dppx {
 // ============================================================================
 // K0: classification + slot scan
 // ============================================================================
-constexpr int kClassifyThreads = 256;
+constexpr int kClassifyThreads = 128;
 
 __device__ __forceinline__ uint32_t sum_bytes4(uint32_t w) { return __dp4a(w, 0x01010101u, 0u); }
 
-// Exclusive block scan of 0/1 flags (256 threads). Returns the exclusive
-// prefix; *total receives the block total. Uses `warp_tot` (8 words) of smem.
+// Exclusive block scan of 0/1 flags (kClassifyThreads threads). Returns the
+// exclusive prefix; *total receives the block total. Uses `warp_tot` of smem.
 __device__ __forceinline__ uint32_t block_scan_flags(bool flag, uint32_t* warp_tot,
                                                      uint32_t* total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -55,7 +55,7 @@ __device__ __forceinline__ uint32_t block_scan_flags(bool flag, uint32_t* warp_t
   return before + in_warp;
 }
 
-// Exclusive block scan of u32 values (256 threads).
+// Exclusive block scan of u32 values (kClassifyThreads threads).
 __device__ __forceinline__ uint32_t block_scan_u32(uint32_t v, uint32_t* warp_tot,
                                                    uint32_t* total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -79,27 +79,64 @@ __device__ __forceinline__ uint32_t block_scan_u32(uint32_t v, uint32_t* warp_to
   return before + x - v;
 }
 
+// Mask sum of cell (r, c). Rows are reflected (image.cpp:105-110); interior
+// cells use aligned vector loads with all rows issued before the reduction.
+template <int B>
+__device__ __forceinline__ uint32_t mask_cell_sum_vec(const ClassifyArgs& a, const uint8_t* base,
+                                                      int r, int j0) {
+  uint32_t s = 0;
+  if constexpr (B % 16 == 0) {
+    constexpr int K = B / 16;
+    uint4 v[B][K];
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      const uint4* p = reinterpret_cast<const uint4*>(
+          base + static_cast<int64_t>(reflect_index(r * B + i, a.g.M)) * a.mpitch + j0);
+#pragma unroll
+      for (int k = 0; k < K; ++k) v[i][k] = __ldg(p + k);
+    }
+#pragma unroll
+    for (int i = 0; i < B; ++i)
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        s += sum_bytes4(v[i][k].x) + sum_bytes4(v[i][k].y) + sum_bytes4(v[i][k].z) +
+             sum_bytes4(v[i][k].w);
+  } else {
+    constexpr int K = B / 4;
+    uint32_t v[B][K];
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      const uint32_t* p = reinterpret_cast<const uint32_t*>(
+          base + static_cast<int64_t>(reflect_index(r * B + i, a.g.M)) * a.mpitch + j0);
+#pragma unroll
+      for (int k = 0; k < K; ++k) v[i][k] = __ldg(p + k);
+    }
+#pragma unroll
+    for (int i = 0; i < B; ++i)
+#pragma unroll
+      for (int k = 0; k < K; ++k) s += sum_bytes4(v[i][k]);
+  }
+  return s;
+}
+
 __device__ __forceinline__ uint32_t mask_cell_sum(const ClassifyArgs& a, const uint8_t* base,
                                                   int r, int c) {
   const BatchGeom& g = a.g;
   const int b = g.b;
   const int j0 = c * b;
+  if (j0 + b <= g.N && a.vec > 1) {
+    if (a.vec == 16) {
+      if (b == 16) return mask_cell_sum_vec<16>(a, base, r, j0);
+      if (b == 32) return mask_cell_sum_vec<32>(a, base, r, j0);
+    } else {
+      if (b == 4) return mask_cell_sum_vec<4>(a, base, r, j0);
+      if (b == 8) return mask_cell_sum_vec<8>(a, base, r, j0);
+    }
+  }
   uint32_t s = 0;
-  const bool inside = j0 + b <= g.N;
   for (int i = r * b; i < r * b + b; ++i) {
     const uint8_t* row = base + static_cast<int64_t>(reflect_index(i, g.M)) * a.mpitch;
-    if (inside && a.vec == 16) {
-      const uint4* p = reinterpret_cast<const uint4*>(row + j0);
-      for (int k = 0; k < b / 16; ++k) {
-        const uint4 v = __ldg(p + k);
-        s += sum_bytes4(v.x) + sum_bytes4(v.y) + sum_bytes4(v.z) + sum_bytes4(v.w);
-      }
-    } else if (inside && a.vec == 4) {
-      const uint32_t* p = reinterpret_cast<const uint32_t*>(row + j0);
-      for (int k = 0; k < b / 4; ++k) s += sum_bytes4(__ldg(p + k));
-    } else {
-      for (int j = j0; j < j0 + b; ++j) s += __ldg(row + reflect_index(j, g.N));
-    }
+    for (int j = j0; j < j0 + b; ++j) s += __ldg(row + reflect_index(j, g.N));
   }
   return s;
 }
@@ -200,16 +237,32 @@ __device__ __forceinline__ int64_t stat_offset(const StatsArgs& a, bool simple, 
   return base + S_tot + static_cast<int64_t>(slot_c) * a.g.n * a.g.n + sr * a.g.n + sc;
 }
 
-__device__ __forceinline__ uint32_t stat_value(const StatsArgs& a, uint32_t sum, bool whole_cell,
-                                               int f, int ch, int r, int c, int sr, int sc) {
-  const uint32_t plane = static_cast<uint32_t>(f * a.g.C + ch);
-  const double mean = cell_mean(sum, whole_cell ? a.area : a.sub_area);
-  const uint64_t cs =
-      a.noise.kind == DPPX_NOISE_KEYED ? key_cell(a.noise.mixed_seeds[plane], r, c) : 0ull;
-  NoiseView nv{a.noise.kind, a.noise.frame_base, a.noise.mixed_seeds, a.noise.injected};
-  const double noise = draw_noise(nv, plane, f, ch, cs, r, c, sr, sc, r * a.g.GC + c, a.g.G,
-                                  a.g.n, whole_cell ? a.sigma : a.sigma_sub);
-  return finalize_value(mean, noise);
+// 64 noise bits of statistic (r, c, sr, sc) of plane (f, ch). `cs` is the
+// KEYED per-cell state key_cell(mix64(seed), r, c) (noise.cpp:86-91).
+__device__ __noinline__ uint64_t philox_call(uint64_t seed, uint32_t frame, uint32_t ch, uint32_t r,
+                                             uint32_t c, uint32_t sr, uint32_t sc) {
+  return philox_bits(seed, frame, ch, r, c, sr, sc);
+}
+
+__device__ __forceinline__ uint64_t draw_bits(const StatsArgs& a, uint64_t cs, int f, int ch, int r,
+                                              int c, int sr, int sc) {
+  if (a.noise.kind == DPPX_NOISE_KEYED) return key_sub(cs, sr, sc);
+  if (a.noise.kind == DPPX_NOISE_PHILOX)  // out of line: keeps the hot loop small
+    return philox_call(a.noise.mixed_seeds[0], a.noise.frame_base + f, ch, r, c, sr, sc);
+  return 0ull;
+}
+
+__device__ __forceinline__ double injected_at(const StatsArgs& a, int f, int ch, int g_idx, int sr,
+                                              int sc) {
+  if (a.noise.kind != DPPX_NOISE_INJECTED) return 0.0;
+  const int64_t plane = static_cast<int64_t>(f) * a.g.C + ch;
+  return a.noise.injected[((plane * a.g.G + g_idx) * a.g.n + sr) * a.g.n + sc];
+}
+
+__device__ __forceinline__ uint64_t cell_state(const StatsArgs& a, int f, int ch, int r, int c) {
+  return a.noise.kind == DPPX_NOISE_KEYED
+             ? key_cell(a.noise.mixed_seeds[static_cast<int64_t>(f) * a.g.C + ch], r, c)
+             : 0ull;
 }
 
 // ============================================================================
@@ -309,8 +362,9 @@ __device__ __forceinline__ void accumulate_row(const uint8_t* row, uint32_t (&ac
 // Values of the C channels of one statistic, computed by the GL lanes of a
 // lane group (each lane draws a subset of channels) and shared by shuffles.
 template <int C, int GL>
-__device__ __forceinline__ void group_values(const StatsArgs& a, bool active, const uint32_t (&sum)[C],
-                                             bool whole, int f, int r, int c, int sr, int sc,
+__device__ __forceinline__ void group_values(const StatsArgs& a, const DrawEnv& env, bool active,
+                                             const uint32_t (&sum)[C], const uint64_t (&cs)[C],
+                                             int f, int r, int c, int sr, int sc,
                                              uint32_t (&val)[C]) {
   const int lane = threadIdx.x & 31;
   const int li = lane % GL;
@@ -321,10 +375,15 @@ __device__ __forceinline__ void group_values(const StatsArgs& a, bool active, co
     uint32_t v = 0;
     if (active && ch < C) {
       uint32_t s = sum[0];
+      uint64_t st = cs[0];
 #pragma unroll
       for (int k = 1; k < C; ++k)
-        if (ch == k) s = sum[k];
-      v = stat_value(a, s, whole, f, ch, r, c, sr, sc);
+        if (ch == k) {
+          s = sum[k];
+          st = cs[k];
+        }
+      v = quantize_stat(env, s, draw_bits(a, st, f, ch, r, c, sr, sc),
+                        injected_at(a, f, ch, r * a.g.GC + c, sr, sc));
     }
 #pragma unroll
     for (int k = c0; k < C && k < c0 + GL; ++k)
@@ -381,6 +440,8 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats_tma(const StatsArgs a) 
   // ---------------- consumer warps ----------------
   const int t = threadIdx.x;  // strip index within the tile
   const BatchGeom& g = a.g;
+  const DrawEnv env_cell = make_env(a.noise.kind, a.exact_noise != 0, a.area, a.sigma);
+  const DrawEnv env_sub = make_env(a.noise.kind, a.exact_noise != 0, a.sub_area, a.sigma_sub);
   int k = 0;
   for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++k) {
     const int s = k % S;
@@ -402,6 +463,9 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats_tma(const StatsArgs a) 
     const int vbytes = valid_bytes<C>(a, p.px0);
     const int copy = vbytes & ~15;
     const int need = min(kTilePx, g.GC * B - p.px0) * C;
+    uint64_t cs[C];
+#pragma unroll
+    for (int ch = 0; ch < C; ++ch) cs[ch] = cell_state(a, p.f, ch, p.r, cell);
 
     mbar_wait(&full_bar[s], (k / S) & 1);
 
@@ -424,7 +488,9 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats_tma(const StatsArgs a) 
     const bool emit = a.out != nullptr;
     uint8_t* mystrip = st + t * 4 * C;
 
-#pragma unroll
+    // Not unrolled over vertical subcells: keeps the hot loop small enough for
+    // the instruction cache (the rows inside are unrolled).
+#pragma unroll 1
     for (int vs = 0; vs < NSUB; ++vs) {
       uint32_t acc[C];
 #pragma unroll
@@ -440,7 +506,7 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats_tma(const StatsArgs a) 
 #pragma unroll
           for (int ch = 0; ch < C; ++ch) acc[ch] += __shfl_xor_sync(0xFFFFFFFFu, acc[ch], o);
         uint32_t val[C];
-        group_values<C, SB4>(a, active && !simple, acc, false, p.f, p.r, cell, vs, sc, val);
+        group_values<C, SB4>(a, env_sub, active && !simple, acc, cs, p.f, p.r, cell, vs, sc, val);
         if (active && !simple) {
           if (lic % SB4 == 0) {
             const int64_t off = stat_offset(a, false, gidx, slot_s, S_tot, vs, sc);
@@ -469,7 +535,7 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats_tma(const StatsArgs a) 
       for (int ch = 0; ch < C; ++ch) tot[ch] += __shfl_xor_sync(0xFFFFFFFFu, tot[ch], o);
     {
       uint32_t val[C];
-      group_values<C, B4>(a, active && simple, tot, true, p.f, p.r, cell, 0, 0, val);
+      group_values<C, B4>(a, env_cell, active && simple, tot, cs, p.f, p.r, cell, 0, 0, val);
       if (active && simple) {
         if (lic == 0) {
           const int64_t off = stat_offset(a, true, gidx, slot_s, S_tot, 0, 0);
@@ -527,7 +593,10 @@ __global__ void __launch_bounds__(kGenericThreads) k_stats_generic(const StatsAr
     }
     const int nsub = simple ? 1 : g.n;
     const int side = simple ? g.b : g.sb;
+    const DrawEnv env = make_env(a.noise.kind, a.exact_noise != 0, simple ? a.area : a.sub_area,
+                                 simple ? a.sigma : a.sigma_sub);
     for (int ch = 0; ch < g.C; ++ch) {
+      const uint64_t cs = cell_state(a, f, ch, r, c);
       for (int sr = 0; sr < nsub; ++sr)
         for (int sc = 0; sc < nsub; ++sc) {
           const int i0 = r * g.b + sr * side, j0 = c * g.b + sc * side;
@@ -536,7 +605,8 @@ __global__ void __launch_bounds__(kGenericThreads) k_stats_generic(const StatsAr
             const uint8_t* row = img + static_cast<int64_t>(reflect_index(i, g.M)) * a.pitch;
             for (int j = j0; j < j0 + side; ++j) sum += row[reflect_index(j, g.N) * g.C + ch];
           }
-          const uint32_t v = stat_value(a, sum, simple, f, ch, r, c, simple ? 0 : sr, simple ? 0 : sc);
+          const uint32_t v = quantize_stat(env, sum, draw_bits(a, cs, f, ch, r, c, sr, sc),
+                                           injected_at(a, f, ch, gidx, sr, sc));
           a.stats[static_cast<int64_t>(f * g.C + ch) * a.sstride +
                   stat_offset(a, simple, gidx, slot_s, S_tot, sr, sc)] = static_cast<uint8_t>(v);
           if (a.out) {
@@ -642,6 +712,19 @@ __global__ void k_synth(BatchGeom g, uint32_t data_seed, uint32_t f0, uint8_t* i
   }
 }
 
+// Max |lg2.approx(m) - log2(m)| over every f32 mantissa m in [1, 2): the
+// bound the fast quantization path relies on (dppx_device.cuh).
+__global__ void k_debug_lg2(unsigned int* max_bits) {
+  float worst = 0.f;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < (1u << 23);
+       i += gridDim.x * blockDim.x) {
+    const float m = __uint_as_float(0x3F800000u | i);
+    const double exact = log2(static_cast<double>(m));
+    worst = fmaxf(worst, static_cast<float>(fabs(static_cast<double>(__log2f(m)) - exact)));
+  }
+  atomicMax(max_bits, __float_as_uint(worst));
+}
+
 __global__ void k_debug_laplace(uint64_t mixed_seed, const uint32_t* keys, int count, double sigma,
                                 double* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -717,6 +800,11 @@ cudaError_t launch_synth(const BatchGeom& g, uint32_t seed, uint32_t f0, uint8_t
                          int64_t pitch, int64_t fstride, uint8_t* mask, int64_t mpitch,
                          int64_t mfstride, cudaStream_t s) {
   k_synth<<<148 * 8, 256, 0, s>>>(g, seed, f0, img, pitch, fstride, mask, mpitch, mfstride);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_debug_lg2(unsigned int* out, cudaStream_t s) {
+  k_debug_lg2<<<148 * 4, 256, 0, s>>>(out);
   return cudaGetLastError();
 }
 

@@ -10,12 +10,10 @@ import numpy as np
 import pytest
 
 import oracle
-from tests.conftest import HAVE_GPU
 
 pytestmark = pytest.mark.gpu
 
-if HAVE_GPU:
-    import paper_2511_04261_b200 as dp
+import paper_2511_04261_b200 as dp
 
 FAST_BN = [(4, 1), (8, 1), (8, 2), (16, 1), (16, 2), (16, 4), (32, 1), (32, 2), (32, 4), (32, 8)]
 
@@ -275,3 +273,29 @@ def test_device_entry_points_with_torch(ctx):
     for i in range(2 * C):
         assert bytes(pl_host[i, : ln[i]]) == rp[i]
     assert np.array_equal(out.cpu().numpy().reshape(F, M, N, C)[:2], ri)
+
+
+def test_fast_path_error_bound_holds(ctx):
+    """The bounded f32 path assumes |lg2.approx - log2| <= 2^-21 on [1, 2);
+    checked over all 2^23 mantissas on this device."""
+    err = ctx.lg2_max_error()
+    assert err <= 2.0 ** -21, err
+
+
+@pytest.mark.parametrize("eps,b,n", [(0.5, 16, 4), (0.1, 8, 2), (1.0, 32, 8), (0.5, 4, 1)])
+def test_fast_path_equals_exact_path(ctx, eps, b, n):
+    """Bytes from the bounded fast path == bytes from the f64 reference
+    arithmetic on every statistic (many draws, both KEYED and PHILOX)."""
+    F, M, N, C = 4, 270, 481, 3
+    frames = oracle.synth_frames(7, F, M, N, C)
+    masks = oracle.synth_masks(7, F, M, N)
+    p = dp.make_privacy_params(eps, 16, b, n)
+    for kind in (dp.NOISE_KEYED, dp.NOISE_PHILOX):
+        seeds = dp.plane_seeds(99, F, C) if kind == dp.NOISE_KEYED else [99]
+        fast = ctx.pixelize_adaptive(frames, masks, p, kind, seeds)
+        ctx.set_exact_noise(True)
+        try:
+            exact = ctx.pixelize_adaptive(frames, masks, p, kind, seeds)
+        finally:
+            ctx.set_exact_noise(False)
+        assert fast[0] == exact[0] and np.array_equal(fast[1], exact[1])
