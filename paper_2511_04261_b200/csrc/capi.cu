@@ -79,7 +79,7 @@ struct dppx_ctx {
   cudaStream_t s_in = nullptr, s_out = nullptr;
   std::string err;
   // scratch
-  DevBuf cellinfo, rowcnt, rowprefix, totals, counters, status, seeds, keys, dbl;
+  DevBuf cellinfo, rowcnt, rowprefix, totals, counters, status, seeds, keys, dbl, work;
   uint64_t* seeds_pinned = nullptr;
   size_t seeds_pinned_n = 0;
   cudaEvent_t seeds_ev = nullptr;
@@ -335,6 +335,9 @@ int run_stats(dppx_ctx* ctx, StatsArgs& a) {
       per_sm = it->second;
     }
     const int grid = static_cast<int>(std::min<int64_t>(units, static_cast<int64_t>(std::max(per_sm, 1)) * ctx->sms));
+    if (int rc = ensure(ctx, ctx->work, 16)) return rc;
+    a.work_counter = static_cast<int*>(ctx->work.p);
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->work.p, 0, sizeof(int), ctx->stream));
     timing_begin(ctx, DPPX_K_STATS, &pt);
     CUDA_TRY(ctx, launch_stats_tma(k, a, grid, smem, ctx->stream));
   } else {
@@ -750,7 +753,7 @@ void dppx_ctx_destroy(dppx_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
   DevBuf* bufs[] = {&ctx->cellinfo, &ctx->rowcnt, &ctx->rowprefix, &ctx->totals, &ctx->counters,
-                    &ctx->status, &ctx->seeds, &ctx->keys, &ctx->dbl};
+                    &ctx->status, &ctx->seeds, &ctx->keys, &ctx->dbl, &ctx->work};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (int s = 0; s < 2; ++s) {

@@ -64,6 +64,7 @@ struct StatsArgs {
   int tiles_per_row;
   int units;
   int stages;
+  int* work_counter;         // zeroed before each launch; units are claimed dynamically
 };
 
 // K2: statistics -> pixels.

@@ -335,18 +335,19 @@ __device__ __forceinline__ void pattern_words(const uint32_t (&v)[C], uint32_t (
   }
 }
 
-// Per-channel byte sums of one 4-px strip row held in C words.
+// Per-channel byte sums of one 4-px strip row held in C words, added to acc.
+// Each row's partial starts from zero so rows form independent dp4a chains.
 template <int C>
 __device__ __forceinline__ void accumulate_row(const uint8_t* row, uint32_t (&acc)[C]) {
   const uint32_t* w = reinterpret_cast<const uint32_t*>(row);
   if constexpr (C == 1) {
-    acc[0] = __dp4a(w[0], 0x01010101u, acc[0]);
+    acc[0] += __dp4a(w[0], 0x01010101u, 0u);
   } else if constexpr (C == 3) {
     const uint32_t w0 = w[0], w1 = w[1], w2 = w[2];
     // bytes: w0 = R G B R, w1 = G B R G, w2 = B R G B (little-endian)
-    acc[0] = __dp4a(w0, 0x01000001u, __dp4a(w1, 0x00010000u, __dp4a(w2, 0x00000100u, acc[0])));
-    acc[1] = __dp4a(w0, 0x00000100u, __dp4a(w1, 0x01000001u, __dp4a(w2, 0x00010000u, acc[1])));
-    acc[2] = __dp4a(w0, 0x00010000u, __dp4a(w1, 0x00000100u, __dp4a(w2, 0x01000001u, acc[2])));
+    acc[0] += __dp4a(w0, 0x01000001u, __dp4a(w1, 0x00010000u, __dp4a(w2, 0x00000100u, 0u)));
+    acc[1] += __dp4a(w0, 0x00000100u, __dp4a(w1, 0x01000001u, __dp4a(w2, 0x00010000u, 0u)));
+    acc[2] += __dp4a(w0, 0x00010000u, __dp4a(w1, 0x00000100u, __dp4a(w2, 0x01000001u, 0u)));
   } else {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -401,14 +402,17 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats_tma(const StatsArgs a) 
   static_assert(SB % 4 == 0 && 32 % B4 == 0, "fast-path geometry");
 
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full_bar[kMaxStages];
-  __shared__ __align__(8) uint64_t done_bar[kMaxStages];
+  __shared__ __align__(8) uint64_t full_bar[kMaxStages];  // TMA bytes landed
+  __shared__ __align__(8) uint64_t id_bar[kMaxStages];    // stage_unit[s] published
+  __shared__ __align__(8) uint64_t done_bar[kMaxStages];  // consumers finished the stage
+  __shared__ int stage_unit[kMaxStages];                  // unit in stage s, -1 = no more work
 
   const int S = a.stages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full_bar[s], 1);
+      mbar_init(&id_bar[s], 1);
       mbar_init(&done_bar[s], kConsumers);
     }
     fence_mbarrier_init();
@@ -417,20 +421,33 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats_tma(const StatsArgs a) 
 
   if (warp == kConsumers / 32) {
     // ---------------- producer warp: TMA loads + bulk stores ----------------
+    // Units (frame, grid row, 512-px tile) are claimed from a global counter so
+    // heavy (complex-cell) tiles spread over all CTAs.
     if (lane == 0) {
       int k = 0;
-      for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++k) {
+      int done_units = 0;  // units of this CTA already stored
+      for (;; ++k) {
         const int s = k % S;
         if (k >= S) {
           mbar_wait(&done_bar[s], ((k / S) - 1) & 1);
-          if (a.out) store_unit<C, B>(a, u - S * static_cast<int>(gridDim.x), smem + s * STAGE);
+          if (a.out) store_unit<C, B>(a, stage_unit[s], smem + s * STAGE);
+          ++done_units;
+        }
+        int u = atomicAdd(a.work_counter, 1);
+        if (u >= a.units) u = -1;
+        stage_unit[s] = u;
+        mbar_arrive(&id_bar[s]);
+        if (u < 0) {
+          mbar_arrive_expect_tx(&full_bar[s], 0);
+          break;
         }
         load_unit<C, B>(a, u, smem + s * STAGE, &full_bar[s]);
       }
-      for (int j = k > S ? k - S : 0; j < k; ++j) {
+      // k units were loaded; units [done_units, k) still need their store.
+      for (int j = done_units; j < k; ++j) {
         const int s = j % S;
         mbar_wait(&done_bar[s], (j / S) & 1);
-        if (a.out) store_unit<C, B>(a, blockIdx.x + j * gridDim.x, smem + s * STAGE);
+        if (a.out) store_unit<C, B>(a, stage_unit[s], smem + s * STAGE);
       }
       bulk_wait_all();
     }
@@ -442,10 +459,12 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats_tma(const StatsArgs a) 
   const BatchGeom& g = a.g;
   const DrawEnv env_cell = make_env(a.noise.kind, a.exact_noise != 0, a.area, a.sigma);
   const DrawEnv env_sub = make_env(a.noise.kind, a.exact_noise != 0, a.sub_area, a.sigma_sub);
-  int k = 0;
-  for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++k) {
+  for (int k = 0;; ++k) {
     const int s = k % S;
     uint8_t* st = smem + s * STAGE;
+    mbar_wait(&id_bar[s], (k / S) & 1);
+    const int u = *reinterpret_cast<volatile int*>(&stage_unit[s]);
+    if (u < 0) break;
     const UnitPos p = decode_unit(a, u);
     const int cell = p.px0 / B + t / B4;
     const int lic = t % B4;        // lane within cell
