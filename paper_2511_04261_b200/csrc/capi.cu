@@ -2,6 +2,8 @@
 // scratch, pinned staging), argument validation with the reference's error
 // semantics, kernel selection, and the pinned double-buffered
 // H2D -> K0/K1 -> D2H pipeline of the host entry points.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -19,14 +21,14 @@
 #include "dppx_params.h"
 
 namespace dppx {
-using StatsKernel = void (*)(const StatsArgs);
+using StatsKernel = void (*)(const CUtensorMap, const CUtensorMap, const StatsArgs);
 StatsKernel select_stats_kernel(int C, int b, int n, bool adaptive);
 int stats_threads();
 int stats_tile_px();
 int stats_max_stages();
 cudaError_t launch_classify(const ClassifyArgs& a, cudaStream_t s);
-cudaError_t launch_stats_tma(StatsKernel k, const StatsArgs& a, int grid, size_t smem,
-                             cudaStream_t s);
+cudaError_t launch_stats_tma(StatsKernel k, const CUtensorMap& tin, const CUtensorMap& tout,
+                             const StatsArgs& a, int grid, size_t smem, cudaStream_t s);
 cudaError_t launch_stats_generic(const StatsArgs& a, cudaStream_t s);
 cudaError_t launch_expand(const ExpandArgs& a, cudaStream_t s);
 cudaError_t launch_synth(const BatchGeom& g, uint32_t seed, uint32_t f0, uint8_t* img,
@@ -173,6 +175,34 @@ void collect_timings(dppx_ctx* ctx) {
   ctx->pending.clear();
 }
 
+// ---- TMA tensor maps ---------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// F frames x M rows x (row_bytes / 8) u64 elements, box (box_bytes / 8) x rows x 1.
+bool encode_frames_map(CUtensorMap* m, const void* base, int64_t row_bytes, int M, int F,
+                       int64_t pitch, int64_t fstride, int box_bytes, int box_rows) {
+  auto enc = tensor_map_encoder();
+  if (!enc || row_bytes < 8) return false;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(row_bytes / 8), static_cast<cuuint64_t>(M),
+                              static_cast<cuuint64_t>(F)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(pitch), static_cast<cuuint64_t>(fstride)};
+  const cuuint32_t box[3] = {static_cast<cuuint32_t>(box_bytes / 8), static_cast<cuuint32_t>(box_rows), 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // ---- validation mirroring the reference's throws ----------------------------
 int geometry(dppx_ctx* ctx, int M, int N, int C, int F, int b, int n, BatchGeom* g,
              bool check_pad) {
@@ -311,12 +341,23 @@ int run_stats(dppx_ctx* ctx, StatsArgs& a) {
   const bool aligned = aligned16(a.img) && a.pitch % 16 == 0 && a.fstride % 16 == 0 &&
                        (!a.out || (aligned16(a.out) && a.opitch % 16 == 0 && a.ofstride % 16 == 0));
   PendingTiming pt;
-  if (k && aligned && g.F > 0) {
-    const int tile = stats_tile_px();
+  CUtensorMap tin{}, tout{};
+  const int tile = stats_tile_px();
+  const int64_t row_bytes = static_cast<int64_t>(g.N) * g.C;
+  bool maps = k && aligned && g.F > 0 && tile * g.C / 8 <= 256 && g.b <= 256 &&
+              encode_frames_map(&tin, a.img, row_bytes, g.M, g.F, a.pitch, a.fstride, tile * g.C, g.b);
+  if (maps && a.out)
+    maps = encode_frames_map(&tout, a.out, row_bytes, g.M, g.F, a.opitch, a.ofstride, tile * g.C, g.b);
+  if (maps && !a.out) tout = tin;
+  if (maps) {
+    a.tensor_in_bytes = static_cast<int>(row_bytes / 8 * 8);
+    a.tensor_out_bytes = a.tensor_in_bytes;
     a.tiles_per_row = (g.GC * g.b + tile - 1) / tile;
     const int64_t units = static_cast<int64_t>(g.F) * g.GR * a.tiles_per_row;
     if (units > 0x7FFFFFFF) return set_err(ctx, DPPX_ERR_INVALID, "batch too large for one launch");
     a.units = static_cast<int>(units);
+    a.div_tiles = make_fastdiv(static_cast<uint32_t>(a.tiles_per_row));
+    a.div_rows = make_fastdiv(static_cast<uint32_t>(g.GR));
     const size_t stage = static_cast<size_t>(g.b) * tile * g.C;
     int S = static_cast<int>((72 * 1024) / stage);
     S = std::max(2, std::min(stats_max_stages(), S));
@@ -339,7 +380,7 @@ int run_stats(dppx_ctx* ctx, StatsArgs& a) {
     a.work_counter = static_cast<int*>(ctx->work.p);
     CUDA_TRY(ctx, cudaMemsetAsync(ctx->work.p, 0, sizeof(int), ctx->stream));
     timing_begin(ctx, DPPX_K_STATS, &pt);
-    CUDA_TRY(ctx, launch_stats_tma(k, a, grid, smem, ctx->stream));
+    CUDA_TRY(ctx, launch_stats_tma(k, tin, tout, a, grid, smem, ctx->stream));
   } else {
     timing_begin(ctx, DPPX_K_GENERIC, &pt);
     if (g.F > 0) CUDA_TRY(ctx, launch_stats_generic(a, ctx->stream));

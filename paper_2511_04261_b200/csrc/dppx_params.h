@@ -8,6 +8,28 @@
 
 namespace dppx {
 
+// n / d for n < 2^31 by multiply-shift: s = 31 + ceil(log2 d), m = ceil(2^s / d)
+// (then n*m / 2^s < n/d + 1/d, so the floor is exact).
+struct FastDiv {
+  uint32_t d, m, s;
+#ifdef __CUDACC__
+  __host__ __device__
+#endif
+  uint32_t div(uint32_t n) const {
+    return static_cast<uint32_t>((static_cast<uint64_t>(n) * m) >> s);
+  }
+};
+
+inline FastDiv make_fastdiv(uint32_t d) {
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;
+  FastDiv f;
+  f.d = d;
+  f.s = 31 + l;
+  f.m = static_cast<uint32_t>(((1ull << f.s) + d - 1) / d);
+  return f;
+}
+
 // Geometry of one batch (GridGeometry image.hpp:71-82, plus batch shape).
 struct BatchGeom {
   int M, N, C, F;         // rows, cols, channels, frames
@@ -65,6 +87,9 @@ struct StatsArgs {
   int units;
   int stages;
   int* work_counter;         // zeroed before each launch; units are claimed dynamically
+  FastDiv div_tiles, div_rows;
+  int tensor_in_bytes;       // row bytes covered by the input tensor map (N*C rounded down to 8)
+  int tensor_out_bytes;      // same for the output tensor map
 };
 
 // K2: statistics -> pixels.

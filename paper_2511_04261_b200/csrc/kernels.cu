@@ -18,6 +18,7 @@
 //                      adaptive.cpp:181-245.
 //  K1g k_stats_generic same semantics for any b, n, C and alignment.
 //  K2  k_expand        statistics -> pixels (broadcast_means / reassemble).
+#include <cuda.h>  // CUtensorMap (type only; encoded on the host via the driver entry point)
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -279,10 +280,11 @@ struct UnitPos {
 
 __device__ __forceinline__ UnitPos decode_unit(const StatsArgs& a, int u) {
   UnitPos p;
-  p.tile = u % a.tiles_per_row;
-  const int rest = u / a.tiles_per_row;
-  p.r = rest % a.g.GR;
-  p.f = rest / a.g.GR;
+  const uint32_t rest = a.div_tiles.div(static_cast<uint32_t>(u));
+  p.tile = u - static_cast<int>(rest * a.div_tiles.d);
+  const uint32_t f = a.div_rows.div(rest);
+  p.r = static_cast<int>(rest - f * a.div_rows.d);
+  p.f = static_cast<int>(f);
   p.px0 = p.tile * kTilePx;
   return p;
 }
@@ -292,9 +294,29 @@ __device__ __forceinline__ int valid_bytes(const StatsArgs& a, int px0) {
   return min(kTilePx, a.g.N - px0) * C;
 }
 
+// A band whose rows run past M needs mirrored rows (image.cpp:105-110): it is
+// staged row by row with 1-D bulk copies; every other band is one 3-D box.
+template <int B>
+__device__ __forceinline__ bool band_reflects(const StatsArgs& a, int r) {
+  return (r + 1) * B > a.g.M;
+}
+
+// Bytes of each smem row that the producer's copies deliver for unit p.
 template <int C, int B>
-__device__ __forceinline__ void load_unit(const StatsArgs& a, int u, uint8_t* st, uint64_t* bar) {
+__device__ __forceinline__ int staged_bytes(const StatsArgs& a, const UnitPos& p) {
+  if (band_reflects<B>(a, p.r)) return valid_bytes<C>(a, p.px0) & ~15;
+  return max(0, min(kTilePx * C, a.tensor_in_bytes - p.px0 * C));
+}
+
+template <int C, int B>
+__device__ __forceinline__ void load_unit(const StatsArgs& a, const CUtensorMap* tm, int u,
+                                          uint8_t* st, uint64_t* bar) {
   const UnitPos p = decode_unit(a, u);
+  if (!band_reflects<B>(a, p.r)) {
+    mbar_arrive_expect_tx(bar, B * kTilePx * C);  // full box, OOB bytes zero-filled
+    tma_load_3d(st, tm, p.px0 * C / 8, p.r * B, p.f, bar);
+    return;
+  }
   const uint32_t copy = static_cast<uint32_t>(valid_bytes<C>(a, p.px0)) & ~15u;
   mbar_arrive_expect_tx(bar, copy * B);
   if (copy == 0) return;
@@ -306,16 +328,14 @@ __device__ __forceinline__ void load_unit(const StatsArgs& a, int u, uint8_t* st
   }
 }
 
+// One 3-D box store: rows >= M and bytes past the tensor's row are clipped by
+// the TMA unit; the consumers write the (< 8) bytes past tensor_out_bytes.
 template <int C, int B>
-__device__ __forceinline__ void store_unit(const StatsArgs& a, int u, const uint8_t* st) {
+__device__ __forceinline__ void store_unit(const StatsArgs& a, const CUtensorMap* tm, int u,
+                                           const uint8_t* st) {
   const UnitPos p = decode_unit(a, u);
-  const uint32_t copy = static_cast<uint32_t>(valid_bytes<C>(a, p.px0)) & ~15u;
-  if (copy == 0) return;
-  uint8_t* dst = a.out + static_cast<int64_t>(p.f) * a.ofstride + static_cast<int64_t>(p.px0) * C;
-  const int rows = min(B, a.g.M - p.r * B);
-#pragma unroll 1
-  for (int i = 0; i < rows; ++i)
-    bulk_s2g(dst + static_cast<int64_t>(p.r * B + i) * a.opitch, st + i * (kTilePx * C), copy);
+  if (p.px0 * C >= a.tensor_out_bytes) return;
+  tma_store_3d(tm, p.px0 * C / 8, p.r * B, p.f, st);
   bulk_commit();
   bulk_wait_read_all();
 }
@@ -393,7 +413,9 @@ __device__ __forceinline__ void group_values(const StatsArgs& a, const DrawEnv& 
 }
 
 template <int C, int B4, int NSUB, bool ADAPTIVE>
-__global__ void __launch_bounds__(kStatsThreads) k_stats_tma(const StatsArgs a) {
+__global__ void __launch_bounds__(kStatsThreads)
+    k_stats_tma(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
+                const StatsArgs a) {
   constexpr int B = 4 * B4;
   constexpr int SB = B / NSUB;
   constexpr int SB4 = SB / 4;
@@ -424,13 +446,15 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats_tma(const StatsArgs a) 
     // Units (frame, grid row, 512-px tile) are claimed from a global counter so
     // heavy (complex-cell) tiles spread over all CTAs.
     if (lane == 0) {
+      prefetch_tmap(&tm_in);
+      prefetch_tmap(&tm_out);
       int k = 0;
       int done_units = 0;  // units of this CTA already stored
       for (;; ++k) {
         const int s = k % S;
         if (k >= S) {
           mbar_wait(&done_bar[s], ((k / S) - 1) & 1);
-          if (a.out) store_unit<C, B>(a, stage_unit[s], smem + s * STAGE);
+          if (a.out) store_unit<C, B>(a, &tm_out, stage_unit[s], smem + s * STAGE);
           ++done_units;
         }
         int u = atomicAdd(a.work_counter, 1);
@@ -441,13 +465,13 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats_tma(const StatsArgs a) 
           mbar_arrive_expect_tx(&full_bar[s], 0);
           break;
         }
-        load_unit<C, B>(a, u, smem + s * STAGE, &full_bar[s]);
+        load_unit<C, B>(a, &tm_in, u, smem + s * STAGE, &full_bar[s]);
       }
       // k units were loaded; units [done_units, k) still need their store.
       for (int j = done_units; j < k; ++j) {
         const int s = j % S;
         mbar_wait(&done_bar[s], (j / S) & 1);
-        if (a.out) store_unit<C, B>(a, stage_unit[s], smem + s * STAGE);
+        if (a.out) store_unit<C, B>(a, &tm_out, stage_unit[s], smem + s * STAGE);
       }
       bulk_wait_all();
     }
@@ -480,7 +504,8 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats_tma(const StatsArgs a) 
       S_tot = __ldg(&a.totals[p.f]);
     }
     const int vbytes = valid_bytes<C>(a, p.px0);
-    const int copy = vbytes & ~15;
+    const int copy = staged_bytes<C, B>(a, p);  // bytes per row the producer staged
+    const int scopy = max(0, min(kTilePx * C, a.tensor_out_bytes - p.px0 * C));  // stored by TMA
     const int need = min(kTilePx, g.GC * B - p.px0) * C;
     uint64_t cs[C];
 #pragma unroll
@@ -574,12 +599,12 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats_tma(const StatsArgs a) 
       }
     }
 
-    // Output bytes past the last 16-byte multiple of the row are written here
-    // (the bulk store covers [0, copy)).
-    if (emit && active && (t + 1) * 4 * C > copy && t * 4 * C < vbytes) {
+    // Output bytes past the tensor map's row extent are written here (the
+    // TMA store covers [0, scopy)).
+    if (emit && active && (t + 1) * 4 * C > scopy && t * 4 * C < vbytes) {
       const int rows = min(B, g.M - p.r * B);
       for (int i = 0; i < rows; ++i)
-        for (int x = max(t * 4 * C, copy); x < min((t + 1) * 4 * C, vbytes); ++x)
+        for (int x = max(t * 4 * C, scopy); x < min((t + 1) * 4 * C, vbytes); ++x)
           a.out[static_cast<int64_t>(p.f) * a.ofstride + static_cast<int64_t>(p.r * B + i) * a.opitch +
                 static_cast<int64_t>(p.px0) * C + x] = st[i * ROWB + x];
     }
@@ -756,7 +781,7 @@ __global__ void k_debug_laplace(uint64_t mixed_seed, const uint32_t* keys, int c
 // ============================================================================
 // Host-side launchers (called from capi.cu)
 // ============================================================================
-using StatsKernel = void (*)(const StatsArgs);
+using StatsKernel = void (*)(const CUtensorMap, const CUtensorMap, const StatsArgs);
 
 template <int C, bool AD>
 StatsKernel pick_b(int b, int n) {
@@ -795,9 +820,9 @@ cudaError_t launch_classify(const ClassifyArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_stats_tma(StatsKernel k, const StatsArgs& a, int grid, size_t smem,
-                             cudaStream_t s) {
-  k<<<grid, kStatsThreads, smem, s>>>(a);
+cudaError_t launch_stats_tma(StatsKernel k, const CUtensorMap& tin, const CUtensorMap& tout,
+                             const StatsArgs& a, int grid, size_t smem, cudaStream_t s) {
+  k<<<grid, kStatsThreads, smem, s>>>(tin, tout, a);
   return cudaGetLastError();
 }
 

@@ -73,7 +73,8 @@ def test_fast_path_uniform_matches_oracle(ctx, C, b):
         seeds = dp.plane_seeds(7, 2, C)
         ctx.reset_stats()
         means, img = ctx.pixelize_uniform(frames, p, dp.NOISE_KEYED, seeds)
-        assert ctx.stats()["launches"]["stats_tma"] >= 1
+        if N * C >= 16:  # narrower rows cannot form a TMA box: generic kernel
+            assert ctx.stats()["launches"]["stats_tma"] >= 1
         rm, ri = _oracle_uniform(frames, p, "keyed", seeds)
         assert np.array_equal(means, rm), (M, N)
         assert np.array_equal(img, ri), (M, N)
