@@ -1,0 +1,95 @@
+"""The oracle reproduces the committed fixtures made from the reference itself
+(tests/golden/make_golden.py over oracle/_ref, i.e. /root/reference compiled
+from its sources). Pins the restatement even where /root/reference is absent."""
+import hashlib
+import json
+import os
+
+import numpy as np
+
+import oracle
+
+G = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def ulps(a, b):
+    return abs(np.array([a]).view(np.int64)[0] - np.array([b]).view(np.int64)[0])
+
+
+def test_noise_vectors():
+    d = json.load(open(os.path.join(G, "noise.json")))
+    worst = 0
+    for v in d["draws"]:
+        seed = int(v["seed"])
+        assert oracle.keyed_bits(seed, *v["key"]) == int(v["bits"])
+        assert oracle.uniform_from_bits(int(v["bits"])) == float.fromhex(v["u"])
+        worst = max(worst, ulps(oracle.laplace_at(seed, *v["key"], v["sigma"]),
+                                float.fromhex(v["laplace"])))
+    # glibc log1p is IFUNC-dispatched per CPU; identical on the generating host
+    assert worst <= 2
+    assert oracle.uniform_from_bits(0) == float.fromhex(d["ends"]["u_of_0"])
+    assert oracle.uniform_from_bits(2**64 - 1) == float.fromhex(d["ends"]["u_of_max"])
+
+
+def test_small_cases():
+    z = np.load(os.path.join(G, "small_cases.npz"))
+    ids = sorted({k.split("_")[0] for k in z.files})
+    assert len(ids) == 40
+    for k in ids:
+        M, N, b, n, m, has = (int(x) for x in z[f"{k}_params"])
+        eps = float(z[f"{k}_eps"][0])
+        seed = int(z[f"{k}_seed"][0])
+        kind = "none" if has < 0 else "keyed"
+        p = oracle.make_privacy_params(eps, m, b, n)
+        img, mask = z[f"{k}_img"], z[f"{k}_mask"]
+        means, uimg = oracle.pixelize_uniform(img, b, oracle.make_privacy_params(eps, m, b).sigma,
+                                              kind, [seed])
+        assert np.array_equal(means[0], z[f"{k}_umeans"]) and np.array_equal(uimg, z[f"{k}_uimg"]), k
+        pl, aimg = oracle.pixelize_adaptive(img, mask, b, n, p.sigma, p.sigma_sub, kind, [seed])
+        assert pl[0] == z[f"{k}_payload"].tobytes() and np.array_equal(aimg, z[f"{k}_aimg"]), k
+        assert np.array_equal(oracle.reassemble(pl[0], M, N, b, n), aimg)
+        ref1 = oracle.pixelize_reference(img, b, oracle.make_privacy_params(eps, m, b).sigma,
+                                         None if has < 0 else seed)
+        assert np.array_equal(ref1, z[f"{k}_refimg"]), k
+
+
+def test_shaped_cases():
+    z = np.load(os.path.join(G, "shaped_cases.npz"))
+    names = sorted({k.rsplit("_", 1)[0] for k in z.files if k.endswith("_spec")})
+    assert len(names) == 5
+    for name in names:
+        M, N, b, n, m = (int(x) for x in z[f"{name}_spec"])
+        eps = float(z[f"{name}_eps"][0])
+        frame = oracle.synth_frames(3, 1, M, N, 3)[0]
+        mask = oracle.synth_masks(3, 1, M, N)[0]
+        assert hashlib.sha256(frame.tobytes()).digest() == z[f"{name}_inputsha"].tobytes()
+        assert hashlib.sha256(mask.tobytes()).digest() == z[f"{name}_masksha"].tobytes()
+        p = oracle.make_privacy_params(eps, m, b, n)
+        seeds = [oracle.derive_plane_seed(42, 3, ch) for ch in range(3)]
+        if f"{name}_ch0_payload" in z.files:
+            pls, img = oracle.pixelize_adaptive(frame, mask, b, n, p.sigma, p.sigma_sub, "keyed",
+                                                seeds)
+            for ch in range(3):
+                assert pls[ch] == z[f"{name}_ch{ch}_payload"].tobytes(), (name, ch)
+        else:
+            means, img = oracle.pixelize_uniform(frame, b, p.sigma, "keyed", seeds)
+            for ch in range(3):
+                assert np.array_equal(means[ch], z[f"{name}_ch{ch}_means"]), (name, ch)
+        for ch in range(3):
+            plane = np.ascontiguousarray(img[:, :, ch])
+            assert hashlib.sha256(plane.tobytes()).digest() == z[f"{name}_ch{ch}_imgsha"].tobytes()
+
+
+def test_record_payloads():
+    z = np.load(os.path.join(G, "records.npz"))
+    img = np.ascontiguousarray(oracle.synth_frames(0, 1, 576, 768, 1)[0, :, :, 0])
+    rec = z["pets_uniform_b16"].tobytes()
+    assert rec[:4] == b"DPPX" and len(rec) == 1752  # record size law (acceptance 5)
+    p = oracle.make_privacy_params(0.5, 16, 16)
+    means, _ = oracle.pixelize_uniform(img, 16, p.sigma, "keyed", [11])
+    assert rec[20:-4] == means[0].tobytes()
+    rec = z["pets_adaptive_b16n4"].tobytes()
+    mask = oracle.synth_masks(0, 1, 576, 768)[0]
+    p = oracle.make_privacy_params(0.5, 16, 16, 4)
+    pl, _ = oracle.pixelize_adaptive(img, mask, 16, 4, p.sigma, p.sigma_sub, "keyed", [11])
+    assert rec[20:-4] == pl[0]

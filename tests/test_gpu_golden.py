@@ -1,0 +1,51 @@
+"""The GPU path reproduces the fixtures generated from the reference itself
+(tests/golden/, see make_golden.py): small random cases through the
+reference-shaped API, BASELINE shapes as RGB batches with derived plane seeds."""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2511_04261_b200 as dp
+
+pytestmark = pytest.mark.gpu
+G = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def test_small_cases_through_dropin_api(ctx):
+    z = np.load(os.path.join(G, "small_cases.npz"))
+    for k in sorted({k.split("_")[0] for k in z.files}):
+        M, N, b, n, m, has = (int(x) for x in z[f"{k}_params"])
+        eps = float(z[f"{k}_eps"][0])
+        seed = None if has < 0 else int(z[f"{k}_seed"][0])
+        u = dp.pixelize_parallel(z[f"{k}_img"], dp.make_privacy_params(eps, m, b), seed)
+        assert np.array_equal(u.means.values, z[f"{k}_umeans"]) and np.array_equal(u.image, z[f"{k}_uimg"]), k
+        a = dp.pixelize_adaptive(z[f"{k}_img"], z[f"{k}_mask"], dp.make_privacy_params(eps, m, b, n), seed)
+        assert a.means.payload() == z[f"{k}_payload"].tobytes() and np.array_equal(a.image, z[f"{k}_aimg"]), k
+        assert np.array_equal(dp.reassemble(a.means, M, N), a.image)
+        assert np.array_equal(dp.broadcast_means(u.means, M, N), u.image)
+
+
+def test_shaped_cases_rgb(ctx):
+    z = np.load(os.path.join(G, "shaped_cases.npz"))
+    for name in sorted({k.rsplit("_", 1)[0] for k in z.files if k.endswith("_spec")}):
+        M, N, b, n, m = (int(x) for x in z[f"{name}_spec"])
+        eps = float(z[f"{name}_eps"][0])
+        frames = oracle.synth_frames(3, 1, M, N, 3)
+        masks = oracle.synth_masks(3, 1, M, N)
+        seeds = dp.plane_seeds(42, 1, 3, frame0=3)
+        if f"{name}_ch0_payload" in z.files:
+            pls, img = ctx.pixelize_adaptive(frames, masks, dp.make_privacy_params(eps, m, b, n),
+                                             dp.NOISE_KEYED, seeds)
+            for ch in range(3):
+                assert pls[ch] == z[f"{name}_ch{ch}_payload"].tobytes(), (name, ch)
+        else:
+            means, img = ctx.pixelize_uniform(frames, dp.make_privacy_params(eps, m, b),
+                                              dp.NOISE_KEYED, seeds)
+            for ch in range(3):
+                assert np.array_equal(means[ch], z[f"{name}_ch{ch}_means"]), (name, ch)
+        for ch in range(3):
+            plane = np.ascontiguousarray(img[0, :, :, ch])
+            assert hashlib.sha256(plane.tobytes()).digest() == z[f"{name}_ch{ch}_imgsha"].tobytes()

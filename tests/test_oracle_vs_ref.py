@@ -1,0 +1,57 @@
+"""Live: the C restatement vs the reference compiled from /root/reference
+(oracle/_ref). Skipped where the reference library was not built."""
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.skipif(oracle.ref is None, reason="oracle/_ref not built")
+
+
+def test_random_geometries_bit_exact():
+    rng = np.random.default_rng(99)
+    done = 0
+    while done < 150:
+        M, N = int(rng.integers(1, 70)), int(rng.integers(1, 70))
+        b = int(rng.integers(1, min(max(M, N), 16) + 1))
+        n = int(rng.choice([d for d in range(1, b + 1) if b % d == 0]))
+        g = oracle.grid_dims(M, N, b)
+        img = rng.integers(0, 256, (M, N), dtype=np.uint8)
+        mask = rng.integers(0, 2, (M, N), dtype=np.uint8)
+        eps, m = float(rng.choice([0.1, 0.5, 2.0])), int(rng.integers(1, 40))
+        seed = int(rng.integers(0, 2**63))
+        if (g.pad_rows or g.pad_cols) and (g.pad_rows >= M or g.pad_cols >= N):
+            with pytest.raises(ValueError):
+                oracle.ref.pixelize_parallel(img, eps, m, b, seed)
+            with pytest.raises(oracle.OracleError):
+                oracle.pixelize_uniform(img, b, 1.0)
+            continue
+        p = oracle.make_privacy_params(eps, m, b, n)
+        rp = oracle.ref.make_privacy_params(eps, m, b, n)
+        assert (p.sigma, p.sigma_sub, p.delta) == (rp["sigma"], rp["sigma_sub"], rp["delta"])
+        ri, rm = oracle.ref.pixelize_parallel(img, eps, m, b, seed)
+        om, oi = oracle.pixelize_uniform(img, b, oracle.make_privacy_params(eps, m, b).sigma,
+                                         "keyed", [seed])
+        assert np.array_equal(rm, om[0]) and np.array_equal(ri, oi)
+        ra, rpl = oracle.ref.pixelize_adaptive(img, mask, eps, m, b, n, seed)
+        opl, oa = oracle.pixelize_adaptive(img, mask, b, n, p.sigma, p.sigma_sub, "keyed", [seed])
+        assert rpl == opl[0] and np.array_equal(ra, oa)
+        assert np.array_equal(oracle.ref.reconstruct_adaptive(rpl, M, N, b, n), ra)
+        assert np.array_equal(oracle.ref.pixelize_reference(img, eps, m, b, seed),
+                              oracle.pixelize_reference(img, b, oracle.make_privacy_params(
+                                  eps, m, b).sigma, seed))
+        done += 1
+
+
+def test_reference_release_gate_runs():
+    """The reference's own acceptance gate (tests/acceptance_main.cpp) built
+    from its sources: every criterion but the host-dependent speedup floor (8)
+    must pass."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(oracle.__file__), "_ref", "dppix_acceptance")
+    if not os.path.exists(exe):
+        pytest.skip("dppix_acceptance not built")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600).stdout
+    fails = [ln for ln in out.splitlines() if " FAIL " in ln and "[ 8]" not in ln]
+    assert not fails, out
