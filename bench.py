@@ -219,6 +219,7 @@ def main():
     import torch
 
     import paper_2511_04261_b200 as dp
+    from paper_2511_04261_b200 import shard as sh
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -247,7 +248,8 @@ def main():
     pitch = ((N * C + 15) // 16) * 16
     mpitch = ((N + 15) // 16) * 16
     d = dp._desc(M, N, C, F, pitch=pitch, mpitch=mpitch, opitch=pitch)
-    frame0 = rank * F
+    my = sh.weak_shard(rank, world, F)  # global frame indices key the noise
+    frame0 = my.frame0
     img = torch.empty((F, M, pitch), dtype=torch.uint8, device=dev)
     out = torch.empty_like(img)
     mask = torch.empty((F, M, mpitch), dtype=torch.uint8, device=dev) if adaptive else None
@@ -259,7 +261,7 @@ def main():
         sstride = G
     stats = torch.zeros((F * C, sstride), dtype=torch.uint8, device=dev)
     lens = torch.zeros(F * C, dtype=torch.int32, device=dev)
-    seeds = dp.plane_seeds(42, F, C, frame0=frame0)
+    seeds = sh.plane_seed_list(42, my, C)
     nz, keep = dp.Context._noise(dp.NOISE_KEYED, seeds)
 
     def step():
