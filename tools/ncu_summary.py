@@ -63,9 +63,9 @@ def full(rep):
             print()
 
 
-def traffic(rep, workload):
+def traffic(rep, workload, pattern="k_stats"):
     kernels, units = raw(rep)
-    k = kernels[0]
+    k = next(x for x in kernels if pattern in x.get("Kernel Name", ""))
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     rd = num(k["dram__bytes_read.sum"]) * scale.get(units["dram__bytes_read.sum"], 1)
     wr = num(k["dram__bytes_write.sum"]) * scale.get(units["dram__bytes_write.sum"], 1)
@@ -74,7 +74,7 @@ def traffic(rep, workload):
     data = {}
     if os.path.exists(path):
         data = json.load(open(path))
-    data[workload] = int(rd + wr)
+    data[workload] = int(rd + wr)  # K1 DRAM read + write bytes per launch
     json.dump(data, open(path, "w"), indent=1, sort_keys=True)
     print(json.dumps(data))
 
