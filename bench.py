@@ -56,7 +56,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="venice")
     ap.add_argument("--frames", type=int, default=0, help="override frames per GPU")
-    ap.add_argument("--e2e-frames", type=int, default=120)
+    ap.add_argument("--e2e-frames", type=int, default=0,
+                    help="frames per e2e step (default: ~1 GB of input, <= frames per GPU)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU-work seconds for the reference sample")
@@ -80,6 +81,7 @@ class ClockSampler:
         self.device = device
         self.samples = []  # (sm_mhz, max_mhz, reasons_bitmask)
         self._stop = threading.Event()
+        self._ready = threading.Event()
         self._t = None
 
     def _run(self):
@@ -88,12 +90,14 @@ class ClockSampler:
             nv.nvmlInit()
             h = nv.nvmlDeviceGetHandleByIndex(self.device)
             mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            self._ready.set()
             while not self._stop.is_set():
                 self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), mx,
                                      nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
                 self._stop.wait(0.002)
             nv.nvmlShutdown()
         except Exception:
+            self._ready.set()
             while not self._stop.is_set():
                 try:
                     out = subprocess.run(
@@ -109,7 +113,8 @@ class ClockSampler:
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
-        time.sleep(0.05)
+        self._ready.wait(30)
+        time.sleep(0.01)  # at least a few samples before the region starts
         return self
 
     def __exit__(self, *a):
@@ -323,7 +328,7 @@ def main():
     # ---- e2e: public host API, pinned host buffers ----
     e2e = None
     if not args.no_e2e:
-        Fe = min(F, args.e2e_frames)
+        Fe = min(F, args.e2e_frames or max(1, (1 << 30) // (M * N * (C + (1 if adaptive else 0)))))
         hbytes = Fe * M * N * C
         h_img = torch.empty((Fe, M, N, C), dtype=torch.uint8).pin_memory()
         h_img.copy_(img[:Fe, :, : N * C].reshape(Fe, M, N, C).cpu())
@@ -351,6 +356,23 @@ def main():
                                                    h_out.data_ptr())
             ctx._check(rc, "e2e")
 
+        # link roofline: pinned copies of the same byte counts, each direction alone
+        def link_gbs(nbytes, h2d):
+            hb = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+            db = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+            for _ in range(2):
+                (db.copy_(hb, non_blocking=True) if h2d else hb.copy_(db, non_blocking=True))
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(3):
+                (db.copy_(hb, non_blocking=True) if h2d else hb.copy_(db, non_blocking=True))
+            e1.record()
+            e1.synchronize()
+            return 3 * nbytes / (e0.elapsed_time(e1) / 1e3) / 1e9
+
+        h2d_link = link_gbs(1 << 30, True)
+        d2h_link = link_gbs(1 << 30, False)
         for _ in range(2):
             e2e_step()
         ctx.reset_stats()
@@ -367,6 +389,10 @@ def main():
                "d2h_bytes_per_step": es["d2h_bytes"] // args.e2e_steps,
                "frames_per_step": Fe, "ms_per_step": round(e_ms, 3),
                "frames_per_sec": round(Fe * world / (e_ms / 1e3), 3),
+               "link_gbs": {"h2d": round(h2d_link, 1), "d2h": round(d2h_link, 1)},
+               "link_frac": round(max(es["h2d_bytes"] / args.e2e_steps / (h2d_link * 1e9),
+                                      es["d2h_bytes"] / args.e2e_steps / (d2h_link * 1e9))
+                                  / (e_ms / 1e3), 4),
                "path": "dppx_pixelize_adaptive (host pointers, pinned, chunked H2D/K0/K1/D2H "
                        "pipeline on 3 streams)" if adaptive else "dppx_pixelize_uniform"}
         del h_img, h_mask, h_out, h_stats

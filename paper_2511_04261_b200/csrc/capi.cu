@@ -506,6 +506,26 @@ int read_status(dppx_ctx* ctx) {
 }
 
 // ---- host pipeline -----------------------------------------------------------
+// Copy Fk frames of M rows x width bytes between pitched layouts with as few
+// copy operations as the strides allow (one linear copy when both sides are
+// dense, one 2-D copy when frames are row-contiguous, else one per frame).
+cudaError_t copy_frames(void* dst, int64_t dpitch, int64_t dfs, const void* src, int64_t spitch,
+                        int64_t sfs, int64_t width, int M, int Fk, cudaMemcpyKind kind,
+                        cudaStream_t st) {
+  auto* d = static_cast<uint8_t*>(dst);
+  const auto* s = static_cast<const uint8_t*>(src);
+  if (dpitch == width && spitch == width && dfs == width * M && sfs == width * M)
+    return cudaMemcpyAsync(d, s, static_cast<size_t>(width) * M * Fk, kind, st);
+  if (dfs == dpitch * M && sfs == spitch * M)
+    return cudaMemcpy2DAsync(d, dpitch, s, spitch, width, static_cast<size_t>(M) * Fk, kind, st);
+  for (int f = 0; f < Fk; ++f) {
+    const cudaError_t e =
+        cudaMemcpy2DAsync(d + f * dfs, dpitch, s + f * sfs, spitch, width, M, kind, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 enum class HostOp { Uniform, Adaptive, Broadcast, Reassemble };
 
 int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uint8_t* img,
@@ -556,8 +576,10 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
   const int64_t dfs = dpitch * M, dmfs = dmpitch * M;
   const int64_t per_frame = (pix ? dfs : 0) + (op == HostOp::Adaptive ? dmfs : 0) +
                             (out ? dfs : 0) + dstride * C;
+  // ~16 chunks per call keeps pipeline fill + drain small; 8..96 MB per chunk.
+  const int64_t target = std::min<int64_t>(96ll << 20, std::max<int64_t>(8ll << 20, per_frame * F / 16));
   int K = ctx->chunk_frames > 0 ? ctx->chunk_frames
-                                : static_cast<int>(std::max<int64_t>(1, (96ll << 20) / per_frame));
+                                : static_cast<int>(std::max<int64_t>(1, target / per_frame));
   K = std::max(1, std::min(K, F));
   const int chunks = (F + K - 1) / K;
   const bool inj = pix && nz && nz->kind == DPPX_NOISE_INJECTED;
@@ -583,22 +605,15 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
     uint8_t* dstats = static_cast<uint8_t*>(ctx->stats[s].p);
     uint32_t* dlens = static_cast<uint32_t*>(ctx->lens[s].p);
     if (pix) {
-      CUDA_TRY(ctx, cudaMemcpy2DAsync(dimg, dpitch, img + static_cast<int64_t>(f0) * d->frame_stride,
-                                      d->pitch, static_cast<size_t>(N) * C, M, cudaMemcpyHostToDevice,
-                                      ctx->s_in));
-      // frames beyond the first of the chunk (frame strides may differ)
-      for (int f = 1; f < Fk; ++f)
-        CUDA_TRY(ctx, cudaMemcpy2DAsync(dimg + f * dfs, dpitch,
-                                        img + static_cast<int64_t>(f0 + f) * d->frame_stride, d->pitch,
-                                        static_cast<size_t>(N) * C, M, cudaMemcpyHostToDevice,
-                                        ctx->s_in));
+      CUDA_TRY(ctx, copy_frames(dimg, dpitch, dfs, img + static_cast<int64_t>(f0) * d->frame_stride,
+                                d->pitch, d->frame_stride, static_cast<int64_t>(N) * C, M, Fk,
+                                cudaMemcpyHostToDevice, ctx->s_in));
       ctx->kstats.h2d_bytes += static_cast<uint64_t>(Fk) * M * N * C;
     }
     if (op == HostOp::Adaptive) {
-      for (int f = 0; f < Fk; ++f)
-        CUDA_TRY(ctx, cudaMemcpy2DAsync(dmask + f * dmfs, dmpitch,
-                                        mask + static_cast<int64_t>(f0 + f) * d->mask_frame_stride,
-                                        d->mask_pitch, N, M, cudaMemcpyHostToDevice, ctx->s_in));
+      CUDA_TRY(ctx, copy_frames(dmask, dmpitch, dmfs,
+                                mask + static_cast<int64_t>(f0) * d->mask_frame_stride, d->mask_pitch,
+                                d->mask_frame_stride, N, M, Fk, cudaMemcpyHostToDevice, ctx->s_in));
       ctx->kstats.h2d_bytes += static_cast<uint64_t>(Fk) * M * N;
     }
     if (!pix) {
@@ -660,11 +675,9 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
       }
     }
     if (out) {
-      for (int f = 0; f < Fk; ++f)
-        CUDA_TRY(ctx, cudaMemcpy2DAsync(out + static_cast<int64_t>(f0 + f) * d->out_frame_stride,
-                                        d->out_pitch, dout + f * dfs, dpitch,
-                                        static_cast<size_t>(N) * C, M, cudaMemcpyDeviceToHost,
-                                        ctx->s_out));
+      CUDA_TRY(ctx, copy_frames(out + static_cast<int64_t>(f0) * d->out_frame_stride, d->out_pitch,
+                                d->out_frame_stride, dout, dpitch, dfs, static_cast<int64_t>(N) * C,
+                                M, Fk, cudaMemcpyDeviceToHost, ctx->s_out));
       ctx->kstats.d2h_bytes += static_cast<uint64_t>(Fk) * M * N * C;
     }
     CUDA_TRY(ctx, cudaEventRecord(ctx->out_done[s], ctx->s_out));

@@ -483,33 +483,63 @@ __global__ void __launch_bounds__(kStatsThreads)
   const BatchGeom& g = a.g;
   const DrawEnv env_cell = make_env(a.noise.kind, a.exact_noise != 0, a.area, a.sigma);
   const DrawEnv env_sub = make_env(a.noise.kind, a.exact_noise != 0, a.sub_area, a.sigma_sub);
+  // Per-unit metadata (K0's cell info, row prefix, simple total, plane seeds)
+  // is loaded one unit ahead so its L2 latency hides behind a unit of work.
+  struct Meta {
+    int u;
+    uint32_t info, rowpre, stot;
+    uint64_t seed[C];
+  };
+  auto load_meta = [&](int k_next) {
+    Meta m;
+    const int sn = k_next % S;
+    mbar_wait(&id_bar[sn], (k_next / S) & 1);
+    m.u = *reinterpret_cast<volatile int*>(&stage_unit[sn]);
+    m.info = 1u;
+    m.rowpre = m.stot = 0;
+#pragma unroll
+    for (int ch = 0; ch < C; ++ch) m.seed[ch] = 0;
+    if (m.u >= 0) {
+      const UnitPos q = decode_unit(a, m.u);
+      const int qcell = q.px0 / B + t / B4;
+      if (ADAPTIVE && qcell < g.GC) {
+        m.info = __ldg(&a.cellinfo[static_cast<int64_t>(q.f) * g.G + q.r * g.GC + qcell]);
+        m.rowpre = __ldg(&a.rowprefix[static_cast<int64_t>(q.f) * g.GR + q.r]);
+        m.stot = __ldg(&a.totals[q.f]);
+      }
+      if (a.noise.kind == DPPX_NOISE_KEYED) {
+#pragma unroll
+        for (int ch = 0; ch < C; ++ch)
+          m.seed[ch] = __ldg(&a.noise.mixed_seeds[static_cast<int64_t>(q.f) * C + ch]);
+      }
+    }
+    return m;
+  };
+  Meta next = load_meta(0);
   for (int k = 0;; ++k) {
     const int s = k % S;
     uint8_t* st = smem + s * STAGE;
-    mbar_wait(&id_bar[s], (k / S) & 1);
-    const int u = *reinterpret_cast<volatile int*>(&stage_unit[s]);
+    const Meta cur = next;
+    const int u = cur.u;
     if (u < 0) break;
+    next = load_meta(k + 1);  // the producer publishes ids S-1 units ahead
     const UnitPos p = decode_unit(a, u);
     const int cell = p.px0 / B + t / B4;
     const int lic = t % B4;        // lane within cell
     const int sc = lic / SB4;      // subcell column
     const bool active = cell < g.GC;
     const int gidx = p.r * g.GC + cell;
-    bool simple = true;
-    uint32_t slot_s = 0, S_tot = 0;
-    if (ADAPTIVE && active) {
-      const uint32_t info = __ldg(&a.cellinfo[static_cast<int64_t>(p.f) * g.G + gidx]);
-      simple = info & 1u;
-      slot_s = __ldg(&a.rowprefix[static_cast<int64_t>(p.f) * g.GR + p.r]) + (info >> 1);
-      S_tot = __ldg(&a.totals[p.f]);
-    }
+    const bool simple = !ADAPTIVE || (cur.info & 1u);
+    const uint32_t slot_s = cur.rowpre + (cur.info >> 1);
+    const uint32_t S_tot = cur.stot;
     const int vbytes = valid_bytes<C>(a, p.px0);
     const int copy = staged_bytes<C, B>(a, p);  // bytes per row the producer staged
     const int scopy = max(0, min(kTilePx * C, a.tensor_out_bytes - p.px0 * C));  // stored by TMA
     const int need = min(kTilePx, g.GC * B - p.px0) * C;
     uint64_t cs[C];
 #pragma unroll
-    for (int ch = 0; ch < C; ++ch) cs[ch] = cell_state(a, p.f, ch, p.r, cell);
+    for (int ch = 0; ch < C; ++ch)
+      cs[ch] = a.noise.kind == DPPX_NOISE_KEYED ? key_cell(cur.seed[ch], p.r, cell) : 0ull;
 
     mbar_wait(&full_bar[s], (k / S) & 1);
 
