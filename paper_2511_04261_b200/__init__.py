@@ -29,7 +29,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libdppx_gpu.so")
+LIB_PATH = os.environ.get("DPPX_LIB") or os.path.join(_HERE, "lib", "libdppx_gpu.so")  # A/B override
 DROPIN_PATH = os.path.join(_HERE, "lib", "libdppix_gpu.so")
 
 if not os.path.exists(LIB_PATH):

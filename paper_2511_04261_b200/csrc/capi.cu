@@ -22,7 +22,7 @@
 
 namespace dppx {
 using StatsKernel = void (*)(const CUtensorMap, const CUtensorMap, const StatsArgs);
-StatsKernel select_stats_kernel(int C, int b, int n, bool adaptive);
+StatsKernel select_stats_kernel(int C, int b, int n, bool adaptive, bool packed);
 int stats_threads();
 int stats_tile_px();
 int stats_max_stages();
@@ -35,6 +35,8 @@ cudaError_t launch_synth(const BatchGeom& g, uint32_t seed, uint32_t f0, uint8_t
                          int64_t pitch, int64_t fstride, uint8_t* mask, int64_t mpitch,
                          int64_t mfstride, cudaStream_t s);
 cudaError_t launch_debug_lg2(unsigned int* out, cudaStream_t s);
+cudaError_t launch_repitch(uint8_t* dst, int64_t dpitch, const uint8_t* src, int64_t spitch,
+                           int64_t width, int64_t rows, cudaStream_t s);
 cudaError_t launch_debug_laplace(uint64_t mixed, const uint32_t* keys, int count, double sigma,
                                  double* out, cudaStream_t s);
 }  // namespace dppx
@@ -86,7 +88,7 @@ struct dppx_ctx {
   size_t seeds_pinned_n = 0;
   cudaEvent_t seeds_ev = nullptr;
   // host-pipeline staging (2 slots)
-  DevBuf img[2], mask[2], out[2], stats[2], lens[2], inj[2], sd[2];
+  DevBuf img[2], mask[2], out[2], stats[2], lens[2], inj[2], sd[2], dense[2], dense_mask[2];
   uint64_t* sd_pinned[2] = {nullptr, nullptr};
   size_t sd_pinned_n[2] = {0, 0};
   cudaEvent_t in_done[2] = {}, comp_done[2] = {}, out_done[2] = {};
@@ -337,23 +339,46 @@ int classify(dppx_ctx* ctx, const BatchGeom& g, int planes, bool from_payload, c
 // K1 (fast, TMA-staged) when the geometry and alignment allow, else K1g.
 int run_stats(dppx_ctx* ctx, StatsArgs& a) {
   const BatchGeom& g = a.g;
-  StatsKernel k = select_stats_kernel(g.C, g.b, g.n, a.adaptive != 0);
+  StatsKernel k = nullptr;
   const bool aligned = aligned16(a.img) && a.pitch % 16 == 0 && a.fstride % 16 == 0 &&
                        (!a.out || (aligned16(a.out) && a.opitch % 16 == 0 && a.ofstride % 16 == 0));
   PendingTiming pt;
   CUtensorMap tin{}, tout{};
   const int tile = stats_tile_px();
   const int64_t row_bytes = static_cast<int64_t>(g.N) * g.C;
-  bool maps = k && aligned && g.F > 0 && tile * g.C / 8 <= 256 && g.b <= 256 &&
-              encode_frames_map(&tin, a.img, row_bytes, g.M, g.F, a.pitch, a.fstride, tile * g.C, g.b);
+  // Narrow frames: pack several padded frame rows side by side in one tile.
+  const int padded_px = g.GC * g.b;
+  const int64_t stage_bytes = static_cast<int64_t>(g.b) * tile * g.C;
+  a.pack = 1;
+  a.slot_px = tile;
+  if (2 * padded_px <= tile && (padded_px * g.C) % 16 == 0) {
+    const int64_t stride = round_up(static_cast<int64_t>(g.b) * padded_px * g.C, 128);
+    const int pk = static_cast<int>(std::min<int64_t>(tile / padded_px, stage_bytes / stride));
+    if (pk >= 2) {
+      a.pack = pk;
+      a.slot_px = padded_px;
+    }
+  }
+  a.slot_stride = static_cast<int>(round_up(static_cast<int64_t>(g.b) * a.slot_px * g.C, 128));
+  k = select_stats_kernel(g.C, g.b, g.n, a.adaptive != 0, a.pack > 1);
+  a.row_slack = a.pitch >= round_up(row_bytes, 16) ? 1 : 0;
+  const int box_bytes = a.slot_px * g.C;
+  // Input rows: the tensor's inner extent is rounded UP to 8 bytes when the
+  // pitch has slack (the stray bytes past N*C are overwritten by the mirror
+  // fill), so no row tail has to be gathered from global memory.
+  const int64_t in_row = a.row_slack ? round_up(row_bytes, 8) : row_bytes / 8 * 8;
+  bool maps = k && aligned && g.F > 0 && box_bytes / 8 <= 256 && g.b <= 256 &&
+              static_cast<int64_t>(a.pack) * a.slot_stride <= stage_bytes &&
+              encode_frames_map(&tin, a.img, in_row, g.M, g.F, a.pitch, a.fstride, box_bytes, g.b);
   if (maps && a.out)
-    maps = encode_frames_map(&tout, a.out, row_bytes, g.M, g.F, a.opitch, a.ofstride, tile * g.C, g.b);
+    maps = encode_frames_map(&tout, a.out, row_bytes, g.M, g.F, a.opitch, a.ofstride, box_bytes, g.b);
   if (maps && !a.out) tout = tin;
   if (maps) {
-    a.tensor_in_bytes = static_cast<int>(row_bytes / 8 * 8);
-    a.tensor_out_bytes = a.tensor_in_bytes;
-    a.tiles_per_row = (g.GC * g.b + tile - 1) / tile;
-    const int64_t units = static_cast<int64_t>(g.F) * g.GR * a.tiles_per_row;
+    a.tensor_in_bytes = static_cast<int>(in_row);
+    a.tensor_out_bytes = static_cast<int>(row_bytes / 8 * 8);
+    a.tiles_per_row = a.pack > 1 ? 1 : (padded_px + tile - 1) / tile;
+    const int64_t groups = (g.F + a.pack - 1) / a.pack;
+    const int64_t units = groups * g.GR * a.tiles_per_row;
     if (units > 0x7FFFFFFF) return set_err(ctx, DPPX_ERR_INVALID, "batch too large for one launch");
     a.units = static_cast<int>(units);
     a.div_tiles = make_fastdiv(static_cast<uint32_t>(a.tiles_per_row));
@@ -581,9 +606,32 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
   int K = ctx->chunk_frames > 0 ? ctx->chunk_frames
                                 : static_cast<int>(std::max<int64_t>(1, target / per_frame));
   K = std::max(1, std::min(K, F));
-  const int chunks = (F + K - 1) / K;
+  // Chunk schedule: 1, 2, 4, ... ramp up, K-frame chunks, mirrored ramp down, so
+  // the first H2D and the last D2H (the unoverlapped fill and drain) are small.
+  std::vector<int> sizes;
+  {
+    std::vector<int> up;
+    int sum_up = 0;
+    for (int c = 1; c < K && 2 * (sum_up + c) < F; c *= 2) {
+      up.push_back(c);
+      sum_up += c;
+    }
+    const int rem = F - 2 * sum_up;
+    const int mid = (rem + K - 1) / K;
+    sizes = up;
+    for (int i = 0; i < mid; ++i) sizes.push_back(rem / mid + (i < rem % mid ? 1 : 0));
+    sizes.insert(sizes.end(), up.rbegin(), up.rend());
+  }
+  const int chunks = static_cast<int>(sizes.size());
   const bool inj = pix && nz && nz->kind == DPPX_NOISE_INJECTED;
   const size_t inj_plane = G * static_cast<size_t>(adaptive ? n * n : 1);
+  const int64_t row = static_cast<int64_t>(N) * C;
+  // Dense linear PCIe transfers + on-device re-pitch when the kernels' 16-byte
+  // pitch differs from a dense host layout (e.g. 178 x 3 = 534-byte rows).
+  const bool dense_in = pix && dpitch != row && d->pitch == row && d->frame_stride == row * M;
+  const bool dense_mask = op == HostOp::Adaptive && dmpitch != N && d->mask_pitch == N &&
+                          d->mask_frame_stride == static_cast<int64_t>(N) * M;
+  const bool dense_out = out && dpitch != row && d->out_pitch == row && d->out_frame_stride == row * M;
   for (int s = 0; s < 2 && s < chunks; ++s) {
     if (pix && ensure(ctx, ctx->img[s], static_cast<size_t>(dfs) * K)) return DPPX_ERR_OOM;
     if (op == HostOp::Adaptive && ensure(ctx, ctx->mask[s], static_cast<size_t>(dmfs) * K))
@@ -592,11 +640,16 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
     if (ensure(ctx, ctx->stats[s], static_cast<size_t>(dstride) * C * K)) return DPPX_ERR_OOM;
     if (ensure(ctx, ctx->lens[s], sizeof(uint32_t) * C * K)) return DPPX_ERR_OOM;
     if (inj && ensure(ctx, ctx->inj[s], sizeof(double) * inj_plane * C * K)) return DPPX_ERR_OOM;
+    if ((dense_in || dense_out) && ensure(ctx, ctx->dense[s], static_cast<size_t>(row) * M * K))
+      return DPPX_ERR_OOM;
+    if (dense_mask && ensure(ctx, ctx->dense_mask[s], static_cast<size_t>(N) * M * K))
+      return DPPX_ERR_OOM;
   }
   cudaStream_t comp = ctx->stream;
+  int f0 = 0;
   for (int ci = 0; ci < chunks; ++ci) {
     const int s = ci & 1;
-    const int f0 = ci * K, Fk = std::min(K, F - f0);
+    const int Fk = sizes[ci];
     // ---- H2D (input stream): wait until chunk ci-2 released this slot ----
     if (ci >= 2) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->s_in, ctx->comp_done[s], 0));
     uint8_t* dimg = static_cast<uint8_t*>(ctx->img[s].p);
@@ -604,16 +657,29 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
     uint8_t* dout = static_cast<uint8_t*>(ctx->out[s].p);
     uint8_t* dstats = static_cast<uint8_t*>(ctx->stats[s].p);
     uint32_t* dlens = static_cast<uint32_t*>(ctx->lens[s].p);
+    uint8_t* ddense = static_cast<uint8_t*>(ctx->dense[s].p);
+    uint8_t* ddmask = static_cast<uint8_t*>(ctx->dense_mask[s].p);
     if (pix) {
-      CUDA_TRY(ctx, copy_frames(dimg, dpitch, dfs, img + static_cast<int64_t>(f0) * d->frame_stride,
-                                d->pitch, d->frame_stride, static_cast<int64_t>(N) * C, M, Fk,
-                                cudaMemcpyHostToDevice, ctx->s_in));
-      ctx->kstats.h2d_bytes += static_cast<uint64_t>(Fk) * M * N * C;
+      if (dense_in)
+        CUDA_TRY(ctx, cudaMemcpyAsync(ddense, img + static_cast<int64_t>(f0) * d->frame_stride,
+                                      static_cast<size_t>(row) * M * Fk, cudaMemcpyHostToDevice,
+                                      ctx->s_in));
+      else
+        CUDA_TRY(ctx, copy_frames(dimg, dpitch, dfs, img + static_cast<int64_t>(f0) * d->frame_stride,
+                                  d->pitch, d->frame_stride, row, M, Fk, cudaMemcpyHostToDevice,
+                                  ctx->s_in));
+      ctx->kstats.h2d_bytes += static_cast<uint64_t>(Fk) * M * row;
     }
     if (op == HostOp::Adaptive) {
-      CUDA_TRY(ctx, copy_frames(dmask, dmpitch, dmfs,
-                                mask + static_cast<int64_t>(f0) * d->mask_frame_stride, d->mask_pitch,
-                                d->mask_frame_stride, N, M, Fk, cudaMemcpyHostToDevice, ctx->s_in));
+      if (dense_mask)
+        CUDA_TRY(ctx, cudaMemcpyAsync(ddmask, mask + static_cast<int64_t>(f0) * d->mask_frame_stride,
+                                      static_cast<size_t>(N) * M * Fk, cudaMemcpyHostToDevice,
+                                      ctx->s_in));
+      else
+        CUDA_TRY(ctx, copy_frames(dmask, dmpitch, dmfs,
+                                  mask + static_cast<int64_t>(f0) * d->mask_frame_stride,
+                                  d->mask_pitch, d->mask_frame_stride, N, M, Fk,
+                                  cudaMemcpyHostToDevice, ctx->s_in));
       ctx->kstats.h2d_bytes += static_cast<uint64_t>(Fk) * M * N;
     }
     if (!pix) {
@@ -635,6 +701,18 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
     // ---- compute ----
     CUDA_TRY(ctx, cudaStreamWaitEvent(comp, ctx->in_done[s], 0));
     if (ci >= 2) CUDA_TRY(ctx, cudaStreamWaitEvent(comp, ctx->out_done[s], 0));
+    if (dense_in) {
+      PendingTiming pt;
+      timing_begin(ctx, DPPX_K_AUX, &pt);
+      CUDA_TRY(ctx, launch_repitch(dimg, dpitch, ddense, row, row, static_cast<int64_t>(M) * Fk, comp));
+      timing_end(ctx, &pt);
+    }
+    if (dense_mask) {
+      PendingTiming pt;
+      timing_begin(ctx, DPPX_K_AUX, &pt);
+      CUDA_TRY(ctx, launch_repitch(dmask, dmpitch, ddmask, N, N, static_cast<int64_t>(M) * Fk, comp));
+      timing_end(ctx, &pt);
+    }
     dppx_frames_desc dd = *d;
     dd.frames = Fk;
     dd.pitch = dpitch;
@@ -659,6 +737,12 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
       rc = expand_dev(ctx, &dd, dstats, dstride, in_lens ? dlens : nullptr, b, n, dout, adaptive);
     }
     if (rc) return rc;
+    if (dense_out) {
+      PendingTiming pt;
+      timing_begin(ctx, DPPX_K_AUX, &pt);
+      CUDA_TRY(ctx, launch_repitch(ddense, row, dout, dpitch, row, static_cast<int64_t>(M) * Fk, comp));
+      timing_end(ctx, &pt);
+    }
     CUDA_TRY(ctx, cudaEventRecord(ctx->comp_done[s], comp));
     // ---- D2H (output stream) ----
     CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->s_out, ctx->comp_done[s], 0));
@@ -675,12 +759,18 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
       }
     }
     if (out) {
-      CUDA_TRY(ctx, copy_frames(out + static_cast<int64_t>(f0) * d->out_frame_stride, d->out_pitch,
-                                d->out_frame_stride, dout, dpitch, dfs, static_cast<int64_t>(N) * C,
-                                M, Fk, cudaMemcpyDeviceToHost, ctx->s_out));
-      ctx->kstats.d2h_bytes += static_cast<uint64_t>(Fk) * M * N * C;
+      if (dense_out)
+        CUDA_TRY(ctx, cudaMemcpyAsync(out + static_cast<int64_t>(f0) * d->out_frame_stride, ddense,
+                                      static_cast<size_t>(row) * M * Fk, cudaMemcpyDeviceToHost,
+                                      ctx->s_out));
+      else
+        CUDA_TRY(ctx, copy_frames(out + static_cast<int64_t>(f0) * d->out_frame_stride, d->out_pitch,
+                                  d->out_frame_stride, dout, dpitch, dfs, row, M, Fk,
+                                  cudaMemcpyDeviceToHost, ctx->s_out));
+      ctx->kstats.d2h_bytes += static_cast<uint64_t>(Fk) * M * row;
     }
     CUDA_TRY(ctx, cudaEventRecord(ctx->out_done[s], ctx->s_out));
+    f0 += Fk;
   }
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->s_out));
   CUDA_TRY(ctx, cudaStreamSynchronize(comp));
@@ -794,7 +884,7 @@ int dppx_ctx_create(int32_t device, dppx_ctx** out) {
   // Verify that the sm_100a kernels load on this device (no silent fallback).
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(
-                                     select_stats_kernel(3, 16, 4, true))) != cudaSuccess) {
+                                     select_stats_kernel(3, 16, 4, true, false))) != cudaSuccess) {
     dppx_ctx_destroy(ctx);
     return DPPX_ERR_NO_DEVICE;
   }
@@ -812,7 +902,7 @@ void dppx_ctx_destroy(dppx_ctx* ctx) {
     if (b->p) cudaFree(b->p);
   for (int s = 0; s < 2; ++s) {
     DevBuf* sb[] = {&ctx->img[s], &ctx->mask[s], &ctx->out[s], &ctx->stats[s],
-                    &ctx->lens[s], &ctx->inj[s], &ctx->sd[s]};
+                    &ctx->lens[s], &ctx->inj[s], &ctx->sd[s], &ctx->dense[s], &ctx->dense_mask[s]};
     for (DevBuf* b : sb)
       if (b->p) cudaFree(b->p);
     if (ctx->sd_pinned[s]) cudaFreeHost(ctx->sd_pinned[s]);

@@ -90,6 +90,12 @@ struct StatsArgs {
   FastDiv div_tiles, div_rows;
   int tensor_in_bytes;       // row bytes covered by the input tensor map (N*C rounded down to 8)
   int tensor_out_bytes;      // same for the output tensor map
+  // A unit stages `pack` frames side by side ("slots"): narrow frames (e.g.
+  // 178 px) share one tile instead of leaving most lanes idle. Wide frames use
+  // pack = 1 and a 512-px slot. Smem: slot j at j*slot_stride, its rows at
+  // slot_px*C bytes (the TMA box is stored densely).
+  int pack, slot_px, slot_stride;
+  int row_slack;             // 1: input pitch >= roundup(N*C, 16), loads may read the slack
 };
 
 // K2: statistics -> pixels.

@@ -21,6 +21,7 @@
 #include <cuda.h>  // CUtensorMap (type only; encoded on the host via the driver entry point)
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "dppx_device.cuh"
@@ -275,23 +276,35 @@ constexpr int kStatsThreads = kConsumers + 32;
 constexpr int kMaxStages = 4;
 
 struct UnitPos {
-  int f, r, tile, px0;
+  int fg, r, tile, px0;  // frame group (frames fg*pack + j), grid row, column tile
 };
 
+template <bool PACKED>
 __device__ __forceinline__ UnitPos decode_unit(const StatsArgs& a, int u) {
   UnitPos p;
   const uint32_t rest = a.div_tiles.div(static_cast<uint32_t>(u));
   p.tile = u - static_cast<int>(rest * a.div_tiles.d);
-  const uint32_t f = a.div_rows.div(rest);
-  p.r = static_cast<int>(rest - f * a.div_rows.d);
-  p.f = static_cast<int>(f);
-  p.px0 = p.tile * kTilePx;
+  const uint32_t fg = a.div_rows.div(rest);
+  p.r = static_cast<int>(rest - fg * a.div_rows.d);
+  p.fg = static_cast<int>(fg);
+  p.px0 = PACKED ? 0 : p.tile * kTilePx;  // packed units are one tile wide
   return p;
 }
 
-template <int C>
+// Slot geometry: compile-time for wide frames (one 512-px slot per unit).
+template <bool PACKED>
+__device__ __forceinline__ int slot_px(const StatsArgs& a) {
+  return PACKED ? a.slot_px : kTilePx;
+}
+template <bool PACKED>
+__device__ __forceinline__ int units_pack(const StatsArgs& a) {
+  return PACKED ? a.pack : 1;
+}
+
+// Real bytes of a slot row starting at column px0.
+template <int C, bool PACKED>
 __device__ __forceinline__ int valid_bytes(const StatsArgs& a, int px0) {
-  return min(kTilePx, a.g.N - px0) * C;
+  return min(slot_px<PACKED>(a), a.g.N - px0) * C;
 }
 
 // A band whose rows run past M needs mirrored rows (image.cpp:105-110): it is
@@ -301,41 +314,62 @@ __device__ __forceinline__ bool band_reflects(const StatsArgs& a, int r) {
   return (r + 1) * B > a.g.M;
 }
 
-// Bytes of each smem row that the producer's copies deliver for unit p.
-template <int C, int B>
-__device__ __forceinline__ int staged_bytes(const StatsArgs& a, const UnitPos& p) {
-  if (band_reflects<B>(a, p.r)) return valid_bytes<C>(a, p.px0) & ~15;
-  return max(0, min(kTilePx * C, a.tensor_in_bytes - p.px0 * C));
+// Bytes per row a 1-D bulk copy stages (multiple of 16): rounded up into the
+// pitch slack when the rows have it, else down (the rest is filled by threads).
+template <int C, bool PACKED>
+__device__ __forceinline__ int bulk_row_bytes(const StatsArgs& a, int px0) {
+  const int v = valid_bytes<C, PACKED>(a, px0);
+  return a.row_slack ? min(slot_px<PACKED>(a) * C, (v + 15) & ~15) : (v & ~15);
 }
 
-template <int C, int B>
+// Bytes of each smem slot row that the producer's copies deliver.
+template <int C, int B, bool PACKED>
+__device__ __forceinline__ int staged_bytes(const StatsArgs& a, const UnitPos& p) {
+  if (band_reflects<B>(a, p.r)) return bulk_row_bytes<C, PACKED>(a, p.px0);
+  return max(0, min(slot_px<PACKED>(a) * C, a.tensor_in_bytes - p.px0 * C));
+}
+
+template <int C, int B, bool PACKED>
 __device__ __forceinline__ void load_unit(const StatsArgs& a, const CUtensorMap* tm, int u,
                                           uint8_t* st, uint64_t* bar) {
-  const UnitPos p = decode_unit(a, u);
+  const UnitPos p = decode_unit<PACKED>(a, u);
+  const int srb = slot_px<PACKED>(a) * C;
+  const int pk = units_pack<PACKED>(a);
+  const int nf = PACKED ? min(pk, a.g.F - p.fg * pk) : 1;
   if (!band_reflects<B>(a, p.r)) {
-    mbar_arrive_expect_tx(bar, B * kTilePx * C);  // full box, OOB bytes zero-filled
-    tma_load_3d(st, tm, p.px0 * C / 8, p.r * B, p.f, bar);
+    mbar_arrive_expect_tx(bar, nf * B * srb);  // full boxes, OOB bytes zero-filled
+    for (int j = 0; j < nf; ++j)
+      tma_load_3d(st + j * a.slot_stride, tm, p.px0 * C / 8, p.r * B, p.fg * pk + j, bar);
     return;
   }
-  const uint32_t copy = static_cast<uint32_t>(valid_bytes<C>(a, p.px0)) & ~15u;
-  mbar_arrive_expect_tx(bar, copy * B);
+  const uint32_t copy = static_cast<uint32_t>(bulk_row_bytes<C, PACKED>(a, p.px0));
+  mbar_arrive_expect_tx(bar, copy * B * nf);
   if (copy == 0) return;
-  const uint8_t* src = a.img + static_cast<int64_t>(p.f) * a.fstride + static_cast<int64_t>(p.px0) * C;
 #pragma unroll 1
-  for (int i = 0; i < B; ++i) {
-    const int srow = reflect_index(p.r * B + i, a.g.M);
-    bulk_g2s(st + i * (kTilePx * C), src + static_cast<int64_t>(srow) * a.pitch, copy, bar);
+  for (int j = 0; j < nf; ++j) {
+    const uint8_t* src = a.img + static_cast<int64_t>(p.fg * pk + j) * a.fstride +
+                         static_cast<int64_t>(p.px0) * C;
+#pragma unroll 1
+    for (int i = 0; i < B; ++i) {
+      const int srow = reflect_index(p.r * B + i, a.g.M);
+      bulk_g2s(st + j * a.slot_stride + i * srb, src + static_cast<int64_t>(srow) * a.pitch, copy,
+               bar);
+    }
   }
 }
 
-// One 3-D box store: rows >= M and bytes past the tensor's row are clipped by
-// the TMA unit; the consumers write the (< 8) bytes past tensor_out_bytes.
-template <int C, int B>
+// One 3-D box store per slot: rows >= M and bytes past the tensor's row are
+// clipped by the TMA unit; the consumers write the (< 8) bytes past
+// tensor_out_bytes.
+template <int C, int B, bool PACKED>
 __device__ __forceinline__ void store_unit(const StatsArgs& a, const CUtensorMap* tm, int u,
                                            const uint8_t* st) {
-  const UnitPos p = decode_unit(a, u);
+  const UnitPos p = decode_unit<PACKED>(a, u);
   if (p.px0 * C >= a.tensor_out_bytes) return;
-  tma_store_3d(tm, p.px0 * C / 8, p.r * B, p.f, st);
+  const int pk = units_pack<PACKED>(a);
+  const int nf = PACKED ? min(pk, a.g.F - p.fg * pk) : 1;
+  for (int j = 0; j < nf; ++j)
+    tma_store_3d(tm, p.px0 * C / 8, p.r * B, p.fg * pk + j, st + j * a.slot_stride);
   bulk_commit();
   bulk_wait_read_all();
 }
@@ -412,7 +446,7 @@ __device__ __forceinline__ void group_values(const StatsArgs& a, const DrawEnv& 
   }
 }
 
-template <int C, int B4, int NSUB, bool ADAPTIVE>
+template <int C, int B4, int NSUB, bool ADAPTIVE, bool PACKED>
 __global__ void __launch_bounds__(kStatsThreads)
     k_stats_tma(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
                 const StatsArgs a) {
@@ -454,7 +488,7 @@ __global__ void __launch_bounds__(kStatsThreads)
         const int s = k % S;
         if (k >= S) {
           mbar_wait(&done_bar[s], ((k / S) - 1) & 1);
-          if (a.out) store_unit<C, B>(a, &tm_out, stage_unit[s], smem + s * STAGE);
+          if (a.out) store_unit<C, B, PACKED>(a, &tm_out, stage_unit[s], smem + s * STAGE);
           ++done_units;
         }
         int u = atomicAdd(a.work_counter, 1);
@@ -465,13 +499,13 @@ __global__ void __launch_bounds__(kStatsThreads)
           mbar_arrive_expect_tx(&full_bar[s], 0);
           break;
         }
-        load_unit<C, B>(a, &tm_in, u, smem + s * STAGE, &full_bar[s]);
+        load_unit<C, B, PACKED>(a, &tm_in, u, smem + s * STAGE, &full_bar[s]);
       }
       // k units were loaded; units [done_units, k) still need their store.
       for (int j = done_units; j < k; ++j) {
         const int s = j % S;
         mbar_wait(&done_bar[s], (j / S) & 1);
-        if (a.out) store_unit<C, B>(a, &tm_out, stage_unit[s], smem + s * STAGE);
+        if (a.out) store_unit<C, B, PACKED>(a, &tm_out, stage_unit[s], smem + s * STAGE);
       }
       bulk_wait_all();
     }
@@ -490,6 +524,13 @@ __global__ void __launch_bounds__(kStatsThreads)
     uint32_t info, rowpre, stot;
     uint64_t seed[C];
   };
+  // Slot of this thread's 4-px strip (fixed for the kernel). Wide frames
+  // (PACKED = false) have one 512-px slot: the compiler folds all of this.
+  const int my_j = PACKED ? (4 * t) / a.slot_px : 0;
+  const bool in_slot = my_j < (PACKED ? a.pack : 1);
+  const int jj = in_slot ? my_j : 0;
+  const int lpx = 4 * t - jj * (PACKED ? a.slot_px : kTilePx);  // strip column in its slot
+  const int srb = PACKED ? a.slot_px * C : kTilePx * C;         // smem bytes per slot row
   auto load_meta = [&](int k_next) {
     Meta m;
     const int sn = k_next % S;
@@ -500,17 +541,20 @@ __global__ void __launch_bounds__(kStatsThreads)
 #pragma unroll
     for (int ch = 0; ch < C; ++ch) m.seed[ch] = 0;
     if (m.u >= 0) {
-      const UnitPos q = decode_unit(a, m.u);
-      const int qcell = q.px0 / B + t / B4;
-      if (ADAPTIVE && qcell < g.GC) {
-        m.info = __ldg(&a.cellinfo[static_cast<int64_t>(q.f) * g.G + q.r * g.GC + qcell]);
-        m.rowpre = __ldg(&a.rowprefix[static_cast<int64_t>(q.f) * g.GR + q.r]);
-        m.stot = __ldg(&a.totals[q.f]);
-      }
-      if (a.noise.kind == DPPX_NOISE_KEYED) {
+      const UnitPos q = decode_unit<PACKED>(a, m.u);
+      const int qf = q.fg * units_pack<PACKED>(a) + jj;
+      const int qcell = PACKED ? (q.px0 + lpx) / B : q.px0 / B + t / B4;
+      if (!PACKED || qf < g.F) {
+        if (ADAPTIVE && qcell < g.GC) {
+          m.info = __ldg(&a.cellinfo[static_cast<int64_t>(qf) * g.G + q.r * g.GC + qcell]);
+          m.rowpre = __ldg(&a.rowprefix[static_cast<int64_t>(qf) * g.GR + q.r]);
+          m.stot = __ldg(&a.totals[qf]);
+        }
+        if (a.noise.kind == DPPX_NOISE_KEYED) {
 #pragma unroll
-        for (int ch = 0; ch < C; ++ch)
-          m.seed[ch] = __ldg(&a.noise.mixed_seeds[static_cast<int64_t>(q.f) * C + ch]);
+          for (int ch = 0; ch < C; ++ch)
+            m.seed[ch] = __ldg(&a.noise.mixed_seeds[static_cast<int64_t>(qf) * C + ch]);
+        }
       }
     }
     return m;
@@ -523,19 +567,21 @@ __global__ void __launch_bounds__(kStatsThreads)
     const int u = cur.u;
     if (u < 0) break;
     next = load_meta(k + 1);  // the producer publishes ids S-1 units ahead
-    const UnitPos p = decode_unit(a, u);
-    const int cell = p.px0 / B + t / B4;
+    const UnitPos p = decode_unit<PACKED>(a, u);
+    const int f = p.fg * units_pack<PACKED>(a) + jj;  // this thread's frame
+    const int cell = PACKED ? (p.px0 + lpx) / B : p.px0 / B + t / B4;
     const int lic = t % B4;        // lane within cell
     const int sc = lic / SB4;      // subcell column
-    const bool active = cell < g.GC;
+    const bool active = (!PACKED || (in_slot && f < g.F)) && cell < g.GC;
     const int gidx = p.r * g.GC + cell;
     const bool simple = !ADAPTIVE || (cur.info & 1u);
     const uint32_t slot_s = cur.rowpre + (cur.info >> 1);
     const uint32_t S_tot = cur.stot;
-    const int vbytes = valid_bytes<C>(a, p.px0);
-    const int copy = staged_bytes<C, B>(a, p);  // bytes per row the producer staged
-    const int scopy = max(0, min(kTilePx * C, a.tensor_out_bytes - p.px0 * C));  // stored by TMA
-    const int need = min(kTilePx, g.GC * B - p.px0) * C;
+    const int vbytes = valid_bytes<C, PACKED>(a, p.px0);
+    const int copy = staged_bytes<C, B, PACKED>(a, p);  // bytes per row the producer staged
+    const int scopy = max(0, min(srb, a.tensor_out_bytes - p.px0 * C));  // stored by TMA
+    const int need = min(slot_px<PACKED>(a), g.GC * B - p.px0) * C;
+    const int nf = PACKED ? min(a.pack, g.F - p.fg * a.pack) : 1;
     uint64_t cs[C];
 #pragma unroll
     for (int ch = 0; ch < C; ++ch)
@@ -543,24 +589,58 @@ __global__ void __launch_bounds__(kStatsThreads)
 
     mbar_wait(&full_bar[s], (k / S) & 1);
 
-    if (copy < need) {  // tail + mirrored columns (image.cpp:105-110), from global
-      const int span = need - copy;
-      for (int e = t; e < B * span; e += kConsumers) {
-        const int i = e / span, x = copy + e % span;
-        const int px = p.px0 + x / C, ch = x % C;
-        const int srow = reflect_index(p.r * B + i, g.M);
-        st[i * ROWB + x] = __ldg(a.img + static_cast<int64_t>(p.f) * a.fstride +
-                                 static_cast<int64_t>(srow) * a.pitch +
-                                 static_cast<int64_t>(reflect_index(px, g.N)) * C + ch);
+    if constexpr (!PACKED) {
+      // Row tail + mirrored columns (image.cpp:105-110), from global. Starts at
+      // min(copy, vbytes): stray pitch-slack bytes a rounded-up copy brought
+      // in are padded columns and get their mirrored values too.
+      const int fs = min(copy, vbytes);
+      if (fs < need) {
+        const int span = need - fs;
+        for (int e = t; e < B * span; e += kConsumers) {
+          const int i = e / span, x = fs + e % span;
+          const int px = p.px0 + x / C, ch = x % C;
+          const int srow = reflect_index(p.r * B + i, g.M);
+          st[i * srb + x] = __ldg(a.img + static_cast<int64_t>(f) * a.fstride +
+                                  static_cast<int64_t>(srow) * a.pitch +
+                                  static_cast<int64_t>(reflect_index(px, g.N)) * C + ch);
+        }
+        named_bar_sync(1, kConsumers);
       }
-      named_bar_sync(1, kConsumers);
+    } else {
+      const int fstart = min(copy, vbytes);
+      if (fstart < need) {
+        // Row tail not covered by the staged copy (global) and mirrored columns
+        // (image.cpp:105-110), including any stray pitch-slack bytes the copy
+        // brought in: from the staged row in smem when the source byte is there,
+        // else from global. smem sources lie in [0, fstart), targets in
+        // [fstart, need): disjoint, so one barrier suffices.
+        const int span = need - fstart;
+        for (int e = t; e < nf * B * span; e += kConsumers) {
+          const int j = e / (B * span), e2 = e - j * (B * span);
+          const int i = e2 / span, x = fstart + e2 % span;
+          const int ch = x % C;
+          const int spx = reflect_index(p.px0 + x / C, g.N);  // source column
+          const int sx = (spx - p.px0) * C + ch;               // its byte in the slot row
+          uint8_t* rowp = st + j * a.slot_stride + i * srb;
+          uint8_t v;
+          if (sx >= 0 && sx < fstart) {
+            v = rowp[sx];
+          } else {
+            const int srow = reflect_index(p.r * B + i, g.M);
+            v = __ldg(a.img + static_cast<int64_t>(p.fg * units_pack<PACKED>(a) + j) * a.fstride +
+                      static_cast<int64_t>(srow) * a.pitch + static_cast<int64_t>(spx) * C + ch);
+          }
+          rowp[x] = v;
+        }
+        named_bar_sync(1, kConsumers);
+      }
     }
 
     uint32_t tot[C];
 #pragma unroll
     for (int ch = 0; ch < C; ++ch) tot[ch] = 0;
     const bool emit = a.out != nullptr;
-    uint8_t* mystrip = st + t * 4 * C;
+    uint8_t* mystrip = st + jj * a.slot_stride + lpx * C;
 
     // Not unrolled over vertical subcells: keeps the hot loop small enough for
     // the instruction cache (the rows inside are unrolled).
@@ -570,7 +650,7 @@ __global__ void __launch_bounds__(kStatsThreads)
 #pragma unroll
       for (int ch = 0; ch < C; ++ch) acc[ch] = 0;
 #pragma unroll
-      for (int i = 0; i < SB; ++i) accumulate_row<C>(mystrip + (vs * SB + i) * ROWB, acc);
+      for (int i = 0; i < SB; ++i) accumulate_row<C>(mystrip + (vs * SB + i) * srb, acc);
 #pragma unroll
       for (int ch = 0; ch < C; ++ch) tot[ch] += acc[ch];
       if constexpr (ADAPTIVE) {
@@ -580,13 +660,13 @@ __global__ void __launch_bounds__(kStatsThreads)
 #pragma unroll
           for (int ch = 0; ch < C; ++ch) acc[ch] += __shfl_xor_sync(0xFFFFFFFFu, acc[ch], o);
         uint32_t val[C];
-        group_values<C, SB4>(a, env_sub, active && !simple, acc, cs, p.f, p.r, cell, vs, sc, val);
+        group_values<C, SB4>(a, env_sub, active && !simple, acc, cs, f, p.r, cell, vs, sc, val);
         if (active && !simple) {
           if (lic % SB4 == 0) {
             const int64_t off = stat_offset(a, false, gidx, slot_s, S_tot, vs, sc);
 #pragma unroll
             for (int ch = 0; ch < C; ++ch)
-              a.stats[static_cast<int64_t>(p.f * C + ch) * a.sstride + off] =
+              a.stats[static_cast<int64_t>(f * C + ch) * a.sstride + off] =
                   static_cast<uint8_t>(val[ch]);
           }
           if (emit) {
@@ -596,7 +676,7 @@ __global__ void __launch_bounds__(kStatsThreads)
             for (int i = 0; i < SB; ++i)
 #pragma unroll
               for (int q = 0; q < C; ++q)
-                reinterpret_cast<uint32_t*>(mystrip + (vs * SB + i) * ROWB)[q] = w[q];
+                reinterpret_cast<uint32_t*>(mystrip + (vs * SB + i) * srb)[q] = w[q];
           }
         }
       }
@@ -609,13 +689,13 @@ __global__ void __launch_bounds__(kStatsThreads)
       for (int ch = 0; ch < C; ++ch) tot[ch] += __shfl_xor_sync(0xFFFFFFFFu, tot[ch], o);
     {
       uint32_t val[C];
-      group_values<C, B4>(a, env_cell, active && simple, tot, cs, p.f, p.r, cell, 0, 0, val);
+      group_values<C, B4>(a, env_cell, active && simple, tot, cs, f, p.r, cell, 0, 0, val);
       if (active && simple) {
         if (lic == 0) {
           const int64_t off = stat_offset(a, true, gidx, slot_s, S_tot, 0, 0);
 #pragma unroll
           for (int ch = 0; ch < C; ++ch)
-            a.stats[static_cast<int64_t>(p.f * C + ch) * a.sstride + off] =
+            a.stats[static_cast<int64_t>(f * C + ch) * a.sstride + off] =
                 static_cast<uint8_t>(val[ch]);
         }
         if (emit) {
@@ -624,19 +704,20 @@ __global__ void __launch_bounds__(kStatsThreads)
 #pragma unroll
           for (int i = 0; i < B; ++i)
 #pragma unroll
-            for (int q = 0; q < C; ++q) reinterpret_cast<uint32_t*>(mystrip + i * ROWB)[q] = w[q];
+            for (int q = 0; q < C; ++q) reinterpret_cast<uint32_t*>(mystrip + i * srb)[q] = w[q];
         }
       }
     }
 
     // Output bytes past the tensor map's row extent are written here (the
-    // TMA store covers [0, scopy)).
-    if (emit && active && (t + 1) * 4 * C > scopy && t * 4 * C < vbytes) {
+    // TMA store covers [0, scopy) of each slot row).
+    const int lx0 = lpx * C;
+    if (emit && active && lx0 + 4 * C > scopy && lx0 < vbytes) {
       const int rows = min(B, g.M - p.r * B);
       for (int i = 0; i < rows; ++i)
-        for (int x = max(t * 4 * C, scopy); x < min((t + 1) * 4 * C, vbytes); ++x)
-          a.out[static_cast<int64_t>(p.f) * a.ofstride + static_cast<int64_t>(p.r * B + i) * a.opitch +
-                static_cast<int64_t>(p.px0) * C + x] = st[i * ROWB + x];
+        for (int x = max(lx0, scopy); x < min(lx0 + 4 * C, vbytes); ++x)
+          a.out[static_cast<int64_t>(f) * a.ofstride + static_cast<int64_t>(p.r * B + i) * a.opitch +
+                static_cast<int64_t>(p.px0) * C + x] = st[jj * a.slot_stride + i * srb + x];
     }
 
     fence_proxy_async_smem();
@@ -799,6 +880,31 @@ __global__ void k_debug_lg2(unsigned int* max_bits) {
   atomicMax(max_bits, __float_as_uint(worst));
 }
 
+// Row re-pitch for the host pipeline: PCIe moves dense rows (one linear copy),
+// the kernels want 16-byte pitched rows (TMA). rows x width bytes.
+__global__ void k_repitch(uint8_t* __restrict__ dst, int64_t dpitch, const uint8_t* __restrict__ src,
+                          int64_t spitch, int64_t width, int64_t rows) {
+  const int64_t chunks = (width + 15) / 16;
+  const int64_t total = rows * chunks;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = e / chunks, x0 = (e - r * chunks) * 16;
+    const uint8_t* sp = src + r * spitch + x0;
+    uint8_t* dp = dst + r * dpitch + x0;
+    const int64_t n = width - x0 < 16 ? width - x0 : 16;
+    if (n == 16 && ((reinterpret_cast<uintptr_t>(dp) | reinterpret_cast<uintptr_t>(sp)) & 15) == 0) {
+      *reinterpret_cast<uint4*>(dp) = __ldg(reinterpret_cast<const uint4*>(sp));
+    } else {
+      uint8_t v[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = k < n ? __ldg(sp + k) : 0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        if (k < n) dp[k] = v[k];
+    }
+  }
+}
+
 __global__ void k_debug_laplace(uint64_t mixed_seed, const uint32_t* keys, int count, double sigma,
                                 double* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -813,10 +919,10 @@ __global__ void k_debug_laplace(uint64_t mixed_seed, const uint32_t* keys, int c
 // ============================================================================
 using StatsKernel = void (*)(const CUtensorMap, const CUtensorMap, const StatsArgs);
 
-template <int C, bool AD>
+template <int C, bool AD, bool PK>
 StatsKernel pick_b(int b, int n) {
 #define DPPX_CASE(B4v, NS)                 \
-  if (b == 4 * (B4v) && n == (NS)) return k_stats_tma<C, B4v, NS, AD>;
+  if (b == 4 * (B4v) && n == (NS)) return k_stats_tma<C, B4v, NS, AD, PK>;
   DPPX_CASE(1, 1)
   DPPX_CASE(2, 1)
   DPPX_CASE(4, 1)
@@ -833,10 +939,16 @@ StatsKernel pick_b(int b, int n) {
   return nullptr;
 }
 
-StatsKernel select_stats_kernel(int C, int b, int n, bool adaptive) {
+StatsKernel select_stats_kernel(int C, int b, int n, bool adaptive, bool packed) {
   if (!adaptive && n != 1) return nullptr;
-  if (C == 1) return adaptive ? pick_b<1, true>(b, n) : pick_b<1, false>(b, n);
-  if (C == 3) return adaptive ? pick_b<3, true>(b, n) : pick_b<3, false>(b, n);
+  if (C == 1) {
+    if (packed) return adaptive ? pick_b<1, true, true>(b, n) : pick_b<1, false, true>(b, n);
+    return adaptive ? pick_b<1, true, false>(b, n) : pick_b<1, false, false>(b, n);
+  }
+  if (C == 3) {
+    if (packed) return adaptive ? pick_b<3, true, true>(b, n) : pick_b<3, false, true>(b, n);
+    return adaptive ? pick_b<3, true, false>(b, n) : pick_b<3, false, false>(b, n);
+  }
   return nullptr;
 }
 
@@ -874,6 +986,14 @@ cudaError_t launch_synth(const BatchGeom& g, uint32_t seed, uint32_t f0, uint8_t
                          int64_t pitch, int64_t fstride, uint8_t* mask, int64_t mpitch,
                          int64_t mfstride, cudaStream_t s) {
   k_synth<<<148 * 8, 256, 0, s>>>(g, seed, f0, img, pitch, fstride, mask, mpitch, mfstride);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_repitch(uint8_t* dst, int64_t dpitch, const uint8_t* src, int64_t spitch,
+                           int64_t width, int64_t rows, cudaStream_t s) {
+  const int64_t work = rows * ((width + 15) / 16);
+  const int blocks = static_cast<int>(std::min<int64_t>((work + 255) / 256, 148 * 16));
+  k_repitch<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(dst, dpitch, src, spitch, width, rows);
   return cudaGetLastError();
 }
 

@@ -300,3 +300,19 @@ def test_fast_path_equals_exact_path(ctx, eps, b, n):
         finally:
             ctx.set_exact_noise(False)
         assert fast[0] == exact[0] and np.array_equal(fast[1], exact[1])
+
+
+@pytest.mark.parametrize("b,n,C", [(16, 4, 3), (16, 1, 3), (8, 2, 1), (32, 8, 3), (4, 1, 3)])
+def test_narrow_frames_packed_per_unit(ctx, b, n, C):
+    """Narrow frames (CelebA 178x218) share a staged tile ("slots"); odd frame
+    counts leave a partial last group. Bit-exact vs the oracle."""
+    F, M, N = 5, 218, 178
+    frames = oracle.synth_frames(11, F, M, N, C)
+    masks = oracle.synth_masks(11, F, M, N)
+    p = dp.make_privacy_params(0.5, 16, b, n)
+    seeds = dp.plane_seeds(5, F, C, frame0=11)
+    ctx.reset_stats()
+    pls, img = ctx.pixelize_adaptive(frames, masks, p, dp.NOISE_KEYED, seeds)
+    assert ctx.stats()["launches"]["stats_tma"] >= 1
+    rp, ri = _oracle_adaptive(frames, masks, p, "keyed", seeds)
+    assert pls == rp and np.array_equal(img, ri)
