@@ -531,6 +531,17 @@ __global__ void __launch_bounds__(kStatsThreads)
   const int jj = in_slot ? my_j : 0;
   const int lpx = 4 * t - jj * (PACKED ? a.slot_px : kTilePx);  // strip column in its slot
   const int srb = PACKED ? a.slot_px * C : kTilePx * C;         // smem bytes per slot row
+  // Packed mode: byte offsets of the mirrored sources of the padding bytes
+  // [N*C, GC*b*C) of a slot row (image.cpp:105-110), shared by all units.
+  __shared__ uint16_t fill_src[128];
+  if (PACKED) {
+    const int v0 = g.N * C, pad = (g.GC * B - g.N) * C;
+    for (int x = t; x < pad && x < 128; x += kConsumers) {
+      const int cpx = (v0 + x) / C, ch = (v0 + x) - cpx * C;
+      fill_src[x] = static_cast<uint16_t>(reflect_index(cpx, g.N) * C + ch);
+    }
+    named_bar_sync(1, kConsumers);
+  }
   auto load_meta = [&](int k_next) {
     Meta m;
     const int sn = k_next % S;
@@ -589,48 +600,45 @@ __global__ void __launch_bounds__(kStatsThreads)
 
     mbar_wait(&full_bar[s], (k / S) & 1);
 
-    if constexpr (!PACKED) {
-      // Row tail + mirrored columns (image.cpp:105-110), from global. Starts at
-      // min(copy, vbytes): stray pitch-slack bytes a rounded-up copy brought
-      // in are padded columns and get their mirrored values too.
-      const int fs = min(copy, vbytes);
-      if (fs < need) {
-        const int span = need - fs;
-        for (int e = t; e < B * span; e += kConsumers) {
-          const int i = e / span, x = fs + e % span;
-          const int px = p.px0 + x / C, ch = x % C;
-          const int srow = reflect_index(p.r * B + i, g.M);
-          st[i * srb + x] = __ldg(a.img + static_cast<int64_t>(f) * a.fstride +
-                                  static_cast<int64_t>(srow) * a.pitch +
-                                  static_cast<int64_t>(reflect_index(px, g.N)) * C + ch);
+    // Row tail not covered by the staged copy and mirrored padding columns
+    // (image.cpp:105-110), including stray pitch-slack bytes a rounded-up copy
+    // brought in. Work is split as (slot row, column lane) so no index needs a
+    // runtime division. A mirrored byte is read from the staged row in smem when
+    // it is there (sources lie in [0, fs), targets in [fs, need): disjoint),
+    // else from global memory.
+    if (PACKED && a.row_slack) {
+      // Packed slots always start at column 0 and the staged rows always cover
+      // the real bytes: the mirror map of the padding is the same for every
+      // row of every unit (precomputed in fill_src).
+      const int span = need - vbytes;
+      if (span > 0) {
+        constexpr int kLanes = 8;
+        for (int pr = t / kLanes; pr < nf * B; pr += kConsumers / kLanes) {
+          const int j = pr / B, i = pr - j * B;
+          uint8_t* rowp = st + j * a.slot_stride + i * srb;
+          for (int x = t % kLanes; x < span; x += kLanes) rowp[vbytes + x] = rowp[fill_src[x]];
         }
         named_bar_sync(1, kConsumers);
       }
     } else {
-      const int fstart = min(copy, vbytes);
-      if (fstart < need) {
-        // Row tail not covered by the staged copy (global) and mirrored columns
-        // (image.cpp:105-110), including any stray pitch-slack bytes the copy
-        // brought in: from the staged row in smem when the source byte is there,
-        // else from global. smem sources lie in [0, fstart), targets in
-        // [fstart, need): disjoint, so one barrier suffices.
-        const int span = need - fstart;
-        for (int e = t; e < nf * B * span; e += kConsumers) {
-          const int j = e / (B * span), e2 = e - j * (B * span);
-          const int i = e2 / span, x = fstart + e2 % span;
-          const int ch = x % C;
-          const int spx = reflect_index(p.px0 + x / C, g.N);  // source column
-          const int sx = (spx - p.px0) * C + ch;               // its byte in the slot row
-          uint8_t* rowp = st + j * a.slot_stride + i * srb;
-          uint8_t v;
-          if (sx >= 0 && sx < fstart) {
-            v = rowp[sx];
-          } else {
-            const int srow = reflect_index(p.r * B + i, g.M);
-            v = __ldg(a.img + static_cast<int64_t>(p.fg * units_pack<PACKED>(a) + j) * a.fstride +
-                      static_cast<int64_t>(srow) * a.pitch + static_cast<int64_t>(spx) * C + ch);
+      const int fs = min(copy, vbytes);
+      if (fs < need) {
+        constexpr int kLanes = 4;  // consumer threads per slot row
+        const int rows_total = nf * B;
+        for (int pr = t / kLanes; pr < rows_total; pr += kConsumers / kLanes) {
+          const int j = pr / B, i = pr - j * B;  // B is a compile-time power of two
+          uint8_t* rowp = st + j * (PACKED ? a.slot_stride : 0) + i * srb;
+          const int frame = p.fg * units_pack<PACKED>(a) + j;
+          const int srow = reflect_index(p.r * B + i, g.M);
+          const uint8_t* grow = a.img + static_cast<int64_t>(frame) * a.fstride +
+                                static_cast<int64_t>(srow) * a.pitch;
+          for (int x = fs + (t % kLanes); x < need; x += kLanes) {
+            const int cpx = x / C, ch = x - cpx * C;  // C is a compile-time constant
+            const int spx = reflect_index(p.px0 + cpx, g.N);
+            const int sx = (spx - p.px0) * C + ch;
+            rowp[x] = (sx >= 0 && sx < fs) ? rowp[sx]
+                                           : __ldg(grow + static_cast<int64_t>(spx) * C + ch);
           }
-          rowp[x] = v;
         }
         named_bar_sync(1, kConsumers);
       }
