@@ -19,6 +19,7 @@
  *   dppix::reassemble           adaptive.hpp:78          dppx_reassemble[_dev]
  *   dppix::reconstruct          record.hpp:63            dppx_reassemble / dppx_broadcast_means
  *   dppix::classify_regions     adaptive.hpp:45-46       dppx_classify_regions
+ *   dppix::encode / decode      record.hpp:55-61         dppx_encode_record / dppx_decode_record
  *   RecordError / invalid_argument  errors.hpp:22-55     dppx_status codes
  *
  * Conventions
@@ -61,7 +62,10 @@ typedef enum {
   DPPX_ERR_CORRUPT = 2,   /* RecordError(corrupt_record) (adaptive.cpp:192-210) */
   DPPX_ERR_CUDA = 3,      /* std::runtime_error: CUDA failure                  */
   DPPX_ERR_OOM = 4,       /* std::bad_alloc                                    */
-  DPPX_ERR_NO_DEVICE = 5  /* no sm_100 device / kernels not loadable           */
+  DPPX_ERR_NO_DEVICE = 5, /* no sm_100 device / kernels not loadable           */
+  DPPX_ERR_NOT_A_RECORD = 6,        /* RecordError(not_a_record)             */
+  DPPX_ERR_UNSUPPORTED_VERSION = 7, /* RecordError(unsupported_version)      */
+  DPPX_ERR_CORRUPTION = 8           /* RecordError(corruption): CRC mismatch */
 } dppx_status;
 
 typedef enum {
@@ -193,6 +197,24 @@ int dppx_reassemble(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* 
  * ignored): per-frame G float mask means at mask_means + f*G. */
 int dppx_classify_regions(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* mask,
                           int32_t b, float* mask_means);
+
+/* ---- .dppx records (record.hpp:48-71, record.cpp:124-278; host only) ------ */
+/* Decoded header of a record; the payload is bytes[payload_offset, +payload_len). */
+typedef struct {
+  int32_t height, width, b, n, mode; /* mode 1 = uniform, 2 = adaptive */
+  uint32_t payload_offset, payload_len;
+} dppx_record_info;
+
+uint32_t dppx_crc32(uint32_t crc, const uint8_t* data, size_t len); /* zlib-compatible */
+size_t dppx_record_size(size_t payload_len);                         /* 20 + payload + 4 */
+/* Header + payload (a statistics plane as the kernels wrote it) + CRC32.
+ * DPPX_ERR_INVALID mirrors encode's std::invalid_argument (record.cpp:124-150). */
+int dppx_encode_record(int32_t height, int32_t width, int32_t b, int32_t n, int32_t mode,
+                       const uint8_t* payload, size_t payload_len, uint8_t* out, size_t cap,
+                       size_t* out_len);
+/* decode's checks in order: NOT_A_RECORD, CORRUPT (truncated header), CORRUPTION
+ * (CRC), UNSUPPORTED_VERSION, CORRUPT (mode/reserved/dims/fields/lengths/count). */
+int dppx_decode_record(const uint8_t* bytes, size_t len, dppx_record_info* info);
 
 /* Diagnostics for parity tests: the device noise of `count` keys
  * (keys[4*i..4*i+3] = r, c, sr, sc) for one plane seed at scale sigma. */

@@ -40,6 +40,7 @@ if not os.path.exists(LIB_PATH):
 _lib = C.CDLL(LIB_PATH)
 
 OK, ERR_INVALID, ERR_CORRUPT, ERR_CUDA, ERR_OOM, ERR_NO_DEVICE = range(6)
+ERR_NOT_A_RECORD, ERR_UNSUPPORTED_VERSION, ERR_CORRUPTION = 6, 7, 8
 NOISE_NONE, NOISE_KEYED, NOISE_PHILOX, NOISE_INJECTED = range(4)
 K_CLASSIFY, K_STATS, K_GENERIC, K_EXPAND, K_AUX, K_COUNT = range(6)
 KERNEL_FAMILIES = ("classify", "stats_tma", "stats_generic", "expand", "aux")
@@ -74,6 +75,11 @@ class FramesDesc(C.Structure):
 class Noise(C.Structure):
     _fields_ = [("kind", C.c_int32), ("frame_base", C.c_uint32),
                 ("plane_seeds", C.POINTER(C.c_uint64)), ("injected", C.POINTER(C.c_double))]
+
+
+class RecordInfo(C.Structure):
+    _fields_ = [("height", C.c_int32), ("width", C.c_int32), ("b", C.c_int32), ("n", C.c_int32),
+                ("mode", C.c_int32), ("payload_offset", C.c_uint32), ("payload_len", C.c_uint32)]
 
 
 class KernelStats(C.Structure):
@@ -129,6 +135,11 @@ ABI = {
     "dppx_broadcast_means": (C.c_int, [_ctxp, _descp, _vp, C.c_int32, _vp]),
     "dppx_reassemble": (C.c_int, [_ctxp, _descp, _vp, C.c_int64, _vp, C.c_int32, C.c_int32, _vp]),
     "dppx_classify_regions": (C.c_int, [_ctxp, _descp, _vp, C.c_int32, _vp]),
+    "dppx_crc32": (C.c_uint32, [C.c_uint32, _vp, C.c_size_t]),
+    "dppx_record_size": (C.c_size_t, [C.c_size_t]),
+    "dppx_encode_record": (C.c_int, [C.c_int32] * 5 + [_vp, C.c_size_t, _vp, C.c_size_t,
+                                                       C.POINTER(C.c_size_t)]),
+    "dppx_decode_record": (C.c_int, [_vp, C.c_size_t, C.POINTER(RecordInfo)]),
     "dppx_debug_device_laplace": (C.c_int, [_ctxp, C.c_uint64, _vp, C.c_int32, C.c_double, _vp]),
     "dppx_debug_lg2_max_error": (C.c_int, [_ctxp, C.POINTER(C.c_double)]),
 }
@@ -159,6 +170,12 @@ def _raise(rc, msg):
         raise ValueError(msg)
     if rc == ERR_CORRUPT:
         raise RecordError(msg)
+    if rc == ERR_NOT_A_RECORD:
+        raise RecordError(msg, "not_a_record")
+    if rc == ERR_UNSUPPORTED_VERSION:
+        raise RecordError(msg, "unsupported_version")
+    if rc == ERR_CORRUPTION:
+        raise RecordError(msg, "corruption")
     if rc == ERR_OOM:
         raise MemoryError(msg)
     if rc == ERR_NO_DEVICE:
@@ -605,7 +622,68 @@ def classify_regions(mask, geom: Geometry) -> RegionClassification:
     return RegionClassification(geom, mm, (mm > np.float32(0.5)).astype(np.uint8))
 
 
+# ---------------------------------------------------------------- .dppx records
+def crc32(data: bytes, crc: int = 0) -> int:
+    buf = np.frombuffer(data, np.uint8)
+    return _lib.dppx_crc32(crc, buf.ctypes.data if len(buf) else None, len(buf))
+
+
+def encode_record(height: int, width: int, b: int, n: int, payload: bytes,
+                  adaptive: bool) -> bytes:
+    """encode (record.cpp:124-175) around a statistics plane (the compact store)."""
+    buf = np.frombuffer(payload, np.uint8)
+    out = np.zeros(_lib.dppx_record_size(len(buf)), np.uint8)
+    n_out = C.c_size_t(0)
+    rc = _lib.dppx_encode_record(height, width, b, n, 2 if adaptive else 1,
+                                 buf.ctypes.data if len(buf) else None, len(buf),
+                                 out.ctypes.data, len(out), C.byref(n_out))
+    if rc != OK:
+        _raise(rc, "encode: payload or header fields inconsistent")
+    return out.tobytes()
+
+
+@dataclasses.dataclass
+class PixelRecord:
+    """dppix::PixelRecord (record.hpp:37-46): dims plus GridMeans or AdaptiveMeans."""
+    height: int
+    width: int
+    payload: object  # GridMeans | AdaptiveMeans
+
+    def mode(self) -> int:
+        return 1 if isinstance(self.payload, GridMeans) else 2
+
+
+def encode(record: PixelRecord) -> bytes:
+    p = record.payload
+    if isinstance(p, GridMeans):
+        return encode_record(record.height, record.width, p.geometry.b, 1,
+                             bytes(np.asarray(p.values, np.uint8)), False)
+    return encode_record(record.height, record.width, p.geometry.b, p.n, p.payload(), True)
+
+
+def decode(data: bytes) -> PixelRecord:
+    """decode (record.cpp:177-278) with the reference's RecordError taxonomy."""
+    buf = np.frombuffer(data, np.uint8)
+    info = RecordInfo()
+    rc = _lib.dppx_decode_record(buf.ctypes.data if len(buf) else None, len(buf), C.byref(info))
+    if rc != OK:
+        _raise(rc, f"decode: status {rc}")
+    body = bytes(buf[info.payload_offset: info.payload_offset + info.payload_len])
+    geom = grid_dims(info.height, info.width, info.b)
+    if info.mode == 1:
+        return PixelRecord(info.height, info.width, GridMeans(geom, np.frombuffer(body, np.uint8).copy()))
+    return PixelRecord(info.height, info.width, parse_adaptive_payload(body, geom, info.n))
+
+
+def reconstruct(record: PixelRecord) -> np.ndarray:
+    """reconstruct (record.cpp:280-286) on the GPU."""
+    if isinstance(record.payload, GridMeans):
+        return broadcast_means(record.payload, record.height, record.width)
+    return reassemble(record.payload, record.height, record.width)
+
+
 __all__ = [
+    "crc32", "encode_record", "encode", "decode", "reconstruct", "PixelRecord", "RecordInfo",
     "Context", "default_context", "grid_dims", "make_privacy_params", "sensitivity", "keyed_bits",
     "laplace_at", "derive_plane_seed", "plane_seeds", "adaptive_payload_capacity",
     "pixelize_parallel", "pixelize_adaptive", "broadcast_means", "reassemble", "classify_regions",

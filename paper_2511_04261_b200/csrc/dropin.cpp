@@ -6,6 +6,8 @@
 // std::runtime_error (there is no CPU fallback).
 #include <cmath>
 #include <cstdlib>
+#include <fstream>
+#include <iterator>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -17,6 +19,7 @@
 #include "dppix/image.hpp"
 #include "dppix/noise.hpp"
 #include "dppix/pixelize.hpp"
+#include "dppix/record.hpp"
 #include "dppx_gpu.h"
 
 namespace dppix {
@@ -397,6 +400,117 @@ GrayImage reassemble(const AdaptiveMeans& means, int height, int width) {
                         geom.b, n, out.pixels.data()),
         "reassemble");
   return out;
+}
+
+// --------------------------------------------------------------- record.hpp
+RecordMode PixelRecord::mode() const {
+  return std::holds_alternative<GridMeans>(payload) ? RecordMode::uniform : RecordMode::adaptive;
+}
+
+int PixelRecord::grid_side() const {
+  return std::holds_alternative<GridMeans>(payload) ? std::get<GridMeans>(payload).geometry.b
+                                                    : std::get<AdaptiveMeans>(payload).geometry.b;
+}
+
+int PixelRecord::subgrid_factor() const {
+  return std::holds_alternative<GridMeans>(payload) ? 1 : std::get<AdaptiveMeans>(payload).n;
+}
+
+std::vector<std::uint8_t> encode(const PixelRecord& record) {
+  const int b = record.grid_side(), n = record.subgrid_factor();
+  if (record.height < 1 || record.width < 1)
+    throw std::invalid_argument("encode: dimensions must be >= 1");
+  if (b < 1 || b > std::max(record.height, record.width))
+    throw std::invalid_argument("encode: invalid grid side");
+  if (n < 1 || b % n != 0) throw std::invalid_argument("encode: subgrid factor must divide grid side");
+  const GridGeometry geom = grid_dims(record.height, record.width, b);
+  const std::size_t G = geom.grid_count();
+  std::vector<std::uint8_t> payload;
+  if (const GridMeans* u = std::get_if<GridMeans>(&record.payload)) {  // record.cpp:143-147
+    if (u->geometry != geom || u->values.size() != G)
+      throw std::invalid_argument("encode: uniform payload length mismatch");
+    payload = u->values;
+  } else {  // record.cpp:148-171
+    const AdaptiveMeans& am = std::get<AdaptiveMeans>(record.payload);
+    const RegionClassification& cls = am.classification;
+    const std::size_t S = static_cast<std::size_t>(cls.simple_count());
+    if (am.geometry != geom || cls.geometry != geom || cls.mask_means.size() != G ||
+        cls.is_simple.size() != G || am.simple_means.size() != S ||
+        am.complex_submeans.size() != (G - S) * static_cast<std::size_t>(n) * n)
+      throw std::invalid_argument("encode: adaptive payload length mismatch");
+    for (std::size_t g = 0; g < G; ++g)
+      if ((cls.is_simple[g] != 0) != simple_from_mean(cls.mask_means[g]))
+        throw std::invalid_argument("encode: classification disagrees with mask means");
+    payload.resize(4 * G + 4);
+    std::memcpy(payload.data(), cls.mask_means.data(), 4 * G);
+    const std::uint32_t S32 = static_cast<std::uint32_t>(S);
+    std::memcpy(payload.data() + 4 * G, &S32, 4);
+    payload.insert(payload.end(), am.simple_means.begin(), am.simple_means.end());
+    payload.insert(payload.end(), am.complex_submeans.begin(), am.complex_submeans.end());
+  }
+  std::vector<std::uint8_t> out(dppx_record_size(payload.size()));
+  std::size_t len = 0;
+  if (dppx_encode_record(record.height, record.width, b, n, static_cast<int>(record.mode()),
+                         payload.data(), payload.size(), out.data(), out.size(), &len) != DPPX_OK)
+    throw std::invalid_argument("encode: payload inconsistent with header fields");
+  out.resize(len);
+  return out;
+}
+
+PixelRecord decode(const std::vector<std::uint8_t>& bytes) {
+  dppx_record_info info{};
+  switch (dppx_decode_record(bytes.data(), bytes.size(), &info)) {
+    case DPPX_OK:
+      break;
+    case DPPX_ERR_NOT_A_RECORD:
+      throw RecordError(RecordErrorKind::not_a_record, "decode: missing DPPX magic");
+    case DPPX_ERR_CORRUPTION:
+      throw RecordError(RecordErrorKind::corruption, "decode: CRC mismatch");
+    case DPPX_ERR_UNSUPPORTED_VERSION:
+      throw RecordError(RecordErrorKind::unsupported_version, "decode: unsupported format version");
+    default:
+      throw RecordError(RecordErrorKind::corrupt_record, "decode: inconsistent record");
+  }
+  PixelRecord rec;
+  rec.height = info.height;
+  rec.width = info.width;
+  const GridGeometry geom = grid_dims(info.height, info.width, info.b);
+  const std::uint8_t* p = bytes.data() + info.payload_offset;
+  if (info.mode == 1) {
+    GridMeans m;
+    m.geometry = geom;
+    m.values.assign(p, p + info.payload_len);
+    rec.payload = std::move(m);
+  } else {
+    AdaptiveMeans am;
+    parse_payload(p, geom, info.n, &am);
+    rec.payload = std::move(am);
+  }
+  return rec;
+}
+
+GrayImage reconstruct(const PixelRecord& record) {  // record.cpp:280-286
+  if (const GridMeans* u = std::get_if<GridMeans>(&record.payload))
+    return broadcast_means(*u, record.height, record.width);
+  return reassemble(std::get<AdaptiveMeans>(record.payload), record.height, record.width);
+}
+
+PixelRecord read_record(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw IoError("read_record: cannot open " + path);
+  std::vector<std::uint8_t> bytes((std::istreambuf_iterator<char>(in)),
+                                  std::istreambuf_iterator<char>());
+  if (in.bad()) throw IoError("read_record: read failed for " + path);
+  return decode(bytes);
+}
+
+void write_record(const PixelRecord& record, const std::string& path) {
+  const std::vector<std::uint8_t> bytes = encode(record);
+  std::ofstream out(path, std::ios::binary | std::ios::trunc);
+  if (!out) throw IoError("write_record: cannot open " + path);
+  out.write(reinterpret_cast<const char*>(bytes.data()), static_cast<std::streamsize>(bytes.size()));
+  out.flush();
+  if (!out) throw IoError("write_record: write failed for " + path);
 }
 
 }  // namespace dppix

@@ -15,6 +15,7 @@
 #include "dppix/image.hpp"
 #include "dppix/noise.hpp"
 #include "dppix/pixelize.hpp"
+#include "dppix/record.hpp"
 
 using namespace dppix;
 
@@ -213,6 +214,53 @@ int main() {
       const AdaptiveResult r = pixelize_adaptive(img, random_mask(rng, h, w),
                                                  make_privacy_params(0.5, 16, b, n), NoiseSeed{rng()});
       CHECK(reassemble(r.means, h, w) == r.image);
+    }
+  }
+  // records: size law, decode(encode) identity, reconstruct == emitted image,
+  // failure taxonomy (test_record.cpp:83-293)
+  {
+    std::mt19937_64 rng(47);
+    for (int round = 0; round < 10; ++round) {
+      const int h = 6 + static_cast<int>(rng() % 50), w = 6 + static_cast<int>(rng() % 50);
+      const int b = 1 + static_cast<int>(rng() % std::min({h, w, 8}));
+      const GrayImage img = random_image(rng, h, w);
+      if (round % 2 == 0) {
+        UniformResult r = pixelize_parallel(img, make_privacy_params(0.5, 16, b), NoiseSeed{rng()});
+        const PixelRecord rec{h, w, r.means};
+        const std::vector<std::uint8_t> bytes = encode(rec);
+        CHECK(bytes.size() == 24 + static_cast<std::size_t>(r.means.geometry.grid_count()));
+        CHECK(decode(bytes) == rec);
+        CHECK(reconstruct(decode(bytes)) == r.image);
+      } else {
+        const int n = b % 2 == 0 ? 2 : 1;
+        AdaptiveResult r = pixelize_adaptive(img, random_mask(rng, h, w),
+                                             make_privacy_params(0.5, 16, b, n), NoiseSeed{rng()});
+        const PixelRecord rec{h, w, r.means};
+        const std::vector<std::uint8_t> bytes = encode(rec);
+        CHECK(decode(bytes) == rec);
+        CHECK(reconstruct(decode(bytes)) == r.image);
+      }
+    }
+    GridMeans one;
+    one.geometry = grid_dims(16, 16, 16);
+    one.values = {200};
+    std::vector<std::uint8_t> bytes = encode(PixelRecord{16, 16, one});
+    CHECK(bytes.size() == 25);
+    std::vector<std::uint8_t> bad = bytes;
+    bad[0] = 'X';
+    try {
+      decode(bad);
+      CHECK(false);
+    } catch (const RecordError& e) {
+      CHECK(e.kind() == RecordErrorKind::not_a_record);
+    }
+    bad = bytes;
+    bad[21] ^= 0x40;
+    try {
+      decode(bad);
+      CHECK(false);
+    } catch (const RecordError& e) {
+      CHECK(e.kind() == RecordErrorKind::corruption);
     }
   }
   std::printf("%d passed, %d failed\n", g_pass, g_fail);

@@ -36,7 +36,9 @@ def test_dropin_library_exports_reference_api():
     for fn in ["dppix::pixelize_parallel(", "dppix::pixelize_adaptive(", "dppix::broadcast_means(",
                "dppix::reassemble(", "dppix::classify_regions(", "dppix::make_privacy_params(",
                "dppix::grid_dims(", "dppix::laplace_at(", "dppix::keyed_bits(",
-               "dppix::mirror_pad(", "dppix::grid_mean(", "dppix::mask_grid_mean("]:
+               "dppix::mirror_pad(", "dppix::grid_mean(", "dppix::mask_grid_mean(",
+               "dppix::encode(", "dppix::decode(", "dppix::reconstruct(", "dppix::read_record(",
+               "dppix::write_record("]:
         assert fn in out, fn
 
 
