@@ -325,6 +325,35 @@ def main():
     traffic = ncu_traffic(args.workload)
     launches_timed = sum(st["launches"].values())
 
+    # ---- standalone reconstruction (reassemble / broadcast_means): K0(payload) + K2 ----
+    recon = None
+    try:
+        ctx.reset_stats()
+        ctx.set_timing(True)
+        reps = 3
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for i in range(reps + 1):
+            if i == 1:
+                r0.record(stream)
+            if adaptive:
+                ctx.reassemble_dev(d, stats, sstride, lens, b, n, out)
+            else:
+                ctx.broadcast_means_dev(d, stats, b, out)
+        r1.record(stream)
+        r1.synchronize()
+        ctx.synchronize()
+        rs = ctx.stats()
+        ctx.set_timing(False)
+        k2_ms = rs["device_ms"]["expand"] / max(1, rs["launches"]["expand"])
+        k2_bytes = F * M * N * C + payload_bytes
+        recon = {"ms_per_call": round(r0.elapsed_time(r1) / reps, 4),
+                 "k2_ms": round(k2_ms, 4),
+                 "k2_gbs": round(k2_bytes / (k2_ms / 1e3) / 1e9, 1),
+                 "k2_frac": round(k2_bytes / (k2_ms / 1e3) / 1e9 / peak, 4),
+                 "k2_algorithmic_bytes": k2_bytes}
+    except Exception as exc:  # reported, never fatal for the headline
+        recon = {"error": str(exc)[:200]}
+
     # ---- e2e: public host API, pinned host buffers ----
     e2e = None
     if not args.no_e2e:
@@ -434,6 +463,7 @@ def main():
                          "k0_ms_per_launch": round(st["device_ms"]["classify"] /
                                                    max(1, st["launches"]["classify"]), 4)},
             "cpu_baseline": cpu,
+            "reconstruct": recon,
             "e2e": e2e,
             "gpu_launches": launches_timed,
             "clocks": clk.summary(),

@@ -31,6 +31,10 @@ cudaError_t launch_stats_tma(StatsKernel k, const CUtensorMap& tin, const CUtens
                              const StatsArgs& a, int grid, size_t smem, cudaStream_t s);
 cudaError_t launch_stats_generic(const StatsArgs& a, cudaStream_t s);
 cudaError_t launch_expand(const ExpandArgs& a, cudaStream_t s);
+using ExpandKernel = void (*)(const CUtensorMap, const ExpandArgs);
+ExpandKernel select_expand_kernel(int C, int b, int n, bool adaptive);
+cudaError_t launch_expand_tma(ExpandKernel k, const CUtensorMap& tout, const ExpandArgs& a,
+                              int grid, size_t smem, cudaStream_t s);
 cudaError_t launch_synth(const BatchGeom& g, uint32_t seed, uint32_t f0, uint8_t* img,
                          int64_t pitch, int64_t fstride, uint8_t* mask, int64_t mpitch,
                          int64_t mfstride, cudaStream_t s);
@@ -514,7 +518,31 @@ int expand_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* stats, i
   }
   PendingTiming pt;
   timing_begin(ctx, DPPX_K_EXPAND, &pt);
-  CUDA_TRY(ctx, launch_expand(e, ctx->stream));
+  // Fast path: staged tile + TMA store (aligned output, b in {4..32}, C in {1,3}).
+  ExpandKernel k = select_expand_kernel(g.C, g.b, g.n, adaptive);
+  const int tile = stats_tile_px();
+  const int64_t row_bytes = static_cast<int64_t>(g.N) * g.C;
+  CUtensorMap tout{};
+  const bool aligned = aligned16(out) && e.opitch % 16 == 0 && e.ofstride % 16 == 0;
+  if (k && aligned && tile * g.C / 8 <= 256 &&
+      encode_frames_map(&tout, out, row_bytes, g.M, g.F, e.opitch, e.ofstride, tile * g.C, g.b)) {
+    e.tiles_per_row = (g.GC * g.b + tile - 1) / tile;
+    e.tensor_out_bytes = static_cast<int>(row_bytes / 8 * 8);
+    e.div_tiles = make_fastdiv(static_cast<uint32_t>(e.tiles_per_row));
+    e.div_rows = make_fastdiv(static_cast<uint32_t>(g.GR));
+    const int64_t units = static_cast<int64_t>(g.F) * g.GR * e.tiles_per_row;
+    const size_t smem = static_cast<size_t>(g.b) * tile * g.C;
+    const auto key = std::make_pair(reinterpret_cast<const void*>(k), smem);
+    if (ctx->occupancy.find(key) == ctx->occupancy.end()) {
+      CUDA_TRY(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+      ctx->occupancy[key] = 1;
+    }
+    if (units > 0x7FFFFFFF) return set_err(ctx, DPPX_ERR_INVALID, "batch too large for one launch");
+    CUDA_TRY(ctx, launch_expand_tma(k, tout, e, static_cast<int>(units), smem, ctx->stream));
+  } else {
+    CUDA_TRY(ctx, launch_expand(e, ctx->stream));
+  }
   timing_end(ctx, &pt);
   return DPPX_OK;
 }

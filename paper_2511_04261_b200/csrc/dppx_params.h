@@ -109,6 +109,10 @@ struct ExpandArgs {
   const uint32_t* totals;    // adaptive: [F*C]
   uint8_t* out;
   int64_t opitch, ofstride;
+  // K2 (staged) only
+  int tiles_per_row;
+  int tensor_out_bytes;
+  FastDiv div_tiles, div_rows;
 };
 
 }  // namespace dppx

@@ -825,6 +825,87 @@ __global__ void __launch_bounds__(kGenericThreads) k_expand(const ExpandArgs a) 
 }
 
 // ============================================================================
+// K2 fast path: one CTA per (frame, grid row, 512-px tile); each thread owns a
+// 4-px strip, looks up its cell's statistics per channel plane (packed slots
+// from K0's per-plane scan), writes the strip pattern into a smem tile and one
+// thread bulk-stores the tile with a 3-D TMA box (clipped at M and N).
+// ============================================================================
+template <int C, int B4, int NSUB, bool ADAPTIVE>
+__global__ void __launch_bounds__(kConsumers)
+    k_expand_tma(const __grid_constant__ CUtensorMap tm_out, const ExpandArgs a) {
+  constexpr int B = 4 * B4, SB = B / NSUB, SB4 = SB / 4, ROWB = kTilePx * C;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const BatchGeom& g = a.g;
+  const int t = threadIdx.x;
+  const int u = blockIdx.x;
+  const uint32_t rest = a.div_tiles.div(static_cast<uint32_t>(u));
+  const int tile = u - static_cast<int>(rest * a.div_tiles.d);
+  const uint32_t fq = a.div_rows.div(rest);
+  const int r = static_cast<int>(rest - fq * a.div_rows.d), f = static_cast<int>(fq);
+  const int px0 = tile * kTilePx;
+  const int cell = px0 / B + t / B4;
+  const int sc = (t % B4) / SB4;
+  const bool active = cell < g.GC;
+  const int gidx = r * g.GC + cell;
+  // value of vertical subcell vs for channel ch (simple cells: one value)
+  uint32_t val[NSUB][C];
+  if (active) {
+#pragma unroll
+    for (int ch = 0; ch < C; ++ch) {
+      const int64_t plane = static_cast<int64_t>(f) * C + ch;
+      const uint8_t* st = a.stats + plane * a.sstride;
+      if constexpr (!ADAPTIVE) {
+        const uint32_t v = __ldg(st + gidx);
+#pragma unroll
+        for (int vs = 0; vs < NSUB; ++vs) val[vs][ch] = v;
+      } else {
+        const uint32_t info = __ldg(&a.cellinfo[plane * g.G + gidx]);
+        const uint32_t slot_s = __ldg(&a.rowprefix[plane * g.GR + r]) + (info >> 1);
+        const int64_t base = 4ll * g.G + 4;
+        if (info & 1u) {
+          const uint32_t v = __ldg(st + base + slot_s);
+#pragma unroll
+          for (int vs = 0; vs < NSUB; ++vs) val[vs][ch] = v;
+        } else {
+          const uint8_t* sub = st + base + __ldg(&a.totals[plane]) +
+                               static_cast<int64_t>(static_cast<uint32_t>(gidx) - slot_s) * NSUB * NSUB;
+#pragma unroll
+          for (int vs = 0; vs < NSUB; ++vs) val[vs][ch] = __ldg(sub + vs * NSUB + sc);
+        }
+      }
+    }
+    uint8_t* mystrip = smem + t * 4 * C;
+#pragma unroll
+    for (int vs = 0; vs < NSUB; ++vs) {
+      uint32_t w[C];
+      pattern_words<C>(val[vs], w);
+#pragma unroll
+      for (int i = 0; i < SB; ++i)
+#pragma unroll
+        for (int q = 0; q < C; ++q) reinterpret_cast<uint32_t*>(mystrip + (vs * SB + i) * ROWB)[q] = w[q];
+    }
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  const int scopy = max(0, min(ROWB, a.tensor_out_bytes - px0 * C));
+  if (t == 0 && scopy > 0) {
+    tma_store_3d(&tm_out, px0 * C / 8, r * B, f, smem);
+    bulk_commit();
+  }
+  // bytes past the tensor's row extent
+  const int vbytes = min(kTilePx, g.N - px0) * C;
+  const int lx0 = t * 4 * C;
+  if (active && lx0 + 4 * C > scopy && lx0 < vbytes) {
+    const int rows = min(B, g.M - r * B);
+    for (int i = 0; i < rows; ++i)
+      for (int x = max(lx0, scopy); x < min(lx0 + 4 * C, vbytes); ++x)
+        a.out[static_cast<int64_t>(f) * a.ofstride + static_cast<int64_t>(r * B + i) * a.opitch +
+              static_cast<int64_t>(px0) * C + x] = smem[i * ROWB + x];
+  }
+  if (t == 0 && scopy > 0) bulk_wait_read_all();
+}
+
+// ============================================================================
 // Synthetic workload generator (mirrors oracle/dppx_oracle.c or_synth_*)
 // ============================================================================
 __device__ __forceinline__ uint32_t hash32(uint32_t x) {
@@ -958,6 +1039,41 @@ StatsKernel select_stats_kernel(int C, int b, int n, bool adaptive, bool packed)
     return adaptive ? pick_b<3, true, false>(b, n) : pick_b<3, false, false>(b, n);
   }
   return nullptr;
+}
+
+using ExpandKernel = void (*)(const CUtensorMap, const ExpandArgs);
+
+template <int C, bool AD>
+ExpandKernel pick_expand(int b, int n) {
+#define DPPX_CASE(B4v, NS) \
+  if (b == 4 * (B4v) && n == (NS)) return k_expand_tma<C, B4v, NS, AD>;
+  DPPX_CASE(1, 1)
+  DPPX_CASE(2, 1)
+  DPPX_CASE(4, 1)
+  DPPX_CASE(8, 1)
+  if constexpr (AD) {
+    DPPX_CASE(2, 2)
+    DPPX_CASE(4, 2)
+    DPPX_CASE(4, 4)
+    DPPX_CASE(8, 2)
+    DPPX_CASE(8, 4)
+    DPPX_CASE(8, 8)
+  }
+#undef DPPX_CASE
+  return nullptr;
+}
+
+ExpandKernel select_expand_kernel(int C, int b, int n, bool adaptive) {
+  if (!adaptive && n != 1) return nullptr;
+  if (C == 1) return adaptive ? pick_expand<1, true>(b, n) : pick_expand<1, false>(b, n);
+  if (C == 3) return adaptive ? pick_expand<3, true>(b, n) : pick_expand<3, false>(b, n);
+  return nullptr;
+}
+
+cudaError_t launch_expand_tma(ExpandKernel k, const CUtensorMap& tout, const ExpandArgs& a,
+                              int grid, size_t smem, cudaStream_t s) {
+  k<<<grid, kConsumers, smem, s>>>(tout, a);
+  return cudaGetLastError();
 }
 
 int stats_threads() { return kStatsThreads; }

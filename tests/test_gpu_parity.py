@@ -316,3 +316,22 @@ def test_narrow_frames_packed_per_unit(ctx, b, n, C):
     assert ctx.stats()["launches"]["stats_tma"] >= 1
     rp, ri = _oracle_adaptive(frames, masks, p, "keyed", seeds)
     assert pls == rp and np.array_equal(img, ri)
+
+
+@pytest.mark.parametrize("b,n,C", [(16, 4, 3), (32, 8, 3), (8, 2, 1), (4, 1, 3), (16, 1, 1)])
+def test_expand_fast_path(ctx, b, n, C):
+    """K2 (staged tile + TMA store) reconstructs payloads/means exactly like
+    the oracle's reassemble/broadcast, on padded and multi-tile shapes."""
+    for M, N in [(1080, 1920), (1083, 1917), (218, 178), (3 * b + 1, 7 * b + 5)]:
+        frames = oracle.synth_frames(2, 2, M, N, C)
+        masks = oracle.synth_masks(2, 2, M, N)
+        p = dp.make_privacy_params(0.5, 16, b, n)
+        seeds = dp.plane_seeds(1, 2, C)
+        pls, img = ctx.pixelize_adaptive(frames, masks, p, dp.NOISE_KEYED, seeds)
+        ctx.reset_stats()
+        out = ctx.reassemble(pls, M, N, b, n, channels=C, frames=2)
+        assert np.array_equal(out, img), (M, N)
+        if n == 1:
+            pu = dp.make_privacy_params(0.5, 16, b)
+            means, uimg = ctx.pixelize_uniform(frames, pu, dp.NOISE_KEYED, seeds)
+            assert np.array_equal(ctx.broadcast_means(means, M, N, b, channels=C, frames=2), uimg)
