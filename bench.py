@@ -239,13 +239,23 @@ def main():
     import paper_2511_04261_b200 as dp
     from paper_2511_04261_b200 import shard as sh
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # One process per GPU (LOCAL_RANK). DPPX_DIST_BACKEND=gloo + DPPX_FORCE_DEVICE
+    # exist only to exercise the multi-rank launcher on a single test GPU (the
+    # ranks never wait on each other's kernels).
+    gpu = int(os.environ.get("DPPX_FORCE_DEVICE", local))
+    backend = os.environ.get("DPPX_DIST_BACKEND", "nccl")
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
+    local = gpu
     pg = None
     if world > 1:
         import torch.distributed as tdist
-        tdist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            tdist.init_process_group("nccl", device_id=dev)
+        else:
+            tdist.init_process_group(backend)
         pg = tdist
+    red_dev = dev if backend == "nccl" else torch.device("cpu")
 
     def barrier():
         if pg:
@@ -255,7 +265,7 @@ def main():
     def allmax(x):
         if not pg:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=red_dev)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         return float(t.item())
 

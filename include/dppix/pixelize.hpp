@@ -20,6 +20,10 @@ struct GridMeans {
 double clip_intensity(double v);
 std::uint8_t quantize_intensity(double v);
 
+// Algorithm 1: no padding, border grids average only their real pixels.
+GrayImage pixelize_reference(const GrayImage& img, const PrivacyParams& params,
+                             const std::optional<NoiseSeed>& seed);
+
 struct UniformResult {
   GrayImage image;
   GridMeans means;

@@ -15,6 +15,7 @@
  *   dppix::laplace_at           noise.hpp:80             dppx_laplace_at (host diagnostic)
  *   dppix::pixelize_parallel    pixelize.hpp:55-58       dppx_pixelize_uniform[_dev]
  *   dppix::pixelize_adaptive    adaptive.hpp:70-73       dppx_pixelize_adaptive[_dev]
+ *   dppix::pixelize_reference   pixelize.hpp:45-46       dppx_pixelize_reference (Algorithm 1)
  *   dppix::broadcast_means      pixelize.hpp:62          dppx_broadcast_means[_dev]
  *   dppix::reassemble           adaptive.hpp:78          dppx_reassemble[_dev]
  *   dppix::reconstruct          record.hpp:63            dppx_reassemble / dppx_broadcast_means
@@ -189,6 +190,11 @@ int dppx_pixelize_adaptive(dppx_ctx* ctx, const dppx_frames_desc* desc, const ui
                            uint32_t* payload_len /* nullable */, uint8_t* out /* nullable */);
 int dppx_broadcast_means(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* means,
                          int32_t b, uint8_t* out);
+/* Algorithm 1 (pixelize.cpp:50-84): no padding, border cells average their real
+ * h x w pixels; means has one byte per cell like dppx_pixelize_uniform. */
+int dppx_pixelize_reference(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* img,
+                            const dppx_privacy_params* params, const dppx_noise* noise,
+                            uint8_t* means, uint8_t* out /* nullable */);
 int dppx_reassemble(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* payload,
                     int64_t payload_stride, const uint32_t* payload_len, int32_t b, int32_t n,
                     uint8_t* out);

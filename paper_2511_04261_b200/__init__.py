@@ -133,6 +133,7 @@ ABI = {
     "dppx_pixelize_adaptive": (C.c_int, [_ctxp, _descp, _vp, _vp, _pp, _np, _vp, C.c_int64, _vp,
                                          _vp]),
     "dppx_broadcast_means": (C.c_int, [_ctxp, _descp, _vp, C.c_int32, _vp]),
+    "dppx_pixelize_reference": (C.c_int, [_ctxp, _descp, _vp, _pp, _np, _vp, _vp]),
     "dppx_reassemble": (C.c_int, [_ctxp, _descp, _vp, C.c_int64, _vp, C.c_int32, C.c_int32, _vp]),
     "dppx_classify_regions": (C.c_int, [_ctxp, _descp, _vp, C.c_int32, _vp]),
     "dppx_crc32": (C.c_uint32, [C.c_uint32, _vp, C.c_size_t]),
@@ -403,6 +404,22 @@ class Context:
         del keep
         return [bytes(buf[i, : lens[i]]) for i in range(F * Cn)], out
 
+    def pixelize_reference(self, frames, params: PrivacyParams, noise=NOISE_NONE, seeds=None,
+                           frame_base=0):
+        """Algorithm 1 (pixelize.cpp:50-84). Returns (means[F*C, G], image)."""
+        frames = np.ascontiguousarray(frames, dtype=np.uint8)
+        F, M, N, Cn = _frames_shape(frames)
+        g = grid_dims(M, N, params.b)
+        means = np.zeros((F * Cn, g.grid_count()), np.uint8)
+        out = np.zeros_like(frames)
+        nz, keep = self._noise(noise, seeds, frame_base, None)
+        d = _desc(M, N, Cn, F)
+        self._check(_lib.dppx_pixelize_reference(self._h, C.byref(d), _ptr(frames), C.byref(params),
+                                                 C.byref(nz), _ptr(means), _ptr(out)),
+                    "pixelize_reference")
+        del keep
+        return means, out
+
     def broadcast_means(self, means, M, N, b, channels=1, frames=1):
         means = np.ascontiguousarray(means, dtype=np.uint8)
         out = np.zeros((frames, M, N, channels), np.uint8)
@@ -574,6 +591,17 @@ def pixelize_adaptive(img, mask, params: PrivacyParams, seed: Optional[int] = No
     return AdaptiveResult(out, parse_adaptive_payload(payloads[0], geom, params.n))
 
 
+def pixelize_reference(img, params: PrivacyParams, seed: Optional[int] = None) -> np.ndarray:
+    """pixelize_reference, Algorithm 1 (pixelize.cpp:50-84), on the GPU."""
+    img = _check_gray(img, "pixelize_reference")
+    if params.n != 1:
+        raise ValueError("pixelize_reference: requires n == 1")
+    _, out = default_context().pixelize_reference(
+        img, params, NOISE_KEYED if seed is not None else NOISE_NONE,
+        [seed] if seed is not None else None)
+    return out
+
+
 def broadcast_means(means: GridMeans, height: int, width: int) -> np.ndarray:
     """broadcast_means (pixelize.cpp:126-150)."""
     if height < 1 or width < 1:
@@ -686,7 +714,7 @@ __all__ = [
     "crc32", "encode_record", "encode", "decode", "reconstruct", "PixelRecord", "RecordInfo",
     "Context", "default_context", "grid_dims", "make_privacy_params", "sensitivity", "keyed_bits",
     "laplace_at", "derive_plane_seed", "plane_seeds", "adaptive_payload_capacity",
-    "pixelize_parallel", "pixelize_adaptive", "broadcast_means", "reassemble", "classify_regions",
+    "pixelize_parallel", "pixelize_adaptive", "pixelize_reference", "broadcast_means", "reassemble", "classify_regions",
     "parse_adaptive_payload", "GridMeans", "UniformResult", "AdaptiveMeans", "AdaptiveResult",
     "RegionClassification", "RecordError", "DeviceUnavailable", "PrivacyParams", "Geometry",
     "FramesDesc", "Noise", "ABI", "LIB_PATH", "DROPIN_PATH",

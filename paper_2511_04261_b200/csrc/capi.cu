@@ -438,10 +438,10 @@ int pixelize_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img, c
                  const dppx_privacy_params* pp, const dppx_noise* nz, const double* dev_injected,
                  uint8_t* stats, int64_t sstride, uint32_t* payload_len, uint8_t* out,
                  bool adaptive, DevBuf& dev_seeds, uint64_t*& pinned, size_t& pinned_n,
-                 cudaEvent_t guard, bool record_guard) {
+                 cudaEvent_t guard, bool record_guard, bool partial = false) {
   BatchGeom g;
   if (int rc = geometry(ctx, d->height, d->width, d->channels, d->frames, pp->b,
-                        adaptive ? pp->n : 1, &g, true))
+                        adaptive ? pp->n : 1, &g, !partial))
     return rc;
   if (d->frames == 0) return DPPX_OK;
   if (!img || !stats || (adaptive && !mask))
@@ -468,6 +468,7 @@ int pixelize_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img, c
   a.sigma = pp->sigma;
   a.sigma_sub = adaptive ? pp->sigma_sub : pp->sigma;
   a.exact_noise = ctx->exact_noise ? 1 : 0;
+  a.partial_borders = partial ? 1 : 0;
   if (int rc = prepare_noise(ctx, nz, g.F * g.C, dev_injected, g, pp, &a.noise, ctx->stream,
                              dev_seeds, pinned, pinned_n, guard, record_guard))
     return rc;
@@ -479,6 +480,13 @@ int pixelize_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img, c
     a.cellinfo = static_cast<const uint32_t*>(ctx->cellinfo.p);
     a.rowprefix = static_cast<const uint32_t*>(ctx->rowprefix.p);
     a.totals = static_cast<const uint32_t*>(ctx->totals.p);
+  }
+  if (partial) {  // Algorithm 1 has no staged fast path (a bench/oracle row)
+    PendingTiming pt;
+    timing_begin(ctx, DPPX_K_GENERIC, &pt);
+    CUDA_TRY(ctx, launch_stats_generic(a, ctx->stream));
+    timing_end(ctx, &pt);
+    return DPPX_OK;
   }
   return run_stats(ctx, a);
 }
@@ -579,13 +587,13 @@ cudaError_t copy_frames(void* dst, int64_t dpitch, int64_t dfs, const void* src,
   return cudaSuccess;
 }
 
-enum class HostOp { Uniform, Adaptive, Broadcast, Reassemble };
+enum class HostOp { Uniform, Adaptive, Broadcast, Reassemble, Reference };
 
 int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uint8_t* img,
                   const uint8_t* mask, const dppx_privacy_params* pp, const dppx_noise* nz,
                   uint8_t* stats, int64_t sstride, uint32_t* lens, const uint32_t* in_lens,
                   int b_arg, int n_arg, uint8_t* out) {
-  const bool pix = op == HostOp::Uniform || op == HostOp::Adaptive;
+  const bool pix = op == HostOp::Uniform || op == HostOp::Adaptive || op == HostOp::Reference;
   const bool adaptive = op == HostOp::Adaptive || op == HostOp::Reassemble;
   if (!d) return set_err(ctx, DPPX_ERR_INVALID, "null frames descriptor");
   const int b = pix ? (pp ? pp->b : 0) : b_arg;
@@ -602,7 +610,7 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
     g.n = n;
     g.sb = b / n;
   } else if (int rc = geometry(ctx, d->height, d->width, d->channels, d->frames, b,
-                               adaptive ? n : 1, &g, pix)) {
+                               adaptive ? n : 1, &g, pix && op != HostOp::Reference)) {
     return rc;
   }
   if (int rc = check_desc(ctx, d, op == HostOp::Adaptive, !pix || out != nullptr)) return rc;
@@ -760,7 +768,8 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
       rc = pixelize_dev(ctx, &dd, dimg, dmask, pp, nz ? &cn : nullptr,
                         inj ? static_cast<const double*>(ctx->inj[s].p) : nullptr, dstats, dstride,
                         adaptive ? dlens : nullptr, out ? dout : nullptr, adaptive, ctx->sd[s],
-                        ctx->sd_pinned[s], ctx->sd_pinned_n[s], ctx->comp_done[s], false);
+                        ctx->sd_pinned[s], ctx->sd_pinned_n[s], ctx->comp_done[s], false,
+                        op == HostOp::Reference);
     } else {
       rc = expand_dev(ctx, &dd, dstats, dstride, in_lens ? dlens : nullptr, b, n, dout, adaptive);
     }
@@ -1091,6 +1100,15 @@ int dppx_pixelize_adaptive(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8
   if (int rc = check_ctx(ctx)) return rc;
   return host_pipeline(ctx, HostOp::Adaptive, d, img, mask, pp, nz, payload, payload_stride,
                        payload_len, nullptr, 0, 0, out);
+}
+
+int dppx_pixelize_reference(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img,
+                            const dppx_privacy_params* pp, const dppx_noise* nz, uint8_t* means,
+                            uint8_t* out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (pp && pp->n != 1) return set_err(ctx, DPPX_ERR_INVALID, "pixelize_reference: requires n == 1");
+  return host_pipeline(ctx, HostOp::Reference, d, img, nullptr, pp, nz, means, 0, nullptr, nullptr, 0,
+                       1, out);
 }
 
 int dppx_broadcast_means(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* means, int32_t b,

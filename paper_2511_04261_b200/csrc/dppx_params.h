@@ -82,6 +82,8 @@ struct StatsArgs {
   double area, sub_area, sigma, sigma_sub;
   NoiseArgs noise;
   int exact_noise;           // 1: always evaluate the f64 reference arithmetic
+  int partial_borders;       // 1: Algorithm 1 (pixelize_reference): border cells average
+                             //    only their h x w real pixels, no mirror padding
   // K1 (staged) only
   int tiles_per_row;
   int units;

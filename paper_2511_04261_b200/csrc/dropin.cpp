@@ -272,6 +272,23 @@ UniformResult pixelize_parallel(const GrayImage& img, const PrivacyParams& param
   return res;
 }
 
+GrayImage pixelize_reference(const GrayImage& img, const PrivacyParams& params,
+                             const std::optional<NoiseSeed>& seed) {
+  check_image(img, "pixelize_reference");
+  if (params.n != 1) throw std::invalid_argument("pixelize_reference: requires n == 1");
+  const GridGeometry geom = grid_dims(img.height, img.width, params.b);
+  GrayImage out = make_image(img.height, img.width);
+  std::vector<std::uint8_t> means(geom.grid_count());
+  const dppx_frames_desc d = gray_desc(img.height, img.width);
+  const dppx_privacy_params p = to_c(params);
+  const std::uint64_t s = seed ? seed->value : 0;
+  dppx_noise nz{seed ? DPPX_NOISE_KEYED : DPPX_NOISE_NONE, 0, &s, nullptr};
+  check(dppx_pixelize_reference(thread_ctx(), &d, img.pixels.data(), &p, &nz, means.data(),
+                                out.pixels.data()),
+        "pixelize_reference");
+  return out;
+}
+
 GrayImage broadcast_means(const GridMeans& means, int height, int width) {
   if (height < 1 || width < 1) throw std::invalid_argument("broadcast_means: dimensions must be >= 1");
   const GridGeometry expected = grid_dims(height, width, means.geometry.b);

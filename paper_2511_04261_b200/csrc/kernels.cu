@@ -756,6 +756,31 @@ __global__ void __launch_bounds__(kGenericThreads) k_stats_generic(const StatsAr
     }
     const int nsub = simple ? 1 : g.n;
     const int side = simple ? g.b : g.sb;
+    if (a.partial_borders) {
+      // pixelize_reference (pixelize.cpp:50-84): the border cell (r, c) covers
+      // h x w real pixels, mean = sum / (h*w), noise keyed (r, c, 0, 0) at sigma.
+      const int i0 = r * g.b, j0 = c * g.b;
+      const int h = min(g.b, g.M - i0), w = min(g.b, g.N - j0);
+      const DrawEnv env = make_env(a.noise.kind, a.exact_noise != 0, static_cast<double>(h) * w,
+                                   a.sigma);
+      for (int ch = 0; ch < g.C; ++ch) {
+        uint32_t sum = 0;
+        for (int i = i0; i < i0 + h; ++i) {
+          const uint8_t* row = img + static_cast<int64_t>(i) * a.pitch;
+          for (int j = j0; j < j0 + w; ++j) sum += row[j * g.C + ch];
+        }
+        const uint32_t v = quantize_stat(env, sum, draw_bits(a, cell_state(a, f, ch, r, c), f, ch, r, c, 0, 0),
+                                         injected_at(a, f, ch, gidx, 0, 0));
+        a.stats[static_cast<int64_t>(f * g.C + ch) * a.sstride + gidx] = static_cast<uint8_t>(v);
+        if (a.out) {
+          uint8_t* o = a.out + static_cast<int64_t>(f) * a.ofstride;
+          for (int i = i0; i < i0 + h; ++i)
+            for (int j = j0; j < j0 + w; ++j)
+              o[static_cast<int64_t>(i) * a.opitch + j * g.C + ch] = static_cast<uint8_t>(v);
+        }
+      }
+      continue;
+    }
     const DrawEnv env = make_env(a.noise.kind, a.exact_noise != 0, simple ? a.area : a.sub_area,
                                  simple ? a.sigma : a.sigma_sub);
     for (int ch = 0; ch < g.C; ++ch) {

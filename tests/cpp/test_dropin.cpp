@@ -95,6 +95,18 @@ int main() {
     CHECK((a.means.complex_submeans == std::vector<std::uint8_t>{3, 5, 11, 13}));
     CHECK(a.image == expected);
   }
+  // Algorithm 1 == Algorithm 2 when grids tile the image (test_pixelize.cpp:92-106)
+  {
+    std::mt19937_64 rng(21);
+    for (int round = 0; round < 15; ++round) {
+      const int b = 1 << (rng() % 4);
+      const int h = b * (1 + static_cast<int>(rng() % 12)), w = b * (1 + static_cast<int>(rng() % 12));
+      const GrayImage img = random_image(rng, h, w);
+      const PrivacyParams p = make_privacy_params(0.5, 16, b);
+      const std::optional<NoiseSeed> seed = NoiseSeed{rng()};
+      CHECK(pixelize_reference(img, p, seed) == pixelize_parallel(img, p, seed).image);
+    }
+  }
   // constant image is a fixed point (test_pixelize.cpp:127-135)
   for (int b : {2, 3, 5}) {
     const GrayImage img = make_image(11, 13, 77);

@@ -49,3 +49,23 @@ def test_shaped_cases_rgb(ctx):
         for ch in range(3):
             plane = np.ascontiguousarray(img[0, :, :, ch])
             assert hashlib.sha256(plane.tobytes()).digest() == z[f"{name}_ch{ch}_imgsha"].tobytes()
+
+
+def test_algorithm1_reference_path(ctx):
+    """pixelize_reference (Algorithm 1, partial border grids) vs the reference
+    itself on the 40 golden cases, and == pixelize_parallel when b | M, N."""
+    z = np.load(os.path.join(G, "small_cases.npz"))
+    for k in sorted({k.split("_")[0] for k in z.files}):
+        M, N, b, n, m, has = (int(x) for x in z[f"{k}_params"])
+        eps = float(z[f"{k}_eps"][0])
+        seed = None if has < 0 else int(z[f"{k}_seed"][0])
+        out = dp.pixelize_reference(z[f"{k}_img"], dp.make_privacy_params(eps, m, b), seed)
+        assert np.array_equal(out, z[f"{k}_refimg"]), k
+    rng = np.random.default_rng(21)  # test_pixelize.cpp:92-106
+    for _ in range(10):
+        b = 1 << int(rng.integers(0, 4))
+        M, N = b * int(rng.integers(1, 13)), b * int(rng.integers(1, 13))
+        img = rng.integers(0, 256, (M, N), dtype=np.uint8)
+        p = dp.make_privacy_params(0.5, 16, b)
+        s = int(rng.integers(0, 2**62))
+        assert np.array_equal(dp.pixelize_reference(img, p, s), dp.pixelize_parallel(img, p, s).image)
