@@ -577,7 +577,6 @@ __global__ void __launch_bounds__(kStatsThreads)
     const Meta cur = next;
     const int u = cur.u;
     if (u < 0) break;
-    next = load_meta(k + 1);  // the producer publishes ids S-1 units ahead
     const UnitPos p = decode_unit<PACKED>(a, u);
     const int f = p.fg * units_pack<PACKED>(a) + jj;  // this thread's frame
     const int cell = PACKED ? (p.px0 + lpx) / B : p.px0 / B + t / B4;
@@ -689,6 +688,11 @@ __global__ void __launch_bounds__(kStatsThreads)
         }
       }
     }
+
+    // Next unit's metadata: requested here (after the staged rows are summed)
+    // rather than at the top, so a 2-stage ring never stalls on the producer's
+    // previous store; its latency hides behind this unit's epilogue.
+    next = load_meta(k + 1);
 
     // whole cell (uniform, or adaptive simple): reduce over B4 strips.
 #pragma unroll
