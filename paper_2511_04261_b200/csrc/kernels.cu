@@ -374,6 +374,28 @@ __device__ __forceinline__ void store_unit(const StatsArgs& a, const CUtensorMap
   bulk_wait_read_all();
 }
 
+// Output bytes of a unit past the output tensor map's row extent (< 8 per row:
+// the TMA store covers [0, tensor_out_bytes)), written by the 32 producer lanes.
+template <int C, int B, bool PACKED>
+__device__ __forceinline__ void store_tail(const StatsArgs& a, int u, const uint8_t* st, int lane) {
+  const UnitPos p = decode_unit<PACKED>(a, u);
+  const int srb = slot_px<PACKED>(a) * C;
+  const int vbytes = valid_bytes<C, PACKED>(a, p.px0);
+  const int scopy = max(0, min(srb, a.tensor_out_bytes - p.px0 * C));
+  if (scopy >= vbytes) return;
+  const int span = vbytes - scopy;
+  const int rows = min(B, a.g.M - p.r * B);
+  const int pk = units_pack<PACKED>(a);
+  const int nf = PACKED ? min(pk, a.g.F - p.fg * pk) : 1;
+  for (int e = lane; e < nf * rows * span; e += 32) {
+    const int jr = e / span, x = scopy + (e - jr * span);
+    const int j = jr / rows, i = jr - j * rows;
+    a.out[static_cast<int64_t>(p.fg * pk + j) * a.ofstride +
+          static_cast<int64_t>(p.r * B + i) * a.opitch + static_cast<int64_t>(p.px0) * C + x] =
+        st[j * a.slot_stride + i * srb + x];
+  }
+}
+
 // Byte k (0..4C-1) of a 4-pixel strip of value v[] (interleaved channels).
 template <int C>
 __device__ __forceinline__ void pattern_words(const uint32_t (&v)[C], uint32_t (&w)[C]) {
@@ -479,36 +501,47 @@ __global__ void __launch_bounds__(kStatsThreads)
     // ---------------- producer warp: TMA loads + bulk stores ----------------
     // Units (frame, grid row, 512-px tile) are claimed from a global counter so
     // heavy (complex-cell) tiles spread over all CTAs.
+    // The whole warp stays in the loop: lane 0 claims units and issues the TMA
+    // copies; all 32 lanes write the few output bytes past the output tensor
+    // map's row extent (keeps that byte loop off the consumer warps).
     if (lane == 0) {
       prefetch_tmap(&tm_in);
       prefetch_tmap(&tm_out);
-      int k = 0;
-      int done_units = 0;  // units of this CTA already stored
-      for (;; ++k) {
-        const int s = k % S;
-        if (k >= S) {
-          mbar_wait(&done_bar[s], ((k / S) - 1) & 1);
-          if (a.out) store_unit<C, B, PACKED>(a, &tm_out, stage_unit[s], smem + s * STAGE);
-          ++done_units;
-        }
-        int u = atomicAdd(a.work_counter, 1);
+    }
+    auto finish_unit = [&](int s, int use) {  // after consumers released stage s
+      mbar_wait(&done_bar[s], use & 1);        // every lane acquires the smem writes
+      if (a.out) {
+        const int uu = stage_unit[s];
+        store_tail<C, B, PACKED>(a, uu, smem + s * STAGE, lane);
+        if (lane == 0) store_unit<C, B, PACKED>(a, &tm_out, uu, smem + s * STAGE);
+      }
+      __syncwarp();
+    };
+    int k = 0;
+    int done_units = 0;  // units of this CTA already stored
+    for (;; ++k) {
+      const int s = k % S;
+      if (k >= S) {
+        finish_unit(s, (k / S) - 1);
+        ++done_units;
+      }
+      int u = 0;
+      if (lane == 0) {
+        u = atomicAdd(a.work_counter, 1);
         if (u >= a.units) u = -1;
         stage_unit[s] = u;
         mbar_arrive(&id_bar[s]);
-        if (u < 0) {
+        if (u < 0)
           mbar_arrive_expect_tx(&full_bar[s], 0);
-          break;
-        }
-        load_unit<C, B, PACKED>(a, &tm_in, u, smem + s * STAGE, &full_bar[s]);
+        else
+          load_unit<C, B, PACKED>(a, &tm_in, u, smem + s * STAGE, &full_bar[s]);
       }
-      // k units were loaded; units [done_units, k) still need their store.
-      for (int j = done_units; j < k; ++j) {
-        const int s = j % S;
-        mbar_wait(&done_bar[s], (j / S) & 1);
-        if (a.out) store_unit<C, B, PACKED>(a, &tm_out, stage_unit[s], smem + s * STAGE);
-      }
-      bulk_wait_all();
+      u = __shfl_sync(0xFFFFFFFFu, u, 0);
+      if (u < 0) break;
     }
+    // k units were loaded; units [done_units, k) still need their store.
+    for (int j = done_units; j < k; ++j) finish_unit(j % S, j / S);
+    if (lane == 0) bulk_wait_all();
     return;
   }
 
@@ -589,7 +622,6 @@ __global__ void __launch_bounds__(kStatsThreads)
     const uint32_t S_tot = cur.stot;
     const int vbytes = valid_bytes<C, PACKED>(a, p.px0);
     const int copy = staged_bytes<C, B, PACKED>(a, p);  // bytes per row the producer staged
-    const int scopy = max(0, min(srb, a.tensor_out_bytes - p.px0 * C));  // stored by TMA
     const int need = min(slot_px<PACKED>(a), g.GC * B - p.px0) * C;
     const int nf = PACKED ? min(a.pack, g.F - p.fg * a.pack) : 1;
     uint64_t cs[C];
@@ -719,17 +751,6 @@ __global__ void __launch_bounds__(kStatsThreads)
             for (int q = 0; q < C; ++q) reinterpret_cast<uint32_t*>(mystrip + i * srb)[q] = w[q];
         }
       }
-    }
-
-    // Output bytes past the tensor map's row extent are written here (the
-    // TMA store covers [0, scopy) of each slot row).
-    const int lx0 = lpx * C;
-    if (emit && active && lx0 + 4 * C > scopy && lx0 < vbytes) {
-      const int rows = min(B, g.M - p.r * B);
-      for (int i = 0; i < rows; ++i)
-        for (int x = max(lx0, scopy); x < min(lx0 + 4 * C, vbytes); ++x)
-          a.out[static_cast<int64_t>(f) * a.ofstride + static_cast<int64_t>(p.r * B + i) * a.opitch +
-                static_cast<int64_t>(p.px0) * C + x] = st[jj * a.slot_stride + i * srb + x];
     }
 
     fence_proxy_async_smem();
