@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -388,8 +389,12 @@ int run_stats(dppx_ctx* ctx, StatsArgs& a) {
     a.div_tiles = make_fastdiv(static_cast<uint32_t>(a.tiles_per_row));
     a.div_rows = make_fastdiv(static_cast<uint32_t>(g.GR));
     const size_t stage = static_cast<size_t>(g.b) * tile * g.C;
-    int S = static_cast<int>((72 * 1024) / stage);
-    S = std::max(2, std::min(stats_max_stages(), S));
+    // Two stages: measured best for every shape on B200 (a 2-deep ring per CTA
+    // with 4 CTAs/SM at b = 16 beats 3-4 deep rings with fewer CTAs; see
+    // profiles/r01_stage_sweep.md).
+    int S = 2;
+    if (const char* env = std::getenv("DPPX_STAGES"))  // tuning knob (2..4)
+      S = std::max(2, std::min(stats_max_stages(), std::atoi(env)));
     a.stages = S;
     const size_t smem = stage * S;
     const auto key = std::make_pair(reinterpret_cast<const void*>(k), smem);
