@@ -264,6 +264,7 @@ int prepare_noise(dppx_ctx* ctx, const dppx_noise* nz, int planes, const double*
   out->frame_base = nz ? nz->frame_base : 0;
   out->mixed_seeds = nullptr;
   out->injected = dev_injected;
+  out->inline_count = 0;
   if (out->kind == DPPX_NOISE_NONE) return DPPX_OK;
   if (out->kind < 0 || out->kind > DPPX_NOISE_INJECTED)
     return set_err(ctx, DPPX_ERR_INVALID, "unknown noise kind");
@@ -276,6 +277,14 @@ int prepare_noise(dppx_ctx* ctx, const dppx_noise* nz, int planes, const double*
     return set_err(ctx, DPPX_ERR_INVALID, "laplace_at: sigma must be > 0");
   if (!nz->plane_seeds) return set_err(ctx, DPPX_ERR_INVALID, "plane_seeds is null");
   const size_t cnt = out->kind == DPPX_NOISE_KEYED ? static_cast<size_t>(planes) : 1;
+  out->inline_count = 0;
+  if (cnt <= static_cast<size_t>(kInlineSeeds)) {  // small batches: seeds in the params
+    for (size_t i = 0; i < cnt; ++i)
+      out->inline_seeds[i] =
+          out->kind == DPPX_NOISE_KEYED ? mix64_h(nz->plane_seeds[i]) : nz->plane_seeds[i];
+    out->inline_count = static_cast<int>(cnt);
+    return DPPX_OK;
+  }
   if (guard) cudaEventSynchronize(guard);  // previous upload from `pinned` has executed
   if (pinned_n < cnt) {
     if (pinned) cudaFreeHost(pinned);
@@ -410,9 +419,9 @@ int run_stats(dppx_ctx* ctx, StatsArgs& a) {
       per_sm = it->second;
     }
     const int grid = static_cast<int>(std::min<int64_t>(units, static_cast<int64_t>(std::max(per_sm, 1)) * ctx->sms));
-    if (int rc = ensure(ctx, ctx->work, 16)) return rc;
+    // Zeroed once at allocation; each launch's last producer resets it.
+    if (int rc = ensure(ctx, ctx->work, 16, /*zero=*/true)) return rc;
     a.work_counter = static_cast<int*>(ctx->work.p);
-    CUDA_TRY(ctx, cudaMemsetAsync(ctx->work.p, 0, sizeof(int), ctx->stream));
     timing_begin(ctx, DPPX_K_STATS, &pt);
     CUDA_TRY(ctx, launch_stats_tma(k, tin, tout, a, grid, smem, ctx->stream));
   } else {

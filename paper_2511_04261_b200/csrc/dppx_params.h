@@ -37,11 +37,21 @@ struct BatchGeom {
   int GR, GC, G, PR, PC;  // grid_dims (image.cpp:48-72)
 };
 
+constexpr int kInlineSeeds = 48;  // planes whose seeds ride in the kernel parameters
+
 struct NoiseArgs {
   int kind;
   uint32_t frame_base;
   const uint64_t* mixed_seeds;  // device: KEYED mix64(seed) per plane; PHILOX [0]=seed
   const double* injected;       // device
+  int inline_count;             // > 0: seeds are in `inline_seeds` (no H2D copy per call)
+  uint64_t inline_seeds[kInlineSeeds];
+
+#ifdef __CUDACC__
+  __device__ __forceinline__ uint64_t seed(int64_t plane) const {
+    return inline_count > 0 ? inline_seeds[plane] : __ldg(&mixed_seeds[plane]);
+  }
+#endif
 };
 
 // K0: region classification + packed-slot scan.

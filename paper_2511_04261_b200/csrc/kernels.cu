@@ -250,7 +250,7 @@ __device__ __forceinline__ uint64_t draw_bits(const StatsArgs& a, uint64_t cs, i
                                               int c, int sr, int sc) {
   if (a.noise.kind == DPPX_NOISE_KEYED) return key_sub(cs, sr, sc);
   if (a.noise.kind == DPPX_NOISE_PHILOX)  // out of line: keeps the hot loop small
-    return philox_call(a.noise.mixed_seeds[0], a.noise.frame_base + f, ch, r, c, sr, sc);
+    return philox_call(a.noise.seed(0), a.noise.frame_base + f, ch, r, c, sr, sc);
   return 0ull;
 }
 
@@ -263,7 +263,7 @@ __device__ __forceinline__ double injected_at(const StatsArgs& a, int f, int ch,
 
 __device__ __forceinline__ uint64_t cell_state(const StatsArgs& a, int f, int ch, int r, int c) {
   return a.noise.kind == DPPX_NOISE_KEYED
-             ? key_cell(a.noise.mixed_seeds[static_cast<int64_t>(f) * a.g.C + ch], r, c)
+             ? key_cell(a.noise.seed(static_cast<int64_t>(f) * a.g.C + ch), r, c)
              : 0ull;
 }
 
@@ -528,7 +528,12 @@ __global__ void __launch_bounds__(kStatsThreads)
       int u = 0;
       if (lane == 0) {
         u = atomicAdd(a.work_counter, 1);
-        if (u >= a.units) u = -1;
+        if (u >= a.units) {
+          // Every producer makes exactly one failing claim; the last one resets
+          // the counter for the next launch (no memset per launch).
+          if (u == a.units + static_cast<int>(gridDim.x) - 1) atomicExch(a.work_counter, 0);
+          u = -1;
+        }
         stage_unit[s] = u;
         mbar_arrive(&id_bar[s]);
         if (u < 0)
@@ -597,7 +602,7 @@ __global__ void __launch_bounds__(kStatsThreads)
         if (a.noise.kind == DPPX_NOISE_KEYED) {
 #pragma unroll
           for (int ch = 0; ch < C; ++ch)
-            m.seed[ch] = __ldg(&a.noise.mixed_seeds[static_cast<int64_t>(qf) * C + ch]);
+            m.seed[ch] = a.noise.seed(static_cast<int64_t>(qf) * C + ch);
         }
       }
     }
