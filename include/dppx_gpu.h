@@ -21,6 +21,7 @@
  *   dppix::reconstruct          record.hpp:63            dppx_reassemble / dppx_broadcast_means
  *   dppix::classify_regions     adaptive.hpp:45-46       dppx_classify_regions
  *   dppix::encode / decode      record.hpp:55-61         dppx_encode_record / dppx_decode_record
+ *   dppix::mse / ssim           metrics.hpp:27-37        dppx_mse / dppx_ssim
  *   RecordError / invalid_argument  errors.hpp:22-55     dppx_status codes
  *
  * Conventions
@@ -221,6 +222,19 @@ int dppx_encode_record(int32_t height, int32_t width, int32_t b, int32_t n, int3
 /* decode's checks in order: NOT_A_RECORD, CORRUPT (truncated header), CORRUPTION
  * (CRC), UNSUPPORTED_VERSION, CORRUPT (mode/reserved/dims/fields/lengths/count). */
 int dppx_decode_record(const uint8_t* bytes, size_t len, dppx_record_info* info);
+
+/* ---- utility metrics (metrics.hpp:27-37, metrics.cpp:26-183) ------------- */
+/* Per channel plane (f, c) of frame batches a (pitch, frame_stride) and b
+ * (out_pitch, out_frame_stride); out[f*C + c]. Bit-identical to the reference:
+ * exact integer sums, the reference's f64 operation order, rows summed in order. */
+int dppx_mse(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* a, const uint8_t* b,
+             double* out);
+int dppx_ssim(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* a, const uint8_t* b,
+              double* out); /* 7x7 uniform window, C1 = 6.5025, C2 = 58.5225 */
+int dppx_mse_dev(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* a, const uint8_t* b,
+                 double* out);
+int dppx_ssim_dev(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* a, const uint8_t* b,
+                  double* out);
 
 /* Diagnostics for parity tests: the device noise of `count` keys
  * (keys[4*i..4*i+3] = r, c, sr, sc) for one plane seed at scale sigma. */

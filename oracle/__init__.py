@@ -88,6 +88,10 @@ lib.or_pixelize_reference.argtypes = [u8p, C.c_int, C.c_int, C.c_int, C.c_double
                                       C.c_uint64, u8p]
 lib.or_synth_frames.argtypes = [C.c_uint32, C.c_uint32, C.c_int, C.c_int, C.c_int, C.c_int,
                                 C.c_long, C.c_long, u8p]
+lib.or_mse.restype = C.c_double
+lib.or_mse.argtypes = [u8p, u8p, C.c_long]
+lib.or_ssim.restype = C.c_double
+lib.or_ssim.argtypes = [u8p, u8p, C.c_int, C.c_int]
 lib.or_synth_masks.argtypes = [C.c_uint32, C.c_int, C.c_int, C.c_int, C.c_long, C.c_long, u8p]
 
 
@@ -242,6 +246,18 @@ def synth_masks(f0, F, M, N):
     return out
 
 
+def mse(a, b):
+    a = np.ascontiguousarray(a, np.uint8)
+    b = np.ascontiguousarray(b, np.uint8)
+    return lib.or_mse(_p(a), _p(b), a.size)
+
+
+def ssim(a, b):
+    a = np.ascontiguousarray(a, np.uint8)
+    b = np.ascontiguousarray(b, np.uint8)
+    return lib.or_ssim(_p(a), _p(b), a.shape[0], a.shape[1])
+
+
 def parse_adaptive_payload(payload: bytes, G, n):
     """Split a DPPX adaptive payload into (mask_means f32[G], S, simple, complex)."""
     mm = np.frombuffer(payload[: 4 * G], "<f4")
@@ -282,6 +298,10 @@ class _Ref:
                                           u32p]
         L.ref_encode_uniform.argtypes = [u8p, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int,
                                          C.c_int, C.c_uint64, u8p, C.c_uint32, u32p]
+        L.ref_mse.restype = C.c_double
+        L.ref_mse.argtypes = [u8p, u8p, C.c_int, C.c_int]
+        L.ref_ssim.restype = C.c_double
+        L.ref_ssim.argtypes = [u8p, u8p, C.c_int, C.c_int, C.c_int]
         L.ref_time_planes.restype = C.c_double
         L.ref_time_planes.argtypes = [u8p, u8p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
                                       C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int]
@@ -377,6 +397,16 @@ class _Ref:
                                                 seed or 0, _p(buf), cap, C.byref(ln)),
                     "encode_uniform")
         return bytes(buf[: ln.value])
+
+    def mse(self, a, b):
+        a = np.ascontiguousarray(a, np.uint8)
+        b = np.ascontiguousarray(b, np.uint8)
+        return self.lib.ref_mse(_p(a), _p(b), a.shape[0], a.shape[1])
+
+    def ssim(self, a, b, threads=1):
+        a = np.ascontiguousarray(a, np.uint8)
+        b = np.ascontiguousarray(b, np.uint8)
+        return self.lib.ref_ssim(_p(a), _p(b), a.shape[0], a.shape[1], threads)
 
     def time_planes(self, planes, masks, uniform, eps, m, b, n, seed, workers):
         planes = np.ascontiguousarray(planes, np.uint8)

@@ -481,3 +481,51 @@ void or_synth_masks(uint32_t f0, int F, int M, int N, long pitch, long frame_str
         dst[(size_t)f * frame_stride + (size_t)i * pitch + j] =
             or_synth_mask(f0 + (uint32_t)f, M, N, i, j);
 }
+
+/* ---- utility metrics (next row) ------------------------------ */
+
+/* mse: metrics.cpp:26-37 (exact u64 sum of squared differences, one divide). */
+double or_mse(const uint8_t* a, const uint8_t* b, long n) {
+  uint64_t s = 0;
+  for (long i = 0; i < n; ++i) {
+    const int64_t d = (int64_t)a[i] - b[i];
+    s += (uint64_t)(d * d);
+  }
+  return (double)s / (double)n;
+}
+
+/* ssim: metrics.cpp:73-183. Window sums are exact integers (the reference's
+ * summed-area tables give the same integers); the per-window f64 sequence and
+ * the row-ordered accumulation follow metrics.cpp:144-182. */
+double or_ssim(const uint8_t* a, const uint8_t* b, int M, int N) {
+  const int W = 7;
+  const double area = 49.0, c1 = 6.5025, c2 = 58.5225;
+  if (M < W || N < W) return -1.0;
+  const int pr = M - W + 1, pc = N - W + 1;
+  double total = 0.0;
+  for (int i = 0; i < pr; ++i) {
+    double acc = 0.0;
+    for (int j = 0; j < pc; ++j) {
+      uint64_t sa = 0, sb = 0, saa = 0, sbb = 0, sab = 0;
+      for (int y = i; y < i + W; ++y)
+        for (int x = j; x < j + W; ++x) {
+          const uint64_t va = a[(size_t)y * N + x], vb = b[(size_t)y * N + x];
+          sa += va;
+          sb += vb;
+          saa += va * va;
+          sbb += vb * vb;
+          sab += va * vb;
+        }
+      const double mu_a = (double)sa / area, mu_b = (double)sb / area;
+      const double raw_aa = (double)saa / area, raw_bb = (double)sbb / area,
+                   raw_ab = (double)sab / area;
+      const double mu_aa = mu_a * mu_a, mu_bb = mu_b * mu_b, mu_ab = mu_a * mu_b;
+      const double var_a = raw_aa - mu_aa, var_b = raw_bb - mu_bb, cov = raw_ab - mu_ab;
+      const double num = (2.0 * mu_ab + c1) * (2.0 * cov + c2);
+      const double den = ((mu_aa + mu_bb) + c1) * ((var_a + var_b) + c2);
+      acc += num / den;
+    }
+    total += acc;
+  }
+  return total / ((double)pr * pc);
+}

@@ -21,6 +21,7 @@
 #include "dppix/adaptive.hpp"
 #include "dppix/errors.hpp"
 #include "dppix/image.hpp"
+#include "dppix/metrics.hpp"
 #include "dppix/noise.hpp"
 #include "dppix/pixelize.hpp"
 #include "dppix/record.hpp"
@@ -213,6 +214,24 @@ int ref_encode_uniform(const uint8_t* img, int M, int N, double eps, int m, int 
     std::memcpy(out, bytes.data(), bytes.size());
     *len = static_cast<uint32_t>(bytes.size());
   });
+}
+
+double ref_mse(const uint8_t* a, const uint8_t* b, int M, int N) {
+  try {
+    return dppix::mse(to_image(a, M, N), to_image(b, M, N));
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1.0;
+  }
+}
+
+double ref_ssim(const uint8_t* a, const uint8_t* b, int M, int N, int threads) {
+  try {
+    return dppix::ssim(to_image(a, M, N), to_image(b, M, N), threads);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1.0;
+  }
 }
 
 // CPU baseline timing: `planes` gray planes (already de-interleaved upstream,

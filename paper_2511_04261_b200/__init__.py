@@ -136,6 +136,10 @@ ABI = {
     "dppx_pixelize_reference": (C.c_int, [_ctxp, _descp, _vp, _pp, _np, _vp, _vp]),
     "dppx_reassemble": (C.c_int, [_ctxp, _descp, _vp, C.c_int64, _vp, C.c_int32, C.c_int32, _vp]),
     "dppx_classify_regions": (C.c_int, [_ctxp, _descp, _vp, C.c_int32, _vp]),
+    "dppx_mse": (C.c_int, [_ctxp, _descp, _vp, _vp, _vp]),
+    "dppx_ssim": (C.c_int, [_ctxp, _descp, _vp, _vp, _vp]),
+    "dppx_mse_dev": (C.c_int, [_ctxp, _descp, _vp, _vp, _vp]),
+    "dppx_ssim_dev": (C.c_int, [_ctxp, _descp, _vp, _vp, _vp]),
     "dppx_crc32": (C.c_uint32, [C.c_uint32, _vp, C.c_size_t]),
     "dppx_record_size": (C.c_size_t, [C.c_size_t]),
     "dppx_encode_record": (C.c_int, [C.c_int32] * 5 + [_vp, C.c_size_t, _vp, C.c_size_t,
@@ -455,6 +459,19 @@ class Context:
                     "classify_regions")
         return mm
 
+    def metrics(self, a, b, which="ssim"):
+        """mse / ssim per channel plane of two frame batches ([F,M,N,C] or [M,N])."""
+        a = np.ascontiguousarray(a, dtype=np.uint8)
+        b = np.ascontiguousarray(b, dtype=np.uint8)
+        if a.shape != b.shape:
+            raise ValueError(f"{which}: images must share dimensions")
+        F, M, N, Cn = _frames_shape(a)
+        out = np.zeros(F * Cn, np.float64)
+        d = _desc(M, N, Cn, F)
+        fn = _lib.dppx_ssim if which == "ssim" else _lib.dppx_mse
+        self._check(fn(self._h, C.byref(d), _ptr(a), _ptr(b), _ptr(out)), which)
+        return out
+
     def device_laplace(self, seed, keys, sigma):
         keys = np.ascontiguousarray(np.asarray(keys, np.uint32).reshape(-1, 4))
         out = np.zeros(len(keys), np.float64)
@@ -639,6 +656,22 @@ def reassemble(means: AdaptiveMeans, height: int, width: int) -> np.ndarray:
     return default_context().reassemble([payload], height, width, geom.b, n)[0, :, :, 0]
 
 
+def mse(a, b) -> float:
+    """mse (metrics.cpp:26-37) on the GPU."""
+    a, b = np.asarray(a), np.asarray(b)
+    if a.shape != b.shape or a.ndim != 2 or a.size == 0:
+        raise ValueError("mse: images must share valid dimensions")
+    return float(default_context().metrics(a, b, "mse")[0])
+
+
+def ssim(a, b, threads: int = 0) -> float:
+    """ssim (metrics.cpp:73-183) on the GPU; `threads` is ignored."""
+    a, b = np.asarray(a), np.asarray(b)
+    if a.shape != b.shape or a.ndim != 2:
+        raise ValueError("ssim: images must share dimensions")
+    return float(default_context().metrics(a, b, "ssim")[0])
+
+
 def classify_regions(mask, geom: Geometry) -> RegionClassification:
     """classify_regions (adaptive.cpp:34-65) on the GPU."""
     mask = np.asarray(mask)
@@ -711,7 +744,7 @@ def reconstruct(record: PixelRecord) -> np.ndarray:
 
 
 __all__ = [
-    "crc32", "encode_record", "encode", "decode", "reconstruct", "PixelRecord", "RecordInfo",
+    "mse", "ssim", "crc32", "encode_record", "encode", "decode", "reconstruct", "PixelRecord", "RecordInfo",
     "Context", "default_context", "grid_dims", "make_privacy_params", "sensitivity", "keyed_bits",
     "laplace_at", "derive_plane_seed", "plane_seeds", "adaptive_payload_capacity",
     "pixelize_parallel", "pixelize_adaptive", "pixelize_reference", "broadcast_means", "reassemble", "classify_regions",

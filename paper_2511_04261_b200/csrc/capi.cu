@@ -40,6 +40,16 @@ cudaError_t launch_synth(const BatchGeom& g, uint32_t seed, uint32_t f0, uint8_t
                          int64_t pitch, int64_t fstride, uint8_t* mask, int64_t mpitch,
                          int64_t mfstride, cudaStream_t s);
 cudaError_t launch_debug_lg2(unsigned int* out, cudaStream_t s);
+struct MetricArgs {
+  int M, N, C, F;
+  const uint8_t* a;
+  int64_t pitch, fstride;
+  const uint8_t* b;
+  int64_t bpitch, bfstride;
+  unsigned long long* sums;
+  double* row_sums;
+};
+cudaError_t launch_metrics(const MetricArgs& m, bool ssim, cudaStream_t s);
 cudaError_t launch_repitch(uint8_t* dst, int64_t dpitch, const uint8_t* src, int64_t spitch,
                            int64_t width, int64_t rows, cudaStream_t s);
 cudaError_t launch_debug_laplace(uint64_t mixed, const uint32_t* keys, int count, double sigma,
@@ -88,7 +98,7 @@ struct dppx_ctx {
   cudaStream_t s_in = nullptr, s_out = nullptr;
   std::string err;
   // scratch
-  DevBuf cellinfo, rowcnt, rowprefix, totals, counters, status, seeds, keys, dbl, work;
+  DevBuf cellinfo, rowcnt, rowprefix, totals, counters, status, seeds, keys, dbl, work, met_a, met_b, met_out;
   uint64_t* seeds_pinned = nullptr;
   size_t seeds_pinned_n = 0;
   cudaEvent_t seeds_ev = nullptr;
@@ -948,7 +958,8 @@ void dppx_ctx_destroy(dppx_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
   DevBuf* bufs[] = {&ctx->cellinfo, &ctx->rowcnt, &ctx->rowprefix, &ctx->totals, &ctx->counters,
-                    &ctx->status, &ctx->seeds, &ctx->keys, &ctx->dbl, &ctx->work};
+                    &ctx->status, &ctx->seeds, &ctx->keys, &ctx->dbl, &ctx->work,
+                    &ctx->met_a, &ctx->met_b, &ctx->met_out};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (int s = 0; s < 2; ++s) {
@@ -1187,6 +1198,103 @@ int dppx_debug_device_laplace(dppx_ctx* ctx, uint64_t seed, const uint32_t* keys
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   CUDA_TRY(ctx, cudaMemcpy(out, ctx->dbl.p, sizeof(double) * count, cudaMemcpyDeviceToHost));
   return DPPX_OK;
+}
+
+// ---- utility metrics (metrics.cpp:26-183) ----------------------------------
+namespace {
+int metric_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* a, const uint8_t* b,
+               bool ssim, double* out) {
+  if (!d || !a || !b || !out) return set_err(ctx, DPPX_ERR_INVALID, "null argument");
+  const int M = d->height, N = d->width, C = d->channels, F = d->frames;
+  if (M < 1 || N < 1 || C < 1 || C > 4 || F < 0)
+    return set_err(ctx, DPPX_ERR_INVALID, ssim ? "ssim: images must share dimensions"
+                                               : "mse: images must share valid dimensions");
+  if (ssim && (M < 7 || N < 7))
+    return set_err(ctx, DPPX_ERR_INVALID, "ssim: images smaller than the 7x7 window");
+  if (F == 0) return DPPX_OK;
+  MetricArgs m{M, N, C, F, a, d->pitch, d->frame_stride, b, d->out_pitch, d->out_frame_stride,
+               nullptr, nullptr};
+  const int64_t P = static_cast<int64_t>(F) * C;
+  const int64_t pr = M - 6;
+  if (int rc = ensure(ctx, ctx->met_out, static_cast<size_t>(ssim ? P * pr * 8 : P * 8))) return rc;
+  if (ssim) {
+    m.row_sums = static_cast<double*>(ctx->met_out.p);
+  } else {
+    m.sums = static_cast<unsigned long long*>(ctx->met_out.p);
+    CUDA_TRY(ctx, cudaMemsetAsync(m.sums, 0, P * 8, ctx->stream));
+  }
+  PendingTiming pt;
+  timing_begin(ctx, DPPX_K_AUX, &pt);
+  CUDA_TRY(ctx, launch_metrics(m, ssim, ctx->stream));
+  timing_end(ctx, &pt);
+  if (ssim) {
+    std::vector<double> rows(static_cast<size_t>(P * pr));
+    CUDA_TRY(ctx, cudaMemcpyAsync(rows.data(), m.row_sums, rows.size() * 8, cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    const double positions = static_cast<double>(pr) * (N - 6);
+    for (int64_t p = 0; p < P; ++p) {  // row partials summed in row order (metrics.cpp:178-182)
+      double total = 0.0;
+      for (int64_t i = 0; i < pr; ++i) total += rows[p * pr + i];
+      out[p] = total / positions;
+    }
+  } else {
+    std::vector<unsigned long long> sums(static_cast<size_t>(P));
+    CUDA_TRY(ctx, cudaMemcpyAsync(sums.data(), m.sums, P * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    for (int64_t p = 0; p < P; ++p)
+      out[p] = static_cast<double>(sums[p]) / static_cast<double>(static_cast<int64_t>(M) * N);
+  }
+  if (ctx->timing) collect_timings(ctx);
+  return DPPX_OK;
+}
+
+int metric_host(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* a, const uint8_t* b,
+                bool ssim, double* out) {
+  if (!d || !a || !b || !out) return set_err(ctx, DPPX_ERR_INVALID, "null argument");
+  if (d->height < 1 || d->width < 1 || d->channels < 1 || d->channels > 4 || d->frames < 0)
+    return set_err(ctx, DPPX_ERR_INVALID, "metrics: invalid dimensions");
+  const int M = d->height, F = d->frames;
+  const int64_t row = static_cast<int64_t>(d->width) * d->channels;
+  if (d->pitch < row || d->out_pitch < row)
+    return set_err(ctx, DPPX_ERR_INVALID, "metrics: pitch too small");
+  const int64_t fs = row * M;
+  if (int rc = ensure(ctx, ctx->met_a, static_cast<size_t>(fs * F))) return rc;
+  if (int rc = ensure(ctx, ctx->met_b, static_cast<size_t>(fs * F))) return rc;
+  CUDA_TRY(ctx, copy_frames(ctx->met_a.p, row, fs, a, d->pitch, d->frame_stride, row, M, F,
+                            cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, copy_frames(ctx->met_b.p, row, fs, b, d->out_pitch, d->out_frame_stride, row, M, F,
+                            cudaMemcpyHostToDevice, ctx->stream));
+  dppx_frames_desc dd = *d;
+  dd.pitch = dd.out_pitch = row;
+  dd.frame_stride = dd.out_frame_stride = fs;
+  return metric_dev(ctx, &dd, static_cast<const uint8_t*>(ctx->met_a.p),
+                    static_cast<const uint8_t*>(ctx->met_b.p), ssim, out);
+}
+}  // namespace
+
+int dppx_mse(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* a, const uint8_t* b,
+             double* out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  return metric_host(ctx, d, a, b, false, out);
+}
+
+int dppx_ssim(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* a, const uint8_t* b,
+              double* out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  return metric_host(ctx, d, a, b, true, out);
+}
+
+int dppx_mse_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* a, const uint8_t* b,
+                 double* out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  return metric_dev(ctx, d, a, b, false, out);
+}
+
+int dppx_ssim_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* a, const uint8_t* b,
+                  double* out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  return metric_dev(ctx, d, a, b, true, out);
 }
 
 int dppx_debug_lg2_max_error(dppx_ctx* ctx, double* out) {

@@ -5,6 +5,7 @@
 // reassembly run on the GPU; a missing or unusable device raises
 // std::runtime_error (there is no CPU fallback).
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <fstream>
 #include <iterator>
@@ -17,6 +18,7 @@
 #include "dppix/adaptive.hpp"
 #include "dppix/errors.hpp"
 #include "dppix/image.hpp"
+#include "dppix/metrics.hpp"
 #include "dppix/noise.hpp"
 #include "dppix/pixelize.hpp"
 #include "dppix/record.hpp"
@@ -528,6 +530,47 @@ void write_record(const PixelRecord& record, const std::string& path) {
   out.write(reinterpret_cast<const char*>(bytes.data()), static_cast<std::streamsize>(bytes.size()));
   out.flush();
   if (!out) throw IoError("write_record: write failed for " + path);
+}
+
+// -------------------------------------------------------------- metrics.hpp
+namespace {
+double metric(const GrayImage& a, const GrayImage& b, bool ssim_metric) {
+  const char* who = ssim_metric ? "ssim" : "mse";
+  if (!a.same_dims(b) || a.height < 1 || a.width < 1)
+    throw std::invalid_argument(std::string(who) +
+                                (ssim_metric ? ": images must share dimensions"
+                                             : ": images must share valid dimensions"));
+  if (ssim_metric && (a.height < 7 || a.width < 7))
+    throw std::invalid_argument("ssim: images smaller than the 7x7 window");
+  dppx_frames_desc d = gray_desc(a.height, a.width);
+  double out = 0.0;
+  const int rc = ssim_metric ? dppx_ssim(thread_ctx(), &d, a.pixels.data(), b.pixels.data(), &out)
+                             : dppx_mse(thread_ctx(), &d, a.pixels.data(), b.pixels.data(), &out);
+  check(rc, who);
+  return out;
+}
+}  // namespace
+
+double mse(const GrayImage& a, const GrayImage& b) { return metric(a, b, false); }
+
+double ssim(const GrayImage& a, const GrayImage& b, int /*threads*/) { return metric(a, b, true); }
+
+std::string format_double(double value) {  // metrics.cpp:185-194 semantics
+  char buf[40];
+  for (const int precision : {15, 16, 17}) {
+    std::snprintf(buf, sizeof(buf), "%.*g", precision, value);
+    if (std::strtod(buf, nullptr) == value) break;
+  }
+  return buf;
+}
+
+std::string csv_header() { return "epsilon,m,b,n,seed,mse,ssim,runtime_ms,record_bytes"; }
+
+std::string csv_row(const MetricReport& r) {
+  return format_double(r.epsilon) + ',' + std::to_string(r.m) + ',' + std::to_string(r.b) + ',' +
+         std::to_string(r.n) + ',' + std::to_string(r.seed) + ',' + format_double(r.mse) + ',' +
+         format_double(r.ssim) + ',' + format_double(r.runtime_ms) + ',' +
+         std::to_string(r.record_bytes);
 }
 
 }  // namespace dppix

@@ -961,6 +961,124 @@ __global__ void __launch_bounds__(kConsumers)
 }
 
 // ============================================================================
+// Utility metrics: mse / ssim of metrics.cpp:26-183, per
+// channel plane of interleaved frames a (pitch/fstride) and b (opitch/ofstride).
+// ============================================================================
+struct MetricArgs {
+  int M, N, C, F;
+  const uint8_t* a;
+  int64_t pitch, fstride;
+  const uint8_t* b;
+  int64_t bpitch, bfstride;
+  unsigned long long* sums;  // mse: [F*C] exact u64 sums of squared differences
+  double* row_sums;          // ssim: [F*C][M-6] per-window-row partials
+};
+
+// Exact SSD per plane: one block per (frame, row band), byte channels by offset.
+__global__ void __launch_bounds__(256) k_mse(const MetricArgs m) {
+  __shared__ unsigned long long part[4];
+  if (threadIdx.x < 4) part[threadIdx.x] = 0ull;
+  __syncthreads();
+  unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};
+  const int rows_per_block = 8;
+  const int f = blockIdx.y;
+  const int row_bytes = m.N * m.C;
+  for (int i = blockIdx.x * rows_per_block; i < min(m.M, (blockIdx.x + 1) * rows_per_block); ++i) {
+    const uint8_t* ra = m.a + static_cast<int64_t>(f) * m.fstride + static_cast<int64_t>(i) * m.pitch;
+    const uint8_t* rb = m.b + static_cast<int64_t>(f) * m.bfstride + static_cast<int64_t>(i) * m.bpitch;
+    for (int x = threadIdx.x; x < row_bytes; x += blockDim.x) {
+      const int d = static_cast<int>(__ldg(ra + x)) - static_cast<int>(__ldg(rb + x));
+      const int ch = m.C == 1 ? 0 : x % m.C;
+      acc[ch] += static_cast<unsigned long long>(d * d);
+    }
+  }
+  for (int ch = 0; ch < m.C; ++ch) atomicAdd(&part[ch], acc[ch]);
+  __syncthreads();
+  if (threadIdx.x < m.C) atomicAdd(&m.sums[f * m.C + threadIdx.x], part[threadIdx.x]);
+}
+
+// One thread per (plane, window row): slides the 7x7 window along the row with
+// exact integer column sums and accumulates the local SSIM in the reference's
+// order (metrics.cpp:144-177): the row partial is bit-identical.
+__global__ void __launch_bounds__(128) k_ssim_rows(const MetricArgs m) {
+  constexpr int W = 7;
+  const int pr = m.M - W + 1, pc = m.N - W + 1;
+  const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t planes = static_cast<int64_t>(m.F) * m.C;
+  if (idx >= planes * pr) return;
+  const int64_t p = idx / pr;
+  const int i = static_cast<int>(idx - p * pr);
+  const int f = static_cast<int>(p / m.C), ch = static_cast<int>(p - static_cast<int64_t>(f) * m.C);
+  const uint8_t* a = m.a + static_cast<int64_t>(f) * m.fstride + static_cast<int64_t>(i) * m.pitch + ch;
+  const uint8_t* b = m.b + static_cast<int64_t>(f) * m.bfstride + static_cast<int64_t>(i) * m.bpitch + ch;
+  uint32_t ring[W][5];
+  uint32_t win[5] = {0u, 0u, 0u, 0u, 0u};
+  auto column = [&](int c, uint32_t (&out)[5]) {
+    uint32_t s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0;
+#pragma unroll
+    for (int y = 0; y < W; ++y) {
+      const uint32_t va = __ldg(a + static_cast<int64_t>(y) * m.pitch + static_cast<int64_t>(c) * m.C);
+      const uint32_t vb = __ldg(b + static_cast<int64_t>(y) * m.bpitch + static_cast<int64_t>(c) * m.C);
+      s0 += va;
+      s1 += vb;
+      s2 += va * va;
+      s3 += vb * vb;
+      s4 += va * vb;
+    }
+    out[0] = s0, out[1] = s1, out[2] = s2, out[3] = s3, out[4] = s4;
+  };
+#pragma unroll
+  for (int c = 0; c < W; ++c) {
+    column(c, ring[c]);
+#pragma unroll
+    for (int q = 0; q < 5; ++q) win[q] += ring[c][q];
+  }
+  const double area = 49.0, c1 = 6.5025, c2 = 58.5225;
+  double acc = 0.0;
+  for (int j = 0; j < pc; ++j) {
+    if (j > 0) {  // slide: drop column j-1, add column j+6 (ring slot (j-1) % 7)
+      const int slot = (j - 1) % W;
+      uint32_t nc[5];
+      column(j + W - 1, nc);
+#pragma unroll
+      for (int k = 0; k < W; ++k)
+        if (k == slot) {
+#pragma unroll
+          for (int q = 0; q < 5; ++q) {
+            win[q] = win[q] - ring[k][q] + nc[q];
+            ring[k][q] = nc[q];
+          }
+        }
+    }
+    const double mu_a = __ddiv_rn(static_cast<double>(win[0]), area);
+    const double mu_b = __ddiv_rn(static_cast<double>(win[1]), area);
+    const double raw_aa = __ddiv_rn(static_cast<double>(win[2]), area);
+    const double raw_bb = __ddiv_rn(static_cast<double>(win[3]), area);
+    const double raw_ab = __ddiv_rn(static_cast<double>(win[4]), area);
+    const double mu_aa = __dmul_rn(mu_a, mu_a), mu_bb = __dmul_rn(mu_b, mu_b),
+                 mu_ab = __dmul_rn(mu_a, mu_b);
+    const double var_a = __dsub_rn(raw_aa, mu_aa), var_b = __dsub_rn(raw_bb, mu_bb),
+                 cov = __dsub_rn(raw_ab, mu_ab);
+    const double num = __dmul_rn(__dadd_rn(__dmul_rn(2.0, mu_ab), c1), __dadd_rn(__dmul_rn(2.0, cov), c2));
+    const double den = __dmul_rn(__dadd_rn(__dadd_rn(mu_aa, mu_bb), c1),
+                                 __dadd_rn(__dadd_rn(var_a, var_b), c2));
+    acc = __dadd_rn(acc, __ddiv_rn(num, den));
+  }
+  m.row_sums[p * pr + i] = acc;
+}
+
+cudaError_t launch_metrics(const MetricArgs& m, bool ssim, cudaStream_t s) {
+  if (!ssim) {
+    dim3 grid((m.M + 7) / 8, m.F);
+    k_mse<<<grid, 256, 0, s>>>(m);
+  } else {
+    const int64_t threads = static_cast<int64_t>(m.F) * m.C * (m.M - 6);
+    k_ssim_rows<<<static_cast<unsigned>((threads + 127) / 128), 128, 0, s>>>(m);
+  }
+  return cudaGetLastError();
+}
+
+// ============================================================================
 // Synthetic workload generator (mirrors oracle/dppx_oracle.c or_synth_*)
 // ============================================================================
 __device__ __forceinline__ uint32_t hash32(uint32_t x) {

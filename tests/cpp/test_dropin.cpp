@@ -15,6 +15,7 @@
 #include "dppix/image.hpp"
 #include "dppix/noise.hpp"
 #include "dppix/pixelize.hpp"
+#include "dppix/metrics.hpp"
 #include "dppix/record.hpp"
 
 using namespace dppix;
@@ -274,6 +275,19 @@ int main() {
     } catch (const RecordError& e) {
       CHECK(e.kind() == RecordErrorKind::corruption);
     }
+  }
+  // metrics (test_metrics.cpp:32-117): KATs and symmetry
+  {
+    GrayImage a = make_image(8, 8, 0), b = make_image(8, 8, 255);
+    CHECK(mse(a, b) == 65025.0);
+    CHECK(mse(a, a) == 0.0);
+    std::mt19937_64 rng(51);
+    const GrayImage x = random_image(rng, 40, 50), y = random_image(rng, 40, 50);
+    CHECK(ssim(x, x) == 1.0);
+    CHECK(ssim(x, y) == ssim(y, x));
+    CHECK(ssim(x, y, 1) == ssim(x, y, 8));
+    CHECK_THROWS_AS(ssim(make_image(6, 9), make_image(6, 9)), std::invalid_argument);
+    CHECK(csv_header() == "epsilon,m,b,n,seed,mse,ssim,runtime_ms,record_bytes");
   }
   std::printf("%d passed, %d failed\n", g_pass, g_fail);
   return g_fail == 0 ? 0 : 1;

@@ -69,3 +69,28 @@ def test_algorithm1_reference_path(ctx):
         p = dp.make_privacy_params(0.5, 16, b)
         s = int(rng.integers(0, 2**62))
         assert np.array_equal(dp.pixelize_reference(img, p, s), dp.pixelize_parallel(img, p, s).image)
+
+
+def test_metrics_bit_identical_to_reference(ctx):
+    """mse / ssim on the GPU == the reference's metrics.cpp (via the oracle,
+    pinned to the reference in tests/test_oracle_vs_ref.py), bit for bit."""
+    rng = np.random.default_rng(17)
+    for M, N in [(7, 7), (19, 33), (218, 178), (576, 768)]:
+        a = rng.integers(0, 256, (M, N), dtype=np.uint8)
+        b = np.clip(a.astype(int) + rng.integers(-40, 40, (M, N)), 0, 255).astype(np.uint8)
+        assert dp.mse(a, b) == oracle.mse(a, b)
+        assert dp.ssim(a, b) == oracle.ssim(a, b)
+        assert dp.ssim(a, a) == 1.0
+    # RGB batches: per channel plane
+    frames = oracle.synth_frames(0, 2, 64, 96, 3)
+    p = dp.make_privacy_params(0.5, 16, 8, 2)
+    masks = oracle.synth_masks(0, 2, 64, 96)
+    _, out = ctx.pixelize_adaptive(frames, masks, p, dp.NOISE_KEYED, dp.plane_seeds(1, 2, 3))
+    s = ctx.metrics(frames, out, "ssim")
+    m = ctx.metrics(frames, out, "mse")
+    for f in range(2):
+        for c in range(3):
+            assert s[f * 3 + c] == oracle.ssim(frames[f, :, :, c], out[f, :, :, c])
+            assert m[f * 3 + c] == oracle.mse(frames[f, :, :, c], out[f, :, :, c])
+    with pytest.raises(ValueError):
+        dp.ssim(np.zeros((6, 9), np.uint8), np.zeros((6, 9), np.uint8))

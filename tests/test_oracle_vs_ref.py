@@ -55,3 +55,12 @@ def test_reference_release_gate_runs():
     out = subprocess.run([exe], capture_output=True, text=True, timeout=600).stdout
     fails = [ln for ln in out.splitlines() if " FAIL " in ln and "[ 8]" not in ln]
     assert not fails, out
+
+
+def test_metrics_restatement_bit_exact():
+    rng = np.random.default_rng(3)
+    for M, N in [(7, 7), (30, 41), (218, 178)]:
+        a = rng.integers(0, 256, (M, N), dtype=np.uint8)
+        b = rng.integers(0, 256, (M, N), dtype=np.uint8)
+        assert oracle.mse(a, b) == oracle.ref.mse(a, b)
+        assert oracle.ssim(a, b) == oracle.ref.ssim(a, b) == oracle.ref.ssim(a, b, 4)
