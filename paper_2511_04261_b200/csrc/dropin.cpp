@@ -129,6 +129,8 @@ std::uint64_t tile_sum(const std::vector<T>& data, int stride, const GridGeometr
 
 }  // namespace
 
+dppx_ctx* dropin_thread_ctx() { return thread_ctx(); }  // used by ingest.cpp
+
 // ---------------------------------------------------------------- image.hpp
 GrayImage make_image(int height, int width, std::uint8_t fill) {
   if (height < 1 || width < 1) throw std::invalid_argument("make_image: dimensions must be >= 1");

@@ -3,6 +3,9 @@
 // a caller written for libdppix.a compiles unchanged and gets the same answers.
 // Exit status 0 iff every check passes (run by tests/test_gpu_dropin.py).
 #include <algorithm>
+#include <filesystem>
+#include <fstream>
+#include <iterator>
 #include <cmath>
 #include <cstdio>
 #include <numeric>
@@ -15,7 +18,9 @@
 #include "dppix/image.hpp"
 #include "dppix/noise.hpp"
 #include "dppix/pixelize.hpp"
+#include "dppix/batch.hpp"
 #include "dppix/metrics.hpp"
+#include "dppix/pgm.hpp"
 #include "dppix/record.hpp"
 
 using namespace dppix;
@@ -288,6 +293,67 @@ int main() {
     CHECK(ssim(x, y, 1) == ssim(x, y, 8));
     CHECK_THROWS_AS(ssim(make_image(6, 9), make_image(6, 9)), std::invalid_argument);
     CHECK(csv_header() == "epsilon,m,b,n,seed,mse,ssim,runtime_ms,record_bytes");
+  }
+  // GPU batch runner == run_single per file (cli.cpp:93-213 semantics)
+  {
+    namespace fs = std::filesystem;
+    const fs::path dir = fs::temp_directory_path() / "dppx_batch_test";
+    fs::remove_all(dir);
+    fs::create_directories(dir / "in");
+    fs::create_directories(dir / "masks");
+    std::mt19937_64 rng(77);
+    const int shapes[5][2] = {{48, 64}, {48, 64}, {33, 70}, {48, 64}, {33, 70}};
+    std::vector<GrayImage> imgs;
+    for (int i = 0; i < 5; ++i) {
+      imgs.push_back(random_image(rng, shapes[i][0], shapes[i][1]));
+      write_pgm(imgs.back(), (dir / "in" / ("f" + std::to_string(i) + ".pgm")).string());
+      GrayImage m = make_image(shapes[i][0], shapes[i][1]);
+      for (auto& v : m.pixels) v = (rng() & 1) ? 255 : 0;
+      if (i != 4) write_pgm(m, (dir / "masks" / ("f" + std::to_string(i) + ".pgm")).string());
+    }
+    { std::ofstream bad((dir / "in" / "zz.pgm").string()); bad << "P2\n1 1\n255\n0\n"; }
+    BatchConfig cfg;
+    cfg.input = (dir / "in").string();
+    cfg.out_dir = (dir / "out").string();
+    cfg.mode = BatchMode::adaptive;
+    cfg.epsilon = 0.5;
+    cfg.m = 16;
+    cfg.b = 8;
+    cfg.n = 2;
+    cfg.seed = NoiseSeed{1234};
+    cfg.mask_path = (dir / "masks").string();
+    cfg.frames_per_call = 2;
+    const std::vector<BatchFileReport> reps = run_batch_gpu(cfg);
+    CHECK(reps.size() == 6);
+    for (int i = 0; i < 4; ++i) {
+      CHECK(reps[i].exit_code == 0);
+      const RegionMask mask = read_mask_pgm((dir / "masks" / ("f" + std::to_string(i) + ".pgm")).string());
+      const AdaptiveResult want = pixelize_adaptive(imgs[i], mask, make_privacy_params(0.5, 16, 8, 2),
+                                                    NoiseSeed{1234});
+      CHECK(read_pgm((dir / "out" / ("f" + std::to_string(i) + ".pix.pgm")).string()) == want.image);
+      const PixelRecord rec = read_record((dir / "out" / ("f" + std::to_string(i) + ".dppx")).string());
+      CHECK(rec == (PixelRecord{imgs[i].height, imgs[i].width, want.means}));
+      CHECK(reps[i].report.mse == mse(imgs[i], want.image));
+      CHECK(reps[i].report.ssim == ssim(imgs[i], want.image));
+      CHECK(reps[i].report.record_bytes == encode(rec).size());
+    }
+    CHECK(reps[4].exit_code == 3);  // no mask for f4 (IoError)
+    CHECK(reps[5].exit_code == 3);  // P2 input (IoError)
+    cfg.mode = BatchMode::uniform;
+    cfg.seed.reset();  // noise-free: epsilon is a label
+    const std::vector<BatchFileReport> u = run_batch_gpu(cfg);
+    CHECK(u[4].exit_code == 0 &&
+          read_pgm((dir / "out" / "f4.pix.pgm").string()) ==
+              pixelize_parallel(imgs[4], make_privacy_params(0.5, 16, 8), std::nullopt).image);
+    cfg.mode = BatchMode::reference;
+    bool usage = false;
+    try {
+      run_batch_gpu(cfg);  // reference mode cannot emit records (cli.cpp:82-85)
+    } catch (const UsageError&) {
+      usage = true;
+    }
+    CHECK(usage);
+    fs::remove_all(dir);
   }
   std::printf("%d passed, %d failed\n", g_pass, g_fail);
   return g_fail == 0 ? 0 : 1;
