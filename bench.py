@@ -45,7 +45,12 @@ WORKLOADS = {
            "reconstruction"),
     "celeba": (218, 178, 3, 100000, 16, 1, 16, 0.5, False,
                "uniform b=16 on a 100k-image batch of 178x218 RGB faces (CelebA shape)"),
+    # one step = the 12-run sweep b in {4,8,16,32} x eps in {0.1,0.5,1} over the batch
+    "sweep": (1083, 1917, 3, 60, 16, 1, 16, 0.5, False,
+              "grid-size/padding sweep b in {4,8,16,32} x eps in {0.1,0.5,1}, uniform m=16, "
+              "60 synthetic 1917x1083 RGB frames (non-divisible dims); value counts frame-runs"),
 }
+SWEEP = [(bb, ee) for bb in (4, 8, 16, 32) for ee in (0.1, 0.5, 1.0)]
 
 
 def parse():
@@ -291,9 +296,20 @@ def main():
     lens = torch.zeros(F * C, dtype=torch.int32, device=dev)
     seeds = sh.plane_seed_list(42, my, C)
     nz, keep = dp.Context._noise(dp.NOISE_KEYED, seeds)
+    sweep = args.workload == "sweep"
+    jobs = []  # (params, means buffer, G) per run of one step
+    if sweep:
+        for bb, ee in SWEEP:
+            gb = dp.grid_dims(M, N, bb).grid_count()
+            jobs.append((dp.make_privacy_params(ee, m, bb),
+                         torch.zeros((F * C, gb), dtype=torch.uint8, device=dev), gb))
+    runs = len(jobs) if sweep else 1
 
     def step():
-        if adaptive:
+        if sweep:
+            for pj, mj, _ in jobs:
+                ctx.pixelize_uniform_dev(d, img, pj, nz, mj, out)
+        elif adaptive:
             ctx.pixelize_adaptive_dev(d, img, mask, p, nz, stats, sstride, lens, out)
         else:
             ctx.pixelize_uniform_dev(d, img, p, nz, stats, out)
@@ -303,6 +319,8 @@ def main():
     ctx.synchronize()
     # payload bytes actually written (for the roofline's algorithmic bytes)
     payload_bytes = int(lens.sum().item()) if adaptive else F * C * G
+    if sweep:
+        payload_bytes = sum(F * C * gj for _, _, gj in jobs) / runs  # mean per K1 launch
     # ---- timed region: device-resident ----
     stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
     ctx.reset_stats()
@@ -320,18 +338,18 @@ def main():
     st = ctx.stats()
     ctx.set_timing(False)
     ms_step = allmax(ms_total / args.steps)
-    frames_total = F * world
+    frames_total = F * world * runs
     value = frames_total * M * N / 1e6 / (ms_step / 1e3)
     fps = frames_total / (ms_step / 1e3)
     # roofline of K1 (dominant kernel): algorithmic bytes / measured duration
     kfam = "stats_tma" if st["launches"]["stats_tma"] else "stats_generic"
     k1_launches = max(1, st["launches"][kfam])
     k1_ms = st["device_ms"][kfam] / k1_launches
-    k1_bytes = F * M * N * C * 2 + payload_bytes  # read frame, write image, write stats
+    k1_bytes = int(F * M * N * C * 2 + payload_bytes)  # read frame, write image, write stats
     k0_bytes = (F * M * N + 4 * G * C * F + 4 * F * C) if adaptive else 0
     peak, peak_src = measured_peak()
     achieved = k1_bytes / (k1_ms / 1e3) / 1e9
-    step_gbs = (k1_bytes + k0_bytes) / (ms_total / args.steps / 1e3) / 1e9
+    step_gbs = (k1_bytes * runs + k0_bytes) / (ms_total / args.steps / 1e3) / 1e9
     traffic = ncu_traffic(args.workload)
     launches_timed = sum(st["launches"].values())
 
@@ -383,7 +401,15 @@ def main():
         nze, keep_e = dp.Context._noise(dp.NOISE_KEYED, seeds_e)
         import ctypes as Ct
 
+        h_means = [torch.zeros((Fe * C, gj), dtype=torch.uint8).pin_memory() for _, _, gj in jobs]
+
         def e2e_step():
+            if sweep:
+                for (pj, _, _), hm in zip(jobs, h_means):
+                    ctx._check(dp._lib.dppx_pixelize_uniform(ctx._h, Ct.byref(de), h_img.data_ptr(),
+                                                             Ct.byref(pj), Ct.byref(nze),
+                                                             hm.data_ptr(), h_out.data_ptr()), "e2e")
+                return
             if adaptive:
                 rc = dp._lib.dppx_pixelize_adaptive(ctx._h, Ct.byref(de), h_img.data_ptr(),
                                                     h_mask.data_ptr(), Ct.byref(p), Ct.byref(nze),
@@ -412,6 +438,24 @@ def main():
 
         h2d_link = link_gbs(1 << 30, True)
         d2h_link = link_gbs(1 << 30, False)
+
+        def duplex_gbs(nbytes):  # both directions at once, on two streams
+            ha = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+            hb = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+            da = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+            db = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+            s1, s2 = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(3):
+                with torch.cuda.stream(s1):
+                    da.copy_(ha, non_blocking=True)
+                with torch.cuda.stream(s2):
+                    hb.copy_(db, non_blocking=True)
+            torch.cuda.synchronize()
+            return 6 * nbytes / (time.perf_counter() - t0) / 1e9
+
+        duplex_link = duplex_gbs(1 << 29)
         for _ in range(2):
             e2e_step()
         ctx.reset_stats()
@@ -423,12 +467,15 @@ def main():
         barrier()
         es = ctx.stats()
         e_ms = allmax((t1 - t0) / args.e2e_steps * 1e3)
-        e2e = {"value": round(Fe * world * M * N / 1e6 / (e_ms / 1e3), 3), "unit": "MP/s",
+        e2e = {"value": round(Fe * runs * world * M * N / 1e6 / (e_ms / 1e3), 3), "unit": "MP/s",
                "h2d_bytes_per_step": es["h2d_bytes"] // args.e2e_steps,
                "d2h_bytes_per_step": es["d2h_bytes"] // args.e2e_steps,
                "frames_per_step": Fe, "ms_per_step": round(e_ms, 3),
-               "frames_per_sec": round(Fe * world / (e_ms / 1e3), 3),
-               "link_gbs": {"h2d": round(h2d_link, 1), "d2h": round(d2h_link, 1)},
+               "frames_per_sec": round(Fe * runs * world / (e_ms / 1e3), 3),
+               "link_gbs": {"h2d": round(h2d_link, 1), "d2h": round(d2h_link, 1),
+                            "duplex": round(duplex_link, 1)},
+               "duplex_frac": round((es["h2d_bytes"] + es["d2h_bytes"]) / args.e2e_steps
+                                    / (duplex_link * 1e9) / (e_ms / 1e3), 4),
                "link_frac": round(max(es["h2d_bytes"] / args.e2e_steps / (h2d_link * 1e9),
                                       es["d2h_bytes"] / args.e2e_steps / (d2h_link * 1e9))
                                   / (e_ms / 1e3), 4),
