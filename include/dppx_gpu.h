@@ -181,6 +181,19 @@ int dppx_reassemble_dev(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8
 int dppx_synth_frames_dev(dppx_ctx* ctx, const dppx_frames_desc* desc, uint32_t data_seed,
                           uint32_t f0, uint8_t* img, uint8_t* mask /* nullable */);
 
+/* EXTENSION (north-star "per-region complexity measure"; no reference
+ * counterpart -- the reference takes external masks): cell
+ * (r, c) is complex iff the variance of its C*b*b mirror-padded samples,
+ * (n*S2 - S1^2)/n^2 from exact integer sums, is >= var_tau. Mask means are
+ * stored as 1.0f / 0.0f so records decode to the same classification.
+ * PRIVACY: the classification is computed from the private frames and is NOT
+ * covered by the epsilon guarantee; use only where that is acceptable. */
+int dppx_pixelize_adaptive_variance_dev(dppx_ctx* ctx, const dppx_frames_desc* desc,
+                                        const uint8_t* img, double var_tau,
+                                        const dppx_privacy_params* params, const dppx_noise* noise,
+                                        uint8_t* payload, int64_t payload_stride,
+                                        uint32_t* payload_len, uint8_t* out /* nullable */);
+
 /* ---- host entry points (pinned pipeline; synchronous) -------------------- */
 int dppx_pixelize_uniform(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* img,
                           const dppx_privacy_params* params, const dppx_noise* noise,
@@ -189,6 +202,11 @@ int dppx_pixelize_adaptive(dppx_ctx* ctx, const dppx_frames_desc* desc, const ui
                            const uint8_t* mask, const dppx_privacy_params* params,
                            const dppx_noise* noise, uint8_t* payload, int64_t payload_stride,
                            uint32_t* payload_len /* nullable */, uint8_t* out /* nullable */);
+int dppx_pixelize_adaptive_variance(dppx_ctx* ctx, const dppx_frames_desc* desc,
+                                    const uint8_t* img, double var_tau,
+                                    const dppx_privacy_params* params, const dppx_noise* noise,
+                                    uint8_t* payload, int64_t payload_stride,
+                                    uint32_t* payload_len, uint8_t* out /* nullable */);
 int dppx_broadcast_means(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* means,
                          int32_t b, uint8_t* out);
 /* Algorithm 1 (pixelize.cpp:50-84): no padding, border cells average their real

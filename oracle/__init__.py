@@ -88,6 +88,12 @@ lib.or_pixelize_reference.argtypes = [u8p, C.c_int, C.c_int, C.c_int, C.c_double
                                       C.c_uint64, u8p]
 lib.or_synth_frames.argtypes = [C.c_uint32, C.c_uint32, C.c_int, C.c_int, C.c_int, C.c_int,
                                 C.c_long, C.c_long, u8p]
+lib.or_classify_variance.argtypes = [u8p, C.c_int, C.c_int, C.c_long, C.c_int, C.c_int,
+                                     C.c_double, C.POINTER(C.c_float)]
+lib.or_pixelize_adaptive_plane_mm.argtypes = [u8p, C.POINTER(C.c_float), C.c_int, C.c_int, C.c_long,
+                                              C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+                                              C.c_double, C.c_int, C.c_uint64, C.c_uint32, f64p,
+                                              u8p, u32p, u8p, C.c_long]
 lib.or_mse.restype = C.c_double
 lib.or_mse.argtypes = [u8p, u8p, C.c_long]
 lib.or_ssim.restype = C.c_double
@@ -202,6 +208,40 @@ def pixelize_adaptive(img, mask, b, n, sigma, sigma_sub, noise="none", seeds=Non
             C.byref(ln), _p(out), N * Cn)
         if rc != 0:
             raise OracleError(f"pixelize_adaptive: rc={rc}")
+        payloads.append(bytes(buf[: ln.value]))
+    return payloads, out
+
+
+def classify_variance(img, b, tau):
+    """EXTENSION: per-cell mask means 1.0 (simple) / 0.0 (variance >= tau)."""
+    img, Cn = _planes(img)
+    M, N = img.shape[:2]
+    g = grid_dims(M, N, b)
+    mm = np.zeros(g.grid_rows * g.grid_cols, np.float32)
+    if lib.or_classify_variance(_p(img), M, N, N * Cn, Cn, b, tau,
+                                mm.ctypes.data_as(C.POINTER(C.c_float))) != 0:
+        raise OracleError("classify_variance: invalid")
+    return mm
+
+
+def pixelize_adaptive_variance(img, b, n, sigma, sigma_sub, tau, noise="none", seeds=None,
+                               frame=0):
+    """EXTENSION: adaptive pixelization with the variance classification."""
+    img, Cn = _planes(img)
+    M, N = img.shape[:2]
+    mm = classify_variance(img, b, tau)
+    cap = lib.or_adaptive_payload_capacity(M, N, b, n)
+    out = np.zeros_like(img)
+    payloads = []
+    for ch in range(Cn):
+        buf = np.zeros(cap, np.uint8)
+        ln = C.c_uint32(0)
+        rc = lib.or_pixelize_adaptive_plane_mm(
+            _p(img), mm.ctypes.data_as(C.POINTER(C.c_float)), M, N, N * Cn, Cn, ch, b, n, sigma,
+            sigma_sub, _NOISE_KIND[noise], int(seeds[ch]) if seeds is not None else 0, frame,
+            None, _p(buf), C.byref(ln), _p(out), N * Cn)
+        if rc != 0:
+            raise OracleError(f"pixelize_adaptive_variance: rc={rc}")
         payloads.append(bytes(buf[: ln.value]))
     return payloads, out
 

@@ -270,11 +270,63 @@ size_t or_adaptive_payload_capacity(int M, int N, int b, int n) {
  * record.cpp:153-171): G x f32 LE mask means | u32 S | S simple means |
  * (G-S)*n*n complex submeans. out (nullable) is reassemble (adaptive.cpp:181-245)
  * of that payload for channel ch. */
+static int adaptive_core(const uint8_t* img, const uint8_t* mask, const float* mm_in, int M, int N,
+                         long pitch, long mask_pitch, int C, int ch, int b, int n, double sigma,
+                         double sigma_sub, int noise_kind, uint64_t seed, uint32_t frame,
+                         const double* injected, uint8_t* payload, uint32_t* payload_len,
+                         uint8_t* out, long out_pitch);
+
 int or_pixelize_adaptive_plane(const uint8_t* img, const uint8_t* mask, int M, int N, long pitch,
                                long mask_pitch, int C, int ch, int b, int n, double sigma,
                                double sigma_sub, int noise_kind, uint64_t seed, uint32_t frame,
                                const double* injected, uint8_t* payload, uint32_t* payload_len,
                                uint8_t* out, long out_pitch) {
+  return adaptive_core(img, mask, NULL, M, N, pitch, mask_pitch, C, ch, b, n, sigma, sigma_sub,
+                       noise_kind, seed, frame, injected, payload, payload_len, out, out_pitch);
+}
+
+/* EXTENSION (no reference counterpart; north-star "complexity measure"):
+ * cell (r, c) of the mirror-padded frame is complex iff the variance of its
+ * C*b*b samples, (n*S2 - S1^2) / n^2 with exact integer sums, is >= tau.
+ * Writes mask means 1.0f (simple) / 0.0f (complex) so the DPPX payload
+ * classifies identically on decode. */
+int or_classify_variance(const uint8_t* img, int M, int N, long pitch, int C, int b, double tau,
+                         float* mm_out) {
+  or_geom g;
+  if (or_grid_dims(M, N, b, &g) != OR_OK || !pad_ok(&g, M, N)) return OR_INVALID;
+  const long long ns = (long long)C * b * b;
+  for (int r = 0; r < g.grid_rows; ++r)
+    for (int c = 0; c < g.grid_cols; ++c) {
+      uint64_t s1 = 0, s2 = 0;
+      for (int i = r * b; i < r * b + b; ++i)
+        for (int j = c * b; j < c * b + b; ++j)
+          for (int k = 0; k < C; ++k) {
+            const uint64_t v = PX(img, pitch, C, k, M, N, i, j);
+            s1 += v;
+            s2 += v * v;
+          }
+      const double num = (double)((long long)(ns * (long long)s2) - (long long)(s1 * s1));
+      const double var = num / ((double)ns * (double)ns);
+      mm_out[(size_t)r * g.grid_cols + c] = var >= tau ? 0.0f : 1.0f;
+    }
+  return OR_OK;
+}
+
+/* Adaptive plane with per-cell mask means supplied (e.g. by or_classify_variance). */
+int or_pixelize_adaptive_plane_mm(const uint8_t* img, const float* mm, int M, int N, long pitch,
+                                  int C, int ch, int b, int n, double sigma, double sigma_sub,
+                                  int noise_kind, uint64_t seed, uint32_t frame,
+                                  const double* injected, uint8_t* payload, uint32_t* payload_len,
+                                  uint8_t* out, long out_pitch) {
+  return adaptive_core(img, NULL, mm, M, N, pitch, 0, C, ch, b, n, sigma, sigma_sub, noise_kind,
+                       seed, frame, injected, payload, payload_len, out, out_pitch);
+}
+
+static int adaptive_core(const uint8_t* img, const uint8_t* mask, const float* mm_in, int M, int N,
+                         long pitch, long mask_pitch, int C, int ch, int b, int n, double sigma,
+                         double sigma_sub, int noise_kind, uint64_t seed, uint32_t frame,
+                         const double* injected, uint8_t* payload, uint32_t* payload_len,
+                         uint8_t* out, long out_pitch) {
   or_geom g;
   if (n < 1 || b % n != 0) return OR_INVALID;
   if (or_grid_dims(M, N, b, &g) != OR_OK || !pad_ok(&g, M, N)) return OR_INVALID;
@@ -290,7 +342,14 @@ int or_pixelize_adaptive_plane(const uint8_t* img, const uint8_t* mask, int M, i
     free(simple);
     return OR_INVALID;
   }
-  classify(mask, mask_pitch, M, N, &g, mm, simple);
+  if (mm_in) {
+    for (int k = 0; k < G; ++k) {
+      mm[k] = mm_in[k];
+      simple[k] = mm_in[k] > 0.5f ? 1 : 0;
+    }
+  } else {
+    classify(mask, mask_pitch, M, N, &g, mm, simple);
+  }
   uint32_t S = 0;
   for (int k = 0; k < G; ++k) S += simple[k];
   memcpy(payload, mm, sizeof(float) * (size_t)G); /* little-endian host */

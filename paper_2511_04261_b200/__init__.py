@@ -133,6 +133,10 @@ ABI = {
     "dppx_pixelize_adaptive": (C.c_int, [_ctxp, _descp, _vp, _vp, _pp, _np, _vp, C.c_int64, _vp,
                                          _vp]),
     "dppx_broadcast_means": (C.c_int, [_ctxp, _descp, _vp, C.c_int32, _vp]),
+    "dppx_pixelize_adaptive_variance": (C.c_int, [_ctxp, _descp, _vp, C.c_double, _pp, _np, _vp,
+                                                  C.c_int64, _vp, _vp]),
+    "dppx_pixelize_adaptive_variance_dev": (C.c_int, [_ctxp, _descp, _vp, C.c_double, _pp, _np,
+                                                      _vp, C.c_int64, _vp, _vp]),
     "dppx_pixelize_reference": (C.c_int, [_ctxp, _descp, _vp, _pp, _np, _vp, _vp]),
     "dppx_reassemble": (C.c_int, [_ctxp, _descp, _vp, C.c_int64, _vp, C.c_int32, C.c_int32, _vp]),
     "dppx_classify_regions": (C.c_int, [_ctxp, _descp, _vp, C.c_int32, _vp]),
@@ -423,6 +427,27 @@ class Context:
                     "pixelize_reference")
         del keep
         return means, out
+
+    def pixelize_adaptive_variance(self, frames, tau: float, params: PrivacyParams,
+                                   noise=NOISE_NONE, seeds=None, frame_base=0):
+        """EXTENSION: adaptive pixelization where a cell is complex iff the
+        variance of its C*b*b samples is >= tau (the classification is derived
+        from the private frames and is not covered by epsilon)."""
+        frames = np.ascontiguousarray(frames, dtype=np.uint8)
+        F, M, N, Cn = _frames_shape(frames)
+        cap = adaptive_payload_capacity(M, N, params.b, params.n)
+        stride = (cap + 3) & ~3
+        buf = np.zeros((F * Cn, stride), np.uint8)
+        lens = np.zeros(F * Cn, np.uint32)
+        out = np.zeros_like(frames)
+        nz, keep = self._noise(noise, seeds, frame_base, None)
+        d = _desc(M, N, Cn, F)
+        self._check(_lib.dppx_pixelize_adaptive_variance(self._h, C.byref(d), _ptr(frames), tau,
+                                                         C.byref(params), C.byref(nz), _ptr(buf),
+                                                         stride, _ptr(lens), _ptr(out)),
+                    "pixelize_adaptive_variance")
+        del keep
+        return [bytes(buf[i, : lens[i]]) for i in range(F * Cn)], out
 
     def broadcast_means(self, means, M, N, b, channels=1, frames=1):
         means = np.ascontiguousarray(means, dtype=np.uint8)

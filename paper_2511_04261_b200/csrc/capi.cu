@@ -109,6 +109,7 @@ struct dppx_ctx {
   cudaEvent_t in_done[2] = {}, comp_done[2] = {}, out_done[2] = {};
   int chunk_frames = 0;
   bool exact_noise = false;
+  double var_tau = 0.0;  // AdaptiveVariance host calls
   // stats
   bool timing = false;
   std::vector<PendingTiming> pending;
@@ -324,18 +325,34 @@ int ensure_scratch(dppx_ctx* ctx, const BatchGeom& g, int planes) {
   return DPPX_OK;
 }
 
+struct VarianceSource {  // extension: classify cells by the frames' own variance
+  const uint8_t* img = nullptr;
+  int64_t pitch = 0, fstride = 0;
+  double tau = 0.0;
+};
+
 int classify(dppx_ctx* ctx, const BatchGeom& g, int planes, bool from_payload, const uint8_t* mask,
              int64_t mpitch, int64_t mfstride, uint8_t* payload, const uint8_t* payload_in,
-             int64_t pstride, uint32_t* payload_len, const uint32_t* in_len) {
+             int64_t pstride, uint32_t* payload_len, const uint32_t* in_len,
+             const VarianceSource* var = nullptr) {
   ClassifyArgs a{};
   a.g = g;
   a.planes = planes;
   a.from_payload = from_payload ? 1 : 0;
+  if (var) {
+    a.from_payload = 2;
+    a.img = var->img;
+    a.pitch = var->pitch;
+    a.fstride = var->fstride;
+    a.var_tau = var->tau;
+    a.img_vec4 = (reinterpret_cast<uintptr_t>(var->img) & 3) == 0 && var->pitch % 4 == 0 &&
+                 var->fstride % 4 == 0 && (g.b * g.C) % 4 == 0;
+  }
   a.mask = mask;
   a.mpitch = mpitch;
   a.mfstride = mfstride;
   a.vec = 1;
-  if (!from_payload) {
+  if (!from_payload && !var) {
     if (g.b % 16 == 0 && aligned16(mask) && mpitch % 16 == 0 && mfstride % 16 == 0) a.vec = 16;
     else if (g.b % 4 == 0 && (reinterpret_cast<uintptr_t>(mask) & 3) == 0 && mpitch % 4 == 0 &&
              mfstride % 4 == 0)
@@ -462,14 +479,18 @@ int pixelize_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img, c
                  const dppx_privacy_params* pp, const dppx_noise* nz, const double* dev_injected,
                  uint8_t* stats, int64_t sstride, uint32_t* payload_len, uint8_t* out,
                  bool adaptive, DevBuf& dev_seeds, uint64_t*& pinned, size_t& pinned_n,
-                 cudaEvent_t guard, bool record_guard, bool partial = false) {
+                 cudaEvent_t guard, bool record_guard, bool partial = false,
+                 double var_tau = std::nan("")) {
   BatchGeom g;
   if (int rc = geometry(ctx, d->height, d->width, d->channels, d->frames, pp->b,
                         adaptive ? pp->n : 1, &g, !partial))
     return rc;
   if (d->frames == 0) return DPPX_OK;
-  if (!img || !stats || (adaptive && !mask))
+  const bool by_variance = adaptive && !std::isnan(var_tau);
+  if (!img || !stats || (adaptive && !mask && !by_variance))
     return set_err(ctx, DPPX_ERR_INVALID, "null image/statistics/mask pointer");
+  if (by_variance && !(var_tau >= 0.0))
+    return set_err(ctx, DPPX_ERR_INVALID, "variance threshold must be >= 0");
   if (adaptive) {
     const size_t cap = dppx_adaptive_payload_capacity(g.M, g.N, g.b, g.n);
     if (sstride < static_cast<int64_t>(cap) || sstride % 4 != 0)
@@ -498,8 +519,9 @@ int pixelize_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img, c
     return rc;
   if (adaptive) {
     if (int rc = ensure_scratch(ctx, g, g.F)) return rc;
+    VarianceSource vs{img, d->pitch, d->frame_stride, var_tau};
     if (int rc = classify(ctx, g, g.F, false, mask, d->mask_pitch, d->mask_frame_stride, stats,
-                          nullptr, sstride, payload_len, nullptr))
+                          nullptr, sstride, payload_len, nullptr, by_variance ? &vs : nullptr))
       return rc;
     a.cellinfo = static_cast<const uint32_t*>(ctx->cellinfo.p);
     a.rowprefix = static_cast<const uint32_t*>(ctx->rowprefix.p);
@@ -611,14 +633,16 @@ cudaError_t copy_frames(void* dst, int64_t dpitch, int64_t dfs, const void* src,
   return cudaSuccess;
 }
 
-enum class HostOp { Uniform, Adaptive, Broadcast, Reassemble, Reference };
+enum class HostOp { Uniform, Adaptive, Broadcast, Reassemble, Reference, AdaptiveVariance };
 
 int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uint8_t* img,
                   const uint8_t* mask, const dppx_privacy_params* pp, const dppx_noise* nz,
                   uint8_t* stats, int64_t sstride, uint32_t* lens, const uint32_t* in_lens,
                   int b_arg, int n_arg, uint8_t* out) {
-  const bool pix = op == HostOp::Uniform || op == HostOp::Adaptive || op == HostOp::Reference;
-  const bool adaptive = op == HostOp::Adaptive || op == HostOp::Reassemble;
+  const bool pix = op == HostOp::Uniform || op == HostOp::Adaptive || op == HostOp::Reference ||
+                   op == HostOp::AdaptiveVariance;
+  const bool adaptive = op == HostOp::Adaptive || op == HostOp::Reassemble ||
+                        op == HostOp::AdaptiveVariance;
   if (!d) return set_err(ctx, DPPX_ERR_INVALID, "null frames descriptor");
   const int b = pix ? (pp ? pp->b : 0) : b_arg;
   const int n = pix ? (pp ? pp->n : 1) : n_arg;
@@ -649,7 +673,7 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
   if (adaptive) {
     const size_t cap = dppx_adaptive_payload_capacity(M, N, b, n);
     dstride = round_up(static_cast<int64_t>(cap), 16);
-    if (sstride < (op == HostOp::Adaptive ? static_cast<int64_t>(cap) : 4ll * g.G + 4))
+    if (sstride < (op != HostOp::Reassemble ? static_cast<int64_t>(cap) : 4ll * g.G + 4))
       return set_err(ctx, DPPX_ERR_INVALID, "payload_stride too small");
     if (op == HostOp::Reassemble) dstride = round_up(std::max<int64_t>(sstride, 16), 16);
   } else {
@@ -793,7 +817,8 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
                         inj ? static_cast<const double*>(ctx->inj[s].p) : nullptr, dstats, dstride,
                         adaptive ? dlens : nullptr, out ? dout : nullptr, adaptive, ctx->sd[s],
                         ctx->sd_pinned[s], ctx->sd_pinned_n[s], ctx->comp_done[s], false,
-                        op == HostOp::Reference);
+                        op == HostOp::Reference,
+                        op == HostOp::AdaptiveVariance ? ctx->var_tau : std::nan(""));
     } else {
       rc = expand_dev(ctx, &dd, dstats, dstride, in_lens ? dlens : nullptr, b, n, dout, adaptive);
     }
@@ -1134,6 +1159,31 @@ int dppx_pixelize_reference(dppx_ctx* ctx, const dppx_frames_desc* d, const uint
   if (pp && pp->n != 1) return set_err(ctx, DPPX_ERR_INVALID, "pixelize_reference: requires n == 1");
   return host_pipeline(ctx, HostOp::Reference, d, img, nullptr, pp, nz, means, 0, nullptr, nullptr, 0,
                        1, out);
+}
+
+int dppx_pixelize_adaptive_variance(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img,
+                                    double var_tau, const dppx_privacy_params* pp,
+                                    const dppx_noise* nz, uint8_t* payload, int64_t payload_stride,
+                                    uint32_t* payload_len, uint8_t* out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (!(var_tau >= 0.0)) return set_err(ctx, DPPX_ERR_INVALID, "variance threshold must be >= 0");
+  ctx->var_tau = var_tau;
+  return host_pipeline(ctx, HostOp::AdaptiveVariance, d, img, nullptr, pp, nz, payload,
+                       payload_stride, payload_len, nullptr, 0, 0, out);
+}
+
+int dppx_pixelize_adaptive_variance_dev(dppx_ctx* ctx, const dppx_frames_desc* d,
+                                        const uint8_t* img, double var_tau,
+                                        const dppx_privacy_params* pp, const dppx_noise* nz,
+                                        uint8_t* payload, int64_t payload_stride,
+                                        uint32_t* payload_len, uint8_t* out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = check_params(ctx, pp, true)) return rc;
+  if (int rc = check_desc(ctx, d, false, out != nullptr)) return rc;
+  if (!(var_tau >= 0.0)) return set_err(ctx, DPPX_ERR_INVALID, "variance threshold must be >= 0");
+  return pixelize_dev(ctx, d, img, nullptr, pp, nz, nz ? nz->injected : nullptr, payload,
+                      payload_stride, payload_len, out, true, ctx->seeds, ctx->seeds_pinned,
+                      ctx->seeds_pinned_n, ctx->seeds_ev, true, false, var_tau);
 }
 
 int dppx_broadcast_means(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* means, int32_t b,

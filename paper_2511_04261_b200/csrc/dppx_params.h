@@ -74,6 +74,12 @@ struct ClassifyArgs {
   uint32_t* counters;        // [P] self-resetting arrival tickets
   int* status;               // set to DPPX_ERR_CORRUPT on inconsistent payloads
   double area;               // (double)b*b
+  // from_payload == 2: variance classification (extension): cell complex iff
+  // var(C*b*b samples) >= var_tau, computed from the frames themselves.
+  const uint8_t* img;
+  int64_t pitch, fstride;
+  int img_vec4;              // rows/cells 4-byte aligned: word loads
+  double var_tau;
 };
 
 // K1 / K1g: fused statistics, noise, compact store and reconstruction.

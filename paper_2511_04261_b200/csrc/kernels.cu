@@ -143,6 +143,45 @@ __device__ __forceinline__ uint32_t mask_cell_sum(const ClassifyArgs& a, const u
   return s;
 }
 
+// EXTENSION (variance complexity): exact S1 = sum x, S2 = sum x^2 over the
+// C*b*b samples of mirror-padded cell (r, c); dp4a(w, w) gives sum of squares.
+__device__ __forceinline__ bool cell_is_complex_var(const ClassifyArgs& a, const uint8_t* base,
+                                                   int r, int c) {
+  const BatchGeom& g = a.g;
+  const int b = g.b, C = g.C;
+  const int j0 = c * b;
+  uint64_t s1 = 0, s2 = 0;
+  const bool inside = j0 + b <= g.N;
+  for (int i = r * b; i < r * b + b; ++i) {
+    const uint8_t* row = base + static_cast<int64_t>(reflect_index(i, g.M)) * a.pitch;
+    if (inside && a.img_vec4) {
+      const uint32_t* p = reinterpret_cast<const uint32_t*>(row + static_cast<int64_t>(j0) * C);
+      uint32_t t1 = 0, t2 = 0;
+      for (int k = 0; k < b * C / 4; ++k) {
+        const uint32_t w = __ldg(p + k);
+        t1 = __dp4a(w, 0x01010101u, t1);
+        t2 = __dp4a(w, w, t2);
+      }
+      s1 += t1;
+      s2 += t2;
+    } else {
+      for (int j = j0; j < j0 + b; ++j) {
+        const uint8_t* px = row + static_cast<int64_t>(reflect_index(j, g.N)) * C;
+        for (int k = 0; k < C; ++k) {
+          const uint32_t v = __ldg(px + k);
+          s1 += v;
+          s2 += v * v;
+        }
+      }
+    }
+  }
+  const long long ns = static_cast<long long>(C) * b * b;
+  const double num = static_cast<double>(ns * static_cast<long long>(s2) -
+                                         static_cast<long long>(s1) * static_cast<long long>(s1));
+  const double var = __ddiv_rn(num, __dmul_rn(static_cast<double>(ns), static_cast<double>(ns)));
+  return var >= a.var_tau;
+}
+
 __global__ void __launch_bounds__(kClassifyThreads) k_classify(const ClassifyArgs a) {
   __shared__ uint32_t warp_tot[kClassifyThreads / 32];
   __shared__ uint32_t s_last;
@@ -151,7 +190,7 @@ __global__ void __launch_bounds__(kClassifyThreads) k_classify(const ClassifyArg
   for (int p = blockIdx.y; p < a.planes; p += gridDim.y) {
     const uint8_t* mbase = a.from_payload ? nullptr : a.mask + static_cast<int64_t>(p) * a.mfstride;
     const float* mm_in =
-        a.from_payload ? reinterpret_cast<const float*>(a.payload_in + p * a.pstride) : nullptr;
+        a.from_payload == 1 ? reinterpret_cast<const float*>(a.payload_in + p * a.pstride) : nullptr;
     uint32_t carry = 0;
     for (int c0 = 0; c0 < g.GC; c0 += kClassifyThreads) {
       const int c = c0 + threadIdx.x;
@@ -159,8 +198,14 @@ __global__ void __launch_bounds__(kClassifyThreads) k_classify(const ClassifyArg
       if (c < g.GC) {
         const int cell = r * g.GC + c;
         float mean;
-        if (a.from_payload) {
+        if (a.from_payload == 1) {
           mean = mm_in[cell];
+        } else if (a.from_payload == 2) {
+          mean = cell_is_complex_var(a, a.img + static_cast<int64_t>(p) * a.fstride, r, c) ? 0.0f
+                                                                                          : 1.0f;
+          for (int ch = 0; ch < g.C; ++ch)
+            reinterpret_cast<float*>(a.payload + (static_cast<int64_t>(p) * g.C + ch) * a.pstride)
+                [cell] = mean;
         } else {
           const uint32_t s = mask_cell_sum(a, mbase, r, c);
           // mask_grid_mean (image.cpp:191-202) then static_cast<float>
@@ -203,7 +248,7 @@ __global__ void __launch_bounds__(kClassifyThreads) k_classify(const ClassifyArg
         a.counters[p] = 0u;  // ready for the next launch
         const uint64_t nn = static_cast<uint64_t>(g.n) * g.n;
         const uint32_t len = static_cast<uint32_t>(4ull * g.G + 4 + S + (g.G - S) * nn);
-        if (a.from_payload) {
+        if (a.from_payload == 1) {
           const uint8_t* q = a.payload_in + p * a.pstride + 4ll * g.G;
           const uint32_t stored = static_cast<uint32_t>(q[0]) | (static_cast<uint32_t>(q[1]) << 8) |
                                   (static_cast<uint32_t>(q[2]) << 16) |

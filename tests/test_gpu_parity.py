@@ -335,3 +335,24 @@ def test_expand_fast_path(ctx, b, n, C):
             pu = dp.make_privacy_params(0.5, 16, b)
             means, uimg = ctx.pixelize_uniform(frames, pu, dp.NOISE_KEYED, seeds)
             assert np.array_equal(ctx.broadcast_means(means, M, N, b, channels=C, frames=2), uimg)
+
+
+@pytest.mark.parametrize("b,n,C", [(16, 4, 3), (8, 2, 1), (32, 8, 3), (5, 1, 3)])
+def test_variance_classification_extension(ctx, b, n, C):
+    """EXTENSION (variance complexity measure) vs its CPU restatement
+    (oracle.classify_variance): identical classification, payloads and image."""
+    F, M, N = 2, 75, 130
+    frames = oracle.synth_frames(4, F, M, N, C)
+    rng = np.random.default_rng(b)
+    frames[:, :40, :60] = 128 + rng.integers(-2, 3, (F, 40, 60, C))  # flat region -> simple
+    p = dp.make_privacy_params(0.5, 16, b, n)
+    seeds = dp.plane_seeds(3, F, C, frame0=4)
+    for tau in (0.0, 50.0, 400.0):
+        pls, img = ctx.pixelize_adaptive_variance(frames, tau, p, dp.NOISE_KEYED, seeds)
+        for f in range(F):
+            rp, ri = oracle.pixelize_adaptive_variance(frames[f], b, n, p.sigma, p.sigma_sub, tau,
+                                                       "keyed", seeds[f * C:(f + 1) * C], frame=f)
+            assert pls[f * C:(f + 1) * C] == rp, (tau, f)
+            assert np.array_equal(img[f], ri)
+        # records made this way reconstruct like any other
+        assert np.array_equal(ctx.reassemble(pls, M, N, b, n, channels=C, frames=F), img)

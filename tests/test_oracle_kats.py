@@ -124,3 +124,14 @@ def test_synthetic_generator_is_deterministic():
     assert np.array_equal(a, b) and a.std() > 20
     m = oracle.synth_masks(0, 1, 1080, 1920)[0]
     assert 0.2 < 1 - m.mean() < 0.3  # ~25 % foreground
+
+
+def test_variance_classification_restatement():
+    """EXTENSION check: the CPU restatement's variance test on hand-made cells."""
+    img = np.zeros((8, 8), np.uint8)
+    img[:4, 4:] = np.array([[0, 255] * 2] * 4)     # cell (0,1): var = 255^2/4
+    mm = oracle.classify_variance(img, 4, 100.0)
+    assert list(mm) == [1.0, 0.0, 1.0, 1.0]
+    assert list(oracle.classify_variance(img, 4, 255.0 ** 2 / 4)) == [1.0, 0.0, 1.0, 1.0]
+    assert list(oracle.classify_variance(img, 4, 255.0 ** 2 / 4 + 1e-9)) == [1.0] * 4
+    assert list(oracle.classify_variance(img, 4, 0.0)) == [0.0] * 4  # var >= 0 always
