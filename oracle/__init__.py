@@ -461,3 +461,22 @@ class _Ref:
 
 _ref_path = os.path.join(HERE, "_ref", "libdppix_ref.so")
 ref = _Ref(_ref_path) if os.path.exists(_ref_path) else None
+
+
+lib.or_log1p_glibc.restype = C.c_double
+lib.or_log1p_glibc.argtypes = [C.c_double]
+lib.or_log1p_glibc_mismatches.restype = C.c_long
+lib.or_log1p_glibc_mismatches.argtypes = [C.c_void_p, C.c_long, C.POINTER(C.c_double)]
+
+
+def log1p_glibc(x: float) -> float:
+    """Restatement of glibc 2.39's FMA-variant log1p (see or_log1p_glibc)."""
+    return lib.or_log1p_glibc(x)
+
+
+def log1p_glibc_mismatches(xs) -> tuple:
+    """(count, first mismatching x) of or_log1p_glibc vs the host libm's log1p."""
+    xs = np.ascontiguousarray(xs, dtype=np.float64)
+    first = C.c_double(0.0)
+    n = lib.or_log1p_glibc_mismatches(xs.ctypes.data, xs.size, C.byref(first))
+    return n, first.value

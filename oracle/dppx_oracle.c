@@ -110,6 +110,94 @@ double or_uniform_from_bits(uint64_t bits) {
   return u;
 }
 
+/* glibc 2.39 log1p (sysdeps/ieee754/dbl-64/s_log1p.c, fdlibm algorithm with
+ * an Estrin-split polynomial) as its x86-64 FMA ifunc variant evaluates it --
+ * the libm the reference's std::log1p (noise.cpp:110) resolves to on FMA
+ * hosts. Test infrastructure: pins the device twin (glibc_log1p in
+ * dppx_device.cuh) against the host libm; the oracle's own noise keeps calling
+ * libm's log1p. Built with -ffp-contract=off, so only the explicit fma() calls
+ * are fused. */
+static uint32_t hi32(double x) { uint64_t b; memcpy(&b, &x, 8); return (uint32_t)(b >> 32); }
+static double with_hi32(double x, uint32_t hi) {
+  uint64_t b; memcpy(&b, &x, 8);
+  b = ((uint64_t)hi << 32) | (b & 0xffffffffu);
+  memcpy(&x, &b, 8);
+  return x;
+}
+double or_log1p_glibc(double x) {
+  const double ln2_hi = 0x1.62e42fee00000p-1, ln2_lo = 0x1.a39ef35793c76p-33;
+  const double Lp1 = 0x1.5555555555593p-1, Lp2 = 0x1.999999997fa04p-2,
+               Lp3 = 0x1.2492494229359p-2, Lp4 = 0x1.c71c51d8e78afp-3,
+               Lp5 = 0x1.7466496cb03dep-3, Lp6 = 0x1.39a09d078c69fp-3,
+               Lp7 = 0x1.2f112df3e5244p-3;
+  const int32_t hx = (int32_t)hi32(x);
+  const int32_t ax = hx & 0x7fffffff;
+  int32_t k = 1, hu = 0;
+  double f = 0.0, c = 0.0;
+  if (hx < 0x3FDA827A) {
+    if (ax >= 0x3ff00000) return x == -1.0 ? -INFINITY : NAN;
+    if (ax < 0x3e200000) return ax < 0x3c900000 ? x : fma(-(x * x), 0.5, x);
+    if (hx > 0 || hx <= (int32_t)0xbfd2bec3) { k = 0; f = x; hu = 1; }
+  } else if (hx >= 0x7ff00000) {
+    return x + x;
+  }
+  if (k != 0) {
+    double u;
+    if (hx < 0x43400000) {
+      u = x + 1.0;
+      hu = (int32_t)hi32(u);
+      k = (hu >> 20) - 1023;
+      c = k > 0 ? 1.0 - (u - x) : x - (u - 1.0);
+      c /= u;
+    } else {
+      u = x;
+      hu = (int32_t)hi32(u);
+      k = (hu >> 20) - 1023;
+      c = 0.0;
+    }
+    hu &= 0x000fffff;
+    if (hu < 0x6a09e) {
+      u = with_hi32(u, (uint32_t)(hu | 0x3ff00000));
+    } else {
+      k += 1;
+      u = with_hi32(u, (uint32_t)(hu | 0x3fe00000));
+      hu = (0x00100000 - hu) >> 2;
+    }
+    f = u - 1.0;
+  }
+  const double hfsq = (f * 0.5) * f;
+  const double dk = (double)k;
+  if (hu == 0) {
+    if (f == 0.0) return k == 0 ? 0.0 : fma(dk, ln2_hi, fma(dk, ln2_lo, c));
+    const double R = fma(-f, 0x1.5555555555555p-1, 1.0) * hfsq;
+    if (k == 0) return f - R;
+    return fma(dk, ln2_hi, -((R - fma(dk, ln2_lo, c)) - f));
+  }
+  const double s = f / (f + 2.0);
+  const double z = s * s;
+  const double R2 = fma(z, Lp3, Lp2), R3 = fma(z, Lp5, Lp4), R4 = fma(z, Lp7, Lp6);
+  const double z2 = z * z, z4 = z2 * z2, z6 = z2 * z4;
+  double R = fma(z, Lp1, z2 * R2);
+  R = fma(z4, R3, R);
+  R = fma(z6, R4, R);
+  const double t = (R + hfsq) * s;
+  if (k == 0) return f - (hfsq - t);
+  return fma(dk, ln2_hi, -((hfsq - (fma(dk, ln2_lo, c) + t)) - f));
+}
+
+/* Number of xs where or_log1p_glibc and the linked libm's log1p differ in any bit. */
+long or_log1p_glibc_mismatches(const double* xs, long n, double* first_bad) {
+  long bad = 0;
+  for (long i = 0; i < n; ++i) {
+    const double a = or_log1p_glibc(xs[i]), b = log1p(xs[i]);
+    if (memcmp(&a, &b, 8) != 0 && !(isnan(a) && isnan(b))) {
+      if (bad == 0 && first_bad) *first_bad = xs[i];
+      ++bad;
+    }
+  }
+  return bad;
+}
+
 /* laplace_from_uniform: noise.cpp:107-110, evaluation order kept:
  * (sign * sigma) * -log1p(-2|u|). */
 double or_laplace_from_uniform(double u, double sigma) {

@@ -13,6 +13,8 @@
 
 #include <cstdint>
 
+#include <math_constants.h>
+
 #include "dppx_params.h"
 
 namespace dppx {
@@ -70,10 +72,87 @@ __device__ __forceinline__ double uniform_from_bits(uint64_t bits) {
   return u;
 }
 
+// log1p exactly as the reference's libm evaluates it. std::log1p (noise.cpp:110)
+// resolves to glibc 2.39's sysdeps/ieee754/dbl-64/s_log1p.c (the fdlibm
+// algorithm with an Estrin-split polynomial) in its x86-64 FMA/AVX2 ifunc
+// variant, i.e. with GCC's FMA contractions. Every operation below, including
+// which ones are fused, follows that compiled sequence, so the noise doubles
+// are bit-identical to the reference's (oracle twin: or_log1p_glibc, checked
+// against the host libm in tests/test_oracle_kats.py). Domain used here:
+// x = -2|u| in (-1, 0]; the other branches are kept for completeness.
+__device__ __noinline__ double glibc_log1p(double x) {
+  const double ln2_hi = 0x1.62e42fee00000p-1, ln2_lo = 0x1.a39ef35793c76p-33;
+  const double Lp1 = 0x1.5555555555593p-1, Lp2 = 0x1.999999997fa04p-2,
+               Lp3 = 0x1.2492494229359p-2, Lp4 = 0x1.c71c51d8e78afp-3,
+               Lp5 = 0x1.7466496cb03dep-3, Lp6 = 0x1.39a09d078c69fp-3,
+               Lp7 = 0x1.2f112df3e5244p-3;
+  const int hx = __double2hiint(x);
+  const int ax = hx & 0x7fffffff;
+  int k = 1, hu = 0;
+  double f = 0.0, c = 0.0;
+  if (hx < 0x3FDA827A) {
+    if (ax >= 0x3ff00000) return x == -1.0 ? -CUDART_INF : CUDART_NAN;
+    if (ax < 0x3e200000) {
+      if (ax < 0x3c900000) return x;
+      return __fma_rn(-__dmul_rn(x, x), 0.5, x);
+    }
+    if (hx > 0 || hx <= static_cast<int>(0xbfd2bec3)) {
+      k = 0;
+      f = x;
+      hu = 1;
+    }
+  } else if (hx >= 0x7ff00000) {
+    return __dadd_rn(x, x);
+  }
+  if (k != 0) {
+    double u;
+    if (hx < 0x43400000) {
+      u = __dadd_rn(x, 1.0);
+      hu = __double2hiint(u);
+      k = (hu >> 20) - 1023;
+      c = k > 0 ? __dsub_rn(1.0, __dsub_rn(u, x)) : __dsub_rn(x, __dsub_rn(u, 1.0));
+      c = __ddiv_rn(c, u);
+    } else {
+      u = x;
+      hu = __double2hiint(u);
+      k = (hu >> 20) - 1023;
+      c = 0.0;
+    }
+    hu &= 0x000fffff;
+    if (hu < 0x6a09e) {
+      u = __hiloint2double(hu | 0x3ff00000, __double2loint(u));
+    } else {
+      k += 1;
+      u = __hiloint2double(hu | 0x3fe00000, __double2loint(u));
+      hu = (0x00100000 - hu) >> 2;
+    }
+    f = __dsub_rn(u, 1.0);
+  }
+  const double hfsq = __dmul_rn(__dmul_rn(f, 0.5), f);
+  const double dk = static_cast<double>(k);
+  if (hu == 0) {
+    if (f == 0.0) return k == 0 ? 0.0 : __fma_rn(dk, ln2_hi, __fma_rn(dk, ln2_lo, c));
+    const double R = __dmul_rn(__fma_rn(-f, 0x1.5555555555555p-1, 1.0), hfsq);
+    if (k == 0) return __dsub_rn(f, R);
+    return __fma_rn(dk, ln2_hi, -__dsub_rn(__dsub_rn(R, __fma_rn(dk, ln2_lo, c)), f));
+  }
+  const double s = __ddiv_rn(f, __dadd_rn(f, 2.0));
+  const double z = __dmul_rn(s, s);
+  const double R2 = __fma_rn(z, Lp3, Lp2), R3 = __fma_rn(z, Lp5, Lp4), R4 = __fma_rn(z, Lp7, Lp6);
+  const double z2 = __dmul_rn(z, z), z4 = __dmul_rn(z2, z2), z6 = __dmul_rn(z2, z4);
+  double R = __fma_rn(z, Lp1, __dmul_rn(z2, R2));
+  R = __fma_rn(z4, R3, R);
+  R = __fma_rn(z6, R4, R);
+  const double t = __dmul_rn(__dadd_rn(R, hfsq), s);
+  if (k == 0) return __dsub_rn(f, __dsub_rn(hfsq, t));
+  const double w = __dsub_rn(hfsq, __dadd_rn(__fma_rn(dk, ln2_lo, c), t));
+  return __fma_rn(dk, ln2_hi, -__dsub_rn(w, f));
+}
+
 // laplace_from_uniform, noise.cpp:107-110: (sign * sigma) * -log1p(-2|u|).
 __device__ __forceinline__ double laplace_from_uniform(double u, double sigma) {
   const double sign = u < 0.0 ? -1.0 : 1.0;
-  const double l = log1p(__dmul_rn(-2.0, fabs(u)));
+  const double l = glibc_log1p(__dmul_rn(-2.0, fabs(u)));
   return __dmul_rn(__dmul_rn(sign, sigma), -l);
 }
 

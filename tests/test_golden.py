@@ -25,8 +25,10 @@ def test_noise_vectors():
         assert oracle.uniform_from_bits(int(v["bits"])) == float.fromhex(v["u"])
         worst = max(worst, ulps(oracle.laplace_at(seed, *v["key"], v["sigma"]),
                                 float.fromhex(v["laplace"])))
-    # glibc log1p is IFUNC-dispatched per CPU; identical on the generating host
-    assert worst <= 2
+    # glibc log1p is IFUNC-dispatched per CPU: identical on FMA hosts (the
+    # generating host), within 2 ulp on others
+    flags = open("/proc/cpuinfo").read().split()
+    assert worst == 0 if ("fma" in flags and "avx2" in flags) else worst <= 2
     assert oracle.uniform_from_bits(0) == float.fromhex(d["ends"]["u_of_0"])
     assert oracle.uniform_from_bits(2**64 - 1) == float.fromhex(d["ends"]["u_of_max"])
 

@@ -14,6 +14,16 @@ pytestmark = pytest.mark.gpu
 G = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
+def test_device_noise_equals_reference_golden_draws(ctx):
+    """Laplace doubles drawn on the device == the reference's laplace_at values
+    recorded in noise.json (bit for bit, incl. the log1p evaluation)."""
+    import json
+    d = json.load(open(os.path.join(G, "noise.json")))
+    for v in d["draws"]:
+        got = ctx.device_laplace(int(v["seed"]), np.array([v["key"]], np.uint32), v["sigma"])[0]
+        assert got == float.fromhex(v["laplace"]), v
+
+
 def test_small_cases_through_dropin_api(ctx):
     z = np.load(os.path.join(G, "small_cases.npz"))
     for k in sorted({k.split("_")[0] for k in z.files}):

@@ -135,3 +135,21 @@ def test_variance_classification_restatement():
     assert list(oracle.classify_variance(img, 4, 255.0 ** 2 / 4)) == [1.0, 0.0, 1.0, 1.0]
     assert list(oracle.classify_variance(img, 4, 255.0 ** 2 / 4 + 1e-9)) == [1.0] * 4
     assert list(oracle.classify_variance(img, 4, 0.0)) == [0.0] * 4  # var >= 0 always
+
+
+def test_log1p_restatement_is_the_host_libm():
+    """The restated glibc log1p (twin of the device's) equals the host libm bit for
+    bit on the noise domain -2|u| and on random bit patterns (FMA hosts: glibc's
+    ifunc picks the FMA variant the restatement follows)."""
+    flags = open("/proc/cpuinfo").read().split()
+    if not ("fma" in flags and "avx2" in flags):
+        pytest.skip("host libm uses the non-FMA log1p variant")
+    rng = np.random.default_rng(11)
+    bits = rng.integers(0, 2**63, 2_000_000, dtype=np.uint64)
+    u = (bits >> np.uint64(11)).astype(np.float64) * 2.0 ** -53 - 0.5
+    assert oracle.log1p_glibc_mismatches(-2.0 * np.abs(u))[0] == 0
+    assert oracle.log1p_glibc_mismatches(rng.integers(0, 2**64, 10**6, dtype=np.uint64)
+                                         .view(np.float64))[0] == 0
+    edge = np.array([0.0, -0.0, -1.0, -1 + 2**-52, -2**-54, -2**-29, -0.2929, -0.29289,
+                     0.41422, -0.5, 1e300, np.inf, -np.inf, np.nan])
+    assert oracle.log1p_glibc_mismatches(edge)[0] == 0
