@@ -20,6 +20,7 @@
 
 #include "../../include/dppx_gpu.h"
 #include "dppx_params.h"
+#include "maskpack.h"
 
 namespace dppx {
 using StatsKernel = void (*)(const CUtensorMap, const CUtensorMap, const StatsArgs);
@@ -110,6 +111,11 @@ struct dppx_ctx {
   int chunk_frames = 0;
   bool exact_noise = false;
   double var_tau = 0.0;  // AdaptiveVariance host calls
+  // bit-packed mask transport (maskpack.h): pinned staging per slot + packer pool
+  dppx::MaskPacker* packer = nullptr;
+  uint32_t* mbits_pinned[2] = {nullptr, nullptr};
+  size_t mbits_pinned_n[2] = {0, 0};
+  int mask_bits_mode = -1;  // -1 unset (env DPPX_MASK_BITS, default on), 0 off, 1 on
   // stats
   bool timing = false;
   std::vector<PendingTiming> pending;
@@ -334,7 +340,7 @@ struct VarianceSource {  // extension: classify cells by the frames' own varianc
 int classify(dppx_ctx* ctx, const BatchGeom& g, int planes, bool from_payload, const uint8_t* mask,
              int64_t mpitch, int64_t mfstride, uint8_t* payload, const uint8_t* payload_in,
              int64_t pstride, uint32_t* payload_len, const uint32_t* in_len,
-             const VarianceSource* var = nullptr) {
+             const VarianceSource* var = nullptr, bool mask_bits = false) {
   ClassifyArgs a{};
   a.g = g;
   a.planes = planes;
@@ -352,7 +358,8 @@ int classify(dppx_ctx* ctx, const BatchGeom& g, int planes, bool from_payload, c
   a.mpitch = mpitch;
   a.mfstride = mfstride;
   a.vec = 1;
-  if (!from_payload && !var) {
+  a.mask_bits = mask_bits ? 1 : 0;
+  if (!from_payload && !var && !mask_bits) {
     if (g.b % 16 == 0 && aligned16(mask) && mpitch % 16 == 0 && mfstride % 16 == 0) a.vec = 16;
     else if (g.b % 4 == 0 && (reinterpret_cast<uintptr_t>(mask) & 3) == 0 && mpitch % 4 == 0 &&
              mfstride % 4 == 0)
@@ -480,7 +487,7 @@ int pixelize_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img, c
                  uint8_t* stats, int64_t sstride, uint32_t* payload_len, uint8_t* out,
                  bool adaptive, DevBuf& dev_seeds, uint64_t*& pinned, size_t& pinned_n,
                  cudaEvent_t guard, bool record_guard, bool partial = false,
-                 double var_tau = std::nan("")) {
+                 double var_tau = std::nan(""), bool mask_bits = false) {
   BatchGeom g;
   if (int rc = geometry(ctx, d->height, d->width, d->channels, d->frames, pp->b,
                         adaptive ? pp->n : 1, &g, !partial))
@@ -521,7 +528,8 @@ int pixelize_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img, c
     if (int rc = ensure_scratch(ctx, g, g.F)) return rc;
     VarianceSource vs{img, d->pitch, d->frame_stride, var_tau};
     if (int rc = classify(ctx, g, g.F, false, mask, d->mask_pitch, d->mask_frame_stride, stats,
-                          nullptr, sstride, payload_len, nullptr, by_variance ? &vs : nullptr))
+                          nullptr, sstride, payload_len, nullptr, by_variance ? &vs : nullptr,
+                          mask_bits))
       return rc;
     a.cellinfo = static_cast<const uint32_t*>(ctx->cellinfo.p);
     a.rowprefix = static_cast<const uint32_t*>(ctx->rowprefix.p);
@@ -716,6 +724,15 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
   const bool dense_mask = op == HostOp::Adaptive && dmpitch != N && d->mask_pitch == N &&
                           d->mask_frame_stride == static_cast<int64_t>(N) * M;
   const bool dense_out = out && dpitch != row && d->out_pitch == row && d->out_frame_stride == row * M;
+  // Bit-packed mask transport: 1/8 of the mask's PCIe bytes (maskpack.h).
+  if (ctx->mask_bits_mode < 0) {
+    const char* env = std::getenv("DPPX_MASK_BITS");
+    ctx->mask_bits_mode = env && env[0] == '0' ? 0 : 1;
+  }
+  const bool try_bits = op == HostOp::Adaptive && ctx->mask_bits_mode == 1;
+  const int64_t wpr = dppx::mask_words_per_row(N);
+  const size_t bits_frame = static_cast<size_t>(wpr) * 4 * M;
+  if (try_bits && !ctx->packer) ctx->packer = dppx::mask_packer_create(0);
   for (int s = 0; s < 2 && s < chunks; ++s) {
     if (pix && ensure(ctx, ctx->img[s], static_cast<size_t>(dfs) * K)) return DPPX_ERR_OOM;
     if (op == HostOp::Adaptive && ensure(ctx, ctx->mask[s], static_cast<size_t>(dmfs) * K))
@@ -728,6 +745,14 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
       return DPPX_ERR_OOM;
     if (dense_mask && ensure(ctx, ctx->dense_mask[s], static_cast<size_t>(N) * M * K))
       return DPPX_ERR_OOM;
+    if (try_bits && ctx->mbits_pinned_n[s] < bits_frame * K) {
+      if (ctx->mbits_pinned[s]) CUDA_TRY(ctx, cudaFreeHost(ctx->mbits_pinned[s]));
+      ctx->mbits_pinned[s] = nullptr;
+      ctx->mbits_pinned_n[s] = 0;
+      CUDA_TRY(ctx, cudaHostAlloc(reinterpret_cast<void**>(&ctx->mbits_pinned[s]), bits_frame * K,
+                                  cudaHostAllocDefault));
+      ctx->mbits_pinned_n[s] = bits_frame * K;
+    }
   }
   cudaStream_t comp = ctx->stream;
   int f0 = 0;
@@ -754,7 +779,20 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
                                   ctx->s_in));
       ctx->kstats.h2d_bytes += static_cast<uint64_t>(Fk) * M * row;
     }
-    if (op == HostOp::Adaptive) {
+    bool bits = false;
+    if (try_bits) {
+      // The slot's staging buffer is free once chunk ci-2's copies finished.
+      if (ci >= 2) CUDA_TRY(ctx, cudaEventSynchronize(ctx->in_done[s]));
+      bits = dppx::pack_mask_bits(ctx->packer, mask + static_cast<int64_t>(f0) * d->mask_frame_stride,
+                                  d->mask_pitch, d->mask_frame_stride, M, N, Fk,
+                                  ctx->mbits_pinned[s], wpr);
+      if (bits) {
+        CUDA_TRY(ctx, cudaMemcpyAsync(dmask, ctx->mbits_pinned[s], bits_frame * Fk,
+                                      cudaMemcpyHostToDevice, ctx->s_in));
+        ctx->kstats.h2d_bytes += static_cast<uint64_t>(bits_frame) * Fk;
+      }
+    }
+    if (op == HostOp::Adaptive && !bits) {
       if (dense_mask)
         CUDA_TRY(ctx, cudaMemcpyAsync(ddmask, mask + static_cast<int64_t>(f0) * d->mask_frame_stride,
                                       static_cast<size_t>(N) * M * Fk, cudaMemcpyHostToDevice,
@@ -791,7 +829,7 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
       CUDA_TRY(ctx, launch_repitch(dimg, dpitch, ddense, row, row, static_cast<int64_t>(M) * Fk, comp));
       timing_end(ctx, &pt);
     }
-    if (dense_mask) {
+    if (dense_mask && !bits) {
       PendingTiming pt;
       timing_begin(ctx, DPPX_K_AUX, &pt);
       CUDA_TRY(ctx, launch_repitch(dmask, dmpitch, ddmask, N, N, static_cast<int64_t>(M) * Fk, comp));
@@ -801,8 +839,8 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
     dd.frames = Fk;
     dd.pitch = dpitch;
     dd.frame_stride = dfs;
-    dd.mask_pitch = dmpitch;
-    dd.mask_frame_stride = dmfs;
+    dd.mask_pitch = bits ? wpr * 4 : dmpitch;
+    dd.mask_frame_stride = bits ? static_cast<int64_t>(bits_frame) : dmfs;
     dd.out_pitch = dpitch;
     dd.out_frame_stride = dfs;
     int rc;
@@ -818,7 +856,7 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
                         adaptive ? dlens : nullptr, out ? dout : nullptr, adaptive, ctx->sd[s],
                         ctx->sd_pinned[s], ctx->sd_pinned_n[s], ctx->comp_done[s], false,
                         op == HostOp::Reference,
-                        op == HostOp::AdaptiveVariance ? ctx->var_tau : std::nan(""));
+                        op == HostOp::AdaptiveVariance ? ctx->var_tau : std::nan(""), bits);
     } else {
       rc = expand_dev(ctx, &dd, dstats, dstride, in_lens ? dlens : nullptr, b, n, dout, adaptive);
     }
@@ -993,12 +1031,14 @@ void dppx_ctx_destroy(dppx_ctx* ctx) {
     for (DevBuf* b : sb)
       if (b->p) cudaFree(b->p);
     if (ctx->sd_pinned[s]) cudaFreeHost(ctx->sd_pinned[s]);
+    if (ctx->mbits_pinned[s]) cudaFreeHost(ctx->mbits_pinned[s]);
     cudaEventDestroy(ctx->in_done[s]);
     cudaEventDestroy(ctx->comp_done[s]);
     cudaEventDestroy(ctx->out_done[s]);
   }
   if (ctx->seeds_pinned) cudaFreeHost(ctx->seeds_pinned);
   cudaEventDestroy(ctx->seeds_ev);
+  dppx::mask_packer_destroy(ctx->packer);
   for (auto& pt : ctx->pending) {
     cudaEventDestroy(pt.start);
     cudaEventDestroy(pt.stop);

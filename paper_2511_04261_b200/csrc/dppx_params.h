@@ -62,6 +62,7 @@ struct ClassifyArgs {
   const uint8_t* mask;       // from_payload == 0
   int64_t mpitch, mfstride;
   int vec;                   // 16, 4 or 1: widest aligned load for the mask rows
+  int mask_bits;             // mask rows are packed bits (u32 words, maskpack.h), mpitch in bytes
   uint8_t* payload;          // from_payload == 0: mask means + S written for C planes
   const uint8_t* payload_in; // from_payload == 1
   int64_t pstride;

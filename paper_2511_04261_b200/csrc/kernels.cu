@@ -121,11 +121,47 @@ __device__ __forceinline__ uint32_t mask_cell_sum_vec(const ClassifyArgs& a, con
   return s;
 }
 
+// Mask sum of cell (r, c) from bit-packed rows (host pipeline transport,
+// maskpack.h): bit (j % 32) of word (j / 32) is mask[i][j] in {0, 1}.
+__device__ __noinline__ uint32_t mask_cell_sum_bits(const ClassifyArgs& a, const uint8_t* base,
+                                                    int r, int c) {
+  const BatchGeom& g = a.g;
+  const int b = g.b;
+  const int j0 = c * b;
+  uint32_t s = 0;
+  if (j0 + b <= g.N) {
+    const int j1 = j0 + b - 1;
+    const int w0 = j0 >> 5, w1 = j1 >> 5;
+    const uint32_t m0 = ~0u << (j0 & 31), m1 = ~0u >> (31 - (j1 & 31));
+    for (int i = r * b; i < r * b + b; ++i) {
+      const uint32_t* row = reinterpret_cast<const uint32_t*>(
+          base + static_cast<int64_t>(reflect_index(i, g.M)) * a.mpitch);
+      if (w0 == w1) {
+        s += __popc(__ldg(row + w0) & m0 & m1);
+      } else {
+        s += __popc(__ldg(row + w0) & m0) + __popc(__ldg(row + w1) & m1);
+        for (int w = w0 + 1; w < w1; ++w) s += __popc(__ldg(row + w));
+      }
+    }
+    return s;
+  }
+  for (int i = r * b; i < r * b + b; ++i) {
+    const uint32_t* row = reinterpret_cast<const uint32_t*>(
+        base + static_cast<int64_t>(reflect_index(i, g.M)) * a.mpitch);
+    for (int j = j0; j < j0 + b; ++j) {
+      const int jj = reflect_index(j, g.N);
+      s += (__ldg(row + (jj >> 5)) >> (jj & 31)) & 1u;
+    }
+  }
+  return s;
+}
+
 __device__ __forceinline__ uint32_t mask_cell_sum(const ClassifyArgs& a, const uint8_t* base,
                                                   int r, int c) {
   const BatchGeom& g = a.g;
   const int b = g.b;
   const int j0 = c * b;
+  if (a.mask_bits) return mask_cell_sum_bits(a, base, r, c);
   if (j0 + b <= g.N && a.vec > 1) {
     if (a.vec == 16) {
       if (b == 16) return mask_cell_sum_vec<16>(a, base, r, j0);

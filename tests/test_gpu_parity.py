@@ -369,3 +369,24 @@ def test_variance_classification_extension(ctx, b, n, C):
             assert np.array_equal(img[f], ri)
         # records made this way reconstruct like any other
         assert np.array_equal(ctx.reassemble(pls, M, N, b, n, channels=C, frames=F), img)
+
+
+def test_mask_transport_bits_and_byte_fallback(ctx):
+    """Host pipeline ships masks as packed bits; a chunk holding mask bytes outside
+    {0, 1} (legal for the reference arithmetic) is sent as bytes instead. Both
+    must give the oracle's payloads, including ragged widths (N % 32 != 0)."""
+    rng = np.random.default_rng(21)
+    for M, N, C, b, n in [(70, 37, 3, 8, 2), (45, 100, 1, 16, 4), (64, 96, 3, 16, 2)]:
+        F = 4
+        frames = rng.integers(0, 256, (F, M, N, C), np.uint8)
+        masks = rng.integers(0, 2, (F, M, N), np.uint8)
+        masks[2] *= 3           # values {0, 3}: mean thresholds differ from bits
+        masks[3, ::3] = 255
+        p = dp.make_privacy_params(0.5, 16, b, n)
+        seeds = dp.plane_seeds(9, F, C)
+        for chunk in (1, 0):
+            ctx.set_chunk_frames(chunk)
+            pls, img = ctx.pixelize_adaptive(frames, masks, p, dp.NOISE_KEYED, seeds)
+            rp, ri = _oracle_adaptive(frames, masks, p, "keyed", seeds)
+            assert pls == rp and np.array_equal(img, ri), (M, N, chunk)
+        ctx.set_chunk_frames(0)
