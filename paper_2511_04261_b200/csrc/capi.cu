@@ -245,6 +245,8 @@ int geometry(dppx_ctx* ctx, int M, int N, int C, int F, int b, int n, BatchGeom*
                    "(use b <= min(M, N))");
   if (n < 1 || b % n != 0)
     return set_err(ctx, DPPX_ERR_INVALID, "invalid subgrid factor");
+  if (static_cast<int64_t>(gg.grid_rows) * gg.grid_cols > 0x7FFFFFFFll)
+    return set_err(ctx, DPPX_ERR_INVALID, "image too large: more than 2^31 - 1 grids per plane");
   g->M = M;
   g->N = N;
   g->C = C;

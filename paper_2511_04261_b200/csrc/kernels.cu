@@ -852,10 +852,11 @@ constexpr int kGenericThreads = 128;
 __global__ void __launch_bounds__(kGenericThreads) k_stats_generic(const StatsArgs a) {
   const BatchGeom& g = a.g;
   const int c = blockIdx.x * kGenericThreads + threadIdx.x;
-  const int r = blockIdx.y;
   if (c >= g.GC) return;
-  const int gidx = r * g.GC + c;
+  // grid-stride over rows and frames: GR or F may exceed the 65535 grid limit
+  for (int r = blockIdx.y; r < g.GR; r += gridDim.y)
   for (int f = blockIdx.z; f < g.F; f += gridDim.z) {
+    const int gidx = r * g.GC + c;
     const uint8_t* img = a.img + static_cast<int64_t>(f) * a.fstride;
     bool simple = true;
     uint32_t slot_s = 0, S_tot = 0;
@@ -926,11 +927,11 @@ __global__ void __launch_bounds__(kGenericThreads) k_stats_generic(const StatsAr
 __global__ void __launch_bounds__(kGenericThreads) k_expand(const ExpandArgs a) {
   const BatchGeom& g = a.g;
   const int c = blockIdx.x * kGenericThreads + threadIdx.x;
-  const int r = blockIdx.y;
   if (c >= g.GC) return;
-  const int gidx = r * g.GC + c;
   const int P = g.F * g.C;
+  for (int r = blockIdx.y; r < g.GR; r += gridDim.y)
   for (int p = blockIdx.z; p < P; p += gridDim.z) {
+    const int gidx = r * g.GC + c;
     const int f = p / g.C, ch = p % g.C;
     const uint8_t* st = a.stats + static_cast<int64_t>(p) * a.sstride;
     uint8_t* o = a.out + static_cast<int64_t>(f) * a.ofstride;
@@ -1062,8 +1063,12 @@ __global__ void __launch_bounds__(256) k_mse(const MetricArgs m) {
   __syncthreads();
   unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};
   const int rows_per_block = 8;
-  const int f = blockIdx.y;
   const int row_bytes = m.N * m.C;
+  for (int f = blockIdx.y; f < m.F; f += gridDim.y) {  // F may exceed the 65535 grid limit
+  for (int ch = 0; ch < 4; ++ch) acc[ch] = 0ull;
+  __syncthreads();
+  if (threadIdx.x < 4) part[threadIdx.x] = 0ull;
+  __syncthreads();
   for (int i = blockIdx.x * rows_per_block; i < min(m.M, (blockIdx.x + 1) * rows_per_block); ++i) {
     const uint8_t* ra = m.a + static_cast<int64_t>(f) * m.fstride + static_cast<int64_t>(i) * m.pitch;
     const uint8_t* rb = m.b + static_cast<int64_t>(f) * m.bfstride + static_cast<int64_t>(i) * m.bpitch;
@@ -1075,7 +1080,8 @@ __global__ void __launch_bounds__(256) k_mse(const MetricArgs m) {
   }
   for (int ch = 0; ch < m.C; ++ch) atomicAdd(&part[ch], acc[ch]);
   __syncthreads();
-  if (threadIdx.x < m.C) atomicAdd(&m.sums[f * m.C + threadIdx.x], part[threadIdx.x]);
+  if (threadIdx.x < m.C) atomicAdd(&m.sums[static_cast<int64_t>(f) * m.C + threadIdx.x], part[threadIdx.x]);
+  }
 }
 
 // One thread per (plane, window row): slides the 7x7 window along the row with
@@ -1150,7 +1156,7 @@ __global__ void __launch_bounds__(128) k_ssim_rows(const MetricArgs m) {
 
 cudaError_t launch_metrics(const MetricArgs& m, bool ssim, cudaStream_t s) {
   if (!ssim) {
-    dim3 grid((m.M + 7) / 8, m.F);
+    dim3 grid((m.M + 7) / 8, m.F < 65535 ? m.F : 65535);
     k_mse<<<grid, 256, 0, s>>>(m);
   } else {
     const int64_t threads = static_cast<int64_t>(m.F) * m.C * (m.M - 6);
@@ -1347,7 +1353,7 @@ cudaError_t launch_stats_tma(StatsKernel k, const CUtensorMap& tin, const CUtens
 }
 
 cudaError_t launch_stats_generic(const StatsArgs& a, cudaStream_t s) {
-  dim3 grid((a.g.GC + kGenericThreads - 1) / kGenericThreads, a.g.GR,
+  dim3 grid((a.g.GC + kGenericThreads - 1) / kGenericThreads, a.g.GR < 65535 ? a.g.GR : 65535,
             a.g.F < 65535 ? a.g.F : 65535);
   k_stats_generic<<<grid, kGenericThreads, 0, s>>>(a);
   return cudaGetLastError();
@@ -1355,7 +1361,8 @@ cudaError_t launch_stats_generic(const StatsArgs& a, cudaStream_t s) {
 
 cudaError_t launch_expand(const ExpandArgs& a, cudaStream_t s) {
   const int P = a.g.F * a.g.C;
-  dim3 grid((a.g.GC + kGenericThreads - 1) / kGenericThreads, a.g.GR, P < 65535 ? P : 65535);
+  dim3 grid((a.g.GC + kGenericThreads - 1) / kGenericThreads, a.g.GR < 65535 ? a.g.GR : 65535,
+            P < 65535 ? P : 65535);
   k_expand<<<grid, kGenericThreads, 0, s>>>(a);
   return cudaGetLastError();
 }

@@ -390,3 +390,34 @@ def test_mask_transport_bits_and_byte_fallback(ctx):
             rp, ri = _oracle_adaptive(frames, masks, p, "keyed", seeds)
             assert pls == rp and np.array_equal(img, ri), (M, N, chunk)
         ctx.set_chunk_frames(0)
+
+
+@pytest.mark.parametrize("M,N,C,b,n", [(70000, 3, 1, 1, 1), (3, 70000, 3, 1, 1), (70001, 5, 1, 2, 2),
+                                       (66000, 8, 3, 4, 2)])
+def test_extreme_aspect_frames(ctx, M, N, C, b, n):
+    """More than 65535 grid rows (or a single very long row): grid-stride launches."""
+    rng = np.random.default_rng(M + N)
+    frames = rng.integers(0, 256, (1, M, N, C), np.uint8)
+    masks = rng.integers(0, 2, (1, M, N), np.uint8)
+    p = dp.make_privacy_params(1.0, 16, b, n)
+    seeds = dp.plane_seeds(5, 1, C)
+    if n == 1:
+        means, img = ctx.pixelize_uniform(frames, p, dp.NOISE_KEYED, seeds)
+        rm, ri = _oracle_uniform(frames, p, "keyed", seeds)
+        assert np.array_equal(means, rm) and np.array_equal(img, ri)
+    pls, img = ctx.pixelize_adaptive(frames, masks, p, dp.NOISE_KEYED, seeds)
+    rp, ri = _oracle_adaptive(frames, masks, p, "keyed", seeds)
+    assert pls == rp and np.array_equal(img, ri)
+    assert np.array_equal(ctx.reassemble(pls, M, N, b, n, channels=C), img)
+
+
+def test_mse_more_than_65535_frames(ctx):
+    F, M, N = 70000, 7, 9
+    rng = np.random.default_rng(4)
+    a = rng.integers(0, 256, (F, M, N, 1), np.uint8)
+    b = rng.integers(0, 256, (F, M, N, 1), np.uint8)
+    got = ctx.metrics(a, b, "mse")
+    d = (a.astype(np.int64) - b.astype(np.int64)) ** 2
+    assert np.allclose(got, d.reshape(F, -1).sum(1) / (M * N), rtol=1e-15, atol=0)
+    for f in (0, 65534, 65535, 65536, F - 1):  # frames past the 65535 grid limit
+        assert got[f] == oracle.mse(a[f], b[f])
