@@ -516,6 +516,13 @@ class Context:
             self._h, C.byref(desc), _ptr(img), C.byref(params), C.byref(noise_struct),
             _ptr(means), _ptr(out)), "pixelize_uniform_dev")
 
+    def pixelize_adaptive_variance_dev(self, desc: FramesDesc, img, tau, params, noise_struct,
+                                       payload, payload_stride, payload_len=None, out=None):
+        self._check(_lib.dppx_pixelize_adaptive_variance_dev(
+            self._h, C.byref(desc), _ptr(img), tau, C.byref(params), C.byref(noise_struct),
+            _ptr(payload), payload_stride, _ptr(payload_len), _ptr(out)),
+            "pixelize_adaptive_variance_dev")
+
     def reassemble_dev(self, desc, payload, payload_stride, payload_len, b, n, out):
         self._check(_lib.dppx_reassemble_dev(self._h, C.byref(desc), _ptr(payload),
                                              payload_stride, _ptr(payload_len), b, n, _ptr(out)),

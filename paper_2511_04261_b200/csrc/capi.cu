@@ -25,6 +25,8 @@
 namespace dppx {
 using StatsKernel = void (*)(const CUtensorMap, const CUtensorMap, const StatsArgs);
 StatsKernel select_stats_kernel(int C, int b, int n, bool adaptive, bool packed);
+StatsKernel select_stats_kernel_var(int C, int b, int n);
+cudaError_t launch_gather_stage(const GatherArgs& a, cudaStream_t s);
 int stats_threads();
 int stats_tile_px();
 int stats_max_stages();
@@ -105,6 +107,7 @@ struct dppx_ctx {
   cudaEvent_t seeds_ev = nullptr;
   // host-pipeline staging (2 slots)
   DevBuf img[2], mask[2], out[2], stats[2], lens[2], inj[2], sd[2], dense[2], dense_mask[2];
+  DevBuf var_flags, var_stage;  // fused variance classification staging
   uint64_t* sd_pinned[2] = {nullptr, nullptr};
   size_t sd_pinned_n[2] = {0, 0};
   cudaEvent_t in_done[2] = {}, comp_done[2] = {}, out_done[2] = {};
@@ -386,7 +389,38 @@ int classify(dppx_ctx* ctx, const BatchGeom& g, int planes, bool from_payload, c
   return DPPX_OK;
 }
 
+constexpr int kNoFusedPath = -1;  // internal: fused variance K1 not applicable
+
+// K0 mode 3: the fused variance K1's per-cell flags -> slots, S, lengths and
+// the 1.0f / 0.0f mask means of every channel payload.
+int classify_flags(dppx_ctx* ctx, const BatchGeom& g, const uint8_t* flags, uint8_t* payload,
+                   int64_t pstride, uint32_t* payload_len) {
+  ClassifyArgs a{};
+  a.g = g;
+  a.planes = g.F;
+  a.from_payload = 3;
+  a.flags = flags;
+  a.vec = 1;
+  a.payload = payload;
+  a.pstride = pstride;
+  a.payload_len = payload_len;
+  a.cellinfo = static_cast<uint32_t*>(ctx->cellinfo.p);
+  a.rowcnt = static_cast<uint32_t*>(ctx->rowcnt.p);
+  a.rowprefix = static_cast<uint32_t*>(ctx->rowprefix.p);
+  a.totals = static_cast<uint32_t*>(ctx->totals.p);
+  a.counters = static_cast<uint32_t*>(ctx->counters.p);
+  a.status = static_cast<int*>(ctx->status.p);
+  a.area = static_cast<double>(g.b) * g.b;
+  PendingTiming pt;
+  timing_begin(ctx, DPPX_K_CLASSIFY, &pt);
+  CUDA_TRY(ctx, launch_classify(a, ctx->stream));
+  timing_end(ctx, &pt);
+  return DPPX_OK;
+}
+
 // K1 (fast, TMA-staged) when the geometry and alignment allow, else K1g.
+// With a.var_flags set (fused variance), only the staged VAR kernel qualifies:
+// returns kNoFusedPath without launching anything when it does not apply.
 int run_stats(dppx_ctx* ctx, StatsArgs& a) {
   const BatchGeom& g = a.g;
   StatsKernel k = nullptr;
@@ -401,7 +435,8 @@ int run_stats(dppx_ctx* ctx, StatsArgs& a) {
   const int64_t stage_bytes = static_cast<int64_t>(g.b) * tile * g.C;
   a.pack = 1;
   a.slot_px = tile;
-  if (2 * padded_px <= tile && (padded_px * g.C) % 16 == 0) {
+  const bool var = a.var_flags != nullptr;
+  if (!var && 2 * padded_px <= tile && (padded_px * g.C) % 16 == 0) {
     const int64_t stride = round_up(static_cast<int64_t>(g.b) * padded_px * g.C, 128);
     const int pk = static_cast<int>(std::min<int64_t>(tile / padded_px, stage_bytes / stride));
     if (pk >= 2) {
@@ -410,7 +445,8 @@ int run_stats(dppx_ctx* ctx, StatsArgs& a) {
     }
   }
   a.slot_stride = static_cast<int>(round_up(static_cast<int64_t>(g.b) * a.slot_px * g.C, 128));
-  k = select_stats_kernel(g.C, g.b, g.n, a.adaptive != 0, a.pack > 1);
+  k = var ? select_stats_kernel_var(g.C, g.b, g.n)
+          : select_stats_kernel(g.C, g.b, g.n, a.adaptive != 0, a.pack > 1);
   a.row_slack = a.pitch >= round_up(row_bytes, 16) ? 1 : 0;
   const int box_bytes = a.slot_px * g.C;
   // Input rows: the tensor's inner extent is rounded UP to 8 bytes when the
@@ -461,6 +497,7 @@ int run_stats(dppx_ctx* ctx, StatsArgs& a) {
     timing_begin(ctx, DPPX_K_STATS, &pt);
     CUDA_TRY(ctx, launch_stats_tma(k, tin, tout, a, grid, smem, ctx->stream));
   } else {
+    if (var) return kNoFusedPath;  // caller takes the 2-pass variance path
     timing_begin(ctx, DPPX_K_GENERIC, &pt);
     if (g.F > 0) CUDA_TRY(ctx, launch_stats_generic(a, ctx->stream));
   }
@@ -526,6 +563,41 @@ int pixelize_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img, c
   if (int rc = prepare_noise(ctx, nz, g.F * g.C, dev_injected, g, pp, &a.noise, ctx->stream,
                              dev_seeds, pinned, pinned_n, guard, record_guard))
     return rc;
+  const char* fused_env = std::getenv("DPPX_VAR_FUSED");  // A/B knob: "0" = 2-pass path
+  if (by_variance && !partial && !(fused_env && fused_env[0] == '0')) {
+    // Fused: K1 classifies each cell by its own variance while summing (one
+    // read of the frames), stages the statistics per cell; K0 (mode 3) turns
+    // the flags into slots and k_gather_stage compacts the payloads.
+    if (int rc = ensure_scratch(ctx, g, g.F)) return rc;
+    const int64_t nn = static_cast<int64_t>(g.n) * g.n;
+    const int64_t stage_stride = round_up(static_cast<int64_t>(g.G) * nn, 16);
+    if (int rc = ensure(ctx, ctx->var_flags, static_cast<size_t>(g.F) * g.G)) return rc;
+    if (int rc = ensure(ctx, ctx->var_stage, static_cast<size_t>(stage_stride) * g.F * g.C)) return rc;
+    StatsArgs v = a;
+    v.var_tau = var_tau;
+    v.var_flags = static_cast<uint8_t*>(ctx->var_flags.p);
+    v.stage = static_cast<uint8_t*>(ctx->var_stage.p);
+    v.stage_stride = stage_stride;
+    const int rc = run_stats(ctx, v);
+    if (rc != kNoFusedPath) {
+      if (rc) return rc;
+      if (int rc2 = classify_flags(ctx, g, v.var_flags, stats, sstride, payload_len)) return rc2;
+      GatherArgs ga{};
+      ga.g = g;
+      ga.stage = v.stage;
+      ga.stage_stride = stage_stride;
+      ga.cellinfo = static_cast<const uint32_t*>(ctx->cellinfo.p);
+      ga.rowprefix = static_cast<const uint32_t*>(ctx->rowprefix.p);
+      ga.totals = static_cast<const uint32_t*>(ctx->totals.p);
+      ga.payload = stats;
+      ga.pstride = sstride;
+      PendingTiming pt;
+      timing_begin(ctx, DPPX_K_AUX, &pt);
+      CUDA_TRY(ctx, launch_gather_stage(ga, ctx->stream));
+      timing_end(ctx, &pt);
+      return DPPX_OK;
+    }
+  }
   if (adaptive) {
     if (int rc = ensure_scratch(ctx, g, g.F)) return rc;
     VarianceSource vs{img, d->pitch, d->frame_stride, var_tau};
@@ -1025,7 +1097,7 @@ void dppx_ctx_destroy(dppx_ctx* ctx) {
   cudaDeviceSynchronize();
   DevBuf* bufs[] = {&ctx->cellinfo, &ctx->rowcnt, &ctx->rowprefix, &ctx->totals, &ctx->counters,
                     &ctx->status, &ctx->seeds, &ctx->keys, &ctx->dbl, &ctx->work,
-                    &ctx->met_a, &ctx->met_b, &ctx->met_out};
+                    &ctx->met_a, &ctx->met_b, &ctx->met_out, &ctx->var_flags, &ctx->var_stage};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (int s = 0; s < 2; ++s) {

@@ -63,6 +63,7 @@ struct ClassifyArgs {
   int64_t mpitch, mfstride;
   int vec;                   // 16, 4 or 1: widest aligned load for the mask rows
   int mask_bits;             // mask rows are packed bits (u32 words, maskpack.h), mpitch in bytes
+  const uint8_t* flags;      // mode 3: per-cell simple flags [F][G] from the fused variance K1
   uint8_t* payload;          // from_payload == 0: mask means + S written for C planes
   const uint8_t* payload_in; // from_payload == 1
   int64_t pstride;
@@ -115,6 +116,26 @@ struct StatsArgs {
   // slot_px*C bytes (the TMA box is stored densely).
   int pack, slot_px, slot_stride;
   int row_slack;             // 1: input pitch >= roundup(N*C, 16), loads may read the slack
+  // EXTENSION, fused variance classification (k_stats_tma<..., VAR = true>):
+  // each cell is classified by its own variance in the same pass; statistics
+  // go to a per-cell staging area (slot positions need the whole frame's simple
+  // count) that K0 (mode 3) + k_gather_stage compact into the payload.
+  double var_tau;
+  uint8_t* var_flags;        // [F][G]: 1 simple, 0 complex
+  uint8_t* stage;            // [F*C][stage_stride]: cell g at g*n*n (+ sr*n + sc)
+  int64_t stage_stride;
+};
+
+// Compaction of fused-variance staging into DPPX payloads (after K0 mode 3).
+struct GatherArgs {
+  BatchGeom g;
+  const uint8_t* stage;
+  int64_t stage_stride;
+  const uint32_t* cellinfo;  // [F][G]
+  const uint32_t* rowprefix; // [F][GR]
+  const uint32_t* totals;    // [F]
+  uint8_t* payload;
+  int64_t pstride;
 };
 
 // K2: statistics -> pixels.

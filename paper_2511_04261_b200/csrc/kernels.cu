@@ -236,9 +236,11 @@ __global__ void __launch_bounds__(kClassifyThreads) k_classify(const ClassifyArg
         float mean;
         if (a.from_payload == 1) {
           mean = mm_in[cell];
-        } else if (a.from_payload == 2) {
-          mean = cell_is_complex_var(a, a.img + static_cast<int64_t>(p) * a.fstride, r, c) ? 0.0f
-                                                                                          : 1.0f;
+        } else if (a.from_payload >= 2) {
+          const bool cx = a.from_payload == 2
+                              ? cell_is_complex_var(a, a.img + static_cast<int64_t>(p) * a.fstride, r, c)
+                              : a.flags[static_cast<int64_t>(p) * g.G + cell] == 0;
+          mean = cx ? 0.0f : 1.0f;
           for (int ch = 0; ch < g.C; ++ch)
             reinterpret_cast<float*>(a.payload + (static_cast<int64_t>(p) * g.C + ch) * a.pstride)
                 [cell] = mean;
@@ -517,6 +519,15 @@ __device__ __forceinline__ void accumulate_row(const uint8_t* row, uint32_t (&ac
   }
 }
 
+// Sum of squares of all bytes of one 4-px strip row (variance extension).
+template <int C>
+__device__ __forceinline__ uint32_t square_row(const uint8_t* row, uint32_t acc) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(row);
+#pragma unroll
+  for (int k = 0; k < (C == 4 ? 4 : C); ++k) acc = __dp4a(w[k], w[k], acc);
+  return acc;
+}
+
 // Values of the C channels of one statistic, computed by the GL lanes of a
 // lane group (each lane draws a subset of channels) and shared by shuffles.
 template <int C, int GL>
@@ -549,7 +560,7 @@ __device__ __forceinline__ void group_values(const StatsArgs& a, const DrawEnv& 
   }
 }
 
-template <int C, int B4, int NSUB, bool ADAPTIVE, bool PACKED>
+template <int C, int B4, int NSUB, bool ADAPTIVE, bool PACKED, bool VAR = false>
 __global__ void __launch_bounds__(kStatsThreads)
     k_stats_tma(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
                 const StatsArgs a) {
@@ -559,6 +570,7 @@ __global__ void __launch_bounds__(kStatsThreads)
   constexpr int ROWB = kTilePx * C;
   constexpr uint32_t STAGE = B * ROWB;
   static_assert(SB % 4 == 0 && 32 % B4 == 0, "fast-path geometry");
+  static_assert(!VAR || (ADAPTIVE && !PACKED), "variance staging: wide adaptive frames only");
 
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full_bar[kMaxStages];  // TMA bytes landed
@@ -675,7 +687,7 @@ __global__ void __launch_bounds__(kStatsThreads)
       const int qf = q.fg * units_pack<PACKED>(a) + jj;
       const int qcell = PACKED ? (q.px0 + lpx) / B : q.px0 / B + t / B4;
       if (!PACKED || qf < g.F) {
-        if (ADAPTIVE && qcell < g.GC) {
+        if (ADAPTIVE && !VAR && qcell < g.GC) {
           m.info = __ldg(&a.cellinfo[static_cast<int64_t>(qf) * g.G + q.r * g.GC + qcell]);
           m.rowpre = __ldg(&a.rowprefix[static_cast<int64_t>(qf) * g.GR + q.r]);
           m.stot = __ldg(&a.totals[qf]);
@@ -761,11 +773,107 @@ __global__ void __launch_bounds__(kStatsThreads)
       }
     }
 
+    const bool emit = a.out != nullptr;
+    uint8_t* mystrip = st + jj * a.slot_stride + lpx * C;
+    if constexpr (VAR) {
+      // Sums of every vertical subcell and the sum of squares, then the
+      // variance test on the whole cell (same integers and IEEE divide as
+      // K0 mode 2 / or_classify_variance), then the draws.
+      uint32_t sub[NSUB][C];
+      uint32_t sq = 0;
+#pragma unroll
+      for (int vs = 0; vs < NSUB; ++vs) {
+#pragma unroll
+        for (int ch = 0; ch < C; ++ch) sub[vs][ch] = 0;
+#pragma unroll
+        for (int i = 0; i < SB; ++i) {
+          const uint8_t* row = mystrip + (vs * SB + i) * srb;
+          accumulate_row<C>(row, sub[vs]);
+          sq = square_row<C>(row, sq);
+        }
+      }
+      next = load_meta(k + 1);
+      uint32_t tot[C];
+      uint32_t s1 = 0;
+#pragma unroll
+      for (int ch = 0; ch < C; ++ch) {
+        tot[ch] = 0;
+#pragma unroll
+        for (int vs = 0; vs < NSUB; ++vs) tot[ch] += sub[vs][ch];
+        s1 += tot[ch];
+      }
+#pragma unroll
+      for (int o = 1; o < B4; o <<= 1) {
+        s1 += __shfl_xor_sync(0xFFFFFFFFu, s1, o);
+        sq += __shfl_xor_sync(0xFFFFFFFFu, sq, o);
+      }
+      const long long ns = static_cast<long long>(C) * B * B;
+      const double num = static_cast<double>(ns * static_cast<long long>(sq) -
+                                             static_cast<long long>(s1) * static_cast<long long>(s1));
+      const bool simple = !(__ddiv_rn(num, __dmul_rn(static_cast<double>(ns), static_cast<double>(ns))) >=
+                            a.var_tau);
+      if (active && lic == 0) a.var_flags[static_cast<int64_t>(f) * g.G + gidx] = simple ? 1 : 0;
+      const int nn = NSUB * NSUB;
+#pragma unroll 1
+      for (int vs = 0; vs < NSUB; ++vs) {
+        uint32_t acc[C];
+#pragma unroll
+        for (int ch = 0; ch < C; ++ch) {
+          acc[ch] = sub[0][ch];
+#pragma unroll
+          for (int q = 1; q < NSUB; ++q)
+            if (q == vs) acc[ch] = sub[q][ch];
+        }
+#pragma unroll
+        for (int o = 1; o < SB4; o <<= 1)
+#pragma unroll
+          for (int ch = 0; ch < C; ++ch) acc[ch] += __shfl_xor_sync(0xFFFFFFFFu, acc[ch], o);
+        uint32_t val[C];
+        group_values<C, SB4>(a, env_sub, active && !simple, acc, cs, f, p.r, cell, vs, sc, val);
+        if (active && !simple) {
+          if (lic % SB4 == 0) {
+#pragma unroll
+            for (int ch = 0; ch < C; ++ch)
+              a.stage[static_cast<int64_t>(f * C + ch) * a.stage_stride +
+                      static_cast<int64_t>(gidx) * nn + vs * NSUB + sc] = static_cast<uint8_t>(val[ch]);
+          }
+          if (emit) {
+            uint32_t w[C];
+            pattern_words<C>(val, w);
+#pragma unroll
+            for (int i = 0; i < SB; ++i)
+#pragma unroll
+              for (int q = 0; q < C; ++q)
+                reinterpret_cast<uint32_t*>(mystrip + (vs * SB + i) * srb)[q] = w[q];
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 1; o < B4; o <<= 1)
+#pragma unroll
+        for (int ch = 0; ch < C; ++ch) tot[ch] += __shfl_xor_sync(0xFFFFFFFFu, tot[ch], o);
+      uint32_t val[C];
+      group_values<C, B4>(a, env_cell, active && simple, tot, cs, f, p.r, cell, 0, 0, val);
+      if (active && simple) {
+        if (lic == 0) {
+#pragma unroll
+          for (int ch = 0; ch < C; ++ch)
+            a.stage[static_cast<int64_t>(f * C + ch) * a.stage_stride + static_cast<int64_t>(gidx) * nn] =
+                static_cast<uint8_t>(val[ch]);
+        }
+        if (emit) {
+          uint32_t w[C];
+          pattern_words<C>(val, w);
+#pragma unroll
+          for (int i = 0; i < B; ++i)
+#pragma unroll
+            for (int q = 0; q < C; ++q) reinterpret_cast<uint32_t*>(mystrip + i * srb)[q] = w[q];
+        }
+      }
+    } else {
     uint32_t tot[C];
 #pragma unroll
     for (int ch = 0; ch < C; ++ch) tot[ch] = 0;
-    const bool emit = a.out != nullptr;
-    uint8_t* mystrip = st + jj * a.slot_stride + lpx * C;
 
     // Not unrolled over vertical subcells: keeps the hot loop small enough for
     // the instruction cache (the rows inside are unrolled).
@@ -838,6 +946,7 @@ __global__ void __launch_bounds__(kStatsThreads)
         }
       }
     }
+    }  // !VAR
 
     fence_proxy_async_smem();
     mbar_arrive(&done_bar[s]);
@@ -1264,6 +1373,35 @@ __global__ void k_debug_laplace(uint64_t mixed_seed, const uint32_t* keys, int c
 }
 
 // ============================================================================
+// Fused-variance compaction: staged per-cell statistics -> DPPX payload slots
+// (simple value at 4G+4+slot, complex block at 4G+4+S+slot_c*n*n), using the
+// slots K0 (mode 3) derived from the flags K1 wrote.
+// ============================================================================
+__global__ void __launch_bounds__(kGenericThreads) k_gather_stage(const GatherArgs a) {
+  const BatchGeom& g = a.g;
+  const int nn = g.n * g.n;
+  const int P = g.F * g.C;
+  for (int p = blockIdx.y; p < P; p += gridDim.y) {
+    const int f = p / g.C;
+    const uint8_t* src = a.stage + static_cast<int64_t>(p) * a.stage_stride;
+    uint8_t* dst = a.payload + static_cast<int64_t>(p) * a.pstride + 4ll * g.G + 4;
+    const uint32_t S = __ldg(&a.totals[f]);
+    for (int gi = blockIdx.x * kGenericThreads + threadIdx.x; gi < g.G; gi += gridDim.x * kGenericThreads) {
+      const uint32_t info = __ldg(&a.cellinfo[static_cast<int64_t>(f) * g.G + gi]);
+      const int r = gi / g.GC;
+      const uint32_t slot_s = __ldg(&a.rowprefix[static_cast<int64_t>(f) * g.GR + r]) + (info >> 1);
+      const uint8_t* cs = src + static_cast<int64_t>(gi) * nn;
+      if (info & 1u) {
+        dst[slot_s] = cs[0];
+      } else {
+        uint8_t* d = dst + S + static_cast<int64_t>(static_cast<uint32_t>(gi) - slot_s) * nn;
+        for (int k = 0; k < nn; ++k) d[k] = cs[k];
+      }
+    }
+  }
+}
+
+// ============================================================================
 // Host-side launchers (called from capi.cu)
 // ============================================================================
 using StatsKernel = void (*)(const CUtensorMap, const CUtensorMap, const StatsArgs);
@@ -1286,6 +1424,35 @@ StatsKernel pick_b(int b, int n) {
   }
 #undef DPPX_CASE
   return nullptr;
+}
+
+template <int C>
+StatsKernel pick_var(int b, int n) {
+#define DPPX_CASE(B4v, NS) \
+  if (b == 4 * (B4v) && n == (NS)) return k_stats_tma<C, B4v, NS, true, false, true>;
+  DPPX_CASE(2, 2)
+  DPPX_CASE(4, 2)
+  DPPX_CASE(4, 4)
+  DPPX_CASE(8, 2)
+  DPPX_CASE(8, 4)
+  DPPX_CASE(8, 8)
+#undef DPPX_CASE
+  return nullptr;
+}
+
+// Fused variance classification (wide frames only; else the 2-pass path).
+StatsKernel select_stats_kernel_var(int C, int b, int n) {
+  if (C == 1) return pick_var<1>(b, n);
+  if (C == 3) return pick_var<3>(b, n);
+  return nullptr;
+}
+
+cudaError_t launch_gather_stage(const GatherArgs& a, cudaStream_t s) {
+  const int P = a.g.F * a.g.C;
+  const int bx = std::min((a.g.G + kGenericThreads - 1) / kGenericThreads, 64);
+  dim3 grid(bx > 0 ? bx : 1, P < 65535 ? P : 65535);
+  k_gather_stage<<<grid, kGenericThreads, 0, s>>>(a);
+  return cudaGetLastError();
 }
 
 StatsKernel select_stats_kernel(int C, int b, int n, bool adaptive, bool packed) {

@@ -421,3 +421,49 @@ def test_mse_more_than_65535_frames(ctx):
     assert np.allclose(got, d.reshape(F, -1).sum(1) / (M * N), rtol=1e-15, atol=0)
     for f in (0, 65534, 65535, 65536, F - 1):  # frames past the 65535 grid limit
         assert got[f] == oracle.mse(a[f], b[f])
+
+
+@pytest.mark.parametrize("C,b,n", [(3, 16, 4), (1, 32, 8), (3, 8, 2)])
+def test_variance_fused_single_pass_equals_two_pass_and_oracle(ctx, C, b, n):
+    """Fused variance K1 (classify while summing, stage, K0 mode 3, gather) ==
+    the 2-pass path (K0 mode 2 + K1) == the CPU restatement, at 1080p (multi-
+    tile rows, padded last grid row for b = 32)."""
+    import os
+    import torch
+    F, M, N = 3, 1080, 1920
+    dev = torch.device("cuda:0")
+    pitch = N * C
+    img = torch.empty((F, M, pitch), dtype=torch.uint8, device=dev)
+    d = dp._desc(M, N, C, F)
+    ctx.synth_frames_dev(d, 101, 0, img, None)
+    ctx.synchronize()
+    host = img.cpu().numpy().reshape(F, M, N, C)
+    p = dp.make_privacy_params(0.5, 16, b, n)
+    cap = dp.adaptive_payload_capacity(M, N, b, n)
+    stride = (cap + 15) & ~15
+    seeds = dp.plane_seeds(42, F, C)
+    nz, keep = dp.Context._noise(dp.NOISE_KEYED, seeds)
+    tau = {16: 5000.0, 32: 1500.0, 8: 4500.0}[b]  # about the median cell variance
+    res = {}
+    for mode in ("1", "0"):
+        os.environ["DPPX_VAR_FUSED"] = mode
+        try:
+            payload = torch.zeros((F * C, stride), dtype=torch.uint8, device=dev)
+            lens = torch.zeros(F * C, dtype=torch.int32, device=dev)
+            out = torch.empty_like(img)
+            ctx.pixelize_adaptive_variance_dev(d, img, tau, p, nz, payload, stride, lens, out)
+            ctx.synchronize()
+        finally:
+            del os.environ["DPPX_VAR_FUSED"]
+        ln = lens.cpu().numpy()
+        pl = payload.cpu().numpy()
+        res[mode] = ([bytes(pl[i, : ln[i]]) for i in range(F * C)], out.cpu().numpy())
+    assert res["1"][0] == res["0"][0] and np.array_equal(res["1"][1], res["0"][1])
+    G = dp.grid_dims(M, N, b).grid_count()
+    S = [int.from_bytes(x[4 * G:4 * G + 4], "little") for x in res["1"][0]]
+    assert 0 < S[0] < G  # a real mix of simple and complex cells
+    f = F - 1
+    rp, ri = oracle.pixelize_adaptive_variance(host[f], b, n, p.sigma, p.sigma_sub, tau, "keyed",
+                                               seeds[f * C:(f + 1) * C], frame=f)
+    assert res["1"][0][f * C:(f + 1) * C] == rp
+    assert np.array_equal(res["1"][1].reshape(F, M, N, C)[f], ri)
