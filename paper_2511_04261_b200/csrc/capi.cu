@@ -570,7 +570,8 @@ int pixelize_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img, c
     // the flags into slots and k_gather_stage compacts the payloads.
     if (int rc = ensure_scratch(ctx, g, g.F)) return rc;
     const int64_t nn = static_cast<int64_t>(g.n) * g.n;
-    const int64_t stage_stride = round_up(static_cast<int64_t>(g.G) * nn, 16);
+    const int64_t stage_cx = round_up(static_cast<int64_t>(g.G), 16);
+    const int64_t stage_stride = round_up(stage_cx + static_cast<int64_t>(g.G) * nn, 16);
     if (int rc = ensure(ctx, ctx->var_flags, static_cast<size_t>(g.F) * g.G)) return rc;
     if (int rc = ensure(ctx, ctx->var_stage, static_cast<size_t>(stage_stride) * g.F * g.C)) return rc;
     StatsArgs v = a;
@@ -578,6 +579,7 @@ int pixelize_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img, c
     v.var_flags = static_cast<uint8_t*>(ctx->var_flags.p);
     v.stage = static_cast<uint8_t*>(ctx->var_stage.p);
     v.stage_stride = stage_stride;
+    v.stage_cx = stage_cx;
     const int rc = run_stats(ctx, v);
     if (rc != kNoFusedPath) {
       if (rc) return rc;
@@ -586,6 +588,7 @@ int pixelize_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img, c
       ga.g = g;
       ga.stage = v.stage;
       ga.stage_stride = stage_stride;
+      ga.stage_cx = stage_cx;
       ga.cellinfo = static_cast<const uint32_t*>(ctx->cellinfo.p);
       ga.rowprefix = static_cast<const uint32_t*>(ctx->rowprefix.p);
       ga.totals = static_cast<const uint32_t*>(ctx->totals.p);

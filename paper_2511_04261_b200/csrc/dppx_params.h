@@ -122,15 +122,16 @@ struct StatsArgs {
   // count) that K0 (mode 3) + k_gather_stage compact into the payload.
   double var_tau;
   uint8_t* var_flags;        // [F][G]: 1 simple, 0 complex
-  uint8_t* stage;            // [F*C][stage_stride]: cell g at g*n*n (+ sr*n + sc)
-  int64_t stage_stride;
+  uint8_t* stage;            // [F*C][stage_stride]: simple value of cell g at g,
+                             // complex block at stage_cx + g*n*n (+ sr*n + sc)
+  int64_t stage_stride, stage_cx;
 };
 
 // Compaction of fused-variance staging into DPPX payloads (after K0 mode 3).
 struct GatherArgs {
   BatchGeom g;
   const uint8_t* stage;
-  int64_t stage_stride;
+  int64_t stage_stride, stage_cx;
   const uint32_t* cellinfo;  // [F][G]
   const uint32_t* rowprefix; // [F][GR]
   const uint32_t* totals;    // [F]

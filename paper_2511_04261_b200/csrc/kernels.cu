@@ -776,32 +776,25 @@ __global__ void __launch_bounds__(kStatsThreads)
     const bool emit = a.out != nullptr;
     uint8_t* mystrip = st + jj * a.slot_stride + lpx * C;
     if constexpr (VAR) {
-      // Sums of every vertical subcell and the sum of squares, then the
-      // variance test on the whole cell (same integers and IEEE divide as
-      // K0 mode 2 / or_classify_variance), then the draws.
-      uint32_t sub[NSUB][C];
+      // Pass 1 over the staged rows: per-channel cell sums and the sum of
+      // squares; the variance test on the whole cell (same integers and IEEE
+      // divide as K0 mode 2 / or_classify_variance); then the draws. Complex
+      // subcell sums are re-read from smem (cheap) instead of being held in
+      // registers, which keeps the kernel at the non-VAR occupancy.
+      uint32_t tot[C];
+#pragma unroll
+      for (int ch = 0; ch < C; ++ch) tot[ch] = 0;
       uint32_t sq = 0;
 #pragma unroll
-      for (int vs = 0; vs < NSUB; ++vs) {
-#pragma unroll
-        for (int ch = 0; ch < C; ++ch) sub[vs][ch] = 0;
-#pragma unroll
-        for (int i = 0; i < SB; ++i) {
-          const uint8_t* row = mystrip + (vs * SB + i) * srb;
-          accumulate_row<C>(row, sub[vs]);
-          sq = square_row<C>(row, sq);
-        }
+      for (int i = 0; i < B; ++i) {
+        const uint8_t* row = mystrip + i * srb;
+        accumulate_row<C>(row, tot);
+        sq = square_row<C>(row, sq);
       }
       next = load_meta(k + 1);
-      uint32_t tot[C];
       uint32_t s1 = 0;
 #pragma unroll
-      for (int ch = 0; ch < C; ++ch) {
-        tot[ch] = 0;
-#pragma unroll
-        for (int vs = 0; vs < NSUB; ++vs) tot[ch] += sub[vs][ch];
-        s1 += tot[ch];
-      }
+      for (int ch = 0; ch < C; ++ch) s1 += tot[ch];
 #pragma unroll
       for (int o = 1; o < B4; o <<= 1) {
         s1 += __shfl_xor_sync(0xFFFFFFFFu, s1, o);
@@ -813,38 +806,37 @@ __global__ void __launch_bounds__(kStatsThreads)
       const bool simple = !(__ddiv_rn(num, __dmul_rn(static_cast<double>(ns), static_cast<double>(ns))) >=
                             a.var_tau);
       if (active && lic == 0) a.var_flags[static_cast<int64_t>(f) * g.G + gidx] = simple ? 1 : 0;
-      const int nn = NSUB * NSUB;
+      constexpr int nn = NSUB * NSUB;
+      if (__any_sync(0xFFFFFFFFu, active && !simple)) {
 #pragma unroll 1
-      for (int vs = 0; vs < NSUB; ++vs) {
-        uint32_t acc[C];
+        for (int vs = 0; vs < NSUB; ++vs) {
+          uint32_t acc[C];
 #pragma unroll
-        for (int ch = 0; ch < C; ++ch) {
-          acc[ch] = sub[0][ch];
+          for (int ch = 0; ch < C; ++ch) acc[ch] = 0;
 #pragma unroll
-          for (int q = 1; q < NSUB; ++q)
-            if (q == vs) acc[ch] = sub[q][ch];
-        }
+          for (int i = 0; i < SB; ++i) accumulate_row<C>(mystrip + (vs * SB + i) * srb, acc);
 #pragma unroll
-        for (int o = 1; o < SB4; o <<= 1)
+          for (int o = 1; o < SB4; o <<= 1)
 #pragma unroll
-          for (int ch = 0; ch < C; ++ch) acc[ch] += __shfl_xor_sync(0xFFFFFFFFu, acc[ch], o);
-        uint32_t val[C];
-        group_values<C, SB4>(a, env_sub, active && !simple, acc, cs, f, p.r, cell, vs, sc, val);
-        if (active && !simple) {
-          if (lic % SB4 == 0) {
+            for (int ch = 0; ch < C; ++ch) acc[ch] += __shfl_xor_sync(0xFFFFFFFFu, acc[ch], o);
+          uint32_t val[C];
+          group_values<C, SB4>(a, env_sub, active && !simple, acc, cs, f, p.r, cell, vs, sc, val);
+          if (active && !simple) {
+            if (lic % SB4 == 0) {
 #pragma unroll
-            for (int ch = 0; ch < C; ++ch)
-              a.stage[static_cast<int64_t>(f * C + ch) * a.stage_stride +
-                      static_cast<int64_t>(gidx) * nn + vs * NSUB + sc] = static_cast<uint8_t>(val[ch]);
-          }
-          if (emit) {
-            uint32_t w[C];
-            pattern_words<C>(val, w);
+              for (int ch = 0; ch < C; ++ch)
+                a.stage[static_cast<int64_t>(f * C + ch) * a.stage_stride + a.stage_cx +
+                        static_cast<int64_t>(gidx) * nn + vs * NSUB + sc] = static_cast<uint8_t>(val[ch]);
+            }
+            if (emit) {
+              uint32_t w[C];
+              pattern_words<C>(val, w);
 #pragma unroll
-            for (int i = 0; i < SB; ++i)
+              for (int i = 0; i < SB; ++i)
 #pragma unroll
-              for (int q = 0; q < C; ++q)
-                reinterpret_cast<uint32_t*>(mystrip + (vs * SB + i) * srb)[q] = w[q];
+                for (int q = 0; q < C; ++q)
+                  reinterpret_cast<uint32_t*>(mystrip + (vs * SB + i) * srb)[q] = w[q];
+            }
           }
         }
       }
@@ -858,7 +850,7 @@ __global__ void __launch_bounds__(kStatsThreads)
         if (lic == 0) {
 #pragma unroll
           for (int ch = 0; ch < C; ++ch)
-            a.stage[static_cast<int64_t>(f * C + ch) * a.stage_stride + static_cast<int64_t>(gidx) * nn] =
+            a.stage[static_cast<int64_t>(f * C + ch) * a.stage_stride + gidx] =
                 static_cast<uint8_t>(val[ch]);
         }
         if (emit) {
@@ -1390,12 +1382,20 @@ __global__ void __launch_bounds__(kGenericThreads) k_gather_stage(const GatherAr
       const uint32_t info = __ldg(&a.cellinfo[static_cast<int64_t>(f) * g.G + gi]);
       const int r = gi / g.GC;
       const uint32_t slot_s = __ldg(&a.rowprefix[static_cast<int64_t>(f) * g.GR + r]) + (info >> 1);
-      const uint8_t* cs = src + static_cast<int64_t>(gi) * nn;
       if (info & 1u) {
-        dst[slot_s] = cs[0];
+        dst[slot_s] = __ldg(src + gi);
+        continue;
+      }
+      const uint8_t* cs = src + a.stage_cx + static_cast<int64_t>(gi) * nn;
+      uint8_t* d = dst + S + static_cast<int64_t>(static_cast<uint32_t>(gi) - slot_s) * nn;
+      if (nn % 4 == 0 && (reinterpret_cast<uintptr_t>(d) & 3) == 0) {
+        for (int k = 0; k < nn; k += 4)
+          *reinterpret_cast<uint32_t*>(d + k) = __ldg(reinterpret_cast<const uint32_t*>(cs + k));
       } else {
-        uint8_t* d = dst + S + static_cast<int64_t>(static_cast<uint32_t>(gi) - slot_s) * nn;
-        for (int k = 0; k < nn; ++k) d[k] = cs[k];
+        for (int k = 0; k < nn; k += 4) {  // staged blocks are 4-byte aligned when nn % 4 == 0
+          const int m = min(4, nn - k);
+          for (int q = 0; q < m; ++q) d[k + q] = __ldg(cs + k + q);
+        }
       }
     }
   }
