@@ -243,8 +243,11 @@ __device__ __forceinline__ DrawEnv make_env(int kind, bool exact_only, double ar
   return e;
 }
 
+// `inj` yields the caller-injected noise value (DPPX_NOISE_INJECTED only); it is
+// evaluated lazily so its index arithmetic stays off the common path.
+template <class Inj>
 __device__ __forceinline__ uint32_t quantize_stat(const DrawEnv& e, uint32_t sum, uint64_t bits,
-                                                  double injected) {
+                                                  const Inj& inj) {
   if (!e.exact_only) {
     if (e.kind == DPPX_NOISE_KEYED || e.kind == DPPX_NOISE_PHILOX) {
       const uint32_t q = fast_quantize(sum, e.inv_area, bits, e.sigmaf, e.margin);
@@ -254,7 +257,8 @@ __device__ __forceinline__ uint32_t quantize_stat(const DrawEnv& e, uint32_t sum
       return static_cast<uint32_t>(floorf(static_cast<float>(sum) * e.inv_area + 0.5f));
     }
   }
-  return exact_quantize(sum, e.area, e.kind, bits, e.sigma, injected);
+  return exact_quantize(sum, e.area, e.kind, bits, e.sigma,
+                        e.kind == DPPX_NOISE_INJECTED ? inj() : 0.0);
 }
 
 // ---- PTX wrappers: mbarrier + bulk async copies (sm_90+ / sm_100a) ---------
@@ -298,6 +302,31 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "}\n" ::"r"(addr),
       "r"(parity), "r"(0x100000u)
       : "memory");
+}
+
+// Wait for a phase with exponential __nanosleep backoff: for the producer warp,
+// whose waits are off the critical path when the consumers are the bottleneck
+// (a spinning try_wait loop there steals issue slots from them).
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 P, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  uint32_t ns = 32;
+  while (!mbar_test(bar, parity)) {
+    __nanosleep(ns);
+    ns = ns < 256 ? 2 * ns : 256;
+  }
 }
 
 // global -> shared bulk copy, completion counted on `bar` (bytes % 16 == 0,

@@ -337,11 +337,24 @@ __device__ __forceinline__ uint64_t draw_bits(const StatsArgs& a, uint64_t cs, i
   return 0ull;
 }
 
-__device__ __forceinline__ double injected_at(const StatsArgs& a, int f, int ch, int g_idx, int sr,
-                                              int sc) {
-  if (a.noise.kind != DPPX_NOISE_INJECTED) return 0.0;
-  const int64_t plane = static_cast<int64_t>(f) * a.g.C + ch;
-  return a.noise.injected[((plane * a.g.G + g_idx) * a.g.n + sr) * a.g.n + sc];
+__device__ __noinline__ double injected_value(const double* inj, int64_t plane, int G, int n,
+                                              int g_idx, int sr, int sc) {
+  return inj[((plane * G + g_idx) * n + sr) * n + sc];
+}
+
+// Lazy handle on one statistic's injected noise value (see quantize_stat):
+// only scalars are captured, so nothing of StatsArgs is copied to local memory.
+struct InjAt {
+  const double* inj;
+  int64_t plane;
+  int G, n, g_idx, sr, sc;
+  __device__ __forceinline__ double operator()() const {
+    return injected_value(inj, plane, G, n, g_idx, sr, sc);
+  }
+};
+
+__device__ __forceinline__ InjAt inj_at(const StatsArgs& a, int f, int ch, int g_idx, int sr, int sc) {
+  return InjAt{a.noise.injected, static_cast<int64_t>(f) * a.g.C + ch, a.g.G, a.g.n, g_idx, sr, sc};
 }
 
 __device__ __forceinline__ uint64_t cell_state(const StatsArgs& a, int f, int ch, int r, int c) {
@@ -552,7 +565,7 @@ __device__ __forceinline__ void group_values(const StatsArgs& a, const DrawEnv& 
           st = cs[k];
         }
       v = quantize_stat(env, s, draw_bits(a, st, f, ch, r, c, sr, sc),
-                        injected_at(a, f, ch, r * a.g.GC + c, sr, sc));
+                        inj_at(a, f, ch, r * a.g.GC + c, sr, sc));
     }
 #pragma unroll
     for (int k = c0; k < C && k < c0 + GL; ++k)
@@ -602,7 +615,8 @@ __global__ void __launch_bounds__(kStatsThreads)
       prefetch_tmap(&tm_out);
     }
     auto finish_unit = [&](int s, int use) {  // after consumers released stage s
-      mbar_wait(&done_bar[s], use & 1);        // every lane acquires the smem writes
+      if (lane == 0) mbar_wait_backoff(&done_bar[s], use & 1);
+      __syncwarp();  // orders the consumers' smem writes (acquired by lane 0) for the warp
       if (a.out) {
         const int uu = stage_unit[s];
         store_tail<C, B, PACKED>(a, uu, smem + s * STAGE, lane);
@@ -983,7 +997,7 @@ __global__ void __launch_bounds__(kGenericThreads) k_stats_generic(const StatsAr
           for (int j = j0; j < j0 + w; ++j) sum += row[j * g.C + ch];
         }
         const uint32_t v = quantize_stat(env, sum, draw_bits(a, cell_state(a, f, ch, r, c), f, ch, r, c, 0, 0),
-                                         injected_at(a, f, ch, gidx, 0, 0));
+                                         inj_at(a, f, ch, gidx, 0, 0));
         a.stats[static_cast<int64_t>(f * g.C + ch) * a.sstride + gidx] = static_cast<uint8_t>(v);
         if (a.out) {
           uint8_t* o = a.out + static_cast<int64_t>(f) * a.ofstride;
@@ -1007,7 +1021,7 @@ __global__ void __launch_bounds__(kGenericThreads) k_stats_generic(const StatsAr
             for (int j = j0; j < j0 + side; ++j) sum += row[reflect_index(j, g.N) * g.C + ch];
           }
           const uint32_t v = quantize_stat(env, sum, draw_bits(a, cs, f, ch, r, c, sr, sc),
-                                           injected_at(a, f, ch, gidx, sr, sc));
+                                           inj_at(a, f, ch, gidx, sr, sc));
           a.stats[static_cast<int64_t>(f * g.C + ch) * a.sstride +
                   stat_offset(a, simple, gidx, slot_s, S_tot, sr, sc)] = static_cast<uint8_t>(v);
           if (a.out) {

@@ -49,12 +49,14 @@ def main():
         ctx.synchronize()
         ctx.reset_stats()
         ctx.set_timing(True)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        evs[0].record(stream)
+        for i in range(args.steps):
             ctx.pixelize_adaptive_variance_dev(d, img, args.tau, p, nz, payload, stride, lens, out)
-        e1.record(stream)
+            evs[i + 1].record(stream)
+        e0, e1 = evs[0], evs[-1]
         e1.synchronize()
+        per = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
         st = ctx.stats()
         ctx.set_timing(False)
         ms = e0.elapsed_time(e1) / args.steps
@@ -62,6 +64,7 @@ def main():
         alg = F * M * N * C * 2 + pay  # frames read once + image written + payloads
         res["fused" if mode == "1" else "two_pass"] = {
             "ms_per_step": round(ms, 4),
+            "step_ms_min_max": [round(min(per), 4), round(max(per), 4)],
             "MP_per_s": round(F * M * N / 1e6 / (ms / 1e3), 1),
             "fps": round(F / (ms / 1e3), 1),
             "algorithmic_GB": round(alg / 1e9, 3),
