@@ -304,31 +304,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-// Wait for a phase with exponential __nanosleep backoff: for the producer warp,
-// whose waits are off the critical path when the consumers are the bottleneck
-// (a spinning try_wait loop there steals issue slots from them).
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n"
-      ".reg .pred P;\n"
-      "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 P, [%1], %2;\n"
-      "selp.u32 %0, 1, 0, P;\n"
-      "}\n"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-
-__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
-  uint32_t ns = 32;
-  while (!mbar_test(bar, parity)) {
-    __nanosleep(ns);
-    ns = ns < 256 ? 2 * ns : 256;
-  }
-}
-
 // global -> shared bulk copy, completion counted on `bar` (bytes % 16 == 0,
 // both addresses 16-byte aligned).
 __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes,

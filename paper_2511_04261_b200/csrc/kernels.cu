@@ -615,8 +615,7 @@ __global__ void __launch_bounds__(kStatsThreads)
       prefetch_tmap(&tm_out);
     }
     auto finish_unit = [&](int s, int use) {  // after consumers released stage s
-      if (lane == 0) mbar_wait_backoff(&done_bar[s], use & 1);
-      __syncwarp();  // orders the consumers' smem writes (acquired by lane 0) for the warp
+      mbar_wait(&done_bar[s], use & 1);        // every lane acquires the smem writes
       if (a.out) {
         const int uu = stage_unit[s];
         store_tail<C, B, PACKED>(a, uu, smem + s * STAGE, lane);
