@@ -492,7 +492,14 @@ def main():
         sample = cpu_reference_sample(M, N, C, b, n, m, eps, adaptive, args.cpu_seconds, frame0)
         if sample is not None:
             t = run_reference_once(sample, M, N, C, b, n, m, eps, adaptive)
+            # single-thread reference on one frame (all C planes), as SURVEY 8(d) asks
+            import oracle
+            k1 = min(C, sample["planes"].shape[0])
+            t1 = oracle.ref.time_planes(sample["planes"][:k1],
+                                        sample["masks"][:k1] if adaptive else None, not adaptive,
+                                        eps, m, b, n, 42, 1)
             cpu = {"value": round(sample["n_frames"] * M * N / 1e6 / t, 3), "unit": "MP/s",
+                   "single_thread_value": round(M * N / 1e6 / (t1 * C / k1), 3),
                    "cores": sample["workers"], "kind": "reference",
                    "sample": f"{sample['n_frames']} frames x {C} planes, pixelize_"
                              f"{'adaptive' if adaptive else 'parallel'} per plane (threads=1), "

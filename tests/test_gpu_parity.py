@@ -171,6 +171,14 @@ def test_philox_stream_is_laplace(ctx):
         cdf = 0.5 * math.exp(t / sigma) if t < 0 else 1 - 0.5 * math.exp(-t / sigma)
         ks = max(ks, abs(emp - cdf))
     assert ks < 1.62762 / math.sqrt(n) * 3, ks
+    # E|X| of Laplace(sigma) is sigma: the quantized residual's mean |x| within 1 %
+    # of its exact expectation (rounding shifts it from sigma).
+    def p_int(v):  # P(round-half-away(noise) == v), noise ~ Laplace(sigma), 128 + noise
+        lo, hi = v - 0.5, v + 0.5
+        cdf = lambda t: 0.5 * math.exp(t / sigma) if t < 0 else 1 - 0.5 * math.exp(-t / sigma)
+        return cdf(hi) - cdf(lo)
+    e_abs = sum(abs(v) * p_int(v) for v in range(-60, 61))
+    assert abs(np.abs(x).mean() - e_abs) < 0.01 * e_abs, (np.abs(x).mean(), e_abs)
     # determinism and frame sensitivity
     again, _ = ctx.pixelize_uniform(frame, p, dp.NOISE_PHILOX, [99], want_image=False)
     other, _ = ctx.pixelize_uniform(frame, p, dp.NOISE_PHILOX, [99], frame_base=1,
