@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <type_traits>
 
 #include "dppx_device.cuh"
 #include "dppx_params.h"
@@ -678,6 +679,19 @@ __global__ void __launch_bounds__(kStatsThreads)
   // Packed mode: byte offsets of the mirrored sources of the padding bytes
   // [N*C, GC*b*C) of a slot row (image.cpp:105-110), shared by all units.
   __shared__ uint16_t fill_src[128];
+  // Per-warp complex-draw tables (see the complex-cell block below).
+  constexpr int CPW = 32 / B4;           // cells per consumer warp
+  constexpr int NN = NSUB * NSUB;
+  using SumT = typename std::conditional<(SB * SB * 255 < 65536), uint16_t, uint32_t>::type;
+  struct CellRec {
+    int cw, f, cell, gidx;
+    int64_t off;
+  };
+  __shared__ SumT csum[VAR ? kConsumers / 32 : 1][VAR ? CPW : 1][VAR ? NN * C : 1];
+  __shared__ CellRec crec[VAR ? kConsumers / 32 : 1][VAR ? CPW : 1];
+  __shared__ uint64_t cstate[VAR ? kConsumers / 32 : 1][VAR ? CPW : 1][C];
+  const int wq = VAR ? (t >> 5) : 0;          // consumer warp
+  const int cw = VAR ? ((t & 31) / B4) : 0;   // cell within the warp
   if (PACKED) {
     const int v0 = g.N * C, pad = (g.GC * B - g.N) * C;
     for (int x = t; x < pad && x < 128; x += kConsumers) {
@@ -728,7 +742,7 @@ __global__ void __launch_bounds__(kStatsThreads)
     const int sc = lic / SB4;      // subcell column
     const bool active = (!PACKED || (in_slot && f < g.F)) && cell < g.GC;
     const int gidx = p.r * g.GC + cell;
-    const bool simple = !ADAPTIVE || (cur.info & 1u);
+    const bool simple0 = !ADAPTIVE || (cur.info & 1u);  // VAR: decided after the sums
     const uint32_t slot_s = cur.rowpre + (cur.info >> 1);
     const uint32_t S_tot = cur.stot;
     const int vbytes = valid_bytes<C, PACKED>(a, p.px0);
@@ -788,15 +802,14 @@ __global__ void __launch_bounds__(kStatsThreads)
 
     const bool emit = a.out != nullptr;
     uint8_t* mystrip = st + jj * a.slot_stride + lpx * C;
+    uint32_t tot[C];
+#pragma unroll
+    for (int ch = 0; ch < C; ++ch) tot[ch] = 0;
+    bool simple = simple0;
     if constexpr (VAR) {
       // Pass 1 over the staged rows: per-channel cell sums and the sum of
       // squares; the variance test on the whole cell (same integers and IEEE
-      // divide as K0 mode 2 / or_classify_variance); then the draws. Complex
-      // subcell sums are re-read from smem (cheap) instead of being held in
-      // registers, which keeps the kernel at the non-VAR occupancy.
-      uint32_t tot[C];
-#pragma unroll
-      for (int ch = 0; ch < C; ++ch) tot[ch] = 0;
+      // divide as K0 mode 2 / or_classify_variance).
       uint32_t sq = 0;
 #pragma unroll
       for (int i = 0; i < B; ++i) {
@@ -816,11 +829,25 @@ __global__ void __launch_bounds__(kStatsThreads)
       const long long ns = static_cast<long long>(C) * B * B;
       const double num = static_cast<double>(ns * static_cast<long long>(sq) -
                                              static_cast<long long>(s1) * static_cast<long long>(s1));
-      const bool simple = !(__ddiv_rn(num, __dmul_rn(static_cast<double>(ns), static_cast<double>(ns))) >=
-                            a.var_tau);
+      simple = !(__ddiv_rn(num, __dmul_rn(static_cast<double>(ns), static_cast<double>(ns))) >=
+                 a.var_tau);
       if (active && lic == 0) a.var_flags[static_cast<int64_t>(f) * g.G + gidx] = simple ? 1 : 0;
-      constexpr int nn = NSUB * NSUB;
-      if (__any_sync(0xFFFFFFFFu, active && !simple)) {
+    }
+
+    if constexpr (ADAPTIVE) {
+      // Complex cells. Direct mode (mask classification): the owner lanes of
+      // each subcell draw its C values (NSUB * ceil(C / SB4) serial draws per
+      // lane); masks are spatially coherent, so warps are mostly all-simple or
+      // all-complex. Compact mode (variance classification, which scatters
+      // complex cells): the owner lanes put the subcell sums into this warp's
+      // smem table and the warp's complex draws (cells x n*n x C) are dealt
+      // round-robin to all 32 lanes, so the lanes of simple cells do not idle
+      // through the serial draws (tools/k1_complex_sweep.py measures both).
+      constexpr bool compact = VAR;
+      const bool cx = active && !simple;
+      const unsigned cx_any = __ballot_sync(0xFFFFFFFFu, cx);
+      __syncwarp();  // the previous unit's reads of this warp's tables are done
+      if (!VAR || cx_any) {
 #pragma unroll 1
         for (int vs = 0; vs < NSUB; ++vs) {
           uint32_t acc[C];
@@ -828,86 +855,87 @@ __global__ void __launch_bounds__(kStatsThreads)
           for (int ch = 0; ch < C; ++ch) acc[ch] = 0;
 #pragma unroll
           for (int i = 0; i < SB; ++i) accumulate_row<C>(mystrip + (vs * SB + i) * srb, acc);
+          if constexpr (!VAR) {
 #pragma unroll
-          for (int o = 1; o < SB4; o <<= 1)
+            for (int ch = 0; ch < C; ++ch) tot[ch] += acc[ch];
+          }
+          if (cx_any) {
 #pragma unroll
-            for (int ch = 0; ch < C; ++ch) acc[ch] += __shfl_xor_sync(0xFFFFFFFFu, acc[ch], o);
-          uint32_t val[C];
-          group_values<C, SB4>(a, env_sub, active && !simple, acc, cs, f, p.r, cell, vs, sc, val);
-          if (active && !simple) {
-            if (lic % SB4 == 0) {
+            for (int o = 1; o < SB4; o <<= 1)
 #pragma unroll
-              for (int ch = 0; ch < C; ++ch)
-                a.stage[static_cast<int64_t>(f * C + ch) * a.stage_stride + a.stage_cx +
-                        static_cast<int64_t>(gidx) * nn + vs * NSUB + sc] = static_cast<uint8_t>(val[ch]);
-            }
-            if (emit) {
-              uint32_t w[C];
-              pattern_words<C>(val, w);
+              for (int ch = 0; ch < C; ++ch) acc[ch] += __shfl_xor_sync(0xFFFFFFFFu, acc[ch], o);
+            if constexpr (compact) {
+              if (cx && lic % SB4 == 0) {
 #pragma unroll
-              for (int i = 0; i < SB; ++i)
+                for (int ch = 0; ch < C; ++ch)
+                  csum[wq][cw][(vs * NSUB + sc) * C + ch] = static_cast<SumT>(acc[ch]);
+              }
+            } else {
+              uint32_t val[C];
+              group_values<C, SB4>(a, env_sub, cx, acc, cs, f, p.r, cell, vs, sc, val);
+              if (cx) {
+                if (lic % SB4 == 0) {
+                  const int64_t off =
+                      VAR ? a.stage_cx + static_cast<int64_t>(gidx) * NN + vs * NSUB + sc
+                          : stat_offset(a, false, gidx, slot_s, S_tot, vs, sc);
+                  uint8_t* dst = VAR ? a.stage : a.stats;
+                  const int64_t pst = VAR ? a.stage_stride : a.sstride;
 #pragma unroll
-                for (int q = 0; q < C; ++q)
-                  reinterpret_cast<uint32_t*>(mystrip + (vs * SB + i) * srb)[q] = w[q];
+                  for (int ch = 0; ch < C; ++ch)
+                    dst[static_cast<int64_t>(f * C + ch) * pst + off] = static_cast<uint8_t>(val[ch]);
+                }
+                if (emit) {
+                  uint32_t w[C];
+                  pattern_words<C>(val, w);
+#pragma unroll
+                  for (int i = 0; i < SB; ++i)
+#pragma unroll
+                    for (int q = 0; q < C; ++q)
+                      reinterpret_cast<uint32_t*>(mystrip + (vs * SB + i) * srb)[q] = w[q];
+                }
+              }
             }
           }
         }
       }
+      if constexpr (!VAR) next = load_meta(k + 1);
+      if (compact && cx_any) {
+        const unsigned leaders = __ballot_sync(0xFFFFFFFFu, cx && lic == 0);
+        if (cx && lic == 0) {
+          const int rank = __popc(leaders & ((1u << (t & 31)) - 1u));
+          CellRec& rec = crec[wq][rank];
+          rec.cw = cw;
+          rec.f = f;
+          rec.cell = cell;
+          rec.gidx = gidx;
+          rec.off = VAR ? a.stage_cx + static_cast<int64_t>(gidx) * NN
+                        : stat_offset(a, false, gidx, slot_s, S_tot, 0, 0);
 #pragma unroll
-      for (int o = 1; o < B4; o <<= 1)
-#pragma unroll
-        for (int ch = 0; ch < C; ++ch) tot[ch] += __shfl_xor_sync(0xFFFFFFFFu, tot[ch], o);
-      uint32_t val[C];
-      group_values<C, B4>(a, env_cell, active && simple, tot, cs, f, p.r, cell, 0, 0, val);
-      if (active && simple) {
-        if (lic == 0) {
-#pragma unroll
-          for (int ch = 0; ch < C; ++ch)
-            a.stage[static_cast<int64_t>(f * C + ch) * a.stage_stride + gidx] =
-                static_cast<uint8_t>(val[ch]);
+          for (int ch = 0; ch < C; ++ch) cstate[wq][rank][ch] = cs[ch];
         }
-        if (emit) {
-          uint32_t w[C];
-          pattern_words<C>(val, w);
-#pragma unroll
-          for (int i = 0; i < B; ++i)
-#pragma unroll
-            for (int q = 0; q < C; ++q) reinterpret_cast<uint32_t*>(mystrip + i * srb)[q] = w[q];
+        __syncwarp();
+        const int work = __popc(leaders) * NN * C;
+        for (int i = t & 31; i < work; i += 32) {
+          const int kk = i / (NN * C), rem = i - kk * (NN * C);
+          const int sidx = rem / C, ch = rem - sidx * C;
+          const int vs = sidx / NSUB, sc2 = sidx - vs * NSUB;
+          const CellRec& rec = crec[wq][kk];
+          const uint32_t sum = csum[wq][rec.cw][rem];
+          const uint32_t v =
+              quantize_stat(env_sub, sum, draw_bits(a, cstate[wq][kk][ch], rec.f, ch, p.r, rec.cell, vs, sc2),
+                            inj_at(a, rec.f, ch, rec.gidx, vs, sc2));
+          uint8_t* base = VAR ? a.stage + static_cast<int64_t>(rec.f * C + ch) * a.stage_stride
+                              : a.stats + static_cast<int64_t>(rec.f * C + ch) * a.sstride;
+          base[rec.off + sidx] = static_cast<uint8_t>(v);
+          csum[wq][rec.cw][rem] = static_cast<SumT>(v);
         }
-      }
-    } else {
-    uint32_t tot[C];
-#pragma unroll
-    for (int ch = 0; ch < C; ++ch) tot[ch] = 0;
-
-    // Not unrolled over vertical subcells: keeps the hot loop small enough for
-    // the instruction cache (the rows inside are unrolled).
+        __syncwarp();
+        if (emit && cx) {
 #pragma unroll 1
-    for (int vs = 0; vs < NSUB; ++vs) {
-      uint32_t acc[C];
+          for (int vs = 0; vs < NSUB; ++vs) {
+            uint32_t val[C];
 #pragma unroll
-      for (int ch = 0; ch < C; ++ch) acc[ch] = 0;
-#pragma unroll
-      for (int i = 0; i < SB; ++i) accumulate_row<C>(mystrip + (vs * SB + i) * srb, acc);
-#pragma unroll
-      for (int ch = 0; ch < C; ++ch) tot[ch] += acc[ch];
-      if constexpr (ADAPTIVE) {
-        // complex subcell (vs, sc): reduce its SB4 strips, draw at sigma_sub.
-#pragma unroll
-        for (int o = 1; o < SB4; o <<= 1)
-#pragma unroll
-          for (int ch = 0; ch < C; ++ch) acc[ch] += __shfl_xor_sync(0xFFFFFFFFu, acc[ch], o);
-        uint32_t val[C];
-        group_values<C, SB4>(a, env_sub, active && !simple, acc, cs, f, p.r, cell, vs, sc, val);
-        if (active && !simple) {
-          if (lic % SB4 == 0) {
-            const int64_t off = stat_offset(a, false, gidx, slot_s, S_tot, vs, sc);
-#pragma unroll
-            for (int ch = 0; ch < C; ++ch)
-              a.stats[static_cast<int64_t>(f * C + ch) * a.sstride + off] =
-                  static_cast<uint8_t>(val[ch]);
-          }
-          if (emit) {
+            for (int ch = 0; ch < C; ++ch) val[ch] = csum[wq][cw][(vs * NSUB + sc) * C + ch];
             uint32_t w[C];
             pattern_words<C>(val, w);
 #pragma unroll
@@ -918,12 +946,14 @@ __global__ void __launch_bounds__(kStatsThreads)
           }
         }
       }
+    } else {
+#pragma unroll
+      for (int i = 0; i < B; ++i) accumulate_row<C>(mystrip + i * srb, tot);
+      // Next unit's metadata: requested here (after the staged rows are
+      // summed) rather than at the top, so a 2-stage ring never stalls on the
+      // producer's previous store; its latency hides behind the epilogue.
+      next = load_meta(k + 1);
     }
-
-    // Next unit's metadata: requested here (after the staged rows are summed)
-    // rather than at the top, so a 2-stage ring never stalls on the producer's
-    // previous store; its latency hides behind this unit's epilogue.
-    next = load_meta(k + 1);
 
     // whole cell (uniform, or adaptive simple): reduce over B4 strips.
 #pragma unroll
@@ -935,11 +965,18 @@ __global__ void __launch_bounds__(kStatsThreads)
       group_values<C, B4>(a, env_cell, active && simple, tot, cs, f, p.r, cell, 0, 0, val);
       if (active && simple) {
         if (lic == 0) {
-          const int64_t off = stat_offset(a, true, gidx, slot_s, S_tot, 0, 0);
+          if constexpr (VAR) {
 #pragma unroll
-          for (int ch = 0; ch < C; ++ch)
-            a.stats[static_cast<int64_t>(f * C + ch) * a.sstride + off] =
-                static_cast<uint8_t>(val[ch]);
+            for (int ch = 0; ch < C; ++ch)
+              a.stage[static_cast<int64_t>(f * C + ch) * a.stage_stride + gidx] =
+                  static_cast<uint8_t>(val[ch]);
+          } else {
+            const int64_t off = stat_offset(a, true, gidx, slot_s, S_tot, 0, 0);
+#pragma unroll
+            for (int ch = 0; ch < C; ++ch)
+              a.stats[static_cast<int64_t>(f * C + ch) * a.sstride + off] =
+                  static_cast<uint8_t>(val[ch]);
+          }
         }
         if (emit) {
           uint32_t w[C];
@@ -951,7 +988,6 @@ __global__ void __launch_bounds__(kStatsThreads)
         }
       }
     }
-    }  // !VAR
 
     fence_proxy_async_smem();
     mbar_arrive(&done_bar[s]);
