@@ -549,28 +549,56 @@ __device__ __forceinline__ void group_values(const StatsArgs& a, const DrawEnv& 
                                              const uint32_t (&sum)[C], const uint64_t (&cs)[C],
                                              int f, int r, int c, int sr, int sc,
                                              uint32_t (&val)[C]) {
+  constexpr int NV = (C + GL - 1) / GL;  // channels this lane draws
+  if (!__any_sync(0xFFFFFFFFu, active)) {  // warp-uniform: nothing to draw
+#pragma unroll
+    for (int k = 0; k < C; ++k) val[k] = 0;
+    return;
+  }
   const int lane = threadIdx.x & 31;
   const int li = lane % GL;
   const int gb = lane - li;
+  uint32_t s[NV], q[NV];
+  uint64_t bits[NV];
 #pragma unroll
-  for (int c0 = 0; c0 < C; c0 += GL) {
-    const int ch = c0 + li;
-    uint32_t v = 0;
-    if (active && ch < C) {
-      uint32_t s = sum[0];
-      uint64_t st = cs[0];
+  for (int j = 0; j < NV; ++j) {
+    const int ch = j * GL + li;
+    s[j] = sum[0];
+    uint64_t st = cs[0];
 #pragma unroll
-      for (int k = 1; k < C; ++k)
-        if (ch == k) {
-          s = sum[k];
-          st = cs[k];
-        }
-      v = quantize_stat(env, s, draw_bits(a, st, f, ch, r, c, sr, sc),
-                        inj_at(a, f, ch, r * a.g.GC + c, sr, sc));
-    }
+    for (int k = 1; k < C; ++k)
+      if (ch == k) {
+        s[j] = sum[k];
+        st = cs[k];
+      }
+    bits[j] = draw_bits(a, st, f, ch, r, c, sr, sc);
+  }
+  // Phase 1: branch-free bounded estimates for all channels (independent
+  // chains the scheduler can interleave); phase 2: the rare exact draws.
+  if (!env.exact_only && (env.kind == DPPX_NOISE_KEYED || env.kind == DPPX_NOISE_PHILOX)) {
 #pragma unroll
-    for (int k = c0; k < C && k < c0 + GL; ++k)
-      val[k] = (GL == 1) ? v : __shfl_sync(0xFFFFFFFFu, v, gb + (k - c0));
+    for (int j = 0; j < NV; ++j) q[j] = fast_quantize(s[j], env.inv_area, bits[j], env.sigmaf, env.margin);
+  } else if (!env.exact_only && env.kind == DPPX_NOISE_NONE && env.pow2) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j)  // sum * 2^-k + 0.5 is exact in f32
+      q[j] = static_cast<uint32_t>(floorf(static_cast<float>(s[j]) * env.inv_area + 0.5f));
+  } else {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) q[j] = 0xFFFFFFFFu;
+  }
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int ch = j * GL + li;
+    if (active && ch < C && q[j] == 0xFFFFFFFFu)
+      q[j] = exact_quantize(s[j], env.area, env.kind, bits[j], env.sigma,
+                            env.kind == DPPX_NOISE_INJECTED ? inj_at(a, f, ch, r * a.g.GC + c, sr, sc)()
+                                                            : 0.0);
+  }
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+#pragma unroll
+    for (int k = j * GL; k < C && k < (j + 1) * GL; ++k)
+      val[k] = (GL == 1) ? q[j] : __shfl_sync(0xFFFFFFFFu, q[j], gb + (k - j * GL));
   }
 }
 
