@@ -124,19 +124,19 @@ __device__ __forceinline__ uint32_t mask_cell_sum_vec(const ClassifyArgs& a, con
 
 // Mask sum of cell (r, c) from bit-packed rows (host pipeline transport,
 // maskpack.h): bit (j % 32) of word (j / 32) is mask[i][j] in {0, 1}.
-__device__ __noinline__ uint32_t mask_cell_sum_bits(const ClassifyArgs& a, const uint8_t* base,
-                                                    int r, int c) {
-  const BatchGeom& g = a.g;
-  const int b = g.b;
+// Scalars only: a reference to the kernel's parameter struct would force a
+// per-thread local-memory copy of it.
+__device__ __noinline__ uint32_t mask_cell_sum_bits(const uint8_t* base, int64_t mpitch, int M, int N,
+                                                    int b, int r, int c) {
   const int j0 = c * b;
   uint32_t s = 0;
-  if (j0 + b <= g.N) {
+  if (j0 + b <= N) {
     const int j1 = j0 + b - 1;
     const int w0 = j0 >> 5, w1 = j1 >> 5;
     const uint32_t m0 = ~0u << (j0 & 31), m1 = ~0u >> (31 - (j1 & 31));
     for (int i = r * b; i < r * b + b; ++i) {
-      const uint32_t* row = reinterpret_cast<const uint32_t*>(
-          base + static_cast<int64_t>(reflect_index(i, g.M)) * a.mpitch);
+      const uint32_t* row =
+          reinterpret_cast<const uint32_t*>(base + static_cast<int64_t>(reflect_index(i, M)) * mpitch);
       if (w0 == w1) {
         s += __popc(__ldg(row + w0) & m0 & m1);
       } else {
@@ -147,10 +147,10 @@ __device__ __noinline__ uint32_t mask_cell_sum_bits(const ClassifyArgs& a, const
     return s;
   }
   for (int i = r * b; i < r * b + b; ++i) {
-    const uint32_t* row = reinterpret_cast<const uint32_t*>(
-        base + static_cast<int64_t>(reflect_index(i, g.M)) * a.mpitch);
+    const uint32_t* row =
+        reinterpret_cast<const uint32_t*>(base + static_cast<int64_t>(reflect_index(i, M)) * mpitch);
     for (int j = j0; j < j0 + b; ++j) {
-      const int jj = reflect_index(j, g.N);
+      const int jj = reflect_index(j, N);
       s += (__ldg(row + (jj >> 5)) >> (jj & 31)) & 1u;
     }
   }
@@ -162,7 +162,7 @@ __device__ __forceinline__ uint32_t mask_cell_sum(const ClassifyArgs& a, const u
   const BatchGeom& g = a.g;
   const int b = g.b;
   const int j0 = c * b;
-  if (a.mask_bits) return mask_cell_sum_bits(a, base, r, c);
+  if (a.mask_bits) return mask_cell_sum_bits(base, a.mpitch, g.M, g.N, b, r, c);
   if (j0 + b <= g.N && a.vec > 1) {
     if (a.vec == 16) {
       if (b == 16) return mask_cell_sum_vec<16>(a, base, r, j0);
