@@ -475,3 +475,64 @@ def test_variance_fused_single_pass_equals_two_pass_and_oracle(ctx, C, b, n):
                                                seeds[f * C:(f + 1) * C], frame=f)
     assert res["1"][0][f * C:(f + 1) * C] == rp
     assert np.array_equal(res["1"][1].reshape(F, M, N, C)[f], ri)
+
+
+def test_randomized_fuzz_against_oracle(ctx):
+    """Randomized sweep over shapes (tiny to multi-tile, padded, ragged), frame
+    counts, channels, (b, n), classification (random / clustered masks,
+    variance), noise kinds and chunking, host entry points vs the oracle."""
+    rng = np.random.default_rng(2025)
+    kinds = {"keyed": dp.NOISE_KEYED, "philox": dp.NOISE_PHILOX, "none": dp.NOISE_NONE}
+    for case in range(150):
+        b, n = FAST_BN[rng.integers(len(FAST_BN))] if rng.random() < 0.8 else \
+            (int(rng.integers(1, 13)), 1)
+        if n == 1 and rng.random() < 0.5 and b % 2 == 0:
+            n = 2
+        C = int(rng.choice([1, 3]))
+        F = int(rng.integers(1, 4))
+        M = int(rng.integers(b, 3 * b + 700 * (rng.random() < 0.3) + 1))
+        N = int(rng.integers(b, 3 * b + 1100 * (rng.random() < 0.3) + 1))
+        frames = rng.integers(0, 256, (F, M, N, C), np.uint8)
+        if rng.random() < 0.5:
+            masks = rng.integers(0, 2, (F, M, N), np.uint8)
+        else:  # clustered: a random rectangle of complex pixels
+            masks = np.ones((F, M, N), np.uint8)
+            i0, j0 = rng.integers(0, M), rng.integers(0, N)
+            masks[:, i0:i0 + M // 2, j0:j0 + N // 2] = 0
+        kind = str(rng.choice(list(kinds)))
+        eps = float(rng.choice([0.1, 0.5, 1.0]))
+        seeds = dp.plane_seeds(int(rng.integers(0, 2**62)), F, C)
+        ctx.set_chunk_frames(int(rng.integers(0, 3)))
+        tag = (case, M, N, C, F, b, n, kind)
+        if kind == "philox":  # the oracle's Philox restatement keys (seed, frame, channel, ...)
+            seeds = [seeds[0]]
+        p = dp.make_privacy_params(eps, 16, b, n)
+        if rng.random() < 0.25:
+            tau = float(rng.choice([0.0, 200.0, 2000.0]))
+            pls, img = ctx.pixelize_adaptive_variance(frames, tau, p, kinds[kind],
+                                                      None if kind == "none" else seeds)
+            for f in range(F):
+                rp, ri = oracle.pixelize_adaptive_variance(
+                    frames[f], b, n, p.sigma, p.sigma_sub, tau, kind,
+                    None if kind == "none" else (seeds * C if kind == "philox" else
+                                                 seeds[f * C:(f + 1) * C]), frame=f)
+                assert pls[f * C:(f + 1) * C] == rp and np.array_equal(img[f], ri), tag
+        elif n > 1 or rng.random() < 0.5:
+            pls, img = ctx.pixelize_adaptive(frames, masks, p, kinds[kind],
+                                             None if kind == "none" else seeds)
+            for f in range(F):
+                rp, ri = oracle.pixelize_adaptive(
+                    frames[f], masks[f], b, n, p.sigma, p.sigma_sub, kind,
+                    None if kind == "none" else (seeds * C if kind == "philox" else
+                                                 seeds[f * C:(f + 1) * C]), frame=f)
+                assert pls[f * C:(f + 1) * C] == rp and np.array_equal(img[f], ri), tag
+            assert np.array_equal(ctx.reassemble(pls, M, N, b, n, channels=C, frames=F), img), tag
+        else:
+            means, img = ctx.pixelize_uniform(frames, p, kinds[kind], None if kind == "none" else seeds)
+            for f in range(F):
+                rm, ri = oracle.pixelize_uniform(
+                    frames[f], b, p.sigma, kind,
+                    None if kind == "none" else (seeds * C if kind == "philox" else
+                                                 seeds[f * C:(f + 1) * C]), frame=f)
+                assert np.array_equal(means[f * C:(f + 1) * C], rm) and np.array_equal(img[f], ri), tag
+    ctx.set_chunk_frames(0)
