@@ -1145,79 +1145,101 @@ __global__ void __launch_bounds__(kGenericThreads) k_expand(const ExpandArgs a) 
 // from K0's per-plane scan), writes the strip pattern into a smem tile and one
 // thread bulk-stores the tile with a 3-D TMA box (clipped at M and N).
 // ============================================================================
-template <int C, int B4, int NSUB, bool ADAPTIVE>
+template <int C, int B4, int NSUB, bool ADAPTIVE, bool PACKED>
 __global__ void __launch_bounds__(kConsumers)
     k_expand_tma(const __grid_constant__ CUtensorMap tm_out, const ExpandArgs a) {
-  constexpr int B = 4 * B4, SB = B / NSUB, SB4 = SB / 4, ROWB = kTilePx * C;
+  constexpr int B = 4 * B4, SB = B / NSUB, SB4 = SB / 4;
   extern __shared__ __align__(128) uint8_t smem[];
   const BatchGeom& g = a.g;
   const int t = threadIdx.x;
-  const int u = blockIdx.x;
-  const uint32_t rest = a.div_tiles.div(static_cast<uint32_t>(u));
-  const int tile = u - static_cast<int>(rest * a.div_tiles.d);
-  const uint32_t fq = a.div_rows.div(rest);
-  const int r = static_cast<int>(rest - fq * a.div_rows.d), f = static_cast<int>(fq);
-  const int px0 = tile * kTilePx;
-  const int cell = px0 / B + t / B4;
+  // This thread's slot (frame within the group) and strip column in it.
+  const int slot_px = PACKED ? a.slot_px : kTilePx;
+  const int my_j = PACKED ? (4 * t) / slot_px : 0;
+  const bool in_slot = my_j < (PACKED ? a.pack : 1);
+  const int jj = in_slot ? my_j : 0;
+  const int lpx = 4 * t - jj * slot_px;
+  const int srb = slot_px * C;  // smem bytes per slot row
   const int sc = (t % B4) / SB4;
-  const bool active = cell < g.GC;
-  const int gidx = r * g.GC + cell;
-  // value of vertical subcell vs for channel ch (simple cells: one value)
-  uint32_t val[NSUB][C];
-  if (active) {
+  if (t == 0) prefetch_tmap(&tm_out);
+  for (int u = blockIdx.x, k = 0; u < a.units; u += gridDim.x, ++k) {
+    uint8_t* buf = smem + (a.buffers == 2 ? (k & 1) : 0) * a.stage_bytes;
+    // The store that last used this buffer must have read it.
+    if (t == 0) {
+      if (a.buffers == 2) bulk_wait_read_1();
+      else bulk_wait_read_all();
+    }
+    __syncthreads();
+    const uint32_t rest = a.div_tiles.div(static_cast<uint32_t>(u));
+    const int tile = u - static_cast<int>(rest * a.div_tiles.d);
+    const uint32_t fq = a.div_rows.div(rest);
+    const int r = static_cast<int>(rest - fq * a.div_rows.d);
+    const int fg = static_cast<int>(fq);
+    const int pk = PACKED ? a.pack : 1;
+    const int nf = PACKED ? min(pk, g.F - fg * pk) : 1;
+    const int f = fg * pk + jj;
+    const int px0 = PACKED ? 0 : tile * kTilePx;
+    const int cell = (px0 + lpx) / B;
+    const bool active = in_slot && jj < nf && cell < g.GC;
+    const int gidx = r * g.GC + cell;
+    uint32_t val[NSUB][C];
+    if (active) {
 #pragma unroll
-    for (int ch = 0; ch < C; ++ch) {
-      const int64_t plane = static_cast<int64_t>(f) * C + ch;
-      const uint8_t* st = a.stats + plane * a.sstride;
-      if constexpr (!ADAPTIVE) {
-        const uint32_t v = __ldg(st + gidx);
-#pragma unroll
-        for (int vs = 0; vs < NSUB; ++vs) val[vs][ch] = v;
-      } else {
-        const uint32_t info = __ldg(&a.cellinfo[plane * g.G + gidx]);
-        const uint32_t slot_s = __ldg(&a.rowprefix[plane * g.GR + r]) + (info >> 1);
-        const int64_t base = 4ll * g.G + 4;
-        if (info & 1u) {
-          const uint32_t v = __ldg(st + base + slot_s);
+      for (int ch = 0; ch < C; ++ch) {
+        const int64_t plane = static_cast<int64_t>(f) * C + ch;
+        const uint8_t* st = a.stats + plane * a.sstride;
+        if constexpr (!ADAPTIVE) {
+          const uint32_t v = __ldg(st + gidx);
 #pragma unroll
           for (int vs = 0; vs < NSUB; ++vs) val[vs][ch] = v;
         } else {
-          const uint8_t* sub = st + base + __ldg(&a.totals[plane]) +
-                               static_cast<int64_t>(static_cast<uint32_t>(gidx) - slot_s) * NSUB * NSUB;
+          const uint32_t info = __ldg(&a.cellinfo[plane * g.G + gidx]);
+          const uint32_t slot_s = __ldg(&a.rowprefix[plane * g.GR + r]) + (info >> 1);
+          const int64_t base = 4ll * g.G + 4;
+          if (info & 1u) {
+            const uint32_t v = __ldg(st + base + slot_s);
 #pragma unroll
-          for (int vs = 0; vs < NSUB; ++vs) val[vs][ch] = __ldg(sub + vs * NSUB + sc);
+            for (int vs = 0; vs < NSUB; ++vs) val[vs][ch] = v;
+          } else {
+            const uint8_t* sub = st + base + __ldg(&a.totals[plane]) +
+                                 static_cast<int64_t>(static_cast<uint32_t>(gidx) - slot_s) * NSUB * NSUB;
+#pragma unroll
+            for (int vs = 0; vs < NSUB; ++vs) val[vs][ch] = __ldg(sub + vs * NSUB + sc);
+          }
         }
       }
+      uint8_t* mystrip = buf + jj * (PACKED ? a.slot_stride : 0) + lpx * C;
+#pragma unroll
+      for (int vs = 0; vs < NSUB; ++vs) {
+        uint32_t w[C];
+        pattern_words<C>(val[vs], w);
+#pragma unroll
+        for (int i = 0; i < SB; ++i)
+#pragma unroll
+          for (int q = 0; q < C; ++q)
+            reinterpret_cast<uint32_t*>(mystrip + (vs * SB + i) * srb)[q] = w[q];
+      }
     }
-    uint8_t* mystrip = smem + t * 4 * C;
-#pragma unroll
-    for (int vs = 0; vs < NSUB; ++vs) {
-      uint32_t w[C];
-      pattern_words<C>(val[vs], w);
-#pragma unroll
-      for (int i = 0; i < SB; ++i)
-#pragma unroll
-        for (int q = 0; q < C; ++q) reinterpret_cast<uint32_t*>(mystrip + (vs * SB + i) * ROWB)[q] = w[q];
+    fence_proxy_async_smem();
+    __syncthreads();
+    const int scopy = max(0, min(srb, a.tensor_out_bytes - px0 * C));
+    if (t == 0 && scopy > 0) {
+      for (int j = 0; j < nf; ++j)
+        tma_store_3d(&tm_out, px0 * C / 8, r * B, fg * pk + j, buf + j * (PACKED ? a.slot_stride : 0));
+    }
+    if (t == 0) bulk_commit();  // one group per unit (possibly empty)
+    // bytes past the tensor's row extent (< 8 per row), from the smem tile
+    const int vbytes = min(slot_px, g.N - px0) * C;
+    const int lx0 = lpx * C;
+    if (active && lx0 + 4 * C > scopy && lx0 < vbytes) {
+      const int rows = min(B, g.M - r * B);
+      const uint8_t* sb = buf + jj * (PACKED ? a.slot_stride : 0);
+      for (int i = 0; i < rows; ++i)
+        for (int x = max(lx0, scopy); x < min(lx0 + 4 * C, vbytes); ++x)
+          a.out[static_cast<int64_t>(f) * a.ofstride + static_cast<int64_t>(r * B + i) * a.opitch +
+                static_cast<int64_t>(px0) * C + x] = sb[i * srb + x];
     }
   }
-  fence_proxy_async_smem();
-  __syncthreads();
-  const int scopy = max(0, min(ROWB, a.tensor_out_bytes - px0 * C));
-  if (t == 0 && scopy > 0) {
-    tma_store_3d(&tm_out, px0 * C / 8, r * B, f, smem);
-    bulk_commit();
-  }
-  // bytes past the tensor's row extent
-  const int vbytes = min(kTilePx, g.N - px0) * C;
-  const int lx0 = t * 4 * C;
-  if (active && lx0 + 4 * C > scopy && lx0 < vbytes) {
-    const int rows = min(B, g.M - r * B);
-    for (int i = 0; i < rows; ++i)
-      for (int x = max(lx0, scopy); x < min(lx0 + 4 * C, vbytes); ++x)
-        a.out[static_cast<int64_t>(f) * a.ofstride + static_cast<int64_t>(r * B + i) * a.opitch +
-              static_cast<int64_t>(px0) * C + x] = smem[i * ROWB + x];
-  }
-  if (t == 0 && scopy > 0) bulk_wait_read_all();
+  if (t == 0) bulk_wait_read_all();  // smem must outlive the stores' reads
 }
 
 // ============================================================================
@@ -1547,10 +1569,10 @@ StatsKernel select_stats_kernel(int C, int b, int n, bool adaptive, bool packed)
 
 using ExpandKernel = void (*)(const CUtensorMap, const ExpandArgs);
 
-template <int C, bool AD>
+template <int C, bool AD, bool PK>
 ExpandKernel pick_expand(int b, int n) {
 #define DPPX_CASE(B4v, NS) \
-  if (b == 4 * (B4v) && n == (NS)) return k_expand_tma<C, B4v, NS, AD>;
+  if (b == 4 * (B4v) && n == (NS)) return k_expand_tma<C, B4v, NS, AD, PK>;
   DPPX_CASE(1, 1)
   DPPX_CASE(2, 1)
   DPPX_CASE(4, 1)
@@ -1567,10 +1589,16 @@ ExpandKernel pick_expand(int b, int n) {
   return nullptr;
 }
 
-ExpandKernel select_expand_kernel(int C, int b, int n, bool adaptive) {
+ExpandKernel select_expand_kernel(int C, int b, int n, bool adaptive, bool packed) {
   if (!adaptive && n != 1) return nullptr;
-  if (C == 1) return adaptive ? pick_expand<1, true>(b, n) : pick_expand<1, false>(b, n);
-  if (C == 3) return adaptive ? pick_expand<3, true>(b, n) : pick_expand<3, false>(b, n);
+  if (C == 1) {
+    if (packed) return adaptive ? pick_expand<1, true, true>(b, n) : pick_expand<1, false, true>(b, n);
+    return adaptive ? pick_expand<1, true, false>(b, n) : pick_expand<1, false, false>(b, n);
+  }
+  if (C == 3) {
+    if (packed) return adaptive ? pick_expand<3, true, true>(b, n) : pick_expand<3, false, true>(b, n);
+    return adaptive ? pick_expand<3, true, false>(b, n) : pick_expand<3, false, false>(b, n);
+  }
   return nullptr;
 }
 
