@@ -134,7 +134,11 @@ MaskPacker* mask_packer_create(int threads) {
   p->nthreads = std::max(1, threads);
   __builtin_cpu_init();
   p->avx2 = __builtin_cpu_supports("avx2");
-  for (int i = 1; i < p->nthreads; ++i) p->workers.emplace_back(&MaskPacker::worker, p, i);
+  try {
+    for (int i = 1; i < p->nthreads; ++i) p->workers.emplace_back(&MaskPacker::worker, p, i);
+  } catch (...) {  // no threads available: pack on the calling thread plus what started
+    p->nthreads = static_cast<int>(p->workers.size()) + 1;
+  }
   return p;
 }
 
