@@ -111,6 +111,8 @@ struct dppx_ctx {
   uint64_t* sd_pinned[2] = {nullptr, nullptr};
   size_t sd_pinned_n[2] = {0, 0};
   cudaEvent_t in_done[2] = {}, comp_done[2] = {}, out_done[2] = {};
+  static constexpr int kMaxBands = 8;
+  cudaEvent_t band_in[kMaxBands] = {}, band_comp[kMaxBands] = {};  // single-frame row bands
   int chunk_frames = 0;
   bool exact_noise = false;
   double var_tau = 0.0;  // AdaptiveVariance host calls
@@ -423,6 +425,7 @@ int classify_flags(dppx_ctx* ctx, const BatchGeom& g, const uint8_t* flags, uint
 // returns kNoFusedPath without launching anything when it does not apply.
 int run_stats(dppx_ctx* ctx, StatsArgs& a) {
   const BatchGeom& g = a.g;
+  if (a.row_count == 0 || g.F == 0) return DPPX_OK;
   StatsKernel k = nullptr;
   const bool aligned = aligned16(a.img) && a.pitch % 16 == 0 && a.fstride % 16 == 0 &&
                        (!a.out || (aligned16(a.out) && a.opitch % 16 == 0 && a.ofstride % 16 == 0));
@@ -464,11 +467,11 @@ int run_stats(dppx_ctx* ctx, StatsArgs& a) {
     a.tensor_out_bytes = static_cast<int>(row_bytes / 8 * 8);
     a.tiles_per_row = a.pack > 1 ? 1 : (padded_px + tile - 1) / tile;
     const int64_t groups = (g.F + a.pack - 1) / a.pack;
-    const int64_t units = groups * g.GR * a.tiles_per_row;
+    const int64_t units = groups * a.row_count * a.tiles_per_row;
     if (units > 0x7FFFFFFF) return set_err(ctx, DPPX_ERR_INVALID, "batch too large for one launch");
     a.units = static_cast<int>(units);
     a.div_tiles = make_fastdiv(static_cast<uint32_t>(a.tiles_per_row));
-    a.div_rows = make_fastdiv(static_cast<uint32_t>(g.GR));
+    a.div_rows = make_fastdiv(static_cast<uint32_t>(a.row_count));
     const size_t stage = static_cast<size_t>(g.b) * tile * g.C;
     // Two stages: measured best for every shape on B200 (a 2-deep ring per CTA
     // with 4 CTAs/SM at b = 16 beats 3-4 deep rings with fewer CTAs; see
@@ -520,13 +523,25 @@ int check_params(dppx_ctx* ctx, const dppx_privacy_params* p, bool adaptive) {
   return DPPX_OK;
 }
 
+// Less common options of pixelize_dev.
+struct PixOpts {
+  bool partial = false;          // Algorithm 1 (pixelize_reference)
+  double var_tau = std::nan("");  // set: variance classification (extension)
+  bool mask_bits = false;        // mask rows are packed bits (host pipeline transport)
+  int row_begin = 0;             // grid rows [row_begin, row_begin + row_count) only
+  int row_count = -1;            // -1: all rows
+  bool classify = true;          // adaptive: run K0 (false: a previous band already did)
+};
+
 // Device-pointer core of both pixelize entry points.
 int pixelize_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img, const uint8_t* mask,
                  const dppx_privacy_params* pp, const dppx_noise* nz, const double* dev_injected,
                  uint8_t* stats, int64_t sstride, uint32_t* payload_len, uint8_t* out,
                  bool adaptive, DevBuf& dev_seeds, uint64_t*& pinned, size_t& pinned_n,
-                 cudaEvent_t guard, bool record_guard, bool partial = false,
-                 double var_tau = std::nan(""), bool mask_bits = false) {
+                 cudaEvent_t guard, bool record_guard, const PixOpts& o = PixOpts()) {
+  const bool partial = o.partial;
+  const double var_tau = o.var_tau;
+  const bool mask_bits = o.mask_bits;
   BatchGeom g;
   if (int rc = geometry(ctx, d->height, d->width, d->channels, d->frames, pp->b,
                         adaptive ? pp->n : 1, &g, !partial))
@@ -560,6 +575,10 @@ int pixelize_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img, c
   a.sigma_sub = adaptive ? pp->sigma_sub : pp->sigma;
   a.exact_noise = ctx->exact_noise ? 1 : 0;
   a.partial_borders = partial ? 1 : 0;
+  a.row_begin = o.row_count < 0 ? 0 : o.row_begin;
+  a.row_count = o.row_count < 0 ? g.GR : o.row_count;
+  if (a.row_begin < 0 || a.row_count < 0 || a.row_begin + a.row_count > g.GR)
+    return set_err(ctx, DPPX_ERR_INVALID, "row band out of range");
   if (int rc = prepare_noise(ctx, nz, g.F * g.C, dev_injected, g, pp, &a.noise, ctx->stream,
                              dev_seeds, pinned, pinned_n, guard, record_guard))
     return rc;
@@ -601,7 +620,11 @@ int pixelize_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img, c
       return DPPX_OK;
     }
   }
-  if (adaptive) {
+  if (adaptive && !o.classify) {  // a previous row band of this call ran K0
+    a.cellinfo = static_cast<const uint32_t*>(ctx->cellinfo.p);
+    a.rowprefix = static_cast<const uint32_t*>(ctx->rowprefix.p);
+    a.totals = static_cast<const uint32_t*>(ctx->totals.p);
+  } else if (adaptive) {
     if (int rc = ensure_scratch(ctx, g, g.F)) return rc;
     VarianceSource vs{img, d->pitch, d->frame_stride, var_tau};
     if (int rc = classify(ctx, g, g.F, false, mask, d->mask_pitch, d->mask_frame_stride, stats,
@@ -748,6 +771,131 @@ cudaError_t copy_frames(void* dst, int64_t dpitch, int64_t dfs, const void* src,
 
 enum class HostOp { Uniform, Adaptive, Broadcast, Reassemble, Reference, AdaptiveVariance };
 
+// Single-frame host calls: there is no second frame to overlap with, so the
+// frame is split into bands of grid rows. Band i's rows are copied in while
+// band i-1 is computed and band i-2 is copied out (H2D, K1, D2H on three
+// streams). Adaptive frames ship the whole mask first (K0 classifies the frame
+// once, before band 0's K1); the statistics are copied out after the last
+// band. Bands are in order on the input stream, so the mirrored rows a last
+// band reads from its predecessor are always resident.
+int host_pipeline_bands(dppx_ctx* ctx, bool adaptive, const dppx_frames_desc* d,
+                        const BatchGeom& g, const uint8_t* img, const uint8_t* mask,
+                        const dppx_privacy_params* pp, const dppx_noise* nz, uint8_t* stats,
+                        int64_t sstride, uint32_t* lens, uint8_t* out, int nb) {
+  const int C = g.C, M = g.M, N = g.N, b = g.b;
+  const int64_t row = static_cast<int64_t>(N) * C;
+  const int64_t dpitch = round_up(row, 16), dfs = dpitch * M;
+  const int64_t dmpitch = round_up(N, 16), dmfs = dmpitch * M;
+  const size_t cap = adaptive ? dppx_adaptive_payload_capacity(M, N, b, g.n) : g.G;
+  const int64_t dstride = adaptive ? round_up(static_cast<int64_t>(cap), 16) : g.G;
+  if (ensure(ctx, ctx->img[0], static_cast<size_t>(dfs))) return DPPX_ERR_OOM;
+  if (out && ensure(ctx, ctx->out[0], static_cast<size_t>(dfs))) return DPPX_ERR_OOM;
+  if (ensure(ctx, ctx->stats[0], static_cast<size_t>(dstride) * C)) return DPPX_ERR_OOM;
+  if (ensure(ctx, ctx->lens[0], sizeof(uint32_t) * C)) return DPPX_ERR_OOM;
+  uint8_t* dimg = static_cast<uint8_t*>(ctx->img[0].p);
+  uint8_t* dout = static_cast<uint8_t*>(ctx->out[0].p);
+  uint8_t* dstats = static_cast<uint8_t*>(ctx->stats[0].p);
+  uint32_t* dlens = static_cast<uint32_t*>(ctx->lens[0].p);
+  cudaStream_t comp = ctx->stream;
+  // The previous call's copies out of these buffers must be done.
+  CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->s_in, ctx->out_done[0], 0));
+  bool bits = false;
+  uint8_t* dmask = nullptr;
+  int64_t mp = dmpitch, mfs = dmfs;
+  if (adaptive) {
+    if (ensure(ctx, ctx->mask[0], static_cast<size_t>(dmfs))) return DPPX_ERR_OOM;
+    dmask = static_cast<uint8_t*>(ctx->mask[0].p);
+    if (ctx->mask_bits_mode == 1) {
+      const int64_t wpr = dppx::mask_words_per_row(N);
+      const size_t bytes = static_cast<size_t>(wpr) * 4 * M;
+      if (!ctx->packer) ctx->packer = dppx::mask_packer_create(0);
+      if (ctx->mbits_pinned_n[0] < bytes) {
+        CUDA_TRY(ctx, cudaStreamSynchronize(ctx->s_in));
+        if (ctx->mbits_pinned[0]) CUDA_TRY(ctx, cudaFreeHost(ctx->mbits_pinned[0]));
+        ctx->mbits_pinned[0] = nullptr;
+        ctx->mbits_pinned_n[0] = 0;
+        CUDA_TRY(ctx, cudaHostAlloc(reinterpret_cast<void**>(&ctx->mbits_pinned[0]), bytes,
+                                    cudaHostAllocDefault));
+        ctx->mbits_pinned_n[0] = bytes;
+      }
+      CUDA_TRY(ctx, cudaEventSynchronize(ctx->in_done[0]));  // staging buffer free
+      bits = dppx::pack_mask_bits(ctx->packer, mask, d->mask_pitch, d->mask_frame_stride, M, N, 1,
+                                  ctx->mbits_pinned[0], wpr);
+      if (bits) {
+        CUDA_TRY(ctx, cudaMemcpyAsync(dmask, ctx->mbits_pinned[0], bytes, cudaMemcpyHostToDevice,
+                                      ctx->s_in));
+        ctx->kstats.h2d_bytes += bytes;
+        mp = wpr * 4;
+        mfs = static_cast<int64_t>(bytes);
+      }
+    }
+    if (!bits) {
+      CUDA_TRY(ctx, cudaMemcpy2DAsync(dmask, dmpitch, mask, d->mask_pitch, N, M,
+                                      cudaMemcpyHostToDevice, ctx->s_in));
+      ctx->kstats.h2d_bytes += static_cast<uint64_t>(N) * M;
+    }
+  }
+  // Band sizes in grid rows (the last band keeps >= 2 rows for its reflections).
+  int sizes[dppx_ctx::kMaxBands];
+  {
+    int left = g.GR;
+    for (int i = 0; i < nb; ++i) {
+      sizes[i] = left / (nb - i);
+      left -= sizes[i];
+    }
+  }
+  dppx_frames_desc dd = *d;
+  dd.pitch = dpitch;
+  dd.frame_stride = dfs;
+  dd.mask_pitch = mp;
+  dd.mask_frame_stride = mfs;
+  dd.out_pitch = dpitch;
+  dd.out_frame_stride = dfs;
+  int r0 = 0;
+  for (int i = 0; i < nb; ++i) {
+    const int r1 = r0 + sizes[i];
+    const int y0 = r0 * b, y1 = std::min(r1 * b, M);
+    CUDA_TRY(ctx, cudaMemcpy2DAsync(dimg + y0 * dpitch, dpitch, img + y0 * d->pitch, d->pitch, row,
+                                    y1 - y0, cudaMemcpyHostToDevice, ctx->s_in));
+    ctx->kstats.h2d_bytes += static_cast<uint64_t>(row) * (y1 - y0);
+    CUDA_TRY(ctx, cudaEventRecord(ctx->band_in[i], ctx->s_in));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(comp, ctx->band_in[i], 0));
+    PixOpts po;
+    po.mask_bits = bits;
+    po.row_begin = r0;
+    po.row_count = r1 - r0;
+    po.classify = i == 0;
+    if (int rc = pixelize_dev(ctx, &dd, dimg, dmask, pp, nz, nullptr, dstats, dstride,
+                              adaptive ? dlens : nullptr, out ? dout : nullptr, adaptive, ctx->sd[0],
+                              ctx->sd_pinned[0], ctx->sd_pinned_n[0], ctx->comp_done[0], false, po))
+      return rc;
+    CUDA_TRY(ctx, cudaEventRecord(ctx->band_comp[i], comp));
+    if (out) {
+      CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->s_out, ctx->band_comp[i], 0));
+      CUDA_TRY(ctx, cudaMemcpy2DAsync(out + y0 * d->out_pitch, d->out_pitch, dout + y0 * dpitch, dpitch,
+                                      row, y1 - y0, cudaMemcpyDeviceToHost, ctx->s_out));
+      ctx->kstats.d2h_bytes += static_cast<uint64_t>(row) * (y1 - y0);
+    }
+    r0 = r1;
+  }
+  CUDA_TRY(ctx, cudaEventRecord(ctx->in_done[0], ctx->s_in));
+  CUDA_TRY(ctx, cudaEventRecord(ctx->comp_done[0], comp));
+  CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->s_out, ctx->comp_done[0], 0));
+  CUDA_TRY(ctx, cudaMemcpy2DAsync(stats, sstride, dstats, dstride, cap, C, cudaMemcpyDeviceToHost,
+                                  ctx->s_out));
+  ctx->kstats.d2h_bytes += static_cast<uint64_t>(cap) * C;
+  if (adaptive && lens) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(lens, dlens, sizeof(uint32_t) * C, cudaMemcpyDeviceToHost,
+                                  ctx->s_out));
+    ctx->kstats.d2h_bytes += sizeof(uint32_t) * C;
+  }
+  CUDA_TRY(ctx, cudaEventRecord(ctx->out_done[0], ctx->s_out));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->s_out));
+  CUDA_TRY(ctx, cudaStreamSynchronize(comp));
+  if (ctx->timing) collect_timings(ctx);
+  return DPPX_OK;
+}
+
 int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uint8_t* img,
                   const uint8_t* mask, const dppx_privacy_params* pp, const dppx_noise* nz,
                   uint8_t* stats, int64_t sstride, uint32_t* lens, const uint32_t* in_lens,
@@ -793,6 +941,23 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
     dstride = static_cast<int64_t>(G);
     sstride = static_cast<int64_t>(G);
   }
+  if (ctx->mask_bits_mode < 0) {
+    const char* env = std::getenv("DPPX_MASK_BITS");
+    ctx->mask_bits_mode = env && env[0] == '0' ? 0 : 1;
+  }
+  {
+    // One frame: pipeline row bands instead of frames (DPPX_BANDS=0 disables).
+    const char* env = std::getenv("DPPX_BANDS");
+    const bool bands_ok = !(env && env[0] == '0');
+    const int64_t frame_bytes = static_cast<int64_t>(M) * N * C;
+    const bool inj_any = nz && nz->kind == DPPX_NOISE_INJECTED;
+    if (bands_ok && F == 1 && (op == HostOp::Uniform || op == HostOp::Adaptive) && !inj_any &&
+        g.GR >= 4 && frame_bytes >= (512 << 10)) {
+      const int nb = static_cast<int>(std::min<int64_t>(
+          {static_cast<int64_t>(dppx_ctx::kMaxBands), g.GR / 2, std::max<int64_t>(2, frame_bytes >> 18)}));
+      return host_pipeline_bands(ctx, adaptive, d, g, img, mask, pp, nz, stats, sstride, lens, out, nb);
+    }
+  }
   const int64_t dpitch = round_up(static_cast<int64_t>(N) * C, 16);
   const int64_t dmpitch = round_up(N, 16);
   const int64_t dfs = dpitch * M, dmfs = dmpitch * M;
@@ -831,10 +996,6 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
                           d->mask_frame_stride == static_cast<int64_t>(N) * M;
   const bool dense_out = out && dpitch != row && d->out_pitch == row && d->out_frame_stride == row * M;
   // Bit-packed mask transport: 1/8 of the mask's PCIe bytes (maskpack.h).
-  if (ctx->mask_bits_mode < 0) {
-    const char* env = std::getenv("DPPX_MASK_BITS");
-    ctx->mask_bits_mode = env && env[0] == '0' ? 0 : 1;
-  }
   const bool try_bits = op == HostOp::Adaptive && ctx->mask_bits_mode == 1;
   const int64_t wpr = dppx::mask_words_per_row(N);
   const size_t bits_frame = static_cast<size_t>(wpr) * 4 * M;
@@ -957,12 +1118,14 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
         if (nz->kind == DPPX_NOISE_KEYED && nz->plane_seeds) cn.plane_seeds = nz->plane_seeds + static_cast<int64_t>(f0) * C;
         if (nz->kind == DPPX_NOISE_PHILOX) cn.frame_base = nz->frame_base + f0;
       }
+      PixOpts po;
+      po.partial = op == HostOp::Reference;
+      if (op == HostOp::AdaptiveVariance) po.var_tau = ctx->var_tau;
+      po.mask_bits = bits;
       rc = pixelize_dev(ctx, &dd, dimg, dmask, pp, nz ? &cn : nullptr,
                         inj ? static_cast<const double*>(ctx->inj[s].p) : nullptr, dstats, dstride,
                         adaptive ? dlens : nullptr, out ? dout : nullptr, adaptive, ctx->sd[s],
-                        ctx->sd_pinned[s], ctx->sd_pinned_n[s], ctx->comp_done[s], false,
-                        op == HostOp::Reference,
-                        op == HostOp::AdaptiveVariance ? ctx->var_tau : std::nan(""), bits);
+                        ctx->sd_pinned[s], ctx->sd_pinned_n[s], ctx->comp_done[s], false, po);
     } else {
       rc = expand_dev(ctx, &dd, dstats, dstride, in_lens ? dlens : nullptr, b, n, dout, adaptive);
     }
@@ -1109,6 +1272,10 @@ int dppx_ctx_create(int32_t device, dppx_ctx** out) {
     cudaEventCreateWithFlags(&ctx->comp_done[s], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->out_done[s], cudaEventDisableTiming);
   }
+  for (int i = 0; i < dppx_ctx::kMaxBands; ++i) {
+    cudaEventCreateWithFlags(&ctx->band_in[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->band_comp[i], cudaEventDisableTiming);
+  }
   cudaEventCreateWithFlags(&ctx->seeds_ev, cudaEventDisableTiming);
   cudaEventRecord(ctx->seeds_ev, ctx->stream);
   // Verify that the sm_100a kernels load on this device (no silent fallback).
@@ -1143,6 +1310,10 @@ void dppx_ctx_destroy(dppx_ctx* ctx) {
     cudaEventDestroy(ctx->out_done[s]);
   }
   if (ctx->seeds_pinned) cudaFreeHost(ctx->seeds_pinned);
+  for (int i = 0; i < dppx_ctx::kMaxBands; ++i) {
+    cudaEventDestroy(ctx->band_in[i]);
+    cudaEventDestroy(ctx->band_comp[i]);
+  }
   cudaEventDestroy(ctx->seeds_ev);
   dppx::mask_packer_destroy(ctx->packer);
   for (auto& pt : ctx->pending) {
@@ -1318,6 +1489,12 @@ int dppx_pixelize_adaptive_variance(dppx_ctx* ctx, const dppx_frames_desc* d, co
                        payload_stride, payload_len, nullptr, 0, 0, out);
 }
 
+static PixOpts var_opts(double tau) {
+  PixOpts o;
+  o.var_tau = tau;
+  return o;
+}
+
 int dppx_pixelize_adaptive_variance_dev(dppx_ctx* ctx, const dppx_frames_desc* d,
                                         const uint8_t* img, double var_tau,
                                         const dppx_privacy_params* pp, const dppx_noise* nz,
@@ -1329,7 +1506,7 @@ int dppx_pixelize_adaptive_variance_dev(dppx_ctx* ctx, const dppx_frames_desc* d
   if (!(var_tau >= 0.0)) return set_err(ctx, DPPX_ERR_INVALID, "variance threshold must be >= 0");
   return pixelize_dev(ctx, d, img, nullptr, pp, nz, nz ? nz->injected : nullptr, payload,
                       payload_stride, payload_len, out, true, ctx->seeds, ctx->seeds_pinned,
-                      ctx->seeds_pinned_n, ctx->seeds_ev, true, false, var_tau);
+                      ctx->seeds_pinned_n, ctx->seeds_ev, true, var_opts(var_tau));
 }
 
 int dppx_broadcast_means(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* means, int32_t b,

@@ -116,6 +116,9 @@ struct StatsArgs {
   // slot_px*C bytes (the TMA box is stored densely).
   int pack, slot_px, slot_stride;
   int row_slack;             // 1: input pitch >= roundup(N*C, 16), loads may read the slack
+  // Grid rows [row_begin, row_begin + row_count) of every frame are processed
+  // (the host pipeline's row bands for single-frame calls); 0 / GR otherwise.
+  int row_begin, row_count;
   // EXTENSION, fused variance classification (k_stats_tma<..., VAR = true>):
   // each cell is classified by its own variance in the same pass; statistics
   // go to a per-cell staging area (slot positions need the whole frame's simple

@@ -382,7 +382,7 @@ __device__ __forceinline__ UnitPos decode_unit(const StatsArgs& a, int u) {
   const uint32_t rest = a.div_tiles.div(static_cast<uint32_t>(u));
   p.tile = u - static_cast<int>(rest * a.div_tiles.d);
   const uint32_t fg = a.div_rows.div(rest);
-  p.r = static_cast<int>(rest - fg * a.div_rows.d);
+  p.r = a.row_begin + static_cast<int>(rest - fg * a.div_rows.d);
   p.fg = static_cast<int>(fg);
   p.px0 = PACKED ? 0 : p.tile * kTilePx;  // packed units are one tile wide
   return p;
@@ -1032,7 +1032,7 @@ __global__ void __launch_bounds__(kGenericThreads) k_stats_generic(const StatsAr
   const int c = blockIdx.x * kGenericThreads + threadIdx.x;
   if (c >= g.GC) return;
   // grid-stride over rows and frames: GR or F may exceed the 65535 grid limit
-  for (int r = blockIdx.y; r < g.GR; r += gridDim.y)
+  for (int r = a.row_begin + blockIdx.y; r < a.row_begin + a.row_count; r += gridDim.y)
   for (int f = blockIdx.z; f < g.F; f += gridDim.z) {
     const int gidx = r * g.GC + c;
     const uint8_t* img = a.img + static_cast<int64_t>(f) * a.fstride;
@@ -1625,7 +1625,8 @@ cudaError_t launch_stats_tma(StatsKernel k, const CUtensorMap& tin, const CUtens
 }
 
 cudaError_t launch_stats_generic(const StatsArgs& a, cudaStream_t s) {
-  dim3 grid((a.g.GC + kGenericThreads - 1) / kGenericThreads, a.g.GR < 65535 ? a.g.GR : 65535,
+  dim3 grid((a.g.GC + kGenericThreads - 1) / kGenericThreads,
+            a.row_count < 65535 ? (a.row_count > 0 ? a.row_count : 1) : 65535,
             a.g.F < 65535 ? a.g.F : 65535);
   k_stats_generic<<<grid, kGenericThreads, 0, s>>>(a);
   return cudaGetLastError();

@@ -536,3 +536,32 @@ def test_randomized_fuzz_against_oracle(ctx):
                                                  seeds[f * C:(f + 1) * C]), frame=f)
                 assert np.array_equal(means[f * C:(f + 1) * C], rm) and np.array_equal(img[f], ri), tag
     ctx.set_chunk_frames(0)
+
+
+@pytest.mark.parametrize("M,N,C,b,n", [(576, 768, 3, 16, 1), (1080, 1920, 3, 16, 4), (1083, 1917, 1, 32, 8),
+                                       (2160, 3840, 3, 32, 8), (200, 1000, 3, 8, 2)])
+def test_single_frame_row_bands(ctx, M, N, C, b, n):
+    """Single-frame host calls are pipelined in row bands (H2D / K1 / D2H
+    overlap within the frame): identical to the oracle and to the unbanded path."""
+    import os
+    rng = np.random.default_rng(M * 7 + N)
+    frame = rng.integers(0, 256, (1, M, N, C), np.uint8)
+    mask = (rng.random((1, M, N)) < 0.6).astype(np.uint8)
+    p = dp.make_privacy_params(0.5, 16, b, n)
+    seeds = dp.plane_seeds(77, 1, C)
+    res = {}
+    for bands in ("1", "0"):
+        os.environ["DPPX_BANDS"] = bands
+        try:
+            if n == 1:
+                res[bands, "u"] = ctx.pixelize_uniform(frame, p, dp.NOISE_KEYED, seeds)
+            res[bands, "a"] = ctx.pixelize_adaptive(frame, mask, p, dp.NOISE_KEYED, seeds)
+        finally:
+            del os.environ["DPPX_BANDS"]
+    if n == 1:
+        rm, ri = oracle.pixelize_uniform(frame[0], b, p.sigma, "keyed", seeds)
+        for bands in ("1", "0"):
+            assert np.array_equal(res[bands, "u"][0], rm) and np.array_equal(res[bands, "u"][1][0], ri)
+    rp, ri = oracle.pixelize_adaptive(frame[0], mask[0], b, n, p.sigma, p.sigma_sub, "keyed", seeds)
+    for bands in ("1", "0"):
+        assert res[bands, "a"][0] == rp and np.array_equal(res[bands, "a"][1][0], ri)
