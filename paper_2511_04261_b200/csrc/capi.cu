@@ -802,7 +802,8 @@ int host_pipeline_bands(dppx_ctx* ctx, bool adaptive, const dppx_frames_desc* d,
   bool bits = false;
   uint8_t* dmask = nullptr;
   int64_t mp = dmpitch, mfs = dmfs;
-  if (adaptive) {
+  // The mask ships right after band 0's rows: packing it overlaps that copy.
+  auto ship_mask = [&]() -> int {
     if (ensure(ctx, ctx->mask[0], static_cast<size_t>(dmfs))) return DPPX_ERR_OOM;
     dmask = static_cast<uint8_t*>(ctx->mask[0].p);
     if (ctx->mask_bits_mode == 1) {
@@ -834,7 +835,9 @@ int host_pipeline_bands(dppx_ctx* ctx, bool adaptive, const dppx_frames_desc* d,
                                       cudaMemcpyHostToDevice, ctx->s_in));
       ctx->kstats.h2d_bytes += static_cast<uint64_t>(N) * M;
     }
-  }
+    return DPPX_OK;
+  };
+  if (adaptive && ensure(ctx, ctx->mask[0], static_cast<size_t>(dmfs))) return DPPX_ERR_OOM;
   // Band sizes in grid rows (the last band keeps >= 2 rows for its reflections).
   int sizes[dppx_ctx::kMaxBands];
   {
@@ -851,14 +854,28 @@ int host_pipeline_bands(dppx_ctx* ctx, bool adaptive, const dppx_frames_desc* d,
   dd.mask_frame_stride = mfs;
   dd.out_pitch = dpitch;
   dd.out_frame_stride = dfs;
+  // DPPX_BAND_TRACE=1: print when each band's copies / kernels finished (timing events).
+  static const bool trace = std::getenv("DPPX_BAND_TRACE") != nullptr;
+  cudaEvent_t tr[3 * dppx_ctx::kMaxBands + 1];
+  if (trace) {
+    for (auto& e : tr) cudaEventCreate(&e);
+    cudaEventRecord(tr[3 * nb], ctx->s_in);
+  }
   int r0 = 0;
   for (int i = 0; i < nb; ++i) {
     const int r1 = r0 + sizes[i];
     const int y0 = r0 * b, y1 = std::min(r1 * b, M);
-    CUDA_TRY(ctx, cudaMemcpy2DAsync(dimg + y0 * dpitch, dpitch, img + y0 * d->pitch, d->pitch, row,
-                                    y1 - y0, cudaMemcpyHostToDevice, ctx->s_in));
+    CUDA_TRY(ctx, copy_frames(dimg + y0 * dpitch, dpitch, dpitch * (y1 - y0), img + y0 * d->pitch,
+                              d->pitch, d->pitch * (y1 - y0), row, y1 - y0, 1,
+                              cudaMemcpyHostToDevice, ctx->s_in));
     ctx->kstats.h2d_bytes += static_cast<uint64_t>(row) * (y1 - y0);
+    if (i == 0 && adaptive) {
+      if (int rc = ship_mask()) return rc;
+      dd.mask_pitch = mp;
+      dd.mask_frame_stride = mfs;
+    }
     CUDA_TRY(ctx, cudaEventRecord(ctx->band_in[i], ctx->s_in));
+    if (trace) cudaEventRecord(tr[3 * i], ctx->s_in);
     CUDA_TRY(ctx, cudaStreamWaitEvent(comp, ctx->band_in[i], 0));
     PixOpts po;
     po.mask_bits = bits;
@@ -870,12 +887,15 @@ int host_pipeline_bands(dppx_ctx* ctx, bool adaptive, const dppx_frames_desc* d,
                               ctx->sd_pinned[0], ctx->sd_pinned_n[0], ctx->comp_done[0], false, po))
       return rc;
     CUDA_TRY(ctx, cudaEventRecord(ctx->band_comp[i], comp));
+    if (trace) cudaEventRecord(tr[3 * i + 1], comp);
     if (out) {
       CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->s_out, ctx->band_comp[i], 0));
-      CUDA_TRY(ctx, cudaMemcpy2DAsync(out + y0 * d->out_pitch, d->out_pitch, dout + y0 * dpitch, dpitch,
-                                      row, y1 - y0, cudaMemcpyDeviceToHost, ctx->s_out));
+      CUDA_TRY(ctx, copy_frames(out + y0 * d->out_pitch, d->out_pitch, d->out_pitch * (y1 - y0),
+                                dout + y0 * dpitch, dpitch, dpitch * (y1 - y0), row, y1 - y0, 1,
+                                cudaMemcpyDeviceToHost, ctx->s_out));
       ctx->kstats.d2h_bytes += static_cast<uint64_t>(row) * (y1 - y0);
     }
+    if (trace) cudaEventRecord(tr[3 * i + 2], ctx->s_out);
     r0 = r1;
   }
   CUDA_TRY(ctx, cudaEventRecord(ctx->in_done[0], ctx->s_in));
@@ -892,6 +912,17 @@ int host_pipeline_bands(dppx_ctx* ctx, bool adaptive, const dppx_frames_desc* d,
   CUDA_TRY(ctx, cudaEventRecord(ctx->out_done[0], ctx->s_out));
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->s_out));
   CUDA_TRY(ctx, cudaStreamSynchronize(comp));
+  if (trace) {
+    for (int i = 0; i < nb; ++i) {
+      float a = 0, k = 0, o = 0;
+      cudaEventElapsedTime(&a, tr[3 * nb], tr[3 * i]);
+      cudaEventElapsedTime(&k, tr[3 * nb], tr[3 * i + 1]);
+      cudaEventElapsedTime(&o, tr[3 * nb], tr[3 * i + 2]);
+      std::fprintf(stderr, "band %d rows %d: in %.1f us, k1 %.1f us, out %.1f us\n", i, sizes[i],
+                   a * 1e3f, k * 1e3f, o * 1e3f);
+    }
+    for (auto& e : tr) cudaEventDestroy(e);
+  }
   if (ctx->timing) collect_timings(ctx);
   return DPPX_OK;
 }
@@ -951,12 +982,13 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
     const bool bands_ok = !(env && env[0] == '0');
     const int64_t frame_bytes = static_cast<int64_t>(M) * N * C;
     const bool inj_any = nz && nz->kind == DPPX_NOISE_INJECTED;
+    // >= 2 MB per band: a band's copies must outlast the ~20 us of host work
+    // that issues it (measured: smaller bands make the pipeline issue-bound).
+    const int nb = static_cast<int>(std::min<int64_t>(
+        {static_cast<int64_t>(dppx_ctx::kMaxBands), g.GR / 2, frame_bytes >> 21}));
     if (bands_ok && F == 1 && (op == HostOp::Uniform || op == HostOp::Adaptive) && !inj_any &&
-        g.GR >= 4 && frame_bytes >= (512 << 10)) {
-      const int nb = static_cast<int>(std::min<int64_t>(
-          {static_cast<int64_t>(dppx_ctx::kMaxBands), g.GR / 2, std::max<int64_t>(2, frame_bytes >> 18)}));
+        nb >= 2)
       return host_pipeline_bands(ctx, adaptive, d, g, img, mask, pp, nz, stats, sstride, lens, out, nb);
-    }
   }
   const int64_t dpitch = round_up(static_cast<int64_t>(N) * C, 16);
   const int64_t dmpitch = round_up(N, 16);
