@@ -715,7 +715,6 @@ int expand_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* stats, i
     // One unit per CTA (many short CTAs hide the statistics-load latency
     // better than a persistent double-buffered loop: measured 0.69 vs 0.88 ms
     // on 600 x 1080p); the kernel loops only if the grid is capped.
-    e.buffers = 1;
     const size_t smem = static_cast<size_t>(e.stage_bytes);
     const auto key = std::make_pair(reinterpret_cast<const void*>(k), smem);
     auto it = ctx->occupancy.find(key);

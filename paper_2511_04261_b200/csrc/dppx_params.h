@@ -153,15 +153,13 @@ struct ExpandArgs {
   const uint32_t* totals;    // adaptive: [F*C]
   uint8_t* out;
   int64_t opitch, ofstride;
-  // K2 (staged) only: persistent CTAs over `units` (frame group, grid row,
-  // tile), two smem tiles so a unit's TMA store overlaps the next unit.
+  // K2 (staged) only: one CTA per unit (frame group, grid row, tile).
   int tiles_per_row;
   int tensor_out_bytes;
   FastDiv div_tiles, div_rows;
   int units;
   int pack, slot_px, slot_stride;  // narrow frames: `pack` frames side by side per tile
-  int stage_bytes;                 // bytes of one smem tile
-  int buffers;                     // smem tiles per CTA (1 or 2)
+  int stage_bytes;                 // bytes of the smem tile
 };
 
 }  // namespace dppx

@@ -1162,12 +1162,9 @@ __global__ void __launch_bounds__(kConsumers)
   const int sc = (t % B4) / SB4;
   if (t == 0) prefetch_tmap(&tm_out);
   for (int u = blockIdx.x, k = 0; u < a.units; u += gridDim.x, ++k) {
-    uint8_t* buf = smem + (a.buffers == 2 ? (k & 1) : 0) * a.stage_bytes;
-    // The store that last used this buffer must have read it.
-    if (t == 0) {
-      if (a.buffers == 2) bulk_wait_read_1();
-      else bulk_wait_read_all();
-    }
+    uint8_t* buf = smem;
+    // A capped grid loops: the previous unit's store must have read the tile.
+    if (t == 0 && k > 0) bulk_wait_read_all();
     __syncthreads();
     const uint32_t rest = a.div_tiles.div(static_cast<uint32_t>(u));
     const int tile = u - static_cast<int>(rest * a.div_tiles.d);
