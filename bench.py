@@ -344,7 +344,8 @@ def main():
     value = frames_total * M * N / 1e6 / (ms_step / 1e3)
     fps = frames_total / (ms_step / 1e3)
     # roofline of K1 (dominant kernel): algorithmic bytes / measured duration
-    kfam = "stats_tma" if st["launches"]["stats_tma"] else "stats_generic"
+    kfam = ("stats_tma" if st["launches"]["stats_tma"] else
+            "stats_rows" if st["launches"].get("stats_rows") else "stats_generic")
     k1_launches = max(1, st["launches"][kfam])
     k1_ms = st["device_ms"][kfam] / k1_launches
     k1_bytes = int(F * M * N * C * 2 + payload_bytes)  # read frame, write image, write stats

@@ -115,7 +115,8 @@ typedef enum {
   DPPX_K_GENERIC = 2,  /* K1g: any b, n, C, alignment                         */
   DPPX_K_EXPAND = 3,   /* K2: statistics -> pixels                            */
   DPPX_K_AUX = 4,      /* synthetic generator, payload checks                 */
-  DPPX_K_COUNT = 5
+  DPPX_K_ROWS = 5,     /* K1r: row-streaming stats for other grid sides        */
+  DPPX_K_COUNT = 6
 } dppx_kernel_family;
 
 typedef struct {

@@ -27,6 +27,9 @@ using StatsKernel = void (*)(const CUtensorMap, const CUtensorMap, const StatsAr
 StatsKernel select_stats_kernel(int C, int b, int n, bool adaptive, bool packed);
 StatsKernel select_stats_kernel_var(int C, int b, int n);
 cudaError_t launch_gather_stage(const GatherArgs& a, cudaStream_t s);
+int rows_smem_bytes(const BatchGeom& g);
+cudaError_t launch_stats_rows(const StatsArgs& a, size_t smem, cudaStream_t s);
+cudaError_t launch_expand_rows(const ExpandArgs& a, size_t smem, cudaStream_t s);
 int stats_threads();
 int stats_tile_px();
 int stats_max_stages();
@@ -501,8 +504,18 @@ int run_stats(dppx_ctx* ctx, StatsArgs& a) {
     CUDA_TRY(ctx, launch_stats_tma(k, tin, tout, a, grid, smem, ctx->stream));
   } else {
     if (var) return kNoFusedPath;  // caller takes the 2-pass variance path
-    timing_begin(ctx, DPPX_K_GENERIC, &pt);
-    if (g.F > 0) CUDA_TRY(ctx, launch_stats_generic(a, ctx->stream));
+    // Other grid sides (b = 12, 24, 30, 40, 64, 128 ...): row-streaming K1r.
+    const int rsm = a.partial_borders ? 0 : rows_smem_bytes(g);
+    const int64_t units = static_cast<int64_t>(g.F) * a.row_count;
+    if (rsm > 0 && units <= 0x7FFFFFFF && !std::getenv("DPPX_NO_ROWS")) {
+      a.units = static_cast<int>(units);
+      a.div_rows = make_fastdiv(static_cast<uint32_t>(a.row_count));
+      timing_begin(ctx, DPPX_K_ROWS, &pt);
+      CUDA_TRY(ctx, launch_stats_rows(a, static_cast<size_t>(rsm), ctx->stream));
+    } else {
+      timing_begin(ctx, DPPX_K_GENERIC, &pt);
+      if (g.F > 0) CUDA_TRY(ctx, launch_stats_generic(a, ctx->stream));
+    }
   }
   timing_end(ctx, &pt);
   return DPPX_OK;
@@ -729,6 +742,9 @@ int expand_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* stats, i
     }
     (void)per_sm;
     CUDA_TRY(ctx, launch_expand_tma(k, tout, e, e.units, smem, ctx->stream));
+  } else if (const int rsm = rows_smem_bytes(g);
+             rsm > 0 && static_cast<int64_t>(g.F) * g.GR <= 0x7FFFFFFF && !std::getenv("DPPX_NO_ROWS")) {
+    CUDA_TRY(ctx, launch_expand_rows(e, static_cast<size_t>(rsm), ctx->stream));
   } else {
     CUDA_TRY(ctx, launch_expand(e, ctx->stream));
   }

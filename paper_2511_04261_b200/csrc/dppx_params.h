@@ -20,6 +20,9 @@ struct FastDiv {
   }
 };
 
+#ifdef __CUDACC__
+__host__ __device__
+#endif
 inline FastDiv make_fastdiv(uint32_t d) {
   uint32_t l = 0;
   while ((1ull << l) < d) ++l;

@@ -1099,6 +1099,272 @@ __global__ void __launch_bounds__(kGenericThreads) k_stats_generic(const StatsAr
 }
 
 // ============================================================================
+// K1r / K2r: row-streaming kernels for grid sides the TMA kernels do not cover
+// (PAPER.md recommends b = 12, 24, 30, 40 and uses up to b = 128): one CTA per
+// (frame, grid row). The b rows of the band are streamed through registers in
+// 16-byte chunks (coalesced, SWAR byte-column sums: two u16 counters per u32),
+// one vertical subcell row (sb rows) at a time; the byte-column sums go to a
+// u16 smem row, subcell sums are reduced from it, complex subcells are drawn
+// immediately and simple cells accumulate in smem; after the band the simple
+// cells are drawn and the reconstructed rows are emitted from one pattern row
+// per vertical subcell (each output row written once, coalesced).
+// ============================================================================
+constexpr int kRowThreads = 256;
+
+struct RowSmem {  // byte offsets into dynamic smem (host and device agree)
+  int vsum, cellsum, flag, slot, simpleval, subval, pattern, total;
+};
+
+__host__ __device__ inline int rows_align16(int x) { return (x + 15) & ~15; }
+
+__host__ __device__ inline RowSmem row_smem_layout(const BatchGeom& g) {
+  RowSmem L;
+  const int PB = g.GC * g.b * g.C;  // padded row bytes
+  const int NS = g.GC * g.n;        // subcell columns per band
+  L.vsum = 0;
+  L.cellsum = L.vsum + rows_align16(2 * PB);
+  L.flag = L.cellsum + rows_align16(4 * g.GC * g.C);
+  L.slot = L.flag + rows_align16(g.GC * g.C);
+  L.simpleval = L.slot + rows_align16(4 * g.GC);
+  L.subval = L.simpleval + rows_align16(g.GC * g.C);
+  L.pattern = L.subval + rows_align16(g.n * NS * g.C);
+  L.total = L.pattern + rows_align16(g.N * g.C);
+  return L;
+}
+
+// Emits rows [r*b, min(r*b + b, M)) of frame f from the smem value tables:
+// pixel x, channel ch of vertical subcell vs takes simpleval[c][ch] (simple
+// cell c = x / b) or subval[vs][x / sb][ch]. One pattern row per vs.
+template <int C, bool ADAPTIVE>
+__device__ void rows_emit(const BatchGeom& g, int r, uint8_t* out_frame, int64_t opitch,
+                          const uint8_t* flag, const uint8_t* simpleval, const uint8_t* subval,
+                          uint8_t* pattern, const FastDiv& div_b, const FastDiv& div_sb, bool vec16) {
+  const int t = threadIdx.x;
+  const int RB = g.N * C, NS = g.GC * g.n;
+  for (int vs = 0; vs < g.n; ++vs) {
+    const int y0 = r * g.b + vs * g.sb;
+    if (y0 >= g.M) break;
+    const int y1 = min(y0 + g.sb, g.M);
+    for (int x = t; x < RB; x += kRowThreads) {
+      const int px = x / C, ch = x - px * C;
+      const int c = static_cast<int>(div_b.div(static_cast<uint32_t>(px)));
+      uint8_t v;
+      if (!ADAPTIVE || flag[c * C + ch]) {
+        v = simpleval[c * C + ch];
+      } else {
+        const int sidx = static_cast<int>(div_sb.div(static_cast<uint32_t>(px)));
+        v = subval[(vs * NS + sidx) * C + ch];
+      }
+      pattern[x] = v;
+    }
+    __syncthreads();
+    for (int y = y0; y < y1; ++y) {
+      uint8_t* orow = out_frame + static_cast<int64_t>(y) * opitch;
+      if (vec16) {
+        const int n16 = RB >> 4;
+        for (int q = t; q < n16; q += kRowThreads)
+          reinterpret_cast<uint4*>(orow)[q] = reinterpret_cast<const uint4*>(pattern)[q];
+        for (int x = (n16 << 4) + t; x < RB; x += kRowThreads) orow[x] = pattern[x];
+      } else {
+        for (int x = t; x < RB; x += kRowThreads) orow[x] = pattern[x];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int C, bool ADAPTIVE, bool VEC16>
+__global__ void __launch_bounds__(kRowThreads, 3) k_stats_rows(const StatsArgs a) {
+  extern __shared__ __align__(16) uint8_t rsm[];
+  const BatchGeom& g = a.g;
+  const RowSmem L = row_smem_layout(g);
+  uint16_t* vsum = reinterpret_cast<uint16_t*>(rsm + L.vsum);
+  uint32_t* cellsum = reinterpret_cast<uint32_t*>(rsm + L.cellsum);
+  uint8_t* flag = rsm + L.flag;
+  uint32_t* slot = reinterpret_cast<uint32_t*>(rsm + L.slot);
+  uint8_t* simpleval = rsm + L.simpleval;
+  uint8_t* subval = rsm + L.subval;
+  uint8_t* pattern = rsm + L.pattern;
+  const int t = threadIdx.x;
+  const int RB = g.N * C, PB = g.GC * g.b * C, NS = g.GC * g.n;
+  const FastDiv div_b = make_fastdiv(static_cast<uint32_t>(g.b));
+  const FastDiv div_sb = make_fastdiv(static_cast<uint32_t>(g.sb));
+  const DrawEnv env_cell = make_env(a.noise.kind, a.exact_noise != 0, a.area, a.sigma);
+  const DrawEnv env_sub = make_env(a.noise.kind, a.exact_noise != 0, a.sub_area, a.sigma_sub);
+  const bool out_vec16 = a.out && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0 &&
+                         (a.opitch & 15) == 0 && (a.ofstride & 15) == 0;
+  for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
+    const int f = static_cast<int>(a.div_rows.div(static_cast<uint32_t>(u)));
+    const int r = a.row_begin + (u - f * a.row_count);
+    const uint8_t* frame = a.img + static_cast<int64_t>(f) * a.fstride;
+    uint32_t S_tot = 0;
+    if (ADAPTIVE) {
+      S_tot = __ldg(&a.totals[f]);
+      const uint32_t rowpre = __ldg(&a.rowprefix[static_cast<int64_t>(f) * g.GR + r]);
+      for (int c = t; c < g.GC; c += kRowThreads) {
+        const uint32_t info = __ldg(&a.cellinfo[static_cast<int64_t>(f) * g.G + r * g.GC + c]);
+#pragma unroll
+        for (int ch = 0; ch < C; ++ch) flag[c * C + ch] = info & 1u;
+        slot[c] = rowpre + (info >> 1);
+      }
+    }
+    for (int e = t; e < g.GC * C; e += kRowThreads) cellsum[e] = 0;
+    __syncthreads();
+    for (int vs = 0; vs < g.n; ++vs) {
+      // ---- byte-column sums of the sb rows of vertical subcell vs ----
+      // Chunk-major: each thread owns 16-byte column chunks and walks the sb
+      // rows for one chunk at a time (8 live SWAR counters, rows unrolled so
+      // several loads are in flight); a warp reads 512 contiguous bytes per row.
+      for (int x0 = t * 16; x0 < PB; x0 += kRowThreads * 16) {
+        uint32_t lo[4] = {0u, 0u, 0u, 0u}, hi[4] = {0u, 0u, 0u, 0u};
+        const uint8_t* colp = frame + x0;
+        const bool fast = VEC16 && x0 + 16 <= RB;
+#pragma unroll 4
+        for (int i = 0; i < g.sb; ++i) {
+          const int srow = reflect_index(r * g.b + vs * g.sb + i, g.M);
+          const uint8_t* rowp = colp + static_cast<int64_t>(srow) * a.pitch;
+          uint32_t w[4];
+          if (fast) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(rowp));
+            w[0] = v.x, w[1] = v.y, w[2] = v.z, w[3] = v.w;
+          } else {
+            const uint8_t* rowbase = rowp - x0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint32_t acc = 0;
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const int x = x0 + 4 * j + k;
+                uint32_t byte = 0;
+                if (x < RB) {
+                  byte = __ldg(rowbase + x);
+                } else if (x < PB) {  // mirrored padding column (image.cpp:105-110)
+                  const int px = x / C, ch = x - px * C;
+                  byte = __ldg(rowbase + static_cast<int64_t>(reflect_index(px, g.N)) * C + ch);
+                }
+                acc |= byte << (8 * k);
+              }
+              w[j] = acc;
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            lo[j] += w[j] & 0x00FF00FFu;
+            hi[j] += (w[j] >> 8) & 0x00FF00FFu;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int x = x0 + 4 * j;
+          if (x + 0 < PB) vsum[x + 0] = static_cast<uint16_t>(lo[j] & 0xFFFFu);
+          if (x + 1 < PB) vsum[x + 1] = static_cast<uint16_t>(hi[j] & 0xFFFFu);
+          if (x + 2 < PB) vsum[x + 2] = static_cast<uint16_t>(lo[j] >> 16);
+          if (x + 3 < PB) vsum[x + 3] = static_cast<uint16_t>(hi[j] >> 16);
+        }
+      }
+      __syncthreads();
+      // ---- subcell sums; complex subcells drawn now, simple cells accumulate ----
+      for (int item = t; item < NS * C; item += kRowThreads) {
+        const int sidx = item / C, ch = item - sidx * C;
+        const int c = sidx / g.n, sc = sidx - c * g.n;
+        uint32_t sum = 0;
+        const uint16_t* vp = vsum + sidx * g.sb * C + ch;
+        for (int k = 0; k < g.sb; ++k) sum += vp[k * C];
+        const int gidx = r * g.GC + c;
+        if (!ADAPTIVE) {  // n == 1: the subcell is the cell
+          const uint64_t cs = cell_state(a, f, ch, r, c);
+          const uint32_t v = quantize_stat(env_cell, sum, draw_bits(a, cs, f, ch, r, c, 0, 0),
+                                           inj_at(a, f, ch, gidx, 0, 0));
+          a.stats[static_cast<int64_t>(f * C + ch) * a.sstride + gidx] = static_cast<uint8_t>(v);
+          simpleval[c * C + ch] = static_cast<uint8_t>(v);
+        } else if (flag[c * C + ch]) {
+          atomicAdd(&cellsum[c * C + ch], sum);
+        } else {
+          const uint64_t cs = cell_state(a, f, ch, r, c);
+          const uint32_t v = quantize_stat(env_sub, sum, draw_bits(a, cs, f, ch, r, c, vs, sc),
+                                           inj_at(a, f, ch, gidx, vs, sc));
+          a.stats[static_cast<int64_t>(f * C + ch) * a.sstride +
+                  stat_offset(a, false, gidx, slot[c], S_tot, vs, sc)] = static_cast<uint8_t>(v);
+          subval[(vs * NS + sidx) * C + ch] = static_cast<uint8_t>(v);
+        }
+      }
+      __syncthreads();
+    }
+    if (ADAPTIVE) {  // simple cells: one draw per channel at sigma
+      for (int item = t; item < g.GC * C; item += kRowThreads) {
+        const int c = item / C, ch = item - c * C;
+        if (!flag[item]) continue;
+        const int gidx = r * g.GC + c;
+        const uint64_t cs = cell_state(a, f, ch, r, c);
+        const uint32_t v = quantize_stat(env_cell, cellsum[item], draw_bits(a, cs, f, ch, r, c, 0, 0),
+                                         inj_at(a, f, ch, gidx, 0, 0));
+        a.stats[static_cast<int64_t>(f * C + ch) * a.sstride +
+                stat_offset(a, true, gidx, slot[c], S_tot, 0, 0)] = static_cast<uint8_t>(v);
+        simpleval[item] = static_cast<uint8_t>(v);
+      }
+      __syncthreads();
+    }
+    if (a.out)
+      rows_emit<C, ADAPTIVE>(g, r, a.out + static_cast<int64_t>(f) * a.ofstride, a.opitch, flag,
+                             simpleval, subval, pattern, div_b, div_sb, out_vec16);
+    __syncthreads();
+  }
+}
+
+// K2r: statistics -> pixels for the same grid sides (broadcast_means /
+// reassemble), one CTA per (plane group = frame, grid row): value tables from
+// the payload slots (K0 run on the payload), then rows_emit.
+template <int C, bool ADAPTIVE>
+__global__ void __launch_bounds__(kRowThreads) k_expand_rows(const ExpandArgs a, int units,
+                                                             FastDiv div_rows) {
+  extern __shared__ __align__(16) uint8_t rsm[];
+  const BatchGeom& g = a.g;
+  const RowSmem L = row_smem_layout(g);
+  uint8_t* flag = rsm + L.flag;
+  uint8_t* simpleval = rsm + L.simpleval;
+  uint8_t* subval = rsm + L.subval;
+  uint8_t* pattern = rsm + L.pattern;
+  const int t = threadIdx.x;
+  const int NS = g.GC * g.n, nn = g.n * g.n;
+  const FastDiv div_b = make_fastdiv(static_cast<uint32_t>(g.b));
+  const FastDiv div_sb = make_fastdiv(static_cast<uint32_t>(g.sb));
+  const bool out_vec16 = (reinterpret_cast<uintptr_t>(a.out) & 15) == 0 && (a.opitch & 15) == 0 &&
+                         (a.ofstride & 15) == 0;
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const int f = static_cast<int>(div_rows.div(static_cast<uint32_t>(u)));
+    const int r = u - f * g.GR;
+    for (int e = t; e < g.GC * C; e += kRowThreads) {
+      const int c = e / C, ch = e - c * C;
+      const int64_t plane = static_cast<int64_t>(f) * C + ch;
+      const uint8_t* st = a.stats + plane * a.sstride;
+      const int gidx = r * g.GC + c;
+      if (!ADAPTIVE) {
+        simpleval[e] = __ldg(st + gidx);
+        continue;
+      }
+      const uint32_t info = __ldg(&a.cellinfo[plane * g.G + gidx]);
+      const uint32_t slot_s = __ldg(&a.rowprefix[plane * g.GR + r]) + (info >> 1);
+      const int64_t base = 4ll * g.G + 4;
+      flag[e] = info & 1u;
+      if (info & 1u) {
+        simpleval[e] = __ldg(st + base + slot_s);
+      } else {
+        const uint8_t* sub = st + base + __ldg(&a.totals[plane]) +
+                             static_cast<int64_t>(static_cast<uint32_t>(gidx) - slot_s) * nn;
+        for (int k = 0; k < nn; ++k) {
+          const int vs = k / g.n, sc = k - vs * g.n;
+          subval[(vs * NS + c * g.n + sc) * C + ch] = __ldg(sub + k);
+        }
+      }
+    }
+    __syncthreads();
+    rows_emit<C, ADAPTIVE>(g, r, a.out + static_cast<int64_t>(f) * a.ofstride, a.opitch, flag,
+                           simpleval, subval, pattern, div_b, div_sb, out_vec16);
+    __syncthreads();
+  }
+}
+
+// ============================================================================
 // K2: statistics -> pixels (broadcast_means pixelize.cpp:126-150,
 //     reassemble adaptive.cpp:181-245). One thread per (plane, grid row, cell).
 // ============================================================================
@@ -1627,6 +1893,54 @@ cudaError_t launch_stats_generic(const StatsArgs& a, cudaStream_t s) {
             a.g.F < 65535 ? a.g.F : 65535);
   k_stats_generic<<<grid, kGenericThreads, 0, s>>>(a);
   return cudaGetLastError();
+}
+
+// Row-streaming kernels: smem bytes needed (0 = not applicable).
+int rows_smem_bytes(const BatchGeom& g) {
+  if (g.C != 1 && g.C != 3 && g.C != 4) return 0;
+  if (g.sb > 257) return 0;  // u16 byte-column counters
+  if (static_cast<int64_t>(g.GC) * g.b * g.C > (1 << 20)) return 0;
+  const RowSmem L = row_smem_layout(g);
+  return L.total <= 200 * 1024 ? L.total : 0;
+}
+
+template <int C>
+cudaError_t launch_rows_c(const StatsArgs& a, size_t smem, bool vec16, cudaStream_t s) {
+  auto k = a.adaptive ? (vec16 ? k_stats_rows<C, true, true> : k_stats_rows<C, true, false>)
+                      : (vec16 ? k_stats_rows<C, false, true> : k_stats_rows<C, false, false>);
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const int grid = a.units < 0x7FFFFFFF ? a.units : 0x7FFFFFFF;
+  k<<<grid, kRowThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stats_rows(const StatsArgs& a, size_t smem, cudaStream_t s) {
+  const bool vec16 = (reinterpret_cast<uintptr_t>(a.img) & 15) == 0 && (a.pitch & 15) == 0 &&
+                     (a.fstride & 15) == 0;
+  if (a.g.C == 1) return launch_rows_c<1>(a, smem, vec16, s);
+  if (a.g.C == 3) return launch_rows_c<3>(a, smem, vec16, s);
+  return launch_rows_c<4>(a, smem, vec16, s);
+}
+
+template <int C>
+cudaError_t launch_expand_rows_c(const ExpandArgs& a, size_t smem, cudaStream_t s) {
+  auto k = a.adaptive ? k_expand_rows<C, true> : k_expand_rows<C, false>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const int64_t units = static_cast<int64_t>(a.g.F) * a.g.GR;
+  const int grid = units < 0x7FFFFFFF ? static_cast<int>(units) : 0x7FFFFFFF;
+  k<<<grid, kRowThreads, smem, s>>>(a, static_cast<int>(std::min<int64_t>(units, 0x7FFFFFFF)),
+                                    make_fastdiv(static_cast<uint32_t>(a.g.GR)));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_expand_rows(const ExpandArgs& a, size_t smem, cudaStream_t s) {
+  if (a.g.C == 1) return launch_expand_rows_c<1>(a, smem, s);
+  if (a.g.C == 3) return launch_expand_rows_c<3>(a, smem, s);
+  return launch_expand_rows_c<4>(a, smem, s);
 }
 
 cudaError_t launch_expand(const ExpandArgs& a, cudaStream_t s) {

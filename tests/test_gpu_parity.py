@@ -565,3 +565,34 @@ def test_single_frame_row_bands(ctx, M, N, C, b, n):
     rp, ri = oracle.pixelize_adaptive(frame[0], mask[0], b, n, p.sigma, p.sigma_sub, "keyed", seeds)
     for bands in ("1", "0"):
         assert res[bands, "a"][0] == rp and np.array_equal(res[bands, "a"][1][0], ri)
+
+
+@pytest.mark.parametrize("b,n,C,M,N", [(12, 1, 3, 131, 250), (12, 3, 3, 131, 250), (24, 4, 1, 100, 300),
+                                       (30, 5, 3, 97, 211), (40, 4, 3, 120, 170), (64, 8, 1, 130, 200),
+                                       (128, 16, 3, 300, 260), (5, 1, 4, 33, 47), (6, 3, 3, 64, 90),
+                                       (128, 1, 1, 129, 300)])
+def test_row_streaming_path(ctx, b, n, C, M, N):
+    """Grid sides outside the TMA set (the paper's b = 12, 24, 30, 40, 128) take
+    the row-streaming K1r / K2r: bit-exact vs the oracle, uniform and adaptive,
+    incl. padded rows/columns; reassemble / broadcast through K2r."""
+    rng = np.random.default_rng(b * 31 + n)
+    F = 2
+    frames = rng.integers(0, 256, (F, M, N, C), np.uint8)
+    masks = (rng.random((F, M, N)) < 0.5).astype(np.uint8)
+    masks[:, : M // 2] = 1
+    p = dp.make_privacy_params(0.5, 16, b, n)
+    seeds = dp.plane_seeds(11, F, C)
+    ctx.reset_stats()
+    ctx.set_timing(True)
+    pls, img = ctx.pixelize_adaptive(frames, masks, p, dp.NOISE_KEYED, seeds)
+    rp, ri = _oracle_adaptive(frames, masks, p, "keyed", seeds)
+    assert pls == rp and np.array_equal(img, ri)
+    assert np.array_equal(ctx.reassemble(pls, M, N, b, n, channels=C, frames=F), img)
+    if n == 1:
+        means, uimg = ctx.pixelize_uniform(frames, p, dp.NOISE_KEYED, seeds)
+        rm, rui = _oracle_uniform(frames, p, "keyed", seeds)
+        assert np.array_equal(means, rm) and np.array_equal(uimg, rui)
+        assert np.array_equal(ctx.broadcast_means(means, M, N, b, channels=C, frames=F), uimg)
+    st = ctx.stats()
+    ctx.set_timing(False)
+    assert st["launches"]["stats_rows"] >= 1, st

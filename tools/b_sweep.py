@@ -1,0 +1,64 @@
+#!/usr/bin/env python3
+"""K1 time and roofline fraction across grid sizes the paper recommends
+(PAPER.md: b = 8, 12, 16, 24 for PETS; 12, 24, 30, 40 for Venice-2; up to
+b = 128, n <= 128 for PPM-100), device-resident 1080p RGB, 120 frames."""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+CASES = [(12, 1), (12, 3), (16, 4), (24, 1), (24, 4), (30, 5), (40, 4), (64, 8), (128, 16), (128, 8)]
+
+
+def main():
+    import torch
+
+    import paper_2511_04261_b200 as dp
+    F, M, N, C = int(sys.argv[1]) if len(sys.argv) > 1 else 120, 1080, 1920, 3
+    dev = torch.device("cuda:0")
+    ctx = dp.Context(0)
+    img = torch.empty((F, M, N * C), dtype=torch.uint8, device=dev)
+    out = torch.empty_like(img)
+    mask = torch.empty((F, M, N), dtype=torch.uint8, device=dev)
+    d = dp._desc(M, N, C, F)
+    ctx.synth_frames_dev(d, 101, 0, img, mask)
+    nz, keep = dp.Context._noise(dp.NOISE_KEYED, dp.plane_seeds(42, F, C))
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    rows = []
+    for b, n in CASES:
+        p = dp.make_privacy_params(0.5, 16, b, n)
+        G = dp.grid_dims(M, N, b).grid_count()
+        adaptive = n > 1
+        if adaptive:
+            cap = dp.adaptive_payload_capacity(M, N, b, n)
+            st = (cap + 15) // 16 * 16
+            stats = torch.zeros((F * C, st), dtype=torch.uint8, device=dev)
+            lens = torch.zeros(F * C, dtype=torch.int32, device=dev)
+            call = lambda: ctx.pixelize_adaptive_dev(d, img, mask, p, nz, stats, st, lens, out)
+        else:
+            stats = torch.zeros((F * C, G), dtype=torch.uint8, device=dev)
+            call = lambda: ctx.pixelize_uniform_dev(d, img, p, nz, stats, out)
+        for _ in range(2):
+            call()
+        ctx.synchronize()
+        ctx.reset_stats()
+        ctx.set_timing(True)
+        for _ in range(5):
+            call()
+        ctx.synchronize()
+        s = ctx.stats()
+        ctx.set_timing(False)
+        fam = ("stats_tma" if s["launches"]["stats_tma"] else
+               "stats_rows" if s["launches"]["stats_rows"] else "stats_generic")
+        ms = s["device_ms"][fam] / max(1, s["launches"][fam])
+        pay = int(lens.sum().item()) if adaptive else F * C * G
+        alg = F * M * N * C * 2 + pay
+        rows.append({"b": b, "n": n, "kernel": fam, "k1_ms": round(ms, 4),
+                     "frac": round(alg / (ms / 1e3) / 1e9 / peak, 4)})
+    print(json.dumps(rows))
+
+
+if __name__ == "__main__":
+    main()
