@@ -1138,24 +1138,24 @@ __host__ __device__ inline RowSmem row_smem_layout(const BatchGeom& g) {
 template <int C, bool ADAPTIVE>
 __device__ void rows_emit(const BatchGeom& g, int r, uint8_t* out_frame, int64_t opitch,
                           const uint8_t* flag, const uint8_t* simpleval, const uint8_t* subval,
-                          uint8_t* pattern, const FastDiv& div_b, const FastDiv& div_sb, bool vec16) {
+                          uint8_t* pattern, const FastDiv& div_n, bool vec16) {
   const int t = threadIdx.x;
   const int RB = g.N * C, NS = g.GC * g.n;
   for (int vs = 0; vs < g.n; ++vs) {
     const int y0 = r * g.b + vs * g.sb;
     if (y0 >= g.M) break;
     const int y1 = min(y0 + g.sb, g.M);
-    for (int x = t; x < RB; x += kRowThreads) {
-      const int px = x / C, ch = x - px * C;
-      const int c = static_cast<int>(div_b.div(static_cast<uint32_t>(px)));
-      uint8_t v;
-      if (!ADAPTIVE || flag[c * C + ch]) {
-        v = simpleval[c * C + ch];
-      } else {
-        const int sidx = static_cast<int>(div_sb.div(static_cast<uint32_t>(px)));
-        v = subval[(vs * NS + sidx) * C + ch];
-      }
-      pattern[x] = v;
+    // pattern row: one thread per subcell column (sb pixels of C fixed values)
+    for (int sidx = t; sidx < NS; sidx += kRowThreads) {
+      const int c = static_cast<int>(div_n.div(static_cast<uint32_t>(sidx)));
+      uint8_t v[C];
+#pragma unroll
+      for (int ch = 0; ch < C; ++ch)
+        v[ch] = (!ADAPTIVE || flag[c * C + ch]) ? simpleval[c * C + ch] : subval[(vs * NS + sidx) * C + ch];
+      const int px0 = sidx * g.sb, px1 = min(px0 + g.sb, g.N);
+      for (int px = px0; px < px1; ++px)
+#pragma unroll
+        for (int ch = 0; ch < C; ++ch) pattern[px * C + ch] = v[ch];
     }
     __syncthreads();
     for (int y = y0; y < y1; ++y) {
@@ -1187,8 +1187,7 @@ __global__ void __launch_bounds__(kRowThreads, 3) k_stats_rows(const StatsArgs a
   uint8_t* pattern = rsm + L.pattern;
   const int t = threadIdx.x;
   const int RB = g.N * C, PB = g.GC * g.b * C, NS = g.GC * g.n;
-  const FastDiv div_b = make_fastdiv(static_cast<uint32_t>(g.b));
-  const FastDiv div_sb = make_fastdiv(static_cast<uint32_t>(g.sb));
+  const FastDiv div_n = make_fastdiv(static_cast<uint32_t>(g.n));
   const DrawEnv env_cell = make_env(a.noise.kind, a.exact_noise != 0, a.area, a.sigma);
   const DrawEnv env_sub = make_env(a.noise.kind, a.exact_noise != 0, a.sub_area, a.sigma_sub);
   const bool out_vec16 = a.out && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0 &&
@@ -1266,7 +1265,7 @@ __global__ void __launch_bounds__(kRowThreads, 3) k_stats_rows(const StatsArgs a
       // ---- subcell sums; complex subcells drawn now, simple cells accumulate ----
       for (int item = t; item < NS * C; item += kRowThreads) {
         const int sidx = item / C, ch = item - sidx * C;
-        const int c = sidx / g.n, sc = sidx - c * g.n;
+        const int c = static_cast<int>(div_n.div(static_cast<uint32_t>(sidx))), sc = sidx - c * g.n;
         uint32_t sum = 0;
         const uint16_t* vp = vsum + sidx * g.sb * C + ch;
         for (int k = 0; k < g.sb; ++k) sum += vp[k * C];
@@ -1306,7 +1305,7 @@ __global__ void __launch_bounds__(kRowThreads, 3) k_stats_rows(const StatsArgs a
     }
     if (a.out)
       rows_emit<C, ADAPTIVE>(g, r, a.out + static_cast<int64_t>(f) * a.ofstride, a.opitch, flag,
-                             simpleval, subval, pattern, div_b, div_sb, out_vec16);
+                             simpleval, subval, pattern, div_n, out_vec16);
     __syncthreads();
   }
 }
@@ -1326,8 +1325,7 @@ __global__ void __launch_bounds__(kRowThreads) k_expand_rows(const ExpandArgs a,
   uint8_t* pattern = rsm + L.pattern;
   const int t = threadIdx.x;
   const int NS = g.GC * g.n, nn = g.n * g.n;
-  const FastDiv div_b = make_fastdiv(static_cast<uint32_t>(g.b));
-  const FastDiv div_sb = make_fastdiv(static_cast<uint32_t>(g.sb));
+  const FastDiv div_n = make_fastdiv(static_cast<uint32_t>(g.n));
   const bool out_vec16 = (reinterpret_cast<uintptr_t>(a.out) & 15) == 0 && (a.opitch & 15) == 0 &&
                          (a.ofstride & 15) == 0;
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -1359,7 +1357,7 @@ __global__ void __launch_bounds__(kRowThreads) k_expand_rows(const ExpandArgs a,
     }
     __syncthreads();
     rows_emit<C, ADAPTIVE>(g, r, a.out + static_cast<int64_t>(f) * a.ofstride, a.opitch, flag,
-                           simpleval, subval, pattern, div_b, div_sb, out_vec16);
+                           simpleval, subval, pattern, div_n, out_vec16);
     __syncthreads();
   }
 }
