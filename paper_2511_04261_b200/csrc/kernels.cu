@@ -1112,6 +1112,7 @@ __global__ void __launch_bounds__(kGenericThreads) k_stats_generic(const StatsAr
 constexpr int kRowThreads = 256;
 
 struct RowSmem {  // byte offsets into dynamic smem (host and device agree)
+  int vg;  // vertical subcells whose byte-column sums are held at once
   int vsum, cellsum, flag, slot, simpleval, subval, pattern, total;
 };
 
@@ -1121,8 +1122,9 @@ __host__ __device__ inline RowSmem row_smem_layout(const BatchGeom& g) {
   RowSmem L;
   const int PB = g.GC * g.b * g.C;  // padded row bytes
   const int NS = g.GC * g.n;        // subcell columns per band
+  L.vg = max(1, min(g.n, (48 * 1024) / (2 * PB)));
   L.vsum = 0;
-  L.cellsum = L.vsum + rows_align16(2 * PB);
+  L.cellsum = L.vsum + rows_align16(2 * PB * L.vg);
   L.flag = L.cellsum + rows_align16(4 * g.GC * g.C);
   L.slot = L.flag + rows_align16(g.GC * g.C);
   L.simpleval = L.slot + rows_align16(4 * g.GC);
@@ -1209,65 +1211,74 @@ __global__ void __launch_bounds__(kRowThreads, 3) k_stats_rows(const StatsArgs a
     }
     for (int e = t; e < g.GC * C; e += kRowThreads) cellsum[e] = 0;
     __syncthreads();
-    for (int vs = 0; vs < g.n; ++vs) {
-      // ---- byte-column sums of the sb rows of vertical subcell vs ----
-      // Chunk-major: each thread owns 16-byte column chunks and walks the sb
-      // rows for one chunk at a time (8 live SWAR counters, rows unrolled so
-      // several loads are in flight); a warp reads 512 contiguous bytes per row.
+    for (int v0 = 0; v0 < g.n; v0 += L.vg) {
+      const int nv = min(L.vg, g.n - v0);
+      // ---- byte-column sums of vertical subcells [v0, v0 + nv) ----
+      // Chunk-major: each thread owns 16-byte column chunks and walks the rows
+      // of one chunk at a time (8 live SWAR counters, flushed per vertical
+      // subcell; rows unrolled so several loads are in flight); a warp reads
+      // 512 contiguous bytes per row.
       for (int x0 = t * 16; x0 < PB; x0 += kRowThreads * 16) {
-        uint32_t lo[4] = {0u, 0u, 0u, 0u}, hi[4] = {0u, 0u, 0u, 0u};
         const uint8_t* colp = frame + x0;
         const bool fast = VEC16 && x0 + 16 <= RB;
+        for (int vg = 0; vg < nv; ++vg) {
+          uint32_t lo[4] = {0u, 0u, 0u, 0u}, hi[4] = {0u, 0u, 0u, 0u};
+          const int row0 = r * g.b + (v0 + vg) * g.sb;
 #pragma unroll 4
-        for (int i = 0; i < g.sb; ++i) {
-          const int srow = reflect_index(r * g.b + vs * g.sb + i, g.M);
-          const uint8_t* rowp = colp + static_cast<int64_t>(srow) * a.pitch;
-          uint32_t w[4];
-          if (fast) {
-            const uint4 v = __ldg(reinterpret_cast<const uint4*>(rowp));
-            w[0] = v.x, w[1] = v.y, w[2] = v.z, w[3] = v.w;
-          } else {
-            const uint8_t* rowbase = rowp - x0;
+          for (int i = 0; i < g.sb; ++i) {
+            const int srow = reflect_index(row0 + i, g.M);
+            const uint8_t* rowp = colp + static_cast<int64_t>(srow) * a.pitch;
+            uint32_t w[4];
+            if (fast) {
+              const uint4 v = __ldg(reinterpret_cast<const uint4*>(rowp));
+              w[0] = v.x, w[1] = v.y, w[2] = v.z, w[3] = v.w;
+            } else {
+              const uint8_t* rowbase = rowp - x0;
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                uint32_t acc = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const int x = x0 + 4 * j + k;
+                  uint32_t byte = 0;
+                  if (x < RB) {
+                    byte = __ldg(rowbase + x);
+                  } else if (x < PB) {  // mirrored padding column (image.cpp:105-110)
+                    const int px = x / C, ch = x - px * C;
+                    byte = __ldg(rowbase + static_cast<int64_t>(reflect_index(px, g.N)) * C + ch);
+                  }
+                  acc |= byte << (8 * k);
+                }
+                w[j] = acc;
+              }
+            }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              uint32_t acc = 0;
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const int x = x0 + 4 * j + k;
-                uint32_t byte = 0;
-                if (x < RB) {
-                  byte = __ldg(rowbase + x);
-                } else if (x < PB) {  // mirrored padding column (image.cpp:105-110)
-                  const int px = x / C, ch = x - px * C;
-                  byte = __ldg(rowbase + static_cast<int64_t>(reflect_index(px, g.N)) * C + ch);
-                }
-                acc |= byte << (8 * k);
-              }
-              w[j] = acc;
+              lo[j] += w[j] & 0x00FF00FFu;
+              hi[j] += (w[j] >> 8) & 0x00FF00FFu;
             }
           }
+          uint16_t* vrow = vsum + vg * PB;
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            lo[j] += w[j] & 0x00FF00FFu;
-            hi[j] += (w[j] >> 8) & 0x00FF00FFu;
+            const int x = x0 + 4 * j;
+            if (x + 0 < PB) vrow[x + 0] = static_cast<uint16_t>(lo[j] & 0xFFFFu);
+            if (x + 1 < PB) vrow[x + 1] = static_cast<uint16_t>(hi[j] & 0xFFFFu);
+            if (x + 2 < PB) vrow[x + 2] = static_cast<uint16_t>(lo[j] >> 16);
+            if (x + 3 < PB) vrow[x + 3] = static_cast<uint16_t>(hi[j] >> 16);
           }
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int x = x0 + 4 * j;
-          if (x + 0 < PB) vsum[x + 0] = static_cast<uint16_t>(lo[j] & 0xFFFFu);
-          if (x + 1 < PB) vsum[x + 1] = static_cast<uint16_t>(hi[j] & 0xFFFFu);
-          if (x + 2 < PB) vsum[x + 2] = static_cast<uint16_t>(lo[j] >> 16);
-          if (x + 3 < PB) vsum[x + 3] = static_cast<uint16_t>(hi[j] >> 16);
         }
       }
       __syncthreads();
       // ---- subcell sums; complex subcells drawn now, simple cells accumulate ----
-      for (int item = t; item < NS * C; item += kRowThreads) {
-        const int sidx = item / C, ch = item - sidx * C;
+      for (int item = t; item < nv * NS * C; item += kRowThreads) {
+        const int vi = item / (NS * C);
+        const int rem = item - vi * (NS * C);
+        const int vs = v0 + vi;
+        const int sidx = rem / C, ch = rem - sidx * C;
         const int c = static_cast<int>(div_n.div(static_cast<uint32_t>(sidx))), sc = sidx - c * g.n;
         uint32_t sum = 0;
-        const uint16_t* vp = vsum + sidx * g.sb * C + ch;
+        const uint16_t* vp = vsum + vi * PB + sidx * g.sb * C + ch;
         for (int k = 0; k < g.sb; ++k) sum += vp[k * C];
         const int gidx = r * g.GC + c;
         if (!ADAPTIVE) {  // n == 1: the subcell is the cell
