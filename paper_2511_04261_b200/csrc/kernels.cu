@@ -1176,7 +1176,7 @@ __device__ void rows_emit(const BatchGeom& g, int r, uint8_t* out_frame, int64_t
 }
 
 template <int C, bool ADAPTIVE, bool VEC16>
-__global__ void __launch_bounds__(kRowThreads, 3) k_stats_rows(const StatsArgs a) {
+__global__ void __launch_bounds__(kRowThreads, 4) k_stats_rows(const StatsArgs a) {
   extern __shared__ __align__(16) uint8_t rsm[];
   const BatchGeom& g = a.g;
   const RowSmem L = row_smem_layout(g);
