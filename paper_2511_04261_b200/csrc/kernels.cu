@@ -1113,7 +1113,7 @@ constexpr int kRowThreads = 256;
 
 struct RowSmem {  // byte offsets into dynamic smem (host and device agree)
   int vg;  // vertical subcells whose byte-column sums are held at once
-  int vsum, cellsum, flag, slot, simpleval, subval, pattern, total;
+  int vsum, cellsum, flag, slot, simpleval, subval, pattern, cstate, total;
 };
 
 __host__ __device__ inline int rows_align16(int x) { return (x + 15) & ~15; }
@@ -1130,7 +1130,8 @@ __host__ __device__ inline RowSmem row_smem_layout(const BatchGeom& g) {
   L.simpleval = L.slot + rows_align16(4 * g.GC);
   L.subval = L.simpleval + rows_align16(g.GC * g.C);
   L.pattern = L.subval + rows_align16(g.n * NS * g.C);
-  L.total = L.pattern + rows_align16(g.N * g.C);
+  L.cstate = L.pattern + rows_align16(g.N * g.C);
+  L.total = L.cstate + 8 * g.GC * g.C;
   return L;
 }
 
@@ -1187,6 +1188,7 @@ __global__ void __launch_bounds__(kRowThreads, 4) k_stats_rows(const StatsArgs a
   uint8_t* simpleval = rsm + L.simpleval;
   uint8_t* subval = rsm + L.subval;
   uint8_t* pattern = rsm + L.pattern;
+  uint64_t* cstate = reinterpret_cast<uint64_t*>(rsm + L.cstate);  // key_cell per (cell, ch)
   const int t = threadIdx.x;
   const int RB = g.N * C, PB = g.GC * g.b * C, NS = g.GC * g.n;
   const FastDiv div_n = make_fastdiv(static_cast<uint32_t>(g.n));
@@ -1209,7 +1211,11 @@ __global__ void __launch_bounds__(kRowThreads, 4) k_stats_rows(const StatsArgs a
         slot[c] = rowpre + (info >> 1);
       }
     }
-    for (int e = t; e < g.GC * C; e += kRowThreads) cellsum[e] = 0;
+    for (int e = t; e < g.GC * C; e += kRowThreads) {
+      cellsum[e] = 0;
+      const int c = e / C, ch = e - c * C;
+      cstate[e] = cell_state(a, f, ch, r, c);  // one mix64 per cell and channel
+    }
     __syncthreads();
     for (int v0 = 0; v0 < g.n; v0 += L.vg) {
       const int nv = min(L.vg, g.n - v0);
@@ -1282,7 +1288,7 @@ __global__ void __launch_bounds__(kRowThreads, 4) k_stats_rows(const StatsArgs a
         for (int k = 0; k < g.sb; ++k) sum += vp[k * C];
         const int gidx = r * g.GC + c;
         if (!ADAPTIVE) {  // n == 1: the subcell is the cell
-          const uint64_t cs = cell_state(a, f, ch, r, c);
+          const uint64_t cs = cstate[c * C + ch];
           const uint32_t v = quantize_stat(env_cell, sum, draw_bits(a, cs, f, ch, r, c, 0, 0),
                                            inj_at(a, f, ch, gidx, 0, 0));
           a.stats[static_cast<int64_t>(f * C + ch) * a.sstride + gidx] = static_cast<uint8_t>(v);
@@ -1290,7 +1296,7 @@ __global__ void __launch_bounds__(kRowThreads, 4) k_stats_rows(const StatsArgs a
         } else if (flag[c * C + ch]) {
           atomicAdd(&cellsum[c * C + ch], sum);
         } else {
-          const uint64_t cs = cell_state(a, f, ch, r, c);
+          const uint64_t cs = cstate[c * C + ch];
           const uint32_t v = quantize_stat(env_sub, sum, draw_bits(a, cs, f, ch, r, c, vs, sc),
                                            inj_at(a, f, ch, gidx, vs, sc));
           a.stats[static_cast<int64_t>(f * C + ch) * a.sstride +
@@ -1305,7 +1311,7 @@ __global__ void __launch_bounds__(kRowThreads, 4) k_stats_rows(const StatsArgs a
         const int c = item / C, ch = item - c * C;
         if (!flag[item]) continue;
         const int gidx = r * g.GC + c;
-        const uint64_t cs = cell_state(a, f, ch, r, c);
+        const uint64_t cs = cstate[item];
         const uint32_t v = quantize_stat(env_cell, cellsum[item], draw_bits(a, cs, f, ch, r, c, 0, 0),
                                          inj_at(a, f, ch, gidx, 0, 0));
         a.stats[static_cast<int64_t>(f * C + ch) * a.sstride +
