@@ -1122,7 +1122,7 @@ __host__ __device__ inline RowSmem row_smem_layout(const BatchGeom& g) {
   RowSmem L;
   const int PB = g.GC * g.b * g.C;  // padded row bytes
   const int NS = g.GC * g.n;        // subcell columns per band
-  L.vg = max(1, min(g.n, (48 * 1024) / (2 * PB)));
+  L.vg = max(1, min(g.n, (24 * 1024) / (2 * PB)));
   L.vsum = 0;
   L.cellsum = L.vsum + rows_align16(2 * PB * L.vg);
   L.flag = L.cellsum + rows_align16(4 * g.GC * g.C);
