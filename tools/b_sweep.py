@@ -55,8 +55,22 @@ def main():
         ms = s["device_ms"][fam] / max(1, s["launches"][fam])
         pay = int(lens.sum().item()) if adaptive else F * C * G
         alg = F * M * N * C * 2 + pay
+        # reconstruction from the statistics (K0 on the payload + K2 / K2r)
+        ctx.reset_stats()
+        ctx.set_timing(True)
+        for _ in range(3):
+            if adaptive:
+                ctx.reassemble_dev(d, stats, st, lens, b, n, out)
+            else:
+                ctx.broadcast_means_dev(d, stats, b, out)
+        ctx.synchronize()
+        s2 = ctx.stats()
+        ctx.set_timing(False)
+        k2 = s2["device_ms"]["expand"] / max(1, s2["launches"]["expand"])
         rows.append({"b": b, "n": n, "kernel": fam, "k1_ms": round(ms, 4),
-                     "frac": round(alg / (ms / 1e3) / 1e9 / peak, 4)})
+                     "frac": round(alg / (ms / 1e3) / 1e9 / peak, 4),
+                     "k2_ms": round(k2, 4),
+                     "k2_frac": round((F * M * N * C + pay) / (k2 / 1e3) / 1e9 / peak, 4)})
     print(json.dumps(rows))
 
 
