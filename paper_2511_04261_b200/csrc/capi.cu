@@ -32,6 +32,7 @@ cudaError_t launch_stats_rows(const StatsArgs& a, size_t smem, cudaStream_t s);
 cudaError_t launch_expand_rows(const ExpandArgs& a, size_t smem, cudaStream_t s);
 int stats_threads();
 int stats_tile_px();
+int stats_tile_px_for(int b);
 int stats_max_stages();
 cudaError_t launch_classify(const ClassifyArgs& a, cudaStream_t s);
 cudaError_t launch_stats_tma(StatsKernel k, const CUtensorMap& tin, const CUtensorMap& tout,
@@ -434,7 +435,7 @@ int run_stats(dppx_ctx* ctx, StatsArgs& a) {
                        (!a.out || (aligned16(a.out) && a.opitch % 16 == 0 && a.ofstride % 16 == 0));
   PendingTiming pt;
   CUtensorMap tin{}, tout{};
-  const int tile = stats_tile_px();
+  const int tile = stats_tile_px_for(g.b);
   const int64_t row_bytes = static_cast<int64_t>(g.N) * g.C;
   // Narrow frames: pack several padded frame rows side by side in one tile.
   const int padded_px = g.GC * g.b;

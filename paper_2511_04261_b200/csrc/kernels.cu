@@ -376,7 +376,9 @@ struct UnitPos {
   int fg, r, tile, px0;  // frame group (frames fg*pack + j), grid row, column tile
 };
 
-template <bool PACKED>
+// TILE: pixels per unit column tile (512 for power-of-two cells; general cell
+// widths use whole cells per warp, see k_stats_tma).
+template <bool PACKED, int TILE = kTilePx>
 __device__ __forceinline__ UnitPos decode_unit(const StatsArgs& a, int u) {
   UnitPos p;
   const uint32_t rest = a.div_tiles.div(static_cast<uint32_t>(u));
@@ -384,14 +386,14 @@ __device__ __forceinline__ UnitPos decode_unit(const StatsArgs& a, int u) {
   const uint32_t fg = a.div_rows.div(rest);
   p.r = a.row_begin + static_cast<int>(rest - fg * a.div_rows.d);
   p.fg = static_cast<int>(fg);
-  p.px0 = PACKED ? 0 : p.tile * kTilePx;  // packed units are one tile wide
+  p.px0 = PACKED ? 0 : p.tile * TILE;  // packed units are one tile wide
   return p;
 }
 
 // Slot geometry: compile-time for wide frames (one 512-px slot per unit).
-template <bool PACKED>
+template <bool PACKED, int TILE = kTilePx>
 __device__ __forceinline__ int slot_px(const StatsArgs& a) {
-  return PACKED ? a.slot_px : kTilePx;
+  return PACKED ? a.slot_px : TILE;
 }
 template <bool PACKED>
 __device__ __forceinline__ int units_pack(const StatsArgs& a) {
@@ -399,9 +401,9 @@ __device__ __forceinline__ int units_pack(const StatsArgs& a) {
 }
 
 // Real bytes of a slot row starting at column px0.
-template <int C, bool PACKED>
+template <int C, bool PACKED, int TILE = kTilePx>
 __device__ __forceinline__ int valid_bytes(const StatsArgs& a, int px0) {
-  return min(slot_px<PACKED>(a), a.g.N - px0) * C;
+  return min(slot_px<PACKED, TILE>(a), a.g.N - px0) * C;
 }
 
 // A band whose rows run past M needs mirrored rows (image.cpp:105-110): it is
@@ -413,24 +415,24 @@ __device__ __forceinline__ bool band_reflects(const StatsArgs& a, int r) {
 
 // Bytes per row a 1-D bulk copy stages (multiple of 16): rounded up into the
 // pitch slack when the rows have it, else down (the rest is filled by threads).
-template <int C, bool PACKED>
+template <int C, bool PACKED, int TILE = kTilePx>
 __device__ __forceinline__ int bulk_row_bytes(const StatsArgs& a, int px0) {
-  const int v = valid_bytes<C, PACKED>(a, px0);
-  return a.row_slack ? min(slot_px<PACKED>(a) * C, (v + 15) & ~15) : (v & ~15);
+  const int v = valid_bytes<C, PACKED, TILE>(a, px0);
+  return a.row_slack ? min(slot_px<PACKED, TILE>(a) * C, (v + 15) & ~15) : (v & ~15);
 }
 
 // Bytes of each smem slot row that the producer's copies deliver.
-template <int C, int B, bool PACKED>
+template <int C, int B, bool PACKED, int TILE = kTilePx>
 __device__ __forceinline__ int staged_bytes(const StatsArgs& a, const UnitPos& p) {
-  if (band_reflects<B>(a, p.r)) return bulk_row_bytes<C, PACKED>(a, p.px0);
-  return max(0, min(slot_px<PACKED>(a) * C, a.tensor_in_bytes - p.px0 * C));
+  if (band_reflects<B>(a, p.r)) return bulk_row_bytes<C, PACKED, TILE>(a, p.px0);
+  return max(0, min(slot_px<PACKED, TILE>(a) * C, a.tensor_in_bytes - p.px0 * C));
 }
 
-template <int C, int B, bool PACKED>
+template <int C, int B, bool PACKED, int TILE = kTilePx>
 __device__ __forceinline__ void load_unit(const StatsArgs& a, const CUtensorMap* tm, int u,
                                           uint8_t* st, uint64_t* bar) {
-  const UnitPos p = decode_unit<PACKED>(a, u);
-  const int srb = slot_px<PACKED>(a) * C;
+  const UnitPos p = decode_unit<PACKED, TILE>(a, u);
+  const int srb = slot_px<PACKED, TILE>(a) * C;
   const int pk = units_pack<PACKED>(a);
   const int nf = PACKED ? min(pk, a.g.F - p.fg * pk) : 1;
   if (!band_reflects<B>(a, p.r)) {
@@ -439,7 +441,7 @@ __device__ __forceinline__ void load_unit(const StatsArgs& a, const CUtensorMap*
       tma_load_3d(st + j * a.slot_stride, tm, p.px0 * C / 8, p.r * B, p.fg * pk + j, bar);
     return;
   }
-  const uint32_t copy = static_cast<uint32_t>(bulk_row_bytes<C, PACKED>(a, p.px0));
+  const uint32_t copy = static_cast<uint32_t>(bulk_row_bytes<C, PACKED, TILE>(a, p.px0));
   mbar_arrive_expect_tx(bar, copy * B * nf);
   if (copy == 0) return;
 #pragma unroll 1
@@ -458,10 +460,10 @@ __device__ __forceinline__ void load_unit(const StatsArgs& a, const CUtensorMap*
 // One 3-D box store per slot: rows >= M and bytes past the tensor's row are
 // clipped by the TMA unit; the consumers write the (< 8) bytes past
 // tensor_out_bytes.
-template <int C, int B, bool PACKED>
+template <int C, int B, bool PACKED, int TILE = kTilePx>
 __device__ __forceinline__ void store_unit(const StatsArgs& a, const CUtensorMap* tm, int u,
                                            const uint8_t* st) {
-  const UnitPos p = decode_unit<PACKED>(a, u);
+  const UnitPos p = decode_unit<PACKED, TILE>(a, u);
   if (p.px0 * C >= a.tensor_out_bytes) return;
   const int pk = units_pack<PACKED>(a);
   const int nf = PACKED ? min(pk, a.g.F - p.fg * pk) : 1;
@@ -473,11 +475,11 @@ __device__ __forceinline__ void store_unit(const StatsArgs& a, const CUtensorMap
 
 // Output bytes of a unit past the output tensor map's row extent (< 8 per row:
 // the TMA store covers [0, tensor_out_bytes)), written by the 32 producer lanes.
-template <int C, int B, bool PACKED>
+template <int C, int B, bool PACKED, int TILE = kTilePx>
 __device__ __forceinline__ void store_tail(const StatsArgs& a, int u, const uint8_t* st, int lane) {
-  const UnitPos p = decode_unit<PACKED>(a, u);
-  const int srb = slot_px<PACKED>(a) * C;
-  const int vbytes = valid_bytes<C, PACKED>(a, p.px0);
+  const UnitPos p = decode_unit<PACKED, TILE>(a, u);
+  const int srb = slot_px<PACKED, TILE>(a) * C;
+  const int vbytes = valid_bytes<C, PACKED, TILE>(a, p.px0);
   const int scopy = max(0, min(srb, a.tensor_out_bytes - p.px0 * C));
   if (scopy >= vbytes) return;
   const int span = vbytes - scopy;
@@ -540,6 +542,24 @@ __device__ __forceinline__ uint32_t square_row(const uint8_t* row, uint32_t acc)
 #pragma unroll
   for (int k = 0; k < (C == 4 ? 4 : C); ++k) acc = __dp4a(w[k], w[k], acc);
   return acc;
+}
+
+// Sum over an aligned group of G lanes (a cell or subcell), result in every lane
+// of the group: butterfly for power-of-two G, else gather at the group's first
+// lane and broadcast (groups never straddle a warp: see k_stats_tma's LPW).
+template <int G>
+__device__ __forceinline__ uint32_t group_sum(uint32_t x) {
+  if constexpr ((G & (G - 1)) == 0) {
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+    return x;
+  } else {
+    const int lane = threadIdx.x & 31;
+    uint32_t sum = x;
+#pragma unroll
+    for (int o = 1; o < G; ++o) sum += __shfl_down_sync(0xFFFFFFFFu, x, o);
+    return __shfl_sync(0xFFFFFFFFu, sum, lane - lane % G);
+  }
 }
 
 // Values of the C channels of one statistic, computed by the GL lanes of a
@@ -609,9 +629,15 @@ __global__ void __launch_bounds__(kStatsThreads)
   constexpr int B = 4 * B4;
   constexpr int SB = B / NSUB;
   constexpr int SB4 = SB / 4;
-  constexpr int ROWB = kTilePx * C;
+  // Strips per warp: whole cells only (a cell is B4 adjacent lanes), so for
+  // B4 not a power of two (b = 12, 24) the last 32 % B4 lanes of each warp
+  // idle and the tile is 16 * LPW px (480 at b = 12 or 24) instead of 512.
+  constexpr int LPW = (32 / B4) * B4;
+  constexpr int TILE = 4 * (kConsumers / 32) * LPW;
+  constexpr int ROWB = TILE * C;
   constexpr uint32_t STAGE = B * ROWB;
-  static_assert(SB % 4 == 0 && 32 % B4 == 0, "fast-path geometry");
+  static_assert(SB % 4 == 0 && B4 <= 32 && B4 % SB4 == 0, "fast-path geometry");
+  static_assert(TILE == kTilePx || !PACKED, "packed slots use 512-px tiles");
   static_assert(!VAR || (ADAPTIVE && !PACKED), "variance staging: wide adaptive frames only");
 
   extern __shared__ __align__(128) uint8_t smem[];
@@ -647,8 +673,8 @@ __global__ void __launch_bounds__(kStatsThreads)
       mbar_wait(&done_bar[s], use & 1);        // every lane acquires the smem writes
       if (a.out) {
         const int uu = stage_unit[s];
-        store_tail<C, B, PACKED>(a, uu, smem + s * STAGE, lane);
-        if (lane == 0) store_unit<C, B, PACKED>(a, &tm_out, uu, smem + s * STAGE);
+        store_tail<C, B, PACKED, TILE>(a, uu, smem + s * STAGE, lane);
+        if (lane == 0) store_unit<C, B, PACKED, TILE>(a, &tm_out, uu, smem + s * STAGE);
       }
       __syncwarp();
     };
@@ -674,7 +700,7 @@ __global__ void __launch_bounds__(kStatsThreads)
         if (u < 0)
           mbar_arrive_expect_tx(&full_bar[s], 0);
         else
-          load_unit<C, B, PACKED>(a, &tm_in, u, smem + s * STAGE, &full_bar[s]);
+          load_unit<C, B, PACKED, TILE>(a, &tm_in, u, smem + s * STAGE, &full_bar[s]);
       }
       u = __shfl_sync(0xFFFFFFFFu, u, 0);
       if (u < 0) break;
@@ -697,13 +723,17 @@ __global__ void __launch_bounds__(kStatsThreads)
     uint32_t info, rowpre, stot;
     uint64_t seed[C];
   };
-  // Slot of this thread's 4-px strip (fixed for the kernel). Wide frames
-  // (PACKED = false) have one 512-px slot: the compiler folds all of this.
-  const int my_j = PACKED ? (4 * t) / a.slot_px : 0;
-  const bool in_slot = my_j < (PACKED ? a.pack : 1);
+  // This thread's 4-px strip in the tile: lanes >= LPW of a warp have none
+  // (only when B4 is not a power of two) and compute on strip 0, inactive.
+  const bool strip_ok = (t & 31) < LPW;
+  const int sx = strip_ok ? (t >> 5) * LPW + (t & 31) : 0;  // strip index
+  // Slot of the strip (fixed for the kernel). Wide frames (PACKED = false)
+  // have one TILE-px slot: the compiler folds all of this.
+  const int my_j = PACKED ? (4 * sx) / a.slot_px : 0;
+  const bool in_slot = strip_ok && my_j < (PACKED ? a.pack : 1);
   const int jj = in_slot ? my_j : 0;
-  const int lpx = 4 * t - jj * (PACKED ? a.slot_px : kTilePx);  // strip column in its slot
-  const int srb = PACKED ? a.slot_px * C : kTilePx * C;         // smem bytes per slot row
+  const int lpx = 4 * sx - jj * (PACKED ? a.slot_px : TILE);  // strip column in its slot
+  const int srb = PACKED ? a.slot_px * C : TILE * C;         // smem bytes per slot row
   // Packed mode: byte offsets of the mirrored sources of the padding bytes
   // [N*C, GC*b*C) of a slot row (image.cpp:105-110), shared by all units.
   __shared__ uint16_t fill_src[128];
@@ -738,9 +768,9 @@ __global__ void __launch_bounds__(kStatsThreads)
 #pragma unroll
     for (int ch = 0; ch < C; ++ch) m.seed[ch] = 0;
     if (m.u >= 0) {
-      const UnitPos q = decode_unit<PACKED>(a, m.u);
+      const UnitPos q = decode_unit<PACKED, TILE>(a, m.u);
       const int qf = q.fg * units_pack<PACKED>(a) + jj;
-      const int qcell = PACKED ? (q.px0 + lpx) / B : q.px0 / B + t / B4;
+      const int qcell = PACKED ? (q.px0 + lpx) / B : q.px0 / B + sx / B4;
       if (!PACKED || qf < g.F) {
         if (ADAPTIVE && !VAR && qcell < g.GC) {
           m.info = __ldg(&a.cellinfo[static_cast<int64_t>(qf) * g.G + q.r * g.GC + qcell]);
@@ -763,19 +793,19 @@ __global__ void __launch_bounds__(kStatsThreads)
     const Meta cur = next;
     const int u = cur.u;
     if (u < 0) break;
-    const UnitPos p = decode_unit<PACKED>(a, u);
+    const UnitPos p = decode_unit<PACKED, TILE>(a, u);
     const int f = p.fg * units_pack<PACKED>(a) + jj;  // this thread's frame
-    const int cell = PACKED ? (p.px0 + lpx) / B : p.px0 / B + t / B4;
-    const int lic = t % B4;        // lane within cell
+    const int cell = PACKED ? (p.px0 + lpx) / B : p.px0 / B + sx / B4;
+    const int lic = sx % B4;       // lane within cell
     const int sc = lic / SB4;      // subcell column
-    const bool active = (!PACKED || (in_slot && f < g.F)) && cell < g.GC;
+    const bool active = in_slot && (!PACKED || f < g.F) && cell < g.GC;
     const int gidx = p.r * g.GC + cell;
     const bool simple0 = !ADAPTIVE || (cur.info & 1u);  // VAR: decided after the sums
     const uint32_t slot_s = cur.rowpre + (cur.info >> 1);
     const uint32_t S_tot = cur.stot;
-    const int vbytes = valid_bytes<C, PACKED>(a, p.px0);
-    const int copy = staged_bytes<C, B, PACKED>(a, p);  // bytes per row the producer staged
-    const int need = min(slot_px<PACKED>(a), g.GC * B - p.px0) * C;
+    const int vbytes = valid_bytes<C, PACKED, TILE>(a, p.px0);
+    const int copy = staged_bytes<C, B, PACKED, TILE>(a, p);  // bytes per row the producer staged
+    const int need = min(slot_px<PACKED, TILE>(a), g.GC * B - p.px0) * C;
     const int nf = PACKED ? min(a.pack, g.F - p.fg * a.pack) : 1;
     uint64_t cs[C];
 #pragma unroll
@@ -849,11 +879,8 @@ __global__ void __launch_bounds__(kStatsThreads)
       uint32_t s1 = 0;
 #pragma unroll
       for (int ch = 0; ch < C; ++ch) s1 += tot[ch];
-#pragma unroll
-      for (int o = 1; o < B4; o <<= 1) {
-        s1 += __shfl_xor_sync(0xFFFFFFFFu, s1, o);
-        sq += __shfl_xor_sync(0xFFFFFFFFu, sq, o);
-      }
+      s1 = group_sum<B4>(s1);
+      sq = group_sum<B4>(sq);
       const long long ns = static_cast<long long>(C) * B * B;
       const double num = static_cast<double>(ns * static_cast<long long>(sq) -
                                              static_cast<long long>(s1) * static_cast<long long>(s1));
@@ -889,9 +916,7 @@ __global__ void __launch_bounds__(kStatsThreads)
           }
           if (cx_any) {
 #pragma unroll
-            for (int o = 1; o < SB4; o <<= 1)
-#pragma unroll
-              for (int ch = 0; ch < C; ++ch) acc[ch] += __shfl_xor_sync(0xFFFFFFFFu, acc[ch], o);
+            for (int ch = 0; ch < C; ++ch) acc[ch] = group_sum<SB4>(acc[ch]);
             if constexpr (compact) {
               if (cx && lic % SB4 == 0) {
 #pragma unroll
@@ -985,9 +1010,7 @@ __global__ void __launch_bounds__(kStatsThreads)
 
     // whole cell (uniform, or adaptive simple): reduce over B4 strips.
 #pragma unroll
-    for (int o = 1; o < B4; o <<= 1)
-#pragma unroll
-      for (int ch = 0; ch < C; ++ch) tot[ch] += __shfl_xor_sync(0xFFFFFFFFu, tot[ch], o);
+    for (int ch = 0; ch < C; ++ch) tot[ch] = group_sum<B4>(tot[ch]);
     {
       uint32_t val[C];
       group_values<C, B4>(a, env_cell, active && simple, tot, cs, f, p.r, cell, 0, 0, val);
@@ -1791,6 +1814,10 @@ StatsKernel pick_b(int b, int n) {
   DPPX_CASE(2, 1)
   DPPX_CASE(4, 1)
   DPPX_CASE(8, 1)
+  if constexpr (!PK) {  // the paper's b = 12, 24 (whole cells per warp, 480-px tiles)
+    DPPX_CASE(3, 1)
+    DPPX_CASE(6, 1)
+  }
   if constexpr (AD) {
     DPPX_CASE(2, 2)
     DPPX_CASE(4, 2)
@@ -1798,6 +1825,12 @@ StatsKernel pick_b(int b, int n) {
     DPPX_CASE(8, 2)
     DPPX_CASE(8, 4)
     DPPX_CASE(8, 8)
+    if constexpr (!PK) {
+      DPPX_CASE(3, 3)
+      DPPX_CASE(6, 2)
+      DPPX_CASE(6, 3)
+      DPPX_CASE(6, 6)
+    }
   }
 #undef DPPX_CASE
   return nullptr;
@@ -1888,6 +1921,13 @@ cudaError_t launch_expand_tma(ExpandKernel k, const CUtensorMap& tout, const Exp
 
 int stats_threads() { return kStatsThreads; }
 int stats_tile_px() { return kTilePx; }
+
+// Tile width of the staged kernel for grid side b (whole cells per warp).
+int stats_tile_px_for(int b) {
+  const int b4 = b / 4;
+  if (b % 4 != 0 || b4 < 1 || b4 > 32) return kTilePx;
+  return 4 * (kConsumers / 32) * ((32 / b4) * b4);
+}
 int stats_max_stages() { return kMaxStages; }
 
 cudaError_t launch_classify(const ClassifyArgs& a, cudaStream_t s) {

@@ -595,4 +595,36 @@ def test_row_streaming_path(ctx, b, n, C, M, N):
         assert np.array_equal(ctx.broadcast_means(means, M, N, b, channels=C, frames=F), uimg)
     st = ctx.stats()
     ctx.set_timing(False)
-    assert st["launches"]["stats_rows"] >= 1, st
+    assert st["launches"]["stats_rows"] + st["launches"]["stats_tma"] >= 1, st
+    assert st["launches"]["stats_generic"] == 0, st
+
+
+
+@pytest.mark.parametrize("b,n,C,M,N", [(12, 1, 3, 131, 1000), (12, 3, 3, 100, 970), (24, 1, 1, 200, 1500),
+                                       (24, 2, 3, 77, 1100), (24, 3, 3, 130, 1450), (24, 6, 1, 99, 980),
+                                       (12, 3, 1, 1080, 1920), (24, 6, 3, 1080, 1920)])
+def test_staged_kernel_whole_cell_warps(ctx, b, n, C, M, N):
+    """b = 12, 24 (the paper's recommended sizes) on the TMA kernel with whole
+    cells per warp (LPW = 30 lanes, 480-px tiles, gather+broadcast lane-group
+    sums): bit-exact vs the oracle, incl. padded rows/columns and multi-tile rows."""
+    rng = np.random.default_rng(b * 7 + n * 3 + C)
+    F = 2
+    frames = rng.integers(0, 256, (F, M, N, C), np.uint8)
+    masks = np.ones((F, M, N), np.uint8)
+    masks[:, M // 4: 3 * M // 4, N // 3: 2 * N // 3] = 0
+    masks[1] = (rng.random((M, N)) < 0.7)
+    p = dp.make_privacy_params(0.5, 16, b, n)
+    seeds = dp.plane_seeds(5, F, C)
+    ctx.reset_stats()
+    ctx.set_timing(True)
+    pls, img = ctx.pixelize_adaptive(frames, masks, p, dp.NOISE_KEYED, seeds)
+    if n == 1:
+        means, uimg = ctx.pixelize_uniform(frames, p, dp.NOISE_KEYED, seeds)
+    st = ctx.stats()
+    ctx.set_timing(False)
+    assert st["launches"]["stats_tma"] >= 1, st
+    rp, ri = _oracle_adaptive(frames, masks, p, "keyed", seeds)
+    assert pls == rp and np.array_equal(img, ri)
+    if n == 1:
+        rm, rui = _oracle_uniform(frames, p, "keyed", seeds)
+        assert np.array_equal(means, rm) and np.array_equal(uimg, rui)
