@@ -1814,9 +1814,11 @@ StatsKernel pick_b(int b, int n) {
   DPPX_CASE(2, 1)
   DPPX_CASE(4, 1)
   DPPX_CASE(8, 1)
-  if constexpr (!PK) {  // the paper's b = 12, 24 (whole cells per warp, 480-px tiles)
+  if constexpr (!PK) {  // the paper's b = 12, 20, 24, 40 (whole cells per warp, 480-px tiles)
     DPPX_CASE(3, 1)
+    DPPX_CASE(5, 1)
     DPPX_CASE(6, 1)
+    DPPX_CASE(10, 1)
   }
   if constexpr (AD) {
     DPPX_CASE(2, 2)
@@ -1827,9 +1829,13 @@ StatsKernel pick_b(int b, int n) {
     DPPX_CASE(8, 8)
     if constexpr (!PK) {
       DPPX_CASE(3, 3)
+      DPPX_CASE(5, 5)
       DPPX_CASE(6, 2)
       DPPX_CASE(6, 3)
       DPPX_CASE(6, 6)
+      DPPX_CASE(10, 2)
+      DPPX_CASE(10, 5)
+      DPPX_CASE(10, 10)
     }
   }
 #undef DPPX_CASE

@@ -602,7 +602,9 @@ def test_row_streaming_path(ctx, b, n, C, M, N):
 
 @pytest.mark.parametrize("b,n,C,M,N", [(12, 1, 3, 131, 1000), (12, 3, 3, 100, 970), (24, 1, 1, 200, 1500),
                                        (24, 2, 3, 77, 1100), (24, 3, 3, 130, 1450), (24, 6, 1, 99, 980),
-                                       (12, 3, 1, 1080, 1920), (24, 6, 3, 1080, 1920)])
+                                       (12, 3, 1, 1080, 1920), (24, 6, 3, 1080, 1920),
+                                       (20, 1, 3, 150, 1000), (20, 5, 3, 97, 990), (40, 1, 3, 170, 1100),
+                                       (40, 2, 1, 95, 1001), (40, 5, 3, 200, 1500), (40, 10, 3, 121, 979)])
 def test_staged_kernel_whole_cell_warps(ctx, b, n, C, M, N):
     """b = 12, 24 (the paper's recommended sizes) on the TMA kernel with whole
     cells per warp (LPW = 30 lanes, 480-px tiles, gather+broadcast lane-group
