@@ -1819,6 +1819,7 @@ StatsKernel pick_b(int b, int n) {
     DPPX_CASE(5, 1)
     DPPX_CASE(6, 1)
     DPPX_CASE(10, 1)
+    DPPX_CASE(16, 1)  // b = 64: 98 KB stages, 1 CTA/SM
   }
   if constexpr (AD) {
     DPPX_CASE(2, 2)
@@ -1836,6 +1837,10 @@ StatsKernel pick_b(int b, int n) {
       DPPX_CASE(10, 2)
       DPPX_CASE(10, 5)
       DPPX_CASE(10, 10)
+      DPPX_CASE(16, 2)
+      DPPX_CASE(16, 4)
+      DPPX_CASE(16, 8)
+      DPPX_CASE(16, 16)
     }
   }
 #undef DPPX_CASE

@@ -604,7 +604,8 @@ def test_row_streaming_path(ctx, b, n, C, M, N):
                                        (24, 2, 3, 77, 1100), (24, 3, 3, 130, 1450), (24, 6, 1, 99, 980),
                                        (12, 3, 1, 1080, 1920), (24, 6, 3, 1080, 1920),
                                        (20, 1, 3, 150, 1000), (20, 5, 3, 97, 990), (40, 1, 3, 170, 1100),
-                                       (40, 2, 1, 95, 1001), (40, 5, 3, 200, 1500), (40, 10, 3, 121, 979)])
+                                       (40, 2, 1, 95, 1001), (40, 5, 3, 200, 1500), (40, 10, 3, 121, 979),
+                                       (64, 1, 3, 200, 1100), (64, 8, 3, 140, 1300), (64, 16, 1, 130, 700)])
 def test_staged_kernel_whole_cell_warps(ctx, b, n, C, M, N):
     """b = 12, 24 (the paper's recommended sizes) on the TMA kernel with whole
     cells per warp (LPW = 30 lanes, 480-px tiles, gather+broadcast lane-group
