@@ -694,9 +694,9 @@ int expand_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* stats, i
   }
   PendingTiming pt;
   timing_begin(ctx, DPPX_K_EXPAND, &pt);
-  // Fast path: persistent CTAs, two staged tiles, TMA box stores (aligned
-  // output, b in {4..32}, C in {1,3}); narrow frames packed side by side.
-  const int tile = stats_tile_px();
+  // Fast path: staged tile, TMA box stores (aligned output, the K1 grid sides,
+  // C in {1,3}); narrow frames packed side by side.
+  const int tile = stats_tile_px_for(g.b);
   const int64_t row_bytes = static_cast<int64_t>(g.N) * g.C;
   const int padded_px = g.GC * g.b;
   const int64_t stage_bytes = static_cast<int64_t>(g.b) * tile * g.C;

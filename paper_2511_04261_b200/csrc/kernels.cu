@@ -1453,17 +1453,22 @@ template <int C, int B4, int NSUB, bool ADAPTIVE, bool PACKED>
 __global__ void __launch_bounds__(kConsumers)
     k_expand_tma(const __grid_constant__ CUtensorMap tm_out, const ExpandArgs a) {
   constexpr int B = 4 * B4, SB = B / NSUB, SB4 = SB / 4;
+  constexpr int LPW = (32 / B4) * B4;                    // whole cells per warp (as K1)
+  constexpr int TILE = 4 * (kConsumers / 32) * LPW;
+  static_assert(TILE == kTilePx || !PACKED, "packed slots use 512-px tiles");
   extern __shared__ __align__(128) uint8_t smem[];
   const BatchGeom& g = a.g;
   const int t = threadIdx.x;
+  const bool strip_ok = (t & 31) < LPW;
+  const int sx = strip_ok ? (t >> 5) * LPW + (t & 31) : 0;  // strip index in the tile
   // This thread's slot (frame within the group) and strip column in it.
-  const int slot_px = PACKED ? a.slot_px : kTilePx;
-  const int my_j = PACKED ? (4 * t) / slot_px : 0;
-  const bool in_slot = my_j < (PACKED ? a.pack : 1);
+  const int slot_px = PACKED ? a.slot_px : TILE;
+  const int my_j = PACKED ? (4 * sx) / slot_px : 0;
+  const bool in_slot = strip_ok && my_j < (PACKED ? a.pack : 1);
   const int jj = in_slot ? my_j : 0;
-  const int lpx = 4 * t - jj * slot_px;
+  const int lpx = 4 * sx - jj * slot_px;
   const int srb = slot_px * C;  // smem bytes per slot row
-  const int sc = (t % B4) / SB4;
+  const int sc = (sx % B4) / SB4;
   if (t == 0) prefetch_tmap(&tm_out);
   for (int u = blockIdx.x, k = 0; u < a.units; u += gridDim.x, ++k) {
     uint8_t* buf = smem;
@@ -1478,7 +1483,7 @@ __global__ void __launch_bounds__(kConsumers)
     const int pk = PACKED ? a.pack : 1;
     const int nf = PACKED ? min(pk, g.F - fg * pk) : 1;
     const int f = fg * pk + jj;
-    const int px0 = PACKED ? 0 : tile * kTilePx;
+    const int px0 = PACKED ? 0 : tile * TILE;
     const int cell = (px0 + lpx) / B;
     const bool active = in_slot && jj < nf && cell < g.GC;
     const int gidx = r * g.GC + cell;
@@ -1899,6 +1904,27 @@ ExpandKernel pick_expand(int b, int n) {
   DPPX_CASE(2, 1)
   DPPX_CASE(4, 1)
   DPPX_CASE(8, 1)
+  if constexpr (!PK) {  // whole-cell warps / large cells (same set as K1)
+    DPPX_CASE(3, 1)
+    DPPX_CASE(5, 1)
+    DPPX_CASE(6, 1)
+    DPPX_CASE(10, 1)
+    DPPX_CASE(16, 1)
+    if constexpr (AD) {
+      DPPX_CASE(3, 3)
+      DPPX_CASE(5, 5)
+      DPPX_CASE(6, 2)
+      DPPX_CASE(6, 3)
+      DPPX_CASE(6, 6)
+      DPPX_CASE(10, 2)
+      DPPX_CASE(10, 5)
+      DPPX_CASE(10, 10)
+      DPPX_CASE(16, 2)
+      DPPX_CASE(16, 4)
+      DPPX_CASE(16, 8)
+      DPPX_CASE(16, 16)
+    }
+  }
   if constexpr (AD) {
     DPPX_CASE(2, 2)
     DPPX_CASE(4, 2)

@@ -628,6 +628,8 @@ def test_staged_kernel_whole_cell_warps(ctx, b, n, C, M, N):
     assert st["launches"]["stats_tma"] >= 1, st
     rp, ri = _oracle_adaptive(frames, masks, p, "keyed", seeds)
     assert pls == rp and np.array_equal(img, ri)
+    assert np.array_equal(ctx.reassemble(pls, M, N, b, n, channels=C, frames=F), img)
     if n == 1:
         rm, rui = _oracle_uniform(frames, p, "keyed", seeds)
         assert np.array_equal(means, rm) and np.array_equal(uimg, rui)
+        assert np.array_equal(ctx.broadcast_means(means, M, N, b, channels=C, frames=F), uimg)
