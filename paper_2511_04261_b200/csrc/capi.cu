@@ -33,6 +33,7 @@ cudaError_t launch_expand_rows(const ExpandArgs& a, size_t smem, cudaStream_t s)
 int stats_threads();
 int stats_tile_px();
 int stats_tile_px_for(int b);
+int expand_packed_tile_px();
 int stats_max_stages();
 cudaError_t launch_classify(const ClassifyArgs& a, cudaStream_t s);
 cudaError_t launch_stats_tma(StatsKernel k, const CUtensorMap& tin, const CUtensorMap& tout,
@@ -696,18 +697,24 @@ int expand_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* stats, i
   timing_begin(ctx, DPPX_K_EXPAND, &pt);
   // Fast path: staged tile, TMA box stores (aligned output, the K1 grid sides,
   // C in {1,3}); narrow frames packed side by side.
-  const int tile = stats_tile_px_for(g.b);
+  int tile = stats_tile_px_for(g.b);
   const int64_t row_bytes = static_cast<int64_t>(g.N) * g.C;
   const int padded_px = g.GC * g.b;
-  const int64_t stage_bytes = static_cast<int64_t>(g.b) * tile * g.C;
+  int64_t stage_bytes = static_cast<int64_t>(g.b) * tile * g.C;
   e.pack = 1;
   e.slot_px = tile;
-  if (2 * padded_px <= tile && (padded_px * g.C) % 16 == 0) {
+  if (tile == stats_tile_px() && 2 * padded_px <= expand_packed_tile_px() &&
+      (padded_px * g.C) % 16 == 0) {
+    // Narrow frames: frame slots side by side in a wider (1024-px) tile.
+    const int ptile = expand_packed_tile_px();
+    const int64_t pstage = static_cast<int64_t>(g.b) * ptile * g.C;
     const int64_t stride = round_up(static_cast<int64_t>(g.b) * padded_px * g.C, 128);
-    const int pk = static_cast<int>(std::min<int64_t>(tile / padded_px, stage_bytes / stride));
+    const int pk = static_cast<int>(std::min<int64_t>(ptile / padded_px, pstage / stride));
     if (pk >= 2) {
       e.pack = pk;
       e.slot_px = padded_px;
+      tile = ptile;
+      stage_bytes = pstage;
     }
   }
   e.slot_stride = static_cast<int>(round_up(static_cast<int64_t>(g.b) * e.slot_px * g.C, 128));

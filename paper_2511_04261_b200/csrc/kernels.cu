@@ -1449,13 +1449,18 @@ __global__ void __launch_bounds__(kGenericThreads) k_expand(const ExpandArgs a) 
 // from K0's per-plane scan), writes the strip pattern into a smem tile and one
 // thread bulk-stores the tile with a 3-D TMA box (clipped at M and N).
 // ============================================================================
+// Packed (narrow-frame) instantiations run 256 threads: a 1024-px tile holds
+// more frame slots per CTA (5 CelebA frames instead of 2).
+constexpr int kExpandPackedThreads = 256;
+
 template <int C, int B4, int NSUB, bool ADAPTIVE, bool PACKED>
-__global__ void __launch_bounds__(kConsumers)
+__global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
     k_expand_tma(const __grid_constant__ CUtensorMap tm_out, const ExpandArgs a) {
   constexpr int B = 4 * B4, SB = B / NSUB, SB4 = SB / 4;
   constexpr int LPW = (32 / B4) * B4;                    // whole cells per warp (as K1)
-  constexpr int TILE = 4 * (kConsumers / 32) * LPW;
-  static_assert(TILE == kTilePx || !PACKED, "packed slots use 512-px tiles");
+  constexpr int NT = PACKED ? kExpandPackedThreads : kConsumers;
+  constexpr int TILE = 4 * (NT / 32) * LPW;
+  static_assert(!PACKED || LPW == 32, "packed slots need power-of-two cells");
   extern __shared__ __align__(128) uint8_t smem[];
   const BatchGeom& g = a.g;
   const int t = threadIdx.x;
@@ -1952,9 +1957,11 @@ ExpandKernel select_expand_kernel(int C, int b, int n, bool adaptive, bool packe
 
 cudaError_t launch_expand_tma(ExpandKernel k, const CUtensorMap& tout, const ExpandArgs& a,
                               int grid, size_t smem, cudaStream_t s) {
-  k<<<grid, kConsumers, smem, s>>>(tout, a);
+  k<<<grid, a.pack > 1 ? kExpandPackedThreads : kConsumers, smem, s>>>(tout, a);
   return cudaGetLastError();
 }
+
+int expand_packed_tile_px() { return 4 * kExpandPackedThreads; }
 
 int stats_threads() { return kStatsThreads; }
 int stats_tile_px() { return kTilePx; }
