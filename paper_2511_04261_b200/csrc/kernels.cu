@@ -1538,16 +1538,18 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
         tma_store_3d(&tm_out, px0 * C / 8, r * B, fg * pk + j, buf + j * (PACKED ? a.slot_stride : 0));
     }
     if (t == 0) bulk_commit();  // one group per unit (possibly empty)
-    // bytes past the tensor's row extent (< 8 per row), from the smem tile
+    // Bytes past the tensor's row extent (< 8 per row and slot), from the smem
+    // tile, spread over the whole CTA (one thread per byte, not per strip).
     const int vbytes = min(slot_px, g.N - px0) * C;
-    const int lx0 = lpx * C;
-    if (active && lx0 + 4 * C > scopy && lx0 < vbytes) {
+    const int span = vbytes - scopy;
+    if (span > 0) {
       const int rows = min(B, g.M - r * B);
-      const uint8_t* sb = buf + jj * (PACKED ? a.slot_stride : 0);
-      for (int i = 0; i < rows; ++i)
-        for (int x = max(lx0, scopy); x < min(lx0 + 4 * C, vbytes); ++x)
-          a.out[static_cast<int64_t>(f) * a.ofstride + static_cast<int64_t>(r * B + i) * a.opitch +
-                static_cast<int64_t>(px0) * C + x] = sb[i * srb + x];
+      for (int e = t; e < nf * rows * span; e += NT) {
+        const int jr = e / span, x = scopy + (e - jr * span);
+        const int j = jr / rows, i = jr - j * rows;
+        a.out[static_cast<int64_t>(fg * pk + j) * a.ofstride + static_cast<int64_t>(r * B + i) * a.opitch +
+              static_cast<int64_t>(px0) * C + x] = buf[j * (PACKED ? a.slot_stride : 0) + i * srb + x];
+      }
     }
   }
   if (t == 0) bulk_wait_read_all();  // smem must outlive the stores' reads
