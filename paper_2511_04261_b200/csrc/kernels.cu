@@ -1474,7 +1474,6 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
   const int lpx = 4 * sx - jj * slot_px;
   const int srb = slot_px * C;  // smem bytes per slot row
   const int sc = (sx % B4) / SB4;
-  if (t == 0) prefetch_tmap(&tm_out);
   for (int u = blockIdx.x, k = 0; u < a.units; u += gridDim.x, ++k) {
     uint8_t* buf = smem;
     // A capped grid loops: the previous unit's store must have read the tile.
