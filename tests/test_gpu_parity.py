@@ -484,8 +484,8 @@ def test_randomized_fuzz_against_oracle(ctx):
     rng = np.random.default_rng(2025)
     kinds = {"keyed": dp.NOISE_KEYED, "philox": dp.NOISE_PHILOX, "none": dp.NOISE_NONE}
     for case in range(150):
-        b, n = FAST_BN[rng.integers(len(FAST_BN))] if rng.random() < 0.8 else \
-            (int(rng.integers(1, 13)), 1)
+        b, n = FAST_BN[rng.integers(len(FAST_BN))] if rng.random() < 0.7 else \
+            (int(rng.choice([12, 20, 24, 40, 5, 7, 9])), 1)
         if n == 1 and rng.random() < 0.5 and b % 2 == 0:
             n = 2
         C = int(rng.choice([1, 3]))
