@@ -371,11 +371,21 @@ int classify(dppx_ctx* ctx, const BatchGeom& g, int planes, bool from_payload, c
   a.mfstride = mfstride;
   a.vec = 1;
   a.mask_bits = mask_bits ? 1 : 0;
+  a.band = 0;
   if (!from_payload && !var && !mask_bits) {
-    if (g.b % 16 == 0 && aligned16(mask) && mpitch % 16 == 0 && mfstride % 16 == 0) a.vec = 16;
+    const bool al16 = aligned16(mask) && mpitch % 16 == 0 && mfstride % 16 == 0;
+    if (g.b % 16 == 0 && al16) a.vec = 16;
     else if (g.b % 4 == 0 && (reinterpret_cast<uintptr_t>(mask) & 3) == 0 && mpitch % 4 == 0 &&
              mfstride % 4 == 0)
       a.vec = 4;
+    // Grid sides without a per-cell vector path: band column sums.
+    const bool per_cell_vec = (a.vec == 16 && (g.b == 16 || g.b == 32)) ||
+                              (a.vec == 4 && (g.b == 4 || g.b == 8));
+    if (!per_cell_vec && g.b >= 4 && g.b <= 257 &&
+        static_cast<int64_t>(g.GC) * g.b * 4 <= 160 * 1024) {
+      a.band = 1;
+      a.vec = al16 ? 16 : 1;
+    }
   }
   a.payload = payload;
   a.payload_in = payload_in;

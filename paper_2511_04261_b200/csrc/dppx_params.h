@@ -67,6 +67,7 @@ struct ClassifyArgs {
   int vec;                   // 16, 4 or 1: widest aligned load for the mask rows
   int mask_bits;             // mask rows are packed bits (u32 words, maskpack.h), mpitch in bytes
   const uint8_t* flags;      // mode 3: per-cell simple flags [F][G] from the fused variance K1
+  int band;                  // mode 0: band column sums in dynamic smem (GC*b u32)
   uint8_t* payload;          // from_payload == 0: mask means + S written for C planes
   const uint8_t* payload_in; // from_payload == 1
   int64_t pstride;

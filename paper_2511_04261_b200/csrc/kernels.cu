@@ -219,15 +219,71 @@ __device__ __forceinline__ bool cell_is_complex_var(const ClassifyArgs& a, const
   return var >= a.var_tau;
 }
 
+// Band column sums for grid sides without a per-cell vector path (b = 12, 20,
+// 24, 40, 64, 128 ...): the block sums its b mask rows column by column with
+// coalesced 16-byte loads (SWAR, two u16 counters per u32: b <= 257), then a
+// cell's sum is b smem reads. One thread per cell reading b x b bytes would
+// leave most of the block idle at large b (30 cells per 1080p row at b = 64).
+__device__ void mask_band_colsums(const ClassifyArgs& a, const uint8_t* mbase, int r,
+                                  uint32_t* colsum) {
+  const BatchGeom& g = a.g;
+  const int W = g.GC * g.b;  // padded columns
+  const bool vec = a.vec == 16;
+  for (int x0 = threadIdx.x * 16; x0 < W; x0 += kClassifyThreads * 16) {
+    uint32_t lo[4] = {0u, 0u, 0u, 0u}, hi[4] = {0u, 0u, 0u, 0u};
+    const bool fast = vec && x0 + 16 <= g.N;
+#pragma unroll 4
+    for (int i = 0; i < g.b; ++i) {
+      const uint8_t* row = mbase + static_cast<int64_t>(reflect_index(r * g.b + i, g.M)) * a.mpitch;
+      uint32_t w[4];
+      if (fast) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(row + x0));
+        w[0] = v.x, w[1] = v.y, w[2] = v.z, w[3] = v.w;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          uint32_t acc = 0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int x = x0 + 4 * j + k;
+            const uint32_t byte = x < W ? __ldg(row + reflect_index(x, g.N)) : 0u;
+            acc |= byte << (8 * k);
+          }
+          w[j] = acc;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        lo[j] += w[j] & 0x00FF00FFu;
+        hi[j] += (w[j] >> 8) & 0x00FF00FFu;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int x = x0 + 4 * j;
+      if (x + 0 < W) colsum[x + 0] = lo[j] & 0xFFFFu;
+      if (x + 1 < W) colsum[x + 1] = hi[j] & 0xFFFFu;
+      if (x + 2 < W) colsum[x + 2] = lo[j] >> 16;
+      if (x + 3 < W) colsum[x + 3] = hi[j] >> 16;
+    }
+  }
+}
+
+template <bool BAND>
 __global__ void __launch_bounds__(kClassifyThreads) k_classify(const ClassifyArgs a) {
   __shared__ uint32_t warp_tot[kClassifyThreads / 32];
   __shared__ uint32_t s_last;
+  extern __shared__ uint32_t colsum[];  // a.band: per padded column mask sums of the band
   const BatchGeom& g = a.g;
   const int r = blockIdx.x;
   for (int p = blockIdx.y; p < a.planes; p += gridDim.y) {
     const uint8_t* mbase = a.from_payload ? nullptr : a.mask + static_cast<int64_t>(p) * a.mfstride;
     const float* mm_in =
         a.from_payload == 1 ? reinterpret_cast<const float*>(a.payload_in + p * a.pstride) : nullptr;
+    if constexpr (BAND) {
+      mask_band_colsums(a, mbase, r, colsum);
+      __syncthreads();
+    }
     uint32_t carry = 0;
     for (int c0 = 0; c0 < g.GC; c0 += kClassifyThreads) {
       const int c = c0 + threadIdx.x;
@@ -246,7 +302,12 @@ __global__ void __launch_bounds__(kClassifyThreads) k_classify(const ClassifyArg
             reinterpret_cast<float*>(a.payload + (static_cast<int64_t>(p) * g.C + ch) * a.pstride)
                 [cell] = mean;
         } else {
-          const uint32_t s = mask_cell_sum(a, mbase, r, c);
+          uint32_t s = 0;
+          if constexpr (BAND) {
+            for (int k = 0; k < g.b; ++k) s += colsum[c * g.b + k];
+          } else {
+            s = mask_cell_sum(a, mbase, r, c);
+          }
           // mask_grid_mean (image.cpp:191-202) then static_cast<float>
           // (adaptive.cpp:59-60).
           mean = __double2float_rn(__ddiv_rn(static_cast<double>(s), a.area));
@@ -1977,7 +2038,17 @@ int stats_max_stages() { return kMaxStages; }
 
 cudaError_t launch_classify(const ClassifyArgs& a, cudaStream_t s) {
   dim3 grid(a.g.GR, a.planes < 65535 ? a.planes : 65535);
-  k_classify<<<grid, kClassifyThreads, 0, s>>>(a);
+  if (!a.band) {
+    k_classify<false><<<grid, kClassifyThreads, 0, s>>>(a);
+    return cudaGetLastError();
+  }
+  const size_t smem = static_cast<size_t>(a.g.GC) * a.g.b * 4;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_classify<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  k_classify<true><<<grid, kClassifyThreads, smem, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -68,7 +68,9 @@ def main():
         s2 = ctx.stats()
         ctx.set_timing(False)
         k2 = s2["device_ms"]["expand"] / max(1, s2["launches"]["expand"])
-        rows.append({"b": b, "n": n, "kernel": fam, "k1_ms": round(ms, 4),
+        k0 = s["device_ms"]["classify"] / max(1, s["launches"]["classify"])
+        rows.append({"b": b, "n": n, "kernel": fam, "k1_ms": round(ms, 4), "k0_ms": round(k0, 4),
+                     "k0_frac": round(F * M * N / (k0 / 1e3) / 1e9 / peak, 4) if adaptive else None,
                      "frac": round(alg / (ms / 1e3) / 1e9 / peak, 4),
                      "k2_ms": round(k2, 4),
                      "k2_frac": round((F * M * N * C + pay) / (k2 / 1e3) / 1e9 / peak, 4)})
