@@ -270,7 +270,7 @@ __device__ void mask_band_colsums(const ClassifyArgs& a, const uint8_t* mbase, i
 }
 
 template <bool BAND>
-__global__ void __launch_bounds__(kClassifyThreads, BAND ? 10 : 1) k_classify(const ClassifyArgs a) {
+__global__ void __launch_bounds__(kClassifyThreads, BAND ? 10 : 8) k_classify(const ClassifyArgs a) {
   __shared__ uint32_t warp_tot[kClassifyThreads / 32];
   __shared__ uint32_t s_last;
   extern __shared__ uint32_t colsum[];  // a.band: per padded column mask sums of the band
