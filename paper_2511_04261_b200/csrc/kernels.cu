@@ -269,6 +269,39 @@ __device__ void mask_band_colsums(const ClassifyArgs& a, const uint8_t* mbase, i
   }
 }
 
+// Bit-packed masks (host pipeline) at large b: items (cell, row) over the
+// whole block, popc per row segment, smem atomics into the cell sums.
+__device__ void mask_band_cellsums_bits(const ClassifyArgs& a, const uint8_t* mbase, int r,
+                                        uint32_t* cellsum) {
+  const BatchGeom& g = a.g;
+  for (int c = threadIdx.x; c < g.GC; c += kClassifyThreads) cellsum[c] = 0;
+  __syncthreads();
+  const FastDiv div_b = make_fastdiv(static_cast<uint32_t>(g.b));
+  for (int item = threadIdx.x; item < g.GC * g.b; item += kClassifyThreads) {
+    const int c = static_cast<int>(div_b.div(static_cast<uint32_t>(item))), i = item - c * g.b;
+    const uint32_t* row = reinterpret_cast<const uint32_t*>(
+        mbase + static_cast<int64_t>(reflect_index(r * g.b + i, g.M)) * a.mpitch);
+    const int j0 = c * g.b;
+    uint32_t sum = 0;
+    if (j0 + g.b <= g.N) {
+      const int j1 = j0 + g.b - 1, w0 = j0 >> 5, w1 = j1 >> 5;
+      const uint32_t m0 = ~0u << (j0 & 31), m1 = ~0u >> (31 - (j1 & 31));
+      if (w0 == w1) {
+        sum = __popc(__ldg(row + w0) & m0 & m1);
+      } else {
+        sum = __popc(__ldg(row + w0) & m0) + __popc(__ldg(row + w1) & m1);
+        for (int w = w0 + 1; w < w1; ++w) sum += __popc(__ldg(row + w));
+      }
+    } else {
+      for (int j = j0; j < j0 + g.b; ++j) {
+        const int jj = reflect_index(j, g.N);
+        sum += (__ldg(row + (jj >> 5)) >> (jj & 31)) & 1u;
+      }
+    }
+    atomicAdd(&cellsum[c], sum);
+  }
+}
+
 template <bool BAND>
 __global__ void __launch_bounds__(kClassifyThreads, BAND ? 10 : 8) k_classify(const ClassifyArgs a) {
   __shared__ uint32_t warp_tot[kClassifyThreads / 32];
@@ -281,7 +314,8 @@ __global__ void __launch_bounds__(kClassifyThreads, BAND ? 10 : 8) k_classify(co
     const float* mm_in =
         a.from_payload == 1 ? reinterpret_cast<const float*>(a.payload_in + p * a.pstride) : nullptr;
     if constexpr (BAND) {
-      mask_band_colsums(a, mbase, r, colsum);
+      if (a.band == 2) mask_band_cellsums_bits(a, mbase, r, colsum);
+      else mask_band_colsums(a, mbase, r, colsum);
       __syncthreads();
     }
     uint32_t carry = 0;
@@ -304,7 +338,11 @@ __global__ void __launch_bounds__(kClassifyThreads, BAND ? 10 : 8) k_classify(co
         } else {
           uint32_t s = 0;
           if constexpr (BAND) {
-            for (int k = 0; k < g.b; ++k) s += colsum[c * g.b + k];
+            if (a.band == 2) {
+              s = colsum[c];
+            } else {
+              for (int k = 0; k < g.b; ++k) s += colsum[c * g.b + k];
+            }
           } else {
             s = mask_cell_sum(a, mbase, r, c);
           }
@@ -2042,7 +2080,7 @@ cudaError_t launch_classify(const ClassifyArgs& a, cudaStream_t s) {
     k_classify<false><<<grid, kClassifyThreads, 0, s>>>(a);
     return cudaGetLastError();
   }
-  const size_t smem = static_cast<size_t>(a.g.GC) * a.g.b * 4;
+  const size_t smem = static_cast<size_t>(a.g.GC) * (a.band == 2 ? 1 : a.g.b) * 4;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_classify<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
