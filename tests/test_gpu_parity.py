@@ -108,9 +108,11 @@ def test_generic_path_random_geometry(ctx):
 
 
 @pytest.mark.parametrize("kind", ["none", "injected"])
-def test_noise_free_and_injected_bit_exact(ctx, kind):
+@pytest.mark.parametrize("b,n", [(16, 4), (12, 3), (24, 4), (30, 5), (64, 8)])
+def test_noise_free_and_injected_bit_exact(ctx, kind, b, n):
+    """TMA K1 (b = 16, whole-cell b = 12, b = 64) and K1r (b = 24 n = 4, b = 30)."""
     rng = np.random.default_rng(11)
-    F, M, N, C, b, n = 3, 100, 260, 3, 16, 4
+    F, M, N, C = 3, 100, 260, 3
     frames = oracle.synth_frames(0, F, M, N, C)
     masks = oracle.synth_masks(0, F, M, N)
     p = dp.make_privacy_params(0.5, 16, b, n)
