@@ -80,7 +80,7 @@ __device__ __forceinline__ double uniform_from_bits(uint64_t bits) {
 // are bit-identical to the reference's (oracle twin: or_log1p_glibc, checked
 // against the host libm in tests/test_oracle_kats.py). Domain used here:
 // x = -2|u| in (-1, 0]; the other branches are kept for completeness.
-__device__ __noinline__ double glibc_log1p(double x) {
+static __device__ __noinline__ double glibc_log1p(double x) {
   const double ln2_hi = 0x1.62e42fee00000p-1, ln2_lo = 0x1.a39ef35793c76p-33;
   const double Lp1 = 0x1.5555555555593p-1, Lp2 = 0x1.999999997fa04p-2,
                Lp3 = 0x1.2492494229359p-2, Lp4 = 0x1.c71c51d8e78afp-3,
@@ -209,7 +209,7 @@ __device__ __forceinline__ uint32_t fast_quantize(uint32_t sum, float inv_area, 
 }
 
 // The reference's f64 arithmetic, step for step (rare path).
-__device__ __noinline__ uint32_t exact_quantize(uint32_t sum, double area, int kind, uint64_t bits,
+static __device__ __noinline__ uint32_t exact_quantize(uint32_t sum, double area, int kind, uint64_t bits,
                                                 double sigma, double injected) {
   const double mean = cell_mean(sum, area);
   double noise = 0.0;

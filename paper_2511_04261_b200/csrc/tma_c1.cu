@@ -1,0 +1,18 @@
+// tma_c1.cu -- K1 / K2 TMA instantiations for C = 1 (see tma_kernels.cuh).
+#include "tma_kernels.cuh"
+
+namespace dppx {
+
+StatsKernel select_stats_tma_c1(int b, int n, bool adaptive, bool packed) {
+  if (packed) return adaptive ? pick_b<1, true, true>(b, n) : pick_b<1, false, true>(b, n);
+  return adaptive ? pick_b<1, true, false>(b, n) : pick_b<1, false, false>(b, n);
+}
+
+StatsKernel select_stats_var_c1(int b, int n) { return pick_var<1>(b, n); }
+
+ExpandKernel select_expand_tma_c1(int b, int n, bool adaptive, bool packed) {
+  if (packed) return adaptive ? pick_expand<1, true, true>(b, n) : pick_expand<1, false, true>(b, n);
+  return adaptive ? pick_expand<1, true, false>(b, n) : pick_expand<1, false, false>(b, n);
+}
+
+}  // namespace dppx

@@ -1,0 +1,916 @@
+// tma_kernels.cuh -- the TMA-staged kernels (K1 k_stats_tma, K2 k_expand_tma)
+// and their per-(C, b, n) selection templates. Instantiated per channel count
+// in tma_c1.cu / tma_c3.cu (separate translation units build in parallel).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <type_traits>
+
+#include "dppx_device.cuh"
+#include "dppx_params.h"
+#include "stats_common.cuh"
+
+namespace dppx {
+
+// ============================================================================
+// K1: TMA-staged persistent kernel (fast path)
+// ============================================================================
+constexpr int kConsumers = 128;            // 4 consumer warps, one 4-px strip each
+constexpr int kTilePx = 4 * kConsumers;    // 512 px per tile
+constexpr int kStatsThreads = kConsumers + 32;
+constexpr int kMaxStages = 4;
+
+struct UnitPos {
+  int fg, r, tile, px0;  // frame group (frames fg*pack + j), grid row, column tile
+};
+
+// TILE: pixels per unit column tile (512 for power-of-two cells; general cell
+// widths use whole cells per warp, see k_stats_tma).
+template <bool PACKED, int TILE = kTilePx>
+__device__ __forceinline__ UnitPos decode_unit(const StatsArgs& a, int u) {
+  UnitPos p;
+  const uint32_t rest = a.div_tiles.div(static_cast<uint32_t>(u));
+  p.tile = u - static_cast<int>(rest * a.div_tiles.d);
+  const uint32_t fg = a.div_rows.div(rest);
+  p.r = a.row_begin + static_cast<int>(rest - fg * a.div_rows.d);
+  p.fg = static_cast<int>(fg);
+  p.px0 = PACKED ? 0 : p.tile * TILE;  // packed units are one tile wide
+  return p;
+}
+
+// Slot geometry: compile-time for wide frames (one 512-px slot per unit).
+template <bool PACKED, int TILE = kTilePx>
+__device__ __forceinline__ int slot_px(const StatsArgs& a) {
+  return PACKED ? a.slot_px : TILE;
+}
+template <bool PACKED>
+__device__ __forceinline__ int units_pack(const StatsArgs& a) {
+  return PACKED ? a.pack : 1;
+}
+
+// Real bytes of a slot row starting at column px0.
+template <int C, bool PACKED, int TILE = kTilePx>
+__device__ __forceinline__ int valid_bytes(const StatsArgs& a, int px0) {
+  return min(slot_px<PACKED, TILE>(a), a.g.N - px0) * C;
+}
+
+// A band whose rows run past M needs mirrored rows (image.cpp:105-110): it is
+// staged row by row with 1-D bulk copies; every other band is one 3-D box.
+template <int B>
+__device__ __forceinline__ bool band_reflects(const StatsArgs& a, int r) {
+  return (r + 1) * B > a.g.M;
+}
+
+// Bytes per row a 1-D bulk copy stages (multiple of 16): rounded up into the
+// pitch slack when the rows have it, else down (the rest is filled by threads).
+template <int C, bool PACKED, int TILE = kTilePx>
+__device__ __forceinline__ int bulk_row_bytes(const StatsArgs& a, int px0) {
+  const int v = valid_bytes<C, PACKED, TILE>(a, px0);
+  return a.row_slack ? min(slot_px<PACKED, TILE>(a) * C, (v + 15) & ~15) : (v & ~15);
+}
+
+// Bytes of each smem slot row that the producer's copies deliver.
+template <int C, int B, bool PACKED, int TILE = kTilePx>
+__device__ __forceinline__ int staged_bytes(const StatsArgs& a, const UnitPos& p) {
+  if (band_reflects<B>(a, p.r)) return bulk_row_bytes<C, PACKED, TILE>(a, p.px0);
+  return max(0, min(slot_px<PACKED, TILE>(a) * C, a.tensor_in_bytes - p.px0 * C));
+}
+
+template <int C, int B, bool PACKED, int TILE = kTilePx>
+__device__ __forceinline__ void load_unit(const StatsArgs& a, const CUtensorMap* tm, int u,
+                                          uint8_t* st, uint64_t* bar) {
+  const UnitPos p = decode_unit<PACKED, TILE>(a, u);
+  const int srb = slot_px<PACKED, TILE>(a) * C;
+  const int pk = units_pack<PACKED>(a);
+  const int nf = PACKED ? min(pk, a.g.F - p.fg * pk) : 1;
+  if (!band_reflects<B>(a, p.r)) {
+    mbar_arrive_expect_tx(bar, nf * B * srb);  // full boxes, OOB bytes zero-filled
+    for (int j = 0; j < nf; ++j)
+      tma_load_3d(st + j * a.slot_stride, tm, p.px0 * C / 8, p.r * B, p.fg * pk + j, bar);
+    return;
+  }
+  const uint32_t copy = static_cast<uint32_t>(bulk_row_bytes<C, PACKED, TILE>(a, p.px0));
+  mbar_arrive_expect_tx(bar, copy * B * nf);
+  if (copy == 0) return;
+#pragma unroll 1
+  for (int j = 0; j < nf; ++j) {
+    const uint8_t* src = a.img + static_cast<int64_t>(p.fg * pk + j) * a.fstride +
+                         static_cast<int64_t>(p.px0) * C;
+#pragma unroll 1
+    for (int i = 0; i < B; ++i) {
+      const int srow = reflect_index(p.r * B + i, a.g.M);
+      bulk_g2s(st + j * a.slot_stride + i * srb, src + static_cast<int64_t>(srow) * a.pitch, copy,
+               bar);
+    }
+  }
+}
+
+// One 3-D box store per slot: rows >= M and bytes past the tensor's row are
+// clipped by the TMA unit; the consumers write the (< 8) bytes past
+// tensor_out_bytes.
+template <int C, int B, bool PACKED, int TILE = kTilePx>
+__device__ __forceinline__ void store_unit(const StatsArgs& a, const CUtensorMap* tm, int u,
+                                           const uint8_t* st) {
+  const UnitPos p = decode_unit<PACKED, TILE>(a, u);
+  if (p.px0 * C >= a.tensor_out_bytes) return;
+  const int pk = units_pack<PACKED>(a);
+  const int nf = PACKED ? min(pk, a.g.F - p.fg * pk) : 1;
+  for (int j = 0; j < nf; ++j)
+    tma_store_3d(tm, p.px0 * C / 8, p.r * B, p.fg * pk + j, st + j * a.slot_stride);
+  bulk_commit();
+  bulk_wait_read_all();
+}
+
+// Output bytes of a unit past the output tensor map's row extent (< 8 per row:
+// the TMA store covers [0, tensor_out_bytes)), written by the 32 producer lanes.
+template <int C, int B, bool PACKED, int TILE = kTilePx>
+__device__ __forceinline__ void store_tail(const StatsArgs& a, int u, const uint8_t* st, int lane) {
+  const UnitPos p = decode_unit<PACKED, TILE>(a, u);
+  const int srb = slot_px<PACKED, TILE>(a) * C;
+  const int vbytes = valid_bytes<C, PACKED, TILE>(a, p.px0);
+  const int scopy = max(0, min(srb, a.tensor_out_bytes - p.px0 * C));
+  if (scopy >= vbytes) return;
+  const int span = vbytes - scopy;
+  const int rows = min(B, a.g.M - p.r * B);
+  const int pk = units_pack<PACKED>(a);
+  const int nf = PACKED ? min(pk, a.g.F - p.fg * pk) : 1;
+  for (int e = lane; e < nf * rows * span; e += 32) {
+    const int jr = e / span, x = scopy + (e - jr * span);
+    const int j = jr / rows, i = jr - j * rows;
+    a.out[static_cast<int64_t>(p.fg * pk + j) * a.ofstride +
+          static_cast<int64_t>(p.r * B + i) * a.opitch + static_cast<int64_t>(p.px0) * C + x] =
+        st[j * a.slot_stride + i * srb + x];
+  }
+}
+
+// Byte k (0..4C-1) of a 4-pixel strip of value v[] (interleaved channels).
+template <int C>
+__device__ __forceinline__ void pattern_words(const uint32_t (&v)[C], uint32_t (&w)[C]) {
+  if constexpr (C == 1) {
+    w[0] = v[0] * 0x01010101u;
+  } else if constexpr (C == 3) {
+    w[0] = v[0] | (v[1] << 8) | (v[2] << 16) | (v[0] << 24);
+    w[1] = v[1] | (v[2] << 8) | (v[0] << 16) | (v[1] << 24);
+    w[2] = v[2] | (v[0] << 8) | (v[1] << 16) | (v[2] << 24);
+  } else {  // C == 4: one pixel per word
+#pragma unroll
+    for (int k = 0; k < 4; ++k) w[k] = v[0] | (v[1] << 8) | (v[2] << 16) | (v[3] << 24);
+  }
+}
+
+// Per-channel byte sums of one 4-px strip row held in C words, added to acc.
+// Each row's partial starts from zero so rows form independent dp4a chains.
+template <int C>
+__device__ __forceinline__ void accumulate_row(const uint8_t* row, uint32_t (&acc)[C]) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(row);
+  if constexpr (C == 1) {
+    acc[0] += __dp4a(w[0], 0x01010101u, 0u);
+  } else if constexpr (C == 3) {
+    const uint32_t w0 = w[0], w1 = w[1], w2 = w[2];
+    // bytes: w0 = R G B R, w1 = G B R G, w2 = B R G B (little-endian)
+    acc[0] += __dp4a(w0, 0x01000001u, __dp4a(w1, 0x00010000u, __dp4a(w2, 0x00000100u, 0u)));
+    acc[1] += __dp4a(w0, 0x00000100u, __dp4a(w1, 0x01000001u, __dp4a(w2, 0x00010000u, 0u)));
+    acc[2] += __dp4a(w0, 0x00010000u, __dp4a(w1, 0x00000100u, __dp4a(w2, 0x01000001u, 0u)));
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t x = w[k];
+      acc[0] += x & 0xFF;
+      acc[1] += (x >> 8) & 0xFF;
+      acc[2] += (x >> 16) & 0xFF;
+      acc[3] += x >> 24;
+    }
+  }
+}
+
+// Sum of squares of all bytes of one 4-px strip row (variance extension).
+template <int C>
+__device__ __forceinline__ uint32_t square_row(const uint8_t* row, uint32_t acc) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(row);
+#pragma unroll
+  for (int k = 0; k < (C == 4 ? 4 : C); ++k) acc = __dp4a(w[k], w[k], acc);
+  return acc;
+}
+
+// Sum over an aligned group of G lanes (a cell or subcell), result in every lane
+// of the group: butterfly for power-of-two G, else gather at the group's first
+// lane and broadcast (groups never straddle a warp: see k_stats_tma's LPW).
+template <int G>
+__device__ __forceinline__ uint32_t group_sum(uint32_t x) {
+  if constexpr ((G & (G - 1)) == 0) {
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+    return x;
+  } else {
+    const int lane = threadIdx.x & 31;
+    uint32_t sum = x;
+#pragma unroll
+    for (int o = 1; o < G; ++o) sum += __shfl_down_sync(0xFFFFFFFFu, x, o);
+    return __shfl_sync(0xFFFFFFFFu, sum, lane - lane % G);
+  }
+}
+
+// Values of the C channels of one statistic, computed by the GL lanes of a
+// lane group (each lane draws a subset of channels) and shared by shuffles.
+template <int C, int GL>
+__device__ __forceinline__ void group_values(const StatsArgs& a, const DrawEnv& env, bool active,
+                                             const uint32_t (&sum)[C], const uint64_t (&cs)[C],
+                                             int f, int r, int c, int sr, int sc,
+                                             uint32_t (&val)[C]) {
+  constexpr int NV = (C + GL - 1) / GL;  // channels this lane draws
+  if (!__any_sync(0xFFFFFFFFu, active)) {  // warp-uniform: nothing to draw
+#pragma unroll
+    for (int k = 0; k < C; ++k) val[k] = 0;
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const int li = lane % GL;
+  const int gb = lane - li;
+  uint32_t s[NV], q[NV];
+  uint64_t bits[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int ch = j * GL + li;
+    s[j] = sum[0];
+    uint64_t st = cs[0];
+#pragma unroll
+    for (int k = 1; k < C; ++k)
+      if (ch == k) {
+        s[j] = sum[k];
+        st = cs[k];
+      }
+    bits[j] = draw_bits(a, st, f, ch, r, c, sr, sc);
+  }
+  // Phase 1: branch-free bounded estimates for all channels (independent
+  // chains the scheduler can interleave); phase 2: the rare exact draws.
+  if (!env.exact_only && (env.kind == DPPX_NOISE_KEYED || env.kind == DPPX_NOISE_PHILOX)) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) q[j] = fast_quantize(s[j], env.inv_area, bits[j], env.sigmaf, env.margin);
+  } else if (!env.exact_only && env.kind == DPPX_NOISE_NONE && env.pow2) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j)  // sum * 2^-k + 0.5 is exact in f32
+      q[j] = static_cast<uint32_t>(floorf(static_cast<float>(s[j]) * env.inv_area + 0.5f));
+  } else {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) q[j] = 0xFFFFFFFFu;
+  }
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int ch = j * GL + li;
+    if (active && ch < C && q[j] == 0xFFFFFFFFu)
+      q[j] = exact_quantize(s[j], env.area, env.kind, bits[j], env.sigma,
+                            env.kind == DPPX_NOISE_INJECTED ? inj_at(a, f, ch, r * a.g.GC + c, sr, sc)()
+                                                            : 0.0);
+  }
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+#pragma unroll
+    for (int k = j * GL; k < C && k < (j + 1) * GL; ++k)
+      val[k] = (GL == 1) ? q[j] : __shfl_sync(0xFFFFFFFFu, q[j], gb + (k - j * GL));
+  }
+}
+
+template <int C, int B4, int NSUB, bool ADAPTIVE, bool PACKED, bool VAR = false>
+__global__ void __launch_bounds__(kStatsThreads)
+    k_stats_tma(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
+                const StatsArgs a) {
+  constexpr int B = 4 * B4;
+  constexpr int SB = B / NSUB;
+  constexpr int SB4 = SB / 4;
+  // Strips per warp: whole cells only (a cell is B4 adjacent lanes), so for
+  // B4 not a power of two (b = 12, 24) the last 32 % B4 lanes of each warp
+  // idle and the tile is 16 * LPW px (480 at b = 12 or 24) instead of 512.
+  constexpr int LPW = (32 / B4) * B4;
+  constexpr int TILE = 4 * (kConsumers / 32) * LPW;
+  constexpr int ROWB = TILE * C;
+  constexpr uint32_t STAGE = B * ROWB;
+  static_assert(SB % 4 == 0 && B4 <= 32 && B4 % SB4 == 0, "fast-path geometry");
+  static_assert(TILE == kTilePx || !PACKED, "packed slots use 512-px tiles");
+  static_assert(!VAR || (ADAPTIVE && !PACKED), "variance staging: wide adaptive frames only");
+
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full_bar[kMaxStages];  // TMA bytes landed
+  __shared__ __align__(8) uint64_t id_bar[kMaxStages];    // stage_unit[s] published
+  __shared__ __align__(8) uint64_t done_bar[kMaxStages];  // consumers finished the stage
+  __shared__ int stage_unit[kMaxStages];                  // unit in stage s, -1 = no more work
+
+  const int S = a.stages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&id_bar[s], 1);
+      mbar_init(&done_bar[s], kConsumers);
+    }
+    fence_mbarrier_init();
+  }
+  __syncthreads();
+
+  if (warp == kConsumers / 32) {
+    // ---------------- producer warp: TMA loads + bulk stores ----------------
+    // Units (frame, grid row, 512-px tile) are claimed from a global counter so
+    // heavy (complex-cell) tiles spread over all CTAs.
+    // The whole warp stays in the loop: lane 0 claims units and issues the TMA
+    // copies; all 32 lanes write the few output bytes past the output tensor
+    // map's row extent (keeps that byte loop off the consumer warps).
+    if (lane == 0) {
+      prefetch_tmap(&tm_in);
+      prefetch_tmap(&tm_out);
+    }
+    auto finish_unit = [&](int s, int use) {  // after consumers released stage s
+      mbar_wait(&done_bar[s], use & 1);        // every lane acquires the smem writes
+      if (a.out) {
+        const int uu = stage_unit[s];
+        store_tail<C, B, PACKED, TILE>(a, uu, smem + s * STAGE, lane);
+        if (lane == 0) store_unit<C, B, PACKED, TILE>(a, &tm_out, uu, smem + s * STAGE);
+      }
+      __syncwarp();
+    };
+    int k = 0;
+    int done_units = 0;  // units of this CTA already stored
+    for (;; ++k) {
+      const int s = k % S;
+      if (k >= S) {
+        finish_unit(s, (k / S) - 1);
+        ++done_units;
+      }
+      int u = 0;
+      if (lane == 0) {
+        u = atomicAdd(a.work_counter, 1);
+        if (u >= a.units) {
+          // Every producer makes exactly one failing claim; the last one resets
+          // the counter for the next launch (no memset per launch).
+          if (u == a.units + static_cast<int>(gridDim.x) - 1) atomicExch(a.work_counter, 0);
+          u = -1;
+        }
+        stage_unit[s] = u;
+        mbar_arrive(&id_bar[s]);
+        if (u < 0)
+          mbar_arrive_expect_tx(&full_bar[s], 0);
+        else
+          load_unit<C, B, PACKED, TILE>(a, &tm_in, u, smem + s * STAGE, &full_bar[s]);
+      }
+      u = __shfl_sync(0xFFFFFFFFu, u, 0);
+      if (u < 0) break;
+    }
+    // k units were loaded; units [done_units, k) still need their store.
+    for (int j = done_units; j < k; ++j) finish_unit(j % S, j / S);
+    if (lane == 0) bulk_wait_all();
+    return;
+  }
+
+  // ---------------- consumer warps ----------------
+  const int t = threadIdx.x;  // strip index within the tile
+  const BatchGeom& g = a.g;
+  const DrawEnv env_cell = make_env(a.noise.kind, a.exact_noise != 0, a.area, a.sigma);
+  const DrawEnv env_sub = make_env(a.noise.kind, a.exact_noise != 0, a.sub_area, a.sigma_sub);
+  // Per-unit metadata (K0's cell info, row prefix, simple total, plane seeds)
+  // is loaded one unit ahead so its L2 latency hides behind a unit of work.
+  struct Meta {
+    int u;
+    uint32_t info, rowpre, stot;
+    uint64_t seed[C];
+  };
+  // This thread's 4-px strip in the tile: lanes >= LPW of a warp have none
+  // (only when B4 is not a power of two) and compute on strip 0, inactive.
+  const bool strip_ok = (t & 31) < LPW;
+  const int sx = strip_ok ? (t >> 5) * LPW + (t & 31) : 0;  // strip index
+  // Slot of the strip (fixed for the kernel). Wide frames (PACKED = false)
+  // have one TILE-px slot: the compiler folds all of this.
+  const int my_j = PACKED ? (4 * sx) / a.slot_px : 0;
+  const bool in_slot = strip_ok && my_j < (PACKED ? a.pack : 1);
+  const int jj = in_slot ? my_j : 0;
+  const int lpx = 4 * sx - jj * (PACKED ? a.slot_px : TILE);  // strip column in its slot
+  const int srb = PACKED ? a.slot_px * C : TILE * C;         // smem bytes per slot row
+  // Packed mode: byte offsets of the mirrored sources of the padding bytes
+  // [N*C, GC*b*C) of a slot row (image.cpp:105-110), shared by all units.
+  __shared__ uint16_t fill_src[128];
+  // Per-warp complex-draw tables (see the complex-cell block below).
+  constexpr int CPW = 32 / B4;           // cells per consumer warp
+  constexpr int NN = NSUB * NSUB;
+  using SumT = typename std::conditional<(SB * SB * 255 < 65536), uint16_t, uint32_t>::type;
+  struct CellRec {
+    int cw, f, cell, gidx;
+    int64_t off;
+  };
+  __shared__ SumT csum[VAR ? kConsumers / 32 : 1][VAR ? CPW : 1][VAR ? NN * C : 1];
+  __shared__ CellRec crec[VAR ? kConsumers / 32 : 1][VAR ? CPW : 1];
+  __shared__ uint64_t cstate[VAR ? kConsumers / 32 : 1][VAR ? CPW : 1][C];
+  const int wq = VAR ? (t >> 5) : 0;          // consumer warp
+  const int cw = VAR ? ((t & 31) / B4) : 0;   // cell within the warp
+  if (PACKED) {
+    const int v0 = g.N * C, pad = (g.GC * B - g.N) * C;
+    for (int x = t; x < pad && x < 128; x += kConsumers) {
+      const int cpx = (v0 + x) / C, ch = (v0 + x) - cpx * C;
+      fill_src[x] = static_cast<uint16_t>(reflect_index(cpx, g.N) * C + ch);
+    }
+    named_bar_sync(1, kConsumers);
+  }
+  auto load_meta = [&](int k_next) {
+    Meta m;
+    const int sn = k_next % S;
+    mbar_wait(&id_bar[sn], (k_next / S) & 1);
+    m.u = *reinterpret_cast<volatile int*>(&stage_unit[sn]);
+    m.info = 1u;
+    m.rowpre = m.stot = 0;
+#pragma unroll
+    for (int ch = 0; ch < C; ++ch) m.seed[ch] = 0;
+    if (m.u >= 0) {
+      const UnitPos q = decode_unit<PACKED, TILE>(a, m.u);
+      const int qf = q.fg * units_pack<PACKED>(a) + jj;
+      const int qcell = PACKED ? (q.px0 + lpx) / B : q.px0 / B + sx / B4;
+      if (!PACKED || qf < g.F) {
+        if (ADAPTIVE && !VAR && qcell < g.GC) {
+          m.info = __ldg(&a.cellinfo[static_cast<int64_t>(qf) * g.G + q.r * g.GC + qcell]);
+          m.rowpre = __ldg(&a.rowprefix[static_cast<int64_t>(qf) * g.GR + q.r]);
+          m.stot = __ldg(&a.totals[qf]);
+        }
+        if (a.noise.kind == DPPX_NOISE_KEYED) {
+#pragma unroll
+          for (int ch = 0; ch < C; ++ch)
+            m.seed[ch] = a.noise.seed(static_cast<int64_t>(qf) * C + ch);
+        }
+      }
+    }
+    return m;
+  };
+  Meta next = load_meta(0);
+  for (int k = 0;; ++k) {
+    const int s = k % S;
+    uint8_t* st = smem + s * STAGE;
+    const Meta cur = next;
+    const int u = cur.u;
+    if (u < 0) break;
+    const UnitPos p = decode_unit<PACKED, TILE>(a, u);
+    const int f = p.fg * units_pack<PACKED>(a) + jj;  // this thread's frame
+    const int cell = PACKED ? (p.px0 + lpx) / B : p.px0 / B + sx / B4;
+    const int lic = sx % B4;       // lane within cell
+    const int sc = lic / SB4;      // subcell column
+    const bool active = in_slot && (!PACKED || f < g.F) && cell < g.GC;
+    const int gidx = p.r * g.GC + cell;
+    const bool simple0 = !ADAPTIVE || (cur.info & 1u);  // VAR: decided after the sums
+    const uint32_t slot_s = cur.rowpre + (cur.info >> 1);
+    const uint32_t S_tot = cur.stot;
+    const int vbytes = valid_bytes<C, PACKED, TILE>(a, p.px0);
+    const int copy = staged_bytes<C, B, PACKED, TILE>(a, p);  // bytes per row the producer staged
+    const int need = min(slot_px<PACKED, TILE>(a), g.GC * B - p.px0) * C;
+    const int nf = PACKED ? min(a.pack, g.F - p.fg * a.pack) : 1;
+    uint64_t cs[C];
+#pragma unroll
+    for (int ch = 0; ch < C; ++ch)
+      cs[ch] = a.noise.kind == DPPX_NOISE_KEYED ? key_cell(cur.seed[ch], p.r, cell) : 0ull;
+
+    mbar_wait(&full_bar[s], (k / S) & 1);
+
+    // Row tail not covered by the staged copy and mirrored padding columns
+    // (image.cpp:105-110), including stray pitch-slack bytes a rounded-up copy
+    // brought in. Work is split as (slot row, column lane) so no index needs a
+    // runtime division. A mirrored byte is read from the staged row in smem when
+    // it is there (sources lie in [0, fs), targets in [fs, need): disjoint),
+    // else from global memory.
+    if (PACKED && a.row_slack) {
+      // Packed slots always start at column 0 and the staged rows always cover
+      // the real bytes: the mirror map of the padding is the same for every
+      // row of every unit (precomputed in fill_src).
+      const int span = need - vbytes;
+      if (span > 0) {
+        constexpr int kLanes = 8;
+        for (int pr = t / kLanes; pr < nf * B; pr += kConsumers / kLanes) {
+          const int j = pr / B, i = pr - j * B;
+          uint8_t* rowp = st + j * a.slot_stride + i * srb;
+          for (int x = t % kLanes; x < span; x += kLanes) rowp[vbytes + x] = rowp[fill_src[x]];
+        }
+        named_bar_sync(1, kConsumers);
+      }
+    } else {
+      const int fs = min(copy, vbytes);
+      if (fs < need) {
+        constexpr int kLanes = 4;  // consumer threads per slot row
+        const int rows_total = nf * B;
+        for (int pr = t / kLanes; pr < rows_total; pr += kConsumers / kLanes) {
+          const int j = pr / B, i = pr - j * B;  // B is a compile-time power of two
+          uint8_t* rowp = st + j * (PACKED ? a.slot_stride : 0) + i * srb;
+          const int frame = p.fg * units_pack<PACKED>(a) + j;
+          const int srow = reflect_index(p.r * B + i, g.M);
+          const uint8_t* grow = a.img + static_cast<int64_t>(frame) * a.fstride +
+                                static_cast<int64_t>(srow) * a.pitch;
+          for (int x = fs + (t % kLanes); x < need; x += kLanes) {
+            const int cpx = x / C, ch = x - cpx * C;  // C is a compile-time constant
+            const int spx = reflect_index(p.px0 + cpx, g.N);
+            const int sx = (spx - p.px0) * C + ch;
+            rowp[x] = (sx >= 0 && sx < fs) ? rowp[sx]
+                                           : __ldg(grow + static_cast<int64_t>(spx) * C + ch);
+          }
+        }
+        named_bar_sync(1, kConsumers);
+      }
+    }
+
+    const bool emit = a.out != nullptr;
+    uint8_t* mystrip = st + jj * a.slot_stride + lpx * C;
+    uint32_t tot[C];
+#pragma unroll
+    for (int ch = 0; ch < C; ++ch) tot[ch] = 0;
+    bool simple = simple0;
+    if constexpr (VAR) {
+      // Pass 1 over the staged rows: per-channel cell sums and the sum of
+      // squares; the variance test on the whole cell (same integers and IEEE
+      // divide as K0 mode 2 / or_classify_variance).
+      uint32_t sq = 0;
+#pragma unroll
+      for (int i = 0; i < B; ++i) {
+        const uint8_t* row = mystrip + i * srb;
+        accumulate_row<C>(row, tot);
+        sq = square_row<C>(row, sq);
+      }
+      next = load_meta(k + 1);
+      uint32_t s1 = 0;
+#pragma unroll
+      for (int ch = 0; ch < C; ++ch) s1 += tot[ch];
+      s1 = group_sum<B4>(s1);
+      sq = group_sum<B4>(sq);
+      const long long ns = static_cast<long long>(C) * B * B;
+      const double num = static_cast<double>(ns * static_cast<long long>(sq) -
+                                             static_cast<long long>(s1) * static_cast<long long>(s1));
+      simple = !(__ddiv_rn(num, __dmul_rn(static_cast<double>(ns), static_cast<double>(ns))) >=
+                 a.var_tau);
+      if (active && lic == 0) a.var_flags[static_cast<int64_t>(f) * g.G + gidx] = simple ? 1 : 0;
+    }
+
+    if constexpr (ADAPTIVE) {
+      // Complex cells. Direct mode (mask classification): the owner lanes of
+      // each subcell draw its C values (NSUB * ceil(C / SB4) serial draws per
+      // lane); masks are spatially coherent, so warps are mostly all-simple or
+      // all-complex. Compact mode (variance classification, which scatters
+      // complex cells): the owner lanes put the subcell sums into this warp's
+      // smem table and the warp's complex draws (cells x n*n x C) are dealt
+      // round-robin to all 32 lanes, so the lanes of simple cells do not idle
+      // through the serial draws (tools/k1_complex_sweep.py measures both).
+      constexpr bool compact = VAR;
+      const bool cx = active && !simple;
+      const unsigned cx_any = __ballot_sync(0xFFFFFFFFu, cx);
+      __syncwarp();  // the previous unit's reads of this warp's tables are done
+      if (!VAR || cx_any) {
+#pragma unroll 1
+        for (int vs = 0; vs < NSUB; ++vs) {
+          uint32_t acc[C];
+#pragma unroll
+          for (int ch = 0; ch < C; ++ch) acc[ch] = 0;
+#pragma unroll
+          for (int i = 0; i < SB; ++i) accumulate_row<C>(mystrip + (vs * SB + i) * srb, acc);
+          if constexpr (!VAR) {
+#pragma unroll
+            for (int ch = 0; ch < C; ++ch) tot[ch] += acc[ch];
+          }
+          if (cx_any) {
+#pragma unroll
+            for (int ch = 0; ch < C; ++ch) acc[ch] = group_sum<SB4>(acc[ch]);
+            if constexpr (compact) {
+              if (cx && lic % SB4 == 0) {
+#pragma unroll
+                for (int ch = 0; ch < C; ++ch)
+                  csum[wq][cw][(vs * NSUB + sc) * C + ch] = static_cast<SumT>(acc[ch]);
+              }
+            } else {
+              uint32_t val[C];
+              group_values<C, SB4>(a, env_sub, cx, acc, cs, f, p.r, cell, vs, sc, val);
+              if (cx) {
+                if (lic % SB4 == 0) {
+                  const int64_t off =
+                      VAR ? a.stage_cx + static_cast<int64_t>(gidx) * NN + vs * NSUB + sc
+                          : stat_offset(a, false, gidx, slot_s, S_tot, vs, sc);
+                  uint8_t* dst = VAR ? a.stage : a.stats;
+                  const int64_t pst = VAR ? a.stage_stride : a.sstride;
+#pragma unroll
+                  for (int ch = 0; ch < C; ++ch)
+                    dst[static_cast<int64_t>(f * C + ch) * pst + off] = static_cast<uint8_t>(val[ch]);
+                }
+                if (emit) {
+                  uint32_t w[C];
+                  pattern_words<C>(val, w);
+#pragma unroll
+                  for (int i = 0; i < SB; ++i)
+#pragma unroll
+                    for (int q = 0; q < C; ++q)
+                      reinterpret_cast<uint32_t*>(mystrip + (vs * SB + i) * srb)[q] = w[q];
+                }
+              }
+            }
+          }
+        }
+      }
+      if constexpr (!VAR) next = load_meta(k + 1);
+      if (compact && cx_any) {
+        const unsigned leaders = __ballot_sync(0xFFFFFFFFu, cx && lic == 0);
+        if (cx && lic == 0) {
+          const int rank = __popc(leaders & ((1u << (t & 31)) - 1u));
+          CellRec& rec = crec[wq][rank];
+          rec.cw = cw;
+          rec.f = f;
+          rec.cell = cell;
+          rec.gidx = gidx;
+          rec.off = VAR ? a.stage_cx + static_cast<int64_t>(gidx) * NN
+                        : stat_offset(a, false, gidx, slot_s, S_tot, 0, 0);
+#pragma unroll
+          for (int ch = 0; ch < C; ++ch) cstate[wq][rank][ch] = cs[ch];
+        }
+        __syncwarp();
+        const int work = __popc(leaders) * NN * C;
+        for (int i = t & 31; i < work; i += 32) {
+          const int kk = i / (NN * C), rem = i - kk * (NN * C);
+          const int sidx = rem / C, ch = rem - sidx * C;
+          const int vs = sidx / NSUB, sc2 = sidx - vs * NSUB;
+          const CellRec& rec = crec[wq][kk];
+          const uint32_t sum = csum[wq][rec.cw][rem];
+          const uint32_t v =
+              quantize_stat(env_sub, sum, draw_bits(a, cstate[wq][kk][ch], rec.f, ch, p.r, rec.cell, vs, sc2),
+                            inj_at(a, rec.f, ch, rec.gidx, vs, sc2));
+          uint8_t* base = VAR ? a.stage + static_cast<int64_t>(rec.f * C + ch) * a.stage_stride
+                              : a.stats + static_cast<int64_t>(rec.f * C + ch) * a.sstride;
+          base[rec.off + sidx] = static_cast<uint8_t>(v);
+          csum[wq][rec.cw][rem] = static_cast<SumT>(v);
+        }
+        __syncwarp();
+        if (emit && cx) {
+#pragma unroll 1
+          for (int vs = 0; vs < NSUB; ++vs) {
+            uint32_t val[C];
+#pragma unroll
+            for (int ch = 0; ch < C; ++ch) val[ch] = csum[wq][cw][(vs * NSUB + sc) * C + ch];
+            uint32_t w[C];
+            pattern_words<C>(val, w);
+#pragma unroll
+            for (int i = 0; i < SB; ++i)
+#pragma unroll
+              for (int q = 0; q < C; ++q)
+                reinterpret_cast<uint32_t*>(mystrip + (vs * SB + i) * srb)[q] = w[q];
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < B; ++i) accumulate_row<C>(mystrip + i * srb, tot);
+      // Next unit's metadata: requested here (after the staged rows are
+      // summed) rather than at the top, so a 2-stage ring never stalls on the
+      // producer's previous store; its latency hides behind the epilogue.
+      next = load_meta(k + 1);
+    }
+
+    // whole cell (uniform, or adaptive simple): reduce over B4 strips.
+#pragma unroll
+    for (int ch = 0; ch < C; ++ch) tot[ch] = group_sum<B4>(tot[ch]);
+    {
+      uint32_t val[C];
+      group_values<C, B4>(a, env_cell, active && simple, tot, cs, f, p.r, cell, 0, 0, val);
+      if (active && simple) {
+        if (lic == 0) {
+          if constexpr (VAR) {
+#pragma unroll
+            for (int ch = 0; ch < C; ++ch)
+              a.stage[static_cast<int64_t>(f * C + ch) * a.stage_stride + gidx] =
+                  static_cast<uint8_t>(val[ch]);
+          } else {
+            const int64_t off = stat_offset(a, true, gidx, slot_s, S_tot, 0, 0);
+#pragma unroll
+            for (int ch = 0; ch < C; ++ch)
+              a.stats[static_cast<int64_t>(f * C + ch) * a.sstride + off] =
+                  static_cast<uint8_t>(val[ch]);
+          }
+        }
+        if (emit) {
+          uint32_t w[C];
+          pattern_words<C>(val, w);
+#pragma unroll
+          for (int i = 0; i < B; ++i)
+#pragma unroll
+            for (int q = 0; q < C; ++q) reinterpret_cast<uint32_t*>(mystrip + i * srb)[q] = w[q];
+        }
+      }
+    }
+
+    fence_proxy_async_smem();
+    mbar_arrive(&done_bar[s]);
+  }
+}
+
+// ============================================================================
+// K2 fast path: one CTA per (frame, grid row, 512-px tile); each thread owns a
+// 4-px strip, looks up its cell's statistics per channel plane (packed slots
+// from K0's per-plane scan), writes the strip pattern into a smem tile and one
+// thread bulk-stores the tile with a 3-D TMA box (clipped at M and N).
+// ============================================================================
+// Packed (narrow-frame) instantiations run 256 threads: a 1024-px tile holds
+// more frame slots per CTA (5 CelebA frames instead of 2).
+constexpr int kExpandPackedThreads = 256;
+
+template <int C, int B4, int NSUB, bool ADAPTIVE, bool PACKED>
+__global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
+    k_expand_tma(const __grid_constant__ CUtensorMap tm_out, const ExpandArgs a) {
+  constexpr int B = 4 * B4, SB = B / NSUB, SB4 = SB / 4;
+  constexpr int LPW = (32 / B4) * B4;                    // whole cells per warp (as K1)
+  constexpr int NT = PACKED ? kExpandPackedThreads : kConsumers;
+  constexpr int TILE = 4 * (NT / 32) * LPW;
+  static_assert(!PACKED || LPW == 32, "packed slots need power-of-two cells");
+  extern __shared__ __align__(128) uint8_t smem[];
+  const BatchGeom& g = a.g;
+  const int t = threadIdx.x;
+  const bool strip_ok = (t & 31) < LPW;
+  const int sx = strip_ok ? (t >> 5) * LPW + (t & 31) : 0;  // strip index in the tile
+  // This thread's slot (frame within the group) and strip column in it.
+  const int slot_px = PACKED ? a.slot_px : TILE;
+  const int my_j = PACKED ? (4 * sx) / slot_px : 0;
+  const bool in_slot = strip_ok && my_j < (PACKED ? a.pack : 1);
+  const int jj = in_slot ? my_j : 0;
+  const int lpx = 4 * sx - jj * slot_px;
+  const int srb = slot_px * C;  // smem bytes per slot row
+  const int sc = (sx % B4) / SB4;
+  for (int u = blockIdx.x, k = 0; u < a.units; u += gridDim.x, ++k) {
+    uint8_t* buf = smem;
+    // A capped grid loops: the previous unit's store must have read the tile.
+    if (t == 0 && k > 0) bulk_wait_read_all();
+    __syncthreads();
+    const uint32_t rest = a.div_tiles.div(static_cast<uint32_t>(u));
+    const int tile = u - static_cast<int>(rest * a.div_tiles.d);
+    const uint32_t fq = a.div_rows.div(rest);
+    const int r = static_cast<int>(rest - fq * a.div_rows.d);
+    const int fg = static_cast<int>(fq);
+    const int pk = PACKED ? a.pack : 1;
+    const int nf = PACKED ? min(pk, g.F - fg * pk) : 1;
+    const int f = fg * pk + jj;
+    const int px0 = PACKED ? 0 : tile * TILE;
+    const int cell = (px0 + lpx) / B;
+    const bool active = in_slot && jj < nf && cell < g.GC;
+    const int gidx = r * g.GC + cell;
+    uint32_t val[NSUB][C];
+    if (active) {
+#pragma unroll
+      for (int ch = 0; ch < C; ++ch) {
+        const int64_t plane = static_cast<int64_t>(f) * C + ch;
+        const uint8_t* st = a.stats + plane * a.sstride;
+        if constexpr (!ADAPTIVE) {
+          const uint32_t v = __ldg(st + gidx);
+#pragma unroll
+          for (int vs = 0; vs < NSUB; ++vs) val[vs][ch] = v;
+        } else {
+          const uint32_t info = __ldg(&a.cellinfo[plane * g.G + gidx]);
+          const uint32_t slot_s = __ldg(&a.rowprefix[plane * g.GR + r]) + (info >> 1);
+          const int64_t base = 4ll * g.G + 4;
+          if (info & 1u) {
+            const uint32_t v = __ldg(st + base + slot_s);
+#pragma unroll
+            for (int vs = 0; vs < NSUB; ++vs) val[vs][ch] = v;
+          } else {
+            const uint8_t* sub = st + base + __ldg(&a.totals[plane]) +
+                                 static_cast<int64_t>(static_cast<uint32_t>(gidx) - slot_s) * NSUB * NSUB;
+#pragma unroll
+            for (int vs = 0; vs < NSUB; ++vs) val[vs][ch] = __ldg(sub + vs * NSUB + sc);
+          }
+        }
+      }
+      uint8_t* mystrip = buf + jj * (PACKED ? a.slot_stride : 0) + lpx * C;
+#pragma unroll
+      for (int vs = 0; vs < NSUB; ++vs) {
+        uint32_t w[C];
+        pattern_words<C>(val[vs], w);
+#pragma unroll
+        for (int i = 0; i < SB; ++i)
+#pragma unroll
+          for (int q = 0; q < C; ++q)
+            reinterpret_cast<uint32_t*>(mystrip + (vs * SB + i) * srb)[q] = w[q];
+      }
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    const int scopy = max(0, min(srb, a.tensor_out_bytes - px0 * C));
+    if (t == 0 && scopy > 0) {
+      for (int j = 0; j < nf; ++j)
+        tma_store_3d(&tm_out, px0 * C / 8, r * B, fg * pk + j, buf + j * (PACKED ? a.slot_stride : 0));
+    }
+    if (t == 0) bulk_commit();  // one group per unit (possibly empty)
+    // Bytes past the tensor's row extent (< 8 per row and slot), from the smem
+    // tile, spread over the whole CTA (one thread per byte, not per strip).
+    const int vbytes = min(slot_px, g.N - px0) * C;
+    const int span = vbytes - scopy;
+    if (span > 0) {
+      const int rows = min(B, g.M - r * B);
+      for (int e = t; e < nf * rows * span; e += NT) {
+        const int jr = e / span, x = scopy + (e - jr * span);
+        const int j = jr / rows, i = jr - j * rows;
+        a.out[static_cast<int64_t>(fg * pk + j) * a.ofstride + static_cast<int64_t>(r * B + i) * a.opitch +
+              static_cast<int64_t>(px0) * C + x] = buf[j * (PACKED ? a.slot_stride : 0) + i * srb + x];
+      }
+    }
+  }
+  if (t == 0) bulk_wait_read_all();  // smem must outlive the stores' reads
+}
+
+using StatsKernel = void (*)(const CUtensorMap, const CUtensorMap, const StatsArgs);
+using ExpandKernel = void (*)(const CUtensorMap, const ExpandArgs);
+
+template <int C, bool AD, bool PK>
+StatsKernel pick_b(int b, int n) {
+#define DPPX_CASE(B4v, NS)                 \
+  if (b == 4 * (B4v) && n == (NS)) return k_stats_tma<C, B4v, NS, AD, PK>;
+  DPPX_CASE(1, 1)
+  DPPX_CASE(2, 1)
+  DPPX_CASE(4, 1)
+  DPPX_CASE(8, 1)
+  if constexpr (!PK) {  // the paper's b = 12, 20, 24, 40 (whole cells per warp, 480-px tiles)
+    DPPX_CASE(3, 1)
+    DPPX_CASE(5, 1)
+    DPPX_CASE(6, 1)
+    DPPX_CASE(10, 1)
+    DPPX_CASE(16, 1)  // b = 64: 98 KB stages, 1 CTA/SM
+  }
+  if constexpr (AD) {
+    DPPX_CASE(2, 2)
+    DPPX_CASE(4, 2)
+    DPPX_CASE(4, 4)
+    DPPX_CASE(8, 2)
+    DPPX_CASE(8, 4)
+    DPPX_CASE(8, 8)
+    if constexpr (!PK) {
+      DPPX_CASE(3, 3)
+      DPPX_CASE(5, 5)
+      DPPX_CASE(6, 2)
+      DPPX_CASE(6, 3)
+      DPPX_CASE(6, 6)
+      DPPX_CASE(10, 2)
+      DPPX_CASE(10, 5)
+      DPPX_CASE(10, 10)
+      DPPX_CASE(16, 2)
+      DPPX_CASE(16, 4)
+      DPPX_CASE(16, 8)
+      DPPX_CASE(16, 16)
+    }
+  }
+#undef DPPX_CASE
+  return nullptr;
+}
+
+template <int C>
+StatsKernel pick_var(int b, int n) {
+#define DPPX_CASE(B4v, NS) \
+  if (b == 4 * (B4v) && n == (NS)) return k_stats_tma<C, B4v, NS, true, false, true>;
+  DPPX_CASE(2, 2)
+  DPPX_CASE(4, 2)
+  DPPX_CASE(4, 4)
+  DPPX_CASE(8, 2)
+  DPPX_CASE(8, 4)
+  DPPX_CASE(8, 8)
+#undef DPPX_CASE
+  return nullptr;
+}
+
+template <int C, bool AD, bool PK>
+ExpandKernel pick_expand(int b, int n) {
+#define DPPX_CASE(B4v, NS) \
+  if (b == 4 * (B4v) && n == (NS)) return k_expand_tma<C, B4v, NS, AD, PK>;
+  DPPX_CASE(1, 1)
+  DPPX_CASE(2, 1)
+  DPPX_CASE(4, 1)
+  DPPX_CASE(8, 1)
+  if constexpr (!PK) {  // whole-cell warps / large cells (same set as K1)
+    DPPX_CASE(3, 1)
+    DPPX_CASE(5, 1)
+    DPPX_CASE(6, 1)
+    DPPX_CASE(10, 1)
+    DPPX_CASE(16, 1)
+    if constexpr (AD) {
+      DPPX_CASE(3, 3)
+      DPPX_CASE(5, 5)
+      DPPX_CASE(6, 2)
+      DPPX_CASE(6, 3)
+      DPPX_CASE(6, 6)
+      DPPX_CASE(10, 2)
+      DPPX_CASE(10, 5)
+      DPPX_CASE(10, 10)
+      DPPX_CASE(16, 2)
+      DPPX_CASE(16, 4)
+      DPPX_CASE(16, 8)
+      DPPX_CASE(16, 16)
+    }
+  }
+  if constexpr (AD) {
+    DPPX_CASE(2, 2)
+    DPPX_CASE(4, 2)
+    DPPX_CASE(4, 4)
+    DPPX_CASE(8, 2)
+    DPPX_CASE(8, 4)
+    DPPX_CASE(8, 8)
+  }
+#undef DPPX_CASE
+  return nullptr;
+}
+
+// Per-channel-count selectors (defined in tma_c1.cu / tma_c3.cu).
+StatsKernel select_stats_tma_c1(int b, int n, bool adaptive, bool packed);
+StatsKernel select_stats_tma_c3(int b, int n, bool adaptive, bool packed);
+StatsKernel select_stats_var_c1(int b, int n);
+StatsKernel select_stats_var_c3(int b, int n);
+ExpandKernel select_expand_tma_c1(int b, int n, bool adaptive, bool packed);
+ExpandKernel select_expand_tma_c3(int b, int n, bool adaptive, bool packed);
+
+}  // namespace dppx
