@@ -16,8 +16,13 @@
 //                      noise adaptive.cpp:147-170 pixelize.cpp:109-117,
 //                      broadcast_means pixelize.cpp:126-150, reassemble
 //                      adaptive.cpp:181-245.
-//  K1g k_stats_generic same semantics for any b, n, C and alignment.
-//  K2  k_expand        statistics -> pixels (broadcast_means / reassemble).
+//                      (K1 and its staged K2 k_expand_tma live in
+//                      tma_kernels.cuh, instantiated in tma_c1.cu / tma_c3.cu.)
+//  K1r k_stats_rows    row-streaming statistics for the other grid sides.
+//  K1g k_stats_generic same semantics for any b, n, C and alignment
+//                      (Algorithm 1, and shapes K1r cannot hold).
+//  K2  k_expand        statistics -> pixels (broadcast_means / reassemble);
+//                      K2r k_expand_rows for the K1r grid sides.
 #include <cuda.h>  // CUtensorMap (type only; encoded on the host via the driver entry point)
 #include <cuda_runtime.h>
 
