@@ -505,6 +505,7 @@ constexpr int kRowThreads = 256;
 
 struct RowSmem {  // byte offsets into dynamic smem (host and device agree)
   int vg;  // vertical subcells whose byte-column sums are held at once
+  int sub_global;  // complex values too many for smem (large n): emit reads the payload
   int vsum, cellsum, flag, slot, simpleval, subval, pattern, cstate, total;
 };
 
@@ -521,7 +522,8 @@ __host__ __device__ inline RowSmem row_smem_layout(const BatchGeom& g) {
   L.slot = L.flag + rows_align16(g.GC * g.C);
   L.simpleval = L.slot + rows_align16(4 * g.GC);
   L.subval = L.simpleval + rows_align16(g.GC * g.C);
-  L.pattern = L.subval + rows_align16(g.n * NS * g.C);
+  L.sub_global = g.n * NS * g.C > 48 * 1024;
+  L.pattern = L.subval + (L.sub_global ? rows_align16(4 * g.GC * g.C) : rows_align16(g.n * NS * g.C));
   L.cstate = L.pattern + rows_align16(g.N * g.C);
   L.total = L.cstate + 8 * g.GC * g.C;
   return L;
@@ -530,9 +532,11 @@ __host__ __device__ inline RowSmem row_smem_layout(const BatchGeom& g) {
 // Emits rows [r*b, min(r*b + b, M)) of frame f from the smem value tables:
 // pixel x, channel ch of vertical subcell vs takes simpleval[c][ch] (simple
 // cell c = x / b) or subval[vs][x / sb][ch]. One pattern row per vs.
-template <int C, bool ADAPTIVE>
+// `sub(vs, sidx, c, ch)`: value of complex subcell column sidx (cell c) in
+// vertical subcell vs, from the smem table or, at large n, the payload.
+template <int C, bool ADAPTIVE, class SubFn>
 __device__ void rows_emit(const BatchGeom& g, int r, uint8_t* out_frame, int64_t opitch,
-                          const uint8_t* flag, const uint8_t* simpleval, const uint8_t* subval,
+                          const uint8_t* flag, const uint8_t* simpleval, const SubFn& sub,
                           uint8_t* pattern, const FastDiv& div_n, bool vec16) {
   const int t = threadIdx.x;
   const int RB = g.N * C, NS = g.GC * g.n;
@@ -546,7 +550,7 @@ __device__ void rows_emit(const BatchGeom& g, int r, uint8_t* out_frame, int64_t
       uint8_t v[C];
 #pragma unroll
       for (int ch = 0; ch < C; ++ch)
-        v[ch] = (!ADAPTIVE || flag[c * C + ch]) ? simpleval[c * C + ch] : subval[(vs * NS + sidx) * C + ch];
+        v[ch] = (!ADAPTIVE || flag[c * C + ch]) ? simpleval[c * C + ch] : sub(vs, sidx, c, ch);
       const int px0 = sidx * g.sb, px1 = min(px0 + g.sb, g.N);
       for (int px = px0; px < px1; ++px)
 #pragma unroll
@@ -693,7 +697,7 @@ __global__ void __launch_bounds__(kRowThreads, 4) k_stats_rows(const StatsArgs a
                                            inj_at(a, f, ch, gidx, vs, sc));
           a.stats[static_cast<int64_t>(f * C + ch) * a.sstride +
                   stat_offset(a, false, gidx, slot[c], S_tot, vs, sc)] = static_cast<uint8_t>(v);
-          subval[(vs * NS + sidx) * C + ch] = static_cast<uint8_t>(v);
+          if (!L.sub_global) subval[(vs * NS + sidx) * C + ch] = static_cast<uint8_t>(v);
         }
       }
       __syncthreads();
@@ -712,9 +716,16 @@ __global__ void __launch_bounds__(kRowThreads, 4) k_stats_rows(const StatsArgs a
       }
       __syncthreads();
     }
-    if (a.out)
+    if (a.out) {
+      auto sub = [&](int vs, int sidx, int c, int ch) -> uint8_t {
+        if (!L.sub_global) return subval[(vs * NS + sidx) * C + ch];
+        const int gidx = r * g.GC + c;  // written above by this block (visible after the barrier)
+        return a.stats[static_cast<int64_t>(f * C + ch) * a.sstride +
+                       stat_offset(a, false, gidx, slot[c], S_tot, vs, sidx - c * g.n)];
+      };
       rows_emit<C, ADAPTIVE>(g, r, a.out + static_cast<int64_t>(f) * a.ofstride, a.opitch, flag,
-                             simpleval, subval, pattern, div_n, out_vec16);
+                             simpleval, sub, pattern, div_n, out_vec16);
+    }
     __syncthreads();
   }
 }
@@ -731,6 +742,7 @@ __global__ void __launch_bounds__(kRowThreads) k_expand_rows(const ExpandArgs a,
   uint8_t* flag = rsm + L.flag;
   uint8_t* simpleval = rsm + L.simpleval;
   uint8_t* subval = rsm + L.subval;
+  int* cbase = reinterpret_cast<int*>(rsm + L.subval);  // sub_global: complex block offsets
   uint8_t* pattern = rsm + L.pattern;
   const int t = threadIdx.x;
   const int NS = g.GC * g.n, nn = g.n * g.n;
@@ -756,17 +768,26 @@ __global__ void __launch_bounds__(kRowThreads) k_expand_rows(const ExpandArgs a,
       if (info & 1u) {
         simpleval[e] = __ldg(st + base + slot_s);
       } else {
-        const uint8_t* sub = st + base + __ldg(&a.totals[plane]) +
-                             static_cast<int64_t>(static_cast<uint32_t>(gidx) - slot_s) * nn;
-        for (int k = 0; k < nn; ++k) {
-          const int vs = k / g.n, sc = k - vs * g.n;
-          subval[(vs * NS + c * g.n + sc) * C + ch] = __ldg(sub + k);
+        const int64_t cb = base + __ldg(&a.totals[plane]) +
+                           static_cast<int64_t>(static_cast<uint32_t>(gidx) - slot_s) * nn;
+        if (L.sub_global) {
+          cbase[e] = static_cast<int>(cb);  // complex block of (cell, channel) in its plane
+        } else {
+          for (int k = 0; k < nn; ++k) {
+            const int vs = k / g.n, sc = k - vs * g.n;
+            subval[(vs * NS + c * g.n + sc) * C + ch] = __ldg(st + cb + k);
+          }
         }
       }
     }
     __syncthreads();
+    auto sub = [&](int vs, int sidx, int c, int ch) -> uint8_t {
+      if (!L.sub_global) return subval[(vs * NS + sidx) * C + ch];
+      const uint8_t* st = a.stats + (static_cast<int64_t>(f) * C + ch) * a.sstride;
+      return __ldg(st + cbase[c * C + ch] + vs * g.n + (sidx - c * g.n));
+    };
     rows_emit<C, ADAPTIVE>(g, r, a.out + static_cast<int64_t>(f) * a.ofstride, a.opitch, flag,
-                           simpleval, subval, pattern, div_n, out_vec16);
+                           simpleval, sub, pattern, div_n, out_vec16);
     __syncthreads();
   }
 }

@@ -572,7 +572,8 @@ def test_single_frame_row_bands(ctx, M, N, C, b, n):
 @pytest.mark.parametrize("b,n,C,M,N", [(12, 1, 3, 131, 250), (12, 3, 3, 131, 250), (24, 4, 1, 100, 300),
                                        (30, 5, 3, 97, 211), (40, 4, 3, 120, 170), (64, 8, 1, 130, 200),
                                        (128, 16, 3, 300, 260), (5, 1, 4, 33, 47), (6, 3, 3, 64, 90),
-                                       (128, 1, 1, 129, 300)])
+                                       (128, 1, 1, 129, 300), (128, 128, 1, 300, 900),
+                                       (128, 64, 3, 260, 1400)])
 def test_row_streaming_path(ctx, b, n, C, M, N):
     """Grid sides outside the TMA set (the paper's b = 12, 24, 30, 40, 128) take
     the row-streaming K1r / K2r: bit-exact vs the oracle, uniform and adaptive,
