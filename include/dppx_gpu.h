@@ -111,8 +111,9 @@ typedef struct {
 /* Per kernel-family launch counts and (when timing is on) summed device ms. */
 typedef enum {
   DPPX_K_CLASSIFY = 0, /* K0: mask -> per-cell classification + slot scan */
-  DPPX_K_STATS = 1,    /* K1: TMA-staged fused stats/noise/store/reconstruct */
-  DPPX_K_GENERIC = 2,  /* K1g: any b, n, C, alignment                         */
+  DPPX_K_STATS = 1,    /* K1: TMA-staged fused stats/noise/store/reconstruct  */
+                       /*     (b in {4,8,12,16,20,24,32,40,64}, C in {1,3})     */
+  DPPX_K_GENERIC = 2,  /* K1g: Algorithm 1 and shapes K1r cannot hold          */
   DPPX_K_EXPAND = 3,   /* K2: statistics -> pixels                            */
   DPPX_K_AUX = 4,      /* synthetic generator, payload checks                 */
   DPPX_K_ROWS = 5,     /* K1r: row-streaming stats for other grid sides        */

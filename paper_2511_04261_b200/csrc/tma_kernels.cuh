@@ -40,7 +40,7 @@ __device__ __forceinline__ UnitPos decode_unit(const StatsArgs& a, int u) {
   return p;
 }
 
-// Slot geometry: compile-time for wide frames (one 512-px slot per unit).
+// Slot geometry: compile-time for wide frames (one TILE-px slot per unit).
 template <bool PACKED, int TILE = kTilePx>
 __device__ __forceinline__ int slot_px(const StatsArgs& a) {
   return PACKED ? a.slot_px : TILE;
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(kStatsThreads)
 
   if (warp == kConsumers / 32) {
     // ---------------- producer warp: TMA loads + bulk stores ----------------
-    // Units (frame, grid row, 512-px tile) are claimed from a global counter so
+    // Units (frame, grid row, TILE-px tile) are claimed from a global counter so
     // heavy (complex-cell) tiles spread over all CTAs.
     // The whole warp stays in the loop: lane 0 claims units and issues the TMA
     // copies; all 32 lanes write the few output bytes past the output tensor
@@ -696,7 +696,7 @@ __global__ void __launch_bounds__(kStatsThreads)
 }
 
 // ============================================================================
-// K2 fast path: one CTA per (frame, grid row, 512-px tile); each thread owns a
+// K2 fast path: one CTA per (frame, grid row, TILE-px tile); each thread owns a
 // 4-px strip, looks up its cell's statistics per channel plane (packed slots
 // from K0's per-plane scan), writes the strip pattern into a smem tile and one
 // thread bulk-stores the tile with a 3-D TMA box (clipped at M and N).
