@@ -242,6 +242,12 @@ int dppx_encode_record(int32_t height, int32_t width, int32_t b, int32_t n, int3
 /* decode's checks in order: NOT_A_RECORD, CORRUPT (truncated header), CORRUPTION
  * (CRC), UNSUPPORTED_VERSION, CORRUPT (mode/reserved/dims/fields/lengths/count). */
 int dppx_decode_record(const uint8_t* bytes, size_t len, dppx_record_info* info);
+/* reconstruct(decode(bytes)) (record.hpp:63, record.cpp:280-286): decodes the
+ * record with the checks above, then expands it on the GPU (broadcast_means
+ * for uniform, reassemble for adaptive) into out (height x width bytes, dense;
+ * out_cap >= height * width). Status codes as dppx_decode_record / the expanders. */
+int dppx_reconstruct_record(dppx_ctx* ctx, const uint8_t* bytes, size_t len, uint8_t* out,
+                            size_t out_cap);
 
 /* ---- utility metrics (metrics.hpp:27-37, metrics.cpp:26-183) ------------- */
 /* Per channel plane (f, c) of frame batches a (pitch, frame_stride) and b

@@ -149,6 +149,7 @@ ABI = {
     "dppx_encode_record": (C.c_int, [C.c_int32] * 5 + [_vp, C.c_size_t, _vp, C.c_size_t,
                                                        C.POINTER(C.c_size_t)]),
     "dppx_decode_record": (C.c_int, [_vp, C.c_size_t, C.POINTER(RecordInfo)]),
+    "dppx_reconstruct_record": (C.c_int, [_ctxp, _vp, C.c_size_t, _vp, C.c_size_t]),
     "dppx_debug_device_laplace": (C.c_int, [_ctxp, C.c_uint64, _vp, C.c_int32, C.c_double, _vp]),
     "dppx_debug_lg2_max_error": (C.c_int, [_ctxp, C.POINTER(C.c_double)]),
 }
@@ -448,6 +449,18 @@ class Context:
                     "pixelize_adaptive_variance")
         del keep
         return [bytes(buf[i, : lens[i]]) for i in range(F * Cn)], out
+
+    def reconstruct_record(self, record: bytes) -> np.ndarray:
+        """dppx_reconstruct_record: decode a .dppx record and expand it on the GPU."""
+        info = RecordInfo()
+        buf = np.frombuffer(record, np.uint8).copy()
+        rc = _lib.dppx_decode_record(_ptr(buf), buf.size, C.byref(info))
+        if rc != OK:
+            raise RecordError(f"decode: status {rc}")
+        out = np.zeros((info.height, info.width), np.uint8)
+        self._check(_lib.dppx_reconstruct_record(self._h, _ptr(buf), buf.size, _ptr(out), out.size),
+                    "reconstruct_record")
+        return out
 
     def broadcast_means(self, means, M, N, b, channels=1, frames=1):
         means = np.ascontiguousarray(means, dtype=np.uint8)

@@ -1587,6 +1587,28 @@ int dppx_broadcast_means(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t
                        const_cast<uint8_t*>(means), 0, nullptr, nullptr, b, 1, out);
 }
 
+int dppx_reconstruct_record(dppx_ctx* ctx, const uint8_t* bytes, size_t len, uint8_t* out,
+                            size_t out_cap) {
+  if (int rc = check_ctx(ctx)) return rc;
+  dppx_record_info info{};
+  if (int rc = dppx_decode_record(bytes, len, &info))
+    return set_err(ctx, rc, "decode: record rejected (status %d)", rc);
+  const size_t need = static_cast<size_t>(info.height) * static_cast<size_t>(info.width);
+  if (!out || out_cap < need) return set_err(ctx, DPPX_ERR_INVALID, "reconstruct: output too small");
+  dppx_frames_desc d{};
+  d.height = info.height;
+  d.width = info.width;
+  d.channels = 1;
+  d.frames = 1;
+  d.pitch = d.mask_pitch = d.out_pitch = info.width;
+  d.frame_stride = d.mask_frame_stride = d.out_frame_stride = static_cast<int64_t>(need);
+  const uint8_t* payload = bytes + info.payload_offset;
+  if (info.mode == 1) return dppx_broadcast_means(ctx, &d, payload, info.b, out);
+  const uint32_t plen = info.payload_len;
+  return dppx_reassemble(ctx, &d, payload, static_cast<int64_t>((plen + 3) & ~3u), &plen, info.b,
+                         info.n, out);
+}
+
 int dppx_reassemble(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* payload,
                     int64_t payload_stride, const uint32_t* payload_len, int32_t b, int32_t n,
                     uint8_t* out) {

@@ -636,3 +636,26 @@ def test_staged_kernel_whole_cell_warps(ctx, b, n, C, M, N):
         rm, rui = _oracle_uniform(frames, p, "keyed", seeds)
         assert np.array_equal(means, rm) and np.array_equal(uimg, rui)
         assert np.array_equal(ctx.broadcast_means(means, M, N, b, channels=C, frames=F), uimg)
+
+
+@pytest.mark.parametrize("b,n", [(16, 4), (16, 1), (12, 3), (30, 5), (7, 1)])
+def test_reconstruct_record_c_abi(ctx, b, n):
+    """dppx_reconstruct_record (reconstruct(decode(bytes)), record.cpp:280-286)
+    on records written by the codec from GPU payloads: equals the image the
+    pixelization emitted; a flipped byte is rejected by decode's CRC check."""
+    rng = np.random.default_rng(b * 5 + n)
+    M, N = 137, 211
+    img = rng.integers(0, 256, (1, M, N, 1), np.uint8)
+    mask = (rng.random((1, M, N)) < 0.6).astype(np.uint8)
+    p = dp.make_privacy_params(0.5, 16, b, n)
+    if n == 1:
+        means, out = ctx.pixelize_uniform(img, p, dp.NOISE_KEYED, [123])
+        rec = dp.encode_record(M, N, b, 1, bytes(means[0]), False)
+    else:
+        pls, out = ctx.pixelize_adaptive(img, mask, p, dp.NOISE_KEYED, [123])
+        rec = dp.encode_record(M, N, b, n, pls[0], True)
+    assert np.array_equal(ctx.reconstruct_record(rec), out[0, :, :, 0])
+    bad = bytearray(rec)
+    bad[len(bad) // 2] ^= 0x40
+    with pytest.raises(dp.RecordError):
+        ctx.reconstruct_record(bytes(bad))
