@@ -526,6 +526,8 @@ def main():
                          "traffic": traffic, "kernel": f"K1 {kfam}",
                          "algorithmic_bytes_per_launch": k1_bytes,
                          "avg_launch_ms": round(k1_ms, 4), "peak_source": peak_src,
+                         # context only: HGX nominal 7.7 TB/s (B200_PROFILING.md)
+                         "frac_of_nominal_7700": round(achieved / 7700.0, 4),
                          "step_gbs_incl_K0": round(step_gbs, 1),
                          "step_frac_incl_K0": round(step_gbs / peak, 4),
                          "k0_ms_per_launch": round(st["device_ms"]["classify"] /
