@@ -372,7 +372,7 @@ int classify(dppx_ctx* ctx, const BatchGeom& g, int planes, bool from_payload, c
   a.vec = 1;
   a.mask_bits = mask_bits ? 1 : 0;
   a.band = 0;
-  if (!from_payload && !var && mask_bits && g.b >= 12) a.band = 2;  // bits: per-(cell, row) popc
+  if (!from_payload && !var && mask_bits && g.b >= 48) a.band = 2;  // bits, large b: per-(cell, row) popc
   if (!from_payload && !var && !mask_bits) {
     const bool al16 = aligned16(mask) && mpitch % 16 == 0 && mfstride % 16 == 0;
     if (g.b % 16 == 0 && al16) a.vec = 16;
