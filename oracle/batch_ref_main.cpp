@@ -1,0 +1,35 @@
+// Test infrastructure: the reference's own run_batch (cli.cpp:175-213),
+// compiled unmodified from /root/reference by oracle/Makefile, timed around
+// the call. Used only by tools/batch_bench.py as the reference arm.
+// usage: dppix_batch_ref in_dir out_dir u|a mask_dir eps m b n seed threads
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
+#include "dppix/cli.hpp"
+
+int main(int argc, char** argv) {
+  if (argc != 11) {
+    std::fprintf(stderr, "usage: %s in out u|a masks eps m b n seed threads\n", argv[0]);
+    return 2;
+  }
+  dppix::RunConfig cfg;
+  cfg.input = argv[1];
+  cfg.out_dir = argv[2];
+  cfg.mode = argv[3][0] == 'a' ? dppix::RunMode::adaptive : dppix::RunMode::uniform;
+  cfg.mask_path = argv[4];
+  cfg.epsilon = std::atof(argv[5]);
+  cfg.m = std::atoi(argv[6]);
+  cfg.b = std::atoi(argv[7]);
+  cfg.n = std::atoi(argv[8]);
+  cfg.seed = dppix::NoiseSeed{std::strtoull(argv[9], nullptr, 10)};
+  cfg.threads = std::atoi(argv[10]);
+  const auto t0 = std::chrono::steady_clock::now();
+  const auto reports = dppix::run_batch(cfg);
+  const auto t1 = std::chrono::steady_clock::now();
+  int failures = 0;
+  for (const auto& r : reports) failures += r.exit_code != 0;
+  std::printf("{\"files\": %zu, \"seconds\": %.6f, \"failures\": %d}\n", reports.size(),
+              std::chrono::duration<double>(t1 - t0).count(), failures);
+  return failures ? 1 : 0;
+}

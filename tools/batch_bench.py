@@ -1,0 +1,81 @@
+#!/usr/bin/env python3
+"""Batch runner, end to end on files: the reference's run_batch
+(cli.cpp:175-213, compiled from its sources: oracle/_ref/dppix_batch_ref) vs
+run_batch_gpu (include/dppix/batch.hpp: tests/cpp/batch_gpu) on the same
+directory of P5 PGM frames + paired masks. Both write <stem>.pix.pgm and
+<stem>.dppx and run the reconstruct check + metrics; the tool times both and
+compares every output file byte for byte.
+
+usage (GPU box): python tools/batch_bench.py [--files 64] [--height 1080] [--width 1920]
+"""
+import argparse
+import filecmp
+import json
+import os
+import shutil
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def write_pgm(path, img):
+    h, w = img.shape
+    with open(path, "wb") as f:
+        f.write(f"P5\n{w} {h}\n255\n".encode())
+        f.write(img.tobytes())
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--files", type=int, default=64)
+    ap.add_argument("--height", type=int, default=1080)
+    ap.add_argument("--width", type=int, default=1920)
+    ap.add_argument("--mode", default="a", choices=["a", "u"])
+    ap.add_argument("--b", type=int, default=16)
+    ap.add_argument("--n", type=int, default=4)
+    ap.add_argument("--dir", default="/tmp/dppx_batch")
+    args = ap.parse_args()
+    import numpy as np
+
+    import oracle
+    M, N, F = args.height, args.width, args.files
+    shutil.rmtree(args.dir, ignore_errors=True)
+    d_in, d_mask = os.path.join(args.dir, "in"), os.path.join(args.dir, "masks")
+    d_ref, d_gpu = os.path.join(args.dir, "out_ref"), os.path.join(args.dir, "out_gpu")
+    for d in (d_in, d_mask, d_ref, d_gpu):
+        os.makedirs(d)
+    frames = oracle.synth_frames(0, F, M, N, 1)[..., 0]
+    masks = oracle.synth_masks(0, F, M, N)
+    for i in range(F):
+        write_pgm(os.path.join(d_in, f"f{i:05d}.pgm"), frames[i])
+        write_pgm(os.path.join(d_mask, f"f{i:05d}.pgm"), (masks[i] * 255).astype(np.uint8))
+    n = args.n if args.mode == "a" else 1
+    common = [args.mode, d_mask, "0.5", "16", str(args.b), str(n), "42"]
+    threads = str(os.cpu_count() or 1)
+    ref_bin = os.path.join(ROOT, "oracle", "_ref", "dppix_batch_ref")
+    gpu_bin = os.path.join(ROOT, "tests", "cpp", "batch_gpu")
+    ref = json.loads(subprocess.run([ref_bin, d_in, d_ref] + common + [threads], check=True,
+                                    capture_output=True, text=True).stdout)
+    # GPU arm: one warm-up pass (context creation, module load), then the timed one
+    subprocess.run([gpu_bin, d_in, d_gpu] + common + ["0"], check=True, capture_output=True)
+    gpu = json.loads(subprocess.run([gpu_bin, d_in, d_gpu] + common + ["0"], check=True,
+                                    capture_output=True, text=True).stdout)
+    names = sorted(os.listdir(d_ref))
+    same = names == sorted(os.listdir(d_gpu)) and all(
+        filecmp.cmp(os.path.join(d_ref, x), os.path.join(d_gpu, x), shallow=False) for x in names)
+    mp = F * M * N / 1e6
+    print(json.dumps({
+        "workload": f"{F} P5 files {N}x{M} gray, {'adaptive' if args.mode == 'a' else 'uniform'} "
+                    f"b{args.b} n{n} eps 0.5 m 16, same seed per file (run_batch), outputs "
+                    ".pix.pgm + .dppx, reconstruct check + metrics",
+        "reference": {**ref, "threads": int(threads), "MP_per_s": round(mp / ref["seconds"], 1)},
+        "gpu": {**gpu, "MP_per_s": round(mp / gpu["seconds"], 1)},
+        "speedup": round(ref["seconds"] / gpu["seconds"], 2),
+        "outputs_identical": same, "output_files": len(names)}))
+    shutil.rmtree(args.dir, ignore_errors=True)
+
+
+if __name__ == "__main__":
+    main()
