@@ -17,6 +17,7 @@
 #include <functional>
 #include <limits>
 #include <map>
+#include <memory>
 #include <thread>
 #include <utility>
 
@@ -76,18 +77,12 @@ void parallel_over(int count, int workers, const std::function<void(int)>& body)
   throw std::runtime_error(msg);
 }
 
-struct Pinned {  // pinned host staging (dppx_host_alloc)
+struct HostBuf {  // pageable host batch buffer (no zero fill)
+  std::unique_ptr<uint8_t[]> mem;
   uint8_t* p = nullptr;
-  size_t n = 0;
-  explicit Pinned(size_t bytes) : n(bytes) {
-    void* q = nullptr;
-    if (dppx_host_alloc(bytes ? bytes : 1, &q) != DPPX_OK) throw std::bad_alloc();
-    p = static_cast<uint8_t*>(q);
-  }
-  ~Pinned() { dppx_host_free(p); }
-  Pinned(const Pinned&) = delete;
-  Pinned& operator=(const Pinned&) = delete;
+  explicit HostBuf(size_t bytes) : mem(new uint8_t[bytes ? bytes : 1]), p(mem.get()) {}
 };
+
 
 }  // namespace
 
@@ -219,12 +214,14 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
       const int F = static_cast<int>(std::min<size_t>(K, members.size() - c0));
       const std::vector<int> chunk(members.begin() + c0, members.begin() + c0 + F);
       try {
-        Pinned in(plane * F), out(plane * F), mk(cfg.mode == BatchMode::adaptive ? plane * F : 0);
-        for (int k = 0; k < F; ++k) {
+        // Pageable batch buffers: pinning hundreds of MB per call costs more
+        // than the driver-staged copies of pageable memory (measured).
+        HostBuf in(plane * F), out(plane * F), mk(cfg.mode == BatchMode::adaptive ? plane * F : 0);
+        parallel_over(F, io, [&](int k) {
           std::memcpy(in.p + k * plane, imgs[chunk[k]].pixels.data(), plane);
           if (cfg.mode == BatchMode::adaptive)
             std::memcpy(mk.p + k * plane, masks[chunk[k]].values.data(), plane);
-        }
+        });
         dppx_frames_desc d{M, N, 1, F, N, static_cast<int64_t>(plane), N, static_cast<int64_t>(plane),
                            N, static_cast<int64_t>(plane)};
         std::vector<uint64_t> seeds(F, cfg.seed ? cfg.seed->value : 0);
@@ -261,7 +258,7 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
               throw std::invalid_argument("encode: payload inconsistent");
           }
           if (cfg.reconstruct_check) {
-            Pinned rebuilt(plane * F);
+            HostBuf rebuilt(plane * F);
             std::vector<uint8_t> payload(cap * F);
             std::vector<uint32_t> plen(F);
             for (int k = 0; k < F; ++k) {  // decode, then rebuild from the decoded payload
