@@ -11,6 +11,8 @@
 #include <cctype>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <filesystem>
 #include <fstream>
@@ -167,6 +169,11 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
     reports[i].error = err.what();
     reports[i].exit_code = batch_exit_code_for(err);
   };
+  // DPPX_BATCH_TRACE=1: per-phase wall times on stderr.
+  static const bool trace = std::getenv("DPPX_BATCH_TRACE") != nullptr;
+  auto tnow = [] { return std::chrono::steady_clock::now(); };
+  auto tms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+  const auto T0 = tnow();
   // ---- ingest (host threads) ----
   parallel_over(nfile, io, [&](int i) {
     reports[i].input = inputs[i];
@@ -190,6 +197,8 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
       fail(i, err);
     }
   });
+  const auto T1 = tnow();
+  if (trace) std::fprintf(stderr, "batch: ingest %.1f ms\n", tms(T0, T1));
   // ---- group by shape, GPU calls of up to frames_per_call frames ----
   std::map<std::pair<int, int>, std::vector<int>> groups;
   for (int i = 0; i < nfile; ++i)
@@ -244,6 +253,7 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
         else
           rc = dppx_pixelize_reference(ctx, &d, in.p, &pp, &nz, stats.data(), out.p);
         const auto t1 = std::chrono::steady_clock::now();
+        if (trace) std::fprintf(stderr, "batch: pixelize %d frames %.1f ms\n", F, tms(t0, t1));
         if (rc != DPPX_OK) raise_status(rc, "pixelize");
         const double per_ms = std::chrono::duration<double, std::milli>(t1 - t0).count() / F;
         // ---- records + reconstruct check (cli.cpp:132-146), on the GPU ----
@@ -280,11 +290,15 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
               }
           }
         }
+        const auto t2 = tnow();
+        if (trace) std::fprintf(stderr, "batch: records + reconstruct check %.1f ms\n", tms(t1, t2));
         // ---- metrics on the GPU (cli.cpp:164-171) ----
         std::vector<double> mses(F), ssims(F, std::numeric_limits<double>::quiet_NaN());
         if (dppx_mse(ctx, &d, in.p, out.p, mses.data()) != DPPX_OK) raise_status(DPPX_ERR_CUDA, "mse");
         if (M >= 7 && N >= 7 && dppx_ssim(ctx, &d, in.p, out.p, ssims.data()) != DPPX_OK)
           raise_status(DPPX_ERR_CUDA, "ssim");
+        const auto t3 = tnow();
+        if (trace) std::fprintf(stderr, "batch: metrics %.1f ms\n", tms(t2, t3));
         // ---- outputs (host threads) ----
         parallel_over(F, io, [&](int k) {
           const int i = chunk[k];
@@ -322,6 +336,7 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
             fail(i, err);
           }
         });
+        if (trace) std::fprintf(stderr, "batch: outputs %.1f ms\n", tms(t3, tnow()));
       } catch (const std::exception& err) {
         for (int i : chunk)
           if (reports[i].exit_code == 0) fail(i, err);
