@@ -257,6 +257,10 @@ int dppx_mse(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* a, cons
              double* out);
 int dppx_ssim(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* a, const uint8_t* b,
               double* out); /* 7x7 uniform window, C1 = 6.5025, C2 = 58.5225 */
+/* Both metrics from one upload of a and b (the batch runner's per-file
+ * mse + ssim, cli.cpp:164-171); either output may be NULL. */
+int dppx_metrics(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* a, const uint8_t* b,
+                 double* mse_out, double* ssim_out);
 int dppx_mse_dev(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* a, const uint8_t* b,
                  double* out);
 int dppx_ssim_dev(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* a, const uint8_t* b,

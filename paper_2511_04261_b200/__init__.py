@@ -142,6 +142,7 @@ ABI = {
     "dppx_classify_regions": (C.c_int, [_ctxp, _descp, _vp, C.c_int32, _vp]),
     "dppx_mse": (C.c_int, [_ctxp, _descp, _vp, _vp, _vp]),
     "dppx_ssim": (C.c_int, [_ctxp, _descp, _vp, _vp, _vp]),
+    "dppx_metrics": (C.c_int, [_ctxp, _descp, _vp, _vp, _vp, _vp]),
     "dppx_mse_dev": (C.c_int, [_ctxp, _descp, _vp, _vp, _vp]),
     "dppx_ssim_dev": (C.c_int, [_ctxp, _descp, _vp, _vp, _vp]),
     "dppx_crc32": (C.c_uint32, [C.c_uint32, _vp, C.c_size_t]),
@@ -289,6 +290,31 @@ def _frames_shape(img):
     return s[0], s[1], s[2], s[3]
 
 
+def pinned_empty(shape, dtype=np.uint8) -> np.ndarray:
+    """Page-locked host array (torch's pinned allocator; the array keeps the
+    tensor alive). Host calls on pinned buffers DMA directly; pageable ones are
+    staged through the context's pinned buffers by host threads."""
+    import torch
+    t = torch.empty(tuple(shape), dtype=getattr(torch, np.dtype(dtype).name), pin_memory=True)
+    a = t.numpy()
+    holder = _PinnedArray(a)
+    holder._tensor = t
+    return holder
+
+
+class _PinnedArray(np.ndarray):
+    def __new__(cls, a):
+        return np.asarray(a).view(cls)
+
+
+def _out_image(frames, out, want_image):
+    if out is None:
+        return np.zeros_like(frames) if want_image else None
+    if out.shape != frames.shape or out.dtype != np.uint8 or not out.flags.c_contiguous:
+        raise ValueError("out must be a C-contiguous uint8 array of the frames' shape")
+    return out
+
+
 class Context:
     """One dppx_ctx: a device, its streams, scratch and pinned staging.
 
@@ -378,13 +404,14 @@ class Context:
 
     # ---- host entry points (numpy in / numpy out)
     def pixelize_uniform(self, frames, params: PrivacyParams, noise=NOISE_NONE, seeds=None,
-                         frame_base=0, injected=None, want_image=True):
-        """frames: uint8 [F,M,N,C] (or [M,N], [M,N,C]). Returns (means[F*C, G], image)."""
+                         frame_base=0, injected=None, want_image=True, out=None):
+        """frames: uint8 [F,M,N,C] (or [M,N], [M,N,C]). Returns (means[F*C, G], image).
+        `out` (optional, frames' shape) receives the image, e.g. a pinned_empty buffer."""
         frames = np.ascontiguousarray(frames, dtype=np.uint8)
         F, M, N, Cn = _frames_shape(frames)
         g = grid_dims(M, N, params.b)
         means = np.zeros((F * Cn, g.grid_count()), np.uint8)
-        out = np.zeros_like(frames) if want_image else None
+        out = _out_image(frames, out, want_image)
         nz, keep = self._noise(noise, seeds, frame_base, injected)
         d = _desc(M, N, Cn, F)
         self._check(_lib.dppx_pixelize_uniform(self._h, C.byref(d), _ptr(frames), C.byref(params),
@@ -394,9 +421,9 @@ class Context:
         return means, out
 
     def pixelize_adaptive(self, frames, masks, params: PrivacyParams, noise=NOISE_NONE,
-                          seeds=None, frame_base=0, injected=None, want_image=True):
+                          seeds=None, frame_base=0, injected=None, want_image=True, out=None):
         """frames uint8 [F,M,N,C], masks uint8 [F,M,N]. Returns (payloads: list of bytes per
-        plane (f*C + c), image)."""
+        plane (f*C + c), image). `out` as in pixelize_uniform."""
         frames = np.ascontiguousarray(frames, dtype=np.uint8)
         F, M, N, Cn = _frames_shape(frames)
         masks = np.ascontiguousarray(masks, dtype=np.uint8).reshape(F, M, N)
@@ -404,7 +431,7 @@ class Context:
         stride = (cap + 3) & ~3
         buf = np.zeros((F * Cn, stride), np.uint8)
         lens = np.zeros(F * Cn, np.uint32)
-        out = np.zeros_like(frames) if want_image else None
+        out = _out_image(frames, out, want_image)
         nz, keep = self._noise(noise, seeds, frame_base, injected)
         d = _desc(M, N, Cn, F)
         self._check(_lib.dppx_pixelize_adaptive(self._h, C.byref(d), _ptr(frames), _ptr(masks),
@@ -498,7 +525,8 @@ class Context:
         return mm
 
     def metrics(self, a, b, which="ssim"):
-        """mse / ssim per channel plane of two frame batches ([F,M,N,C] or [M,N])."""
+        """mse / ssim per channel plane of two frame batches ([F,M,N,C] or [M,N]);
+        which="both" returns (mse, ssim) from one upload (dppx_metrics)."""
         a = np.ascontiguousarray(a, dtype=np.uint8)
         b = np.ascontiguousarray(b, dtype=np.uint8)
         if a.shape != b.shape:
@@ -506,6 +534,11 @@ class Context:
         F, M, N, Cn = _frames_shape(a)
         out = np.zeros(F * Cn, np.float64)
         d = _desc(M, N, Cn, F)
+        if which == "both":
+            out2 = np.zeros(F * Cn, np.float64)
+            self._check(_lib.dppx_metrics(self._h, C.byref(d), _ptr(a), _ptr(b), _ptr(out),
+                                          _ptr(out2)), which)
+            return out, out2
         fn = _lib.dppx_ssim if which == "ssim" else _lib.dppx_mse
         self._check(fn(self._h, C.byref(d), _ptr(a), _ptr(b), _ptr(out)), which)
         return out

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -126,6 +127,14 @@ struct dppx_ctx {
   uint32_t* mbits_pinned[2] = {nullptr, nullptr};
   size_t mbits_pinned_n[2] = {0, 0};
   int mask_bits_mode = -1;  // -1 unset (env DPPX_MASK_BITS, default on), 0 off, 1 on
+  // pageable caller buffers: pinned staging per slot, filled / drained by host threads
+  uint8_t* stg_in[2] = {nullptr, nullptr};
+  uint8_t* stg_out[2] = {nullptr, nullptr};
+  size_t stg_in_n[2] = {0, 0}, stg_out_n[2] = {0, 0};
+  cudaEvent_t stg_ev[2] = {};
+  uint8_t* piece[2] = {nullptr, nullptr};  // h2d_frames pieces
+  size_t piece_n[2] = {0, 0};
+  cudaEvent_t piece_ev[2] = {};
   // stats
   bool timing = false;
   std::vector<PendingTiming> pending;
@@ -805,6 +814,65 @@ cudaError_t copy_frames(void* dst, int64_t dpitch, int64_t dfs, const void* src,
 
 enum class HostOp { Uniform, Adaptive, Broadcast, Reassemble, Reference, AdaptiveVariance };
 
+// Page-locked (or device / managed) memory the DMA engines can read directly.
+bool host_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type != cudaMemoryTypeUnregistered;
+}
+
+int grow_pinned(dppx_ctx* ctx, uint8_t*& buf, size_t& have, size_t need) {
+  if (have >= need) return DPPX_OK;
+  if (buf) CUDA_TRY(ctx, cudaFreeHost(buf));
+  buf = nullptr;
+  have = 0;
+  CUDA_TRY(ctx, cudaHostAlloc(reinterpret_cast<void**>(&buf), need, cudaHostAllocDefault));
+  have = need;
+  return DPPX_OK;
+}
+
+// Host -> device copy of F frames (rows of `row` bytes). A pinned source is one
+// DMA; a pageable one is cut into ~16 MB pieces of whole rows that host threads
+// copy into two pinned buffers in turn, so the host copies overlap the DMA.
+int h2d_frames(dppx_ctx* ctx, uint8_t* dst, int64_t dpitch, int64_t dfs, const uint8_t* src,
+               int64_t spitch, int64_t sfs, int64_t row, int M, int F, cudaStream_t st) {
+  if (host_pinned(src)) {
+    CUDA_TRY(ctx, copy_frames(dst, dpitch, dfs, src, spitch, sfs, row, M, F, cudaMemcpyHostToDevice, st));
+    return DPPX_OK;
+  }
+  if (!ctx->packer) ctx->packer = dppx::mask_packer_create(0);
+  const int64_t rows = static_cast<int64_t>(F) * M;
+  const int64_t per = std::max<int64_t>(1, (int64_t{16} << 20) / dpitch);
+  const bool linear = dfs == static_cast<int64_t>(M) * dpitch;  // dst row r at r * dpitch
+  for (int s = 0; s < 2; ++s) {
+    if (int rc = grow_pinned(ctx, ctx->piece[s], ctx->piece_n[s], static_cast<size_t>(per * dpitch)))
+      return rc;
+    if (!ctx->piece_ev[s]) CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->piece_ev[s], cudaEventDisableTiming));
+  }
+  int64_t r0 = 0;
+  for (int k = 0; r0 < rows; ++k) {
+    int64_t r1 = std::min(rows, r0 + per);
+    if (!linear) r1 = std::min(r1, (r0 / M + 1) * M);  // pieces stay inside one frame
+    const int s = k & 1;
+    // the buffer's previous DMA (this call's piece k-2, or an earlier call's)
+    CUDA_TRY(ctx, cudaEventSynchronize(ctx->piece_ev[s]));
+    uint8_t* buf = ctx->piece[s];
+    dppx::pool_for(ctx->packer, r1 - r0, [&](int64_t a, int64_t b) {
+      for (int64_t r = r0 + a; r < r0 + b; ++r)
+        std::memcpy(buf + (r - r0) * dpitch, src + (r / M) * sfs + (r % M) * spitch, static_cast<size_t>(row));
+    });
+    uint8_t* d0 = dst + (r0 / M) * dfs + (r0 % M) * dpitch;
+    const size_t bytes = static_cast<size_t>(r1 - r0 - 1) * dpitch + row;
+    CUDA_TRY(ctx, cudaMemcpyAsync(d0, buf, bytes, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->piece_ev[s], st));
+    r0 = r1;
+  }
+  return DPPX_OK;
+}
+
 // Single-frame host calls: there is no second frame to overlap with, so the
 // frame is split into bands of grid rows. Band i's rows are copied in while
 // band i-1 is computed and band i-2 is copied out (H2D, K1, D2H on three
@@ -965,6 +1033,11 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
                   const uint8_t* mask, const dppx_privacy_params* pp, const dppx_noise* nz,
                   uint8_t* stats, int64_t sstride, uint32_t* lens, const uint32_t* in_lens,
                   int b_arg, int n_arg, uint8_t* out) {
+  static const bool trace = std::getenv("DPPX_PIPE_TRACE") != nullptr;
+  const auto tp0 = std::chrono::steady_clock::now();
+  auto tp_ms = [&] {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count();
+  };
   const bool pix = op == HostOp::Uniform || op == HostOp::Adaptive || op == HostOp::Reference ||
                    op == HostOp::AdaptiveVariance;
   const bool adaptive = op == HostOp::Adaptive || op == HostOp::Reassemble ||
@@ -1021,7 +1094,7 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
     const int nb = static_cast<int>(std::min<int64_t>(
         {static_cast<int64_t>(dppx_ctx::kMaxBands), g.GR / 2, frame_bytes >> 21}));
     if (bands_ok && F == 1 && (op == HostOp::Uniform || op == HostOp::Adaptive) && !inj_any &&
-        nb >= 2)
+        nb >= 2 && host_pinned(img) && (!out || host_pinned(out)))
       return host_pipeline_bands(ctx, adaptive, d, g, img, mask, pp, nz, stats, sstride, lens, out, nb);
   }
   const int64_t dpitch = round_up(static_cast<int64_t>(N) * C, 16);
@@ -1057,16 +1130,28 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
   const int64_t row = static_cast<int64_t>(N) * C;
   // Dense linear PCIe transfers + on-device re-pitch when the kernels' 16-byte
   // pitch differs from a dense host layout (e.g. 178 x 3 = 534-byte rows).
-  const bool dense_in = pix && dpitch != row && d->pitch == row && d->frame_stride == row * M;
+  // Pageable caller buffers: host threads copy rows into / out of pinned
+  // staging in the device layout, so the DMA runs at pinned speed (the
+  // driver's own pageable path is serial and several times slower).
+  const bool stage_in = pix && !host_pinned(img);
+  const bool stage_out = out && !host_pinned(out);
+  const bool dense_in = !stage_in && pix && dpitch != row && d->pitch == row && d->frame_stride == row * M;
   const bool dense_mask = op == HostOp::Adaptive && dmpitch != N && d->mask_pitch == N &&
                           d->mask_frame_stride == static_cast<int64_t>(N) * M;
-  const bool dense_out = out && dpitch != row && d->out_pitch == row && d->out_frame_stride == row * M;
+  const bool dense_out = !stage_out && out && dpitch != row && d->out_pitch == row &&
+                         d->out_frame_stride == row * M;
   // Bit-packed mask transport: 1/8 of the mask's PCIe bytes (maskpack.h).
   const bool try_bits = op == HostOp::Adaptive && ctx->mask_bits_mode == 1;
   const int64_t wpr = dppx::mask_words_per_row(N);
   const size_t bits_frame = static_cast<size_t>(wpr) * 4 * M;
-  if (try_bits && !ctx->packer) ctx->packer = dppx::mask_packer_create(0);
+  if ((try_bits || stage_in || stage_out) && !ctx->packer) ctx->packer = dppx::mask_packer_create(0);
   for (int s = 0; s < 2 && s < chunks; ++s) {
+    if (stage_in)
+      if (int rc = grow_pinned(ctx, ctx->stg_in[s], ctx->stg_in_n[s], static_cast<size_t>(dfs) * K)) return rc;
+    if (stage_out)
+      if (int rc = grow_pinned(ctx, ctx->stg_out[s], ctx->stg_out_n[s], static_cast<size_t>(dfs) * K)) return rc;
+    if (stage_out && !ctx->stg_ev[s])
+      CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->stg_ev[s], cudaEventDisableTiming));
     if (pix && ensure(ctx, ctx->img[s], static_cast<size_t>(dfs) * K)) return DPPX_ERR_OOM;
     if (op == HostOp::Adaptive && ensure(ctx, ctx->mask[s], static_cast<size_t>(dmfs) * K))
       return DPPX_ERR_OOM;
@@ -1088,6 +1173,28 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
     }
   }
   cudaStream_t comp = ctx->stream;
+  if (trace)
+    std::fprintf(stderr, "pipe: op %d F %d K %d chunks %d stage_in %d stage_out %d setup %.2f ms\n",
+                 static_cast<int>(op), F, K, chunks, stage_in, stage_out, tp_ms());
+  // Row copies between a caller frame range and pinned staging (device layout).
+  auto stage_rows = [&](uint8_t* dst, int64_t dp, int64_t dfst, const uint8_t* src, int64_t sp,
+                        int64_t sfs, int Fk) {
+    dppx::pool_for(ctx->packer, static_cast<int64_t>(Fk) * M, [&](int64_t r0, int64_t r1) {
+      for (int64_t r = r0; r < r1; ++r) {
+        const int64_t f = r / M, i = r % M;
+        std::memcpy(dst + f * dfst + i * dp, src + f * sfs + i * sp, static_cast<size_t>(row));
+      }
+    });
+  };
+  int pend_f0[2] = {-1, -1}, pend_fk[2] = {0, 0};
+  auto drain = [&](int s) -> int {  // staged output of slot s -> caller buffer
+    if (pend_f0[s] < 0) return DPPX_OK;
+    CUDA_TRY(ctx, cudaEventSynchronize(ctx->stg_ev[s]));
+    stage_rows(out + static_cast<int64_t>(pend_f0[s]) * d->out_frame_stride, d->out_pitch,
+               d->out_frame_stride, ctx->stg_out[s], dpitch, dfs, pend_fk[s]);
+    pend_f0[s] = -1;
+    return DPPX_OK;
+  };
   int f0 = 0;
   for (int ci = 0; ci < chunks; ++ci) {
     const int s = ci & 1;
@@ -1101,7 +1208,14 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
     uint32_t* dlens = static_cast<uint32_t*>(ctx->lens[s].p);
     uint8_t* ddense = static_cast<uint8_t*>(ctx->dense[s].p);
     uint8_t* ddmask = static_cast<uint8_t*>(ctx->dense_mask[s].p);
-    if (pix) {
+    if (pix && stage_in) {
+      if (ci >= 2) CUDA_TRY(ctx, cudaEventSynchronize(ctx->in_done[s]));
+      stage_rows(ctx->stg_in[s], dpitch, dfs, img + static_cast<int64_t>(f0) * d->frame_stride, d->pitch,
+                 d->frame_stride, Fk);
+      CUDA_TRY(ctx, cudaMemcpyAsync(dimg, ctx->stg_in[s], static_cast<size_t>(dfs) * Fk,
+                                    cudaMemcpyHostToDevice, ctx->s_in));
+      ctx->kstats.h2d_bytes += static_cast<uint64_t>(Fk) * M * row;
+    } else if (pix) {
       if (dense_in)
         CUDA_TRY(ctx, cudaMemcpyAsync(ddense, img + static_cast<int64_t>(f0) * d->frame_stride,
                                       static_cast<size_t>(row) * M * Fk, cudaMemcpyHostToDevice,
@@ -1217,7 +1331,15 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
         ctx->kstats.d2h_bytes += sizeof(uint32_t) * Fk * C;
       }
     }
-    if (out) {
+    if (out && stage_out) {
+      if (int rc2 = drain(s)) return rc2;  // chunk ci-2's rows leave the slot first
+      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->stg_out[s], dout, static_cast<size_t>(dfs) * Fk,
+                                    cudaMemcpyDeviceToHost, ctx->s_out));
+      CUDA_TRY(ctx, cudaEventRecord(ctx->stg_ev[s], ctx->s_out));
+      pend_f0[s] = f0;
+      pend_fk[s] = Fk;
+      ctx->kstats.d2h_bytes += static_cast<uint64_t>(Fk) * M * row;
+    } else if (out) {
       if (dense_out)
         CUDA_TRY(ctx, cudaMemcpyAsync(out + static_cast<int64_t>(f0) * d->out_frame_stride, ddense,
                                       static_cast<size_t>(row) * M * Fk, cudaMemcpyDeviceToHost,
@@ -1231,8 +1353,14 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
     CUDA_TRY(ctx, cudaEventRecord(ctx->out_done[s], ctx->s_out));
     f0 += Fk;
   }
+  if (trace) std::fprintf(stderr, "pipe: issued %.2f ms\n", tp_ms());
+  for (int k = 0; k < 2; ++k) {  // oldest pending slot first
+    const int s = (chunks + k) & 1;
+    if (int rc2 = drain(s)) return rc2;
+  }
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->s_out));
   CUDA_TRY(ctx, cudaStreamSynchronize(comp));
+  if (trace) std::fprintf(stderr, "pipe: done %.2f ms\n", tp_ms());
   if (ctx->timing) collect_timings(ctx);
   if (!pix) return read_status(ctx);
   return DPPX_OK;
@@ -1371,6 +1499,11 @@ void dppx_ctx_destroy(dppx_ctx* ctx) {
       if (b->p) cudaFree(b->p);
     if (ctx->sd_pinned[s]) cudaFreeHost(ctx->sd_pinned[s]);
     if (ctx->mbits_pinned[s]) cudaFreeHost(ctx->mbits_pinned[s]);
+    if (ctx->stg_in[s]) cudaFreeHost(ctx->stg_in[s]);
+    if (ctx->stg_out[s]) cudaFreeHost(ctx->stg_out[s]);
+    if (ctx->stg_ev[s]) cudaEventDestroy(ctx->stg_ev[s]);
+    if (ctx->piece[s]) cudaFreeHost(ctx->piece[s]);
+    if (ctx->piece_ev[s]) cudaEventDestroy(ctx->piece_ev[s]);
     cudaEventDestroy(ctx->in_done[s]);
     cudaEventDestroy(ctx->comp_done[s]);
     cudaEventDestroy(ctx->out_done[s]);
@@ -1711,8 +1844,8 @@ int metric_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* a, const
 }
 
 int metric_host(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* a, const uint8_t* b,
-                bool ssim, double* out) {
-  if (!d || !a || !b || !out) return set_err(ctx, DPPX_ERR_INVALID, "null argument");
+                double* mse_out, double* ssim_out) {
+  if (!d || !a || !b || (!mse_out && !ssim_out)) return set_err(ctx, DPPX_ERR_INVALID, "null argument");
   if (d->height < 1 || d->width < 1 || d->channels < 1 || d->channels > 4 || d->frames < 0)
     return set_err(ctx, DPPX_ERR_INVALID, "metrics: invalid dimensions");
   const int M = d->height, F = d->frames;
@@ -1722,28 +1855,38 @@ int metric_host(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* a, cons
   const int64_t fs = row * M;
   if (int rc = ensure(ctx, ctx->met_a, static_cast<size_t>(fs * F))) return rc;
   if (int rc = ensure(ctx, ctx->met_b, static_cast<size_t>(fs * F))) return rc;
-  CUDA_TRY(ctx, copy_frames(ctx->met_a.p, row, fs, a, d->pitch, d->frame_stride, row, M, F,
-                            cudaMemcpyHostToDevice, ctx->stream));
-  CUDA_TRY(ctx, copy_frames(ctx->met_b.p, row, fs, b, d->out_pitch, d->out_frame_stride, row, M, F,
-                            cudaMemcpyHostToDevice, ctx->stream));
+  auto* da = static_cast<uint8_t*>(ctx->met_a.p);
+  auto* db = static_cast<uint8_t*>(ctx->met_b.p);
+  if (int rc = h2d_frames(ctx, da, row, fs, a, d->pitch, d->frame_stride, row, M, F, ctx->stream)) return rc;
+  if (int rc = h2d_frames(ctx, db, row, fs, b, d->out_pitch, d->out_frame_stride, row, M, F, ctx->stream))
+    return rc;
   dppx_frames_desc dd = *d;
   dd.pitch = dd.out_pitch = row;
   dd.frame_stride = dd.out_frame_stride = fs;
-  return metric_dev(ctx, &dd, static_cast<const uint8_t*>(ctx->met_a.p),
-                    static_cast<const uint8_t*>(ctx->met_b.p), ssim, out);
+  if (mse_out)
+    if (int rc = metric_dev(ctx, &dd, da, db, false, mse_out)) return rc;
+  if (ssim_out)
+    if (int rc = metric_dev(ctx, &dd, da, db, true, ssim_out)) return rc;
+  return DPPX_OK;
 }
 }  // namespace
 
 int dppx_mse(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* a, const uint8_t* b,
              double* out) {
   if (int rc = check_ctx(ctx)) return rc;
-  return metric_host(ctx, d, a, b, false, out);
+  return metric_host(ctx, d, a, b, out, nullptr);
 }
 
 int dppx_ssim(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* a, const uint8_t* b,
               double* out) {
   if (int rc = check_ctx(ctx)) return rc;
-  return metric_host(ctx, d, a, b, true, out);
+  return metric_host(ctx, d, a, b, nullptr, out);
+}
+
+int dppx_metrics(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* a, const uint8_t* b,
+                 double* mse_out, double* ssim_out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  return metric_host(ctx, d, a, b, mse_out, ssim_out);
 }
 
 int dppx_mse_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* a, const uint8_t* b,

@@ -294,9 +294,9 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
         if (trace) std::fprintf(stderr, "batch: records + reconstruct check %.1f ms\n", tms(t1, t2));
         // ---- metrics on the GPU (cli.cpp:164-171) ----
         std::vector<double> mses(F), ssims(F, std::numeric_limits<double>::quiet_NaN());
-        if (dppx_mse(ctx, &d, in.p, out.p, mses.data()) != DPPX_OK) raise_status(DPPX_ERR_CUDA, "mse");
-        if (M >= 7 && N >= 7 && dppx_ssim(ctx, &d, in.p, out.p, ssims.data()) != DPPX_OK)
-          raise_status(DPPX_ERR_CUDA, "ssim");
+        if (dppx_metrics(ctx, &d, in.p, out.p, mses.data(), M >= 7 && N >= 7 ? ssims.data() : nullptr) !=
+            DPPX_OK)
+          raise_status(DPPX_ERR_CUDA, "metrics");
         const auto t3 = tnow();
         if (trace) std::fprintf(stderr, "batch: metrics %.1f ms\n", tms(t2, t3));
         // ---- outputs (host threads) ----

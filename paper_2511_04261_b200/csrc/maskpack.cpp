@@ -175,4 +175,12 @@ bool pack_mask_bits(MaskPacker* p, const uint8_t* src, int64_t pitch, int64_t fs
   return ok.load();
 }
 
+void pool_for(MaskPacker* p, int64_t n, const std::function<void(int64_t, int64_t)>& body) {
+  const int parts = p->nthreads;
+  p->run([&](int id) {
+    const int64_t b0 = n * id / parts, b1 = n * (id + 1) / parts;
+    if (b0 < b1) body(b0, b1);
+  });
+}
+
 }  // namespace dppx

@@ -10,6 +10,7 @@
 // sends that chunk's bytes instead.
 #pragma once
 #include <cstdint>
+#include <functional>
 
 namespace dppx {
 
@@ -26,5 +27,9 @@ inline int64_t mask_words_per_row(int N) { return (static_cast<int64_t>(N) + 31)
 // any byte is > 1 (dst contents are then unspecified).
 bool pack_mask_bits(MaskPacker* p, const uint8_t* src, int64_t pitch, int64_t fstride, int M, int N,
                     int F, uint32_t* dst, int64_t wpr);
+
+// Runs body(begin, end) over [0, n) split evenly across the pool's threads
+// (the caller takes one share). Used for pageable <-> pinned staging copies.
+void pool_for(MaskPacker* p, int64_t n, const std::function<void(int64_t, int64_t)>& body);
 
 }  // namespace dppx

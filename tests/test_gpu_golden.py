@@ -98,6 +98,8 @@ def test_metrics_bit_identical_to_reference(ctx):
     _, out = ctx.pixelize_adaptive(frames, masks, p, dp.NOISE_KEYED, dp.plane_seeds(1, 2, 3))
     s = ctx.metrics(frames, out, "ssim")
     m = ctx.metrics(frames, out, "mse")
+    m2, s2 = ctx.metrics(frames, out, "both")
+    assert np.array_equal(m2, m) and np.array_equal(s2, s)
     for f in range(2):
         for c in range(3):
             assert s[f * 3 + c] == oracle.ssim(frames[f, :, :, c], out[f, :, :, c])

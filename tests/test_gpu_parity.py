@@ -543,11 +543,14 @@ def test_randomized_fuzz_against_oracle(ctx):
 @pytest.mark.parametrize("M,N,C,b,n", [(576, 768, 3, 16, 1), (1080, 1920, 3, 16, 4), (1083, 1917, 1, 32, 8),
                                        (2160, 3840, 3, 32, 8), (200, 1000, 3, 8, 2)])
 def test_single_frame_row_bands(ctx, M, N, C, b, n):
-    """Single-frame host calls are pipelined in row bands (H2D / K1 / D2H
-    overlap within the frame): identical to the oracle and to the unbanded path."""
+    """Single-frame host calls on pinned buffers are pipelined in row bands (H2D /
+    K1 / D2H overlap within the frame): identical to the oracle and to the
+    unbanded path."""
     import os
     rng = np.random.default_rng(M * 7 + N)
-    frame = rng.integers(0, 256, (1, M, N, C), np.uint8)
+    frame = dp.pinned_empty((1, M, N, C))
+    frame[...] = rng.integers(0, 256, (1, M, N, C), np.uint8)
+    out = dp.pinned_empty((1, M, N, C))
     mask = (rng.random((1, M, N)) < 0.6).astype(np.uint8)
     p = dp.make_privacy_params(0.5, 16, b, n)
     seeds = dp.plane_seeds(77, 1, C)
@@ -556,8 +559,10 @@ def test_single_frame_row_bands(ctx, M, N, C, b, n):
         os.environ["DPPX_BANDS"] = bands
         try:
             if n == 1:
-                res[bands, "u"] = ctx.pixelize_uniform(frame, p, dp.NOISE_KEYED, seeds)
-            res[bands, "a"] = ctx.pixelize_adaptive(frame, mask, p, dp.NOISE_KEYED, seeds)
+                m, im = ctx.pixelize_uniform(frame, p, dp.NOISE_KEYED, seeds, out=out)
+                res[bands, "u"] = m, im.copy()
+            pl, im = ctx.pixelize_adaptive(frame, mask, p, dp.NOISE_KEYED, seeds, out=out)
+            res[bands, "a"] = pl, im.copy()
         finally:
             del os.environ["DPPX_BANDS"]
     if n == 1:
@@ -659,3 +664,52 @@ def test_reconstruct_record_c_abi(ctx, b, n):
     bad[len(bad) // 2] ^= 0x40
     with pytest.raises(dp.RecordError):
         ctx.reconstruct_record(bytes(bad))
+
+
+@pytest.mark.parametrize("M,N,C,F", [(1080, 1920, 3, 5), (97, 178, 3, 9), (2600, 1700, 1, 1)])
+def test_pageable_staging_matches_pinned(ctx, M, N, C, F):
+    """Pageable host buffers go through pinned staging filled / drained by host
+    threads (in the device row pitch, e.g. 178 x 3 = 534-byte rows); pinned ones
+    DMA directly. Every input/output combination gives the same bytes."""
+    rng = np.random.default_rng(M + N + F)
+    pageable = rng.integers(0, 256, (F, M, N, C), np.uint8)
+    pinned = dp.pinned_empty(pageable.shape)
+    pinned[...] = pageable
+    masks = (rng.random((F, M, N)) < 0.5).astype(np.uint8)
+    p = dp.make_privacy_params(0.5, 16, 16, 4)
+    pu = dp.make_privacy_params(0.5, 16, 16, 1)
+    seeds = dp.plane_seeds(3, F, C)
+    res = []
+    for chunk in (0, 2):
+        ctx.set_chunk_frames(chunk)
+        for src in (pageable, pinned):
+            for dst in (None, dp.pinned_empty(pageable.shape)):
+                pl, im = ctx.pixelize_adaptive(src, masks, p, dp.NOISE_KEYED, seeds, out=dst)
+                im = im.copy()
+                m, um = ctx.pixelize_uniform(src, pu, dp.NOISE_KEYED, seeds, out=dst)
+                res.append((pl, im, m, um.copy()))
+    ctx.set_chunk_frames(0)
+    for r in res[1:]:
+        assert r[0] == res[0][0] and np.array_equal(r[1], res[0][1])
+        assert np.array_equal(r[2], res[0][2]) and np.array_equal(r[3], res[0][3])
+    if F <= 9 and M * N < 10**6:
+        rp, ri = _oracle_adaptive(pageable, masks, p, "keyed", seeds)
+        assert res[0][0] == rp and np.array_equal(res[0][1], ri)
+
+
+def test_metrics_staged_upload_pieces(ctx):
+    """Pageable metric inputs are uploaded in ~16 MB pinned pieces that cross
+    frame boundaries (24 MB here); pinned inputs go in one DMA. Same values."""
+    F, M, N = 4, 2000, 3001
+    rng = np.random.default_rng(8)
+    a = rng.integers(0, 256, (F, M, N, 1), np.uint8)
+    b = np.clip(a.astype(np.int16) + rng.integers(-9, 9, a.shape), 0, 255).astype(np.uint8)
+    m, s = ctx.metrics(a, b, "both")
+    pa, pb = dp.pinned_empty(a.shape), dp.pinned_empty(b.shape)
+    pa[...] = a
+    pb[...] = b
+    pm, ps = ctx.metrics(pa, pb, "both")
+    assert np.array_equal(m, pm) and np.array_equal(s, ps)
+    d = (a.astype(np.int64) - b.astype(np.int64)) ** 2
+    assert np.allclose(m, d.reshape(F, -1).sum(1) / (M * N), rtol=1e-15, atol=0)
+    assert m[3] == oracle.mse(a[3], b[3]) and s[3] == oracle.ssim(a[3, :, :, 0], b[3, :, :, 0])
