@@ -239,14 +239,32 @@ __device__ void mask_band_colsums(const ClassifyArgs& a, const uint8_t* mbase, i
   for (int x0 = threadIdx.x * 16; x0 < W; x0 += kClassifyThreads * 16) {
     uint32_t lo[4] = {0u, 0u, 0u, 0u}, hi[4] = {0u, 0u, 0u, 0u};
     const bool fast = vec && x0 + 16 <= g.N;
-#pragma unroll 4
-    for (int i = 0; i < g.b; ++i) {
+    if (fast) {
+      // 8 rows' loads in flight per thread before any of them is summed
+      for (int i0 = 0; i0 < g.b; i0 += 8) {
+        uint4 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          v[k] = make_uint4(0u, 0u, 0u, 0u);
+          if (i0 + k < g.b)
+            v[k] = __ldg(reinterpret_cast<const uint4*>(
+                mbase + static_cast<int64_t>(reflect_index(r * g.b + i0 + k, g.M)) * a.mpitch + x0));
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t w[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            lo[j] += w[j] & 0x00FF00FFu;
+            hi[j] += (w[j] >> 8) & 0x00FF00FFu;
+          }
+        }
+      }
+    }
+    for (int i = 0; i < (fast ? 0 : g.b); ++i) {
       const uint8_t* row = mbase + static_cast<int64_t>(reflect_index(r * g.b + i, g.M)) * a.mpitch;
       uint32_t w[4];
-      if (fast) {
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(row + x0));
-        w[0] = v.x, w[1] = v.y, w[2] = v.z, w[3] = v.w;
-      } else {
+      {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           uint32_t acc = 0;

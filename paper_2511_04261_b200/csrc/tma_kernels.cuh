@@ -185,6 +185,41 @@ __device__ __forceinline__ void accumulate_row(const uint8_t* row, uint32_t (&ac
   }
 }
 
+// Per-channel byte sums of the pixels selected by m (m[ch][q]: dp4a weights of
+// word q for channel ch) of one 4-px strip row: a subcell boundary inside the
+// strip (subcell sides that are not a multiple of 4 px).
+template <int C>
+__device__ __forceinline__ void accumulate_row_masked(const uint8_t* row,
+                                                      const uint32_t (&m)[C][C == 4 ? 4 : C],
+                                                      uint32_t (&acc)[C]) {
+  constexpr int NW = C == 4 ? 4 : C;
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(row);
+  uint32_t x[NW];
+#pragma unroll
+  for (int q = 0; q < NW; ++q) x[q] = w[q];
+#pragma unroll
+  for (int ch = 0; ch < C; ++ch) {
+    uint32_t s = 0;
+#pragma unroll
+    for (int q = 0; q < NW; ++q) s = __dp4a(x[q], m[ch][q], s);
+    acc[ch] += s;
+  }
+}
+
+// Strip words whose pixels [0, split) take va[] and the rest vb[].
+template <int C>
+__device__ __forceinline__ void pattern_words_split(const uint32_t (&va)[C], const uint32_t (&vb)[C],
+                                                    int split, uint32_t (&w)[C == 4 ? 4 : C]) {
+  constexpr int NW = C == 4 ? 4 : C;
+#pragma unroll
+  for (int q = 0; q < NW; ++q) w[q] = 0;
+#pragma unroll
+  for (int pos = 0; pos < 4 * C; ++pos) {
+    const int k = pos / C, ch = pos % C;
+    w[pos / 4] |= (k < split ? va[ch] : vb[ch]) << (8 * (pos % 4));
+  }
+}
+
 // Sum of squares of all bytes of one 4-px strip row (variance extension).
 template <int C>
 __device__ __forceinline__ uint32_t square_row(const uint8_t* row, uint32_t acc) {
@@ -279,6 +314,10 @@ __global__ void __launch_bounds__(kStatsThreads)
   constexpr int B = 4 * B4;
   constexpr int SB = B / NSUB;
   constexpr int SB4 = SB / 4;
+  // Subcell sides that are not a multiple of 4 px (b = 24 n = 4: 6 px): a
+  // strip can straddle two subcells; each lane splits its strip sums at the
+  // boundary and the subcell sums meet in per-warp smem (compact draw mode).
+  constexpr bool STR = (SB % 4) != 0;
   // Strips per warp: whole cells only (a cell is B4 adjacent lanes), so for
   // B4 not a power of two (b = 12, 24) the last 32 % B4 lanes of each warp
   // idle and the tile is 16 * LPW px (480 at b = 12 or 24) instead of 512.
@@ -286,7 +325,8 @@ __global__ void __launch_bounds__(kStatsThreads)
   constexpr int TILE = 4 * (kConsumers / 32) * LPW;
   constexpr int ROWB = TILE * C;
   constexpr uint32_t STAGE = B * ROWB;
-  static_assert(SB % 4 == 0 && B4 <= 32 && B4 % SB4 == 0, "fast-path geometry");
+  static_assert(B4 <= 32 && (STR ? (SB >= 4 && ADAPTIVE && !VAR && !PACKED) : B4 % SB4 == 0),
+                "fast-path geometry");
   static_assert(TILE == kTilePx || !PACKED, "packed slots use 512-px tiles");
   static_assert(!VAR || (ADAPTIVE && !PACKED), "variance staging: wide adaptive frames only");
 
@@ -390,16 +430,32 @@ __global__ void __launch_bounds__(kStatsThreads)
   // Per-warp complex-draw tables (see the complex-cell block below).
   constexpr int CPW = 32 / B4;           // cells per consumer warp
   constexpr int NN = NSUB * NSUB;
-  using SumT = typename std::conditional<(SB * SB * 255 < 65536), uint16_t, uint32_t>::type;
+  using SumT = typename std::conditional<(SB * SB * 255 < 65536 && !STR), uint16_t, uint32_t>::type;
+  constexpr bool TABLES = VAR || STR;
   struct CellRec {
     int cw, f, cell, gidx;
     int64_t off;
   };
-  __shared__ SumT csum[VAR ? kConsumers / 32 : 1][VAR ? CPW : 1][VAR ? NN * C : 1];
-  __shared__ CellRec crec[VAR ? kConsumers / 32 : 1][VAR ? CPW : 1];
-  __shared__ uint64_t cstate[VAR ? kConsumers / 32 : 1][VAR ? CPW : 1][C];
-  const int wq = VAR ? (t >> 5) : 0;          // consumer warp
-  const int cw = VAR ? ((t & 31) / B4) : 0;   // cell within the warp
+  __shared__ SumT csum[TABLES ? kConsumers / 32 : 1][TABLES ? CPW : 1][TABLES ? NN * C : 1];
+  __shared__ CellRec crec[TABLES ? kConsumers / 32 : 1][TABLES ? CPW : 1];
+  __shared__ uint64_t cstate[TABLES ? kConsumers / 32 : 1][TABLES ? CPW : 1][C];
+  const int wq = TABLES ? (t >> 5) : 0;          // consumer warp
+  const int cw = TABLES ? ((t & 31) / B4) : 0;   // cell within the warp
+  // STR: this strip's first subcell column, the pixels [0, split) in it, and
+  // the dp4a weights selecting those pixels per channel.
+  const int str_px = 4 * (sx % B4);
+  const int str_sa = STR ? str_px / SB : 0;
+  const int str_split = STR ? min(4, (str_sa + 1) * SB - str_px) : 4;
+  uint32_t str_m[C][C == 4 ? 4 : C];
+#pragma unroll
+  for (int ch = 0; ch < C; ++ch)
+#pragma unroll
+    for (int q = 0; q < (C == 4 ? 4 : C); ++q) str_m[ch][q] = 0;
+  if constexpr (STR) {
+#pragma unroll
+    for (int pos = 0; pos < 4 * C; ++pos)
+      if (pos / C < str_split) str_m[pos % C][pos / 4] |= 1u << (8 * (pos % 4));
+  }
   if (PACKED) {
     const int v0 = g.N * C, pad = (g.GC * B - g.N) * C;
     for (int x = t; x < pad && x < 128; x += kConsumers) {
@@ -548,10 +604,16 @@ __global__ void __launch_bounds__(kStatsThreads)
       // smem table and the warp's complex draws (cells x n*n x C) are dealt
       // round-robin to all 32 lanes, so the lanes of simple cells do not idle
       // through the serial draws (tools/k1_complex_sweep.py measures both).
-      constexpr bool compact = VAR;
+      constexpr bool compact = VAR || STR;
       const bool cx = active && !simple;
       const unsigned cx_any = __ballot_sync(0xFFFFFFFFu, cx);
       __syncwarp();  // the previous unit's reads of this warp's tables are done
+      if constexpr (STR) {
+        if (cx_any) {  // subcell sums accumulate with smem atomics
+          for (int i = t & 31; i < CPW * NN * C; i += 32) (&csum[wq][0][0])[i] = 0;
+          __syncwarp();
+        }
+      }
       if (!VAR || cx_any) {
 #pragma unroll 1
         for (int vs = 0; vs < NSUB; ++vs) {
@@ -564,7 +626,24 @@ __global__ void __launch_bounds__(kStatsThreads)
 #pragma unroll
             for (int ch = 0; ch < C; ++ch) tot[ch] += acc[ch];
           }
-          if (cx_any) {
+          if constexpr (STR) {
+            if (cx_any) {
+              uint32_t part[C];
+#pragma unroll
+              for (int ch = 0; ch < C; ++ch) part[ch] = 0;
+#pragma unroll
+              for (int i = 0; i < SB; ++i)
+                accumulate_row_masked<C>(mystrip + (vs * SB + i) * srb, str_m, part);
+              if (cx) {
+                SumT* cs0 = &csum[wq][cw][(vs * NSUB + str_sa) * C];
+#pragma unroll
+                for (int ch = 0; ch < C; ++ch) {
+                  atomicAdd(cs0 + ch, part[ch]);
+                  if (str_split < 4) atomicAdd(cs0 + C + ch, acc[ch] - part[ch]);
+                }
+              }
+            }
+          } else if (cx_any) {
 #pragma unroll
             for (int ch = 0; ch < C; ++ch) acc[ch] = group_sum<SB4>(acc[ch]);
             if constexpr (compact) {
@@ -637,10 +716,21 @@ __global__ void __launch_bounds__(kStatsThreads)
 #pragma unroll 1
           for (int vs = 0; vs < NSUB; ++vs) {
             uint32_t val[C];
-#pragma unroll
-            for (int ch = 0; ch < C; ++ch) val[ch] = csum[wq][cw][(vs * NSUB + sc) * C + ch];
             uint32_t w[C];
-            pattern_words<C>(val, w);
+            if constexpr (STR) {
+              uint32_t vb[C];
+              const SumT* cs0 = &csum[wq][cw][(vs * NSUB + str_sa) * C];
+#pragma unroll
+              for (int ch = 0; ch < C; ++ch) {
+                val[ch] = cs0[ch];
+                vb[ch] = str_split < 4 ? cs0[C + ch] : val[ch];
+              }
+              pattern_words_split<C>(val, vb, str_split, w);
+            } else {
+#pragma unroll
+              for (int ch = 0; ch < C; ++ch) val[ch] = csum[wq][cw][(vs * NSUB + sc) * C + ch];
+              pattern_words<C>(val, w);
+            }
 #pragma unroll
             for (int i = 0; i < SB; ++i)
 #pragma unroll
@@ -844,6 +934,13 @@ StatsKernel pick_b(int b, int n) {
       DPPX_CASE(16, 4)
       DPPX_CASE(16, 8)
       DPPX_CASE(16, 16)
+      // subcell sides that are not a multiple of 4 px (STR: split strips)
+      DPPX_CASE(3, 2)
+      DPPX_CASE(5, 2)
+      DPPX_CASE(5, 4)
+      DPPX_CASE(6, 4)
+      DPPX_CASE(10, 4)
+      DPPX_CASE(10, 8)
     }
   }
 #undef DPPX_CASE
