@@ -614,7 +614,59 @@ __global__ void __launch_bounds__(kStatsThreads)
           __syncwarp();
         }
       }
-      if (!VAR || cx_any) {
+      // Direct mode with many vertical subcells (NSUB >= 8): two at a time, so
+      // the two subcells' draw chains overlap (a store of one subcell's pattern
+      // would otherwise order the next subcell's smem reads behind its draws).
+      constexpr bool PAIRS = !compact && NSUB >= 8 && NSUB % 2 == 0;
+      if constexpr (PAIRS) {
+#pragma unroll 1
+        for (int vs = 0; vs < NSUB; vs += 2) {
+          uint32_t acc0[C], acc1[C];
+#pragma unroll
+          for (int ch = 0; ch < C; ++ch) acc0[ch] = acc1[ch] = 0;
+#pragma unroll
+          for (int i = 0; i < SB; ++i) {
+            accumulate_row<C>(mystrip + (vs * SB + i) * srb, acc0);
+            accumulate_row<C>(mystrip + ((vs + 1) * SB + i) * srb, acc1);
+          }
+#pragma unroll
+          for (int ch = 0; ch < C; ++ch) tot[ch] += acc0[ch] + acc1[ch];
+          if (cx_any) {
+#pragma unroll
+            for (int ch = 0; ch < C; ++ch) {
+              acc0[ch] = group_sum<SB4>(acc0[ch]);
+              acc1[ch] = group_sum<SB4>(acc1[ch]);
+            }
+            uint32_t val0[C], val1[C];
+            group_values<C, SB4>(a, env_sub, cx, acc0, cs, f, p.r, cell, vs, sc, val0);
+            group_values<C, SB4>(a, env_sub, cx, acc1, cs, f, p.r, cell, vs + 1, sc, val1);
+            if (cx) {
+              if (lic % SB4 == 0) {
+                const int64_t off = stat_offset(a, false, gidx, slot_s, S_tot, vs, sc);
+#pragma unroll
+                for (int ch = 0; ch < C; ++ch) {
+                  a.stats[static_cast<int64_t>(f * C + ch) * a.sstride + off] = static_cast<uint8_t>(val0[ch]);
+                  a.stats[static_cast<int64_t>(f * C + ch) * a.sstride + off + NSUB] =
+                      static_cast<uint8_t>(val1[ch]);
+                }
+              }
+              if (emit) {
+                uint32_t w0[C], w1[C];
+                pattern_words<C>(val0, w0);
+                pattern_words<C>(val1, w1);
+#pragma unroll
+                for (int i = 0; i < SB; ++i)
+#pragma unroll
+                  for (int q = 0; q < C; ++q) {
+                    reinterpret_cast<uint32_t*>(mystrip + (vs * SB + i) * srb)[q] = w0[q];
+                    reinterpret_cast<uint32_t*>(mystrip + ((vs + 1) * SB + i) * srb)[q] = w1[q];
+                  }
+              }
+            }
+          }
+        }
+      }
+      if (!PAIRS && (!VAR || cx_any)) {
 #pragma unroll 1
         for (int vs = 0; vs < NSUB; ++vs) {
           uint32_t acc[C];
@@ -697,19 +749,60 @@ __global__ void __launch_bounds__(kStatsThreads)
         }
         __syncwarp();
         const int work = __popc(leaders) * NN * C;
-        for (int i = t & 31; i < work; i += 32) {
-          const int kk = i / (NN * C), rem = i - kk * (NN * C);
-          const int sidx = rem / C, ch = rem - sidx * C;
-          const int vs = sidx / NSUB, sc2 = sidx - vs * NSUB;
-          const CellRec& rec = crec[wq][kk];
-          const uint32_t sum = csum[wq][rec.cw][rem];
-          const uint32_t v =
-              quantize_stat(env_sub, sum, draw_bits(a, cstate[wq][kk][ch], rec.f, ch, p.r, rec.cell, vs, sc2),
-                            inj_at(a, rec.f, ch, rec.gidx, vs, sc2));
-          uint8_t* base = VAR ? a.stage + static_cast<int64_t>(rec.f * C + ch) * a.stage_stride
-                              : a.stats + static_cast<int64_t>(rec.f * C + ch) * a.sstride;
-          base[rec.off + sidx] = static_cast<uint8_t>(v);
-          csum[wq][rec.cw][rem] = static_cast<SumT>(v);
+        // Keyed stream, bounded fast path: batches of kBatch draws per lane with
+        // no calls in the first phase (sums, keys and f32 estimates of all
+        // kBatch draws are independent chains the scheduler interleaves; the
+        // K1 CTAs run few warps, so one draw at a time is latency-bound), then
+        // the rare exact draws and the stores.
+        // (Not for VAR: measured slower there, its kernel is register-bound.)
+        const bool keyed_fast = !VAR && !env_sub.exact_only && a.noise.kind == DPPX_NOISE_KEYED;
+        constexpr int kBatch = 4;
+        if (keyed_fast) {
+          for (int i0 = 0; i0 < work; i0 += 32 * kBatch) {
+            uint32_t sum[kBatch], q[kBatch];
+            uint64_t bits[kBatch];
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+              const int i = min(i0 + j * 32 + (t & 31), work - 1);  // clamped: always valid
+              const int kk = i / (NN * C), rem = i - kk * (NN * C);
+              const int sidx = rem / C, ch = rem - sidx * C;
+              const int vs = sidx / NSUB, sc2 = sidx - vs * NSUB;
+              sum[j] = csum[wq][crec[wq][kk].cw][rem];
+              bits[j] = key_sub(cstate[wq][kk][ch], vs, sc2);
+              q[j] = fast_quantize(sum[j], env_sub.inv_area, bits[j], env_sub.sigmaf, env_sub.margin);
+            }
+            __syncwarp();  // all of the batch's sums are read before any is overwritten
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+              const int i = i0 + j * 32 + (t & 31);
+              if (i < work) {
+                const int kk = i / (NN * C), rem = i - kk * (NN * C);
+                const int sidx = rem / C, ch = rem - sidx * C;
+                const CellRec& rec = crec[wq][kk];
+                uint32_t v = q[j];
+                if (v == 0xFFFFFFFFu) v = exact_quantize(sum[j], env_sub.area, env_sub.kind, bits[j], env_sub.sigma, 0.0);
+                uint8_t* base = VAR ? a.stage + static_cast<int64_t>(rec.f * C + ch) * a.stage_stride
+                                    : a.stats + static_cast<int64_t>(rec.f * C + ch) * a.sstride;
+                base[rec.off + sidx] = static_cast<uint8_t>(v);
+                csum[wq][rec.cw][rem] = static_cast<SumT>(v);
+              }
+            }
+          }
+        } else {
+          for (int i = t & 31; i < work; i += 32) {
+            const int kk = i / (NN * C), rem = i - kk * (NN * C);
+            const int sidx = rem / C, ch = rem - sidx * C;
+            const int vs = sidx / NSUB, sc2 = sidx - vs * NSUB;
+            const CellRec& rec = crec[wq][kk];
+            const uint32_t sum = csum[wq][rec.cw][rem];
+            const uint32_t v =
+                quantize_stat(env_sub, sum, draw_bits(a, cstate[wq][kk][ch], rec.f, ch, p.r, rec.cell, vs, sc2),
+                              inj_at(a, rec.f, ch, rec.gidx, vs, sc2));
+            uint8_t* base = VAR ? a.stage + static_cast<int64_t>(rec.f * C + ch) * a.stage_stride
+                                : a.stats + static_cast<int64_t>(rec.f * C + ch) * a.sstride;
+            base[rec.off + sidx] = static_cast<uint8_t>(v);
+            csum[wq][rec.cw][rem] = static_cast<SumT>(v);
+          }
         }
         __syncwarp();
         if (emit && cx) {
