@@ -314,8 +314,8 @@ __global__ void __launch_bounds__(kStatsThreads)
   constexpr int B = 4 * B4;
   constexpr int SB = B / NSUB;
   constexpr int SB4 = SB / 4;
-  // Subcell sides that are not a multiple of 4 px (b = 24 n = 4: 6 px): a
-  // strip can straddle two subcells; each lane splits its strip sums at the
+  // Subcell sides that are not a multiple of 4 px (b = 24 n = 4: 6 px; 2 or
+  // 3 px): a strip can straddle two subcells; each lane splits its strip sums at the
   // boundary and the subcell sums meet in per-warp smem (compact draw mode).
   constexpr bool STR = (SB % 4) != 0;
   // Strips per warp: whole cells only (a cell is B4 adjacent lanes), so for
@@ -325,7 +325,8 @@ __global__ void __launch_bounds__(kStatsThreads)
   constexpr int TILE = 4 * (kConsumers / 32) * LPW;
   constexpr int ROWB = TILE * C;
   constexpr uint32_t STAGE = B * ROWB;
-  static_assert(B4 <= 32 && (STR ? (SB >= 4 && ADAPTIVE && !VAR && !PACKED) : B4 % SB4 == 0),
+  // (SB >= 2: a strip meets at most two subcells.)
+  static_assert(B4 <= 32 && (STR ? (SB >= 2 && ADAPTIVE && !VAR && !PACKED) : B4 % SB4 == 0),
                 "fast-path geometry");
   static_assert(TILE == kTilePx || !PACKED, "packed slots use 512-px tiles");
   static_assert(!VAR || (ADAPTIVE && !PACKED), "variance staging: wide adaptive frames only");
@@ -892,6 +893,8 @@ template <int C, int B4, int NSUB, bool ADAPTIVE, bool PACKED>
 __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
     k_expand_tma(const __grid_constant__ CUtensorMap tm_out, const ExpandArgs a) {
   constexpr int B = 4 * B4, SB = B / NSUB, SB4 = SB / 4;
+  constexpr bool STR = (SB % 4) != 0;  // strips meet two subcells (as K1)
+  static_assert(!STR || (ADAPTIVE && !PACKED && SB >= 2), "split strips: wide adaptive frames");
   constexpr int LPW = (32 / B4) * B4;                    // whole cells per warp (as K1)
   constexpr int NT = PACKED ? kExpandPackedThreads : kConsumers;
   constexpr int TILE = 4 * (NT / 32) * LPW;
@@ -908,7 +911,10 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
   const int jj = in_slot ? my_j : 0;
   const int lpx = 4 * sx - jj * slot_px;
   const int srb = slot_px * C;  // smem bytes per slot row
-  const int sc = (sx % B4) / SB4;
+  const int sc = STR ? 0 : (sx % B4) / SB4;
+  const int str_px = 4 * (sx % B4);
+  const int str_sa = STR ? str_px / SB : 0;
+  const int str_split = STR ? min(4, (str_sa + 1) * SB - str_px) : 4;
   for (int u = blockIdx.x, k = 0; u < a.units; u += gridDim.x, ++k) {
     uint8_t* buf = smem;
     // A capped grid loops: the previous unit's store must have read the tile.
@@ -927,6 +933,7 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
     const bool active = in_slot && jj < nf && cell < g.GC;
     const int gidx = r * g.GC + cell;
     uint32_t val[NSUB][C];
+    uint32_t valb[STR ? NSUB : 1][C];  // STR: the strip's second subcell
     if (active) {
 #pragma unroll
       for (int ch = 0; ch < C; ++ch) {
@@ -943,12 +950,22 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
           if (info & 1u) {
             const uint32_t v = __ldg(st + base + slot_s);
 #pragma unroll
-            for (int vs = 0; vs < NSUB; ++vs) val[vs][ch] = v;
+            for (int vs = 0; vs < NSUB; ++vs) {
+              val[vs][ch] = v;
+              if constexpr (STR) valb[vs][ch] = v;
+            }
           } else {
             const uint8_t* sub = st + base + __ldg(&a.totals[plane]) +
                                  static_cast<int64_t>(static_cast<uint32_t>(gidx) - slot_s) * NSUB * NSUB;
 #pragma unroll
-            for (int vs = 0; vs < NSUB; ++vs) val[vs][ch] = __ldg(sub + vs * NSUB + sc);
+            for (int vs = 0; vs < NSUB; ++vs) {
+              if constexpr (STR) {
+                val[vs][ch] = __ldg(sub + vs * NSUB + str_sa);
+                valb[vs][ch] = str_split < 4 ? __ldg(sub + vs * NSUB + str_sa + 1) : val[vs][ch];
+              } else {
+                val[vs][ch] = __ldg(sub + vs * NSUB + sc);
+              }
+            }
           }
         }
       }
@@ -956,7 +973,10 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
 #pragma unroll
       for (int vs = 0; vs < NSUB; ++vs) {
         uint32_t w[C];
-        pattern_words<C>(val[vs], w);
+        if constexpr (STR)
+          pattern_words_split<C>(val[vs], valb[vs], str_split, w);
+        else
+          pattern_words<C>(val[vs], w);
 #pragma unroll
         for (int i = 0; i < SB; ++i)
 #pragma unroll
@@ -1034,6 +1054,10 @@ StatsKernel pick_b(int b, int n) {
       DPPX_CASE(6, 4)
       DPPX_CASE(10, 4)
       DPPX_CASE(10, 8)
+      DPPX_CASE(2, 4)   // subcells of 2 or 3 px
+      DPPX_CASE(3, 4)
+      DPPX_CASE(4, 8)
+      DPPX_CASE(6, 8)
     }
   }
 #undef DPPX_CASE
@@ -1081,6 +1105,12 @@ ExpandKernel pick_expand(int b, int n) {
       DPPX_CASE(16, 4)
       DPPX_CASE(16, 8)
       DPPX_CASE(16, 16)
+      // split strips, subcells of 2 or 3 px (K2r measured faster for the
+      // 5, 6 and 10 px subcells: 0.84-0.92 vs 0.69-0.79 of HBM)
+      DPPX_CASE(2, 4)
+      DPPX_CASE(3, 4)
+      DPPX_CASE(4, 8)
+      DPPX_CASE(6, 8)
     }
   }
   if constexpr (AD) {

@@ -717,7 +717,8 @@ def test_metrics_staged_upload_pieces(ctx):
 
 
 @pytest.mark.parametrize("C", [1, 3])
-@pytest.mark.parametrize("b,n", [(12, 2), (20, 2), (20, 4), (24, 4), (40, 4), (40, 8)])
+@pytest.mark.parametrize("b,n", [(12, 2), (20, 2), (20, 4), (24, 4), (40, 4), (40, 8), (8, 4), (12, 4),
+                                 (16, 8), (24, 8)])
 def test_straddling_subcells_on_tma_path(ctx, C, b, n):
     """Subcell sides that are not a multiple of 4 px (6, 10, 5): K1's 4-px
     strips straddle subcell boundaries, lanes split their sums and the subcell
@@ -737,6 +738,8 @@ def test_straddling_subcells_on_tma_path(ctx, C, b, n):
             assert ctx.stats()["launches"]["stats_tma"] >= 1
         rp, ri = _oracle_adaptive(frames, masks, p, "keyed", seeds)
         assert pls == rp and np.array_equal(img, ri), (M, N)
+        # K2 (split strips too) rebuilds the same image from the payloads
+        assert np.array_equal(ctx.reassemble(pls, M, N, b, n, channels=C, frames=F), ri), (M, N)
         G = dp.grid_dims(M, N, b).grid_count()
         inj = rng.laplace(0, 30, (F * C, G * n * n))
         pls, img = ctx.pixelize_adaptive(frames, masks, p, dp.NOISE_INJECTED, None, injected=inj)
