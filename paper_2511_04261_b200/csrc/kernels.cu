@@ -590,8 +590,12 @@ __device__ void rows_emit(const BatchGeom& g, int r, uint8_t* out_frame, int64_t
   }
 }
 
-template <int C, bool ADAPTIVE, bool VEC16>
+// CW: bytes per column chunk (16, or 8 when 16-byte chunks would leave the
+// CTA's last pass mostly idle: 5775-byte padded rows = 361 chunks of 16 over
+// 256 threads, the load phase then ends at a barrier half the block waits at).
+template <int C, bool ADAPTIVE, bool VEC16, int CW>
 __global__ void __launch_bounds__(kRowThreads, 4) k_stats_rows(const StatsArgs a) {
+  constexpr int NW = CW / 4;
   extern __shared__ __align__(16) uint8_t rsm[];
   const BatchGeom& g = a.g;
   const RowSmem L = row_smem_layout(g);
@@ -638,24 +642,31 @@ __global__ void __launch_bounds__(kRowThreads, 4) k_stats_rows(const StatsArgs a
       // of one chunk at a time (8 live SWAR counters, flushed per vertical
       // subcell; rows unrolled so several loads are in flight); a warp reads
       // 512 contiguous bytes per row.
-      for (int x0 = t * 16; x0 < PB; x0 += kRowThreads * 16) {
+      for (int x0 = t * CW; x0 < PB; x0 += kRowThreads * CW) {
         const uint8_t* colp = frame + x0;
-        const bool fast = VEC16 && x0 + 16 <= RB;
+        const bool fast = VEC16 && x0 + CW <= RB;
         for (int vg = 0; vg < nv; ++vg) {
-          uint32_t lo[4] = {0u, 0u, 0u, 0u}, hi[4] = {0u, 0u, 0u, 0u};
+          uint32_t lo[NW], hi[NW];
+#pragma unroll
+          for (int j = 0; j < NW; ++j) lo[j] = hi[j] = 0u;
           const int row0 = r * g.b + (v0 + vg) * g.sb;
 #pragma unroll 4
           for (int i = 0; i < g.sb; ++i) {
             const int srow = reflect_index(row0 + i, g.M);
             const uint8_t* rowp = colp + static_cast<int64_t>(srow) * a.pitch;
-            uint32_t w[4];
+            uint32_t w[NW];
             if (fast) {
-              const uint4 v = __ldg(reinterpret_cast<const uint4*>(rowp));
-              w[0] = v.x, w[1] = v.y, w[2] = v.z, w[3] = v.w;
+              if constexpr (CW == 16) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(rowp));
+                w[0] = v.x, w[1] = v.y, w[2] = v.z, w[3] = v.w;
+              } else {
+                const uint2 v = __ldg(reinterpret_cast<const uint2*>(rowp));
+                w[0] = v.x, w[1] = v.y;
+              }
             } else {
               const uint8_t* rowbase = rowp - x0;
 #pragma unroll
-              for (int j = 0; j < 4; ++j) {
+              for (int j = 0; j < NW; ++j) {
                 uint32_t acc = 0;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
@@ -673,14 +684,14 @@ __global__ void __launch_bounds__(kRowThreads, 4) k_stats_rows(const StatsArgs a
               }
             }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < NW; ++j) {
               lo[j] += w[j] & 0x00FF00FFu;
               hi[j] += (w[j] >> 8) & 0x00FF00FFu;
             }
           }
           uint16_t* vrow = vsum + vg * PB;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
+          for (int j = 0; j < NW; ++j) {
             const int x = x0 + 4 * j;
             if (x + 0 < PB) vrow[x + 0] = static_cast<uint16_t>(lo[j] & 0xFFFFu);
             if (x + 1 < PB) vrow[x + 1] = static_cast<uint16_t>(hi[j] & 0xFFFFu);
@@ -1199,16 +1210,34 @@ int rows_smem_bytes(const BatchGeom& g) {
   return L.total <= 200 * 1024 ? L.total : 0;
 }
 
-template <int C>
-cudaError_t launch_rows_c(const StatsArgs& a, size_t smem, bool vec16, cudaStream_t s) {
-  auto k = a.adaptive ? (vec16 ? k_stats_rows<C, true, true> : k_stats_rows<C, true, false>)
-                      : (vec16 ? k_stats_rows<C, false, true> : k_stats_rows<C, false, false>);
+template <int C, int CW>
+cudaError_t launch_rows_cw(const StatsArgs& a, size_t smem, bool vec16, cudaStream_t s) {
+  auto k = a.adaptive ? (vec16 ? k_stats_rows<C, true, true, CW> : k_stats_rows<C, true, false, CW>)
+                      : (vec16 ? k_stats_rows<C, false, true, CW> : k_stats_rows<C, false, false, CW>);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const int grid = a.units < 0x7FFFFFFF ? a.units : 0x7FFFFFFF;
   k<<<grid, kRowThreads, smem, s>>>(a);
   return cudaGetLastError();
+}
+
+// Busy fraction of the CTA's column-chunk passes for chunk width cw.
+inline double rows_chunk_balance(int pb, int cw) {
+  const int chunks = (pb + cw - 1) / cw;
+  const int passes = (chunks + kRowThreads - 1) / kRowThreads;
+  return static_cast<double>(chunks) / (static_cast<double>(passes) * kRowThreads);
+}
+
+template <int C>
+cudaError_t launch_rows_c(const StatsArgs& a, size_t smem, bool vec16, cudaStream_t s) {
+  // Measured (tools/b_sweep.py uniform, 1080p RGB): 8-byte chunks win only when
+  // the row has mirrored padding columns (b = 7, 9, 11, 13, 14, 17-19: 5-11 %
+  // faster) and lose 10-14 % on unpadded rows (b = 6, 10, 15, 30, 128).
+  const int pb = a.g.GC * a.g.b * C;
+  if (pb != a.g.N * C && rows_chunk_balance(pb, 8) > rows_chunk_balance(pb, 16) + 0.15)
+    return launch_rows_cw<C, 8>(a, smem, vec16, s);
+  return launch_rows_cw<C, 16>(a, smem, vec16, s);
 }
 
 cudaError_t launch_stats_rows(const StatsArgs& a, size_t smem, cudaStream_t s) {

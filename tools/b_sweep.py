@@ -1,7 +1,8 @@
 #!/usr/bin/env python3
 """K1 time and roofline fraction across grid sizes the paper recommends
 (PAPER.md: b = 8, 12, 16, 24 for PETS; 12, 24, 30, 40 for Venice-2; up to
-b = 128, n <= 128 for PPM-100), device-resident 1080p RGB, 120 frames."""
+b = 128, n <= 128 for PPM-100), device-resident 1080p RGB, 120 frames.
+usage: b_sweep.py [frames] [uniform]   (uniform: b = 2..20, 30, 128 with n = 1)"""
 import json
 import os
 import sys
@@ -19,6 +20,9 @@ def main():
 
     import paper_2511_04261_b200 as dp
     F, M, N, C = int(sys.argv[1]) if len(sys.argv) > 1 else 120, 1080, 1920, 3
+    cases = CASES
+    if len(sys.argv) > 2 and sys.argv[2] == "uniform":  # the paper's b = 2..20 sweep (+ 30, 128)
+        cases = [(b, 1) for b in list(range(2, 21)) + [30, 128]]
     dev = torch.device("cuda:0")
     ctx = dp.Context(0)
     img = torch.empty((F, M, N * C), dtype=torch.uint8, device=dev)
@@ -29,7 +33,7 @@ def main():
     nz, keep = dp.Context._noise(dp.NOISE_KEYED, dp.plane_seeds(42, F, C))
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
     rows = []
-    for b, n in CASES:
+    for b, n in cases:
         p = dp.make_privacy_params(0.5, 16, b, n)
         G = dp.grid_dims(M, N, b).grid_count()
         adaptive = n > 1
