@@ -482,7 +482,7 @@ int run_stats(dppx_ctx* ctx, StatsArgs& a) {
   // fill), so no row tail has to be gathered from global memory.
   const int64_t in_row = a.row_slack ? round_up(row_bytes, 8) : row_bytes / 8 * 8;
   bool maps = k && aligned && g.F > 0 && box_bytes / 8 <= 256 && g.b <= 256 &&
-              static_cast<int64_t>(a.pack) * a.slot_stride <= stage_bytes &&
+              (a.pack == 1 || static_cast<int64_t>(a.pack) * a.slot_stride <= stage_bytes) &&
               encode_frames_map(&tin, a.img, in_row, g.M, g.F, a.pitch, a.fstride, box_bytes, g.b);
   if (maps && a.out)
     maps = encode_frames_map(&tout, a.out, row_bytes, g.M, g.F, a.opitch, a.ofstride, box_bytes, g.b);
@@ -497,7 +497,8 @@ int run_stats(dppx_ctx* ctx, StatsArgs& a) {
     a.units = static_cast<int>(units);
     a.div_tiles = make_fastdiv(static_cast<uint32_t>(a.tiles_per_row));
     a.div_rows = make_fastdiv(static_cast<uint32_t>(a.row_count));
-    const size_t stage = static_cast<size_t>(g.b) * tile * g.C;
+    // (128-byte aligned stages: equal to b * tile * C for every b % 4 == 0 kernel)
+    const size_t stage = static_cast<size_t>(round_up(static_cast<int64_t>(g.b) * tile * g.C, 128));
     // Two stages: measured best for every shape on B200 (a 2-deep ring per CTA
     // with 4 CTAs/SM at b = 16 beats 3-4 deep rings with fewer CTAs; see
     // profiles/r01_stage_sweep.md).

@@ -880,6 +880,198 @@ __global__ void __launch_bounds__(kStatsThreads)
 }
 
 // ============================================================================
+// K1u: uniform pixelization (n = 1) for grid sides that are not a multiple of
+// 4 px (the paper's b = 2..20 sweep, b = 30 for Venice-2). Same producer (TMA
+// box loads / stores, 2-stage ring, dynamic unit claims) as K1; tiles are whole
+// cells and a multiple of 16 px (TILE = lcm(b, 16) * k <= 512). A consumer's
+// 4-px strip meets at most two cells (b >= 2): it splits its per-channel row
+// sums at the cell boundary (dp4a byte masks), both parts meet in a per-CTA
+// smem cell table (shared-memory atomics), one thread per (cell, channel)
+// draws, and each strip writes its reconstructed pixels from the table.
+// ============================================================================
+constexpr int ku_gcd(int x, int y) { return y == 0 ? x : ku_gcd(y, x % y); }
+constexpr int ku_tile(int b) { return (b * 16 / ku_gcd(b, 16)) * (512 / (b * 16 / ku_gcd(b, 16))); }
+
+template <int C, int B>
+__global__ void __launch_bounds__(kStatsThreads)
+    k_uniform_tma(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
+                  const StatsArgs a) {
+  constexpr int TILE = ku_tile(B);
+  constexpr int ROWB = TILE * C;
+  constexpr uint32_t STAGE = (B * ROWB + 127) & ~127;  // TMA destinations: 128-byte aligned
+  constexpr int NCELL = TILE / B;  // cells per tile
+  constexpr int NSTRIP = TILE / 4;
+  static_assert(B >= 2 && B % 4 != 0 && TILE % B == 0 && TILE % 16 == 0 && NSTRIP <= kConsumers,
+                "K1u geometry");
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full_bar[kMaxStages];
+  __shared__ __align__(8) uint64_t id_bar[kMaxStages];
+  __shared__ __align__(8) uint64_t done_bar[kMaxStages];
+  __shared__ int stage_unit[kMaxStages];
+  __shared__ uint32_t cellsum[NCELL * C];
+  __shared__ uint8_t cellval[NCELL * C];
+
+  const int S = a.stages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&id_bar[s], 1);
+      mbar_init(&done_bar[s], kConsumers);
+    }
+    fence_mbarrier_init();
+  }
+  for (int i = threadIdx.x; i < NCELL * C; i += blockDim.x) cellsum[i] = 0;
+  __syncthreads();
+
+  if (warp == kConsumers / 32) {  // producer warp, as in k_stats_tma
+    if (lane == 0) {
+      prefetch_tmap(&tm_in);
+      prefetch_tmap(&tm_out);
+    }
+    auto finish_unit = [&](int s, int use) {
+      mbar_wait(&done_bar[s], use & 1);
+      if (a.out) {
+        const int uu = stage_unit[s];
+        store_tail<C, B, false, TILE>(a, uu, smem + s * STAGE, lane);
+        if (lane == 0) store_unit<C, B, false, TILE>(a, &tm_out, uu, smem + s * STAGE);
+      }
+      __syncwarp();
+    };
+    int k = 0, done_units = 0;
+    for (;; ++k) {
+      const int s = k % S;
+      if (k >= S) {
+        finish_unit(s, (k / S) - 1);
+        ++done_units;
+      }
+      int u = 0;
+      if (lane == 0) {
+        u = atomicAdd(a.work_counter, 1);
+        if (u >= a.units) {
+          if (u == a.units + static_cast<int>(gridDim.x) - 1) atomicExch(a.work_counter, 0);
+          u = -1;
+        }
+        stage_unit[s] = u;
+        mbar_arrive(&id_bar[s]);
+        if (u < 0)
+          mbar_arrive_expect_tx(&full_bar[s], 0);
+        else
+          load_unit<C, B, false, TILE>(a, &tm_in, u, smem + s * STAGE, &full_bar[s]);
+      }
+      u = __shfl_sync(0xFFFFFFFFu, u, 0);
+      if (u < 0) break;
+    }
+    for (int j = done_units; j < k; ++j) finish_unit(j % S, j / S);
+    if (lane == 0) bulk_wait_all();
+    return;
+  }
+
+  // ---------------- consumer warps ----------------
+  const int t = threadIdx.x;
+  const BatchGeom& g = a.g;
+  const DrawEnv env_cell = make_env(a.noise.kind, a.exact_noise != 0, a.area, a.sigma);
+  const bool strip_ok = t < NSTRIP;
+  const int lpx = 4 * (strip_ok ? t : 0);
+  const int ca = lpx / B;                          // first cell of the strip (in the tile)
+  const int split = min(4, (ca + 1) * B - lpx);    // pixels [0, split) are in cell ca
+  uint32_t m[C][C == 4 ? 4 : C];
+#pragma unroll
+  for (int ch = 0; ch < C; ++ch)
+#pragma unroll
+    for (int q = 0; q < (C == 4 ? 4 : C); ++q) m[ch][q] = 0;
+#pragma unroll
+  for (int pos = 0; pos < 4 * C; ++pos)
+    if (pos / C < split) m[pos % C][pos / 4] |= 1u << (8 * (pos % 4));
+
+  for (int k = 0;; ++k) {
+    const int s = k % S;
+    uint8_t* st = smem + s * STAGE;
+    mbar_wait(&id_bar[s], (k / S) & 1);
+    const int u = *reinterpret_cast<volatile int*>(&stage_unit[s]);
+    if (u < 0) break;
+    const UnitPos p = decode_unit<false, TILE>(a, u);
+    const int f = p.fg;
+    const int cell0 = p.px0 / B;
+    const int ncell = min(NCELL, g.GC - cell0);
+    const bool active = strip_ok && ca < ncell;
+    const bool has_b = split < 4 && ca + 1 < ncell;
+    const int vbytes = valid_bytes<C, false, TILE>(a, p.px0);
+    const int copy = staged_bytes<C, B, false, TILE>(a, p);
+    const int need = min(TILE, g.GC * B - p.px0) * C;
+
+    mbar_wait(&full_bar[s], (k / S) & 1);
+    // Mirrored padding columns and any unstaged row tail (as k_stats_tma).
+    const int fs = min(copy, vbytes);
+    if (fs < need) {
+      constexpr int kLanes = 4;
+      for (int pr = t / kLanes; pr < B; pr += kConsumers / kLanes) {
+        uint8_t* rowp = st + pr * ROWB;
+        const int srow = reflect_index(p.r * B + pr, g.M);
+        const uint8_t* grow = a.img + static_cast<int64_t>(f) * a.fstride + static_cast<int64_t>(srow) * a.pitch;
+        for (int x = fs + (t % kLanes); x < need; x += kLanes) {
+          const int cpx = x / C, ch = x - cpx * C;
+          const int spx = reflect_index(p.px0 + cpx, g.N);
+          const int sx = (spx - p.px0) * C + ch;
+          rowp[x] = (sx >= 0 && sx < fs) ? rowp[sx] : __ldg(grow + static_cast<int64_t>(spx) * C + ch);
+        }
+      }
+      named_bar_sync(1, kConsumers);
+    }
+
+    // Strip sums over the band, split at the cell boundary.
+    uint32_t acc[C], part[C];
+#pragma unroll
+    for (int ch = 0; ch < C; ++ch) acc[ch] = part[ch] = 0;
+    const uint8_t* mystrip = st + lpx * C;
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      accumulate_row<C>(mystrip + i * ROWB, acc);
+      accumulate_row_masked<C>(mystrip + i * ROWB, m, part);
+    }
+    if (active) {
+#pragma unroll
+      for (int ch = 0; ch < C; ++ch) {
+        atomicAdd(&cellsum[ca * C + ch], part[ch]);
+        if (has_b) atomicAdd(&cellsum[(ca + 1) * C + ch], acc[ch] - part[ch]);
+      }
+    }
+    named_bar_sync(1, kConsumers);
+    // One draw per (cell, channel): channel-major items so a warp's statistic
+    // stores are contiguous in each plane.
+    for (int item = t; item < ncell * C; item += kConsumers) {
+      const int ch = item / ncell, c = item - ch * ncell;
+      const int gc = cell0 + c, gidx = p.r * g.GC + gc;
+      const uint32_t sum = cellsum[c * C + ch];
+      cellsum[c * C + ch] = 0;  // ready for the next unit
+      const uint32_t v = quantize_stat(env_cell, sum, draw_bits(a, cell_state(a, f, ch, p.r, gc), f, ch, p.r, gc, 0, 0),
+                                       inj_at(a, f, ch, gidx, 0, 0));
+      a.stats[static_cast<int64_t>(f * C + ch) * a.sstride + gidx] = static_cast<uint8_t>(v);
+      cellval[c * C + ch] = static_cast<uint8_t>(v);
+    }
+    named_bar_sync(1, kConsumers);
+    if (a.out && active) {
+      uint32_t va[C], vb[C];
+#pragma unroll
+      for (int ch = 0; ch < C; ++ch) {
+        va[ch] = cellval[ca * C + ch];
+        vb[ch] = has_b ? cellval[(ca + 1) * C + ch] : va[ch];
+      }
+      uint32_t w[C == 4 ? 4 : C];
+      pattern_words_split<C>(va, vb, split, w);
+      uint8_t* ms = st + lpx * C;
+#pragma unroll
+      for (int i = 0; i < B; ++i)
+#pragma unroll
+        for (int q = 0; q < (C == 4 ? 4 : C); ++q) reinterpret_cast<uint32_t*>(ms + i * ROWB)[q] = w[q];
+    }
+    fence_proxy_async_smem();
+    mbar_arrive(&done_bar[s]);
+  }
+}
+
+
+// ============================================================================
 // K2 fast path: one CTA per (frame, grid row, TILE-px tile); each thread owns a
 // 4-px strip, looks up its cell's statistics per channel plane (packed slots
 // from K0's per-plane scan), writes the strip pattern into a smem tile and one
@@ -1012,6 +1204,29 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
 using StatsKernel = void (*)(const CUtensorMap, const CUtensorMap, const StatsArgs);
 using ExpandKernel = void (*)(const CUtensorMap, const ExpandArgs);
 
+template <int C>
+StatsKernel pick_uniform_any(int b) {
+#define DPPX_CASE(BV) \
+  if (b == (BV)) return k_uniform_tma<C, BV>;
+  DPPX_CASE(2)
+  DPPX_CASE(3)
+  DPPX_CASE(5)
+  DPPX_CASE(6)
+  DPPX_CASE(7)
+  DPPX_CASE(9)
+  DPPX_CASE(10)
+  DPPX_CASE(11)
+  DPPX_CASE(13)
+  DPPX_CASE(14)
+  DPPX_CASE(15)
+  DPPX_CASE(17)
+  DPPX_CASE(18)
+  DPPX_CASE(19)
+  DPPX_CASE(30)
+#undef DPPX_CASE
+  return nullptr;
+}
+
 template <int C, bool AD, bool PK>
 StatsKernel pick_b(int b, int n) {
 #define DPPX_CASE(B4v, NS)                 \
@@ -1129,6 +1344,8 @@ ExpandKernel pick_expand(int b, int n) {
 StatsKernel select_stats_tma_c1(int b, int n, bool adaptive, bool packed);
 StatsKernel select_stats_tma_c3(int b, int n, bool adaptive, bool packed);
 StatsKernel select_stats_var_c1(int b, int n);
+StatsKernel select_uniform_any_c1(int b);
+StatsKernel select_uniform_any_c3(int b);
 StatsKernel select_stats_var_c3(int b, int n);
 ExpandKernel select_expand_tma_c1(int b, int n, bool adaptive, bool packed);
 ExpandKernel select_expand_tma_c3(int b, int n, bool adaptive, bool packed);

@@ -748,3 +748,33 @@ def test_straddling_subcells_on_tma_path(ctx, C, b, n):
         pls, img = ctx.pixelize_adaptive(frames, masks, p, dp.NOISE_NONE, None)
         rp, ri = _oracle_adaptive(frames, masks, p, "none", None)
         assert pls == rp and np.array_equal(img, ri), (M, N)
+
+
+@pytest.mark.parametrize("C", [1, 3])
+@pytest.mark.parametrize("b", [2, 3, 5, 6, 7, 9, 10, 11, 13, 14, 15, 17, 18, 19, 30])
+def test_uniform_any_grid_side_on_tma_path(ctx, C, b):
+    """Uniform pixelization for grid sides that are not a multiple of 4 px (the
+    paper's b = 2..20 sweep, b = 30): K1u tiles of whole cells, strips split at
+    cell boundaries, per-CTA smem cell sums. Ragged sizes (mirrored rows and
+    columns, partial last tile), keyed / injected / noise-free, vs the oracle;
+    K2 rebuilds the same image from the means."""
+    rng = np.random.default_rng(b * 7 + C)
+    for M, N in [(5 * b + 3, 1000), (2 * b + 1, 1500 + b)]:
+        F = 2
+        frames = rng.integers(0, 256, (F, M, N, C), np.uint8)
+        p = dp.make_privacy_params(0.5, 16, b)
+        seeds = dp.plane_seeds(b, F, C)
+        ctx.reset_stats()
+        means, img = ctx.pixelize_uniform(frames, p, dp.NOISE_KEYED, seeds)
+        assert ctx.stats()["launches"]["stats_tma"] >= 1, ctx.stats()["launches"]
+        rm, ri = _oracle_uniform(frames, p, "keyed", seeds)
+        assert np.array_equal(means, rm) and np.array_equal(img, ri), (M, N)
+        assert np.array_equal(ctx.broadcast_means(means, M, N, b, channels=C, frames=F), ri)
+        G = dp.grid_dims(M, N, b).grid_count()
+        inj = rng.laplace(0, 30, (F * C, G))
+        means, img = ctx.pixelize_uniform(frames, p, dp.NOISE_INJECTED, None, injected=inj)
+        rm, ri = _oracle_uniform(frames, p, "injected", None, injected=inj)
+        assert np.array_equal(means, rm) and np.array_equal(img, ri), (M, N)
+        means, img = ctx.pixelize_uniform(frames, p, dp.NOISE_NONE, None)
+        rm, ri = _oracle_uniform(frames, p, "none", None)
+        assert np.array_equal(means, rm) and np.array_equal(img, ri), (M, N)
