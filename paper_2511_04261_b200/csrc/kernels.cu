@@ -1140,7 +1140,7 @@ cudaError_t launch_gather_stage(const GatherArgs& a, cudaStream_t s) {
 
 StatsKernel select_stats_kernel(int C, int b, int n, bool adaptive, bool packed) {
   if (!adaptive && n != 1) return nullptr;
-  if (!adaptive && !packed && b % 4 != 0) {  // K1u: uniform, grid sides not a multiple of 4 px
+  if (!adaptive && !packed && (b % 4 != 0 || b == 128)) {  // K1u: uniform, b % 4 != 0 or b = 128
     if (C == 1) return select_uniform_any_c1(b);
     if (C == 3) return select_uniform_any_c3(b);
     return nullptr;
@@ -1170,7 +1170,7 @@ int stats_tile_px() { return kTilePx; }
 
 // Tile width of the staged kernel for grid side b (whole cells per warp).
 int stats_tile_px_for(int b) {
-  if (b % 4 != 0 && b >= 2 && b <= 32) return ku_tile(b);  // K1u tiles (whole cells, 16-px multiple)
+  if ((b % 4 != 0 && b >= 2 && b <= 32) || b == 128) return ku_tile(b);  // K1u tiles
   const int b4 = b / 4;
   if (b % 4 != 0 || b4 < 1 || b4 > 32) return kTilePx;
   return 4 * (kConsumers / 32) * ((32 / b4) * b4);

@@ -890,7 +890,14 @@ __global__ void __launch_bounds__(kStatsThreads)
 // draws, and each strip writes its reconstructed pixels from the table.
 // ============================================================================
 constexpr int ku_gcd(int x, int y) { return y == 0 ? x : ku_gcd(y, x % y); }
-constexpr int ku_tile(int b) { return (b * 16 / ku_gcd(b, 16)) * (512 / (b * 16 / ku_gcd(b, 16))); }
+constexpr int ku_lcm16(int b) { return b * 16 / ku_gcd(b, 16); }
+// Whole cells, a multiple of 16 px, <= 512 px and <= ~100 KB per RGB stage
+// (b = 128: 256-px tiles, two 98 KB stages).
+constexpr int ku_tile(int b) {
+  return ku_lcm16(b) * (((512 < 102400 / (3 * b)) ? 512 : 102400 / (3 * b)) / ku_lcm16(b) > 0
+                            ? ((512 < 102400 / (3 * b)) ? 512 : 102400 / (3 * b)) / ku_lcm16(b)
+                            : 1);
+}
 
 template <int C, int B>
 __global__ void __launch_bounds__(kStatsThreads)
@@ -901,7 +908,8 @@ __global__ void __launch_bounds__(kStatsThreads)
   constexpr uint32_t STAGE = (B * ROWB + 127) & ~127;  // TMA destinations: 128-byte aligned
   constexpr int NCELL = TILE / B;  // cells per tile
   constexpr int NSTRIP = TILE / 4;
-  static_assert(B >= 2 && B % 4 != 0 && TILE % B == 0 && TILE % 16 == 0 && NSTRIP <= kConsumers,
+  static_assert(B >= 2 && (B % 4 != 0 || B == 128) && TILE % B == 0 && TILE % 16 == 0 &&
+                    NSTRIP <= kConsumers,
                 "K1u geometry");
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full_bar[kMaxStages];
@@ -1223,6 +1231,7 @@ StatsKernel pick_uniform_any(int b) {
   DPPX_CASE(18)
   DPPX_CASE(19)
   DPPX_CASE(30)
+  DPPX_CASE(128)  // PPM-100's largest grid (K1 stages would not fit two per CTA)
 #undef DPPX_CASE
   return nullptr;
 }

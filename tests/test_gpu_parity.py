@@ -751,7 +751,7 @@ def test_straddling_subcells_on_tma_path(ctx, C, b, n):
 
 
 @pytest.mark.parametrize("C", [1, 3])
-@pytest.mark.parametrize("b", [2, 3, 5, 6, 7, 9, 10, 11, 13, 14, 15, 17, 18, 19, 30])
+@pytest.mark.parametrize("b", [2, 3, 5, 6, 7, 9, 10, 11, 13, 14, 15, 17, 18, 19, 30, 128])
 def test_uniform_any_grid_side_on_tma_path(ctx, C, b):
     """Uniform pixelization for grid sides that are not a multiple of 4 px (the
     paper's b = 2..20 sweep, b = 30): K1u tiles of whole cells, strips split at
