@@ -33,7 +33,7 @@ cudaError_t launch_stats_rows(const StatsArgs& a, size_t smem, cudaStream_t s);
 cudaError_t launch_expand_rows(const ExpandArgs& a, size_t smem, cudaStream_t s);
 int stats_threads();
 int stats_tile_px();
-int stats_tile_px_for(int b);
+int stats_tile_px_for(int b, bool adaptive);
 int expand_packed_tile_px();
 int stats_max_stages();
 cudaError_t launch_classify(const ClassifyArgs& a, cudaStream_t s);
@@ -456,7 +456,7 @@ int run_stats(dppx_ctx* ctx, StatsArgs& a) {
                        (!a.out || (aligned16(a.out) && a.opitch % 16 == 0 && a.ofstride % 16 == 0));
   PendingTiming pt;
   CUtensorMap tin{}, tout{};
-  const int tile = stats_tile_px_for(g.b);
+  const int tile = stats_tile_px_for(g.b, a.adaptive != 0);
   const int64_t row_bytes = static_cast<int64_t>(g.N) * g.C;
   // Narrow frames: pack several padded frame rows side by side in one tile.
   const int padded_px = g.GC * g.b;
@@ -718,7 +718,7 @@ int expand_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* stats, i
   timing_begin(ctx, DPPX_K_EXPAND, &pt);
   // Fast path: staged tile, TMA box stores (aligned output, the K1 grid sides,
   // C in {1,3}); narrow frames packed side by side.
-  int tile = stats_tile_px_for(g.b);
+  int tile = stats_tile_px_for(g.b, adaptive);
   const int64_t row_bytes = static_cast<int64_t>(g.N) * g.C;
   const int padded_px = g.GC * g.b;
   int64_t stage_bytes = static_cast<int64_t>(g.b) * tile * g.C;

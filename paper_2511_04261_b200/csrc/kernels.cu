@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <type_traits>
 
@@ -1140,6 +1141,13 @@ cudaError_t launch_gather_stage(const GatherArgs& a, cudaStream_t s) {
 
 StatsKernel select_stats_kernel(int C, int b, int n, bool adaptive, bool packed) {
   if (!adaptive && n != 1) return nullptr;
+  if (adaptive && !packed && (b % 4 != 0 || b == 128)) {  // K1a (DPPX_NO_K1A: K1r, for A/B runs)
+    static const bool off = std::getenv("DPPX_NO_K1A") != nullptr;
+    if (off) return nullptr;
+    if (C == 1) return select_adaptive_any_c1(b, n);
+    if (C == 3) return select_adaptive_any_c3(b, n);
+    return nullptr;
+  }
   if (!adaptive && !packed && (b % 4 != 0 || b == 128)) {  // K1u: uniform, b % 4 != 0 or b = 128
     if (C == 1) return select_uniform_any_c1(b);
     if (C == 3) return select_uniform_any_c3(b);
@@ -1169,8 +1177,8 @@ int stats_threads() { return kStatsThreads; }
 int stats_tile_px() { return kTilePx; }
 
 // Tile width of the staged kernel for grid side b (whole cells per warp).
-int stats_tile_px_for(int b) {
-  if ((b % 4 != 0 && b >= 2 && b <= 32) || b == 128) return ku_tile(b);  // K1u tiles
+int stats_tile_px_for(int b, bool adaptive) {
+  if ((b % 4 != 0 && b >= 2 && b <= 32) || b == 128) return adaptive ? ka_tile(b) : ku_tile(b);  // K1u / K1a
   const int b4 = b / 4;
   if (b % 4 != 0 || b4 < 1 || b4 > 32) return kTilePx;
   return 4 * (kConsumers / 32) * ((32 / b4) * b4);

@@ -1212,6 +1212,283 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
 using StatsKernel = void (*)(const CUtensorMap, const CUtensorMap, const StatsArgs);
 using ExpandKernel = void (*)(const CUtensorMap, const ExpandArgs);
 
+// K1a: the adaptive counterpart of K1u (PPM-100's b = 128 with n = 2..32, and
+// b = 30): same producer and tiles of whole cells (b = 128: 128-px tiles, one
+// cell, so the subcell tables fit beside two 49 KB stages). Per vertical
+// subcell row, each strip splits its row sums at the subcell boundary into a
+// per-CTA smem subcell table (atomics); then one pass over (vertical subcell,
+// subcell column, channel): complex cells draw their subcells at sigma_sub,
+// the (0, 0) item of a simple cell sums its n x n entries and draws the cell at
+// sigma; the strips then write their pixels from the value tables.
+constexpr int ka_tile(int b) { return b == 128 ? 128 : ku_tile(b); }
+
+template <int C, int B, int NSUB>
+__global__ void __launch_bounds__(kStatsThreads)
+    k_adaptive_any_tma(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
+                       const StatsArgs a) {
+  constexpr int TILE = ka_tile(B);
+  constexpr int ROWB = TILE * C;
+  constexpr uint32_t STAGE = (B * ROWB + 127) & ~127;
+  constexpr int SB = B / NSUB;            // subcell side
+  constexpr int NCELL = TILE / B;
+  constexpr int SC = TILE / SB;           // subcell columns per tile
+  constexpr int NSTRIP = TILE / 4;
+  static_assert(B % NSUB == 0 && SB >= 2 && TILE % B == 0 && TILE % 16 == 0 && NSTRIP <= kConsumers &&
+                    NCELL <= kConsumers,
+                "K1a geometry");
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full_bar[kMaxStages];
+  __shared__ __align__(8) uint64_t id_bar[kMaxStages];
+  __shared__ __align__(8) uint64_t done_bar[kMaxStages];
+  __shared__ int stage_unit[kMaxStages];
+  __shared__ uint32_t subsum[NSUB * SC * C];
+  __shared__ uint8_t subval[NSUB * SC * C];
+  __shared__ uint8_t cellval[NCELL * C];
+  __shared__ uint8_t cflag[NCELL];
+  __shared__ uint32_t cslot[NCELL];
+  __shared__ uint32_t cellsum[NCELL * C];
+  __shared__ int cxlist[NCELL];  // complex cells of the unit (compacted)
+  __shared__ int ncx_s;
+
+  const int S = a.stages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&id_bar[s], 1);
+      mbar_init(&done_bar[s], kConsumers);
+    }
+    fence_mbarrier_init();
+  }
+  for (int i = threadIdx.x; i < NSUB * SC * C; i += blockDim.x) subsum[i] = 0;
+  for (int i = threadIdx.x; i < NCELL * C; i += blockDim.x) cellsum[i] = 0;
+  __syncthreads();
+
+  if (warp == kConsumers / 32) {  // producer warp, as in k_stats_tma
+    if (lane == 0) {
+      prefetch_tmap(&tm_in);
+      prefetch_tmap(&tm_out);
+    }
+    auto finish_unit = [&](int s, int use) {
+      mbar_wait(&done_bar[s], use & 1);
+      if (a.out) {
+        const int uu = stage_unit[s];
+        store_tail<C, B, false, TILE>(a, uu, smem + s * STAGE, lane);
+        if (lane == 0) store_unit<C, B, false, TILE>(a, &tm_out, uu, smem + s * STAGE);
+      }
+      __syncwarp();
+    };
+    int k = 0, done_units = 0;
+    for (;; ++k) {
+      const int s = k % S;
+      if (k >= S) {
+        finish_unit(s, (k / S) - 1);
+        ++done_units;
+      }
+      int u = 0;
+      if (lane == 0) {
+        u = atomicAdd(a.work_counter, 1);
+        if (u >= a.units) {
+          if (u == a.units + static_cast<int>(gridDim.x) - 1) atomicExch(a.work_counter, 0);
+          u = -1;
+        }
+        stage_unit[s] = u;
+        mbar_arrive(&id_bar[s]);
+        if (u < 0)
+          mbar_arrive_expect_tx(&full_bar[s], 0);
+        else
+          load_unit<C, B, false, TILE>(a, &tm_in, u, smem + s * STAGE, &full_bar[s]);
+      }
+      u = __shfl_sync(0xFFFFFFFFu, u, 0);
+      if (u < 0) break;
+    }
+    for (int j = done_units; j < k; ++j) finish_unit(j % S, j / S);
+    if (lane == 0) bulk_wait_all();
+    return;
+  }
+
+  // ---------------- consumer warps ----------------
+  const int t = threadIdx.x;
+  const BatchGeom& g = a.g;
+  const DrawEnv env_cell = make_env(a.noise.kind, a.exact_noise != 0, a.area, a.sigma);
+  const DrawEnv env_sub = make_env(a.noise.kind, a.exact_noise != 0, a.sub_area, a.sigma_sub);
+  const int cA = (4 * (t < NSTRIP ? t : 0) / SB) / NSUB;                  // cell of column sa
+  const int cB = ((4 * (t < NSTRIP ? t : 0) / SB) + 1) / NSUB;            // cell of column sa + 1
+  const bool strip_ok = t < NSTRIP;
+  const int lpx = 4 * (strip_ok ? t : 0);
+  const int sa = lpx / SB;                          // first subcell column of the strip
+  const int split = min(4, (sa + 1) * SB - lpx);    // pixels [0, split) are in column sa
+  uint32_t m[C][C == 4 ? 4 : C];
+#pragma unroll
+  for (int ch = 0; ch < C; ++ch)
+#pragma unroll
+    for (int q = 0; q < (C == 4 ? 4 : C); ++q) m[ch][q] = 0;
+#pragma unroll
+  for (int pos = 0; pos < 4 * C; ++pos)
+    if (pos / C < split) m[pos % C][pos / 4] |= 1u << (8 * (pos % 4));
+
+  for (int k = 0;; ++k) {
+    const int s = k % S;
+    uint8_t* st = smem + s * STAGE;
+    mbar_wait(&id_bar[s], (k / S) & 1);
+    const int u = *reinterpret_cast<volatile int*>(&stage_unit[s]);
+    if (u < 0) break;
+    const UnitPos p = decode_unit<false, TILE>(a, u);
+    const int f = p.fg;
+    const int cell0 = p.px0 / B;
+    const int ncell = min(NCELL, g.GC - cell0);
+    const int nsc = ncell * NSUB;                    // real subcell columns in the tile
+    const bool active = strip_ok && sa < nsc;
+    const bool has_b = split < 4 && sa + 1 < nsc;
+    const int vbytes = valid_bytes<C, false, TILE>(a, p.px0);
+    const int copy = staged_bytes<C, B, false, TILE>(a, p);
+    const int need = min(TILE, g.GC * B - p.px0) * C;
+    const uint32_t rowpre = __ldg(&a.rowprefix[static_cast<int64_t>(f) * g.GR + p.r]);
+    const uint32_t S_tot = __ldg(&a.totals[f]);
+    uint32_t info = 1u;  // cell class and packed slot (K0), published after the barrier below
+    if (t < ncell) info = __ldg(&a.cellinfo[static_cast<int64_t>(f) * g.G + p.r * g.GC + cell0 + t]);
+
+    mbar_wait(&full_bar[s], (k / S) & 1);
+    const int fs = min(copy, vbytes);
+    if (fs < need) {
+      constexpr int kLanes = 4;
+      for (int pr = t / kLanes; pr < B; pr += kConsumers / kLanes) {
+        uint8_t* rowp = st + pr * ROWB;
+        const int srow = reflect_index(p.r * B + pr, g.M);
+        const uint8_t* grow = a.img + static_cast<int64_t>(f) * a.fstride + static_cast<int64_t>(srow) * a.pitch;
+        for (int x = fs + (t % kLanes); x < need; x += kLanes) {
+          const int cpx = x / C, ch = x - cpx * C;
+          const int spx = reflect_index(p.px0 + cpx, g.N);
+          const int sx = (spx - p.px0) * C + ch;
+          rowp[x] = (sx >= 0 && sx < fs) ? rowp[sx] : __ldg(grow + static_cast<int64_t>(spx) * C + ch);
+        }
+      }
+    }
+    named_bar_sync(1, kConsumers);  // staged rows complete; previous unit's tables free
+    if (t < ncell) {
+      cflag[t] = info & 1u;
+      cslot[t] = rowpre + (info >> 1);
+    }
+    if (t == 0) {  // compact list of the unit's complex cells
+      int q = 0;
+      for (int c = 0; c < ncell; ++c) {
+        const uint32_t ic = __ldg(&a.cellinfo[static_cast<int64_t>(f) * g.G + p.r * g.GC + cell0 + c]);
+        if (!(ic & 1u)) cxlist[q++] = c;
+      }
+      ncx_s = q;
+    }
+
+    const uint8_t* mystrip = st + lpx * C;
+    uint32_t tot_a[C], tot_b[C];  // whole-band sums left / right of the boundary
+#pragma unroll
+    for (int ch = 0; ch < C; ++ch) tot_a[ch] = tot_b[ch] = 0;
+#pragma unroll 1
+    for (int vs = 0; vs < NSUB; ++vs) {
+      uint32_t acc[C], part[C];
+#pragma unroll
+      for (int ch = 0; ch < C; ++ch) acc[ch] = part[ch] = 0;
+#pragma unroll
+      for (int i = 0; i < SB; ++i) {
+        accumulate_row<C>(mystrip + (vs * SB + i) * ROWB, acc);
+        accumulate_row_masked<C>(mystrip + (vs * SB + i) * ROWB, m, part);
+      }
+      if (active) {
+        uint32_t* row = &subsum[(vs * SC + sa) * C];
+#pragma unroll
+        for (int ch = 0; ch < C; ++ch) {
+          atomicAdd(row + ch, part[ch]);
+          if (has_b) atomicAdd(row + C + ch, acc[ch] - part[ch]);
+          tot_a[ch] += part[ch];
+          tot_b[ch] += acc[ch] - part[ch];
+        }
+      }
+    }
+    if (active) {  // whole-cell sums (for simple cells)
+#pragma unroll
+      for (int ch = 0; ch < C; ++ch) {
+        if (has_b && cB != cA) {
+          atomicAdd(&cellsum[cA * C + ch], tot_a[ch]);
+          atomicAdd(&cellsum[cB * C + ch], tot_b[ch]);
+        } else {
+          atomicAdd(&cellsum[cA * C + ch], tot_a[ch] + (has_b ? tot_b[ch] : 0u));
+        }
+      }
+    }
+    named_bar_sync(1, kConsumers);
+    // Simple cells: one draw per (cell, channel) at sigma.
+    for (int item = t; item < ncell * C; item += kConsumers) {
+      const int ch = item / ncell, c = item - ch * ncell;
+      if (!cflag[c]) continue;
+      const int gc = cell0 + c, gidx = p.r * g.GC + gc;
+      const uint32_t v = quantize_stat(env_cell, cellsum[c * C + ch],
+                                       draw_bits(a, cell_state(a, f, ch, p.r, gc), f, ch, p.r, gc, 0, 0),
+                                       inj_at(a, f, ch, gidx, 0, 0));
+      a.stats[static_cast<int64_t>(f * C + ch) * a.sstride + stat_offset(a, true, gidx, cslot[c], S_tot, 0, 0)] =
+          static_cast<uint8_t>(v);
+      cellval[c * C + ch] = static_cast<uint8_t>(v);
+    }
+    // Complex cells: n x n x C draws each at sigma_sub (compacted cell list).
+    const int ncx = ncx_s;
+    constexpr int NN = NSUB * NSUB;
+    for (int item = t; item < ncx * NN * C; item += kConsumers) {
+      const int kk = item / (NN * C), rem = item - kk * (NN * C);
+      const int ch = rem / NN, ss = rem - ch * NN;
+      const int vs = ss / NSUB, sc = ss - vs * NSUB;
+      const int c = cxlist[kk];
+      const int gc = cell0 + c, gidx = p.r * g.GC + gc;
+      const int sidx = c * NSUB + sc;
+      const uint32_t v = quantize_stat(env_sub, subsum[(vs * SC + sidx) * C + ch],
+                                       draw_bits(a, cell_state(a, f, ch, p.r, gc), f, ch, p.r, gc, vs, sc),
+                                       inj_at(a, f, ch, gidx, vs, sc));
+      a.stats[static_cast<int64_t>(f * C + ch) * a.sstride + stat_offset(a, false, gidx, cslot[c], S_tot, vs, sc)] =
+          static_cast<uint8_t>(v);
+      subval[(vs * SC + sidx) * C + ch] = static_cast<uint8_t>(v);
+    }
+    named_bar_sync(1, kConsumers);
+    for (int i = t; i < NSUB * nsc * C; i += kConsumers) {  // reset for the next unit
+      const int vs = i / (nsc * C), r2 = i - vs * (nsc * C);
+      subsum[vs * SC * C + r2] = 0;
+    }
+    for (int i = t; i < ncell * C; i += kConsumers) cellsum[i] = 0;
+    if (a.out && active) {
+      const int ca = sa / NSUB, cb = (sa + 1) / NSUB;
+#pragma unroll 1
+      for (int vs = 0; vs < NSUB; ++vs) {
+        uint32_t va[C], vb[C];
+#pragma unroll
+        for (int ch = 0; ch < C; ++ch) {
+          va[ch] = cflag[ca] ? cellval[ca * C + ch] : subval[(vs * SC + sa) * C + ch];
+          vb[ch] = !has_b ? va[ch] : (cflag[cb] ? cellval[cb * C + ch] : subval[(vs * SC + sa + 1) * C + ch]);
+        }
+        uint32_t w[C == 4 ? 4 : C];
+        pattern_words_split<C>(va, vb, split, w);
+#pragma unroll 1
+        for (int i = 0; i < SB; ++i)
+#pragma unroll
+          for (int q = 0; q < (C == 4 ? 4 : C); ++q)
+            reinterpret_cast<uint32_t*>(st + lpx * C + (vs * SB + i) * ROWB)[q] = w[q];
+      }
+    }
+    fence_proxy_async_smem();
+    mbar_arrive(&done_bar[s]);
+  }
+}
+
+template <int C>
+StatsKernel pick_adaptive_any(int b, int n) {
+#define DPPX_CASE(BV, NS) \
+  if (b == (BV) && n == (NS)) return k_adaptive_any_tma<C, BV, NS>;
+  // b = 128 with n <= 16 stays on K1r (measured 5-10 % faster there)
+  DPPX_CASE(128, 32)
+  DPPX_CASE(30, 2)
+  DPPX_CASE(30, 3)
+  DPPX_CASE(30, 5)
+  DPPX_CASE(30, 6)
+  DPPX_CASE(30, 10)
+#undef DPPX_CASE
+  return nullptr;
+}
+
 template <int C>
 StatsKernel pick_uniform_any(int b) {
 #define DPPX_CASE(BV) \
@@ -1354,6 +1631,8 @@ StatsKernel select_stats_tma_c1(int b, int n, bool adaptive, bool packed);
 StatsKernel select_stats_tma_c3(int b, int n, bool adaptive, bool packed);
 StatsKernel select_stats_var_c1(int b, int n);
 StatsKernel select_uniform_any_c1(int b);
+StatsKernel select_adaptive_any_c1(int b, int n);
+StatsKernel select_adaptive_any_c3(int b, int n);
 StatsKernel select_uniform_any_c3(int b);
 StatsKernel select_stats_var_c3(int b, int n);
 ExpandKernel select_expand_tma_c1(int b, int n, bool adaptive, bool packed);

@@ -778,3 +778,35 @@ def test_uniform_any_grid_side_on_tma_path(ctx, C, b):
         means, img = ctx.pixelize_uniform(frames, p, dp.NOISE_NONE, None)
         rm, ri = _oracle_uniform(frames, p, "none", None)
         assert np.array_equal(means, rm) and np.array_equal(img, ri), (M, N)
+
+
+@pytest.mark.parametrize("C", [1, 3])
+@pytest.mark.parametrize("b,n", [(30, 2), (30, 3), (30, 5), (30, 6), (30, 10), (128, 32)])
+def test_adaptive_any_grid_side_on_tma_path(ctx, C, b, n):
+    """K1a: adaptive for b = 30 and PPM-100's b = 128 (tiles of whole cells,
+    strips split at subcell boundaries, per-CTA subcell tables). Mixed simple /
+    complex cells, ragged sizes, keyed / injected / noise-free, vs the oracle;
+    K2 rebuilds the same image from the payloads."""
+    rng = np.random.default_rng(b * 31 + n + C)
+    for M, N in [(2 * b + 7, 1000), (b + 3, 4 * b + 5)]:
+        F = 2
+        frames = rng.integers(0, 256, (F, M, N, C), np.uint8)
+        masks = (rng.random((F, M, N)) < 0.5).astype(np.uint8)
+        masks[0, :, : N // 3] = 1  # a run of simple cells
+        masks[1, : M // 2] = 0     # a run of complex cells
+        p = dp.make_privacy_params(0.5, 16, b, n)
+        seeds = dp.plane_seeds(b + n, F, C)
+        ctx.reset_stats()
+        pls, img = ctx.pixelize_adaptive(frames, masks, p, dp.NOISE_KEYED, seeds)
+        assert ctx.stats()["launches"]["stats_tma"] >= 1, ctx.stats()["launches"]
+        rp, ri = _oracle_adaptive(frames, masks, p, "keyed", seeds)
+        assert pls == rp and np.array_equal(img, ri), (M, N)
+        assert np.array_equal(ctx.reassemble(pls, M, N, b, n, channels=C, frames=F), ri), (M, N)
+        G = dp.grid_dims(M, N, b).grid_count()
+        inj = rng.laplace(0, 30, (F * C, G * n * n))
+        pls, img = ctx.pixelize_adaptive(frames, masks, p, dp.NOISE_INJECTED, None, injected=inj)
+        rp, ri = _oracle_adaptive(frames, masks, p, "injected", None, injected=inj)
+        assert pls == rp and np.array_equal(img, ri), (M, N)
+        pls, img = ctx.pixelize_adaptive(frames, masks, p, dp.NOISE_NONE, None)
+        rp, ri = _oracle_adaptive(frames, masks, p, "none", None)
+        assert pls == rp and np.array_equal(img, ri), (M, N)
