@@ -17,3 +17,4 @@ $B1 > $OUT/plain1_$TAG.log 2>&1 && timeout 900 ncu --set full --clock-control no
 echo "ncu_full_rc=$?"
 tail -1 $OUT/bench_$TAG.log | cut -c1-600
 tail -1 $OUT/bench_ref_$TAG.log | cut -c1-300
+timeout 300 python -c "import __graft_entry__ as g; g.build(); g.smoke(); print('smoke ok')" > $OUT/smoke_$TAG.log 2>&1; echo "smoke_rc=$?"; tail -1 $OUT/smoke_$TAG.log
