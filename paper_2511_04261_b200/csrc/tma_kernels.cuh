@@ -1209,6 +1209,73 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
   if (t == 0) bulk_wait_read_all();  // smem must outlive the stores' reads
 }
 
+// K2u: broadcast_means for the K1u grid sides (uniform, b % 4 != 0 or b = 128):
+// K1u's tiles of whole cells; each 4-px strip takes the values of the (at most
+// two) cells it meets and writes its pixels into a smem tile, stored with one
+// 3-D TMA box (the < 8 bytes past the tensor's row extent by the CTA).
+template <int C, int B>
+__global__ void __launch_bounds__(kConsumers) k_expand_uany(const __grid_constant__ CUtensorMap tm_out,
+                                                            const ExpandArgs a) {
+  constexpr int TILE = ku_tile(B);
+  constexpr int ROWB = TILE * C;
+  constexpr int NCELL = TILE / B;
+  constexpr int NSTRIP = TILE / 4;
+  static_assert(NSTRIP <= kConsumers && TILE % B == 0, "K2u geometry");
+  extern __shared__ __align__(128) uint8_t smem[];
+  const BatchGeom& g = a.g;
+  const int t = threadIdx.x;
+  const bool strip_ok = t < NSTRIP;
+  const int lpx = 4 * (strip_ok ? t : 0);
+  const int ca = lpx / B;
+  const int split = min(4, (ca + 1) * B - lpx);
+  for (int u = blockIdx.x, k = 0; u < a.units; u += gridDim.x, ++k) {
+    if (t == 0 && k > 0) bulk_wait_read_all();
+    __syncthreads();
+    const uint32_t rest = a.div_tiles.div(static_cast<uint32_t>(u));
+    const int tile = u - static_cast<int>(rest * a.div_tiles.d);
+    const uint32_t fq = a.div_rows.div(rest);
+    const int r = static_cast<int>(rest - fq * a.div_rows.d);
+    const int f = static_cast<int>(fq);
+    const int px0 = tile * TILE;
+    const int cell0 = px0 / B;
+    const int ncell = min(NCELL, g.GC - cell0);
+    const bool active = strip_ok && ca < ncell;
+    const bool has_b = split < 4 && ca + 1 < ncell;
+    if (active) {
+      uint32_t va[C], vb[C];
+#pragma unroll
+      for (int ch = 0; ch < C; ++ch) {
+        const uint8_t* st = a.stats + (static_cast<int64_t>(f) * C + ch) * a.sstride + r * g.GC + cell0 + ca;
+        va[ch] = __ldg(st);
+        vb[ch] = has_b ? __ldg(st + 1) : va[ch];
+      }
+      uint32_t w[C == 4 ? 4 : C];
+      pattern_words_split<C>(va, vb, split, w);
+#pragma unroll 4
+      for (int i = 0; i < B; ++i)
+#pragma unroll
+        for (int q = 0; q < (C == 4 ? 4 : C); ++q)
+          reinterpret_cast<uint32_t*>(smem + i * ROWB + lpx * C)[q] = w[q];
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    const int scopy = max(0, min(ROWB, a.tensor_out_bytes - px0 * C));
+    if (t == 0 && scopy > 0) tma_store_3d(&tm_out, px0 * C / 8, r * B, f, smem);
+    if (t == 0) bulk_commit();
+    const int vbytes = min(TILE, g.N - px0) * C;
+    const int span = vbytes - scopy;
+    if (span > 0) {
+      const int rows = min(B, g.M - r * B);
+      for (int e = t; e < rows * span; e += kConsumers) {
+        const int i = e / span, x = scopy + (e - i * span);
+        a.out[static_cast<int64_t>(f) * a.ofstride + static_cast<int64_t>(r * B + i) * a.opitch +
+              static_cast<int64_t>(px0) * C + x] = smem[i * ROWB + x];
+      }
+    }
+  }
+  if (t == 0) bulk_wait_read_all();
+}
+
 using StatsKernel = void (*)(const CUtensorMap, const CUtensorMap, const StatsArgs);
 using ExpandKernel = void (*)(const CUtensorMap, const ExpandArgs);
 
@@ -1626,12 +1693,38 @@ ExpandKernel pick_expand(int b, int n) {
   return nullptr;
 }
 
+template <int C>
+ExpandKernel pick_expand_uany(int b) {
+#define DPPX_CASE(BV) \
+  if (b == (BV)) return k_expand_uany<C, BV>;
+  DPPX_CASE(2)
+  DPPX_CASE(3)
+  DPPX_CASE(5)
+  DPPX_CASE(6)
+  DPPX_CASE(7)
+  DPPX_CASE(9)
+  DPPX_CASE(10)
+  DPPX_CASE(11)
+  DPPX_CASE(13)
+  DPPX_CASE(14)
+  DPPX_CASE(15)
+  DPPX_CASE(17)
+  DPPX_CASE(18)
+  DPPX_CASE(19)
+  DPPX_CASE(30)
+  DPPX_CASE(128)
+#undef DPPX_CASE
+  return nullptr;
+}
+
 // Per-channel-count selectors (defined in tma_c1.cu / tma_c3.cu).
 StatsKernel select_stats_tma_c1(int b, int n, bool adaptive, bool packed);
 StatsKernel select_stats_tma_c3(int b, int n, bool adaptive, bool packed);
 StatsKernel select_stats_var_c1(int b, int n);
 StatsKernel select_uniform_any_c1(int b);
 StatsKernel select_adaptive_any_c1(int b, int n);
+ExpandKernel select_expand_uany_c1(int b);
+ExpandKernel select_expand_uany_c3(int b);
 StatsKernel select_adaptive_any_c3(int b, int n);
 StatsKernel select_uniform_any_c3(int b);
 StatsKernel select_stats_var_c3(int b, int n);
