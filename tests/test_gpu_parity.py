@@ -542,7 +542,9 @@ def test_randomized_fuzz_against_oracle(ctx):
 
 @pytest.mark.parametrize("M,N,C,b,n", [(576, 768, 3, 16, 1), (1080, 1920, 3, 16, 4), (1083, 1917, 1, 32, 8),
                                        (2160, 3840, 3, 32, 8), (200, 1000, 3, 8, 2),
-                                       (1080, 1920, 3, 24, 4), (1085, 1921, 1, 40, 8)])
+                                       (1080, 1920, 3, 24, 4), (1085, 1921, 1, 40, 8),
+                                       (1080, 1920, 3, 30, 5), (1085, 1921, 3, 7, 1),
+                                       (2160, 3840, 1, 128, 32)])
 def test_single_frame_row_bands(ctx, M, N, C, b, n):
     """Single-frame host calls on pinned buffers are pipelined in row bands (H2D /
     K1 / D2H overlap within the frame): identical to the oracle and to the
