@@ -1160,6 +1160,11 @@ StatsKernel select_stats_kernel(int C, int b, int n, bool adaptive, bool packed)
 
 ExpandKernel select_expand_kernel(int C, int b, int n, bool adaptive, bool packed) {
   if (!adaptive && n != 1) return nullptr;
+  if (adaptive && !packed && (b % 4 != 0 || b == 128)) {  // K2a
+    if (C == 1) return select_expand_aany_c1(b, n);
+    if (C == 3) return select_expand_aany_c3(b, n);
+    return nullptr;
+  }
   if (!adaptive && !packed && (b % 4 != 0 || b == 128)) {  // K2u
     if (C == 1) return select_expand_uany_c1(b);
     if (C == 3) return select_expand_uany_c3(b);

@@ -16,6 +16,8 @@ StatsKernel select_adaptive_any_c1(int b, int n) { return pick_adaptive_any<1>(b
 
 ExpandKernel select_expand_uany_c1(int b) { return pick_expand_uany<1>(b); }
 
+ExpandKernel select_expand_aany_c1(int b, int n) { return pick_expand_aany<1>(b, n); }
+
 ExpandKernel select_expand_tma_c1(int b, int n, bool adaptive, bool packed) {
   if (packed) return adaptive ? pick_expand<1, true, true>(b, n) : pick_expand<1, false, true>(b, n);
   return adaptive ? pick_expand<1, true, false>(b, n) : pick_expand<1, false, false>(b, n);

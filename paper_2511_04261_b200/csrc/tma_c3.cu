@@ -16,6 +16,8 @@ StatsKernel select_adaptive_any_c3(int b, int n) { return pick_adaptive_any<3>(b
 
 ExpandKernel select_expand_uany_c3(int b) { return pick_expand_uany<3>(b); }
 
+ExpandKernel select_expand_aany_c3(int b, int n) { return pick_expand_aany<3>(b, n); }
+
 ExpandKernel select_expand_tma_c3(int b, int n, bool adaptive, bool packed) {
   if (packed) return adaptive ? pick_expand<3, true, true>(b, n) : pick_expand<3, false, true>(b, n);
   return adaptive ? pick_expand<3, true, false>(b, n) : pick_expand<3, false, false>(b, n);

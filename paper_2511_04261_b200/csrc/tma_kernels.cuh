@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(kStatsThreads)
     const int f = p.fg * units_pack<PACKED>(a) + jj;  // this thread's frame
     const int cell = PACKED ? (p.px0 + lpx) / B : p.px0 / B + sx / B4;
     const int lic = sx % B4;       // lane within cell
-    const int sc = lic / SB4;      // subcell column
+    const int sc = lic / (SB4 > 0 ? SB4 : 1);  // subcell column (unused for split strips)
     const bool active = in_slot && (!PACKED || f < g.F) && cell < g.GC;
     const int gidx = p.r * g.GC + cell;
     const bool simple0 = !ADAPTIVE || (cur.info & 1u);  // VAR: decided after the sums
@@ -899,6 +899,9 @@ constexpr int ku_tile(int b) {
                             : 1);
 }
 
+// K1a / K2a tiles (b = 128: 128 px, so the subcell tables fit beside two stages).
+constexpr int ka_tile(int b) { return b == 128 ? 128 : ku_tile(b); }
+
 template <int C, int B>
 __global__ void __launch_bounds__(kStatsThreads)
     k_uniform_tma(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
@@ -1276,6 +1279,110 @@ __global__ void __launch_bounds__(kConsumers) k_expand_uany(const __grid_constan
   if (t == 0) bulk_wait_read_all();
 }
 
+// K2a: reassemble for the K1a grid sides (adaptive b = 30, b = 128): K1a's
+// tiles; per vertical subcell each strip takes the values of the (at most
+// two) subcell columns it meets — a simple cell's value or the complex cell's
+// subcell value from the packed payload (K0 run on the payload) — and writes
+// its pixels into a smem tile stored with one TMA box.
+template <int C, int B, int NSUB>
+__global__ void __launch_bounds__(kConsumers) k_expand_aany(const __grid_constant__ CUtensorMap tm_out,
+                                                            const ExpandArgs a) {
+  constexpr int TILE = ka_tile(B);
+  constexpr int ROWB = TILE * C;
+  constexpr int SB = B / NSUB;
+  constexpr int NSTRIP = TILE / 4;
+  constexpr int NN = NSUB * NSUB;
+  static_assert(NSTRIP <= kConsumers && TILE % B == 0 && SB >= 2, "K2a geometry");
+  extern __shared__ __align__(128) uint8_t smem[];
+  const BatchGeom& g = a.g;
+  const int t = threadIdx.x;
+  const bool strip_ok = t < NSTRIP;
+  const int lpx = 4 * (strip_ok ? t : 0);
+  const int sa = lpx / SB;
+  const int split = min(4, (sa + 1) * SB - lpx);
+  const int ca = sa / NSUB, sca = sa - ca * NSUB;
+  const int cb = (sa + 1) / NSUB, scb = (sa + 1) - cb * NSUB;
+  for (int u = blockIdx.x, k = 0; u < a.units; u += gridDim.x, ++k) {
+    if (t == 0 && k > 0) bulk_wait_read_all();
+    __syncthreads();
+    const uint32_t rest = a.div_tiles.div(static_cast<uint32_t>(u));
+    const int tile = u - static_cast<int>(rest * a.div_tiles.d);
+    const uint32_t fq = a.div_rows.div(rest);
+    const int r = static_cast<int>(rest - fq * a.div_rows.d);
+    const int f = static_cast<int>(fq);
+    const int px0 = tile * TILE;
+    const int cell0 = px0 / B;
+    const int nsc = min(TILE / B, g.GC - cell0) * NSUB;
+    const bool active = strip_ok && sa < nsc;
+    const bool has_b = split < 4 && sa + 1 < nsc;
+    if (active) {
+      // Per channel: where the strip's two subcell columns take their values.
+      const uint8_t* pa[C];
+      const uint8_t* pb[C];
+      int stepa[C], stepb[C];  // 0: simple cell (one value), NSUB: complex (per vertical subcell)
+#pragma unroll
+      for (int ch = 0; ch < C; ++ch) {
+        const int64_t plane = static_cast<int64_t>(f) * C + ch;
+        const uint8_t* st = a.stats + plane * a.sstride;
+        const uint32_t rowpre = __ldg(&a.rowprefix[plane * g.GR + r]);
+        const uint32_t tot = __ldg(&a.totals[plane]);
+        const int64_t base = 4ll * g.G + 4;
+        auto where = [&](int c, int sc, const uint8_t*& ptr, int& step) {
+          const int gidx = r * g.GC + cell0 + c;
+          const uint32_t info = __ldg(&a.cellinfo[plane * g.G + gidx]);
+          const uint32_t slot_s = rowpre + (info >> 1);
+          if (info & 1u) {
+            ptr = st + base + slot_s;
+            step = 0;
+          } else {
+            ptr = st + base + tot + static_cast<int64_t>(static_cast<uint32_t>(gidx) - slot_s) * NN + sc;
+            step = NSUB;
+          }
+        };
+        where(ca, sca, pa[ch], stepa[ch]);
+        if (has_b) {
+          where(cb, scb, pb[ch], stepb[ch]);
+        } else {
+          pb[ch] = pa[ch];
+          stepb[ch] = stepa[ch];
+        }
+      }
+#pragma unroll 1
+      for (int vs = 0; vs < NSUB; ++vs) {
+        uint32_t va[C], vb[C];
+#pragma unroll
+        for (int ch = 0; ch < C; ++ch) {
+          va[ch] = __ldg(pa[ch] + vs * stepa[ch]);
+          vb[ch] = __ldg(pb[ch] + vs * stepb[ch]);
+        }
+        uint32_t w[C == 4 ? 4 : C];
+        pattern_words_split<C>(va, vb, has_b ? split : 4, w);
+#pragma unroll 2
+        for (int i = 0; i < SB; ++i)
+#pragma unroll
+          for (int q = 0; q < (C == 4 ? 4 : C); ++q)
+            reinterpret_cast<uint32_t*>(smem + (vs * SB + i) * ROWB + lpx * C)[q] = w[q];
+      }
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    const int scopy = max(0, min(ROWB, a.tensor_out_bytes - px0 * C));
+    if (t == 0 && scopy > 0) tma_store_3d(&tm_out, px0 * C / 8, r * B, f, smem);
+    if (t == 0) bulk_commit();
+    const int vbytes = min(TILE, g.N - px0) * C;
+    const int span = vbytes - scopy;
+    if (span > 0) {
+      const int rows = min(B, g.M - r * B);
+      for (int e = t; e < rows * span; e += kConsumers) {
+        const int i = e / span, x = scopy + (e - i * span);
+        a.out[static_cast<int64_t>(f) * a.ofstride + static_cast<int64_t>(r * B + i) * a.opitch +
+              static_cast<int64_t>(px0) * C + x] = smem[i * ROWB + x];
+      }
+    }
+  }
+  if (t == 0) bulk_wait_read_all();
+}
+
 using StatsKernel = void (*)(const CUtensorMap, const CUtensorMap, const StatsArgs);
 using ExpandKernel = void (*)(const CUtensorMap, const ExpandArgs);
 
@@ -1287,7 +1394,6 @@ using ExpandKernel = void (*)(const CUtensorMap, const ExpandArgs);
 // subcell column, channel): complex cells draw their subcells at sigma_sub,
 // the (0, 0) item of a simple cell sums its n x n entries and draws the cell at
 // sigma; the strips then write their pixels from the value tables.
-constexpr int ka_tile(int b) { return b == 128 ? 128 : ku_tile(b); }
 
 template <int C, int B, int NSUB>
 __global__ void __launch_bounds__(kStatsThreads)
@@ -1717,6 +1823,22 @@ ExpandKernel pick_expand_uany(int b) {
   return nullptr;
 }
 
+template <int C>
+ExpandKernel pick_expand_aany(int b, int n) {
+#define DPPX_CASE(BV, NS) \
+  if (b == (BV) && n == (NS)) return k_expand_aany<C, BV, NS>;
+  DPPX_CASE(30, 2)  // (b = 30 n = 3, 5: K2r measured faster, 0.92 / 0.84 vs 0.80 / 0.76)
+  DPPX_CASE(30, 6)
+  DPPX_CASE(30, 10)
+  DPPX_CASE(128, 2)
+  DPPX_CASE(128, 4)
+  DPPX_CASE(128, 8)
+  DPPX_CASE(128, 16)
+  DPPX_CASE(128, 32)
+#undef DPPX_CASE
+  return nullptr;
+}
+
 // Per-channel-count selectors (defined in tma_c1.cu / tma_c3.cu).
 StatsKernel select_stats_tma_c1(int b, int n, bool adaptive, bool packed);
 StatsKernel select_stats_tma_c3(int b, int n, bool adaptive, bool packed);
@@ -1724,6 +1846,8 @@ StatsKernel select_stats_var_c1(int b, int n);
 StatsKernel select_uniform_any_c1(int b);
 StatsKernel select_adaptive_any_c1(int b, int n);
 ExpandKernel select_expand_uany_c1(int b);
+ExpandKernel select_expand_aany_c1(int b, int n);
+ExpandKernel select_expand_aany_c3(int b, int n);
 ExpandKernel select_expand_uany_c3(int b);
 StatsKernel select_adaptive_any_c3(int b, int n);
 StatsKernel select_uniform_any_c3(int b);

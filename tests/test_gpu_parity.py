@@ -783,7 +783,7 @@ def test_uniform_any_grid_side_on_tma_path(ctx, C, b):
 
 
 @pytest.mark.parametrize("C", [1, 3])
-@pytest.mark.parametrize("b,n", [(30, 2), (30, 3), (30, 5), (30, 6), (30, 10), (128, 32)])
+@pytest.mark.parametrize("b,n", [(30, 2), (30, 3), (30, 5), (30, 6), (30, 10), (128, 32), (128, 8)])
 def test_adaptive_any_grid_side_on_tma_path(ctx, C, b, n):
     """K1a: adaptive for b = 30 and PPM-100's b = 128 (tiles of whole cells,
     strips split at subcell boundaries, per-CTA subcell tables). Mixed simple /
@@ -800,7 +800,8 @@ def test_adaptive_any_grid_side_on_tma_path(ctx, C, b, n):
         seeds = dp.plane_seeds(b + n, F, C)
         ctx.reset_stats()
         pls, img = ctx.pixelize_adaptive(frames, masks, p, dp.NOISE_KEYED, seeds)
-        assert ctx.stats()["launches"]["stats_tma"] >= 1, ctx.stats()["launches"]
+        if (b, n) != (128, 8):  # (K1r keeps b = 128 with n <= 16; its K2 is K2a)
+            assert ctx.stats()["launches"]["stats_tma"] >= 1, ctx.stats()["launches"]
         rp, ri = _oracle_adaptive(frames, masks, p, "keyed", seeds)
         assert pls == rp and np.array_equal(img, ri), (M, N)
         assert np.array_equal(ctx.reassemble(pls, M, N, b, n, channels=C, frames=F), ri), (M, N)
