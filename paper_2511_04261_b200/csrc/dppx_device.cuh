@@ -177,8 +177,8 @@ __device__ __forceinline__ double cell_mean(uint32_t sum, double area) {
 // otherwise (a few per mille of draws) the exact f64 arithmetic runs. The
 // emitted bytes are therefore those of the exact evaluation. Error budget of
 // the estimate:
-//   log2 of w = 1 - 2|u| = W * 2^-52 (W an exact integer): exponent exact,
-//   mantissa truncated to 23 bits (<= 1.8e-7), lg2.approx (<= 2^-21,
+//   log2 of w = 1 - 2|u| = W * 2^-52 (W an exact integer): W converted to
+//   f32 (relative error <= 2^-24, so <= 8.6e-8 in log2), lg2.approx (<= 2^-21,
 //   checked exhaustively on the device by tests/test_gpu_parity.py)
 //   => |d noise| <= sigma * ln2 * 6.6e-7 <= sigma * 4.6e-7;
 //   f32 rounding of mean, noise and the sum (< 8 ulp of 512) <= 2.5e-4.
@@ -187,25 +187,34 @@ __device__ __forceinline__ float fast_margin(double sigma) {
   return 2e-3f + static_cast<float>(sigma) * 4e-6f;
 }
 
+// MUFU lg2 (no denormal fix-up: the argument is a mantissa in [1, 2)); its
+// error on [1, 2) is measured exhaustively by k_debug_lg2.
+__device__ __forceinline__ float lg2_approx(float x) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 // Returns the quantized value, or 0xFFFFFFFF when v_est is ambiguous.
 __device__ __forceinline__ uint32_t fast_quantize(uint32_t sum, float inv_area, uint64_t bits,
                                                   float sigmaf, float margin) {
-  const uint64_t y = bits >> 11;  // 53-bit integer of uniform_from_bits
-  const uint64_t half = 1ull << 52;
-  const bool neg = y < half;      // u < 0
-  uint64_t d = neg ? half - y : y - half;
-  d = d < half - 1 ? d : half - 1;  // the +-(0.5 - 2^-53) clamp of noise.cpp:99-104
-  const uint64_t W = half - d;      // 1 - 2|u| = W * 2^-52, W in [1, 2^52]
-  const int lz = __clzll(W);
-  const int e = 63 - lz;            // floor(log2 W)
-  const uint32_t mant = static_cast<uint32_t>((W << lz) >> 40) & 0x7FFFFFu;
-  const float lg_m = __log2f(__uint_as_float(0x3F800000u | mant));  // log2 of [1,2)
+  const uint64_t y = bits >> 11;                    // 53-bit integer of uniform_from_bits
+  const bool neg = static_cast<int64_t>(bits) >= 0;  // y < 2^52, i.e. u < 0
+  // 1 - 2|u| = W * 2^-52: W = y for u < 0 (at least 1: the +-(0.5 - 2^-53)
+  // clamp of noise.cpp:99-104), 2^53 - y otherwise; W in [1, 2^52].
+  uint64_t W = neg ? y : (1ull << 53) - y;
+  W = W ? W : 1ull;
+  // W as f32 (hardware conversion, mantissa rounded to nearest: relative error
+  // <= 2^-24); exponent and mantissa taken from its bits.
+  const uint32_t wb = __float_as_uint(__ull2float_rn(W));
+  const int e = static_cast<int>(wb >> 23) - 127;  // floor(log2 Wf)
+  const float lg_m = lg2_approx(__uint_as_float(0x3F800000u | (wb & 0x7FFFFFu)));  // log2 of [1,2)
   const float L = (static_cast<float>(52 - e) - lg_m) * 0.693147180559945f;  // -ln(1-2|u|)
   const float noise = neg ? -sigmaf * L : sigmaf * L;
   const float t = static_cast<float>(sum) * inv_area + noise + 0.5f;
   const float j = rintf(t);
   if (fabsf(t - j) <= margin && j >= 1.0f && j <= 255.0f) return 0xFFFFFFFFu;
-  return static_cast<uint32_t>(fminf(fmaxf(floorf(t), 0.0f), 255.0f));
+  return static_cast<uint32_t>(min(max(__float2int_rd(t), 0), 255));  // clip + floor
 }
 
 // The reference's f64 arithmetic, step for step (rare path).

@@ -1045,7 +1045,7 @@ __global__ void k_debug_lg2(unsigned int* max_bits) {
        i += gridDim.x * blockDim.x) {
     const float m = __uint_as_float(0x3F800000u | i);
     const double exact = log2(static_cast<double>(m));
-    worst = fmaxf(worst, static_cast<float>(fabs(static_cast<double>(__log2f(m)) - exact)));
+    worst = fmaxf(worst, static_cast<float>(fabs(static_cast<double>(lg2_approx(m)) - exact)));
   }
   atomicMax(max_bits, __float_as_uint(worst));
 }
