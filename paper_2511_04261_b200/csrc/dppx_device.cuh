@@ -199,14 +199,14 @@ __device__ __forceinline__ float lg2_approx(float x) {
 __device__ __forceinline__ uint32_t fast_quantize(uint32_t sum, float inv_area, uint64_t bits,
                                                   float sigmaf, float margin) {
   const uint64_t y = bits >> 11;                    // 53-bit integer of uniform_from_bits
-  const bool neg = static_cast<int64_t>(bits) >= 0;  // y < 2^52, i.e. u < 0
+  const bool neg = static_cast<int32_t>(bits >> 32) >= 0;  // y < 2^52, i.e. u < 0
   // 1 - 2|u| = W * 2^-52: W = y for u < 0 (at least 1: the +-(0.5 - 2^-53)
-  // clamp of noise.cpp:99-104), 2^53 - y otherwise; W in [1, 2^52].
-  uint64_t W = neg ? y : (1ull << 53) - y;
-  W = W ? W : 1ull;
+  // clamp of noise.cpp:99-104, applied below on the f32 value), 2^53 - y
+  // otherwise; W in [1, 2^52].
+  const uint64_t W = neg ? y : (1ull << 53) - y;
   // W as f32 (hardware conversion, mantissa rounded to nearest: relative error
-  // <= 2^-24); exponent and mantissa taken from its bits.
-  const uint32_t wb = __float_as_uint(__ull2float_rn(W));
+  // <= 2^-24; W = 0 becomes 1); exponent and mantissa taken from its bits.
+  const uint32_t wb = __float_as_uint(fmaxf(__ull2float_rn(W), 1.0f));
   const int e = static_cast<int>(wb >> 23) - 127;  // floor(log2 Wf)
   const float lg_m = lg2_approx(__uint_as_float(0x3F800000u | (wb & 0x7FFFFFu)));  // log2 of [1,2)
   const float L = (static_cast<float>(52 - e) - lg_m) * 0.693147180559945f;  // -ln(1-2|u|)
