@@ -308,7 +308,7 @@ __device__ __forceinline__ void group_values(const StatsArgs& a, const DrawEnv& 
 }
 
 template <int C, int B4, int NSUB, bool ADAPTIVE, bool PACKED, bool VAR = false>
-__global__ void __launch_bounds__(kStatsThreads)
+__global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? 6 : 0)
     k_stats_tma(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
                 const StatsArgs a) {
   constexpr int B = 4 * B4;
