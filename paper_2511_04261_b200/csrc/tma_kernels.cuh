@@ -1050,8 +1050,15 @@ __global__ void __launch_bounds__(kStatsThreads)
     named_bar_sync(1, kConsumers);
     // One draw per (cell, channel): channel-major items so a warp's statistic
     // stores are contiguous in each plane.
-    for (int item = t; item < ncell * C; item += kConsumers) {
-      const int ch = item / ncell, c = item - ch * ncell;
+    // Channel-major items. Small cells (many draws per unit): the compile-time
+    // tile cell count as divisor, skipping cells past the frame (last tile);
+    // larger cells: the runtime count (measured faster there, e.g. b = 11).
+    constexpr bool kStaticItems = B <= 8;
+    const int icell = kStaticItems ? NCELL : ncell;
+    for (int item = t; item < icell * C; item += kConsumers) {
+      const int ch = kStaticItems ? item / NCELL : item / ncell;
+      const int c = item - ch * icell;
+      if (kStaticItems && c >= ncell) continue;
       const int gc = cell0 + c, gidx = p.r * g.GC + gc;
       const uint32_t sum = cellsum[c * C + ch];
       cellsum[c * C + ch] = 0;  // ready for the next unit
