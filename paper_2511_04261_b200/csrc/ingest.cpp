@@ -259,14 +259,16 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
         // ---- records + reconstruct check (cli.cpp:132-146), on the GPU ----
         std::vector<std::vector<uint8_t>> recs(F);
         if (cfg.mode != BatchMode::reference) {
-          for (int k = 0; k < F; ++k) {
+          std::vector<char> enc_ok(F, 1);
+          parallel_over(F, io, [&](int k) {  // header + CRC32 per file, independent
             recs[k].resize(dppx_record_size(lens[k]));
             size_t len = 0;
-            if (dppx_encode_record(M, N, cfg.b, n, cfg.mode == BatchMode::adaptive ? 2 : 1,
-                                   stats.data() + k * cap, lens[k], recs[k].data(), recs[k].size(),
-                                   &len) != DPPX_OK)
-              throw std::invalid_argument("encode: payload inconsistent");
-          }
+            enc_ok[k] = dppx_encode_record(M, N, cfg.b, n, cfg.mode == BatchMode::adaptive ? 2 : 1,
+                                           stats.data() + k * cap, lens[k], recs[k].data(), recs[k].size(),
+                                           &len) == DPPX_OK;
+          });
+          for (int k = 0; k < F; ++k)
+            if (!enc_ok[k]) throw std::invalid_argument("encode: payload inconsistent");
           if (cfg.reconstruct_check) {
             HostBuf rebuilt(plane * F);
             std::vector<uint8_t> payload(cap * F);
@@ -283,8 +285,12 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
                                                   plen.data(), cfg.b, n, rebuilt.p)
                                 : dppx_broadcast_means(ctx, &d, payload.data(), cfg.b, rebuilt.p);
             if (rrc != DPPX_OK) raise_status(rrc, "reconstruct");
+            std::vector<char> same(F, 1);
+            parallel_over(F, io, [&](int k) {
+              same[k] = std::memcmp(rebuilt.p + k * plane, out.p + k * plane, plane) == 0;
+            });
             for (int k = 0; k < F; ++k)
-              if (std::memcmp(rebuilt.p + k * plane, out.p + k * plane, plane) != 0) {
+              if (!same[k]) {
                 fail(chunk[k], ConsistencyError("reconstruction does not match the emitted image for " +
                                                 inputs[chunk[k]]));
               }
