@@ -68,6 +68,8 @@ def parse():
                     help="target CPU-work seconds for the reference sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-pad-scratch", action="store_true",
+                    help="never write output row padding (A/B of dppx_ctx_set_out_pad_scratch)")
     ap.add_argument("--chunk-frames", type=int, default=0,
                     help="host pipeline frames per chunk (0 = automatic)")
     return ap.parse_args()
@@ -277,6 +279,9 @@ def main():
         return float(t.item())
 
     ctx = dp.Context(local)
+    # `out` below is the bench's own buffer: its row padding (pitch - N*C) is
+    # scratch, so rows may end on whole 32-byte sectors (dppx_ctx_set_out_pad_scratch).
+    ctx.set_out_pad_scratch(not args.no_pad_scratch)
     geom = dp.grid_dims(M, N, b)
     G = geom.grid_count()
     p = dp.make_privacy_params(eps, m, b, n)
@@ -537,7 +542,11 @@ def main():
                        "l2": (f"working set {working_set / 1e9:.4f} GB < 2 x 126 MB L2: each step timed "
                               "alone after a 512 MB write that evicts L2" if flush_l2 else
                               f"working set {working_set / 1e9:.2f} GB > 2 x 126 MB L2, no flush needed"),
-                       "parallelism": f"frame-parallel x{world}, no collective on the data path"},
+                       "parallelism": f"frame-parallel x{world}, no collective on the data path",
+                       "out_pad": ("none (N*C % 16 == 0)" if pitch == N * C else
+                                   "output row padding never written" if args.no_pad_scratch else
+                                   f"rows padded {N * C} -> {pitch} B, padding declared scratch: "
+                                   "stores end on whole 32-B sectors")},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic, "kernel": f"K1 {kfam}",

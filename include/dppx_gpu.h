@@ -158,6 +158,14 @@ int dppx_ctx_reset_stats(dppx_ctx* ctx);
 /* 1: evaluate every statistic with the reference's f64 arithmetic (no bounded
  * f32 fast path); the bytes produced are identical either way. */
 int dppx_ctx_set_exact_noise(dppx_ctx* ctx, int32_t on);
+/* Output row padding, bytes [N*C, out_pitch), of the device entry points.
+ * Default 0: stores stay within [0, round_up(N*C, 8)) of each row (the
+ * 8-byte TMA element), so up to 7 padding bytes may receive unspecified values.
+ * 1: the caller declares the padding scratch; stores may end every row on a
+ * whole 32-byte sector, [0, min(out_pitch, round_up(N*C, 32))), removing
+ * partial-sector DRAM writes. Pixels [0, N*C) are identical either way. The
+ * host entry points always use it on their own staging buffers. */
+int dppx_ctx_set_out_pad_scratch(dppx_ctx* ctx, int32_t on);
 /* Frames per pipeline chunk of the host entry points (0 = automatic). */
 int dppx_ctx_set_chunk_frames(dppx_ctx* ctx, int32_t frames);
 

@@ -120,6 +120,7 @@ ABI = {
     "dppx_ctx_reset_stats": (C.c_int, [_ctxp]),
     "dppx_ctx_set_chunk_frames": (C.c_int, [_ctxp, C.c_int32]),
     "dppx_ctx_set_exact_noise": (C.c_int, [_ctxp, C.c_int32]),
+    "dppx_ctx_set_out_pad_scratch": (C.c_int, [_ctxp, C.c_int32]),
     "dppx_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(_vp)]),
     "dppx_host_free": (None, [_vp]),
     "dppx_pixelize_uniform_dev": (C.c_int, [_ctxp, _descp, _vp, _pp, _np, _vp, _vp]),
@@ -366,6 +367,10 @@ class Context:
     def set_exact_noise(self, on: bool):
         """Force the f64 reference arithmetic for every statistic (testing)."""
         self._check(_lib.dppx_ctx_set_exact_noise(self._h, 1 if on else 0), "set_exact_noise")
+
+    def set_out_pad_scratch(self, on: bool):
+        """Declare output pitch padding scratch: rows may end on whole 32-byte sectors."""
+        self._check(_lib.dppx_ctx_set_out_pad_scratch(self._h, 1 if on else 0), "set_out_pad_scratch")
 
     def lg2_max_error(self) -> float:
         v = C.c_double()

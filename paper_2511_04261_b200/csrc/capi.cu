@@ -121,6 +121,7 @@ struct dppx_ctx {
   cudaEvent_t band_in[kMaxBands] = {}, band_comp[kMaxBands] = {};  // single-frame row bands
   int chunk_frames = 0;
   bool exact_noise = false;
+  bool out_pad_scratch = false;  // dppx_ctx_set_out_pad_scratch
   double var_tau = 0.0;  // AdaptiveVariance host calls
   // bit-packed mask transport (maskpack.h): pinned staging per slot + packer pool
   dppx::MaskPacker* packer = nullptr;
@@ -244,6 +245,20 @@ bool encode_frames_map(CUtensorMap* m, const void* base, int64_t row_bytes, int 
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<void*>(base), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Output rows for the TMA store maps: N*C bytes rounded down to 8 (the < 8
+// byte tail is stored by threads), or, when the caller declared the pitch
+// padding scratch (dppx_ctx_set_out_pad_scratch), N*C rounded up to whole
+// 32-byte sectors within the pitch: every row then ends in a full sector, with
+// no partial-sector DRAM writes and no thread-stored tail (CelebA 178 x 218:
+// K2 3.38 -> 1.63 ms, K1 80 -> 98 % of measured HBM; profiles/r01m_*).
+int64_t out_map_row_bytes(const dppx_ctx* ctx, int64_t row_bytes, int64_t opitch) {
+  if (ctx->out_pad_scratch) {
+    const int64_t r = std::min<int64_t>(opitch, (row_bytes + 31) / 32 * 32) / 8 * 8;
+    if (r >= row_bytes) return r;
+  }
+  return row_bytes / 8 * 8;
 }
 
 // ---- validation mirroring the reference's throws ----------------------------
@@ -485,11 +500,12 @@ int run_stats(dppx_ctx* ctx, StatsArgs& a) {
               (a.pack == 1 || static_cast<int64_t>(a.pack) * a.slot_stride <= stage_bytes) &&
               encode_frames_map(&tin, a.img, in_row, g.M, g.F, a.pitch, a.fstride, box_bytes, g.b);
   if (maps && a.out)
-    maps = encode_frames_map(&tout, a.out, row_bytes, g.M, g.F, a.opitch, a.ofstride, box_bytes, g.b);
+    maps = encode_frames_map(&tout, a.out, out_map_row_bytes(ctx, row_bytes, a.opitch), g.M, g.F, a.opitch, a.ofstride,
+                              box_bytes, g.b);
   if (maps && !a.out) tout = tin;
   if (maps) {
     a.tensor_in_bytes = static_cast<int>(in_row);
-    a.tensor_out_bytes = static_cast<int>(row_bytes / 8 * 8);
+    a.tensor_out_bytes = static_cast<int>(a.out ? out_map_row_bytes(ctx, row_bytes, a.opitch) : row_bytes / 8 * 8);
     a.tiles_per_row = a.pack > 1 ? 1 : (padded_px + tile - 1) / tile;
     const int64_t groups = (g.F + a.pack - 1) / a.pack;
     const int64_t units = groups * a.row_count * a.tiles_per_row;
@@ -745,9 +761,10 @@ int expand_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* stats, i
   const bool aligned = aligned16(out) && e.opitch % 16 == 0 && e.ofstride % 16 == 0;
   const int box_bytes = e.slot_px * g.C;
   if (k && aligned && box_bytes / 8 <= 256 &&
-      encode_frames_map(&tout, out, row_bytes, g.M, g.F, e.opitch, e.ofstride, box_bytes, g.b)) {
+      encode_frames_map(&tout, out, out_map_row_bytes(ctx, row_bytes, e.opitch), g.M, g.F, e.opitch, e.ofstride,
+                        box_bytes, g.b)) {
     e.tiles_per_row = e.pack > 1 ? 1 : (padded_px + tile - 1) / tile;
-    e.tensor_out_bytes = static_cast<int>(row_bytes / 8 * 8);
+    e.tensor_out_bytes = static_cast<int>(out_map_row_bytes(ctx, row_bytes, e.opitch));
     e.div_tiles = make_fastdiv(static_cast<uint32_t>(e.tiles_per_row));
     e.div_rows = make_fastdiv(static_cast<uint32_t>(g.GR));
     const int64_t groups = (g.F + e.pack - 1) / e.pack;
@@ -1292,6 +1309,13 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
     dd.out_pitch = dpitch;
     dd.out_frame_stride = dfs;
     int rc;
+    // dout is the ctx's own staging buffer: its pitch padding is scratch.
+    struct PadScratch {
+      dppx_ctx* c;
+      bool prev;
+      ~PadScratch() { c->out_pad_scratch = prev; }
+    } pad_scope{ctx, ctx->out_pad_scratch};
+    ctx->out_pad_scratch = true;
     if (pix) {
       dppx_noise cn{};
       if (nz) {
@@ -1570,6 +1594,12 @@ int dppx_ctx_reset_stats(dppx_ctx* ctx) {
 int dppx_ctx_set_chunk_frames(dppx_ctx* ctx, int32_t frames) {
   if (!ctx || frames < 0) return DPPX_ERR_INVALID;
   ctx->chunk_frames = frames;
+  return DPPX_OK;
+}
+
+int dppx_ctx_set_out_pad_scratch(dppx_ctx* ctx, int32_t on) {
+  if (!ctx) return DPPX_ERR_INVALID;
+  ctx->out_pad_scratch = on != 0;
   return DPPX_OK;
 }
 

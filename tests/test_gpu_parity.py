@@ -813,3 +813,48 @@ def test_adaptive_any_grid_side_on_tma_path(ctx, C, b, n):
         pls, img = ctx.pixelize_adaptive(frames, masks, p, dp.NOISE_NONE, None)
         rp, ri = _oracle_adaptive(frames, masks, p, "none", None)
         assert pls == rp and np.array_equal(img, ri), (M, N)
+
+
+@pytest.mark.parametrize("M,N,C,b,n", [(218, 178, 3, 16, 4), (218, 178, 3, 16, 1), (83, 1917, 3, 8, 2),
+                                       (100, 301, 1, 4, 1), (64, 250, 3, 30, 5), (40, 96, 3, 12, 3)])
+def test_out_pad_scratch_pixels_identical(ctx, M, N, C, b, n):
+    """dppx_ctx_set_out_pad_scratch: pixels [0, N*C) of every output row are
+    the same with and without it (fused K1 output and K2 reassemble); padding
+    past the row's next 8-byte boundary is untouched when it is off, past its
+    last 32-byte sector when on (include/dppx_gpu.h)."""
+    import torch
+    F = 7
+    dev = torch.device("cuda:0")
+    row = N * C
+    pitch = (row + 15) // 16 * 16
+    opitch = (row + 63) // 64 * 64 + 64  # slack past the row's last sector
+    mpitch = (N + 15) // 16 * 16
+    d = dp._desc(M, N, C, F, pitch=pitch, mpitch=mpitch, opitch=opitch)
+    img = torch.empty((F, M, pitch), dtype=torch.uint8, device=dev)
+    mask = torch.empty((F, M, mpitch), dtype=torch.uint8, device=dev)
+    ctx.synth_frames_dev(d, 5, 0, img, mask)
+    p = dp.make_privacy_params(0.5, 16, b, n)
+    cap = dp.adaptive_payload_capacity(M, N, b, n)
+    stride = (cap + 15) // 16 * 16
+    nz, keep = dp.Context._noise(dp.NOISE_KEYED, dp.plane_seeds(42, F, C))
+    outs = {}
+    try:
+        for on in (False, True):
+            ctx.set_out_pad_scratch(on)
+            payload = torch.zeros((F * C, stride), dtype=torch.uint8, device=dev)
+            lens = torch.zeros(F * C, dtype=torch.int32, device=dev)
+            o1 = torch.full((F, M, opitch), 0xA5, dtype=torch.uint8, device=dev)
+            o2 = torch.full_like(o1, 0xA5)
+            ctx.pixelize_adaptive_dev(d, img, mask, p, nz, payload, stride, lens, o1)
+            ctx.reassemble_dev(d, payload, stride, lens, b, n, o2)
+            ctx.synchronize()
+            outs[on] = (o1.cpu().numpy(), o2.cpu().numpy())
+    finally:
+        ctx.set_out_pad_scratch(False)
+    sector_end = min(opitch, (row + 31) // 32 * 32)
+    for k in range(2):
+        off, on = outs[False][k], outs[True][k]
+        assert np.array_equal(off[:, :, :row], on[:, :, :row])
+        assert np.array_equal(off[:, :, :row], outs[False][0][:, :, :row])
+        assert (off[:, :, min(opitch, (row + 7) // 8 * 8):] == 0xA5).all()
+        assert (on[:, :, sector_end:] == 0xA5).all()
