@@ -229,9 +229,36 @@ def reference_arm(args, wl):
 # ----------------------------------------------------------------------------
 # our arm
 # ----------------------------------------------------------------------------
+def free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def self_spawn(args):
+    """`bench.py --gpus N` (N > 1) outside torchrun: re-exec under
+    torch.distributed.run with N ranks on this node (one process per GPU), the
+    launch the driver itself uses; rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    sys.stdout.flush()
+    os.execvpe(cmd[0], cmd, env)
+
+
 def main():
     args = parse()
     world, rank, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        self_spawn(args)
+    if world > 1 and args.gpus != world and rank == 0:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; using {world} ranks",
+              file=sys.stderr)
     wl = WORKLOADS[args.workload]
     M, N, C, F, b, n, m, eps, adaptive, desc = wl
     if args.frames:
@@ -260,6 +287,10 @@ def main():
     if world > 1:
         import torch.distributed as tdist
         if backend == "nccl":
+            # Communicator init lines (nranks) for the driver's log; NCCL carries
+            # only the barrier and the end-of-run max/sum of timings.
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             tdist.init_process_group("nccl", device_id=dev)
         else:
             tdist.init_process_group(backend)

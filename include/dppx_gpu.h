@@ -159,8 +159,9 @@ int dppx_ctx_reset_stats(dppx_ctx* ctx);
  * f32 fast path); the bytes produced are identical either way. */
 int dppx_ctx_set_exact_noise(dppx_ctx* ctx, int32_t on);
 /* Output row padding, bytes [N*C, out_pitch), of the device entry points.
- * Default 0: stores stay within [0, round_up(N*C, 8)) of each row (the
- * 8-byte TMA element), so up to 7 padding bytes may receive unspecified values.
+ * Default 0: every kernel stores exactly the bytes [0, N*C) of each row, so
+ * the output may be a window of a larger image (neighbouring bytes are never
+ * touched; tests/test_gpu_parity.py::test_default_stores_are_window_safe).
  * 1: the caller declares the padding scratch; stores may end every row on a
  * whole 32-byte sector, [0, min(out_pitch, round_up(N*C, 32))), removing
  * partial-sector DRAM writes. Pixels [0, N*C) are identical either way. The
@@ -227,6 +228,45 @@ int dppx_pixelize_reference(dppx_ctx* ctx, const dppx_frames_desc* desc, const u
 int dppx_reassemble(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* payload,
                     int64_t payload_stride, const uint32_t* payload_len, int32_t b, int32_t n,
                     uint8_t* out);
+
+/* ---- multi-GPU runner (one host thread + one ctx per device) -------------
+ * The reference's multi-image parallelism is run_batch's file-level
+ * parallel_for (cli.cpp:194-211). A group owns one persistent host thread and
+ * one dppx_ctx per listed device; dppx_group_* entry points take the same
+ * arguments as the host entry points above, split the F frames into
+ * contiguous blocks (one per device) and run them concurrently. There is no
+ * collective on the data path: noise is keyed per plane / global frame, never
+ * by device, so results are byte-identical to one ctx over the whole batch.
+ * devices == NULL: every visible sm_100 device (at most `count` if count > 0).
+ * A device may be listed twice (two contexts, e.g. to test the runner on one GPU). */
+typedef struct dppx_group dppx_group;
+int dppx_group_create(const int32_t* devices, int32_t count, dppx_group** out);
+void dppx_group_destroy(dppx_group* group);
+int32_t dppx_group_size(const dppx_group* group);
+int32_t dppx_group_device(const dppx_group* group, int32_t worker);
+/* The worker's context (for configuration between group calls only). */
+dppx_ctx* dppx_group_ctx(dppx_group* group, int32_t worker);
+const char* dppx_group_last_error(const dppx_group* group);
+/* Dynamic parallel-for over the workers: each task runs once, on whichever
+ * worker thread claims it next, with that worker's ctx. Returns the status of
+ * the lowest-numbered failing task (its message in dppx_group_last_error). */
+int dppx_group_run(dppx_group* group, int32_t tasks,
+                   int (*fn)(dppx_ctx* ctx, int32_t worker, int32_t task, void* user), void* user);
+int dppx_group_pixelize_uniform(dppx_group* group, const dppx_frames_desc* desc,
+                                const uint8_t* img, const dppx_privacy_params* params,
+                                const dppx_noise* noise, uint8_t* means, uint8_t* out);
+int dppx_group_pixelize_adaptive(dppx_group* group, const dppx_frames_desc* desc,
+                                 const uint8_t* img, const uint8_t* mask,
+                                 const dppx_privacy_params* params, const dppx_noise* noise,
+                                 uint8_t* payload, int64_t payload_stride, uint32_t* payload_len,
+                                 uint8_t* out);
+int dppx_group_broadcast_means(dppx_group* group, const dppx_frames_desc* desc,
+                               const uint8_t* means, int32_t b, uint8_t* out);
+int dppx_group_reassemble(dppx_group* group, const dppx_frames_desc* desc, const uint8_t* payload,
+                          int64_t payload_stride, const uint32_t* payload_len, int32_t b,
+                          int32_t n, uint8_t* out);
+/* Launch counts and transfer bytes summed over the workers; device_ms is the max. */
+int dppx_group_get_stats(dppx_group* group, dppx_kernel_stats* out);
 
 /* classify_regions (adaptive.cpp:34-65) of F masks (desc mask fields; channels
  * ignored): per-frame G float mask means at mask_means + f*G. */

@@ -154,6 +154,20 @@ ABI = {
     "dppx_reconstruct_record": (C.c_int, [_ctxp, _vp, C.c_size_t, _vp, C.c_size_t]),
     "dppx_debug_device_laplace": (C.c_int, [_ctxp, C.c_uint64, _vp, C.c_int32, C.c_double, _vp]),
     "dppx_debug_lg2_max_error": (C.c_int, [_ctxp, C.POINTER(C.c_double)]),
+    "dppx_group_create": (C.c_int, [C.POINTER(C.c_int32), C.c_int32, C.POINTER(_vp)]),
+    "dppx_group_destroy": (None, [_vp]),
+    "dppx_group_size": (C.c_int32, [_vp]),
+    "dppx_group_device": (C.c_int32, [_vp, C.c_int32]),
+    "dppx_group_ctx": (_ctxp, [_vp, C.c_int32]),
+    "dppx_group_last_error": (C.c_char_p, [_vp]),
+    "dppx_group_run": (C.c_int, [_vp, C.c_int32, _vp, _vp]),
+    "dppx_group_pixelize_uniform": (C.c_int, [_vp, _descp, _vp, _pp, _np, _vp, _vp]),
+    "dppx_group_pixelize_adaptive": (C.c_int, [_vp, _descp, _vp, _vp, _pp, _np, _vp, C.c_int64,
+                                               _vp, _vp]),
+    "dppx_group_broadcast_means": (C.c_int, [_vp, _descp, _vp, C.c_int32, _vp]),
+    "dppx_group_reassemble": (C.c_int, [_vp, _descp, _vp, C.c_int64, _vp, C.c_int32, C.c_int32,
+                                        _vp]),
+    "dppx_group_get_stats": (C.c_int, [_vp, C.POINTER(KernelStats)]),
 }
 for _name, (_res, _args) in ABI.items():
     _f = getattr(_lib, _name)
@@ -345,7 +359,14 @@ class Context:
 
     def _check(self, rc, who):
         if rc != OK:
-            _raise(rc, f"{who}: {_lib.dppx_ctx_last_error(self._h).decode()}")
+            _raise(rc, f"{who}: {self._last_error()}")
+
+    def _last_error(self) -> str:
+        return _lib.dppx_ctx_last_error(self._h).decode()
+
+    @staticmethod
+    def _api(name):  # host entry point of one context (Group: of a device group)
+        return getattr(_lib, "dppx_" + name)
 
     # ---- plumbing
     @property
@@ -419,7 +440,7 @@ class Context:
         out = _out_image(frames, out, want_image)
         nz, keep = self._noise(noise, seeds, frame_base, injected)
         d = _desc(M, N, Cn, F)
-        self._check(_lib.dppx_pixelize_uniform(self._h, C.byref(d), _ptr(frames), C.byref(params),
+        self._check(self._api("pixelize_uniform")(self._h, C.byref(d), _ptr(frames), C.byref(params),
                                                C.byref(nz), _ptr(means), _ptr(out)),
                     "pixelize_uniform")
         del keep
@@ -439,7 +460,7 @@ class Context:
         out = _out_image(frames, out, want_image)
         nz, keep = self._noise(noise, seeds, frame_base, injected)
         d = _desc(M, N, Cn, F)
-        self._check(_lib.dppx_pixelize_adaptive(self._h, C.byref(d), _ptr(frames), _ptr(masks),
+        self._check(self._api("pixelize_adaptive")(self._h, C.byref(d), _ptr(frames), _ptr(masks),
                                                 C.byref(params), C.byref(nz), _ptr(buf), stride,
                                                 _ptr(lens), _ptr(out)), "pixelize_adaptive")
         del keep
@@ -498,7 +519,7 @@ class Context:
         means = np.ascontiguousarray(means, dtype=np.uint8)
         out = np.zeros((frames, M, N, channels), np.uint8)
         d = _desc(M, N, channels, frames)
-        self._check(_lib.dppx_broadcast_means(self._h, C.byref(d), _ptr(means), b, _ptr(out)),
+        self._check(self._api("broadcast_means")(self._h, C.byref(d), _ptr(means), b, _ptr(out)),
                     "broadcast_means")
         return out
 
@@ -512,7 +533,7 @@ class Context:
         lens = np.array([len(p) for p in payloads], np.uint32)
         out = np.zeros((frames, M, N, channels), np.uint8)
         d = _desc(M, N, channels, frames)
-        self._check(_lib.dppx_reassemble(self._h, C.byref(d), _ptr(buf), stride,
+        self._check(self._api("reassemble")(self._h, C.byref(d), _ptr(buf), stride,
                                          _ptr(lens) if check_lengths else None, b, n, _ptr(out)),
                     "reassemble")
         return out
@@ -589,6 +610,83 @@ class Context:
 
 
 _tls = threading.local()
+
+
+class Group(Context):
+    """A multi-GPU runner (dppx_group_*): one persistent host thread and one
+    context per device; the host entry points of :class:`Context`
+    (pixelize_uniform / pixelize_adaptive / broadcast_means / reassemble)
+    split their frames into contiguous per-device blocks with no collective.
+    Results are byte-identical to one Context (noise is keyed per plane).
+    ``devices=None``: every visible sm_100 device; a device may repeat."""
+
+    def __init__(self, devices=None):
+        h = _vp()
+        if devices is None:
+            rc = _lib.dppx_group_create(None, 0, C.byref(h))
+        else:
+            arr = (C.c_int32 * len(devices))(*devices)
+            rc = _lib.dppx_group_create(arr, len(devices), C.byref(h))
+        if rc != OK:
+            _raise(rc, f"dppx_group_create({devices}) failed with status {rc}")
+        self._g = h
+        self._h = h  # the entry points take the group handle in the ctx position
+        self.devices = [_lib.dppx_group_device(h, i) for i in range(_lib.dppx_group_size(h))]
+        self.device = self.devices[0]
+
+    def close(self):
+        if getattr(self, "_g", None):
+            _lib.dppx_group_destroy(self._g)
+            self._g = self._h = None
+
+    def _last_error(self) -> str:
+        return _lib.dppx_group_last_error(self._g).decode()
+
+    @staticmethod
+    def _api(name):
+        return getattr(_lib, "dppx_group_" + name)
+
+    def worker_context(self, i: int) -> "Context":
+        """Non-owning view of worker i's context (configure it between group calls)."""
+        c = Context.__new__(Context)
+        c._h = _lib.dppx_group_ctx(self._g, i)
+        c.device = self.devices[i]
+        c.close = lambda: None
+        return c
+
+    def stats(self) -> dict:
+        s = KernelStats()
+        _lib.dppx_group_get_stats(self._g, C.byref(s))
+        return {"launches": {k: int(s.launches[i]) for i, k in enumerate(KERNEL_FAMILIES)},
+                "device_ms": {k: float(s.device_ms[i]) for i, k in enumerate(KERNEL_FAMILIES)},
+                "h2d_bytes": int(s.h2d_bytes), "d2h_bytes": int(s.d2h_bytes)}
+
+    def reset_stats(self):
+        for i in range(len(self.devices)):
+            _lib.dppx_ctx_reset_stats(_lib.dppx_group_ctx(self._g, i))
+
+    def synchronize(self):
+        for i in range(len(self.devices)):
+            self._check(_lib.dppx_ctx_synchronize(_lib.dppx_group_ctx(self._g, i)), "synchronize")
+
+    def set_timing(self, on: bool):
+        for i in range(len(self.devices)):
+            _lib.dppx_ctx_set_timing(_lib.dppx_group_ctx(self._g, i), 1 if on else 0)
+
+
+def _group_unsupported(name):
+    def f(self, *a, **k):
+        raise NotImplementedError(f"Group.{name}: use worker_context(i).{name} (per-device call)")
+    return f
+
+
+for _name in ("stream", "set_stream", "set_chunk_frames", "set_exact_noise", "set_out_pad_scratch",
+              "lg2_max_error", "pixelize_reference", "pixelize_adaptive_variance",
+              "reconstruct_record", "classify_regions", "metrics", "device_laplace",
+              "pixelize_adaptive_dev", "pixelize_uniform_dev", "pixelize_adaptive_variance_dev",
+              "reassemble_dev", "broadcast_means_dev", "synth_frames_dev"):
+    setattr(Group, _name, property(lambda self, _n=_name: _group_unsupported(_n).__get__(self))
+            if _name == "stream" else _group_unsupported(_name))
 
 
 def default_context() -> Context:

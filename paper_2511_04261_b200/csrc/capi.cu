@@ -112,7 +112,9 @@ struct dppx_ctx {
   size_t seeds_pinned_n = 0;
   cudaEvent_t seeds_ev = nullptr;
   // host-pipeline staging (2 slots)
-  DevBuf img[2], mask[2], out[2], stats[2], lens[2], inj[2], sd[2], dense[2], dense_mask[2];
+  DevBuf img[2], mask[2], out[2], stats[2], lens[2], inj[2], sd[2], dense[2], dense_out[2],
+      dense_mask[2];  // dense (input) and dense_out never alias: chunk ci+2's H2D may run
+                      // while chunk ci's D2H is still reading its output
   DevBuf var_flags, var_stage;  // fused variance classification staging
   uint64_t* sd_pinned[2] = {nullptr, nullptr};
   size_t sd_pinned_n[2] = {0, 0};
@@ -236,7 +238,7 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 bool encode_frames_map(CUtensorMap* m, const void* base, int64_t row_bytes, int M, int F,
                        int64_t pitch, int64_t fstride, int box_bytes, int box_rows) {
   auto enc = tensor_map_encoder();
-  if (!enc || row_bytes < 8) return false;
+  if (!enc || row_bytes < 16) return false;
   const cuuint64_t dims[3] = {static_cast<cuuint64_t>(row_bytes / 8), static_cast<cuuint64_t>(M),
                               static_cast<cuuint64_t>(F)};
   const cuuint64_t strides[2] = {static_cast<cuuint64_t>(pitch), static_cast<cuuint64_t>(fstride)};
@@ -247,18 +249,22 @@ bool encode_frames_map(CUtensorMap* m, const void* base, int64_t row_bytes, int 
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Output rows for the TMA store maps: N*C bytes rounded down to 8 (the < 8
-// byte tail is stored by threads), or, when the caller declared the pitch
+// Output rows for the TMA store maps: N*C bytes rounded down to 16 (the < 16
+// byte tail is stored by threads; the TMA unit moves whole 16-byte granules,
+// so an extent that ends mid-granule -- an odd number of 8-byte elements --
+// would let a box store write up to 8 bytes past the row: measured, and
+// pinned by tests/test_gpu_parity.py::test_default_stores_are_window_safe),
+// or, when the caller declared the pitch
 // padding scratch (dppx_ctx_set_out_pad_scratch), N*C rounded up to whole
 // 32-byte sectors within the pitch: every row then ends in a full sector, with
 // no partial-sector DRAM writes and no thread-stored tail (CelebA 178 x 218:
 // K2 3.38 -> 1.63 ms, K1 80 -> 98 % of measured HBM; profiles/r01m_*).
 int64_t out_map_row_bytes(const dppx_ctx* ctx, int64_t row_bytes, int64_t opitch) {
   if (ctx->out_pad_scratch) {
-    const int64_t r = std::min<int64_t>(opitch, (row_bytes + 31) / 32 * 32) / 8 * 8;
+    const int64_t r = std::min<int64_t>(opitch, (row_bytes + 31) / 32 * 32) / 16 * 16;
     if (r >= row_bytes) return r;
   }
-  return row_bytes / 8 * 8;
+  return row_bytes / 16 * 16;
 }
 
 // ---- validation mirroring the reference's throws ----------------------------
@@ -376,7 +382,8 @@ struct VarianceSource {  // extension: classify cells by the frames' own varianc
 int classify(dppx_ctx* ctx, const BatchGeom& g, int planes, bool from_payload, const uint8_t* mask,
              int64_t mpitch, int64_t mfstride, uint8_t* payload, const uint8_t* payload_in,
              int64_t pstride, uint32_t* payload_len, const uint32_t* in_len,
-             const VarianceSource* var = nullptr, bool mask_bits = false) {
+             const VarianceSource* var = nullptr, bool mask_bits = false,
+             int64_t plen_limit = -1) {
   ClassifyArgs a{};
   a.g = g;
   a.planes = planes;
@@ -415,6 +422,7 @@ int classify(dppx_ctx* ctx, const BatchGeom& g, int planes, bool from_payload, c
   a.payload = payload;
   a.payload_in = payload_in;
   a.pstride = pstride;
+  a.plen_limit = plen_limit < 0 ? pstride : plen_limit;
   a.payload_len = payload_len;
   a.in_len = in_len;
   a.cellinfo = static_cast<uint32_t*>(ctx->cellinfo.p);
@@ -495,7 +503,9 @@ int run_stats(dppx_ctx* ctx, StatsArgs& a) {
   // Input rows: the tensor's inner extent is rounded UP to 8 bytes when the
   // pitch has slack (the stray bytes past N*C are overwritten by the mirror
   // fill), so no row tail has to be gathered from global memory.
-  const int64_t in_row = a.row_slack ? round_up(row_bytes, 8) : row_bytes / 8 * 8;
+  // (Whole 16-byte granules, like the output maps: a load extent ending
+  // mid-granule could touch up to 8 bytes past the row.)
+  const int64_t in_row = a.row_slack ? round_up(row_bytes, 16) : row_bytes / 16 * 16;
   bool maps = k && aligned && g.F > 0 && box_bytes / 8 <= 256 && g.b <= 256 &&
               (a.pack == 1 || static_cast<int64_t>(a.pack) * a.slot_stride <= stage_bytes) &&
               encode_frames_map(&tin, a.img, in_row, g.M, g.F, a.pitch, a.fstride, box_bytes, g.b);
@@ -505,7 +515,7 @@ int run_stats(dppx_ctx* ctx, StatsArgs& a) {
   if (maps && !a.out) tout = tin;
   if (maps) {
     a.tensor_in_bytes = static_cast<int>(in_row);
-    a.tensor_out_bytes = static_cast<int>(a.out ? out_map_row_bytes(ctx, row_bytes, a.opitch) : row_bytes / 8 * 8);
+    a.tensor_out_bytes = static_cast<int>(a.out ? out_map_row_bytes(ctx, row_bytes, a.opitch) : row_bytes / 16 * 16);
     a.tiles_per_row = a.pack > 1 ? 1 : (padded_px + tile - 1) / tile;
     const int64_t groups = (g.F + a.pack - 1) / a.pack;
     const int64_t units = groups * a.row_count * a.tiles_per_row;
@@ -698,7 +708,9 @@ int pixelize_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img, c
 }
 
 int expand_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* stats, int64_t sstride,
-               const uint32_t* in_len, int b, int n, uint8_t* out, bool adaptive) {
+               const uint32_t* in_len, int b, int n, uint8_t* out, bool adaptive,
+               int64_t caller_stride = -1) {
+  if (caller_stride < 0) caller_stride = sstride;
   BatchGeom g;
   if (int rc = geometry(ctx, d->height, d->width, d->channels, d->frames, b, adaptive ? n : 1, &g,
                         false)) {
@@ -722,9 +734,14 @@ int expand_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* stats, i
   if (adaptive) {
     if (sstride < 4ll * g.G + 4 || sstride % 4 != 0)
       return set_err(ctx, DPPX_ERR_INVALID, "payload_stride too small or not a multiple of 4");
+    // The shortest valid payload (every cell simple) is 5G + 4 bytes: a slot
+    // that cannot hold it holds no valid payload (adaptive.cpp:192-210).
+    if (caller_stride < 5ll * g.G + 4)
+      return set_err(ctx, DPPX_ERR_CORRUPT, "reassemble: payload shorter than its mask means imply");
     const int P = g.F * g.C;
     if (int rc = ensure_scratch(ctx, g, P)) return rc;
-    if (int rc = classify(ctx, g, P, true, nullptr, 0, 0, nullptr, stats, sstride, nullptr, in_len))
+    if (int rc = classify(ctx, g, P, true, nullptr, 0, 0, nullptr, stats, sstride, nullptr, in_len,
+                          nullptr, false, caller_stride))
       return rc;
     e.cellinfo = static_cast<const uint32_t*>(ctx->cellinfo.p);
     e.rowprefix = static_cast<const uint32_t*>(ctx->rowprefix.p);
@@ -1177,7 +1194,9 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
     if (ensure(ctx, ctx->stats[s], static_cast<size_t>(dstride) * C * K)) return DPPX_ERR_OOM;
     if (ensure(ctx, ctx->lens[s], sizeof(uint32_t) * C * K)) return DPPX_ERR_OOM;
     if (inj && ensure(ctx, ctx->inj[s], sizeof(double) * inj_plane * C * K)) return DPPX_ERR_OOM;
-    if ((dense_in || dense_out) && ensure(ctx, ctx->dense[s], static_cast<size_t>(row) * M * K))
+    if (dense_in && ensure(ctx, ctx->dense[s], static_cast<size_t>(row) * M * K))
+      return DPPX_ERR_OOM;
+    if (dense_out && ensure(ctx, ctx->dense_out[s], static_cast<size_t>(row) * M * K))
       return DPPX_ERR_OOM;
     if (dense_mask && ensure(ctx, ctx->dense_mask[s], static_cast<size_t>(N) * M * K))
       return DPPX_ERR_OOM;
@@ -1225,6 +1244,7 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
     uint8_t* dstats = static_cast<uint8_t*>(ctx->stats[s].p);
     uint32_t* dlens = static_cast<uint32_t*>(ctx->lens[s].p);
     uint8_t* ddense = static_cast<uint8_t*>(ctx->dense[s].p);
+    uint8_t* ddense_out = static_cast<uint8_t*>(ctx->dense_out[s].p);
     uint8_t* ddmask = static_cast<uint8_t*>(ctx->dense_mask[s].p);
     if (pix && stage_in) {
       if (ci >= 2) CUDA_TRY(ctx, cudaEventSynchronize(ctx->in_done[s]));
@@ -1332,13 +1352,14 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
                         adaptive ? dlens : nullptr, out ? dout : nullptr, adaptive, ctx->sd[s],
                         ctx->sd_pinned[s], ctx->sd_pinned_n[s], ctx->comp_done[s], false, po);
     } else {
-      rc = expand_dev(ctx, &dd, dstats, dstride, in_lens ? dlens : nullptr, b, n, dout, adaptive);
+      rc = expand_dev(ctx, &dd, dstats, dstride, in_lens ? dlens : nullptr, b, n, dout, adaptive,
+                      sstride);
     }
     if (rc) return rc;
     if (dense_out) {
       PendingTiming pt;
       timing_begin(ctx, DPPX_K_AUX, &pt);
-      CUDA_TRY(ctx, launch_repitch(ddense, row, dout, dpitch, row, static_cast<int64_t>(M) * Fk, comp));
+      CUDA_TRY(ctx, launch_repitch(ddense_out, row, dout, dpitch, row, static_cast<int64_t>(M) * Fk, comp));
       timing_end(ctx, &pt);
     }
     CUDA_TRY(ctx, cudaEventRecord(ctx->comp_done[s], comp));
@@ -1366,7 +1387,7 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
       ctx->kstats.d2h_bytes += static_cast<uint64_t>(Fk) * M * row;
     } else if (out) {
       if (dense_out)
-        CUDA_TRY(ctx, cudaMemcpyAsync(out + static_cast<int64_t>(f0) * d->out_frame_stride, ddense,
+        CUDA_TRY(ctx, cudaMemcpyAsync(out + static_cast<int64_t>(f0) * d->out_frame_stride, ddense_out,
                                       static_cast<size_t>(row) * M * Fk, cudaMemcpyDeviceToHost,
                                       ctx->s_out));
       else
@@ -1518,8 +1539,8 @@ void dppx_ctx_destroy(dppx_ctx* ctx) {
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (int s = 0; s < 2; ++s) {
-    DevBuf* sb[] = {&ctx->img[s], &ctx->mask[s], &ctx->out[s], &ctx->stats[s],
-                    &ctx->lens[s], &ctx->inj[s], &ctx->sd[s], &ctx->dense[s], &ctx->dense_mask[s]};
+    DevBuf* sb[] = {&ctx->img[s], &ctx->mask[s], &ctx->out[s], &ctx->stats[s], &ctx->lens[s],
+                    &ctx->inj[s], &ctx->sd[s], &ctx->dense[s], &ctx->dense_out[s], &ctx->dense_mask[s]};
     for (DevBuf* b : sb)
       if (b->p) cudaFree(b->p);
     if (ctx->sd_pinned[s]) cudaFreeHost(ctx->sd_pinned[s]);
@@ -1557,7 +1578,17 @@ void* dppx_ctx_stream(dppx_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stre
 
 int dppx_ctx_set_stream(dppx_ctx* ctx, void* stream) {
   if (!ctx) return DPPX_ERR_INVALID;
-  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  cudaStream_t next = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  if (next != ctx->stream) {
+    // The ctx-wide scratch (work counter, cell info, row scan, seeds) may still
+    // be in use by kernels on the old stream: order the new stream after them.
+    CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    cudaEvent_t e = get_event(ctx);
+    CUDA_TRY(ctx, cudaEventRecord(e, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(next, e, 0));
+    ctx->event_pool.push_back(e);  // reusable: the wait captured the recorded state
+  }
+  ctx->stream = next;
   return DPPX_OK;
 }
 

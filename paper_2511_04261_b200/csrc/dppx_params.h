@@ -71,6 +71,7 @@ struct ClassifyArgs {
   uint8_t* payload;          // from_payload == 0: mask means + S written for C planes
   const uint8_t* payload_in; // from_payload == 1
   int64_t pstride;
+  int64_t plen_limit;        // from_payload == 1: longest legal payload (caller's stride)
   uint32_t* payload_len;     // nullable (written)
   const uint32_t* in_len;    // nullable (checked, from_payload == 1)
   uint32_t* cellinfo;        // [P][G]  (intra-row exclusive simple prefix << 1) | simple

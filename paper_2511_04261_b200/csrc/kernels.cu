@@ -418,8 +418,10 @@ __global__ void __launch_bounds__(kClassifyThreads, BAND ? 10 : 8) k_classify(co
                                   (static_cast<uint32_t>(q[2]) << 16) |
                                   (static_cast<uint32_t>(q[3]) << 24);
           // decode's simple-count and length checks (record.cpp:253-270).
-          if (stored != S || (a.in_len && a.in_len[p] != len) || len > a.pstride)
+          if (stored != S || (a.in_len && a.in_len[p] != len) || len > a.plen_limit) {
             atomicExch(a.status, DPPX_ERR_CORRUPT);
+            s_last = 2u;  // plane p is corrupt: neutralise its slots below
+          }
         } else {
           for (int ch = 0; ch < g.C; ++ch) {
             const int64_t q = (static_cast<int64_t>(p) * g.C + ch) * a.pstride + 4ll * g.G;
@@ -427,6 +429,19 @@ __global__ void __launch_bounds__(kClassifyThreads, BAND ? 10 : 8) k_classify(co
             if (a.payload_len) a.payload_len[static_cast<int64_t>(p) * g.C + ch] = len;
           }
         }
+      }
+      __syncthreads();
+      if (s_last == 2u) {
+        // Corrupt payload (reassemble throws RecordError, adaptive.cpp:192-210):
+        // the expanders launched after this kernel must not follow its slot
+        // offsets past the payload. Every cell becomes "simple, slot 0", which
+        // reads byte 4G+4 (the host requires payload_stride >= 5G+4, the
+        // shortest valid payload), and the plane's output is discarded.
+        for (int64_t i = threadIdx.x; i < g.G; i += kClassifyThreads)
+          a.cellinfo[static_cast<int64_t>(p) * g.G + i] = 1u;
+        for (int i = threadIdx.x; i < g.GR; i += kClassifyThreads)
+          a.rowprefix[static_cast<int64_t>(p) * g.GR + i] = 0u;
+        if (threadIdx.x == 0) a.totals[p] = 0u;
       }
     }
     __syncthreads();

@@ -108,7 +108,7 @@ __device__ __forceinline__ void load_unit(const StatsArgs& a, const CUtensorMap*
 }
 
 // One 3-D box store per slot: rows >= M and bytes past the tensor's row are
-// clipped by the TMA unit; the consumers write the (< 8) bytes past
+// clipped by the TMA unit; the consumers write the (< 16) bytes past
 // tensor_out_bytes.
 template <int C, int B, bool PACKED, int TILE = kTilePx>
 __device__ __forceinline__ void store_unit(const StatsArgs& a, const CUtensorMap* tm, int u,
@@ -123,7 +123,7 @@ __device__ __forceinline__ void store_unit(const StatsArgs& a, const CUtensorMap
   bulk_wait_read_all();
 }
 
-// Output bytes of a unit past the output tensor map's row extent (< 8 per row:
+// Output bytes of a unit past the output tensor map's row extent (< 16 per row:
 // the TMA store covers [0, tensor_out_bytes)), written by the 32 producer lanes.
 template <int C, int B, bool PACKED, int TILE = kTilePx>
 __device__ __forceinline__ void store_tail(const StatsArgs& a, int u, const uint8_t* st, int lane) {
@@ -1202,7 +1202,7 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
         tma_store_3d(&tm_out, px0 * C / 8, r * B, fg * pk + j, buf + j * (PACKED ? a.slot_stride : 0));
     }
     if (t == 0) bulk_commit();  // one group per unit (possibly empty)
-    // Bytes past the tensor's row extent (< 8 per row and slot), from the smem
+    // Bytes past the tensor's row extent (< 16 per row and slot), from the smem
     // tile, spread over the whole CTA (one thread per byte, not per strip).
     const int vbytes = min(slot_px, g.N - px0) * C;
     const int span = vbytes - scopy;
@@ -1222,7 +1222,7 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
 // K2u: broadcast_means for the K1u grid sides (uniform, b % 4 != 0 or b = 128):
 // K1u's tiles of whole cells; each 4-px strip takes the values of the (at most
 // two) cells it meets and writes its pixels into a smem tile, stored with one
-// 3-D TMA box (the < 8 bytes past the tensor's row extent by the CTA).
+// 3-D TMA box (the < 16 bytes past the tensor's row extent by the CTA).
 template <int C, int B>
 __global__ void __launch_bounds__(kConsumers) k_expand_uany(const __grid_constant__ CUtensorMap tm_out,
                                                             const ExpandArgs a) {

@@ -125,10 +125,52 @@ def records():
                         **{k: np.frombuffer(v, np.uint8) for k, v in recs.items()})
 
 
+def config_digests():
+    """Every BASELINE config and every kernel family's grid side, RGB, pinned
+    to the reference by sha256 (payload / means bytes and image per plane):
+    config 4 (4K adaptive b32 n8), all 12 sweep runs of config 3, CelebA
+    uniform + adaptive, and the paper's other grid sides at 1080p (b = 12, 24,
+    30, 40, 64, 128 with n up to 32). Inputs are the deterministic synthetic
+    frames (oracle.synth_frames / synth_masks, frame 5), plane seeds derived
+    from (42, frame 5, channel)."""
+    specs = [("4k_adaptive_b32n8", 2160, 3840, 32, 8, 16, 0.5, True)]
+    for b in (4, 8, 16, 32):
+        for eps in (0.1, 0.5, 1.0):
+            specs.append((f"sweep_b{b}_eps{eps}", 1083, 1917, b, 1, 16, eps, False))
+    specs += [("celeba_uniform_b16", 218, 178, 16, 1, 16, 0.5, False),
+              ("pets_adaptive_b16n4", 576, 768, 16, 4, 16, 0.5, True)]
+    for b, n in ((12, 1), (12, 3), (24, 4), (24, 8), (30, 1), (30, 5), (30, 10), (40, 4), (40, 8),
+                 (64, 16), (64, 8), (128, 8), (128, 16), (128, 32), (16, 8), (20, 5), (2, 2), (7, 1)):
+        specs.append((f"1080p_b{b}n{n}", 1080, 1920, b, n, 16, 0.5, n > 1 or b in (30, 128)))
+    out = {}
+    frames = {}
+    for name, M, N, b, n, m, eps, adaptive in specs:
+        if (M, N) not in frames:
+            frames[(M, N)] = (oracle.synth_frames(5, 1, M, N, 3)[0], oracle.synth_masks(5, 1, M, N)[0])
+        frame, mask = frames[(M, N)]
+        ent = {"M": M, "N": N, "b": b, "n": n, "m": m, "eps": eps, "adaptive": adaptive,
+               "input_sha": sha(frame), "mask_sha": sha(mask), "planes": []}
+        for ch in range(3):
+            plane = np.ascontiguousarray(frame[:, :, ch])
+            seed = oracle.derive_plane_seed(42, 5, ch)
+            if adaptive:
+                img, payload = ref.pixelize_adaptive(plane, mask, eps, m, b, n, seed)
+                stats = np.frombuffer(payload, np.uint8)
+            else:
+                img, stats = ref.pixelize_parallel(plane, eps, m, b, seed)
+            ent["planes"].append({"stats_len": int(stats.size), "stats_sha": sha(stats),
+                                  "image_sha": sha(img)})
+        out[name] = ent
+    json.dump({"source": "reference pixelize_parallel / pixelize_adaptive via oracle/_ref",
+               "frame": 5, "seed": 42, "cases": out},
+              open(os.path.join(HERE, "config_digests.json"), "w"), indent=1)
+
+
 if __name__ == "__main__":
     noise_vectors()
     small_cases()
     shaped_cases()
     records()
+    config_digests()
     for f in sorted(os.listdir(HERE)):
         print(f, os.path.getsize(os.path.join(HERE, f)))

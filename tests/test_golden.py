@@ -95,3 +95,29 @@ def test_record_payloads():
     p = oracle.make_privacy_params(0.5, 16, 16, 4)
     pl, _ = oracle.pixelize_adaptive(img, mask, 16, 4, p.sigma, p.sigma_sub, "keyed", [11])
     assert rec[20:-4] == pl[0]
+
+
+def test_config_digests():
+    """The C restatement reproduces the reference's digests for every BASELINE
+    config and the paper's other grid sides (config_digests.json)."""
+    cases = json.load(open(os.path.join(G, "config_digests.json")))["cases"]
+    frames = {}
+    for name, c in sorted(cases.items()):
+        M, N, b, n = c["M"], c["N"], c["b"], c["n"]
+        if (M, N) not in frames:
+            frames[(M, N)] = (oracle.synth_frames(5, 1, M, N, 3)[0], oracle.synth_masks(5, 1, M, N)[0])
+        frame, mask = frames[(M, N)]
+        assert hashlib.sha256(frame.tobytes()).hexdigest() == c["input_sha"]
+        assert hashlib.sha256(mask.tobytes()).hexdigest() == c["mask_sha"]
+        seeds = [oracle.derive_plane_seed(42, 5, ch) for ch in range(3)]
+        p = oracle.make_privacy_params(c["eps"], c["m"], b, n)
+        if c["adaptive"]:
+            pls, img = oracle.pixelize_adaptive(frame, mask, b, n, p.sigma, p.sigma_sub, "keyed", seeds)
+            stats = [np.frombuffer(x, np.uint8) for x in pls]
+        else:
+            means, img = oracle.pixelize_uniform(frame, b, p.sigma, "keyed", seeds)
+            stats = list(means)
+        for ch, pl in enumerate(c["planes"]):
+            assert hashlib.sha256(stats[ch].tobytes()).hexdigest() == pl["stats_sha"], (name, ch)
+            plane = np.ascontiguousarray(img[:, :, ch])
+            assert hashlib.sha256(plane.tobytes()).hexdigest() == pl["image_sha"], (name, ch)

@@ -1,0 +1,91 @@
+"""Multi-GPU paths on one B200 (the pool gives one GPU per call): the C++
+device-group runner (dppx_group_*: one host thread + ctx per listed device;
+here the same device listed several times) and the multi-rank bench launch
+(one process per rank, gloo for the plumbing, every rank on GPU 0). Both are
+checked byte-for-byte against a single context over the whole batch: noise is
+keyed per plane / global frame, never by device or rank."""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+import paper_2511_04261_b200 as dp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("workers", [2, 3])
+@pytest.mark.parametrize("M,N,C,b,n", [(72, 136, 3, 16, 4), (218, 178, 3, 16, 4), (61, 253, 3, 30, 5)])
+def test_group_matches_single_context(ctx, workers, M, N, C, b, n):
+    F = 7  # uneven blocks over 2 and 3 workers
+    frames = oracle.synth_frames(11, F, M, N, C)
+    masks = oracle.synth_masks(11, F, M, N)
+    g = dp.Group([0] * workers)
+    try:
+        assert g.devices == [0] * workers
+        p = dp.make_privacy_params(0.5, 16, b, n)
+        seeds = dp.plane_seeds(42, F, C)
+        G = dp.grid_dims(M, N, b).grid_count()
+        inj = np.random.default_rng(1).laplace(0, 20, (F * C, G * n * n))
+        for kind, sd, injected in ((dp.NOISE_KEYED, seeds, None), (dp.NOISE_PHILOX, [99], None),
+                                   (dp.NOISE_INJECTED, None, inj), (dp.NOISE_NONE, None, None)):
+            pa, ia = g.pixelize_adaptive(frames, masks, p, kind, sd, frame_base=5, injected=injected)
+            pb, ib = ctx.pixelize_adaptive(frames, masks, p, kind, sd, frame_base=5, injected=injected)
+            assert pa == pb and np.array_equal(ia, ib), kind
+        back = g.reassemble(pa, M, N, b, n, channels=C, frames=F)
+        assert np.array_equal(back, ia)
+        pu = dp.make_privacy_params(0.5, 16, b)
+        ma, ua = g.pixelize_uniform(frames, pu, dp.NOISE_KEYED, seeds)
+        mb, ub = ctx.pixelize_uniform(frames, pu, dp.NOISE_KEYED, seeds)
+        assert np.array_equal(ma, mb) and np.array_equal(ua, ub)
+        assert np.array_equal(g.broadcast_means(ma, M, N, b, channels=C, frames=F), ua)
+        st = g.stats()
+        assert st["launches"]["classify"] >= workers  # every worker ran kernels
+        # errors keep the reference taxonomy
+        bad = [bytes(len(pa[0]))] * (F * C)
+        with pytest.raises(dp.RecordError):
+            g.reassemble(bad, M, N, b, n, channels=C, frames=F)
+        with pytest.raises(ValueError):
+            g.pixelize_uniform(frames, dp.make_privacy_params(0.5, 16, b, n) if n > 1 else
+                               dp.make_privacy_params(0.5, 16, 4 * max(M, N)), dp.NOISE_KEYED, seeds)
+    finally:
+        g.close()
+
+
+def _run(cmd, env_extra, timeout=600):
+    env = dict(os.environ, **env_extra)
+    return subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=timeout)
+
+
+def test_two_rank_shards_byte_identical_on_gpu(tmp_path):
+    """tools/shard_check.py under torchrun: 2 ranks (gloo plumbing, both on GPU
+    0 -- the ranks never wait on each other's kernels) each pixelize their
+    strong shard of a 9-frame clip through the GPU path; rank 0 gathers the
+    digests and compares them with a 1-rank run of the whole clip."""
+    out = tmp_path / "shard.json"
+    r = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+              "--master-addr=127.0.0.1", "--master-port=29517", "tools/shard_check.py", str(out)],
+             {"DPPX_DIST_BACKEND": "gloo", "DPPX_FORCE_DEVICE": "0"})
+    assert r.returncode == 0, r.stderr[-3000:]
+    res = json.loads(out.read_text())
+    assert res["world"] == 2 and res["identical"], res
+    assert res["frames"] == [5, 4]
+
+
+def test_bench_self_spawns_ranks():
+    """`bench.py --gpus 2` without torchrun re-launches itself with 2 ranks and
+    reports n_gpus = 2 (weak scaling: each rank owns its frames)."""
+    r = _run([sys.executable, "bench.py", "--gpus", "2", "--frames", "24", "--steps", "3",
+              "--warmup", "3", "--no-cpu-baseline", "--e2e-frames", "8", "--e2e-steps", "1"],
+             {"DPPX_DIST_BACKEND": "gloo", "DPPX_FORCE_DEVICE": "0"})
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
+    assert line["config"]["frames_per_gpu"] == 24

@@ -43,6 +43,37 @@ def test_random_geometries_bit_exact():
         done += 1
 
 
+def test_large_grid_sides_bit_exact():
+    """Live pin of the grid sides the paper and the BASELINE configs use beyond
+    the random sweep above: b in {24, 30, 32, 40, 64, 128} with every n that
+    divides b up to 32, on shapes up to 300 x 300 (padded and unpadded)."""
+    rng = np.random.default_rng(424)
+    cases = 0
+    for b in (24, 30, 32, 40, 64, 128):
+        ns = [d for d in range(1, min(b, 32) + 1) if b % d == 0]
+        for n in ns:
+            for _ in range(3):
+                M = int(rng.integers(b // 2 + 1, 301))
+                N = int(rng.integers(b // 2 + 1, 301))
+                g = oracle.grid_dims(M, N, b)
+                if (g.pad_rows or g.pad_cols) and (g.pad_rows >= M or g.pad_cols >= N):
+                    M, N = max(M, b), max(N, b)  # reflection needs pad < M, N
+                img = rng.integers(0, 256, (M, N), dtype=np.uint8)
+                mask = (rng.random((M, N)) < rng.choice([0.2, 0.5, 0.8])).astype(np.uint8)
+                eps, m = float(rng.choice([0.1, 0.5, 2.0])), int(rng.integers(1, 40))
+                seed = int(rng.integers(0, 2**63))
+                p = oracle.make_privacy_params(eps, m, b, n)
+                ra, rpl = oracle.ref.pixelize_adaptive(img, mask, eps, m, b, n, seed)
+                opl, oa = oracle.pixelize_adaptive(img, mask, b, n, p.sigma, p.sigma_sub, "keyed", [seed])
+                assert rpl == opl[0] and np.array_equal(ra, oa), (M, N, b, n)
+                if n == 1:
+                    ri, rm = oracle.ref.pixelize_parallel(img, eps, m, b, seed)
+                    om, oi = oracle.pixelize_uniform(img, b, p.sigma, "keyed", [seed])
+                    assert np.array_equal(rm, om[0]) and np.array_equal(ri, oi), (M, N, b)
+                cases += 1
+    assert cases == 123
+
+
 def test_reference_release_gate_runs():
     """The reference's own acceptance gate (tests/acceptance_main.cpp) built
     from its sources: every criterion but the host-dependent speedup floor (8)
