@@ -1,8 +1,11 @@
 // dppix/batch.hpp -- GPU batch runner: the reference's run_batch
 // (proj/src/cli.cpp:175-213 over run_single cli.cpp:93-173) re-planned for the
 // GPU. Files are read by host threads, grouped by shape, and pixelized F frames
-// per call through the pinned pipeline; results and side effects match
-// running run_single on each file (same seed for every file, cli.cpp:200-201).
+// per call through the pinned pipeline, the calls spread over every GPU of the
+// node (one host thread + ctx per GPU); results and side effects match running
+// run_single on each file (same seed for every file, cli.cpp:200-201).
+// dppix::run_batch (dppix/cli.hpp) is this runner behind the reference's
+// RunConfig signature.
 #pragma once
 
 #include <cstdint>
@@ -32,6 +35,9 @@ struct BatchConfig {
   bool reconstruct_check = true;  // decode + reconstruct must equal the image
   int frames_per_call = 64;       // GPU batch size per shape group
   int io_threads = 0;             // 0: hardware_concurrency
+  // GPUs the chunks are spread over (one host thread + ctx each, dppx_group);
+  // empty: env DPPX_BATCH_DEVICES ("0,1,...") if set, else every visible sm_100 GPU.
+  std::vector<int> devices;
 };
 
 struct BatchFileReport {

@@ -1,0 +1,636 @@
+// runner.cpp -- the host side around the path: PGM ingest (pgm.hpp), the
+// multi-GPU batch runner (batch.hpp) and the reference's orchestration API
+// (cli.hpp: run_single / run_batch / run_sweep / run_bench / run_reconstruct /
+// run_verify / exit_code_for, cli.cpp:93-401 semantics) over the GPU drop-in.
+//
+// PGM files are read with one read of the whole file and parsed from memory
+// (a cursor over the bytes, no iostream tokenizing). The batch runner reads
+// files on host threads, groups frames by shape and sends up to
+// frames_per_call frames per C-ABI call; the calls of all shape groups are
+// claimed dynamically by the workers of a device group (one host thread +
+// dppx_ctx per GPU), each running its chunk's pixelize, records, GPU
+// reconstruct check and GPU metrics on its own device.
+#include <sys/stat.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <filesystem>
+#include <functional>
+#include <limits>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <thread>
+#include <utility>
+
+#include "dppix/adaptive.hpp"
+#include "dppix/batch.hpp"
+#include "dppix/cli.hpp"
+#include "dppix/errors.hpp"
+#include "dppix/pgm.hpp"
+#include "dppix/pixelize.hpp"
+#include "dppix/record.hpp"
+#include "dppx_gpu.h"
+
+namespace dppix {
+namespace fs = std::filesystem;
+
+namespace {
+
+// ---------------------------------------------------------------- PGM bytes
+// Whole file in memory (one fread); a missing / unreadable file is an IoError.
+std::vector<std::uint8_t> slurp(const std::string& path, const char* who) {
+  std::unique_ptr<std::FILE, int (*)(std::FILE*)> f(std::fopen(path.c_str(), "rb"), &std::fclose);
+  if (!f) throw IoError(std::string(who) + ": cannot open " + path);
+  struct stat st {};
+  std::vector<std::uint8_t> buf;
+  if (fstat(fileno(f.get()), &st) == 0 && st.st_size > 0) buf.resize(static_cast<size_t>(st.st_size));
+  size_t got = buf.empty() ? 0 : std::fread(buf.data(), 1, buf.size(), f.get());
+  buf.resize(got);
+  return buf;
+}
+
+// Netpbm P5 header: "P5", width, height, maxval, each preceded by whitespace
+// or '#' comments running to the end of the line, then ONE whitespace byte
+// and the raster (pgm.cpp:54-83 accepts exactly this; P2 is rejected).
+struct PgmView {
+  int width = 0, height = 0;
+  size_t raster = 0;  // offset of the first pixel
+};
+
+PgmView parse_pgm(const std::vector<std::uint8_t>& b, const std::string& path) {
+  auto bad = [&](const std::string& why) { return IoError("read_pgm: " + why + " (" + path + ")"); };
+  if (b.size() < 2 || b[0] != 'P' || b[1] != '5') throw bad("not a binary P5 graymap");
+  size_t at = 2;
+  auto space = [](std::uint8_t c) { return c == ' ' || c == '\t' || c == '\n' || c == '\r' || c == '\v' || c == '\f'; };
+  auto number = [&](const char* what) -> long long {
+    for (;;) {  // skip separators and comments
+      if (at >= b.size()) throw bad(std::string("header ends before ") + what);
+      if (b[at] == '#') {
+        while (at < b.size() && b[at] != '\n') ++at;
+      } else if (space(b[at])) {
+        ++at;
+      } else {
+        break;
+      }
+    }
+    if (b[at] < '0' || b[at] > '9') throw bad(std::string(what) + " is not a number");
+    long long v = 0;
+    while (at < b.size() && b[at] >= '0' && b[at] <= '9') {
+      v = v * 10 + (b[at++] - '0');
+      if (v > std::numeric_limits<int>::max()) throw bad(std::string(what) + " out of range");
+    }
+    return v;
+  };
+  PgmView v;
+  v.width = static_cast<int>(number("width"));
+  v.height = static_cast<int>(number("height"));
+  const long long maxval = number("maxval");
+  if (v.width < 1 || v.height < 1) throw bad("dimensions must be >= 1");
+  if (maxval != 255) throw bad("only maxval 255 is supported");
+  if (at >= b.size() || !space(b[at])) throw bad("no whitespace byte before the raster");
+  v.raster = at + 1;
+  if (b.size() - v.raster < static_cast<size_t>(v.width) * v.height) throw bad("raster is truncated");
+  return v;
+}
+
+[[noreturn]] void raise_status(dppx_ctx* ctx, int rc, const std::string& who) {
+  const std::string msg = who + ": " + (ctx ? dppx_ctx_last_error(ctx) : "");
+  if (rc == DPPX_ERR_INVALID) throw std::invalid_argument(msg);
+  if (rc == DPPX_ERR_CORRUPT) throw RecordError(RecordErrorKind::corrupt_record, msg);
+  if (rc == DPPX_ERR_OOM) throw std::bad_alloc();
+  throw std::runtime_error(msg);
+}
+
+void parallel_over(int count, int workers, const std::function<void(int)>& body) {
+  workers = std::max(1, std::min(workers, count));
+  std::atomic<int> next{0};
+  std::vector<std::thread> pool;
+  for (int w = 1; w < workers; ++w)
+    pool.emplace_back([&] {
+      for (int i = next++; i < count; i = next++) body(i);
+    });
+  for (int i = next++; i < count; i = next++) body(i);
+  for (auto& t : pool) t.join();
+}
+
+struct HostBuf {  // pageable host batch buffer (no zero fill)
+  std::unique_ptr<uint8_t[]> mem;
+  uint8_t* p = nullptr;
+  explicit HostBuf(size_t bytes) : mem(new uint8_t[bytes ? bytes : 1]), p(mem.get()) {}
+};
+
+// Process-wide device group per device list (contexts and worker threads are
+// created once; run_batch calls reuse them).
+dppx_group* shared_group(const std::vector<int>& want) {
+  static std::mutex mu;
+  static std::map<std::vector<int>, std::unique_ptr<dppx_group, void (*)(dppx_group*)>> groups;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = groups.find(want);
+  if (it != groups.end()) return it->second.get();
+  dppx_group* g = nullptr;
+  const int rc = want.empty() ? dppx_group_create(nullptr, 0, &g)
+                              : dppx_group_create(want.data(), static_cast<int32_t>(want.size()), &g);
+  if (rc != DPPX_OK)
+    throw std::runtime_error("dppix: no usable sm_100 GPU for the batch runner (status " +
+                             std::to_string(rc) + ")");
+  groups.emplace(want, std::unique_ptr<dppx_group, void (*)(dppx_group*)>(g, &dppx_group_destroy));
+  return g;
+}
+
+std::vector<int> batch_devices(const BatchConfig& cfg) {
+  if (!cfg.devices.empty()) return cfg.devices;
+  std::vector<int> out;
+  if (const char* env = std::getenv("DPPX_BATCH_DEVICES")) {
+    std::stringstream ss(env);
+    std::string tok;
+    while (std::getline(ss, tok, ','))
+      if (!tok.empty()) out.push_back(std::atoi(tok.c_str()));
+  }
+  return out;
+}
+
+int group_task_trampoline(dppx_ctx* ctx, int32_t worker, int32_t task, void* user) {
+  (*static_cast<std::function<void(dppx_ctx*, int, int)>*>(user))(ctx, worker, task);
+  return DPPX_OK;
+}
+
+// cli.cpp:78-89 (validate_run_config): flag combinations wrong for every input.
+void validate(bool have_seed, double epsilon, bool reference_mode, bool emit_record,
+              bool adaptive_mode, bool mask_empty) {
+  if (!(epsilon > 0.0) && have_seed) throw UsageError("--epsilon must be > 0");
+  if (reference_mode && emit_record)
+    throw UsageError("reference mode keeps no grid statistics and cannot emit records");
+  if (adaptive_mode && mask_empty) throw UsageError("adaptive mode requires --mask");
+}
+
+// cli.cpp:43-58 (mask_path_for): a mask directory pairs masks by input stem.
+std::string paired_mask(const std::string& mask_path, const std::string& input) {
+  if (mask_path.empty()) throw UsageError("adaptive mode requires --mask");
+  std::error_code ec;
+  if (fs::is_directory(mask_path, ec)) {
+    const fs::path p = fs::path(mask_path) / (fs::path(input).stem().string() + ".pgm");
+    if (!fs::exists(p, ec)) throw IoError("no mask for " + input + " (expected " + p.string() + ")");
+    return p.string();
+  }
+  return mask_path;
+}
+
+void make_out_dir(const std::string& dir) {
+  std::error_code ec;
+  fs::create_directories(dir, ec);
+  if (ec) throw IoError("cannot create output directory " + dir + ": " + ec.message());
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- pgm.hpp
+GrayImage read_pgm(const std::string& path) {
+  const std::vector<std::uint8_t> bytes = slurp(path, "read_pgm");
+  const PgmView v = parse_pgm(bytes, path);
+  GrayImage img = make_image(v.height, v.width);
+  std::memcpy(img.pixels.data(), bytes.data() + v.raster, img.pixels.size());
+  return img;
+}
+
+void write_pgm(const GrayImage& img, const std::string& path) {
+  if (img.height < 1 || img.width < 1 ||
+      img.pixels.size() != static_cast<std::size_t>(img.height) * img.width)
+    throw IoError("write_pgm: image buffer does not match its dimensions (" + path + ")");
+  char head[64];
+  const int hn = std::snprintf(head, sizeof(head), "P5\n%d %d\n255\n", img.width, img.height);
+  std::unique_ptr<std::FILE, int (*)(std::FILE*)> f(std::fopen(path.c_str(), "wb"), &std::fclose);
+  if (!f) throw IoError("write_pgm: cannot create " + path);
+  const bool ok = std::fwrite(head, 1, static_cast<size_t>(hn), f.get()) == static_cast<size_t>(hn) &&
+                  std::fwrite(img.pixels.data(), 1, img.pixels.size(), f.get()) == img.pixels.size();
+  if (!ok || std::fflush(f.get()) != 0) throw IoError("write_pgm: short write to " + path);
+}
+
+RegionMask read_mask_pgm(const std::string& path) {  // pgm.cpp:112-119: >= 128 -> simple
+  const std::vector<std::uint8_t> bytes = slurp(path, "read_mask_pgm");
+  const PgmView v = parse_pgm(bytes, path);
+  RegionMask mask = make_mask(v.height, v.width, 0);
+  const std::uint8_t* src = bytes.data() + v.raster;
+  for (std::size_t i = 0; i < mask.values.size(); ++i) mask.values[i] = src[i] >> 7;
+  return mask;
+}
+
+// ---------------------------------------------------------------- batch.hpp
+int batch_exit_code_for(const std::exception& err) { return exit_code_for(err); }
+
+std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
+  validate(cfg.seed.has_value(), cfg.epsilon, cfg.mode == BatchMode::reference, cfg.emit_record,
+           cfg.mode == BatchMode::adaptive, cfg.mask_path.empty());
+  std::vector<std::string> inputs;
+  std::error_code ec;
+  if (fs::is_directory(cfg.input, ec)) {
+    for (const fs::directory_entry& e : fs::directory_iterator(cfg.input))
+      if (e.is_regular_file() && e.path().extension() == ".pgm") inputs.push_back(e.path().string());
+    std::sort(inputs.begin(), inputs.end());
+    if (inputs.empty()) throw IoError("no .pgm inputs under " + cfg.input);
+  } else {
+    inputs.push_back(cfg.input);
+  }
+  const int nfile = static_cast<int>(inputs.size());
+  const int io = cfg.io_threads > 0 ? cfg.io_threads
+                                    : static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  std::vector<BatchFileReport> reports(nfile);
+  std::vector<GrayImage> imgs(nfile);
+  std::vector<RegionMask> masks(cfg.mode == BatchMode::adaptive ? nfile : 0);
+  std::vector<char> ok(nfile, 0);
+  std::mutex fail_mu;
+  auto fail = [&](int i, const std::exception& err) {
+    std::lock_guard<std::mutex> lk(fail_mu);
+    if (reports[i].exit_code != 0) return;
+    reports[i].error = err.what();
+    reports[i].exit_code = exit_code_for(err);
+  };
+  // DPPX_BATCH_TRACE=1: per-phase wall times on stderr.
+  static const bool trace = std::getenv("DPPX_BATCH_TRACE") != nullptr;
+  auto tnow = [] { return std::chrono::steady_clock::now(); };
+  auto tms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+  const auto T0 = tnow();
+  // ---- ingest (host threads) ----
+  parallel_over(nfile, io, [&](int i) {
+    reports[i].input = inputs[i];
+    try {
+      imgs[i] = read_pgm(inputs[i]);
+      if (cfg.mode == BatchMode::adaptive) {
+        masks[i] = read_mask_pgm(paired_mask(cfg.mask_path, inputs[i]));
+        if (masks[i].height != imgs[i].height || masks[i].width != imgs[i].width)
+          throw UsageError("mask dimensions do not match image: " + inputs[i]);
+      }
+      ok[i] = 1;
+    } catch (const std::exception& err) {
+      fail(i, err);
+    }
+  });
+  if (trace) std::fprintf(stderr, "batch: ingest %.1f ms\n", tms(T0, tnow()));
+  // ---- shape groups -> chunks of up to frames_per_call frames ----
+  std::map<std::pair<int, int>, std::vector<int>> groups;
+  for (int i = 0; i < nfile; ++i)
+    if (ok[i]) groups[{imgs[i].height, imgs[i].width}].push_back(i);
+  std::vector<std::vector<int>> chunks;
+  const int K = std::max(1, cfg.frames_per_call);
+  for (auto& kv : groups)
+    for (size_t c0 = 0; c0 < kv.second.size(); c0 += K)
+      chunks.emplace_back(kv.second.begin() + c0,
+                          kv.second.begin() + std::min(kv.second.size(), c0 + K));
+  const double eff_eps = cfg.epsilon > 0.0 ? cfg.epsilon : 1.0;  // cli.cpp:97-102
+  const int n = cfg.mode == BatchMode::adaptive ? cfg.n : 1;
+  if (!chunks.empty() && (cfg.emit_image || cfg.emit_record)) make_out_dir(cfg.out_dir);
+  if (chunks.empty()) return reports;
+  dppx_group* grp = shared_group(batch_devices(cfg));
+  const int workers = dppx_group_size(grp);
+  const int io_per = std::max(1, io / std::max(1, std::min<int>(workers, static_cast<int>(chunks.size()))));
+
+  std::function<void(dppx_ctx*, int, int)> task = [&](dppx_ctx* ctx, int, int t) {
+    const std::vector<int>& chunk = chunks[t];
+    const int F = static_cast<int>(chunk.size());
+    const int M = imgs[chunk[0]].height, N = imgs[chunk[0]].width;
+    try {
+      dppx_privacy_params pp;
+      if (dppx_make_privacy_params(eff_eps, cfg.m, cfg.b, n, &pp) != DPPX_OK)
+        throw std::invalid_argument("make_privacy_params: invalid parameters");
+      const size_t plane = static_cast<size_t>(M) * N;
+      const auto t0 = tnow();
+      HostBuf in(plane * F), out(plane * F), mk(cfg.mode == BatchMode::adaptive ? plane * F : 0);
+      parallel_over(F, io_per, [&](int k) {
+        std::memcpy(in.p + k * plane, imgs[chunk[k]].pixels.data(), plane);
+        if (cfg.mode == BatchMode::adaptive) std::memcpy(mk.p + k * plane, masks[chunk[k]].values.data(), plane);
+      });
+      const dppx_frames_desc d{M, N, 1, F, N, static_cast<int64_t>(plane), N, static_cast<int64_t>(plane),
+                               N, static_cast<int64_t>(plane)};
+      std::vector<uint64_t> seeds(F, cfg.seed ? cfg.seed->value : 0);  // same seed per file, cli.cpp:200-201
+      const dppx_noise nz{cfg.seed ? DPPX_NOISE_KEYED : DPPX_NOISE_NONE, 0, seeds.data(), nullptr};
+      dppx_geometry g;
+      if (dppx_grid_dims(M, N, cfg.b, &g) != DPPX_OK)
+        throw std::invalid_argument("grid_dims: grid side b exceeds both image dimensions");
+      const size_t G = static_cast<size_t>(g.grid_rows) * g.grid_cols;
+      const size_t cap = cfg.mode == BatchMode::adaptive
+                             ? (dppx_adaptive_payload_capacity(M, N, cfg.b, n) + 3) & ~size_t{3}
+                             : G;
+      std::vector<uint8_t> stats(cap * F);
+      std::vector<uint32_t> lens(F, static_cast<uint32_t>(G));
+      const auto tp0 = tnow();
+      int rc;
+      if (cfg.mode == BatchMode::adaptive)
+        rc = dppx_pixelize_adaptive(ctx, &d, in.p, mk.p, &pp, &nz, stats.data(), static_cast<int64_t>(cap),
+                                    lens.data(), out.p);
+      else if (cfg.mode == BatchMode::uniform)
+        rc = dppx_pixelize_uniform(ctx, &d, in.p, &pp, &nz, stats.data(), out.p);
+      else
+        rc = dppx_pixelize_reference(ctx, &d, in.p, &pp, &nz, stats.data(), out.p);
+      const auto tp1 = tnow();
+      if (rc != DPPX_OK) raise_status(ctx, rc, "pixelize");
+      const double per_ms = tms(tp0, tp1) / F;
+      // ---- records + reconstruct check (cli.cpp:132-146), on the GPU ----
+      std::vector<std::vector<uint8_t>> recs(F);
+      if (cfg.mode != BatchMode::reference) {
+        std::vector<char> enc_ok(F, 1);
+        parallel_over(F, io_per, [&](int k) {  // header + CRC32 per file
+          recs[k].resize(dppx_record_size(lens[k]));
+          size_t len = 0;
+          enc_ok[k] = dppx_encode_record(M, N, cfg.b, n, cfg.mode == BatchMode::adaptive ? 2 : 1,
+                                         stats.data() + k * cap, lens[k], recs[k].data(), recs[k].size(),
+                                         &len) == DPPX_OK;
+        });
+        for (int k = 0; k < F; ++k)
+          if (!enc_ok[k]) throw std::invalid_argument("encode: payload inconsistent");
+        if (cfg.reconstruct_check) {
+          HostBuf rebuilt(plane * F);
+          std::vector<uint8_t> payload(cap * F);
+          std::vector<uint32_t> plen(F);
+          for (int k = 0; k < F; ++k) {  // decode, then rebuild from the decoded payload
+            dppx_record_info info{};
+            if (dppx_decode_record(recs[k].data(), recs[k].size(), &info) != DPPX_OK)
+              throw RecordError(RecordErrorKind::corrupt_record, "decode failed");
+            std::memcpy(payload.data() + k * cap, recs[k].data() + info.payload_offset, info.payload_len);
+            plen[k] = info.payload_len;
+          }
+          const int rrc = cfg.mode == BatchMode::adaptive
+                              ? dppx_reassemble(ctx, &d, payload.data(), static_cast<int64_t>(cap),
+                                                plen.data(), cfg.b, n, rebuilt.p)
+                              : dppx_broadcast_means(ctx, &d, payload.data(), cfg.b, rebuilt.p);
+          if (rrc != DPPX_OK) raise_status(ctx, rrc, "reconstruct");
+          for (int k = 0; k < F; ++k)
+            if (std::memcmp(rebuilt.p + k * plane, out.p + k * plane, plane) != 0)
+              fail(chunk[k], ConsistencyError("reconstruction does not match the emitted image for " +
+                                              inputs[chunk[k]]));
+        }
+      }
+      // ---- metrics on the GPU (cli.cpp:164-171) ----
+      std::vector<double> mses(F), ssims(F, std::numeric_limits<double>::quiet_NaN());
+      if (dppx_metrics(ctx, &d, in.p, out.p, mses.data(), M >= 7 && N >= 7 ? ssims.data() : nullptr) != DPPX_OK)
+        raise_status(ctx, DPPX_ERR_CUDA, "metrics");
+      // ---- outputs (host threads) ----
+      parallel_over(F, io_per, [&](int k) {
+        const int i = chunk[k];
+        if (reports[i].exit_code != 0) return;
+        try {
+          const std::string stem = fs::path(inputs[i]).stem().string();
+          if (cfg.emit_image) {
+            GrayImage pix = make_image(M, N);
+            std::memcpy(pix.pixels.data(), out.p + k * plane, plane);
+            const std::string path = (fs::path(cfg.out_dir) / (stem + ".pix.pgm")).string();
+            write_pgm(pix, path);
+            reports[i].written.push_back(path);
+          }
+          if (cfg.mode != BatchMode::reference && cfg.emit_record) {
+            const std::string path = (fs::path(cfg.out_dir) / (stem + ".dppx")).string();
+            std::unique_ptr<std::FILE, int (*)(std::FILE*)> f(std::fopen(path.c_str(), "wb"), &std::fclose);
+            if (!f || std::fwrite(recs[k].data(), 1, recs[k].size(), f.get()) != recs[k].size() ||
+                std::fflush(f.get()) != 0)
+              throw IoError("write_record: cannot write " + path);
+            reports[i].written.push_back(path);
+          }
+          MetricReport& r = reports[i].report;
+          r.epsilon = cfg.epsilon;
+          r.m = cfg.m;
+          r.b = cfg.b;
+          r.n = n;
+          r.seed = cfg.seed ? cfg.seed->value : 0;
+          r.mse = mses[k];
+          r.ssim = ssims[k];
+          r.runtime_ms = per_ms;
+          r.record_bytes = recs[k].size();
+        } catch (const std::exception& err) {
+          fail(i, err);
+        }
+      });
+      if (trace)
+        std::fprintf(stderr, "batch: chunk %d (%d x %dx%d): stage %.1f pixelize %.1f rest %.1f ms\n", t, F, M, N,
+                     tms(t0, tp0), tms(tp0, tp1), tms(tp1, tnow()));
+    } catch (const std::exception& err) {
+      for (int i : chunk) fail(i, err);
+    }
+  };
+  const int grc = dppx_group_run(grp, static_cast<int32_t>(chunks.size()), &group_task_trampoline, &task);
+  if (grc != DPPX_OK) raise_status(nullptr, grc, "run_batch");
+  if (trace) std::fprintf(stderr, "batch: total %.1f ms on %d GPU worker(s)\n", tms(T0, tnow()), workers);
+  return reports;
+}
+
+// ---------------------------------------------------------------- cli.hpp
+int exit_code_for(const std::exception& err) {  // cli.cpp:386-401
+  if (dynamic_cast<const ConsistencyError*>(&err)) return kExitConsistency;
+  if (dynamic_cast<const RecordError*>(&err)) return kExitRecord;
+  if (dynamic_cast<const IoError*>(&err)) return kExitIo;
+  if (dynamic_cast<const UsageError*>(&err) || dynamic_cast<const std::invalid_argument*>(&err))
+    return kExitUsage;
+  return 1;
+}
+
+RunOutcome run_single(const RunConfig& cfg) {  // cli.cpp:93-173
+  validate(cfg.seed.has_value(), cfg.epsilon, cfg.mode == RunMode::reference, cfg.emit_record,
+           cfg.mode == RunMode::adaptive, cfg.mask_path.empty());
+  const GrayImage img = read_pgm(cfg.input);
+  const PrivacyParams params = make_privacy_params(cfg.epsilon > 0.0 ? cfg.epsilon : 1.0, cfg.m, cfg.b,
+                                                   cfg.mode == RunMode::adaptive ? cfg.n : 1);
+  using Clock = std::chrono::steady_clock;
+  GrayImage pixelized;
+  std::optional<PixelRecord> record;
+  Clock::time_point start, stop;
+  if (cfg.mode == RunMode::adaptive) {
+    const RegionMask mask = read_mask_pgm(paired_mask(cfg.mask_path, cfg.input));
+    if (mask.height != img.height || mask.width != img.width)
+      throw UsageError("mask dimensions do not match image: " + cfg.input);
+    start = Clock::now();
+    AdaptiveResult r = pixelize_adaptive(img, mask, params, cfg.seed, cfg.threads);
+    stop = Clock::now();
+    pixelized = std::move(r.image);
+    record = PixelRecord{img.height, img.width, std::move(r.means)};
+  } else if (cfg.mode == RunMode::uniform) {
+    start = Clock::now();
+    UniformResult r = pixelize_parallel(img, params, cfg.seed, cfg.threads);
+    stop = Clock::now();
+    pixelized = std::move(r.image);
+    record = PixelRecord{img.height, img.width, std::move(r.means)};
+  } else {
+    start = Clock::now();
+    pixelized = pixelize_reference(img, params, cfg.seed);
+    stop = Clock::now();
+  }
+  RunOutcome out;
+  std::vector<std::uint8_t> bytes;
+  if (record) {
+    bytes = encode(*record);
+    if (cfg.reconstruct_check && !(reconstruct(decode(bytes)) == pixelized))
+      throw ConsistencyError("reconstruction does not match the emitted image for " + cfg.input);
+  }
+  const std::string stem = fs::path(cfg.input).stem().string();
+  if (cfg.emit_image || cfg.emit_record) make_out_dir(cfg.out_dir);
+  if (cfg.emit_image) {
+    const std::string p = (fs::path(cfg.out_dir) / (stem + ".pix.pgm")).string();
+    write_pgm(pixelized, p);
+    out.written.push_back(p);
+  }
+  if (record && cfg.emit_record) {
+    const std::string p = (fs::path(cfg.out_dir) / (stem + ".dppx")).string();
+    write_record(*record, p);
+    out.written.push_back(p);
+  }
+  MetricReport& r = out.report;
+  r.epsilon = cfg.epsilon;
+  r.m = cfg.m;
+  r.b = cfg.b;
+  r.n = params.n;
+  r.seed = cfg.seed ? cfg.seed->value : 0;
+  r.mse = mse(img, pixelized);
+  r.ssim = img.height >= 7 && img.width >= 7 ? ssim(img, pixelized, cfg.threads)
+                                              : std::numeric_limits<double>::quiet_NaN();
+  r.runtime_ms = std::chrono::duration<double, std::milli>(stop - start).count();
+  r.record_bytes = bytes.size();
+  return out;
+}
+
+std::vector<FileReport> run_batch(const RunConfig& cfg) {  // cli.cpp:175-213, on every GPU
+  BatchConfig b;
+  b.input = cfg.input;
+  b.out_dir = cfg.out_dir;
+  b.mode = cfg.mode == RunMode::adaptive ? BatchMode::adaptive
+           : cfg.mode == RunMode::reference ? BatchMode::reference : BatchMode::uniform;
+  b.epsilon = cfg.epsilon;
+  b.m = cfg.m;
+  b.b = cfg.b;
+  b.n = cfg.n;
+  b.seed = cfg.seed;
+  b.mask_path = cfg.mask_path;
+  b.emit_image = cfg.emit_image;
+  b.emit_record = cfg.emit_record;
+  b.reconstruct_check = cfg.reconstruct_check;
+  std::vector<FileReport> out;
+  for (BatchFileReport& r : run_batch_gpu(b))
+    out.push_back(FileReport{std::move(r.input), r.report, std::move(r.written), std::move(r.error), r.exit_code});
+  return out;
+}
+
+SweepResult run_sweep(const RunConfig& cfg) {  // cli.cpp:231-288
+  RunConfig base = cfg;
+  base.emit_image = false;
+  base.emit_record = false;
+  if (base.epsilon_list.empty() || base.m_list.empty() || base.b_list.empty() || base.n_list.empty() ||
+      base.seed_list.empty())
+    throw UsageError("sweep lists must be non-empty");
+  if (base.mode == RunMode::reference) throw UsageError("sweep supports uniform and adaptive modes only");
+  if (base.mode == RunMode::uniform &&
+      std::any_of(base.n_list.begin(), base.n_list.end(), [](int v) { return v != 1; }))
+    throw UsageError("uniform sweeps require n == 1");
+  std::sort(base.epsilon_list.begin(), base.epsilon_list.end());
+  std::sort(base.m_list.begin(), base.m_list.end());
+  std::sort(base.b_list.begin(), base.b_list.end());
+  std::sort(base.n_list.begin(), base.n_list.end());
+  std::sort(base.seed_list.begin(), base.seed_list.end());
+  auto quote = [](const std::string& s) {
+    std::string q = "\"";
+    for (char c : s) q += c == '"' ? std::string("\"\"") : std::string(1, c);
+    return q + "\"";
+  };
+  SweepResult res;
+  std::ostringstream csv;
+  csv << csv_header() << ",error\n";
+  for (double eps : base.epsilon_list)
+    for (int m : base.m_list)
+      for (int b : base.b_list)
+        for (int n : base.n_list)
+          for (std::uint64_t seed : base.seed_list) {
+            RunConfig one = base;
+            one.epsilon = eps;
+            one.m = m;
+            one.b = b;
+            one.n = n;
+            one.seed = NoiseSeed{seed};
+            try {
+              csv << csv_row(run_single(one).report) << ",\n";
+            } catch (const std::exception& err) {
+              ++res.failures;
+              MetricReport blank;
+              blank.epsilon = eps;
+              blank.m = m;
+              blank.b = b;
+              blank.n = n;
+              blank.seed = seed;
+              csv << csv_row(blank) << ',' << quote(err.what()) << '\n';
+            }
+          }
+  res.csv = csv.str();
+  return res;
+}
+
+BenchResult run_bench(const RunConfig& cfg) {  // cli.cpp:303-336
+  if (cfg.repeat < 1 || cfg.warmup < 0) throw UsageError("bench requires repeat >= 1 and warmup >= 0");
+  const GrayImage img = read_pgm(cfg.input);
+  const PrivacyParams params = make_privacy_params(cfg.epsilon > 0.0 ? cfg.epsilon : 1.0, cfg.m, cfg.b, 1);
+  using Clock = std::chrono::steady_clock;
+  auto ms = [](Clock::time_point a, Clock::time_point b) {
+    return std::chrono::duration<double, std::milli>(b - a).count();
+  };
+  BenchResult res;
+  for (int round = -cfg.warmup; round < cfg.repeat; ++round) {
+    const auto t0 = Clock::now();
+    const GrayImage seq = pixelize_reference(img, params, cfg.seed);
+    const auto t1 = Clock::now();
+    const UniformResult par = pixelize_parallel(img, params, cfg.seed, cfg.threads);
+    const auto t2 = Clock::now();
+    if (round >= 0) {
+      res.reference_ms.push_back(ms(t0, t1));
+      res.parallel_ms.push_back(ms(t1, t2));
+    }
+    if (img.height % params.b == 0 && img.width % params.b == 0 && !(seq == par.image))
+      throw ConsistencyError("bench: reference and parallel paths disagree");
+  }
+  auto median = [](std::vector<double> v) {
+    std::sort(v.begin(), v.end());
+    const size_t h = v.size() / 2;
+    return v.size() % 2 ? v[h] : 0.5 * (v[h - 1] + v[h]);
+  };
+  res.median_reference_ms = median(res.reference_ms);
+  res.median_parallel_ms = median(res.parallel_ms);
+  res.speedup = res.median_parallel_ms > 0.0 ? res.median_reference_ms / res.median_parallel_ms
+                                             : std::numeric_limits<double>::infinity();
+  return res;
+}
+
+std::string bench_text(const BenchResult& r) {
+  std::ostringstream o;
+  o << "reference_ms:";
+  for (double v : r.reference_ms) o << ' ' << format_double(v);
+  o << "\nparallel_ms:";
+  for (double v : r.parallel_ms) o << ' ' << format_double(v);
+  o << "\nmedian_reference_ms: " << format_double(r.median_reference_ms)
+    << "\nmedian_parallel_ms: " << format_double(r.median_parallel_ms)
+    << "\nspeedup: " << format_double(r.speedup) << '\n';
+  return o.str();
+}
+
+std::string run_reconstruct(const std::string& record_path, const std::string& out_dir) {
+  const GrayImage img = reconstruct(read_record(record_path));
+  make_out_dir(out_dir);
+  const std::string p = (fs::path(out_dir) / (fs::path(record_path).stem().string() + ".rec.pgm")).string();
+  write_pgm(img, p);
+  return p;
+}
+
+std::string run_verify(const std::string& record_path, const std::string& image_path) {
+  const PixelRecord rec = read_record(record_path);
+  const GrayImage rebuilt = reconstruct(rec);
+  std::ostringstream o;
+  o << record_path << ": mode=" << (rec.mode() == RecordMode::uniform ? "uniform" : "adaptive")
+    << " dims=" << rec.height << 'x' << rec.width << " b=" << rec.grid_side()
+    << " n=" << rec.subgrid_factor();
+  if (!image_path.empty()) {
+    if (!(rebuilt == read_pgm(image_path)))
+      throw ConsistencyError("verify: reconstruction differs from " + image_path);
+    o << " matches=" << image_path;
+  }
+  o << " ok";
+  return o.str();
+}
+
+}  // namespace dppix

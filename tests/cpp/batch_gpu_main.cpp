@@ -8,8 +8,8 @@
 #include "dppix/pixelize.hpp"
 
 int main(int argc, char** argv) {
-  if (argc != 11) {
-    std::fprintf(stderr, "usage: %s in out u|a masks eps m b n seed threads\n", argv[0]);
+  if (argc != 11 && argc != 12) {
+    std::fprintf(stderr, "usage: %s in out u|a masks eps m b n seed threads [frames_per_call]\n", argv[0]);
     return 2;
   }
   dppix::BatchConfig cfg;
@@ -22,6 +22,7 @@ int main(int argc, char** argv) {
   cfg.b = std::atoi(argv[7]);
   cfg.n = std::atoi(argv[8]);
   cfg.seed = dppix::NoiseSeed{std::strtoull(argv[9], nullptr, 10)};
+  if (argc == 12) cfg.frames_per_call = std::atoi(argv[11]);
   {  // context creation and module loading happen here, outside the timed region
     dppix::GrayImage tiny = dppix::make_image(8, 8, 7);
     (void)dppix::pixelize_parallel(tiny, dppix::make_privacy_params(1.0, 1, 4), std::nullopt);

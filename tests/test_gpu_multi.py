@@ -89,3 +89,55 @@ def test_bench_self_spawns_ranks():
     line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
     assert line["config"]["frames_per_gpu"] == 24
+
+
+def _write_pgm(path, img):
+    h, w = img.shape
+    with open(path, "wb") as f:
+        f.write(f"P5\n{w} {h}\n255\n".encode())
+        f.write(img.tobytes())
+
+
+@pytest.mark.parametrize("mode", ["a", "u"])
+def test_batch_runner_multi_worker_equals_reference_run_batch(tmp_path, mode):
+    """run_batch_gpu (dppix::run_batch) with its chunks spread over 1 and 3
+    workers (DPPX_BATCH_DEVICES=0 / 0,0,0: one host thread + ctx each) writes
+    the same .pix.pgm / .dppx bytes as the reference's own run_batch
+    (oracle/_ref/dppix_batch_ref, cli.cpp:175-213, compiled from its sources)."""
+    import filecmp
+    ref_bin = os.path.join(ROOT, "oracle", "_ref", "dppix_batch_ref")
+    gpu_bin = os.path.join(ROOT, "tests", "cpp", "batch_gpu")
+    if not os.path.exists(gpu_bin):
+        pytest.skip("tests/cpp/batch_gpu not built")
+    d_in, d_mask = tmp_path / "in", tmp_path / "masks"
+    d_in.mkdir()
+    d_mask.mkdir()
+    k = 0
+    for (M, N, F) in ((64, 96, 7), (72, 136, 5), (218, 178, 4)):
+        frames = oracle.synth_frames(k, F, M, N, 1)[..., 0]
+        masks = oracle.synth_masks(k, F, M, N)
+        for i in range(F):
+            _write_pgm(str(d_in / f"f{k:03d}.pgm"), frames[i])
+            _write_pgm(str(d_mask / f"f{k:03d}.pgm"), (masks[i] * 255).astype(np.uint8))
+            k += 1
+    n = "4" if mode == "a" else "1"
+    common = [mode, str(d_mask), "0.5", "16", "16", n, "42", "0", "2"]  # 2 frames per call: 9 chunks
+    outs = {}
+    for devs in ("0", "0,0,0"):
+        d_out = tmp_path / f"out_{devs.replace(',', '')}"
+        r = _run([gpu_bin, str(d_in), str(d_out)] + common, {"DPPX_BATCH_DEVICES": devs})
+        assert r.returncode == 0, r.stderr[-2000:]
+        assert json.loads(r.stdout)["failures"] == 0
+        outs[devs] = d_out
+    names = sorted(os.listdir(outs["0"]))
+    assert len(names) == 2 * k
+    for x in names:
+        assert filecmp.cmp(outs["0"] / x, outs["0,0,0"] / x, shallow=False), x
+    if os.path.exists(ref_bin):
+        d_ref = tmp_path / "out_ref"
+        r = subprocess.run([ref_bin, str(d_in), str(d_ref)] + common[:-2] + ["4"], capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        assert sorted(os.listdir(d_ref)) == names
+        for x in names:
+            assert filecmp.cmp(outs["0,0,0"] / x, d_ref / x, shallow=False), x
