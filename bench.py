@@ -160,6 +160,44 @@ def ncu_traffic(workload):
         return None
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def workload_config(args, wl, F, world):
+    """The `config` object of BOTH arms (same keys and values, so the driver's
+    same-config check compares like with like)."""
+    M, N, C, _, b, n, m, eps, adaptive, desc = wl
+    pitch = ((N * C + 15) // 16) * 16
+    mpitch = ((N + 15) // 16) * 16
+    working_set = 2 * F * M * pitch + (F * M * mpitch if adaptive else 0)
+    flush_l2 = working_set < 2 * 126 * 2**20
+    cfg = {"workload": desc, "frames_per_gpu": F, "shape": f"{N}x{M}x{C}",
+           "b": b, "n": n, "m": m, "epsilon": eps,
+           "noise": "keyed splitmix64 + inverse-CDF Laplace (reference stream), "
+                    "per-(frame, channel) derived plane seeds",
+           "mask": "u8 centred ellipse (0.4M x 0.2N), ~25% complex" if adaptive else None,
+           "l2": (f"working set {working_set / 1e9:.4f} GB < 2 x 126 MB L2: each step timed "
+                  "alone after a 512 MB write that evicts L2" if flush_l2 else
+                  f"working set {working_set / 1e9:.2f} GB > 2 x 126 MB L2, no flush needed"),
+           "parallelism": f"frame-parallel x{world}, no collective on the data path",
+           "out_pad": ("none (N*C % 16 == 0)" if pitch == N * C else
+                       "output row padding never written" if args.no_pad_scratch else
+                       f"rows padded {N * C} -> {pitch} B, padding declared scratch: "
+                       "stores end on whole 32-B sectors")}
+    if args.workload == "sweep":
+        cfg["runs"] = [f"b{bb} eps{ee}" for bb, ee in SWEEP]
+    return cfg, working_set, flush_l2
+
+
 # ----------------------------------------------------------------------------
 # reference CPU arm (oracle/_ref = the reference compiled from its sources)
 # ----------------------------------------------------------------------------
@@ -191,8 +229,8 @@ def run_reference_once(sample, M, N, C, b, n, m, eps, adaptive):
                                   42, sample["workers"])
 
 
-def reference_arm(args, wl):
-    M, N, C, F, b, n, m, eps, adaptive, desc = wl
+def reference_arm(args, wl, F, world):
+    M, N, C, _, b, n, m, eps, adaptive, desc = wl
     import oracle
     if oracle.ref is None:
         print(json.dumps({"impl": "reference", "unavailable":
@@ -203,20 +241,22 @@ def reference_arm(args, wl):
     for _ in range(args.warmup):
         run_reference_once(sample, M, N, C, b, n, m, eps, adaptive)
     times = [run_reference_once(sample, M, N, C, b, n, m, eps, adaptive) for _ in range(args.steps)]
-    t = sum(times) / len(times)
+    t = statistics.median(times)  # median over the K steps (each a whole bounded sample)
     mp = sample["n_frames"] * M * N / 1e6
     value = mp / t
+    cfg, _, _ = workload_config(args, wl, F, world)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "MP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "frames_per_sec": round(sample["n_frames"] / t, 3),
-        "config": {"workload": desc, "sample_frames": sample["n_frames"],
-                   "shape": f"{N}x{M}x{C}"},
+        "config": cfg,
         "cpu_baseline": {"value": round(value, 3), "unit": "MP/s", "cores": sample["workers"],
-                         "kind": "reference",
-                         "sample": f"{sample['n_frames']} frames x {C} planes of the workload, "
+                         "kind": "reference", "cpu_model": cpu_model(),
+                         "statistic": f"median of {args.steps} steps",
+                         "step_seconds": [round(x, 4) for x in times],
+                         "sample": f"{sample['n_frames']} frames x {C} planes of the workload per step, "
                                    f"pixelize_{'adaptive' if adaptive else 'parallel'} per plane "
                                    f"(threads=1), frame-parallel over {sample['workers']} threads "
                                    "(run_batch scheme, cli.cpp:175-213)"},
@@ -266,7 +306,7 @@ def main():
 
     if args.impl == "reference":
         if rank == 0:
-            reference_arm(args, wl)
+            reference_arm(args, wl, F, world)
         return
 
     import numpy as np
@@ -364,8 +404,7 @@ def main():
     ctx.reset_stats()
     ctx.set_timing(True)
     barrier()
-    working_set = 2 * F * M * pitch + (F * M * mpitch if adaptive else 0)
-    flush_l2 = working_set < 2 * 126 * 2**20  # would stay L2-resident between steps
+    config, working_set, flush_l2 = workload_config(args, wl, F, world)
     scratch = torch.empty(512 * 2**20, dtype=torch.uint8, device=dev) if flush_l2 else None
     with ClockSampler(local) as clk:
         if flush_l2:
@@ -542,9 +581,10 @@ def main():
     # ---- CPU reference baseline (rank 0, N = 1 only) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        sample = cpu_reference_sample(M, N, C, b, n, m, eps, adaptive, args.cpu_seconds, frame0)
+        sample = cpu_reference_sample(M, N, C, b, n, m, eps, adaptive, args.cpu_seconds / 3, frame0)
         if sample is not None:
-            t = run_reference_once(sample, M, N, C, b, n, m, eps, adaptive)
+            runs = sorted(run_reference_once(sample, M, N, C, b, n, m, eps, adaptive) for _ in range(3))
+            t = runs[1]  # median of 3
             # single-thread reference on one frame (all C planes), as SURVEY 8(d) asks
             import oracle
             k1 = min(C, sample["planes"].shape[0])
@@ -553,7 +593,8 @@ def main():
                                         eps, m, b, n, 42, 1)
             cpu = {"value": round(sample["n_frames"] * M * N / 1e6 / t, 3), "unit": "MP/s",
                    "single_thread_value": round(M * N / 1e6 / (t1 * C / k1), 3),
-                   "cores": sample["workers"], "kind": "reference",
+                   "cores": sample["workers"], "kind": "reference", "cpu_model": cpu_model(),
+                   "statistic": "median of 3 runs", "run_seconds": [round(x, 4) for x in runs],
                    "sample": f"{sample['n_frames']} frames x {C} planes, pixelize_"
                              f"{'adaptive' if adaptive else 'parallel'} per plane (threads=1), "
                              f"frame-parallel over {sample['workers']} threads, {t:.2f} s wall"}
@@ -565,19 +606,7 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic",
             "frames_per_sec": round(fps, 1),
-            "config": {"workload": desc, "frames_per_gpu": F, "shape": f"{N}x{M}x{C}",
-                       "b": b, "n": n, "m": m, "epsilon": eps,
-                       "noise": "keyed splitmix64 + inverse-CDF Laplace (reference stream), "
-                                "per-(frame, channel) derived plane seeds",
-                       "mask": "u8 centred ellipse (0.4M x 0.2N), ~25% complex" if adaptive else None,
-                       "l2": (f"working set {working_set / 1e9:.4f} GB < 2 x 126 MB L2: each step timed "
-                              "alone after a 512 MB write that evicts L2" if flush_l2 else
-                              f"working set {working_set / 1e9:.2f} GB > 2 x 126 MB L2, no flush needed"),
-                       "parallelism": f"frame-parallel x{world}, no collective on the data path",
-                       "out_pad": ("none (N*C % 16 == 0)" if pitch == N * C else
-                                   "output row padding never written" if args.no_pad_scratch else
-                                   f"rows padded {N * C} -> {pitch} B, padding declared scratch: "
-                                   "stores end on whole 32-B sectors")},
+            "config": config,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic, "kernel": f"K1 {kfam}",

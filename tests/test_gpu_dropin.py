@@ -51,4 +51,4 @@ def test_reference_unit_suites_on_dropin(ctx):
     r = subprocess.run([_gate_exe("dppix_unit_gpu")], capture_output=True, text=True, timeout=900)
     print(r.stdout, r.stderr[-5000:])
     assert r.returncode == 0, r.stderr[-5000:]
-    assert "0 failed" in r.stdout
+    assert "test cases: 84 | 84 passed | 0 failed" in r.stdout, r.stdout
