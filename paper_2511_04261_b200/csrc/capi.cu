@@ -105,6 +105,7 @@ struct dppx_ctx {
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;  // compute stream (own or user's)
   cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaStream_t s_meta = nullptr;  // payload lengths D2H, ahead of the image copies on s_out
   std::string err;
   // scratch
   DevBuf cellinfo, rowcnt, rowprefix, totals, counters, status, seeds, keys, dbl, work, met_a, met_b, met_out;
@@ -119,6 +120,11 @@ struct dppx_ctx {
   uint64_t* sd_pinned[2] = {nullptr, nullptr};
   size_t sd_pinned_n[2] = {0, 0};
   cudaEvent_t in_done[2] = {}, comp_done[2] = {}, out_done[2] = {};
+  // exact-length payload D2H: per slot, the chunk's lengths land in pinned
+  // memory first (lens_ev), then only the written bytes of each payload move
+  uint32_t* lens_pinned[2] = {nullptr, nullptr};
+  size_t lens_pinned_n[2] = {0, 0};
+  cudaEvent_t lens_ev[2] = {};
   static constexpr int kMaxBands = 8;
   cudaEvent_t band_in[kMaxBands] = {}, band_comp[kMaxBands] = {};  // single-frame row bands
   int chunk_frames = 0;
@@ -1177,6 +1183,14 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
                          d->out_frame_stride == row * M;
   // Bit-packed mask transport: 1/8 of the mask's PCIe bytes (maskpack.h).
   const bool try_bits = op == HostOp::Adaptive && ctx->mask_bits_mode == 1;
+  // Adaptive payloads leave the device with their written length only (4G + 4
+  // + S + (G - S) n^2 per plane, known once K0 has run), not the slot capacity:
+  // each chunk's lengths go D2H on s_meta right after its kernels, and the
+  // chunk's payload spans are issued one chunk later (DPPX_EXACT_PAYLOAD=0:
+  // copy whole slots, for A/B runs).
+  static const bool exact_env = !(std::getenv("DPPX_EXACT_PAYLOAD") &&
+                                  std::getenv("DPPX_EXACT_PAYLOAD")[0] == '0');
+  const bool exact_payload = pix && adaptive && exact_env;
   const int64_t wpr = dppx::mask_words_per_row(N);
   const size_t bits_frame = static_cast<size_t>(wpr) * 4 * M;
   if ((try_bits || stage_in || stage_out) && !ctx->packer) ctx->packer = dppx::mask_packer_create(0);
@@ -1200,6 +1214,14 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
       return DPPX_ERR_OOM;
     if (dense_mask && ensure(ctx, ctx->dense_mask[s], static_cast<size_t>(N) * M * K))
       return DPPX_ERR_OOM;
+    if (exact_payload && ctx->lens_pinned_n[s] < static_cast<size_t>(C) * K) {
+      if (ctx->lens_pinned[s]) CUDA_TRY(ctx, cudaFreeHost(ctx->lens_pinned[s]));
+      ctx->lens_pinned[s] = nullptr;
+      ctx->lens_pinned_n[s] = 0;
+      CUDA_TRY(ctx, cudaHostAlloc(reinterpret_cast<void**>(&ctx->lens_pinned[s]),
+                                  sizeof(uint32_t) * C * K, cudaHostAllocDefault));
+      ctx->lens_pinned_n[s] = static_cast<size_t>(C) * K;
+    }
     if (try_bits && ctx->mbits_pinned_n[s] < bits_frame * K) {
       if (ctx->mbits_pinned[s]) CUDA_TRY(ctx, cudaFreeHost(ctx->mbits_pinned[s]));
       ctx->mbits_pinned[s] = nullptr;
@@ -1230,6 +1252,44 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
     stage_rows(out + static_cast<int64_t>(pend_f0[s]) * d->out_frame_stride, d->out_pitch,
                d->out_frame_stride, ctx->stg_out[s], dpitch, dfs, pend_fk[s]);
     pend_f0[s] = -1;
+    return DPPX_OK;
+  };
+  std::vector<int> chunk_f0(chunks, 0);
+  std::vector<void*> span_dst, span_src;
+  std::vector<size_t> span_len;
+  const size_t cap_plane = adaptive ? dppx_adaptive_payload_capacity(M, N, b, n) : G;
+  // Exact-length D2H of chunk cj's payloads (its lengths are in lens_pinned),
+  // then the slot's out_done (image + payload copies of chunk cj queued).
+  auto issue_payload = [&](int cj) -> int {
+    const int sj = cj & 1, Fj = sizes[cj];
+    CUDA_TRY(ctx, cudaEventSynchronize(ctx->lens_ev[sj]));
+    const uint32_t* ln = ctx->lens_pinned[sj];
+    if (lens) std::memcpy(lens + static_cast<int64_t>(chunk_f0[cj]) * C, ln, sizeof(uint32_t) * Fj * C);
+    const int P = Fj * C;
+    span_dst.resize(P);
+    span_src.resize(P);
+    span_len.resize(P);
+    uint8_t* dst0 = stats + static_cast<int64_t>(chunk_f0[cj]) * C * sstride;
+    const uint8_t* src0 = static_cast<const uint8_t*>(ctx->stats[sj].p);
+    uint64_t bytes = 0;
+    for (int q = 0; q < P; ++q) {
+      span_dst[q] = dst0 + static_cast<int64_t>(q) * sstride;
+      span_src[q] = const_cast<uint8_t*>(src0 + static_cast<int64_t>(q) * dstride);
+      span_len[q] = std::min<size_t>(ln[q], cap_plane);  // (a corrupt length never over-reads the slot)
+      bytes += span_len[q];
+    }
+    cudaMemcpyAttributes attr{};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    size_t attr_idx = 0, fail_idx = 0;
+    if (cudaMemcpyBatchAsync(span_dst.data(), span_src.data(), span_len.data(), P, &attr, &attr_idx, 1,
+                             &fail_idx, ctx->s_out) != cudaSuccess) {
+      cudaGetLastError();  // batch API unavailable: one copy per span
+      for (int q = 0; q < P; ++q)
+        CUDA_TRY(ctx, cudaMemcpyAsync(span_dst[q], span_src[q], span_len[q], cudaMemcpyDeviceToHost,
+                                      ctx->s_out));
+    }
+    ctx->kstats.d2h_bytes += bytes;
+    CUDA_TRY(ctx, cudaEventRecord(ctx->out_done[sj], ctx->s_out));
     return DPPX_OK;
   };
   int f0 = 0;
@@ -1365,7 +1425,18 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
     CUDA_TRY(ctx, cudaEventRecord(ctx->comp_done[s], comp));
     // ---- D2H (output stream) ----
     CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->s_out, ctx->comp_done[s], 0));
-    if (pix) {
+    if (exact_payload) {
+      // this chunk's lengths, ahead of the image copies queued on s_out
+      CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->s_meta, ctx->comp_done[s], 0));
+      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->lens_pinned[s], dlens, sizeof(uint32_t) * Fk * C,
+                                    cudaMemcpyDeviceToHost, ctx->s_meta));
+      CUDA_TRY(ctx, cudaEventRecord(ctx->lens_ev[s], ctx->s_meta));
+      ctx->kstats.d2h_bytes += sizeof(uint32_t) * Fk * C;
+      // the previous chunk's payload spans go first: its slot is released
+      // (out_done) before this chunk's image copy is queued behind it
+      if (ci >= 1)
+        if (int rc2 = issue_payload(ci - 1)) return rc2;
+    } else if (pix) {
       const size_t w = adaptive ? dppx_adaptive_payload_capacity(M, N, b, n) : G;
       CUDA_TRY(ctx, cudaMemcpy2DAsync(stats + static_cast<int64_t>(f0) * C * sstride, sstride, dstats,
                                       dstride, w, static_cast<size_t>(Fk) * C, cudaMemcpyDeviceToHost,
@@ -1396,9 +1467,12 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
                                   cudaMemcpyDeviceToHost, ctx->s_out));
       ctx->kstats.d2h_bytes += static_cast<uint64_t>(Fk) * M * row;
     }
-    CUDA_TRY(ctx, cudaEventRecord(ctx->out_done[s], ctx->s_out));
+    if (!exact_payload) CUDA_TRY(ctx, cudaEventRecord(ctx->out_done[s], ctx->s_out));
+    chunk_f0[ci] = f0;
     f0 += Fk;
   }
+  if (exact_payload && chunks > 0)
+    if (int rc2 = issue_payload(chunks - 1)) return rc2;
   if (trace) std::fprintf(stderr, "pipe: issued %.2f ms\n", tp_ms());
   for (int k = 0; k < 2; ++k) {  // oldest pending slot first
     const int s = (chunks + k) & 1;
@@ -1502,7 +1576,8 @@ int dppx_ctx_create(int32_t device, dppx_ctx** out) {
   if (cudaSetDevice(device) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->s_in, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&ctx->s_out, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaStreamCreateWithFlags(&ctx->s_out, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->s_meta, cudaStreamNonBlocking) != cudaSuccess) {
     delete ctx;
     return DPPX_ERR_CUDA;
   }
@@ -1511,6 +1586,7 @@ int dppx_ctx_create(int32_t device, dppx_ctx** out) {
     cudaEventCreateWithFlags(&ctx->in_done[s], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->comp_done[s], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->out_done[s], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->lens_ev[s], cudaEventDisableTiming);
   }
   for (int i = 0; i < dppx_ctx::kMaxBands; ++i) {
     cudaEventCreateWithFlags(&ctx->band_in[i], cudaEventDisableTiming);
@@ -1553,6 +1629,8 @@ void dppx_ctx_destroy(dppx_ctx* ctx) {
     cudaEventDestroy(ctx->in_done[s]);
     cudaEventDestroy(ctx->comp_done[s]);
     cudaEventDestroy(ctx->out_done[s]);
+    cudaEventDestroy(ctx->lens_ev[s]);
+    if (ctx->lens_pinned[s]) cudaFreeHost(ctx->lens_pinned[s]);
   }
   if (ctx->seeds_pinned) cudaFreeHost(ctx->seeds_pinned);
   for (int i = 0; i < dppx_ctx::kMaxBands; ++i) {
@@ -1569,6 +1647,7 @@ void dppx_ctx_destroy(dppx_ctx* ctx) {
   cudaStreamDestroy(ctx->own_stream);
   cudaStreamDestroy(ctx->s_in);
   cudaStreamDestroy(ctx->s_out);
+  cudaStreamDestroy(ctx->s_meta);
   delete ctx;
 }
 

@@ -991,3 +991,29 @@ def test_reassemble_malformed_payload_stays_in_bounds(ctx, M, N, C, b, n):
     pls, img = ctx.pixelize_adaptive(frames, masks, p, dp.NOISE_NONE, None)
     rp, ri = _oracle_adaptive(frames, masks, p, "none", None)
     assert pls == rp and np.array_equal(img, ri)
+
+
+def test_host_pipeline_ships_only_written_payload_bytes(ctx):
+    """Host adaptive calls copy each payload's written length D2H (plus the
+    lengths), not the slot capacity: d2h bytes == image + sum(len) + 4/plane.
+    Payloads stay identical to the oracle, pinned and pageable, over many chunks."""
+    M, N, C, F = 72, 136, 3, 23
+    frames = oracle.synth_frames(4, F, M, N, C)
+    masks = oracle.synth_masks(4, F, M, N)
+    p = dp.make_privacy_params(0.5, 16, 16, 4)
+    seeds = dp.plane_seeds(42, F, C)
+    rp, ri = _oracle_adaptive(frames, masks, p, "keyed", seeds)
+    for pinned in (False, True):
+        fr, mk = frames, masks
+        if pinned:
+            fr = dp.pinned_empty(frames.shape)
+            fr[:] = frames
+            mk = dp.pinned_empty(masks.shape)
+            mk[:] = masks
+        ctx.set_chunk_frames(4)
+        ctx.reset_stats()
+        pls, img = ctx.pixelize_adaptive(fr, mk, p, dp.NOISE_KEYED, seeds)
+        ctx.set_chunk_frames(0)
+        st = ctx.stats()
+        assert pls == rp and np.array_equal(img, ri)
+        assert st["d2h_bytes"] == F * M * N * C + sum(len(x) for x in pls) + 4 * F * C, st
