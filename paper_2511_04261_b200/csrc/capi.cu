@@ -120,8 +120,8 @@ struct dppx_ctx {
   uint64_t* sd_pinned[2] = {nullptr, nullptr};
   size_t sd_pinned_n[2] = {0, 0};
   cudaEvent_t in_done[2] = {}, comp_done[2] = {}, out_done[2] = {};
-  // exact-length payload D2H: per slot, the chunk's lengths land in pinned
-  // memory first (lens_ev), then only the written bytes of each payload move
+  // written-length payload D2H: per slot, the chunk's lengths land in pinned
+  // memory first (lens_ev), then only the written bytes of the payloads move
   uint32_t* lens_pinned[2] = {nullptr, nullptr};
   size_t lens_pinned_n[2] = {0, 0};
   cudaEvent_t lens_ev[2] = {};
@@ -1183,11 +1183,11 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
                          d->out_frame_stride == row * M;
   // Bit-packed mask transport: 1/8 of the mask's PCIe bytes (maskpack.h).
   const bool try_bits = op == HostOp::Adaptive && ctx->mask_bits_mode == 1;
-  // Adaptive payloads leave the device with their written length only (4G + 4
-  // + S + (G - S) n^2 per plane, known once K0 has run), not the slot capacity:
-  // each chunk's lengths go D2H on s_meta right after its kernels, and the
-  // chunk's payload spans are issued one chunk later (DPPX_EXACT_PAYLOAD=0:
-  // copy whole slots, for A/B runs).
+  // Adaptive payloads leave the device with their written length (4G + 4 + S +
+  // (G - S) n^2 per plane, known once K0 has run), not the slot capacity: each
+  // chunk's lengths go D2H on s_meta right after its kernels, and the chunk's
+  // payloads are copied one chunk later (DPPX_EXACT_PAYLOAD=0: copy whole
+  // slots, for A/B runs).
   static const bool exact_env = !(std::getenv("DPPX_EXACT_PAYLOAD") &&
                                   std::getenv("DPPX_EXACT_PAYLOAD")[0] == '0');
   const bool exact_payload = pix && adaptive && exact_env;
@@ -1255,40 +1255,24 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
     return DPPX_OK;
   };
   std::vector<int> chunk_f0(chunks, 0);
-  std::vector<void*> span_dst, span_src;
-  std::vector<size_t> span_len;
   const size_t cap_plane = adaptive ? dppx_adaptive_payload_capacity(M, N, b, n) : G;
-  // Exact-length D2H of chunk cj's payloads (its lengths are in lens_pinned),
-  // then the slot's out_done (image + payload copies of chunk cj queued).
+  // D2H of chunk cj's payloads (its lengths are in lens_pinned): one 2-D copy
+  // of the chunk's longest written payload per plane slot -- the planes of a
+  // chunk share their masks frame by frame, so this is within a few bytes of
+  // the written total -- then the slot's out_done (chunk cj's image and
+  // payload copies are queued).
   auto issue_payload = [&](int cj) -> int {
     const int sj = cj & 1, Fj = sizes[cj];
     CUDA_TRY(ctx, cudaEventSynchronize(ctx->lens_ev[sj]));
     const uint32_t* ln = ctx->lens_pinned[sj];
     if (lens) std::memcpy(lens + static_cast<int64_t>(chunk_f0[cj]) * C, ln, sizeof(uint32_t) * Fj * C);
-    const int P = Fj * C;
-    span_dst.resize(P);
-    span_src.resize(P);
-    span_len.resize(P);
-    uint8_t* dst0 = stats + static_cast<int64_t>(chunk_f0[cj]) * C * sstride;
-    const uint8_t* src0 = static_cast<const uint8_t*>(ctx->stats[sj].p);
-    uint64_t bytes = 0;
-    for (int q = 0; q < P; ++q) {
-      span_dst[q] = dst0 + static_cast<int64_t>(q) * sstride;
-      span_src[q] = const_cast<uint8_t*>(src0 + static_cast<int64_t>(q) * dstride);
-      span_len[q] = std::min<size_t>(ln[q], cap_plane);  // (a corrupt length never over-reads the slot)
-      bytes += span_len[q];
-    }
-    cudaMemcpyAttributes attr{};
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    size_t attr_idx = 0, fail_idx = 0;
-    if (cudaMemcpyBatchAsync(span_dst.data(), span_src.data(), span_len.data(), P, &attr, &attr_idx, 1,
-                             &fail_idx, ctx->s_out) != cudaSuccess) {
-      cudaGetLastError();  // batch API unavailable: one copy per span
-      for (int q = 0; q < P; ++q)
-        CUDA_TRY(ctx, cudaMemcpyAsync(span_dst[q], span_src[q], span_len[q], cudaMemcpyDeviceToHost,
-                                      ctx->s_out));
-    }
-    ctx->kstats.d2h_bytes += bytes;
+    size_t w = 0;
+    for (int q = 0; q < Fj * C; ++q) w = std::max<size_t>(w, ln[q]);
+    w = std::min(w, cap_plane);  // (a corrupt length never over-reads the slot)
+    CUDA_TRY(ctx, cudaMemcpy2DAsync(stats + static_cast<int64_t>(chunk_f0[cj]) * C * sstride, sstride,
+                                    ctx->stats[sj].p, dstride, w, static_cast<size_t>(Fj) * C,
+                                    cudaMemcpyDeviceToHost, ctx->s_out));
+    ctx->kstats.d2h_bytes += static_cast<uint64_t>(w) * Fj * C;
     CUDA_TRY(ctx, cudaEventRecord(ctx->out_done[sj], ctx->s_out));
     return DPPX_OK;
   };
@@ -1432,7 +1416,7 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
                                     cudaMemcpyDeviceToHost, ctx->s_meta));
       CUDA_TRY(ctx, cudaEventRecord(ctx->lens_ev[s], ctx->s_meta));
       ctx->kstats.d2h_bytes += sizeof(uint32_t) * Fk * C;
-      // the previous chunk's payload spans go first: its slot is released
+      // the previous chunk's payloads go first: its slot is released
       // (out_done) before this chunk's image copy is queued behind it
       if (ci >= 1)
         if (int rc2 = issue_payload(ci - 1)) return rc2;

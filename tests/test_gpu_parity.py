@@ -994,9 +994,10 @@ def test_reassemble_malformed_payload_stays_in_bounds(ctx, M, N, C, b, n):
 
 
 def test_host_pipeline_ships_only_written_payload_bytes(ctx):
-    """Host adaptive calls copy each payload's written length D2H (plus the
-    lengths), not the slot capacity: d2h bytes == image + sum(len) + 4/plane.
-    Payloads stay identical to the oracle, pinned and pageable, over many chunks."""
+    """Host adaptive calls copy the written payload lengths D2H (per chunk, the
+    longest written payload of the chunk's planes, plus the lengths), not the
+    slot capacity. Payloads stay identical to the oracle, pinned and pageable,
+    over many chunks."""
     M, N, C, F = 72, 136, 3, 23
     frames = oracle.synth_frames(4, F, M, N, C)
     masks = oracle.synth_masks(4, F, M, N)
@@ -1016,4 +1017,7 @@ def test_host_pipeline_ships_only_written_payload_bytes(ctx):
         ctx.set_chunk_frames(0)
         st = ctx.stats()
         assert pls == rp and np.array_equal(img, ri)
-        assert st["d2h_bytes"] == F * M * N * C + sum(len(x) for x in pls) + 4 * F * C, st
+        lo = F * M * N * C + sum(len(x) for x in pls) + 4 * F * C
+        hi = F * M * N * C + F * C * max(len(x) for x in pls) + 4 * F * C
+        cap = F * M * N * C + F * C * dp.adaptive_payload_capacity(M, N, 16, 4) + 4 * F * C
+        assert lo <= st["d2h_bytes"] <= hi < cap, (st, lo, hi, cap)
