@@ -117,7 +117,8 @@ typedef enum {
   DPPX_K_EXPAND = 3,   /* K2: statistics -> pixels                            */
   DPPX_K_AUX = 4,      /* synthetic generator, payload checks                 */
   DPPX_K_ROWS = 5,     /* K1r: row-streaming stats for other grid sides        */
-  DPPX_K_COUNT = 6
+  DPPX_K_SWEEP = 6,    /* K1s: one-read statistics of a grid-size x eps sweep  */
+  DPPX_K_COUNT = 7
 } dppx_kernel_family;
 
 typedef struct {
@@ -191,6 +192,23 @@ int dppx_reassemble_dev(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8
 /* Synthetic workload (bench / tests): frames f0..f0+F-1, see oracle/dppx_oracle.c. */
 int dppx_synth_frames_dev(dppx_ctx* ctx, const dppx_frames_desc* desc, uint32_t data_seed,
                           uint32_t f0, uint8_t* img, uint8_t* mask /* nullable */);
+
+/* One HBM read of the frames for every run of a uniform grid-size x epsilon
+ * sweep (run_sweep cli.cpp:231-288 / SURVEY 8(d) config 3). Run (i, j) is
+ * pixelize_parallel with grid side b_list[i] and epsilon eps_list[j] (m and
+ * noise shared): statistics at means[i*ne + j] (F*C planes of G_i bytes, as
+ * dppx_pixelize_uniform_dev) and, if out != NULL and out[i*ne + j] != NULL, its
+ * reconstructed image there (desc out_pitch / out_frame_stride). Bytes are
+ * identical to separate dppx_pixelize_uniform_dev calls. Grid sides in
+ * {4, 8, 16, 32} (KEYED / PHILOX / NONE noise, C in {1, 3}, 16-byte aligned
+ * frames): one statistics kernel reads each frame once -- 4-px cell sums over
+ * the largest padded extent aggregate exactly to the larger sides, and the
+ * keyed bits and Laplace magnitude of a cell are drawn once for all eps --
+ * then one broadcast per run writes the images. Other lists run per b. */
+int dppx_pixelize_uniform_sweep_dev(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* img,
+                                    int32_t nb, const int32_t* b_list, int32_t ne,
+                                    const double* eps_list, int32_t m, const dppx_noise* noise,
+                                    uint8_t* const* means, uint8_t* const* out /* nullable */);
 
 /* EXTENSION (north-star "per-region complexity measure"; no reference
  * counterpart -- the reference takes external masks): cell

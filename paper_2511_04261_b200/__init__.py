@@ -42,8 +42,8 @@ _lib = C.CDLL(LIB_PATH)
 OK, ERR_INVALID, ERR_CORRUPT, ERR_CUDA, ERR_OOM, ERR_NO_DEVICE = range(6)
 ERR_NOT_A_RECORD, ERR_UNSUPPORTED_VERSION, ERR_CORRUPTION = 6, 7, 8
 NOISE_NONE, NOISE_KEYED, NOISE_PHILOX, NOISE_INJECTED = range(4)
-K_CLASSIFY, K_STATS, K_GENERIC, K_EXPAND, K_AUX, K_ROWS, K_COUNT = range(7)
-KERNEL_FAMILIES = ("classify", "stats_tma", "stats_generic", "expand", "aux", "stats_rows")
+K_CLASSIFY, K_STATS, K_GENERIC, K_EXPAND, K_AUX, K_ROWS, K_SWEEP, K_COUNT = range(8)
+KERNEL_FAMILIES = ("classify", "stats_tma", "stats_generic", "expand", "aux", "stats_rows", "sweep")
 
 
 class Geometry(C.Structure):
@@ -130,6 +130,9 @@ ABI = {
     "dppx_reassemble_dev": (C.c_int, [_ctxp, _descp, _vp, C.c_int64, _vp, C.c_int32, C.c_int32,
                                       _vp]),
     "dppx_synth_frames_dev": (C.c_int, [_ctxp, _descp, C.c_uint32, C.c_uint32, _vp, _vp]),
+    "dppx_pixelize_uniform_sweep_dev": (C.c_int, [_ctxp, _descp, _vp, C.c_int32, C.POINTER(C.c_int32),
+                                                  C.c_int32, C.POINTER(C.c_double), C.c_int32, _np,
+                                                  C.POINTER(_vp), C.POINTER(_vp)]),
     "dppx_pixelize_uniform": (C.c_int, [_ctxp, _descp, _vp, _pp, _np, _vp, _vp]),
     "dppx_pixelize_adaptive": (C.c_int, [_ctxp, _descp, _vp, _vp, _pp, _np, _vp, C.c_int64, _vp,
                                          _vp]),
@@ -604,6 +607,20 @@ class Context:
         self._check(_lib.dppx_broadcast_means_dev(self._h, C.byref(desc), _ptr(means), b,
                                                   _ptr(out)), "broadcast_means_dev")
 
+    def pixelize_uniform_sweep_dev(self, desc: FramesDesc, img, b_list, eps_list, m, noise_struct,
+                                   means, out=None):
+        """One read of the frames for every (b, eps) run of a uniform sweep
+        (dppx_pixelize_uniform_sweep_dev). means / out: sequences of device
+        tensors in run order (i * len(eps_list) + j); out entries may be None."""
+        nb, ne = len(b_list), len(eps_list)
+        bl = (C.c_int32 * nb)(*b_list)
+        el = (C.c_double * ne)(*eps_list)
+        mp = (_vp * (nb * ne))(*[t.data_ptr() for t in means])
+        op = None if out is None else (_vp * (nb * ne))(*[None if t is None else t.data_ptr() for t in out])
+        self._check(_lib.dppx_pixelize_uniform_sweep_dev(self._h, C.byref(desc), _ptr(img), nb, bl, ne, el, m,
+                                                         C.byref(noise_struct), mp, op),
+                    "pixelize_uniform_sweep_dev")
+
     def synth_frames_dev(self, desc, data_seed, f0, img, mask=None):
         self._check(_lib.dppx_synth_frames_dev(self._h, C.byref(desc), data_seed, f0, _ptr(img),
                                                _ptr(mask)), "synth_frames_dev")
@@ -684,6 +701,7 @@ for _name in ("stream", "set_stream", "set_chunk_frames", "set_exact_noise", "se
               "lg2_max_error", "pixelize_reference", "pixelize_adaptive_variance",
               "reconstruct_record", "classify_regions", "metrics", "device_laplace",
               "pixelize_adaptive_dev", "pixelize_uniform_dev", "pixelize_adaptive_variance_dev",
+              "pixelize_uniform_sweep_dev",
               "reassemble_dev", "broadcast_means_dev", "synth_frames_dev"):
     setattr(Group, _name, property(lambda self, _n=_name: _group_unsupported(_n).__get__(self))
             if _name == "stream" else _group_unsupported(_name))

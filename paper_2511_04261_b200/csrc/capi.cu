@@ -63,6 +63,24 @@ cudaError_t launch_repitch(uint8_t* dst, int64_t dpitch, const uint8_t* src, int
                            int64_t width, int64_t rows, cudaStream_t s);
 cudaError_t launch_debug_laplace(uint64_t mixed, const uint32_t* keys, int count, double sigma,
                                  double* out, cudaStream_t s);
+constexpr int kSweepMaxLevels = 4;
+constexpr int kSweepMaxEps = 4;
+struct SweepLevels {  // sweep.cu
+  int nlev;
+  int ne;
+  uint32_t active;
+  int GR[kSweepMaxLevels], GC[kSweepMaxLevels];
+  int64_t G[kSweepMaxLevels];
+  double area[kSweepMaxLevels];
+  double sigma[kSweepMaxLevels][kSweepMaxEps];
+  float sigmaf[kSweepMaxLevels][kSweepMaxEps];
+  float margin[kSweepMaxLevels][kSweepMaxEps];
+  uint8_t* means[kSweepMaxLevels][kSweepMaxEps];
+};
+using SweepKernel = void (*)(const CUtensorMap, const StatsArgs, const SweepLevels);
+SweepKernel select_sweep_kernel(int C, int nlev);
+cudaError_t launch_sweep(SweepKernel k, const CUtensorMap& tin, const StatsArgs& a, const SweepLevels& L,
+                         int grid, size_t smem, cudaStream_t s);
 }  // namespace dppx
 
 using namespace dppx;
@@ -1724,6 +1742,145 @@ int dppx_pixelize_uniform_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const ui
   return pixelize_dev(ctx, d, img, nullptr, pp, nz, nz ? nz->injected : nullptr, means, g.G,
                       nullptr, out, false, ctx->seeds, ctx->seeds_pinned, ctx->seeds_pinned_n,
                       ctx->seeds_ev, true);
+}
+
+int dppx_pixelize_uniform_sweep_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img,
+                                    int32_t nb, const int32_t* b_list, int32_t ne, const double* eps_list,
+                                    int32_t m, const dppx_noise* nz, uint8_t* const* means,
+                                    uint8_t* const* out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (nb < 1 || ne < 1 || !b_list || !eps_list || !means)
+    return set_err(ctx, DPPX_ERR_INVALID, "sweep lists must be non-empty");
+  if (int rc = check_desc(ctx, d, false, out != nullptr)) return rc;
+  // Every run is a valid pixelize_parallel call (make_privacy_params, grid_dims,
+  // mirror_pad checks), as run_sweep would find it.
+  std::vector<dppx_privacy_params> pp(static_cast<size_t>(nb) * ne);
+  for (int i = 0; i < nb; ++i) {
+    BatchGeom gi;
+    if (int rc = geometry(ctx, d->height, d->width, d->channels, d->frames, b_list[i], 1, &gi, true)) return rc;
+    for (int j = 0; j < ne; ++j)
+      if (dppx_make_privacy_params(eps_list[j], m, b_list[i], 1, &pp[i * ne + j]) != DPPX_OK)
+        return set_err(ctx, DPPX_ERR_INVALID, "make_privacy_params: invalid sweep parameters");
+    for (int j = 0; j < ne; ++j)
+      if (!means[i * ne + j]) return set_err(ctx, DPPX_ERR_INVALID, "null means pointer");
+  }
+  if (d->frames == 0) return DPPX_OK;
+  if (!img) return set_err(ctx, DPPX_ERR_INVALID, "null image pointer");
+  // Fused one-read path?
+  int bmax = 0;
+  uint32_t active = 0;
+  bool fused = ne <= kSweepMaxEps && (d->channels == 1 || d->channels == 3) &&
+               (!nz || nz->kind != DPPX_NOISE_INJECTED) && !std::getenv("DPPX_NO_SWEEP") &&
+               aligned16(img) && d->pitch % 16 == 0 && d->frame_stride % 16 == 0;
+  for (int i = 0; i < nb && fused; ++i) {
+    const int b = b_list[i];
+    const int lv = b == 4 ? 0 : b == 8 ? 1 : b == 16 ? 2 : b == 32 ? 3 : -1;
+    if (lv < 0 || (active >> lv) & 1u) fused = false;
+    else active |= 1u << lv;
+    bmax = std::max(bmax, b);
+  }
+  const int nlev = bmax == 8 ? 2 : bmax == 16 ? 3 : bmax == 32 ? 4 : 0;
+  SweepKernel k = fused ? select_sweep_kernel(d->channels, nlev) : nullptr;
+  BatchGeom g;
+  if (k && geometry(ctx, d->height, d->width, d->channels, d->frames, bmax, 1, &g, true) != DPPX_OK) {
+    k = nullptr;  // the largest side's padding would exceed the image: per-run path
+    ctx->err.clear();
+  }
+  if (!k) {
+    for (int i = 0; i < nb; ++i)
+      for (int j = 0; j < ne; ++j)
+        if (int rc = dppx_pixelize_uniform_dev(ctx, d, img, &pp[i * ne + j], nz, means[i * ne + j],
+                                               out ? out[i * ne + j] : nullptr))
+          return rc;
+    return DPPX_OK;
+  }
+  StatsArgs a{};
+  a.g = g;
+  a.img = img;
+  a.pitch = d->pitch;
+  a.fstride = d->frame_stride;
+  a.exact_noise = ctx->exact_noise ? 1 : 0;
+  a.row_begin = 0;
+  a.row_count = g.GR;
+  if (int rc = prepare_noise(ctx, nz, g.F * g.C, nullptr, g, &pp[0], &a.noise, ctx->stream, ctx->seeds,
+                             ctx->seeds_pinned, ctx->seeds_pinned_n, ctx->seeds_ev, true))
+    return rc;
+  SweepLevels L{};
+  L.nlev = nlev;
+  L.ne = ne;
+  L.active = active;
+  for (int lv = 0; lv < nlev; ++lv) {
+    dppx_geometry gg;
+    dppx_grid_dims(d->height, d->width, 4 << lv, &gg);
+    L.GR[lv] = gg.grid_rows;
+    L.GC[lv] = gg.grid_cols;
+    L.G[lv] = static_cast<int64_t>(gg.grid_rows) * gg.grid_cols;
+    L.area[lv] = static_cast<double>(4 << lv) * (4 << lv);
+  }
+  for (int i = 0; i < nb; ++i) {
+    const int lv = b_list[i] == 4 ? 0 : b_list[i] == 8 ? 1 : b_list[i] == 16 ? 2 : 3;
+    for (int j = 0; j < ne; ++j) {
+      L.sigma[lv][j] = pp[i * ne + j].sigma;
+      L.sigmaf[lv][j] = static_cast<float>(pp[i * ne + j].sigma);
+      L.margin[lv][j] = 2e-3f + static_cast<float>(pp[i * ne + j].sigma) * 4e-6f;  // fast_margin
+      L.means[lv][j] = means[i * ne + j];
+    }
+  }
+  const int64_t row_bytes = static_cast<int64_t>(g.N) * g.C;
+  const int tile = stats_tile_px();
+  a.pack = 1;
+  a.slot_px = tile;
+  a.slot_stride = static_cast<int>(round_up(static_cast<int64_t>(g.b) * tile * g.C, 128));
+  a.row_slack = a.pitch >= round_up(row_bytes, 16) ? 1 : 0;
+  const int64_t in_row = a.row_slack ? round_up(row_bytes, 16) : row_bytes / 16 * 16;
+  CUtensorMap tin{};
+  if (!encode_frames_map(&tin, img, in_row, g.M, g.F, a.pitch, a.fstride, tile * g.C, g.b)) {
+    for (int i = 0; i < nb; ++i)
+      for (int j = 0; j < ne; ++j)
+        if (int rc = dppx_pixelize_uniform_dev(ctx, d, img, &pp[i * ne + j], nz, means[i * ne + j],
+                                               out ? out[i * ne + j] : nullptr))
+          return rc;
+    return DPPX_OK;
+  }
+  a.tensor_in_bytes = static_cast<int>(in_row);
+  a.tiles_per_row = (g.GC * g.b + tile - 1) / tile;
+  const int64_t units = static_cast<int64_t>(g.F) * g.GR * a.tiles_per_row;
+  if (units > 0x7FFFFFFF) return set_err(ctx, DPPX_ERR_INVALID, "batch too large for one launch");
+  a.units = static_cast<int>(units);
+  a.div_tiles = make_fastdiv(static_cast<uint32_t>(a.tiles_per_row));
+  a.div_rows = make_fastdiv(static_cast<uint32_t>(g.GR));
+  a.stages = 2;
+  const size_t smem = static_cast<size_t>(round_up(static_cast<int64_t>(g.b) * tile * g.C, 128)) * 2;
+  const auto key = std::make_pair(reinterpret_cast<const void*>(k), smem);
+  int per_sm = 0;
+  auto it = ctx->occupancy.find(key);
+  if (it == ctx->occupancy.end()) {
+    CUDA_TRY(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, stats_threads(), smem));
+    ctx->occupancy[key] = per_sm;
+  } else {
+    per_sm = it->second;
+  }
+  const int grid = static_cast<int>(std::min<int64_t>(units, static_cast<int64_t>(std::max(per_sm, 1)) * ctx->sms));
+  if (int rc = ensure(ctx, ctx->work, 16, /*zero=*/true)) return rc;
+  a.work_counter = static_cast<int*>(ctx->work.p);
+  PendingTiming pt;
+  timing_begin(ctx, DPPX_K_SWEEP, &pt);
+  CUDA_TRY(ctx, launch_sweep(k, tin, a, L, grid, smem, ctx->stream));
+  timing_end(ctx, &pt);
+  // The runs' images: broadcast_means of their statistics (write-only K2).
+  if (out) {
+    for (int i = 0; i < nb; ++i)
+      for (int j = 0; j < ne; ++j)
+        if (out[i * ne + j]) {
+          dppx_geometry gg;
+          dppx_grid_dims(d->height, d->width, b_list[i], &gg);
+          if (int rc = expand_dev(ctx, d, means[i * ne + j], static_cast<int64_t>(gg.grid_rows) * gg.grid_cols,
+                                  nullptr, b_list[i], 1, out[i * ne + j], false))
+            return rc;
+        }
+  }
+  return DPPX_OK;
 }
 
 int dppx_pixelize_adaptive_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img,

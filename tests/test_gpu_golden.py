@@ -137,3 +137,41 @@ def test_config_digests_rgb(ctx, name):
         assert hashlib.sha256(stats[ch].tobytes()).hexdigest() == pl["stats_sha"], (name, ch)
         plane = np.ascontiguousarray(img[0, :, :, ch])
         assert hashlib.sha256(plane.tobytes()).hexdigest() == pl["image_sha"], (name, ch)
+
+
+def test_one_read_sweep_matches_reference_digests(ctx):
+    """K1s (dppx_pixelize_uniform_sweep_dev): ONE read of the 1917 x 1083 RGB
+    frame for all 12 (b, eps) runs of config 3; every run's means and image
+    equal the reference's own (config_digests.json sweep_b*_eps*)."""
+    import torch
+    cases = _config_cases()
+    M, N, C = 1083, 1917, 3
+    bl, el = [4, 8, 16, 32], [0.1, 0.5, 1.0]
+    dev = torch.device("cuda:0")
+    pitch = (N * C + 15) // 16 * 16
+    d = dp._desc(M, N, C, 1, pitch=pitch, opitch=pitch)
+    frames = oracle.synth_frames(5, 1, M, N, C)
+    img = torch.zeros((1, M, pitch), dtype=torch.uint8, device=dev)
+    img[:, :, :N * C] = torch.from_numpy(frames.reshape(1, M, N * C)).to(dev)
+    nz, keep = dp.Context._noise(dp.NOISE_KEYED, dp.plane_seeds(42, 1, 3, frame0=5))
+    means, outs = [], []
+    for b in bl:
+        G = dp.grid_dims(M, N, b).grid_count()
+        for _ in el:
+            means.append(torch.zeros((C, G), dtype=torch.uint8, device=dev))
+            outs.append(torch.zeros((1, M, pitch), dtype=torch.uint8, device=dev))
+    ctx.reset_stats()
+    ctx.pixelize_uniform_sweep_dev(d, img, bl, el, 16, nz, means, outs)
+    ctx.synchronize()
+    assert ctx.stats()["launches"]["sweep"] == 1 and ctx.stats()["launches"]["stats_tma"] == 0
+    k = 0
+    for b in bl:
+        for e in el:
+            c = cases[f"sweep_b{b}_eps{e}"]
+            mh = means[k].cpu().numpy()
+            im = outs[k].cpu().numpy()[0, :, :N * C].reshape(M, N, C)
+            for ch, pl in enumerate(c["planes"]):
+                assert hashlib.sha256(mh[ch].tobytes()).hexdigest() == pl["stats_sha"], (b, e, ch)
+                plane = np.ascontiguousarray(im[:, :, ch])
+                assert hashlib.sha256(plane.tobytes()).hexdigest() == pl["image_sha"], (b, e, ch)
+            k += 1

@@ -1021,3 +1021,59 @@ def test_host_pipeline_ships_only_written_payload_bytes(ctx):
         hi = F * M * N * C + F * C * max(len(x) for x in pls) + 4 * F * C
         cap = F * M * N * C + F * C * dp.adaptive_payload_capacity(M, N, 16, 4) + 4 * F * C
         assert lo <= st["d2h_bytes"] <= hi < cap, (st, lo, hi, cap)
+
+
+@pytest.mark.parametrize("M,N,C,bl,el,kind", [
+    (1083, 1917, 3, [4, 8, 16, 32], [0.1, 0.5, 1.0], "keyed"),
+    (61, 99, 3, [4, 8, 16, 32], [0.1, 0.5, 1.0], "philox"),
+    (61, 99, 1, [4, 8, 16, 32], [0.5, 2.0], "keyed"),
+    (77, 530, 3, [8, 32], [0.1, 0.5, 1.0], "keyed"),
+    (40, 1100, 3, [16], [0.3, 1.0, 3.0, 9.0], "keyed"),
+    (64, 64, 3, [4, 8], [1.0], "none"),
+    (33, 50, 3, [4, 8, 16, 32], [0.5, 1.0, 2.0], "keyed"),
+    (50, 70, 3, [4, 12, 16], [0.5, 1.0, 2.0], "keyed"),  # 12: per-run path
+])
+def test_one_read_sweep_equals_separate_runs(ctx, M, N, C, bl, el, kind):
+    """The one-read sweep kernel's statistics and images are byte-identical to
+    separate pixelize_uniform_dev runs (themselves pinned to the oracle), for
+    keyed / Philox / no noise, inactive levels, eps lists of 1-4, and grid
+    sides outside the power-of-two chain (per-run fallback)."""
+    import torch
+    dev = torch.device("cuda:0")
+    F = 3
+    pitch = (N * C + 15) // 16 * 16
+    d = dp._desc(M, N, C, F, pitch=pitch, opitch=pitch)
+    img = torch.empty((F, M, pitch), dtype=torch.uint8, device=dev)
+    ctx.synth_frames_dev(d, 3, 0, img)
+    nk = {"keyed": dp.NOISE_KEYED, "philox": dp.NOISE_PHILOX, "none": dp.NOISE_NONE}[kind]
+    seeds = dp.plane_seeds(9, F, C) if kind == "keyed" else ([9] if kind == "philox" else None)
+    nz, keep = dp.Context._noise(nk, seeds, frame_base=4)
+    means, outs, ref_means, ref_outs = [], [], [], []
+    for b in bl:
+        G = dp.grid_dims(M, N, b).grid_count()
+        for e in el:
+            means.append(torch.zeros((F * C, G), dtype=torch.uint8, device=dev))
+            outs.append(torch.zeros((F, M, pitch), dtype=torch.uint8, device=dev))
+            rm = torch.zeros((F * C, G), dtype=torch.uint8, device=dev)
+            ro = torch.zeros((F, M, pitch), dtype=torch.uint8, device=dev)
+            ctx.pixelize_uniform_dev(d, img, dp.make_privacy_params(e, 16, b), nz, rm, ro)
+            ref_means.append(rm)
+            ref_outs.append(ro)
+    ctx.reset_stats()
+    ctx.pixelize_uniform_sweep_dev(d, img, bl, el, 16, nz, means, outs)
+    ctx.synchronize()
+    fused = all(b in (4, 8, 16, 32) for b in bl) and len(bl) > 1 or bl == [16]
+    assert (ctx.stats()["launches"]["sweep"] == 1) == fused
+    for k in range(len(means)):
+        assert torch.equal(means[k], ref_means[k]), k
+        assert torch.equal(outs[k][:, :, :N * C], ref_outs[k][:, :, :N * C]), k
+    if kind == "keyed" and M * N < 10000:  # and the oracle directly
+        fr = img[:, :, :N * C].cpu().numpy().reshape(F, M, N, C)
+        k = 0
+        for b in bl:
+            for e in el:
+                p = dp.make_privacy_params(e, 16, b)
+                for f in range(F):
+                    rm, ri = oracle.pixelize_uniform(fr[f], b, p.sigma, "keyed", seeds[f * C:(f + 1) * C])
+                    assert np.array_equal(means[k].cpu().numpy()[f * C:(f + 1) * C], rm), (b, e, f)
+                k += 1
