@@ -70,6 +70,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-pad-scratch", action="store_true",
                     help="never write output row padding (A/B of dppx_ctx_set_out_pad_scratch)")
+    ap.add_argument("--sweep-mode", choices=["fused", "runs"], default="fused",
+                    help="sweep workload: one-read K1s + per-run broadcast (fused) or 12 separate "
+                         "K1 runs (runs)")
     ap.add_argument("--chunk-frames", type=int, default=0,
                     help="host pipeline frames per chunk (0 = automatic)")
     return ap.parse_args()
@@ -375,18 +378,25 @@ def main():
     seeds = sh.plane_seed_list(42, my, C)
     nz, keep = dp.Context._noise(dp.NOISE_KEYED, seeds)
     sweep = args.workload == "sweep"
-    jobs = []  # (params, means buffer, G) per run of one step
+    fused = sweep and args.sweep_mode == "fused"
+    jobs = []  # (params, means buffer, G, image buffer) per run of one step
     if sweep:
         for bb, ee in SWEEP:
             gb = dp.grid_dims(M, N, bb).grid_count()
             jobs.append((dp.make_privacy_params(ee, m, bb),
-                         torch.zeros((F * C, gb), dtype=torch.uint8, device=dev), gb))
+                         torch.zeros((F * C, gb), dtype=torch.uint8, device=dev), gb,
+                         out if not fused else torch.empty_like(img)))
     runs = len(jobs) if sweep else 1
+    sweep_b = sorted({bb for bb, _ in SWEEP})
+    sweep_e = sorted({ee for _, ee in SWEEP})
 
     def step():
-        if sweep:
-            for pj, mj, _ in jobs:
-                ctx.pixelize_uniform_dev(d, img, pj, nz, mj, out)
+        if fused:  # one read of the frames, every run's statistics + image
+            ctx.pixelize_uniform_sweep_dev(d, img, sweep_b, sweep_e, m, nz, [j[1] for j in jobs],
+                                           [j[3] for j in jobs])
+        elif sweep:
+            for pj, mj, _, oj in jobs:
+                ctx.pixelize_uniform_dev(d, img, pj, nz, mj, oj)
         elif adaptive:
             ctx.pixelize_adaptive_dev(d, img, mask, p, nz, stats, sstride, lens, out)
         else:
@@ -398,7 +408,7 @@ def main():
     # payload bytes actually written (for the roofline's algorithmic bytes)
     payload_bytes = int(lens.sum().item()) if adaptive else F * C * G
     if sweep:
-        payload_bytes = sum(F * C * gj for _, _, gj in jobs) / runs  # mean per K1 launch
+        payload_bytes = sum(F * C * j[2] for j in jobs) / runs  # mean per K1 launch
     # ---- timed region: device-resident ----
     stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
     ctx.reset_stats()
@@ -437,13 +447,43 @@ def main():
     # roofline of K1 (dominant kernel): algorithmic bytes / measured duration
     kfam = ("stats_tma" if st["launches"]["stats_tma"] else
             "stats_rows" if st["launches"].get("stats_rows") else "stats_generic")
-    k1_launches = max(1, st["launches"][kfam])
-    k1_ms = st["device_ms"][kfam] / k1_launches
-    k1_bytes = int(F * M * N * C * 2 + payload_bytes)  # read frame, write image, write stats
+    sweep_info = None
+    if fused:
+        # K1s reads each frame once and writes 12 means arrays; 12 broadcasts
+        # (K2, write-only) produce the images. The dominant kernel is K2.
+        means_bytes = sum(F * C * j[2] for j in jobs)
+        s_ms = st["device_ms"]["sweep"] / max(1, st["launches"]["sweep"])
+        e_ms = st["device_ms"]["expand"] / max(1, st["launches"]["expand"])
+        s_bytes = F * M * N * C + means_bytes
+        e_bytes = F * M * N * C + means_bytes / runs
+        per_run_bytes = runs * 2 * F * M * N * C + means_bytes  # 12 separate read+write runs
+        one_read_bytes = F * M * N * C * (1 + runs) + 2 * means_bytes
+        step_s = ms_total / args.steps / 1e3
+        pk, _ = measured_peak()
+        sweep_info = {
+            "k1s_ms": round(s_ms, 4), "k1s_algorithmic_bytes": int(s_bytes),
+            "k1s_gbs": round(s_bytes / (s_ms / 1e3) / 1e9, 1),
+            "k1s_frac": round(s_bytes / (s_ms / 1e3) / 1e9 / pk, 4),
+            "k2_ms_per_run": round(e_ms, 4), "k2_algorithmic_bytes_per_run": int(e_bytes),
+            "k2_frac": round(e_bytes / (e_ms / 1e3) / 1e9 / pk, 4),
+            "step_bytes_one_read": int(one_read_bytes),
+            "step_bytes_per_run_accounting": int(per_run_bytes),
+            "step_frac_one_read": round(one_read_bytes / step_s / 1e9 / pk, 4),
+            "step_frac_per_run_accounting": round(per_run_bytes / step_s / 1e9 / pk, 4),
+            "note": "one read of each frame for all 12 runs (K1s), then 12 write-only broadcasts"}
+        kfam = "expand"
+        k1_launches = max(1, st["launches"]["expand"])
+        k1_ms = e_ms
+        k1_bytes = int(e_bytes)
+    else:
+        k1_launches = max(1, st["launches"][kfam])
+        k1_ms = st["device_ms"][kfam] / k1_launches
+        k1_bytes = int(F * M * N * C * 2 + payload_bytes)  # read frame, write image, write stats
     k0_bytes = (F * M * N + 4 * G * C * F + 4 * F * C) if adaptive else 0
     peak, peak_src = measured_peak()
     achieved = k1_bytes / (k1_ms / 1e3) / 1e9
-    step_gbs = (k1_bytes * runs + k0_bytes) / (ms_total / args.steps / 1e3) / 1e9
+    step_gbs = ((sweep_info["step_bytes_one_read"] if fused else k1_bytes * runs + k0_bytes)
+                / (ms_total / args.steps / 1e3) / 1e9)
     traffic = ncu_traffic(args.workload)
     launches_timed = sum(st["launches"].values())
 
@@ -495,11 +535,11 @@ def main():
         nze, keep_e = dp.Context._noise(dp.NOISE_KEYED, seeds_e)
         import ctypes as Ct
 
-        h_means = [torch.zeros((Fe * C, gj), dtype=torch.uint8).pin_memory() for _, _, gj in jobs]
+        h_means = [torch.zeros((Fe * C, j[2]), dtype=torch.uint8).pin_memory() for j in jobs]
 
         def e2e_step():
             if sweep:
-                for (pj, _, _), hm in zip(jobs, h_means):
+                for (pj, _, _, _), hm in zip(jobs, h_means):
                     ctx._check(dp._lib.dppx_pixelize_uniform(ctx._h, Ct.byref(de), h_img.data_ptr(),
                                                              Ct.byref(pj), Ct.byref(nze),
                                                              hm.data_ptr(), h_out.data_ptr()), "e2e")
@@ -609,7 +649,9 @@ def main():
             "config": config,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": traffic, "kernel": f"K1 {kfam}",
+                         "traffic": traffic,
+                         "kernel": ("K2 expand (per-run broadcast of the one-read sweep)" if fused
+                                    else f"K1 {kfam}"),
                          "algorithmic_bytes_per_launch": k1_bytes,
                          "avg_launch_ms": round(k1_ms, 4), "peak_source": peak_src,
                          # context only: HGX nominal 7.7 TB/s (B200_PROFILING.md)
@@ -619,6 +661,7 @@ def main():
                          "k0_ms_per_launch": round(st["device_ms"]["classify"] /
                                                    max(1, st["launches"]["classify"]), 4)},
             "cpu_baseline": cpu,
+            "sweep": sweep_info,
             "reconstruct": recon,
             "e2e": e2e,
             "gpu_launches": launches_timed,
