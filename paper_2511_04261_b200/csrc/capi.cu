@@ -1849,8 +1849,11 @@ int dppx_pixelize_uniform_sweep_dev(dppx_ctx* ctx, const dppx_frames_desc* d, co
   a.units = static_cast<int>(units);
   a.div_tiles = make_fastdiv(static_cast<uint32_t>(a.tiles_per_row));
   a.div_rows = make_fastdiv(static_cast<uint32_t>(g.GR));
-  a.stages = 2;
-  const size_t smem = static_cast<size_t>(round_up(static_cast<int64_t>(g.b) * tile * g.C, 128)) * 2;
+  // One stage per CTA, several CTAs per SM: the consumers release the stage
+  // right after summing it, so the next unit's load overlaps the long draw
+  // phase anyway, and the smaller footprint doubles the resident warps.
+  a.stages = 1;
+  const size_t smem = static_cast<size_t>(round_up(static_cast<int64_t>(g.b) * tile * g.C, 128));
   const auto key = std::make_pair(reinterpret_cast<const void*>(k), smem);
   int per_sm = 0;
   auto it = ctx->occupancy.find(key);

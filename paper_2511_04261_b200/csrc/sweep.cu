@@ -76,7 +76,7 @@ __device__ __forceinline__ void sweep_quantize(const SweepLevels& L, int k, int 
 }
 
 template <int C, int NLEV>
-__global__ void __launch_bounds__(kStatsThreads, 2)
+__global__ void __launch_bounds__(kStatsThreads, 4)
     k_sweep_stats(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ StatsArgs a,
                   const __grid_constant__ SweepLevels L) {
   constexpr int BMAX = 4 << (NLEV - 1);
@@ -226,40 +226,53 @@ __global__ void __launch_bounds__(kStatsThreads, 2)
     named_bar_sync(1, kConsumers);
     // Draws: every statistic of every active level, dealt round-robin to the
     // 128 consumers; within a level, consecutive threads take consecutive
-    // cells of one plane row (coalesced byte stores into every eps run).
+    // cells of one plane row (coalesced byte stores into every eps run). Each
+    // thread takes U statistics per pass and computes their keyed bits first:
+    // U independent mix64 chains the scheduler interleaves.
+    constexpr int U = 4;
 #pragma unroll 1
     for (int lv = 0; lv < NLEV; ++lv) {
       if (!((L.active >> lv) & 1u)) continue;
-      const int side = 4 << lv;
-      const int rows = BMAX / side, cols = TILE / side;
-      const int count = rows * C * cols;
-      const int r0 = p.r * rows, c0 = p.px0 / side;
+      const int lgc = 7 - lv;  // log2(cells per tile row) = log2(512 / (4 << lv))
+      const int rows = Q >> lv;
+      const int count = (rows * C) << lgc;
+      const int r0 = p.r * rows, c0 = p.px0 >> (2 + lv);
       const int GRk = L.GR[lv], GCk = L.GC[lv];
       const int64_t Gk = L.G[lv];
 #pragma unroll 1
-      for (int i = t; i < count; i += kConsumers) {
-        const int c = i % cols;
-        const int rest = i / cols;
-        const int ch = rest % C, q = rest / C;
-        const int rk = r0 + q, ck = c0 + c;
-        if (rk >= GRk || ck >= GCk) continue;
-        const uint32_t sum = lv == 0 ? t4[q][c][ch]
-                             : lv == 1 ? t8[NLEV > 1 ? q : 0][c][ch]
-                             : lv == 2 ? t16[NLEV > 2 ? q : 0][c][ch]
-                                       : t32[0][c][ch];
-        const int64_t plane = static_cast<int64_t>(f) * C + ch;
-        uint64_t bits = 0;
-        if (keyed) {
-          bits = key_sub(key_cell(a.noise.seed(plane), rk, ck), 0, 0);  // key (r, c, 0, 0)
-        } else if (a.noise.kind == DPPX_NOISE_PHILOX) {
-          bits = philox_call(a.noise.seed(0), a.noise.frame_base + f, ch, rk, ck, 0, 0);
+      for (int i0 = t; i0 < count; i0 += U * kConsumers) {
+        uint64_t bits[U];
+        uint32_t sum[U];
+        int64_t off[U];
+        bool ok[U];
+#pragma unroll
+        for (int v = 0; v < U; ++v) {
+          const int i = min(i0 + v * kConsumers, count - 1);
+          const int c = i & ((1 << lgc) - 1);
+          const int rest = i >> lgc;
+          const int ch = rest % C, q = rest / C;
+          const int rk = r0 + q, ck = c0 + c;
+          ok[v] = i0 + v * kConsumers < count && rk < GRk && ck < GCk;
+          sum[v] = lv == 0 ? t4[q][c][ch]
+                   : lv == 1 ? t8[NLEV > 1 ? q : 0][c][ch]
+                   : lv == 2 ? t16[NLEV > 2 ? q : 0][c][ch]
+                             : t32[0][c][ch];
+          const int64_t plane = static_cast<int64_t>(f) * C + ch;
+          bits[v] = keyed ? key_sub(key_cell(a.noise.seed(plane), rk, ck), 0, 0) : 0ull;  // key (r, c, 0, 0)
+          off[v] = plane * Gk + static_cast<int64_t>(rk) * GCk + ck;
+          if (a.noise.kind == DPPX_NOISE_PHILOX && ok[v])
+            bits[v] = philox_call(a.noise.seed(0), a.noise.frame_base + f, ch, rk, ck, 0, 0);
         }
-        const int64_t off = plane * Gk + static_cast<int64_t>(rk) * GCk + ck;
-        if (L.ne == 3) {
-          sweep_quantize<3>(L, lv, 0, sum, bits, a.noise.kind, exact_only, off);
-        } else {
+#pragma unroll
+        for (int v = 0; v < U; ++v) {
+          if (!ok[v]) continue;
+          if (L.ne == 3) {
+            sweep_quantize<3>(L, lv, 0, sum[v], bits[v], a.noise.kind, exact_only, off[v]);
+          } else {
 #pragma unroll 1
-          for (int j = 0; j < L.ne; ++j) sweep_quantize<1>(L, lv, j, sum, bits, a.noise.kind, exact_only, off);
+            for (int j = 0; j < L.ne; ++j)
+              sweep_quantize<1>(L, lv, j, sum[v], bits[v], a.noise.kind, exact_only, off[v]);
+          }
         }
       }
     }
