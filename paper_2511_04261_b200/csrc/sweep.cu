@@ -36,13 +36,26 @@ struct SweepLevels {
   uint8_t* means[kSweepMaxLevels][kSweepMaxEps];  // run (k, j): F*C planes of G[k] bytes
 };
 
+// A statistic whose f32 estimate was ambiguous: evaluated with the exact f64
+// arithmetic after the unit's draw pass, by all consumers together (in line,
+// ~1 in 4 warps would diverge into the f64 path on every pass at b = 4,
+// eps = 0.1, where sigma = 2550 widens the margin).
+struct ExactJob {
+  uint64_t bits;
+  uint8_t* dst;
+  uint32_t sum;
+  uint16_t lv, j;
+};
+constexpr int kSweepQueue = 256;
+
 // Per-eps quantization of one statistic whose noise magnitude is shared:
 // bits -> (sign, L = -ln(1 - 2|u|) in f32), then q_j for every sigma_j with
 // the exact reference arithmetic when the f32 estimate is ambiguous. Runs
 // j0 .. j0 + NE - 1 of level k.
 template <int NE>
 __device__ __forceinline__ void sweep_quantize(const SweepLevels& L, int k, int j0, uint32_t sum,
-                                               uint64_t bits, int kind, bool exact_only, int64_t off) {
+                                               uint64_t bits, int kind, bool exact_only, int64_t off,
+                                               ExactJob* queue, int* qn) {
   const double area = L.area[k];
   const float inv_area = 1.0f / static_cast<float>(area);
   if (kind == DPPX_NOISE_NONE) {
@@ -70,13 +83,21 @@ __device__ __forceinline__ void sweep_quantize(const SweepLevels& L, int k, int 
       if (!(fabsf(t - jr) <= L.margin[k][j0 + j] && jr >= 1.0f && jr <= 255.0f))
         q = static_cast<uint32_t>(min(max(__float2int_rd(t), 0), 255));
     }
-    if (q == 0xFFFFFFFFu) q = exact_quantize(sum, area, kind, bits, L.sigma[k][j0 + j], 0.0);
+    if (q == 0xFFFFFFFFu) {
+      const int slot = atomicAdd(qn, 1);
+      if (slot < kSweepQueue) {
+        queue[slot] = ExactJob{bits, L.means[k][j0 + j] + off, sum, static_cast<uint16_t>(k),
+                               static_cast<uint16_t>(j0 + j)};
+        continue;
+      }
+      q = exact_quantize(sum, area, kind, bits, L.sigma[k][j0 + j], 0.0);  // queue full
+    }
     L.means[k][j0 + j][off] = static_cast<uint8_t>(q);
   }
 }
 
 template <int C, int NLEV>
-__global__ void __launch_bounds__(kStatsThreads, 4)
+__global__ void __launch_bounds__(kStatsThreads, 3)
     k_sweep_stats(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ StatsArgs a,
                   const __grid_constant__ SweepLevels L) {
   constexpr int BMAX = 4 << (NLEV - 1);
@@ -95,6 +116,8 @@ __global__ void __launch_bounds__(kStatsThreads, 4)
   __shared__ uint16_t t8[NLEV > 1 ? Q / 2 : 1][kConsumers / 2][C];
   __shared__ uint16_t t16[NLEV > 2 ? Q / 4 : 1][kConsumers / 4][C];
   __shared__ uint32_t t32[NLEV > 3 ? 1 : 1][kConsumers / 8][C];
+  __shared__ ExactJob queue[kSweepQueue];
+  __shared__ int qn;
 
   const int S = a.stages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -137,6 +160,8 @@ __global__ void __launch_bounds__(kStatsThreads, 4)
   const BatchGeom& g = a.g;  // geometry of the BMAX grid (bands, tiles, padding)
   const bool keyed = a.noise.kind == DPPX_NOISE_KEYED;
   const bool exact_only = a.exact_noise != 0;
+  if (t == 0) qn = 0;
+  named_bar_sync(1, kConsumers);
   for (int k = 0;; ++k) {
     const int s = k % S;
     mbar_wait(&id_bar[s], (k / S) & 1);
@@ -267,16 +292,25 @@ __global__ void __launch_bounds__(kStatsThreads, 4)
         for (int v = 0; v < U; ++v) {
           if (!ok[v]) continue;
           if (L.ne == 3) {
-            sweep_quantize<3>(L, lv, 0, sum[v], bits[v], a.noise.kind, exact_only, off[v]);
+            sweep_quantize<3>(L, lv, 0, sum[v], bits[v], a.noise.kind, exact_only, off[v], queue, &qn);
           } else {
 #pragma unroll 1
             for (int j = 0; j < L.ne; ++j)
-              sweep_quantize<1>(L, lv, j, sum[v], bits[v], a.noise.kind, exact_only, off[v]);
+              sweep_quantize<1>(L, lv, j, sum[v], bits[v], a.noise.kind, exact_only, off[v], queue, &qn);
           }
         }
       }
     }
-    named_bar_sync(1, kConsumers);  // tables are rewritten by the next unit
+    named_bar_sync(1, kConsumers);
+    // the unit's ambiguous statistics, exact f64 reference arithmetic, compacted
+    const int nq = min(qn, kSweepQueue);
+    for (int i = t; i < nq; i += kConsumers) {
+      const ExactJob& e = queue[i];
+      *e.dst = static_cast<uint8_t>(exact_quantize(e.sum, L.area[e.lv], a.noise.kind, e.bits,
+                                                   L.sigma[e.lv][e.j], 0.0));
+    }
+    named_bar_sync(1, kConsumers);  // tables and queue are rewritten by the next unit
+    if (t == 0) qn = 0;
   }
 }
 
