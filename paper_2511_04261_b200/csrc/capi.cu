@@ -162,12 +162,46 @@ struct dppx_ctx {
   uint8_t* piece[2] = {nullptr, nullptr};  // h2d_frames pieces
   size_t piece_n[2] = {0, 0};
   cudaEvent_t piece_ev[2] = {};
+  // single-frame host calls replayed as CUDA graphs (host_single_graph)
+  struct FrameGraph;
+  std::vector<FrameGraph*> graphs;
+  uint64_t* gseeds_pinned = nullptr;  // mixed plane seeds of the next replay
+  DevBuf gseeds;
+  uint8_t* gstats_pinned = nullptr;   // statistics / lengths land here, then the caller's buffers
+  size_t gstats_pinned_n = 0;
   // stats
   bool timing = false;
   std::vector<PendingTiming> pending;
   std::vector<cudaEvent_t> event_pool;
   dppx_kernel_stats kstats{};
   std::map<std::pair<const void*, size_t>, int> occupancy;  // (TMA kernel, smem) -> CTAs/SM
+};
+
+// A single-frame host call captured once per (operation, geometry, privacy
+// parameters, noise kind, band count) and replayed: H2D row bands, K0, K1 row
+// bands and D2H row bands as one graph launch. Per replay only the caller's
+// host pointers (memcpy node parameters) and the mixed plane seeds (a pinned
+// buffer the graph copies from) change.
+struct dppx_ctx::FrameGraph {
+  int op, M, N, C, b, n, kind, exact, nb, want_out;
+  double sigma, sigma_sub;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  struct Copy {
+    cudaGraphNode_t node;
+    cudaMemcpy3DParms p;
+    int which;        // 0: image source, 1: mask source, 2: image destination
+    int64_t offset;   // bytes from the caller's base pointer
+  };
+  std::vector<Copy> copies;
+  const void* cur[3] = {nullptr, nullptr, nullptr};
+  uint64_t launches[DPPX_K_COUNT] = {};
+  uint64_t h2d = 0, d2h = 0;
+  uint64_t last_use = 0;
+  ~FrameGraph() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+  }
 };
 
 namespace {
@@ -617,6 +651,8 @@ struct PixOpts {
   int row_begin = 0;             // grid rows [row_begin, row_begin + row_count) only
   int row_count = -1;            // -1: all rows
   bool classify = true;          // adaptive: run K0 (false: a previous band already did)
+  const uint64_t* seeds_dev = nullptr;  // KEYED: mixed plane seeds already in device memory
+                                        // (graph replays: nothing baked into kernel params)
 };
 
 // Device-pointer core of both pixelize entry points.
@@ -665,9 +701,16 @@ int pixelize_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img, c
   a.row_count = o.row_count < 0 ? g.GR : o.row_count;
   if (a.row_begin < 0 || a.row_count < 0 || a.row_begin + a.row_count > g.GR)
     return set_err(ctx, DPPX_ERR_INVALID, "row band out of range");
-  if (int rc = prepare_noise(ctx, nz, g.F * g.C, dev_injected, g, pp, &a.noise, ctx->stream,
-                             dev_seeds, pinned, pinned_n, guard, record_guard))
+  if (o.seeds_dev && nz && nz->kind == DPPX_NOISE_KEYED) {
+    if (!(pp->sigma > 0.0) || (g.n > 1 && !(pp->sigma_sub > 0.0)))
+      return set_err(ctx, DPPX_ERR_INVALID, "laplace_at: sigma must be > 0");
+    a.noise = NoiseArgs{};
+    a.noise.kind = DPPX_NOISE_KEYED;
+    a.noise.mixed_seeds = o.seeds_dev;
+  } else if (int rc = prepare_noise(ctx, nz, g.F * g.C, dev_injected, g, pp, &a.noise, ctx->stream,
+                                    dev_seeds, pinned, pinned_n, guard, record_guard)) {
     return rc;
+  }
   const char* fused_env = std::getenv("DPPX_VAR_FUSED");  // A/B knob: "0" = 2-pass path
   if (by_variance && !partial && !(fused_env && fused_env[0] == '0')) {
     // Fused: K1 classifies each cell by its own variance while summing (one
@@ -1088,6 +1131,249 @@ int host_pipeline_bands(dppx_ctx* ctx, bool adaptive, const dppx_frames_desc* d,
   return DPPX_OK;
 }
 
+// Single-frame host call as a replayed CUDA graph (see dppx_ctx::FrameGraph).
+// Preconditions (host_pipeline checks): one frame, pinned dense image / mask /
+// output buffers with N*C % 16 == 0 (the device layout), KEYED or no noise.
+int host_single_graph(dppx_ctx* ctx, bool adaptive, const dppx_frames_desc* d, const BatchGeom& g,
+                      const uint8_t* img, const uint8_t* mask, const dppx_privacy_params* pp,
+                      const dppx_noise* nz, uint8_t* stats, int64_t sstride, uint32_t* lens,
+                      uint8_t* out) {
+  const int C = g.C, M = g.M, N = g.N, b = g.b;
+  const int64_t row = static_cast<int64_t>(N) * C;
+  const int64_t dfs = row * M, dmfs = static_cast<int64_t>(N) * M;
+  const size_t G = static_cast<size_t>(g.G);
+  const size_t cap = adaptive ? dppx_adaptive_payload_capacity(M, N, b, g.n) : G;
+  const int64_t dstride = adaptive ? round_up(static_cast<int64_t>(cap), 16) : static_cast<int64_t>(G);
+  const int kind = nz ? nz->kind : DPPX_NOISE_NONE;
+  // Row bands: the H2D of band i+1, K1 of band i and D2H of band i-1 overlap.
+  int nb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(4, dfs >> 18)));
+  if (const char* env = std::getenv("DPPX_GRAPH_BANDS")) nb = std::max(1, std::atoi(env));
+  nb = std::max(1, std::min({nb, g.GR / 2 > 0 ? g.GR / 2 : 1, dppx_ctx::kMaxBands}));
+  dppx_ctx::FrameGraph* fgp = nullptr;
+  for (auto* c : ctx->graphs)
+    if (c->op == (adaptive ? 1 : 0) && c->M == M && c->N == N && c->C == C && c->b == b && c->n == g.n &&
+        c->kind == kind && c->exact == (ctx->exact_noise ? 1 : 0) && c->nb == nb &&
+        c->want_out == (out ? 1 : 0) && c->sigma == pp->sigma && c->sigma_sub == pp->sigma_sub)
+      fgp = c;
+  cudaStream_t comp = ctx->stream;
+  if (!fgp) {
+    // ---- capture ----
+    if (ensure(ctx, ctx->img[0], static_cast<size_t>(dfs))) return DPPX_ERR_OOM;
+    if (out && ensure(ctx, ctx->out[0], static_cast<size_t>(dfs))) return DPPX_ERR_OOM;
+    if (adaptive && ensure(ctx, ctx->mask[0], static_cast<size_t>(dmfs))) return DPPX_ERR_OOM;
+    if (ensure(ctx, ctx->stats[0], static_cast<size_t>(dstride) * C)) return DPPX_ERR_OOM;
+    if (ensure(ctx, ctx->lens[0], sizeof(uint32_t) * C)) return DPPX_ERR_OOM;
+    if (ensure(ctx, ctx->gseeds, sizeof(uint64_t) * C)) return DPPX_ERR_OOM;
+    if (adaptive)
+      if (int rc = ensure_scratch(ctx, g, 1)) return rc;
+    if (int rc = ensure(ctx, ctx->work, 16, /*zero=*/true)) return rc;
+    if (!ctx->gseeds_pinned)
+      CUDA_TRY(ctx, cudaHostAlloc(reinterpret_cast<void**>(&ctx->gseeds_pinned), 8 * 4, cudaHostAllocDefault));
+    const size_t gst = static_cast<size_t>(dstride) * C + 16;
+    if (ctx->gstats_pinned_n < gst) {
+      if (ctx->gstats_pinned) CUDA_TRY(ctx, cudaFreeHost(ctx->gstats_pinned));
+      ctx->gstats_pinned = nullptr;
+      ctx->gstats_pinned_n = 0;
+      CUDA_TRY(ctx, cudaHostAlloc(reinterpret_cast<void**>(&ctx->gstats_pinned), gst, cudaHostAllocDefault));
+      ctx->gstats_pinned_n = gst;
+    }
+    // A graph owns device buffer addresses: drop the cache when it is full.
+    if (ctx->graphs.size() >= 8) {
+      auto old = std::min_element(ctx->graphs.begin(), ctx->graphs.end(),
+                                  [](auto* x, auto* y) { return x->last_use < y->last_use; });
+      delete *old;
+      ctx->graphs.erase(old);
+    }
+    CUDA_TRY(ctx, cudaStreamSynchronize(comp));
+    const bool timing = ctx->timing;
+    const dppx_kernel_stats saved = ctx->kstats;
+    ctx->timing = false;
+    ctx->kstats = dppx_kernel_stats{};
+    uint8_t* dimg = static_cast<uint8_t*>(ctx->img[0].p);
+    uint8_t* dout = static_cast<uint8_t*>(ctx->out[0].p);
+    uint8_t* dmask = static_cast<uint8_t*>(ctx->mask[0].p);
+    uint8_t* dstats = static_cast<uint8_t*>(ctx->stats[0].p);
+    uint32_t* dlens = static_cast<uint32_t*>(ctx->lens[0].p);
+    cudaEvent_t fork = get_event(ctx), join_in = get_event(ctx), join_out = get_event(ctx);
+    int rc = DPPX_OK;
+    auto fail = [&](int code) {
+      cudaGraph_t junk = nullptr;
+      cudaStreamEndCapture(comp, &junk);
+      if (junk) cudaGraphDestroy(junk);
+      cudaGetLastError();
+      ctx->timing = timing;
+      ctx->kstats = saved;
+      return code;
+    };
+    CUDA_TRY(ctx, cudaStreamBeginCapture(comp, cudaStreamCaptureModeRelaxed));
+    uint64_t h2d = 0, d2h = 0;
+    if (cudaEventRecord(fork, comp) != cudaSuccess || cudaStreamWaitEvent(ctx->s_in, fork, 0) != cudaSuccess ||
+        cudaStreamWaitEvent(ctx->s_out, fork, 0) != cudaSuccess)
+      return fail(set_err(ctx, DPPX_ERR_CUDA, "graph capture: fork failed"));
+    if (kind == DPPX_NOISE_KEYED &&
+        cudaMemcpyAsync(ctx->gseeds.p, ctx->gseeds_pinned, sizeof(uint64_t) * C, cudaMemcpyHostToDevice,
+                        ctx->s_in) != cudaSuccess)
+      return fail(set_err(ctx, DPPX_ERR_CUDA, "graph capture: seeds copy"));
+    int sizes[dppx_ctx::kMaxBands];
+    {
+      int left = g.GR;
+      for (int i = 0; i < nb; ++i) {
+        sizes[i] = left / (nb - i);
+        left -= sizes[i];
+      }
+    }
+    dppx_frames_desc dd = *d;
+    dd.pitch = row;
+    dd.frame_stride = dfs;
+    dd.mask_pitch = N;
+    dd.mask_frame_stride = dmfs;
+    dd.out_pitch = row;
+    dd.out_frame_stride = dfs;
+    dppx_noise gn{};
+    if (nz) gn = *nz;
+    int r0 = 0;
+    for (int i = 0; i < nb && rc == DPPX_OK; ++i) {
+      const int r1 = r0 + sizes[i];
+      const int y0 = r0 * b, y1 = std::min(r1 * b, M);
+      if (cudaMemcpyAsync(dimg + y0 * row, img + y0 * row, static_cast<size_t>(row) * (y1 - y0),
+                          cudaMemcpyHostToDevice, ctx->s_in) != cudaSuccess)
+        return fail(set_err(ctx, DPPX_ERR_CUDA, "graph capture: image copy"));
+      h2d += static_cast<uint64_t>(row) * (y1 - y0);
+      if (i == 0 && adaptive) {
+        if (cudaMemcpyAsync(dmask, mask, static_cast<size_t>(dmfs), cudaMemcpyHostToDevice, ctx->s_in) != cudaSuccess)
+          return fail(set_err(ctx, DPPX_ERR_CUDA, "graph capture: mask copy"));
+        h2d += static_cast<uint64_t>(dmfs);
+      }
+      if (cudaEventRecord(ctx->band_in[i], ctx->s_in) != cudaSuccess ||
+          cudaStreamWaitEvent(comp, ctx->band_in[i], 0) != cudaSuccess)
+        return fail(set_err(ctx, DPPX_ERR_CUDA, "graph capture: band order"));
+      PixOpts po;
+      po.row_begin = r0;
+      po.row_count = r1 - r0;
+      po.classify = i == 0;
+      po.seeds_dev = static_cast<const uint64_t*>(ctx->gseeds.p);
+      rc = pixelize_dev(ctx, &dd, dimg, dmask, pp, nz ? &gn : nullptr, nullptr, dstats, dstride,
+                        adaptive ? dlens : nullptr, out ? dout : nullptr, adaptive, ctx->sd[0],
+                        ctx->sd_pinned[0], ctx->sd_pinned_n[0], nullptr, false, po);
+      if (rc) return fail(rc);
+      if (out) {
+        if (cudaEventRecord(ctx->band_comp[i], comp) != cudaSuccess ||
+            cudaStreamWaitEvent(ctx->s_out, ctx->band_comp[i], 0) != cudaSuccess ||
+            cudaMemcpyAsync(out + y0 * row, dout + y0 * row, static_cast<size_t>(row) * (y1 - y0),
+                            cudaMemcpyDeviceToHost, ctx->s_out) != cudaSuccess)
+          return fail(set_err(ctx, DPPX_ERR_CUDA, "graph capture: output copy"));
+        d2h += static_cast<uint64_t>(row) * (y1 - y0);
+      }
+      r0 = r1;
+    }
+    // statistics (+ lengths) into the ctx's pinned staging after the last band
+    if (cudaMemcpyAsync(ctx->gstats_pinned, dstats, static_cast<size_t>(dstride) * C, cudaMemcpyDeviceToHost,
+                        comp) != cudaSuccess ||
+        (adaptive && cudaMemcpyAsync(ctx->gstats_pinned + static_cast<size_t>(dstride) * C, dlens,
+                                     sizeof(uint32_t) * C, cudaMemcpyDeviceToHost, comp) != cudaSuccess))
+      return fail(set_err(ctx, DPPX_ERR_CUDA, "graph capture: statistics copy"));
+    d2h += static_cast<uint64_t>(adaptive ? cap : G) * C + (adaptive ? 4 * C : 0);
+    if (cudaEventRecord(join_in, ctx->s_in) != cudaSuccess || cudaEventRecord(join_out, ctx->s_out) != cudaSuccess ||
+        cudaStreamWaitEvent(comp, join_in, 0) != cudaSuccess || cudaStreamWaitEvent(comp, join_out, 0) != cudaSuccess)
+      return fail(set_err(ctx, DPPX_ERR_CUDA, "graph capture: join failed"));
+    cudaGraph_t graph = nullptr;
+    CUDA_TRY(ctx, cudaStreamEndCapture(comp, &graph));
+    ctx->event_pool.push_back(fork);
+    ctx->event_pool.push_back(join_in);
+    ctx->event_pool.push_back(join_out);
+    auto* ng = new dppx_ctx::FrameGraph();
+    ng->op = adaptive ? 1 : 0;
+    ng->M = M;
+    ng->N = N;
+    ng->C = C;
+    ng->b = b;
+    ng->n = g.n;
+    ng->kind = kind;
+    ng->exact = ctx->exact_noise ? 1 : 0;
+    ng->nb = nb;
+    ng->want_out = out ? 1 : 0;
+    ng->sigma = pp->sigma;
+    ng->sigma_sub = pp->sigma_sub;
+    ng->graph = graph;
+    for (int k = 0; k < DPPX_K_COUNT; ++k) ng->launches[k] = ctx->kstats.launches[k];
+    ng->h2d = h2d;
+    ng->d2h = d2h;
+    ctx->timing = timing;
+    ctx->kstats = saved;
+    // memcpy nodes that touch the caller's buffers (re-pointed per replay)
+    size_t nn = 0;
+    CUDA_TRY(ctx, cudaGraphGetNodes(graph, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    CUDA_TRY(ctx, cudaGraphGetNodes(graph, nodes.data(), &nn));
+    auto inside = [](const void* p, const void* base, int64_t bytes) {
+      return base && p >= base && static_cast<const uint8_t*>(p) < static_cast<const uint8_t*>(base) + bytes;
+    };
+    for (cudaGraphNode_t node : nodes) {
+      cudaGraphNodeType ty;
+      CUDA_TRY(ctx, cudaGraphNodeGetType(node, &ty));
+      if (ty != cudaGraphNodeTypeMemcpy) continue;
+      dppx_ctx::FrameGraph::Copy c{};
+      c.node = node;
+      CUDA_TRY(ctx, cudaGraphMemcpyNodeGetParams(node, &c.p));
+      const void* src = c.p.srcPtr.ptr;
+      const void* dst = c.p.dstPtr.ptr;
+      if (inside(src, img, dfs)) {
+        c.which = 0;
+        c.offset = static_cast<const uint8_t*>(src) - img;
+      } else if (adaptive && inside(src, mask, dmfs)) {
+        c.which = 1;
+        c.offset = static_cast<const uint8_t*>(src) - mask;
+      } else if (out && inside(dst, out, dfs)) {
+        c.which = 2;
+        c.offset = static_cast<const uint8_t*>(dst) - out;
+      } else {
+        continue;
+      }
+      ng->copies.push_back(c);
+    }
+    const cudaError_t ie = cudaGraphInstantiate(&ng->exec, graph, 0);
+    if (ie != cudaSuccess) {
+      delete ng;
+      return set_err(ctx, DPPX_ERR_CUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(ie));
+    }
+    ng->cur[0] = img;
+    ng->cur[1] = mask;
+    ng->cur[2] = out;
+    ctx->graphs.push_back(ng);
+    fgp = ng;
+  }
+  // ---- replay ----
+  static uint64_t tick = 0;
+  fgp->last_use = ++tick;
+  const void* want[3] = {img, mask, out};
+  for (auto& c : fgp->copies) {
+    if (fgp->cur[c.which] == want[c.which]) continue;
+    cudaMemcpy3DParms p = c.p;
+    if (c.which == 2)
+      p.dstPtr.ptr = static_cast<uint8_t*>(const_cast<void*>(want[2])) + c.offset;
+    else
+      p.srcPtr.ptr = const_cast<uint8_t*>(static_cast<const uint8_t*>(want[c.which])) + c.offset;
+    CUDA_TRY(ctx, cudaGraphExecMemcpyNodeSetParams(fgp->exec, c.node, &p));
+  }
+  for (int k = 0; k < 3; ++k) fgp->cur[k] = want[k];
+  if (kind == DPPX_NOISE_KEYED)
+    for (int c = 0; c < C; ++c) ctx->gseeds_pinned[c] = mix64_h(nz->plane_seeds[c]);
+  CUDA_TRY(ctx, cudaGraphLaunch(fgp->exec, comp));
+  CUDA_TRY(ctx, cudaStreamSynchronize(comp));
+  for (int k = 0; k < DPPX_K_COUNT; ++k) ctx->kstats.launches[k] += fgp->launches[k];
+  ctx->kstats.h2d_bytes += fgp->h2d;
+  ctx->kstats.d2h_bytes += fgp->d2h;
+  const uint8_t* st = ctx->gstats_pinned;
+  const uint32_t* ln = reinterpret_cast<const uint32_t*>(st + static_cast<size_t>(dstride) * C);
+  for (int c = 0; c < C; ++c) {
+    const size_t w = adaptive ? std::min<size_t>(ln[c], cap) : G;
+    std::memcpy(stats + static_cast<int64_t>(c) * (adaptive ? sstride : static_cast<int64_t>(G)),
+                st + static_cast<int64_t>(c) * dstride, w);
+    if (adaptive && lens) lens[c] = ln[c];
+  }
+  return DPPX_OK;
+}
+
 int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uint8_t* img,
                   const uint8_t* mask, const dppx_privacy_params* pp, const dppx_noise* nz,
                   uint8_t* stats, int64_t sstride, uint32_t* lens, const uint32_t* in_lens,
@@ -1141,6 +1427,18 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
   if (ctx->mask_bits_mode < 0) {
     const char* env = std::getenv("DPPX_MASK_BITS");
     ctx->mask_bits_mode = env && env[0] == '0' ? 0 : 1;
+  }
+  {
+    // One small frame (below the row-band threshold): a replayed CUDA graph
+    // (DPPX_GRAPH=0 disables).
+    static const bool graphs_on = !(std::getenv("DPPX_GRAPH") && std::getenv("DPPX_GRAPH")[0] == '0');
+    const int64_t row = static_cast<int64_t>(N) * C;
+    const bool small = static_cast<int64_t>(M) * row < (4ll << 20);
+    if (graphs_on && F == 1 && small && (op == HostOp::Uniform || op == HostOp::Adaptive) &&
+        (!nz || nz->kind == DPPX_NOISE_NONE || nz->kind == DPPX_NOISE_KEYED) && row % 16 == 0 &&
+        d->pitch == row && (!out || d->out_pitch == row) && (op != HostOp::Adaptive || d->mask_pitch == N) &&
+        host_pinned(img) && (!out || host_pinned(out)) && (op != HostOp::Adaptive || host_pinned(mask)))
+      return host_single_graph(ctx, op == HostOp::Adaptive, d, g, img, mask, pp, nz, stats, sstride, lens, out);
   }
   {
     // One frame: pipeline row bands instead of frames (DPPX_BANDS=0 disables).
@@ -1635,6 +1933,10 @@ void dppx_ctx_destroy(dppx_ctx* ctx) {
     if (ctx->lens_pinned[s]) cudaFreeHost(ctx->lens_pinned[s]);
   }
   if (ctx->seeds_pinned) cudaFreeHost(ctx->seeds_pinned);
+  for (auto* fgp : ctx->graphs) delete fgp;
+  if (ctx->gseeds.p) cudaFree(ctx->gseeds.p);
+  if (ctx->gseeds_pinned) cudaFreeHost(ctx->gseeds_pinned);
+  if (ctx->gstats_pinned) cudaFreeHost(ctx->gstats_pinned);
   for (int i = 0; i < dppx_ctx::kMaxBands; ++i) {
     cudaEventDestroy(ctx->band_in[i]);
     cudaEventDestroy(ctx->band_comp[i]);
