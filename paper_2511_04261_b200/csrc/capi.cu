@@ -76,11 +76,18 @@ struct SweepLevels {  // sweep.cu
   float sigmaf[kSweepMaxLevels][kSweepMaxEps];
   float margin[kSweepMaxLevels][kSweepMaxEps];
   uint8_t* means[kSweepMaxLevels][kSweepMaxEps];
+  void* sums[kSweepMaxLevels];
+  int srows[kSweepMaxLevels], scols[kSweepMaxLevels];
+  int64_t item0[kSweepMaxLevels + 1];
+  int groups[kSweepMaxLevels];
+  FastDiv div_groups[kSweepMaxLevels], div_rows[kSweepMaxLevels];
+  int planes;
 };
-using SweepKernel = void (*)(const CUtensorMap, const StatsArgs, const SweepLevels);
-SweepKernel select_sweep_kernel(int C, int nlev);
-cudaError_t launch_sweep(SweepKernel k, const CUtensorMap& tin, const StatsArgs& a, const SweepLevels& L,
-                         int grid, size_t smem, cudaStream_t s);
+using SweepSumsKernel = void (*)(const CUtensorMap, const StatsArgs, const SweepLevels);
+SweepSumsKernel select_sweep_kernel(int C, int nlev);
+cudaError_t launch_sweep(SweepSumsKernel k, const CUtensorMap& tin, const StatsArgs& a, const SweepLevels& L,
+                         int grid, size_t smem, int draw_grid, cudaStream_t s);
+int sweep_draw_threads();
 }  // namespace dppx
 
 using namespace dppx;
@@ -135,6 +142,7 @@ struct dppx_ctx {
       dense_mask[2];  // dense (input) and dense_out never alias: chunk ci+2's H2D may run
                       // while chunk ci's D2H is still reading its output
   DevBuf var_flags, var_stage;  // fused variance classification staging
+  DevBuf sweep_sums[4];         // K1s level sums (one-read sweep)
   uint64_t* sd_pinned[2] = {nullptr, nullptr};
   size_t sd_pinned_n[2] = {0, 0};
   cudaEvent_t in_done[2] = {}, comp_done[2] = {}, out_done[2] = {};
@@ -1914,6 +1922,8 @@ void dppx_ctx_destroy(dppx_ctx* ctx) {
                     &ctx->met_a, &ctx->met_b, &ctx->met_out, &ctx->var_flags, &ctx->var_stage};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
+  for (DevBuf& b : ctx->sweep_sums)
+    if (b.p) cudaFree(b.p);
   for (int s = 0; s < 2; ++s) {
     DevBuf* sb[] = {&ctx->img[s], &ctx->mask[s], &ctx->out[s], &ctx->stats[s], &ctx->lens[s],
                     &ctx->inj[s], &ctx->sd[s], &ctx->dense[s], &ctx->dense_out[s], &ctx->dense_mask[s]};
@@ -2082,7 +2092,7 @@ int dppx_pixelize_uniform_sweep_dev(dppx_ctx* ctx, const dppx_frames_desc* d, co
     bmax = std::max(bmax, b);
   }
   const int nlev = bmax == 8 ? 2 : bmax == 16 ? 3 : bmax == 32 ? 4 : 0;
-  SweepKernel k = fused ? select_sweep_kernel(d->channels, nlev) : nullptr;
+  SweepSumsKernel k = fused ? select_sweep_kernel(d->channels, nlev) : nullptr;
   BatchGeom g;
   if (k && geometry(ctx, d->height, d->width, d->channels, d->frames, bmax, 1, &g, true) != DPPX_OK) {
     k = nullptr;  // the largest side's padding would exceed the image: per-run path
@@ -2111,6 +2121,8 @@ int dppx_pixelize_uniform_sweep_dev(dppx_ctx* ctx, const dppx_frames_desc* d, co
   L.nlev = nlev;
   L.ne = ne;
   L.active = active;
+  L.planes = g.F * g.C;
+  int64_t items = 0;
   for (int lv = 0; lv < nlev; ++lv) {
     dppx_geometry gg;
     dppx_grid_dims(d->height, d->width, 4 << lv, &gg);
@@ -2118,7 +2130,20 @@ int dppx_pixelize_uniform_sweep_dev(dppx_ctx* ctx, const dppx_frames_desc* d, co
     L.GC[lv] = gg.grid_cols;
     L.G[lv] = static_cast<int64_t>(gg.grid_rows) * gg.grid_cols;
     L.area[lv] = static_cast<double>(4 << lv) * (4 << lv);
+    // level sums over the largest side's padded extent
+    L.srows[lv] = g.GR * (bmax >> (2 + lv));
+    L.scols[lv] = g.GC * (bmax >> (2 + lv));
+    const size_t bytes = static_cast<size_t>(L.planes) * L.srows[lv] * L.scols[lv] * (lv == 3 ? 4 : 2);
+    if (int rc = ensure(ctx, ctx->sweep_sums[lv], bytes)) return rc;
+    L.sums[lv] = ctx->sweep_sums[lv].p;
+    L.groups[lv] = (L.GC[lv] + 3) / 4;
+    L.div_groups[lv] = make_fastdiv(static_cast<uint32_t>(L.groups[lv]));
+    L.div_rows[lv] = make_fastdiv(static_cast<uint32_t>(L.GR[lv]));
+    L.item0[lv] = items;
+    items += static_cast<int64_t>(L.planes) * L.GR[lv] * L.groups[lv];
   }
+  L.item0[nlev] = items;
+  if (items > 0x7FFFFFFFll) return set_err(ctx, DPPX_ERR_INVALID, "sweep batch too large for one launch");
   for (int i = 0; i < nb; ++i) {
     const int lv = b_list[i] == 4 ? 0 : b_list[i] == 8 ? 1 : b_list[i] == 16 ? 2 : 3;
     for (int j = 0; j < ne; ++j) {
@@ -2151,11 +2176,8 @@ int dppx_pixelize_uniform_sweep_dev(dppx_ctx* ctx, const dppx_frames_desc* d, co
   a.units = static_cast<int>(units);
   a.div_tiles = make_fastdiv(static_cast<uint32_t>(a.tiles_per_row));
   a.div_rows = make_fastdiv(static_cast<uint32_t>(g.GR));
-  // One stage per CTA, several CTAs per SM: the consumers release the stage
-  // right after summing it, so the next unit's load overlaps the long draw
-  // phase anyway, and the smaller footprint doubles the resident warps.
-  a.stages = 1;
-  const size_t smem = static_cast<size_t>(round_up(static_cast<int64_t>(g.b) * tile * g.C, 128));
+  a.stages = 2;  // K1s-sum is a streaming kernel: a 2-deep ring per CTA
+  const size_t smem = static_cast<size_t>(round_up(static_cast<int64_t>(g.b) * tile * g.C, 128)) * 2;
   const auto key = std::make_pair(reinterpret_cast<const void*>(k), smem);
   int per_sm = 0;
   auto it = ctx->occupancy.find(key);
@@ -2170,8 +2192,10 @@ int dppx_pixelize_uniform_sweep_dev(dppx_ctx* ctx, const dppx_frames_desc* d, co
   if (int rc = ensure(ctx, ctx->work, 16, /*zero=*/true)) return rc;
   a.work_counter = static_cast<int*>(ctx->work.p);
   PendingTiming pt;
+  const int draw_grid = static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>((items + sweep_draw_threads() - 1) / sweep_draw_threads(), 8ll * ctx->sms)));
   timing_begin(ctx, DPPX_K_SWEEP, &pt);
-  CUDA_TRY(ctx, launch_sweep(k, tin, a, L, grid, smem, ctx->stream));
+  CUDA_TRY(ctx, launch_sweep(k, tin, a, L, grid, smem, draw_grid, ctx->stream));
   timing_end(ctx, &pt);
   // The runs' images: broadcast_means of their statistics (write-only K2).
   if (out) {

@@ -9,13 +9,19 @@
 // LARGEST padded extent aggregate exactly (integer adds) to every larger
 // power-of-two grid side, and for one plane seed and one cell the keyed bits
 // -- hence u and -log1p(-2|u|) -- do not depend on eps (noise.cpp:86-117):
-// only sigma = 255 m / (b^2 eps) scales them. So one unit of work (frame,
-// BMAX-row band, 512-px column tile) is staged once by TMA, summed once, and
-// every level's cells draw their bits and Laplace magnitude once and quantize
-// once per eps, each with the reference's own f64 fallback for values near a
-// rounding boundary (fast_quantize / exact_quantize, dppx_device.cuh).
-// Statistics only: the reconstructed images of the runs are broadcast_means of
-// these statistics (K2, written by the host entry point).
+// only sigma = 255 m / (b^2 eps) scales them. Two kernels:
+//  * K1s-sum: streams each frame once (TMA-staged BMAX-row bands, 512-px
+//    tiles, dp4a strip sums), aggregates 2x2 per level in registers and writes
+//    every level's cell sums (u16 / u32, ~17 % of the frame's bytes);
+//  * K1s-draw: a flat, high-occupancy pass over the statistics. A thread takes
+//    4 consecutive cells of one plane row, computes their keyed bits and
+//    Laplace magnitude once, quantizes them for every eps and stores 4 bytes
+//    per run at once. Statistics whose f32 estimate sits within the proven
+//    error margin of a rounding boundary go to a per-warp queue that the warp
+//    drains 32 at a time with the reference's exact f64 arithmetic
+//    (exact_quantize), so the f64 path never diverges a warp.
+// Statistics only: the runs' images are broadcast_means of these statistics
+// (K2, issued by the host entry point).
 #include "tma_kernels.cuh"
 
 namespace dppx {
@@ -34,72 +40,25 @@ struct SweepLevels {
   float sigmaf[kSweepMaxLevels][kSweepMaxEps];
   float margin[kSweepMaxLevels][kSweepMaxEps];
   uint8_t* means[kSweepMaxLevels][kSweepMaxEps];  // run (k, j): F*C planes of G[k] bytes
+  // level sums written by K1s-sum: plane p, cell (r, c) of level k at
+  // sums[k] + (p * srows[k] + r) * scols[k] + c (u16; level 3: u32)
+  void* sums[kSweepMaxLevels];
+  int srows[kSweepMaxLevels], scols[kSweepMaxLevels];
+  // K1s-draw work items: 4 consecutive cells of one (plane, row) of level k
+  // (planes x GR[k] rows x groups[k]); items [item0[k], item0[k+1]) are level k's
+  int64_t item0[kSweepMaxLevels + 1];
+  int groups[kSweepMaxLevels];       // ceil(GC[k] / 4)
+  FastDiv div_groups[kSweepMaxLevels], div_rows[kSweepMaxLevels];  // by groups[k], by GR[k]
+  int planes;
 };
 
-// A statistic whose f32 estimate was ambiguous: evaluated with the exact f64
-// arithmetic after the unit's draw pass, by all consumers together (in line,
-// ~1 in 4 warps would diverge into the f64 path on every pass at b = 4,
-// eps = 0.1, where sigma = 2550 widens the margin).
-struct ExactJob {
-  uint64_t bits;
-  uint8_t* dst;
-  uint32_t sum;
-  uint16_t lv, j;
-};
-constexpr int kSweepQueue = 256;
-
-// Per-eps quantization of one statistic whose noise magnitude is shared:
-// bits -> (sign, L = -ln(1 - 2|u|) in f32), then q_j for every sigma_j with
-// the exact reference arithmetic when the f32 estimate is ambiguous. Runs
-// j0 .. j0 + NE - 1 of level k.
-template <int NE>
-__device__ __forceinline__ void sweep_quantize(const SweepLevels& L, int k, int j0, uint32_t sum,
-                                               uint64_t bits, int kind, bool exact_only, int64_t off,
-                                               ExactJob* queue, int* qn) {
-  const double area = L.area[k];
-  const float inv_area = 1.0f / static_cast<float>(area);
-  if (kind == DPPX_NOISE_NONE) {
-    // area = 16^k is a power of two: sum * 2^-m + 0.5 is exact in f32
-    const uint8_t q = static_cast<uint8_t>(floorf(static_cast<float>(sum) * inv_area + 0.5f));
-#pragma unroll
-    for (int j = 0; j < NE; ++j) L.means[k][j0 + j][off] = q;
-    return;
-  }
-  const uint64_t y = bits >> 11;
-  const bool neg = static_cast<int32_t>(bits >> 32) >= 0;
-  const uint64_t W = neg ? y : (1ull << 53) - y;
-  const uint32_t wb = __float_as_uint(fmaxf(__ull2float_rn(W), 1.0f));
-  const int e = static_cast<int>(wb >> 23) - 127;
-  const float lg_m = lg2_approx(__uint_as_float(0x3F800000u | (wb & 0x7FFFFFu)));
-  const float Lf = (static_cast<float>(52 - e) - lg_m) * 0.693147180559945f;
-  const float mean_f = static_cast<float>(sum) * inv_area + 0.5f;
-#pragma unroll
-  for (int j = 0; j < NE; ++j) {
-    uint32_t q = 0xFFFFFFFFu;
-    if (!exact_only) {
-      const float sf = L.sigmaf[k][j0 + j];
-      const float t = mean_f + (neg ? -sf * Lf : sf * Lf);
-      const float jr = rintf(t);
-      if (!(fabsf(t - jr) <= L.margin[k][j0 + j] && jr >= 1.0f && jr <= 255.0f))
-        q = static_cast<uint32_t>(min(max(__float2int_rd(t), 0), 255));
-    }
-    if (q == 0xFFFFFFFFu) {
-      const int slot = atomicAdd(qn, 1);
-      if (slot < kSweepQueue) {
-        queue[slot] = ExactJob{bits, L.means[k][j0 + j] + off, sum, static_cast<uint16_t>(k),
-                               static_cast<uint16_t>(j0 + j)};
-        continue;
-      }
-      q = exact_quantize(sum, area, kind, bits, L.sigma[k][j0 + j], 0.0);  // queue full
-    }
-    L.means[k][j0 + j][off] = static_cast<uint8_t>(q);
-  }
-}
-
+// ============================================================================
+// K1s-sum
+// ============================================================================
 template <int C, int NLEV>
 __global__ void __launch_bounds__(kStatsThreads, 3)
-    k_sweep_stats(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ StatsArgs a,
-                  const __grid_constant__ SweepLevels L) {
+    k_sweep_sums(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ StatsArgs a,
+                 const __grid_constant__ SweepLevels L) {
   constexpr int BMAX = 4 << (NLEV - 1);
   constexpr int TILE = kTilePx;        // 512 px: a multiple of every grid side
   constexpr int ROWB = TILE * C;
@@ -110,14 +69,6 @@ __global__ void __launch_bounds__(kStatsThreads, 3)
   __shared__ __align__(8) uint64_t id_bar[kMaxStages];
   __shared__ __align__(8) uint64_t done_bar[kMaxStages];
   __shared__ int stage_unit[kMaxStages];
-  // Level sums of the unit's cells, [level][cell row][cell col][channel]
-  // (4-px level: every strip; b = 8 << k: owner lanes). u16 holds up to 257 * 255.
-  __shared__ uint16_t t4[Q][kConsumers][C];
-  __shared__ uint16_t t8[NLEV > 1 ? Q / 2 : 1][kConsumers / 2][C];
-  __shared__ uint16_t t16[NLEV > 2 ? Q / 4 : 1][kConsumers / 4][C];
-  __shared__ uint32_t t32[NLEV > 3 ? 1 : 1][kConsumers / 8][C];
-  __shared__ ExactJob queue[kSweepQueue];
-  __shared__ int qn;
 
   const int S = a.stages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -132,7 +83,7 @@ __global__ void __launch_bounds__(kStatsThreads, 3)
   __syncthreads();
 
   if (warp == kConsumers / 32) {
-    // ---------------- producer: unit claims + TMA loads (no stores) ----------------
+    // ---------------- producer: unit claims + TMA loads ----------------
     if (lane == 0) {
       prefetch_tmap(&tm_in);
       for (int k = 0;; ++k) {
@@ -158,10 +109,6 @@ __global__ void __launch_bounds__(kStatsThreads, 3)
   // ---------------- consumers: one 4-px strip each ----------------
   const int t = threadIdx.x;
   const BatchGeom& g = a.g;  // geometry of the BMAX grid (bands, tiles, padding)
-  const bool keyed = a.noise.kind == DPPX_NOISE_KEYED;
-  const bool exact_only = a.exact_noise != 0;
-  if (t == 0) qn = 0;
-  named_bar_sync(1, kConsumers);
   for (int k = 0;; ++k) {
     const int s = k % S;
     mbar_wait(&id_bar[s], (k / S) & 1);
@@ -201,12 +148,20 @@ __global__ void __launch_bounds__(kStatsThreads, 3)
       for (int i = 0; i < 4; ++i) accumulate_row<C>(st + (4 * q + i) * ROWB + 4 * t * C, acc[q]);
     }
     mbar_arrive(&done_bar[s]);
-    // Larger grid sides: 2x2 aggregation per level (vertical in registers,
-    // horizontal across lanes) -- exact integers, b-independent reflection.
+    // Level sums: 2x2 aggregation per level (vertical in registers, horizontal
+    // across lanes) -- exact integers. Stores of a (plane, row) are contiguous
+    // across the owner lanes.
+    const int tile_cells = p.px0 / 4;  // first 4-px cell column of the tile
+    const int64_t P = static_cast<int64_t>(f) * C;
+    auto put16 = [&](int lv, int r, int c, int ch, uint32_t v) {
+      if (c < L.scols[lv])
+        static_cast<uint16_t*>(L.sums[lv])[((P + ch) * L.srows[lv] + r) * L.scols[lv] + c] =
+            static_cast<uint16_t>(v);
+    };
 #pragma unroll
     for (int q = 0; q < Q; ++q)
 #pragma unroll
-      for (int ch = 0; ch < C; ++ch) t4[q][t][ch] = static_cast<uint16_t>(acc[q][ch]);
+      for (int ch = 0; ch < C; ++ch) put16(0, p.r * Q + q, tile_cells + t, ch, acc[q][ch]);
     if constexpr (NLEV > 1) {
       uint32_t v8[Q / 2][C];
 #pragma unroll
@@ -220,7 +175,7 @@ __global__ void __launch_bounds__(kStatsThreads, 3)
 #pragma unroll
         for (int q = 0; q < Q / 2; ++q)
 #pragma unroll
-          for (int ch = 0; ch < C; ++ch) t8[q][t >> 1][ch] = static_cast<uint16_t>(v8[q][ch]);
+          for (int ch = 0; ch < C; ++ch) put16(1, p.r * (Q / 2) + q, tile_cells / 2 + (t >> 1), ch, v8[q][ch]);
       if constexpr (NLEV > 2) {
         uint32_t v16[Q / 4 > 0 ? Q / 4 : 1][C];
 #pragma unroll
@@ -234,7 +189,8 @@ __global__ void __launch_bounds__(kStatsThreads, 3)
 #pragma unroll
           for (int q = 0; q < Q / 4; ++q)
 #pragma unroll
-            for (int ch = 0; ch < C; ++ch) t16[q][t >> 2][ch] = static_cast<uint16_t>(v16[q][ch]);
+            for (int ch = 0; ch < C; ++ch)
+              put16(2, p.r * (Q / 4) + q, tile_cells / 4 + (t >> 2), ch, v16[q][ch]);
         if constexpr (NLEV > 3) {
           uint32_t v32[C];
 #pragma unroll
@@ -242,83 +198,182 @@ __global__ void __launch_bounds__(kStatsThreads, 3)
             v32[ch] = v16[0][ch] + v16[1][ch];
             v32[ch] += __shfl_xor_sync(0xFFFFFFFFu, v32[ch], 4);
           }
-          if ((t & 7) == 0)
+          const int c32 = tile_cells / 8 + (t >> 3);
+          if ((t & 7) == 0 && c32 < L.scols[3])
 #pragma unroll
-            for (int ch = 0; ch < C; ++ch) t32[0][t >> 3][ch] = v32[ch];
+            for (int ch = 0; ch < C; ++ch)
+              static_cast<uint32_t*>(L.sums[3])[((P + ch) * L.srows[3] + p.r) * L.scols[3] + c32] = v32[ch];
         }
       }
     }
-    named_bar_sync(1, kConsumers);
-    // Draws: every statistic of every active level, dealt round-robin to the
-    // 128 consumers; within a level, consecutive threads take consecutive
-    // cells of one plane row (coalesced byte stores into every eps run). Each
-    // thread takes U statistics per pass and computes their keyed bits first:
-    // U independent mix64 chains the scheduler interleaves.
-    constexpr int U = 4;
-#pragma unroll 1
-    for (int lv = 0; lv < NLEV; ++lv) {
-      if (!((L.active >> lv) & 1u)) continue;
-      const int lgc = 7 - lv;  // log2(cells per tile row) = log2(512 / (4 << lv))
-      const int rows = Q >> lv;
-      const int count = (rows * C) << lgc;
-      const int r0 = p.r * rows, c0 = p.px0 >> (2 + lv);
-      const int GRk = L.GR[lv], GCk = L.GC[lv];
-      const int64_t Gk = L.G[lv];
-#pragma unroll 1
-      for (int i0 = t; i0 < count; i0 += U * kConsumers) {
-        uint64_t bits[U];
-        uint32_t sum[U];
-        int64_t off[U];
-        bool ok[U];
-#pragma unroll
-        for (int v = 0; v < U; ++v) {
-          const int i = min(i0 + v * kConsumers, count - 1);
-          const int c = i & ((1 << lgc) - 1);
-          const int rest = i >> lgc;
-          const int ch = rest % C, q = rest / C;
-          const int rk = r0 + q, ck = c0 + c;
-          ok[v] = i0 + v * kConsumers < count && rk < GRk && ck < GCk;
-          sum[v] = lv == 0 ? t4[q][c][ch]
-                   : lv == 1 ? t8[NLEV > 1 ? q : 0][c][ch]
-                   : lv == 2 ? t16[NLEV > 2 ? q : 0][c][ch]
-                             : t32[0][c][ch];
-          const int64_t plane = static_cast<int64_t>(f) * C + ch;
-          bits[v] = keyed ? key_sub(key_cell(a.noise.seed(plane), rk, ck), 0, 0) : 0ull;  // key (r, c, 0, 0)
-          off[v] = plane * Gk + static_cast<int64_t>(rk) * GCk + ck;
-          if (a.noise.kind == DPPX_NOISE_PHILOX && ok[v])
-            bits[v] = philox_call(a.noise.seed(0), a.noise.frame_base + f, ch, rk, ck, 0, 0);
-        }
-#pragma unroll
-        for (int v = 0; v < U; ++v) {
-          if (!ok[v]) continue;
-          if (L.ne == 3) {
-            sweep_quantize<3>(L, lv, 0, sum[v], bits[v], a.noise.kind, exact_only, off[v], queue, &qn);
-          } else {
-#pragma unroll 1
-            for (int j = 0; j < L.ne; ++j)
-              sweep_quantize<1>(L, lv, j, sum[v], bits[v], a.noise.kind, exact_only, off[v], queue, &qn);
-          }
-        }
-      }
-    }
-    named_bar_sync(1, kConsumers);
-    // the unit's ambiguous statistics, exact f64 reference arithmetic, compacted
-    const int nq = min(qn, kSweepQueue);
-    for (int i = t; i < nq; i += kConsumers) {
-      const ExactJob& e = queue[i];
-      *e.dst = static_cast<uint8_t>(exact_quantize(e.sum, L.area[e.lv], a.noise.kind, e.bits,
-                                                   L.sigma[e.lv][e.j], 0.0));
-    }
-    named_bar_sync(1, kConsumers);  // tables and queue are rewritten by the next unit
-    if (t == 0) qn = 0;
   }
 }
 
-using SweepKernel = void (*)(const CUtensorMap, const StatsArgs, const SweepLevels);
+// ============================================================================
+// K1s-draw
+// ============================================================================
+constexpr int kDrawThreads = 256;
+constexpr int kDrawWarps = kDrawThreads / 32;
+constexpr int kDrawQueue = 64;  // per warp; drained 32 at a time
 
-SweepKernel select_sweep_kernel(int C, int nlev) {
+struct ExactJob {
+  uint64_t bits;
+  uint8_t* dst;
+  uint32_t sum;
+  uint16_t lv, j;
+};
+
+// f32 Laplace magnitude of 64 keyed bits (see fast_quantize, dppx_device.cuh,
+// for the error budget): L = -ln(1 - 2|u|), sign from the top bits.
+__device__ __forceinline__ float laplace_mag(uint64_t bits, bool& neg) {
+  const uint64_t y = bits >> 11;
+  neg = static_cast<int32_t>(bits >> 32) >= 0;
+  const uint64_t W = neg ? y : (1ull << 53) - y;
+  const uint32_t wb = __float_as_uint(fmaxf(__ull2float_rn(W), 1.0f));
+  const int e = static_cast<int>(wb >> 23) - 127;
+  const float lg_m = lg2_approx(__uint_as_float(0x3F800000u | (wb & 0x7FFFFFu)));
+  return (static_cast<float>(52 - e) - lg_m) * 0.693147180559945f;
+}
+
+template <int NE>
+__global__ void __launch_bounds__(kDrawThreads)
+    k_sweep_draw(const __grid_constant__ StatsArgs a, const __grid_constant__ SweepLevels L) {
+  __shared__ ExactJob queue[kDrawWarps][kDrawQueue];
+  __shared__ int qn[kDrawWarps];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) qn[w] = 0;
+  __syncwarp();
+  const int kind = a.noise.kind;
+  const bool exact_only = a.exact_noise != 0;
+  const int ne = NE > 0 ? NE : L.ne;
+  // Drain the top `cnt` queued statistics (one per lane) with the exact arithmetic.
+  auto drain = [&](int cnt) {
+    __syncwarp();
+    const int base = qn[w] - cnt;
+    if (lane < cnt) {
+      const ExactJob e = queue[w][base + lane];
+      *e.dst = static_cast<uint8_t>(exact_quantize(e.sum, L.area[e.lv], kind, e.bits, L.sigma[e.lv][e.j], 0.0));
+    }
+    __syncwarp();
+    if (lane == 0) qn[w] = base;
+    __syncwarp();
+  };
+  const int64_t total = L.item0[L.nlev];
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kDrawThreads;
+  // Every warp runs the same number of passes (the queue drains are warp-collective).
+  const int64_t passes = (total + stride - 1) / stride;
+  for (int64_t pass = 0; pass < passes; ++pass) {
+    const int64_t item = pass * stride + static_cast<int64_t>(blockIdx.x) * kDrawThreads + threadIdx.x;
+    bool any = item < total;
+    int lv = 0;
+    if (any) {
+#pragma unroll
+      for (int k = 1; k < kSweepMaxLevels; ++k)
+        if (k < L.nlev && item >= L.item0[k]) lv = k;
+      any = (L.active >> lv) & 1u;
+    }
+    uint32_t sum[4] = {0, 0, 0, 0};
+    uint64_t bits[4] = {0, 0, 0, 0};
+    int nvalid = 0;
+    int64_t off = 0;
+    if (any) {
+      const uint32_t rel = static_cast<uint32_t>(item - L.item0[lv]);
+      const uint32_t prow = L.div_groups[lv].div(rel);         // plane * rows + row
+      const int grp = static_cast<int>(rel - prow * static_cast<uint32_t>(L.groups[lv]));
+      const uint32_t plane = L.div_rows[lv].div(prow);
+      const int GRk = L.GR[lv], GCk = L.GC[lv];
+      const int r = static_cast<int>(prow - plane * static_cast<uint32_t>(GRk));
+      const int c0 = 4 * grp;
+      nvalid = max(0, min(4, GCk - c0));
+      const int f = static_cast<int>(plane / static_cast<uint32_t>(a.g.C));
+      const int ch = static_cast<int>(plane) - f * a.g.C;
+      const int64_t srow = (static_cast<int64_t>(plane) * L.srows[lv] + r) * L.scols[lv] + c0;
+      if (lv < 3) {
+        const uint16_t* s16 = static_cast<const uint16_t*>(L.sums[lv]) + srow;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) sum[v] = v < nvalid ? __ldg(s16 + v) : 0u;
+      } else {
+        const uint32_t* s32 = static_cast<const uint32_t*>(L.sums[3]) + srow;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) sum[v] = v < nvalid ? __ldg(s32 + v) : 0u;
+      }
+      if (kind == DPPX_NOISE_KEYED) {
+        const uint64_t seed = a.noise.seed(plane);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) bits[v] = key_sub(key_cell(seed, r, c0 + v), 0, 0);  // key (r, c, 0, 0)
+      } else if (kind == DPPX_NOISE_PHILOX) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          if (v < nvalid) bits[v] = philox_call(a.noise.seed(0), a.noise.frame_base + f, ch, r, c0 + v, 0, 0);
+      }
+      off = static_cast<int64_t>(plane) * L.G[lv] + static_cast<int64_t>(r) * GCk + c0;
+    }
+    // quantize every cell for every eps; 4 bytes per run at once when aligned
+    float Lf[4];
+    bool neg[4];
+    const float inv_area = any ? 1.0f / static_cast<float>(L.area[lv]) : 0.0f;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      neg[v] = false;
+      Lf[v] = kind == DPPX_NOISE_NONE ? 0.0f : laplace_mag(bits[v], neg[v]);
+    }
+    for (int j = 0; j < ne; ++j) {
+      uint32_t amb = 0;  // cells whose estimate is ambiguous
+      if (any && nvalid > 0) {
+        const float sf = L.sigmaf[lv][j], mg = L.margin[lv][j];
+        uint32_t word = 0;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          uint32_t q;
+          const float t = static_cast<float>(sum[v]) * inv_area + 0.5f +
+                          (kind == DPPX_NOISE_NONE ? 0.0f : (neg[v] ? -sf * Lf[v] : sf * Lf[v]));
+          if (kind == DPPX_NOISE_NONE) {
+            q = static_cast<uint32_t>(floorf(t));  // area = 16^k: exact in f32
+          } else {
+            const float jr = rintf(t);
+            if (exact_only || (fabsf(t - jr) <= mg && jr >= 1.0f && jr <= 255.0f)) amb |= 1u << v;
+            q = static_cast<uint32_t>(min(max(__float2int_rd(t), 0), 255));
+          }
+          word |= q << (8 * v);
+        }
+        uint8_t* dst = L.means[lv][j] + off;
+        if (nvalid == 4 && (reinterpret_cast<uintptr_t>(dst) & 3) == 0) {
+          *reinterpret_cast<uint32_t*>(dst) = word;
+        } else {
+          for (int v = 0; v < nvalid; ++v) dst[v] = static_cast<uint8_t>(word >> (8 * v));
+        }
+        amb &= (1u << nvalid) - 1u;
+      }
+      // queue the ambiguous ones (their stored byte is overwritten when drained)
+      while (true) {
+        const unsigned want = __ballot_sync(0xFFFFFFFFu, amb != 0);
+        if (!want) break;
+        if (qn[w] > kDrawQueue - 32) drain(32);
+        const int rank = __popc(want & ((1u << lane) - 1u));
+        const int base = qn[w];
+        if (amb) {
+          const int v = __ffs(amb) - 1;
+          amb &= amb - 1;
+          queue[w][base + rank] = ExactJob{bits[v], L.means[lv][j] + off + v, sum[v],
+                                           static_cast<uint16_t>(lv), static_cast<uint16_t>(j)};
+        }
+        __syncwarp();
+        if (lane == 0) qn[w] = base + __popc(want);
+        __syncwarp();
+      }
+    }
+    if (qn[w] >= 32) drain(32);
+  }
+  __syncwarp();
+  if (qn[w] > 0) drain(qn[w]);
+}
+
+using SweepSumsKernel = void (*)(const CUtensorMap, const StatsArgs, const SweepLevels);
+using SweepDrawKernel = void (*)(const StatsArgs, const SweepLevels);
+
+SweepSumsKernel select_sweep_kernel(int C, int nlev) {
 #define DPPX_SWEEP(Cv, NL) \
-  if (C == (Cv) && nlev == (NL)) return k_sweep_stats<Cv, NL>;
+  if (C == (Cv) && nlev == (NL)) return k_sweep_sums<Cv, NL>;
   DPPX_SWEEP(1, 2)
   DPPX_SWEEP(1, 3)
   DPPX_SWEEP(1, 4)
@@ -329,10 +384,15 @@ SweepKernel select_sweep_kernel(int C, int nlev) {
   return nullptr;
 }
 
-cudaError_t launch_sweep(SweepKernel k, const CUtensorMap& tin, const StatsArgs& a, const SweepLevels& L,
-                         int grid, size_t smem, cudaStream_t s) {
+cudaError_t launch_sweep(SweepSumsKernel k, const CUtensorMap& tin, const StatsArgs& a, const SweepLevels& L,
+                         int grid, size_t smem, int draw_grid, cudaStream_t s) {
   k<<<grid, kStatsThreads, smem, s>>>(tin, a, L);
+  if (cudaError_t e = cudaGetLastError()) return e;
+  SweepDrawKernel d = L.ne == 3 ? k_sweep_draw<3> : L.ne == 1 ? k_sweep_draw<1> : k_sweep_draw<0>;
+  d<<<draw_grid, kDrawThreads, 0, s>>>(a, L);
   return cudaGetLastError();
 }
+
+int sweep_draw_threads() { return kDrawThreads; }
 
 }  // namespace dppx
