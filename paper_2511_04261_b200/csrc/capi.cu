@@ -156,6 +156,7 @@ struct dppx_ctx {
   int chunk_frames = 0;
   bool exact_noise = false;
   bool out_pad_scratch = false;  // dppx_ctx_set_out_pad_scratch
+  bool force_rows = false;       // zero-copy calls: row-streaming kernels (plain loads/stores)
   double var_tau = 0.0;  // AdaptiveVariance host calls
   // bit-packed mask transport (maskpack.h): pinned staging per slot + packer pool
   dppx::MaskPacker* packer = nullptr;
@@ -564,6 +565,7 @@ int run_stats(dppx_ctx* ctx, StatsArgs& a) {
   a.slot_stride = static_cast<int>(round_up(static_cast<int64_t>(g.b) * a.slot_px * g.C, 128));
   k = var ? select_stats_kernel_var(g.C, g.b, g.n)
           : select_stats_kernel(g.C, g.b, g.n, a.adaptive != 0, a.pack > 1);
+  if (ctx->force_rows) k = nullptr;
   a.row_slack = a.pitch >= round_up(row_bytes, 16) ? 1 : 0;
   const int box_bytes = a.slot_px * g.C;
   // Input rows: the tensor's inner extent is rounded UP to 8 bytes when the
@@ -1139,6 +1141,77 @@ int host_pipeline_bands(dppx_ctx* ctx, bool adaptive, const dppx_frames_desc* d,
   return DPPX_OK;
 }
 
+// Device-accessible alias of a page-locked host buffer (nullptr if none).
+void* mapped_alias(const void* p) {
+  if (!p) return nullptr;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (at.type != cudaMemoryTypeHost) return nullptr;
+  return at.devicePointer;
+}
+
+// Single small frame, zero-copy: the kernels read the caller's page-locked
+// frame (and mask) and write the reconstructed frame straight over PCIe --
+// no staging copies, so no per-copy latency. The row-streaming kernels (plain
+// 16-byte loads / stores) are used; statistics land in the ctx's mapped
+// pinned staging and are copied to the caller's buffers on the host.
+int host_single_zerocopy(dppx_ctx* ctx, bool adaptive, const dppx_frames_desc* d, const BatchGeom& g,
+                         const uint8_t* img, const uint8_t* mask, const dppx_privacy_params* pp,
+                         const dppx_noise* nz, uint8_t* stats, int64_t sstride, uint32_t* lens,
+                         uint8_t* out, bool* used) {
+  *used = false;
+  const int C = g.C;
+  // Only shapes whose kernels never touch a byte past the frame (no padding
+  // columns, 16-byte rows): a read past a host allocation would fault.
+  if (g.PC != 0 || (static_cast<int64_t>(g.N) * C) % 16 != 0 || g.N % 16 != 0 ||
+      d->pitch != static_cast<int64_t>(g.N) * C || (out && d->out_pitch != d->pitch) ||
+      (adaptive && d->mask_pitch != g.N))
+    return DPPX_OK;
+  const size_t G = static_cast<size_t>(g.G);
+  const size_t cap = adaptive ? dppx_adaptive_payload_capacity(g.M, g.N, g.b, g.n) : G;
+  const int64_t dstride = adaptive ? round_up(static_cast<int64_t>(cap), 16) : static_cast<int64_t>(G);
+  const size_t gst = static_cast<size_t>(dstride) * C + 16;
+  if (ctx->gstats_pinned_n < gst) {
+    if (ctx->gstats_pinned) CUDA_TRY(ctx, cudaFreeHost(ctx->gstats_pinned));
+    ctx->gstats_pinned = nullptr;
+    ctx->gstats_pinned_n = 0;
+    CUDA_TRY(ctx, cudaHostAlloc(reinterpret_cast<void**>(&ctx->gstats_pinned), gst, cudaHostAllocMapped));
+    ctx->gstats_pinned_n = gst;
+  }
+  uint8_t* dimg = static_cast<uint8_t*>(mapped_alias(img));
+  uint8_t* dout = out ? static_cast<uint8_t*>(mapped_alias(out)) : nullptr;
+  uint8_t* dmask = adaptive ? static_cast<uint8_t*>(mapped_alias(mask)) : nullptr;
+  uint8_t* dst = static_cast<uint8_t*>(mapped_alias(ctx->gstats_pinned));
+  if (!dimg || (out && !dout) || (adaptive && !dmask) || !dst) return DPPX_OK;  // not mapped: other path
+  *used = true;
+  uint32_t* dlens = reinterpret_cast<uint32_t*>(dst + static_cast<size_t>(dstride) * C);
+  struct Restore {
+    dppx_ctx* c;
+    ~Restore() { c->force_rows = false; }
+  } restore{ctx};
+  ctx->force_rows = true;
+  if (int rc = pixelize_dev(ctx, d, dimg, dmask, pp, nz, nullptr, dst, dstride, adaptive ? dlens : nullptr, dout,
+                            adaptive, ctx->sd[0], ctx->sd_pinned[0], ctx->sd_pinned_n[0], ctx->comp_done[0], true))
+    return rc;
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (ctx->timing) collect_timings(ctx);
+  ctx->kstats.h2d_bytes += static_cast<uint64_t>(g.M) * g.N * C + (adaptive ? static_cast<uint64_t>(g.M) * g.N : 0);
+  ctx->kstats.d2h_bytes += (out ? static_cast<uint64_t>(g.M) * g.N * C : 0);
+  const uint8_t* st = ctx->gstats_pinned;
+  const uint32_t* ln = reinterpret_cast<const uint32_t*>(st + static_cast<size_t>(dstride) * C);
+  for (int c = 0; c < C; ++c) {
+    const size_t w = adaptive ? std::min<size_t>(ln[c], cap) : G;
+    std::memcpy(stats + static_cast<int64_t>(c) * (adaptive ? sstride : static_cast<int64_t>(G)),
+                st + static_cast<int64_t>(c) * dstride, w);
+    if (adaptive && lens) lens[c] = ln[c];
+    ctx->kstats.d2h_bytes += w;
+  }
+  return DPPX_OK;
+}
+
 // Single-frame host call as a replayed CUDA graph (see dppx_ctx::FrameGraph).
 // Preconditions (host_pipeline checks): one frame, pinned dense image / mask /
 // output buffers with N*C % 16 == 0 (the device layout), KEYED or no noise.
@@ -1182,7 +1255,7 @@ int host_single_graph(dppx_ctx* ctx, bool adaptive, const dppx_frames_desc* d, c
       if (ctx->gstats_pinned) CUDA_TRY(ctx, cudaFreeHost(ctx->gstats_pinned));
       ctx->gstats_pinned = nullptr;
       ctx->gstats_pinned_n = 0;
-      CUDA_TRY(ctx, cudaHostAlloc(reinterpret_cast<void**>(&ctx->gstats_pinned), gst, cudaHostAllocDefault));
+      CUDA_TRY(ctx, cudaHostAlloc(reinterpret_cast<void**>(&ctx->gstats_pinned), gst, cudaHostAllocMapped));
       ctx->gstats_pinned_n = gst;
     }
     // A graph owns device buffer addresses: drop the cache when it is full.
@@ -1442,6 +1515,14 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
     static const bool graphs_on = !(std::getenv("DPPX_GRAPH") && std::getenv("DPPX_GRAPH")[0] == '0');
     const int64_t row = static_cast<int64_t>(N) * C;
     const bool small = static_cast<int64_t>(M) * row < (4ll << 20);
+    static const bool zc_on = std::getenv("DPPX_ZEROCOPY") && std::getenv("DPPX_ZEROCOPY")[0] == '1';
+    if (zc_on && F == 1 && small && (op == HostOp::Uniform || op == HostOp::Adaptive) &&
+        (!nz || nz->kind != DPPX_NOISE_INJECTED)) {
+      bool used = false;
+      const int rc = host_single_zerocopy(ctx, op == HostOp::Adaptive, d, g, img, mask, pp, nz, stats, sstride,
+                                          lens, out, &used);
+      if (rc || used) return rc;
+    }
     if (graphs_on && F == 1 && small && (op == HostOp::Uniform || op == HostOp::Adaptive) &&
         (!nz || nz->kind == DPPX_NOISE_NONE || nz->kind == DPPX_NOISE_KEYED) && row % 16 == 0 &&
         d->pitch == row && (!out || d->out_pitch == row) && (op != HostOp::Adaptive || d->mask_pitch == N) &&

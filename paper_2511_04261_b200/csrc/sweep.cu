@@ -235,7 +235,7 @@ __device__ __forceinline__ float laplace_mag(uint64_t bits, bool& neg) {
   return (static_cast<float>(52 - e) - lg_m) * 0.693147180559945f;
 }
 
-template <int NE>
+template <int NE, int KIND>
 __global__ void __launch_bounds__(kDrawThreads)
     k_sweep_draw(const __grid_constant__ StatsArgs a, const __grid_constant__ SweepLevels L) {
   __shared__ ExactJob queue[kDrawWarps][kDrawQueue];
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kDrawThreads)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (lane == 0) qn[w] = 0;
   __syncwarp();
-  const int kind = a.noise.kind;
+  constexpr int kind = KIND;  // noise kind: no per-statistic branches
   const bool exact_only = a.exact_noise != 0;
   const int ne = NE > 0 ? NE : L.ne;
   // Drain the top `cnt` queued statistics (one per lane) with the exact arithmetic.
@@ -317,6 +317,7 @@ __global__ void __launch_bounds__(kDrawThreads)
       neg[v] = false;
       Lf[v] = kind == DPPX_NOISE_NONE ? 0.0f : laplace_mag(bits[v], neg[v]);
     }
+#pragma unroll
     for (int j = 0; j < ne; ++j) {
       uint32_t amb = 0;  // cells whose estimate is ambiguous
       if (any && nvalid > 0) {
@@ -344,22 +345,24 @@ __global__ void __launch_bounds__(kDrawThreads)
         }
         amb &= (1u << nvalid) - 1u;
       }
-      // queue the ambiguous ones (their stored byte is overwritten when drained)
-      while (true) {
-        const unsigned want = __ballot_sync(0xFFFFFFFFu, amb != 0);
-        if (!want) break;
-        if (qn[w] > kDrawQueue - 32) drain(32);
-        const int rank = __popc(want & ((1u << lane) - 1u));
-        const int base = qn[w];
-        if (amb) {
-          const int v = __ffs(amb) - 1;
-          amb &= amb - 1;
-          queue[w][base + rank] = ExactJob{bits[v], L.means[lv][j] + off + v, sum[v],
-                                           static_cast<uint16_t>(lv), static_cast<uint16_t>(j)};
+      // queue the ambiguous ones (their stored byte is overwritten when drained);
+      // cell index v is static in every step, so nothing spills to local memory
+      if (__any_sync(0xFFFFFFFFu, amb != 0)) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const bool mine = (amb >> v) & 1u;
+          const unsigned want = __ballot_sync(0xFFFFFFFFu, mine);
+          if (!want) continue;
+          if (qn[w] > kDrawQueue - 32) drain(32);
+          const int base = qn[w];
+          if (mine)
+            queue[w][base + __popc(want & ((1u << lane) - 1u))] =
+                ExactJob{bits[v], L.means[lv][j] + off + v, sum[v], static_cast<uint16_t>(lv),
+                         static_cast<uint16_t>(j)};
+          __syncwarp();
+          if (lane == 0) qn[w] = base + __popc(want);
+          __syncwarp();
         }
-        __syncwarp();
-        if (lane == 0) qn[w] = base + __popc(want);
-        __syncwarp();
       }
     }
     if (qn[w] >= 32) drain(32);
@@ -388,7 +391,14 @@ cudaError_t launch_sweep(SweepSumsKernel k, const CUtensorMap& tin, const StatsA
                          int grid, size_t smem, int draw_grid, cudaStream_t s) {
   k<<<grid, kStatsThreads, smem, s>>>(tin, a, L);
   if (cudaError_t e = cudaGetLastError()) return e;
-  SweepDrawKernel d = L.ne == 3 ? k_sweep_draw<3> : L.ne == 1 ? k_sweep_draw<1> : k_sweep_draw<0>;
+  const int kind = a.noise.kind;
+  SweepDrawKernel d;
+  if (kind == DPPX_NOISE_KEYED)
+    d = L.ne == 3 ? k_sweep_draw<3, DPPX_NOISE_KEYED> : k_sweep_draw<0, DPPX_NOISE_KEYED>;
+  else if (kind == DPPX_NOISE_PHILOX)
+    d = L.ne == 3 ? k_sweep_draw<3, DPPX_NOISE_PHILOX> : k_sweep_draw<0, DPPX_NOISE_PHILOX>;
+  else
+    d = k_sweep_draw<0, DPPX_NOISE_NONE>;
   d<<<draw_grid, kDrawThreads, 0, s>>>(a, L);
   return cudaGetLastError();
 }
