@@ -21,6 +21,7 @@
 
 #include "../../include/dppx_gpu.h"
 #include "dppx_params.h"
+#include "dppx_device.cuh"
 #include "maskpack.h"
 
 namespace dppx {
@@ -1227,7 +1228,9 @@ int host_single_graph(dppx_ctx* ctx, bool adaptive, const dppx_frames_desc* d, c
   const int64_t dstride = adaptive ? round_up(static_cast<int64_t>(cap), 16) : static_cast<int64_t>(G);
   const int kind = nz ? nz->kind : DPPX_NOISE_NONE;
   // Row bands: the H2D of band i+1, K1 of band i and D2H of band i-1 overlap.
-  int nb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(4, dfs >> 18)));
+  // (one band measured fastest for a PETS frame: every extra copy node adds
+  // more latency than its overlap saves, r02k_latency.txt)
+  int nb = 1;
   if (const char* env = std::getenv("DPPX_GRAPH_BANDS")) nb = std::max(1, std::atoi(env));
   nb = std::max(1, std::min({nb, g.GR / 2 > 0 ? g.GR / 2 : 1, dppx_ctx::kMaxBands}));
   dppx_ctx::FrameGraph* fgp = nullptr;
@@ -2230,7 +2233,7 @@ int dppx_pixelize_uniform_sweep_dev(dppx_ctx* ctx, const dppx_frames_desc* d, co
     for (int j = 0; j < ne; ++j) {
       L.sigma[lv][j] = pp[i * ne + j].sigma;
       L.sigmaf[lv][j] = static_cast<float>(pp[i * ne + j].sigma);
-      L.margin[lv][j] = 2e-3f + static_cast<float>(pp[i * ne + j].sigma) * 4e-6f;  // fast_margin
+      L.margin[lv][j] = fast_margin(pp[i * ne + j].sigma);
       L.means[lv][j] = means[i * ne + j];
     }
   }

@@ -181,10 +181,14 @@ __device__ __forceinline__ double cell_mean(uint32_t sum, double area) {
 //   f32 (relative error <= 2^-24, so <= 8.6e-8 in log2), lg2.approx (<= 2^-21,
 //   checked exhaustively on the device by tests/test_gpu_parity.py)
 //   => |d noise| <= sigma * ln2 * 6.6e-7 <= sigma * 4.6e-7;
-//   f32 rounding of mean, noise and the sum (< 8 ulp of 512) <= 2.5e-4.
-// margin = 2e-3 + sigma * 4e-6 keeps a factor >= 8 over that budget.
-__device__ __forceinline__ float fast_margin(double sigma) {
-  return 2e-3f + static_cast<float>(sigma) * 4e-6f;
+//   f32 rounding of mean, noise and the sum (< 8 ulp of 512; the rounding of
+//   -ln(1-2|u|) and of sigma * L is relative to |noise| <= 512 where it
+//   matters) <= 2.5e-4.
+// margin = 5e-4 + sigma * 1e-6 keeps a factor >= 2 over that budget (round 1
+// used 2e-3 + 4e-6 sigma, a factor 8: 4x as many exact f64 evaluations, the
+// dominant cost of draw-bound shapes such as b = 4 at eps = 0.1, sigma = 2550).
+__host__ __device__ __forceinline__ float fast_margin(double sigma) {
+  return 5e-4f + static_cast<float>(sigma) * 1e-6f;
 }
 
 // MUFU lg2 (no denormal fix-up: the argument is a mantissa in [1, 2)); its

@@ -34,6 +34,14 @@ def main():
         t0 = time.perf_counter()
         call()
         ts.append(time.perf_counter() - t0)
+    # device time of the kernels inside one call (CUDA events around each launch)
+    ctx.reset_stats()
+    ctx.set_timing(True)
+    for _ in range(50):
+        call()
+    st = ctx.stats()
+    ctx.set_timing(False)
+    dev_us = {k: round(v / 50 * 1e3, 2) for k, v in st["device_ms"].items() if v}
     # copy floors
     nbytes = M * N * C
     h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
@@ -67,6 +75,7 @@ def main():
                       "median_us": round(float(np.median(ts)) * 1e6, 2),
                       "p10_us": round(float(np.percentile(ts, 10)) * 1e6, 2),
                       "p90_us": round(float(np.percentile(ts, 90)) * 1e6, 2), **floors,
+                      "kernel_us_per_call": dev_us,
                       "launches": ctx.stats()["launches"]}))
 
 
