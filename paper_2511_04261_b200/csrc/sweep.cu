@@ -87,8 +87,8 @@ __global__ void __launch_bounds__(kStatsThreads, 3)
     if (lane == 0) {
       prefetch_tmap(&tm_in);
       for (int k = 0;; ++k) {
-        const int s = k % S;
-        if (k >= S) mbar_wait(&done_bar[s], ((k / S) - 1) & 1);
+        const int s = ring_slot(k, S);
+        if (k >= S) mbar_wait(&done_bar[s], (ring_lap(k, S) - 1) & 1);
         int u = atomicAdd(a.work_counter, 1);
         if (u >= a.units) {
           if (u == a.units + static_cast<int>(gridDim.x) - 1) atomicExch(a.work_counter, 0);
@@ -110,8 +110,8 @@ __global__ void __launch_bounds__(kStatsThreads, 3)
   const int t = threadIdx.x;
   const BatchGeom& g = a.g;  // geometry of the BMAX grid (bands, tiles, padding)
   for (int k = 0;; ++k) {
-    const int s = k % S;
-    mbar_wait(&id_bar[s], (k / S) & 1);
+    const int s = ring_slot(k, S);
+    mbar_wait(&id_bar[s], ring_lap(k, S) & 1);
     const int u = *reinterpret_cast<volatile int*>(&stage_unit[s]);
     if (u < 0) break;
     const UnitPos p = decode_unit<false, TILE>(a, u);
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kStatsThreads, 3)
     const int vbytes = valid_bytes<C, false, TILE>(a, p.px0);
     const int copy = staged_bytes<C, BMAX, false, TILE>(a, p);
     const int need = min(TILE, g.GC * BMAX - p.px0) * C;
-    mbar_wait(&full_bar[s], (k / S) & 1);
+    mbar_wait(&full_bar[s], ring_lap(k, S) & 1);
     // Mirrored padding columns / unstaged row tail (image.cpp:105-110), as K1.
     const int fs = min(copy, vbytes);
     if (fs < need) {

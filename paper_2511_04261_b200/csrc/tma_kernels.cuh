@@ -22,6 +22,16 @@ constexpr int kTilePx = 4 * kConsumers;    // 512 px per tile
 constexpr int kStatsThreads = kConsumers + 32;
 constexpr int kMaxStages = 4;
 
+// Ring position of unit k in an S-stage ring (S in {2, 3, 4}, the host's
+// choice at run time): slot and lap without a runtime integer division (a
+// division by a non-constant is ~25 instructions, and these run per unit).
+__device__ __forceinline__ int ring_slot(int k, int S) {
+  return S == 2 ? (k & 1) : S == 4 ? (k & 3) : k % 3;
+}
+__device__ __forceinline__ int ring_lap(int k, int S) {
+  return S == 2 ? (k >> 1) : S == 4 ? (k >> 2) : k / 3;
+}
+
 struct UnitPos {
   int fg, r, tile, px0;  // frame group (frames fg*pack + j), grid row, column tile
 };
@@ -372,9 +382,9 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? 6 : 0)
     int k = 0;
     int done_units = 0;  // units of this CTA already stored
     for (;; ++k) {
-      const int s = k % S;
+      const int s = ring_slot(k, S);
       if (k >= S) {
-        finish_unit(s, (k / S) - 1);
+        finish_unit(s, ring_lap(k, S) - 1);
         ++done_units;
       }
       int u = 0;
@@ -397,7 +407,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? 6 : 0)
       if (u < 0) break;
     }
     // k units were loaded; units [done_units, k) still need their store.
-    for (int j = done_units; j < k; ++j) finish_unit(j % S, j / S);
+    for (int j = done_units; j < k; ++j) finish_unit(ring_slot(j, S), ring_lap(j, S));
     if (lane == 0) bulk_wait_all();
     return;
   }
@@ -467,8 +477,8 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? 6 : 0)
   }
   auto load_meta = [&](int k_next) {
     Meta m;
-    const int sn = k_next % S;
-    mbar_wait(&id_bar[sn], (k_next / S) & 1);
+    const int sn = ring_slot(k_next, S);
+    mbar_wait(&id_bar[sn], ring_lap(k_next, S) & 1);
     m.u = *reinterpret_cast<volatile int*>(&stage_unit[sn]);
     m.info = 1u;
     m.rowpre = m.stot = 0;
@@ -495,7 +505,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? 6 : 0)
   };
   Meta next = load_meta(0);
   for (int k = 0;; ++k) {
-    const int s = k % S;
+    const int s = ring_slot(k, S);
     uint8_t* st = smem + s * STAGE;
     const Meta cur = next;
     const int u = cur.u;
@@ -519,7 +529,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? 6 : 0)
     for (int ch = 0; ch < C; ++ch)
       cs[ch] = a.noise.kind == DPPX_NOISE_KEYED ? key_cell(cur.seed[ch], p.r, cell) : 0ull;
 
-    mbar_wait(&full_bar[s], (k / S) & 1);
+    mbar_wait(&full_bar[s], ring_lap(k, S) & 1);
 
     // Row tail not covered by the staged copy and mirrored padding columns
     // (image.cpp:105-110), including stray pitch-slack bytes a rounded-up copy
@@ -951,9 +961,9 @@ __global__ void __launch_bounds__(kStatsThreads)
     };
     int k = 0, done_units = 0;
     for (;; ++k) {
-      const int s = k % S;
+      const int s = ring_slot(k, S);
       if (k >= S) {
-        finish_unit(s, (k / S) - 1);
+        finish_unit(s, ring_lap(k, S) - 1);
         ++done_units;
       }
       int u = 0;
@@ -973,7 +983,7 @@ __global__ void __launch_bounds__(kStatsThreads)
       u = __shfl_sync(0xFFFFFFFFu, u, 0);
       if (u < 0) break;
     }
-    for (int j = done_units; j < k; ++j) finish_unit(j % S, j / S);
+    for (int j = done_units; j < k; ++j) finish_unit(ring_slot(j, S), ring_lap(j, S));
     if (lane == 0) bulk_wait_all();
     return;
   }
@@ -996,9 +1006,9 @@ __global__ void __launch_bounds__(kStatsThreads)
     if (pos / C < split) m[pos % C][pos / 4] |= 1u << (8 * (pos % 4));
 
   for (int k = 0;; ++k) {
-    const int s = k % S;
+    const int s = ring_slot(k, S);
     uint8_t* st = smem + s * STAGE;
-    mbar_wait(&id_bar[s], (k / S) & 1);
+    mbar_wait(&id_bar[s], ring_lap(k, S) & 1);
     const int u = *reinterpret_cast<volatile int*>(&stage_unit[s]);
     if (u < 0) break;
     const UnitPos p = decode_unit<false, TILE>(a, u);
@@ -1011,7 +1021,7 @@ __global__ void __launch_bounds__(kStatsThreads)
     const int copy = staged_bytes<C, B, false, TILE>(a, p);
     const int need = min(TILE, g.GC * B - p.px0) * C;
 
-    mbar_wait(&full_bar[s], (k / S) & 1);
+    mbar_wait(&full_bar[s], ring_lap(k, S) & 1);
     // Mirrored padding columns and any unstaged row tail (as k_stats_tma).
     const int fs = min(copy, vbytes);
     if (fs < need) {
@@ -1460,9 +1470,9 @@ __global__ void __launch_bounds__(kStatsThreads)
     };
     int k = 0, done_units = 0;
     for (;; ++k) {
-      const int s = k % S;
+      const int s = ring_slot(k, S);
       if (k >= S) {
-        finish_unit(s, (k / S) - 1);
+        finish_unit(s, ring_lap(k, S) - 1);
         ++done_units;
       }
       int u = 0;
@@ -1482,7 +1492,7 @@ __global__ void __launch_bounds__(kStatsThreads)
       u = __shfl_sync(0xFFFFFFFFu, u, 0);
       if (u < 0) break;
     }
-    for (int j = done_units; j < k; ++j) finish_unit(j % S, j / S);
+    for (int j = done_units; j < k; ++j) finish_unit(ring_slot(j, S), ring_lap(j, S));
     if (lane == 0) bulk_wait_all();
     return;
   }
@@ -1508,9 +1518,9 @@ __global__ void __launch_bounds__(kStatsThreads)
     if (pos / C < split) m[pos % C][pos / 4] |= 1u << (8 * (pos % 4));
 
   for (int k = 0;; ++k) {
-    const int s = k % S;
+    const int s = ring_slot(k, S);
     uint8_t* st = smem + s * STAGE;
-    mbar_wait(&id_bar[s], (k / S) & 1);
+    mbar_wait(&id_bar[s], ring_lap(k, S) & 1);
     const int u = *reinterpret_cast<volatile int*>(&stage_unit[s]);
     if (u < 0) break;
     const UnitPos p = decode_unit<false, TILE>(a, u);
@@ -1528,7 +1538,7 @@ __global__ void __launch_bounds__(kStatsThreads)
     uint32_t info = 1u;  // cell class and packed slot (K0), published after the barrier below
     if (t < ncell) info = __ldg(&a.cellinfo[static_cast<int64_t>(f) * g.G + p.r * g.GC + cell0 + t]);
 
-    mbar_wait(&full_bar[s], (k / S) & 1);
+    mbar_wait(&full_bar[s], ring_lap(k, S) & 1);
     const int fs = min(copy, vbytes);
     if (fs < need) {
       constexpr int kLanes = 4;
