@@ -442,12 +442,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? 6 : 0)
   constexpr int CPW = 32 / B4;           // cells per consumer warp
   constexpr int NN = NSUB * NSUB;
   using SumT = typename std::conditional<(SB * SB * 255 < 65536 && !STR), uint16_t, uint32_t>::type;
-  // DYN: mask-classified adaptive kernels without paired subcells choose the
-  // complex-draw mode per warp at run time: compact for warps that mix simple
-  // and complex cells (scattered masks), direct otherwise.
-  constexpr bool DYN = ADAPTIVE && !VAR && !STR && !PACKED && !(NSUB >= 8 && NSUB % 2 == 0) &&
-                       NN * C * CPW * 2 <= 1536;
-  constexpr bool TABLES = VAR || STR || DYN;
+  constexpr bool TABLES = VAR || STR;
   struct CellRec {
     int cw, f, cell, gidx;
     int64_t off;
@@ -620,10 +615,9 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? 6 : 0)
       // smem table and the warp's complex draws (cells x n*n x C) are dealt
       // round-robin to all 32 lanes, so the lanes of simple cells do not idle
       // through the serial draws (tools/k1_complex_sweep.py measures both).
+      constexpr bool compact = VAR || STR;
       const bool cx = active && !simple;
       const unsigned cx_any = __ballot_sync(0xFFFFFFFFu, cx);
-      // (warp-uniform) direct when every active strip of the warp is complex
-      const bool compact = VAR || STR || (DYN && cx_any != __ballot_sync(0xFFFFFFFFu, active));
       __syncwarp();  // the previous unit's reads of this warp's tables are done
       if constexpr (STR) {
         if (cx_any) {  // subcell sums accumulate with smem atomics
@@ -634,7 +628,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? 6 : 0)
       // Direct mode with many vertical subcells (NSUB >= 8): two at a time, so
       // the two subcells' draw chains overlap (a store of one subcell's pattern
       // would otherwise order the next subcell's smem reads behind its draws).
-      constexpr bool PAIRS = !(VAR || STR) && NSUB >= 8 && NSUB % 2 == 0;
+      constexpr bool PAIRS = !compact && NSUB >= 8 && NSUB % 2 == 0;
       if constexpr (PAIRS) {
 #pragma unroll 1
         for (int vs = 0; vs < NSUB; vs += 2) {
@@ -715,7 +709,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? 6 : 0)
           } else if (cx_any) {
 #pragma unroll
             for (int ch = 0; ch < C; ++ch) acc[ch] = group_sum<SB4>(acc[ch]);
-            if (TABLES && compact) {
+            if constexpr (compact) {
               if (cx && lic % SB4 == 0) {
 #pragma unroll
                 for (int ch = 0; ch < C; ++ch)
@@ -750,7 +744,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? 6 : 0)
         }
       }
       if constexpr (!VAR) next = load_meta(k + 1);
-      if (TABLES && compact && cx_any) {
+      if (compact && cx_any) {
         const unsigned leaders = __ballot_sync(0xFFFFFFFFu, cx && lic == 0);
         if (cx && lic == 0) {
           const int rank = __popc(leaders & ((1u << (t & 31)) - 1u));
