@@ -80,14 +80,16 @@ struct SweepLevels {  // sweep.cu
   void* sums[kSweepMaxLevels];
   int srows[kSweepMaxLevels], scols[kSweepMaxLevels];
   int64_t item0[kSweepMaxLevels + 1];
+  int64_t item_begin, item_end;
   int groups[kSweepMaxLevels];
   FastDiv div_groups[kSweepMaxLevels], div_rows[kSweepMaxLevels];
   int planes;
 };
 using SweepSumsKernel = void (*)(const CUtensorMap, const StatsArgs, const SweepLevels);
 SweepSumsKernel select_sweep_kernel(int C, int nlev);
-cudaError_t launch_sweep(SweepSumsKernel k, const CUtensorMap& tin, const StatsArgs& a, const SweepLevels& L,
-                         int grid, size_t smem, int draw_grid, cudaStream_t s);
+cudaError_t launch_sweep_sums(SweepSumsKernel k, const CUtensorMap& tin, const StatsArgs& a,
+                              const SweepLevels& L, int grid, size_t smem, cudaStream_t s);
+cudaError_t launch_sweep_draw(const StatsArgs& a, const SweepLevels& L, int max_grid, cudaStream_t s);
 int sweep_draw_threads();
 }  // namespace dppx
 
@@ -2276,14 +2278,24 @@ int dppx_pixelize_uniform_sweep_dev(dppx_ctx* ctx, const dppx_frames_desc* d, co
   if (int rc = ensure(ctx, ctx->work, 16, /*zero=*/true)) return rc;
   a.work_counter = static_cast<int*>(ctx->work.p);
   PendingTiming pt;
-  const int draw_grid = static_cast<int>(std::max<int64_t>(
-      1, std::min<int64_t>((items + sweep_draw_threads() - 1) / sweep_draw_threads(), 8ll * ctx->sms)));
   timing_begin(ctx, DPPX_K_SWEEP, &pt);
-  CUDA_TRY(ctx, launch_sweep(k, tin, a, L, grid, smem, draw_grid, ctx->stream));
-  timing_end(ctx, &pt);
-  // The runs' images: broadcast_means of their statistics (write-only K2).
-  if (out) {
-    for (int i = 0; i < nb; ++i)
+  CUDA_TRY(ctx, launch_sweep_sums(k, tin, a, L, grid, smem, ctx->stream));
+  // Draws, largest grid side first. The broadcasts of the larger sides
+  // (write-only, HBM-bound) then run on a second stream while the 4-px level's
+  // draws (compute-bound, ~3/4 of all statistics) run on the first.
+  const int max_draw_grid = 8 * ctx->sms;
+  auto draw_levels = [&](int lo, int hi) -> int {  // levels [lo, hi)
+    SweepLevels Ld = L;
+    Ld.item_begin = L.item0[lo];
+    Ld.item_end = L.item0[hi];
+    CUDA_TRY(ctx, launch_sweep_draw(a, Ld, max_draw_grid, ctx->stream));
+    return DPPX_OK;
+  };
+  if (nlev > 1)
+    if (int rc = draw_levels(1, nlev)) return rc;
+  auto broadcast_runs = [&](bool level0) -> int {
+    for (int i = 0; i < nb; ++i) {
+      if ((b_list[i] == 4) != level0) continue;
       for (int j = 0; j < ne; ++j)
         if (out[i * ne + j]) {
           dppx_geometry gg;
@@ -2292,6 +2304,30 @@ int dppx_pixelize_uniform_sweep_dev(dppx_ctx* ctx, const dppx_frames_desc* d, co
                                   nullptr, b_list[i], 1, out[i * ne + j], false))
             return rc;
         }
+    }
+    return DPPX_OK;
+  };
+  cudaStream_t main_stream = ctx->stream;
+  cudaEvent_t big_ready = nullptr, aux_done = nullptr;
+  if (out) {
+    big_ready = get_event(ctx);
+    aux_done = get_event(ctx);
+    CUDA_TRY(ctx, cudaEventRecord(big_ready, main_stream));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->s_in, big_ready, 0));
+    ctx->stream = ctx->s_in;  // (the expanders launch on ctx->stream)
+    const int rc = broadcast_runs(false);
+    ctx->stream = main_stream;
+    if (rc) return rc;
+    CUDA_TRY(ctx, cudaEventRecord(aux_done, ctx->s_in));
+  }
+  if (active & 1u)
+    if (int rc = draw_levels(0, 1)) return rc;
+  timing_end(ctx, &pt);
+  if (out) {
+    if (int rc = broadcast_runs(true)) return rc;
+    CUDA_TRY(ctx, cudaStreamWaitEvent(main_stream, aux_done, 0));  // join
+    ctx->event_pool.push_back(big_ready);
+    ctx->event_pool.push_back(aux_done);
   }
   return DPPX_OK;
 }

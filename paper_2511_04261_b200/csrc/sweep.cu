@@ -47,6 +47,7 @@ struct SweepLevels {
   // K1s-draw work items: 4 consecutive cells of one (plane, row) of level k
   // (planes x GR[k] rows x groups[k]); items [item0[k], item0[k+1]) are level k's
   int64_t item0[kSweepMaxLevels + 1];
+  int64_t item_begin, item_end;      // this launch's items (one or more levels)
   int groups[kSweepMaxLevels];       // ceil(GC[k] / 4)
   FastDiv div_groups[kSweepMaxLevels], div_rows[kSweepMaxLevels];  // by groups[k], by GR[k]
   int planes;
@@ -258,13 +259,14 @@ __global__ void __launch_bounds__(kDrawThreads)
     if (lane == 0) qn[w] = base;
     __syncwarp();
   };
-  const int64_t total = L.item0[L.nlev];
+  const int64_t total = L.item_end - L.item_begin;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * kDrawThreads;
   // Every warp runs the same number of passes (the queue drains are warp-collective).
   const int64_t passes = (total + stride - 1) / stride;
   for (int64_t pass = 0; pass < passes; ++pass) {
-    const int64_t item = pass * stride + static_cast<int64_t>(blockIdx.x) * kDrawThreads + threadIdx.x;
-    bool any = item < total;
+    const int64_t rel_item = pass * stride + static_cast<int64_t>(blockIdx.x) * kDrawThreads + threadIdx.x;
+    const int64_t item = L.item_begin + rel_item;
+    bool any = rel_item < total;
     int lv = 0;
     if (any) {
 #pragma unroll
@@ -387,10 +389,18 @@ SweepSumsKernel select_sweep_kernel(int C, int nlev) {
   return nullptr;
 }
 
-cudaError_t launch_sweep(SweepSumsKernel k, const CUtensorMap& tin, const StatsArgs& a, const SweepLevels& L,
-                         int grid, size_t smem, int draw_grid, cudaStream_t s) {
+cudaError_t launch_sweep_sums(SweepSumsKernel k, const CUtensorMap& tin, const StatsArgs& a,
+                              const SweepLevels& L, int grid, size_t smem, cudaStream_t s) {
   k<<<grid, kStatsThreads, smem, s>>>(tin, a, L);
-  if (cudaError_t e = cudaGetLastError()) return e;
+  return cudaGetLastError();
+}
+
+// Draws of items [L.item_begin, L.item_end) (one or more levels).
+cudaError_t launch_sweep_draw(const StatsArgs& a, const SweepLevels& L, int max_grid, cudaStream_t s) {
+  const int64_t items = L.item_end - L.item_begin;
+  if (items <= 0) return cudaSuccess;
+  const int draw_grid = static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>((items + kDrawThreads - 1) / kDrawThreads, max_grid)));
   const int kind = a.noise.kind;
   SweepDrawKernel d;
   if (kind == DPPX_NOISE_KEYED)
