@@ -22,6 +22,12 @@ KEYS = [
     "launch__shared_mem_per_block_dynamic", "launch__occupancy_limit_shared_mem",
     "smsp__cycles_active.avg", "sm__cycles_elapsed.avg", "lts__t_bytes.sum",
     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_adu.avg.pct_of_peak_sustained_active",
+    "smsp__warps_eligible.avg.per_cycle_active",
 ]
 
 
