@@ -334,6 +334,10 @@ int64_t out_map_row_bytes(const dppx_ctx* ctx, int64_t row_bytes, int64_t opitch
     const int64_t r = std::min<int64_t>(opitch, (row_bytes + 31) / 32 * 32) / 16 * 16;
     if (r >= row_bytes) return r;
   }
+  // (DPPX_TAIL32=1: A/B knob, extent down to whole 32-byte sectors so the
+  // row's last, partial sector is written by threads alone)
+  static const bool tail32 = std::getenv("DPPX_TAIL32") && std::getenv("DPPX_TAIL32")[0] == '1';
+  if (tail32 && row_bytes >= 32) return row_bytes / 32 * 32;
   return row_bytes / 16 * 16;
 }
 

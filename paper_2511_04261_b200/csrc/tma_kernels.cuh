@@ -21,6 +21,12 @@ constexpr int kConsumers = 128;            // 4 consumer warps, one 4-px strip e
 constexpr int kTilePx = 4 * kConsumers;    // 512 px per tile
 constexpr int kStatsThreads = kConsumers + 32;
 constexpr int kMaxStages = 4;
+// Direct complex draws take two vertical subcells per iteration from this n up
+// (A/B knob at build time).
+#ifndef DPPX_PAIRS_MIN
+#define DPPX_PAIRS_MIN 8
+#endif
+constexpr int kPairsMinNsub = DPPX_PAIRS_MIN;
 
 // Ring position of unit k in an S-stage ring (S in {2, 3, 4}, the host's
 // choice at run time): slot and lap without a runtime integer division (a
@@ -133,6 +139,31 @@ __device__ __forceinline__ void store_unit(const StatsArgs& a, const CUtensorMap
   bulk_wait_read_all();
 }
 
+// The < 16 bytes of an output row past the store tensor map's extent: the
+// extent is a multiple of 16 bytes and rows / smem slot rows are 16-byte
+// aligned, so the tail is at most four aligned stores (8, 4, 2, 1 bytes)
+// instead of one store per byte (CelebA rows: 6 tail bytes per row).
+__device__ __forceinline__ void copy_row_tail(uint8_t* dst, const uint8_t* src, int n) {
+  if (n >= 16 || ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 7)) {
+    for (int x = 0; x < n; ++x) dst[x] = src[x];
+    return;
+  }
+  int o = 0;
+  if (n & 8) {
+    *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(src);
+    o = 8;
+  }
+  if (n & 4) {
+    *reinterpret_cast<uint32_t*>(dst + o) = *reinterpret_cast<const uint32_t*>(src + o);
+    o += 4;
+  }
+  if (n & 2) {
+    *reinterpret_cast<uint16_t*>(dst + o) = *reinterpret_cast<const uint16_t*>(src + o);
+    o += 2;
+  }
+  if (n & 1) dst[o] = src[o];
+}
+
 // Output bytes of a unit past the output tensor map's row extent (< 16 per row:
 // the TMA store covers [0, tensor_out_bytes)), written by the 32 producer lanes.
 template <int C, int B, bool PACKED, int TILE = kTilePx>
@@ -146,12 +177,11 @@ __device__ __forceinline__ void store_tail(const StatsArgs& a, int u, const uint
   const int rows = min(B, a.g.M - p.r * B);
   const int pk = units_pack<PACKED>(a);
   const int nf = PACKED ? min(pk, a.g.F - p.fg * pk) : 1;
-  for (int e = lane; e < nf * rows * span; e += 32) {
-    const int jr = e / span, x = scopy + (e - jr * span);
-    const int j = jr / rows, i = jr - j * rows;
-    a.out[static_cast<int64_t>(p.fg * pk + j) * a.ofstride +
-          static_cast<int64_t>(p.r * B + i) * a.opitch + static_cast<int64_t>(p.px0) * C + x] =
-        st[j * a.slot_stride + i * srb + x];
+  for (int e = lane; e < nf * rows; e += 32) {  // one row per lane
+    const int j = e / rows, i = e - j * rows;
+    copy_row_tail(a.out + static_cast<int64_t>(p.fg * pk + j) * a.ofstride +
+                      static_cast<int64_t>(p.r * B + i) * a.opitch + static_cast<int64_t>(p.px0) * C + scopy,
+                  st + j * a.slot_stride + i * srb + scopy, span);
   }
 }
 
@@ -628,7 +658,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? 6 : 0)
       // Direct mode with many vertical subcells (NSUB >= 8): two at a time, so
       // the two subcells' draw chains overlap (a store of one subcell's pattern
       // would otherwise order the next subcell's smem reads behind its draws).
-      constexpr bool PAIRS = !compact && NSUB >= 8 && NSUB % 2 == 0;
+      constexpr bool PAIRS = !compact && NSUB >= kPairsMinNsub && NSUB % 2 == 0;
       if constexpr (PAIRS) {
 #pragma unroll 1
         for (int vs = 0; vs < NSUB; vs += 2) {
@@ -1218,11 +1248,11 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
     const int span = vbytes - scopy;
     if (span > 0) {
       const int rows = min(B, g.M - r * B);
-      for (int e = t; e < nf * rows * span; e += NT) {
-        const int jr = e / span, x = scopy + (e - jr * span);
-        const int j = jr / rows, i = jr - j * rows;
-        a.out[static_cast<int64_t>(fg * pk + j) * a.ofstride + static_cast<int64_t>(r * B + i) * a.opitch +
-              static_cast<int64_t>(px0) * C + x] = buf[j * (PACKED ? a.slot_stride : 0) + i * srb + x];
+      for (int e = t; e < nf * rows; e += NT) {  // one row per thread
+        const int j = e / rows, i = e - j * rows;
+        copy_row_tail(a.out + static_cast<int64_t>(fg * pk + j) * a.ofstride +
+                          static_cast<int64_t>(r * B + i) * a.opitch + static_cast<int64_t>(px0) * C + scopy,
+                      buf + j * (PACKED ? a.slot_stride : 0) + i * srb + scopy, span);
       }
     }
   }
@@ -1286,11 +1316,10 @@ __global__ void __launch_bounds__(kConsumers) k_expand_uany(const __grid_constan
     const int span = vbytes - scopy;
     if (span > 0) {
       const int rows = min(B, g.M - r * B);
-      for (int e = t; e < rows * span; e += kConsumers) {
-        const int i = e / span, x = scopy + (e - i * span);
-        a.out[static_cast<int64_t>(f) * a.ofstride + static_cast<int64_t>(r * B + i) * a.opitch +
-              static_cast<int64_t>(px0) * C + x] = smem[i * ROWB + x];
-      }
+      for (int i = t; i < rows; i += kConsumers)  // one row per thread
+        copy_row_tail(a.out + static_cast<int64_t>(f) * a.ofstride + static_cast<int64_t>(r * B + i) * a.opitch +
+                          static_cast<int64_t>(px0) * C + scopy,
+                      smem + i * ROWB + scopy, span);
     }
   }
   if (t == 0) bulk_wait_read_all();
@@ -1390,11 +1419,10 @@ __global__ void __launch_bounds__(kConsumers) k_expand_aany(const __grid_constan
     const int span = vbytes - scopy;
     if (span > 0) {
       const int rows = min(B, g.M - r * B);
-      for (int e = t; e < rows * span; e += kConsumers) {
-        const int i = e / span, x = scopy + (e - i * span);
-        a.out[static_cast<int64_t>(f) * a.ofstride + static_cast<int64_t>(r * B + i) * a.opitch +
-              static_cast<int64_t>(px0) * C + x] = smem[i * ROWB + x];
-      }
+      for (int i = t; i < rows; i += kConsumers)  // one row per thread
+        copy_row_tail(a.out + static_cast<int64_t>(f) * a.ofstride + static_cast<int64_t>(r * B + i) * a.opitch +
+                          static_cast<int64_t>(px0) * C + scopy,
+                      smem + i * ROWB + scopy, span);
     }
   }
   if (t == 0) bulk_wait_read_all();
