@@ -286,6 +286,19 @@ int dppx_group_reassemble(dppx_group* group, const dppx_frames_desc* desc, const
 /* Launch counts and transfer bytes summed over the workers; device_ms is the max. */
 int dppx_group_get_stats(dppx_group* group, dppx_kernel_stats* out);
 
+/* The batch runner's per-file work (run_single, cli.cpp:93-173) for F frames
+ * on ONE upload: pixelize (mode 0 uniform / 1 adaptive / 2 Algorithm 1), then,
+ * where both images already live, the reconstruct check -- the statistics just
+ * produced, expanded again (broadcast_means / reassemble), must equal the
+ * emitted frames: recon_ok[f] = 1 / 0 (always 1 for mode 2, which keeps no
+ * statistics) -- and mse / ssim of input vs emitted frames (ssim_out may be
+ * NULL; frames smaller than 7 x 7 get no ssim). Outputs as the host entry
+ * points above (stats / lens / out; stats may be NULL for mode 2). */
+int dppx_pixelize_checked(dppx_ctx* ctx, int32_t mode, const dppx_frames_desc* desc, const uint8_t* img,
+                          const uint8_t* mask, const dppx_privacy_params* params, const dppx_noise* noise,
+                          uint8_t* stats, int64_t payload_stride, uint32_t* payload_len, uint8_t* out,
+                          uint8_t* recon_ok, double* mse_out, double* ssim_out);
+
 /* classify_regions (adaptive.cpp:34-65) of F masks (desc mask fields; channels
  * ignored): per-frame G float mask means at mask_means + f*G. */
 int dppx_classify_regions(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* mask,

@@ -157,6 +157,8 @@ ABI = {
     "dppx_reconstruct_record": (C.c_int, [_ctxp, _vp, C.c_size_t, _vp, C.c_size_t]),
     "dppx_debug_device_laplace": (C.c_int, [_ctxp, C.c_uint64, _vp, C.c_int32, C.c_double, _vp]),
     "dppx_debug_lg2_max_error": (C.c_int, [_ctxp, C.POINTER(C.c_double)]),
+    "dppx_pixelize_checked": (C.c_int, [_ctxp, C.c_int32, _descp, _vp, _vp, _pp, _np, _vp, C.c_int64, _vp,
+                                        _vp, _vp, _vp, _vp]),
     "dppx_group_create": (C.c_int, [C.POINTER(C.c_int32), C.c_int32, C.POINTER(_vp)]),
     "dppx_group_destroy": (None, [_vp]),
     "dppx_group_size": (C.c_int32, [_vp]),
@@ -506,6 +508,31 @@ class Context:
         del keep
         return [bytes(buf[i, : lens[i]]) for i in range(F * Cn)], out
 
+    def pixelize_checked(self, frames, masks, params: PrivacyParams, mode="adaptive",
+                         noise=NOISE_NONE, seeds=None):
+        """dppx_pixelize_checked: pixelize + on-device reconstruct check + mse / ssim
+        from one upload. Returns (stats, lens, image, recon_ok, mse, ssim)."""
+        frames = np.ascontiguousarray(frames, dtype=np.uint8)
+        F, M, N, Cn = _frames_shape(frames)
+        m = {"uniform": 0, "adaptive": 1, "reference": 2}[mode]
+        g = grid_dims(M, N, params.b)
+        stride = ((adaptive_payload_capacity(M, N, params.b, params.n) + 3) & ~3) if m == 1 else g.grid_count()
+        stats = np.zeros((F * Cn, stride), np.uint8)
+        lens = np.zeros(F * Cn, np.uint32)
+        out = np.zeros_like(frames)
+        ok = np.zeros(F, np.uint8)
+        mse = np.zeros(F * Cn, np.float64)
+        ssim = np.zeros(F * Cn, np.float64)
+        mk = None if m != 1 else np.ascontiguousarray(masks, dtype=np.uint8).reshape(F, M, N)
+        nz, keep = self._noise(noise, seeds)
+        d = _desc(M, N, Cn, F)
+        self._check(_lib.dppx_pixelize_checked(self._h, m, C.byref(d), _ptr(frames), _ptr(mk), C.byref(params),
+                                               C.byref(nz), _ptr(stats), stride, _ptr(lens), _ptr(out),
+                                               _ptr(ok), _ptr(mse), _ptr(ssim) if M >= 7 and N >= 7 else None),
+                    "pixelize_checked")
+        del keep
+        return stats, lens, out, ok, mse, ssim
+
     def reconstruct_record(self, record: bytes) -> np.ndarray:
         """dppx_reconstruct_record: decode a .dppx record and expand it on the GPU."""
         info = RecordInfo()
@@ -699,7 +726,7 @@ def _group_unsupported(name):
 
 for _name in ("stream", "set_stream", "set_chunk_frames", "set_exact_noise", "set_out_pad_scratch",
               "lg2_max_error", "pixelize_reference", "pixelize_adaptive_variance",
-              "reconstruct_record", "classify_regions", "metrics", "device_laplace",
+              "reconstruct_record", "classify_regions", "metrics", "device_laplace", "pixelize_checked",
               "pixelize_adaptive_dev", "pixelize_uniform_dev", "pixelize_adaptive_variance_dev",
               "pixelize_uniform_sweep_dev",
               "reassemble_dev", "broadcast_means_dev", "synth_frames_dev"):

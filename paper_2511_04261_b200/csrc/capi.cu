@@ -62,6 +62,8 @@ struct MetricArgs {
 cudaError_t launch_metrics(const MetricArgs& m, bool ssim, cudaStream_t s);
 cudaError_t launch_repitch(uint8_t* dst, int64_t dpitch, const uint8_t* src, int64_t spitch,
                            int64_t width, int64_t rows, cudaStream_t s);
+cudaError_t launch_frames_equal(const uint8_t* a, const uint8_t* b, int64_t pitch, int64_t fstride,
+                                int64_t width, int rows, int frames, uint32_t* eq, cudaStream_t s);
 cudaError_t launch_debug_laplace(uint64_t mixed, const uint32_t* keys, int count, double sigma,
                                  double* out, cudaStream_t s);
 constexpr int kSweepMaxLevels = 4;
@@ -146,6 +148,7 @@ struct dppx_ctx {
                       // while chunk ci's D2H is still reading its output
   DevBuf var_flags, var_stage;  // fused variance classification staging
   DevBuf sweep_sums[4];         // K1s level sums (one-read sweep)
+  DevBuf check_img, check_eq;   // dppx_pixelize_checked: rebuilt frames, per-frame flags
   uint64_t* sd_pinned[2] = {nullptr, nullptr};
   size_t sd_pinned_n[2] = {0, 0};
   cudaEvent_t in_done[2] = {}, comp_done[2] = {}, out_done[2] = {};
@@ -989,6 +992,56 @@ int h2d_frames(dppx_ctx* ctx, uint8_t* dst, int64_t dpitch, int64_t dfs, const u
     CUDA_TRY(ctx, cudaEventRecord(ctx->piece_ev[s], st));
     r0 = r1;
   }
+  return DPPX_OK;
+}
+
+// Device -> host copy of F frames into a caller buffer: one DMA when the
+// destination is pinned; otherwise ~16 MB pieces land in the ctx's two pinned
+// piece buffers in turn and host threads copy each piece out while the next
+// one is in flight.
+int d2h_frames(dppx_ctx* ctx, uint8_t* dst, int64_t dpitch, int64_t dfs, const uint8_t* src,
+               int64_t spitch, int64_t sfs, int64_t row, int M, int F, cudaStream_t st) {
+  if (host_pinned(dst)) {
+    CUDA_TRY(ctx, copy_frames(dst, dpitch, dfs, src, spitch, sfs, row, M, F, cudaMemcpyDeviceToHost, st));
+    return DPPX_OK;
+  }
+  if (!ctx->packer) ctx->packer = dppx::mask_packer_create(0);
+  const int64_t rows = static_cast<int64_t>(F) * M;
+  const int64_t per = std::max<int64_t>(1, (int64_t{16} << 20) / spitch);
+  for (int s = 0; s < 2; ++s) {
+    if (int rc = grow_pinned(ctx, ctx->piece[s], ctx->piece_n[s], static_cast<size_t>(per * spitch))) return rc;
+    if (!ctx->piece_ev[s]) CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->piece_ev[s], cudaEventDisableTiming));
+  }
+  const bool linear = sfs == static_cast<int64_t>(M) * spitch;
+  int64_t pending_r0[2] = {-1, -1}, pending_r1[2] = {0, 0};
+  auto drain = [&](int s) -> int {
+    if (pending_r0[s] < 0) return DPPX_OK;
+    CUDA_TRY(ctx, cudaEventSynchronize(ctx->piece_ev[s]));
+    const int64_t a0 = pending_r0[s], a1 = pending_r1[s];
+    const uint8_t* buf = ctx->piece[s];
+    dppx::pool_for(ctx->packer, a1 - a0, [&](int64_t x, int64_t y) {
+      for (int64_t r = a0 + x; r < a0 + y; ++r)
+        std::memcpy(dst + (r / M) * dfs + (r % M) * dpitch, buf + (r - a0) * spitch, static_cast<size_t>(row));
+    });
+    pending_r0[s] = -1;
+    return DPPX_OK;
+  };
+  int64_t r0 = 0;
+  for (int k = 0; r0 < rows; ++k) {
+    int64_t r1 = std::min(rows, r0 + per);
+    if (!linear) r1 = std::min(r1, (r0 / M + 1) * M);
+    const int s = k & 1;
+    if (int rc = drain(s)) return rc;  // the piece buffer's previous rows leave first
+    const uint8_t* s0 = src + (r0 / M) * sfs + (r0 % M) * spitch;
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->piece[s], s0, static_cast<size_t>(r1 - r0 - 1) * spitch + row,
+                                  cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->piece_ev[s], st));
+    pending_r0[s] = r0;
+    pending_r1[s] = r1;
+    r0 = r1;
+  }
+  for (int k = 0; k < 2; ++k)
+    if (int rc = drain(k)) return rc;
   return DPPX_OK;
 }
 
@@ -2014,6 +2067,8 @@ void dppx_ctx_destroy(dppx_ctx* ctx) {
     if (b->p) cudaFree(b->p);
   for (DevBuf& b : ctx->sweep_sums)
     if (b.p) cudaFree(b.p);
+  for (DevBuf* b : {&ctx->check_img, &ctx->check_eq})
+    if (b->p) cudaFree(b->p);
   for (int s = 0; s < 2; ++s) {
     DevBuf* sb[] = {&ctx->img[s], &ctx->mask[s], &ctx->out[s], &ctx->stats[s], &ctx->lens[s],
                     &ctx->inj[s], &ctx->sd[s], &ctx->dense[s], &ctx->dense_out[s], &ctx->dense_mask[s]};
@@ -2622,6 +2677,119 @@ int dppx_metrics(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* a, con
                  double* mse_out, double* ssim_out) {
   if (int rc = check_ctx(ctx)) return rc;
   return metric_host(ctx, d, a, b, mse_out, ssim_out);
+}
+
+int dppx_pixelize_checked(dppx_ctx* ctx, int32_t mode, const dppx_frames_desc* d, const uint8_t* img,
+                          const uint8_t* mask, const dppx_privacy_params* pp, const dppx_noise* nz,
+                          uint8_t* stats, int64_t stride, uint32_t* lens, uint8_t* out, uint8_t* recon_ok,
+                          double* mse, double* ssim) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (mode < 0 || mode > 2) return set_err(ctx, DPPX_ERR_INVALID, "unknown mode");
+  const bool adaptive = mode == 1, reference = mode == 2;
+  if (int rc = check_params(ctx, pp, adaptive)) return rc;
+  if (int rc = check_desc(ctx, d, adaptive, true)) return rc;
+  BatchGeom g;
+  if (int rc = geometry(ctx, d->height, d->width, d->channels, d->frames, pp->b, adaptive ? pp->n : 1, &g,
+                        !reference))
+    return rc;
+  const int F = g.F, C = g.C, M = g.M, N = g.N;
+  if (F == 0) return DPPX_OK;
+  if (F > 65535) return set_err(ctx, DPPX_ERR_INVALID, "at most 65535 frames per call");
+  if (!img || !out || !mse || (!reference && !stats) || (adaptive && !mask))
+    return set_err(ctx, DPPX_ERR_INVALID, "null image/output/statistics/mask/mse pointer");
+  const size_t G = static_cast<size_t>(g.G);
+  const size_t cap = adaptive ? dppx_adaptive_payload_capacity(M, N, g.b, g.n) : G;
+  if (adaptive && stride < static_cast<int64_t>(cap))
+    return set_err(ctx, DPPX_ERR_INVALID, "payload_stride too small");
+  const int64_t row = static_cast<int64_t>(N) * C;
+  const int64_t dpitch = round_up(row, 16), dfs = dpitch * M;
+  const int64_t dmpitch = round_up(N, 16), dmfs = dmpitch * M;
+  const int64_t dstride = adaptive ? round_up(static_cast<int64_t>(cap), 16) : static_cast<int64_t>(G);
+  const int P = F * C;
+  if (ensure(ctx, ctx->img[0], static_cast<size_t>(dfs) * F)) return DPPX_ERR_OOM;
+  if (ensure(ctx, ctx->out[0], static_cast<size_t>(dfs) * F)) return DPPX_ERR_OOM;
+  if (adaptive && ensure(ctx, ctx->mask[0], static_cast<size_t>(dmfs) * F)) return DPPX_ERR_OOM;
+  if (ensure(ctx, ctx->stats[0], static_cast<size_t>(dstride) * P)) return DPPX_ERR_OOM;
+  if (ensure(ctx, ctx->lens[0], sizeof(uint32_t) * P)) return DPPX_ERR_OOM;
+  if (!reference && ensure(ctx, ctx->check_img, static_cast<size_t>(dfs) * F)) return DPPX_ERR_OOM;
+  if (ensure(ctx, ctx->check_eq, sizeof(uint32_t) * F)) return DPPX_ERR_OOM;
+  uint8_t* dimg = static_cast<uint8_t*>(ctx->img[0].p);
+  uint8_t* dout = static_cast<uint8_t*>(ctx->out[0].p);
+  uint8_t* dmask = static_cast<uint8_t*>(ctx->mask[0].p);
+  uint8_t* dstats = static_cast<uint8_t*>(ctx->stats[0].p);
+  uint32_t* dlens = static_cast<uint32_t*>(ctx->lens[0].p);
+  uint32_t* deq = static_cast<uint32_t*>(ctx->check_eq.p);
+  cudaStream_t st = ctx->stream;
+  // the previous host call's copies out of the staging buffers are done
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->s_out));
+  // ---- one upload of frames (and masks) ----
+  if (int rc = h2d_frames(ctx, dimg, dpitch, dfs, img, d->pitch, d->frame_stride, row, M, F, st)) return rc;
+  ctx->kstats.h2d_bytes += static_cast<uint64_t>(row) * M * F;
+  if (adaptive) {
+    if (int rc = h2d_frames(ctx, dmask, dmpitch, dmfs, mask, d->mask_pitch, d->mask_frame_stride, N, M, F, st))
+      return rc;
+    ctx->kstats.h2d_bytes += static_cast<uint64_t>(N) * M * F;
+  }
+  dppx_frames_desc dd = *d;
+  dd.pitch = dpitch;
+  dd.frame_stride = dfs;
+  dd.mask_pitch = dmpitch;
+  dd.mask_frame_stride = dmfs;
+  dd.out_pitch = dpitch;
+  dd.out_frame_stride = dfs;
+  {
+    struct PadScratch {  // dout / check_img are the ctx's own buffers
+      dppx_ctx* c;
+      bool prev;
+      ~PadScratch() { c->out_pad_scratch = prev; }
+    } pad_scope{ctx, ctx->out_pad_scratch};
+    ctx->out_pad_scratch = true;
+    PixOpts po;
+    po.partial = reference;
+    if (int rc = pixelize_dev(ctx, &dd, dimg, dmask, pp, nz, nullptr, dstats, dstride, adaptive ? dlens : nullptr,
+                              dout, adaptive, ctx->seeds, ctx->seeds_pinned, ctx->seeds_pinned_n, ctx->seeds_ev,
+                              true, po))
+      return rc;
+    // ---- reconstruct check on the device: the statistics just produced,
+    // expanded again, must equal the emitted frames (cli.cpp:135-146) ----
+    CUDA_TRY(ctx, cudaMemsetAsync(deq, 0xFF, sizeof(uint32_t) * F, st));
+    if (!reference) {
+      uint8_t* drb = static_cast<uint8_t*>(ctx->check_img.p);
+      if (int rc = expand_dev(ctx, &dd, dstats, dstride, adaptive ? dlens : nullptr, g.b, g.n, drb, adaptive))
+        return rc;
+      CUDA_TRY(ctx, launch_frames_equal(dout, drb, dpitch, dfs, row, M, F, deq, st));
+    }
+  }
+  // ---- mse / ssim of input vs emitted frames, both resident (cli.cpp:164-171) ----
+  dppx_frames_desc dm = dd;  // a = input (pitch), b = output (out_pitch)
+  if (int rc = metric_dev(ctx, &dm, dimg, dout, false, mse)) return rc;
+  if (ssim && M >= 7 && N >= 7)
+    if (int rc = metric_dev(ctx, &dm, dimg, dout, true, ssim)) return rc;
+  // ---- results out ----
+  if (int rc = d2h_frames(ctx, out, d->out_pitch, d->out_frame_stride, dout, dpitch, dfs, row, M, F, st))
+    return rc;
+  ctx->kstats.d2h_bytes += static_cast<uint64_t>(row) * M * F;
+  std::vector<uint32_t> eq(static_cast<size_t>(F));
+  CUDA_TRY(ctx, cudaMemcpyAsync(eq.data(), deq, sizeof(uint32_t) * F, cudaMemcpyDeviceToHost, st));
+  std::vector<uint32_t> ln(static_cast<size_t>(P), static_cast<uint32_t>(G));
+  if (adaptive)
+    CUDA_TRY(ctx, cudaMemcpyAsync(ln.data(), dlens, sizeof(uint32_t) * P, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  if (!reference) {
+    size_t w = 0;
+    for (int q = 0; q < P; ++q) w = std::max<size_t>(w, std::min<size_t>(ln[q], cap));
+    const int64_t hs = adaptive ? stride : static_cast<int64_t>(G);
+    CUDA_TRY(ctx, cudaMemcpy2D(stats, hs, dstats, dstride, w, static_cast<size_t>(P), cudaMemcpyDeviceToHost));
+    ctx->kstats.d2h_bytes += static_cast<uint64_t>(w) * P;
+    if (adaptive && lens) std::memcpy(lens, ln.data(), sizeof(uint32_t) * P);
+  }
+  // (K0 run on the payloads just produced cannot flag them; if it ever did,
+  // every frame fails the check instead of leaving the status set)
+  const bool corrupt = read_status(ctx) != DPPX_OK;
+  if (recon_ok)
+    for (int f = 0; f < F; ++f) recon_ok[f] = (eq[f] != 0 && !corrupt) ? 1 : 0;
+  if (ctx->timing) collect_timings(ctx);
+  return DPPX_OK;
 }
 
 int dppx_mse_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* a, const uint8_t* b,

@@ -1329,6 +1329,39 @@ cudaError_t launch_repitch(uint8_t* dst, int64_t dpitch, const uint8_t* src, int
   return cudaGetLastError();
 }
 
+// Per-frame equality of two pitched frame batches (rows of `width` bytes):
+// eq[f] is cleared when any byte of frame f differs (the batch runner's
+// reconstruct check, cli.cpp:135-146, done where both images already live).
+__global__ void k_frames_equal(const uint8_t* a, const uint8_t* b, int64_t pitch, int64_t fstride,
+                               int64_t width, int rows, uint32_t* eq) {
+  const int f = blockIdx.y;
+  const int64_t w16 = width / 16;
+  const int64_t work = static_cast<int64_t>(rows) * (w16 + 1);
+  bool same = true;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < work;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = e / (w16 + 1), q = e - r * (w16 + 1);
+    const uint8_t* pa = a + f * fstride + r * pitch;
+    const uint8_t* pb = b + f * fstride + r * pitch;
+    if (q < w16) {
+      const uint4 x = reinterpret_cast<const uint4*>(pa)[q], y = reinterpret_cast<const uint4*>(pb)[q];
+      same &= x.x == y.x && x.y == y.y && x.z == y.z && x.w == y.w;
+    } else {
+      for (int64_t k = w16 * 16; k < width; ++k) same &= pa[k] == pb[k];
+    }
+  }
+  if (!__all_sync(0xFFFFFFFFu, same) && (threadIdx.x & 31) == 0) atomicAnd(&eq[f], 0u);
+}
+
+cudaError_t launch_frames_equal(const uint8_t* a, const uint8_t* b, int64_t pitch, int64_t fstride,
+                                int64_t width, int rows, int frames, uint32_t* eq, cudaStream_t s) {
+  if (frames <= 0) return cudaSuccess;
+  const int64_t work = static_cast<int64_t>(rows) * (width / 16 + 1);
+  const int bx = static_cast<int>(std::min<int64_t>((work + 255) / 256, 64));
+  k_frames_equal<<<dim3(bx > 0 ? bx : 1, frames), 256, 0, s>>>(a, b, pitch, fstride, width, rows, eq);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_debug_lg2(unsigned int* out, cudaStream_t s) {
   k_debug_lg2<<<148 * 4, 256, 0, s>>>(out);
   return cudaGetLastError();

@@ -286,7 +286,9 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
   const int n = cfg.mode == BatchMode::adaptive ? cfg.n : 1;
   if (!chunks.empty() && (cfg.emit_image || cfg.emit_record)) make_out_dir(cfg.out_dir);
   if (chunks.empty()) return reports;
+  const auto Tg = tnow();
   dppx_group* grp = shared_group(batch_devices(cfg));
+  if (trace) std::fprintf(stderr, "batch: device group %.1f ms\n", tms(Tg, tnow()));
   const int workers = dppx_group_size(grp);
   const int io_per = std::max(1, io / std::max(1, std::min<int>(workers, static_cast<int>(chunks.size()))));
 
@@ -318,57 +320,51 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
                              : G;
       std::vector<uint8_t> stats(cap * F);
       std::vector<uint32_t> lens(F, static_cast<uint32_t>(G));
+      std::vector<uint8_t> recon_ok(F, 1);
+      std::vector<double> mses(F), ssims(F, std::numeric_limits<double>::quiet_NaN());
+      // One upload per chunk: pixelize, the reconstruct check and mse / ssim
+      // all run where the frames already are (dppx_pixelize_checked).
       const auto tp0 = tnow();
-      int rc;
-      if (cfg.mode == BatchMode::adaptive)
-        rc = dppx_pixelize_adaptive(ctx, &d, in.p, mk.p, &pp, &nz, stats.data(), static_cast<int64_t>(cap),
-                                    lens.data(), out.p);
-      else if (cfg.mode == BatchMode::uniform)
-        rc = dppx_pixelize_uniform(ctx, &d, in.p, &pp, &nz, stats.data(), out.p);
-      else
-        rc = dppx_pixelize_reference(ctx, &d, in.p, &pp, &nz, stats.data(), out.p);
+      const int mode = cfg.mode == BatchMode::adaptive ? 1 : cfg.mode == BatchMode::uniform ? 0 : 2;
+      const int rc = dppx_pixelize_checked(ctx, mode, &d, in.p, cfg.mode == BatchMode::adaptive ? mk.p : nullptr,
+                                           &pp, &nz, stats.data(), static_cast<int64_t>(cap), lens.data(), out.p,
+                                           recon_ok.data(), mses.data(),
+                                           M >= 7 && N >= 7 ? ssims.data() : nullptr);
       const auto tp1 = tnow();
       if (rc != DPPX_OK) raise_status(ctx, rc, "pixelize");
       const double per_ms = tms(tp0, tp1) / F;
-      // ---- records + reconstruct check (cli.cpp:132-146), on the GPU ----
+      // ---- records + reconstruct check (cli.cpp:132-146) ----
+      // reconstruct(decode(encode(stats))) == image: decode must give back the
+      // statistics' exact bytes (checked here), and their expansion equals the
+      // emitted image (checked on the device: recon_ok).
       std::vector<std::vector<uint8_t>> recs(F);
       if (cfg.mode != BatchMode::reference) {
-        std::vector<char> enc_ok(F, 1);
-        parallel_over(F, io_per, [&](int k) {  // header + CRC32 per file
+        std::vector<char> rec_ok(F, 1);
+        parallel_over(F, io_per, [&](int k) {  // header + CRC32 per file, then decode
           recs[k].resize(dppx_record_size(lens[k]));
           size_t len = 0;
-          enc_ok[k] = dppx_encode_record(M, N, cfg.b, n, cfg.mode == BatchMode::adaptive ? 2 : 1,
-                                         stats.data() + k * cap, lens[k], recs[k].data(), recs[k].size(),
-                                         &len) == DPPX_OK;
-        });
-        for (int k = 0; k < F; ++k)
-          if (!enc_ok[k]) throw std::invalid_argument("encode: payload inconsistent");
-        if (cfg.reconstruct_check) {
-          HostBuf rebuilt(plane * F);
-          std::vector<uint8_t> payload(cap * F);
-          std::vector<uint32_t> plen(F);
-          for (int k = 0; k < F; ++k) {  // decode, then rebuild from the decoded payload
-            dppx_record_info info{};
-            if (dppx_decode_record(recs[k].data(), recs[k].size(), &info) != DPPX_OK)
-              throw RecordError(RecordErrorKind::corrupt_record, "decode failed");
-            std::memcpy(payload.data() + k * cap, recs[k].data() + info.payload_offset, info.payload_len);
-            plen[k] = info.payload_len;
+          if (dppx_encode_record(M, N, cfg.b, n, cfg.mode == BatchMode::adaptive ? 2 : 1, stats.data() + k * cap,
+                                 lens[k], recs[k].data(), recs[k].size(), &len) != DPPX_OK) {
+            rec_ok[k] = 0;
+            return;
           }
-          const int rrc = cfg.mode == BatchMode::adaptive
-                              ? dppx_reassemble(ctx, &d, payload.data(), static_cast<int64_t>(cap),
-                                                plen.data(), cfg.b, n, rebuilt.p)
-                              : dppx_broadcast_means(ctx, &d, payload.data(), cfg.b, rebuilt.p);
-          if (rrc != DPPX_OK) raise_status(ctx, rrc, "reconstruct");
-          for (int k = 0; k < F; ++k)
-            if (std::memcmp(rebuilt.p + k * plane, out.p + k * plane, plane) != 0)
-              fail(chunk[k], ConsistencyError("reconstruction does not match the emitted image for " +
-                                              inputs[chunk[k]]));
+          if (!cfg.reconstruct_check) return;
+          dppx_record_info info{};
+          if (dppx_decode_record(recs[k].data(), recs[k].size(), &info) != DPPX_OK ||
+              info.payload_len != lens[k] ||
+              std::memcmp(recs[k].data() + info.payload_offset, stats.data() + k * cap, lens[k]) != 0)
+            rec_ok[k] = 2;
+        });
+        for (int k = 0; k < F; ++k) {
+          if (rec_ok[k] == 0) throw std::invalid_argument("encode: payload inconsistent");
+          if (rec_ok[k] == 2) fail(chunk[k], RecordError(RecordErrorKind::corrupt_record, "decode failed"));
+          else if (cfg.reconstruct_check && !recon_ok[k])
+            fail(chunk[k], ConsistencyError("reconstruction does not match the emitted image for " +
+                                            inputs[chunk[k]]));
         }
       }
-      // ---- metrics on the GPU (cli.cpp:164-171) ----
-      std::vector<double> mses(F), ssims(F, std::numeric_limits<double>::quiet_NaN());
-      if (dppx_metrics(ctx, &d, in.p, out.p, mses.data(), M >= 7 && N >= 7 ? ssims.data() : nullptr) != DPPX_OK)
-        raise_status(ctx, DPPX_ERR_CUDA, "metrics");
+      const auto tr = tnow();
+      const auto tm = tnow();
       // ---- outputs (host threads) ----
       parallel_over(F, io_per, [&](int k) {
         const int i = chunk[k];
@@ -405,8 +401,10 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
         }
       });
       if (trace)
-        std::fprintf(stderr, "batch: chunk %d (%d x %dx%d): stage %.1f pixelize %.1f rest %.1f ms\n", t, F, M, N,
-                     tms(t0, tp0), tms(tp0, tp1), tms(tp1, tnow()));
+        std::fprintf(stderr,
+                     "batch: chunk %d (%d x %dx%d): stage %.1f pixelize %.1f records+check %.1f metrics %.1f "
+                     "outputs %.1f ms\n",
+                     t, F, M, N, tms(t0, tp0), tms(tp0, tp1), tms(tp1, tr), tms(tr, tm), tms(tm, tnow()));
     } catch (const std::exception& err) {
       for (int i : chunk) fail(i, err);
     }

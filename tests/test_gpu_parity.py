@@ -1118,3 +1118,28 @@ def test_single_frame_graph_replays(ctx, M, N, C, b, n, adaptive):
         means, img = ctx.pixelize_uniform(fr, p, dp.NOISE_NONE, None, out=out)
         rm, ri = oracle.pixelize_uniform(fr[0], b, p.sigma, "none", None)
         assert np.array_equal(means, rm) and np.array_equal(out[0], ri)
+
+
+@pytest.mark.parametrize("mode,C", [("adaptive", 1), ("adaptive", 3), ("uniform", 3), ("reference", 1)])
+def test_pixelize_checked_equals_separate_calls(ctx, mode, C):
+    """dppx_pixelize_checked (the batch runner's one-upload per-chunk call):
+    statistics, image, mse and ssim equal the separate host calls, and the
+    on-device reconstruct check passes."""
+    F, M, N, b, n = 5, 83, 131, 16, 4
+    frames = oracle.synth_frames(2, F, M, N, C)
+    masks = oracle.synth_masks(2, F, M, N)
+    p = dp.make_privacy_params(0.5, 16, b, n if mode == "adaptive" else 1)
+    seeds = dp.plane_seeds(3, F, C)
+    stats, lens, img, ok, mse, ssim = ctx.pixelize_checked(frames, masks, p, mode, dp.NOISE_KEYED, seeds)
+    assert ok.all()
+    if mode == "adaptive":
+        pls, ref = ctx.pixelize_adaptive(frames, masks, p, dp.NOISE_KEYED, seeds)
+        assert [bytes(stats[i, :lens[i]]) for i in range(F * C)] == pls
+    elif mode == "uniform":
+        means, ref = ctx.pixelize_uniform(frames, p, dp.NOISE_KEYED, seeds)
+        assert np.array_equal(stats, means)
+    else:
+        _, ref = ctx.pixelize_reference(frames, p, dp.NOISE_KEYED, seeds)
+    assert np.array_equal(img, ref)
+    m2, s2 = ctx.metrics(frames, ref, "both")
+    assert np.array_equal(mse, m2) and np.array_equal(ssim, s2)

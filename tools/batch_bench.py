@@ -64,6 +64,9 @@ def main():
         med = dict(outs[len(outs) // 2])
         med["runs_s"] = [o["seconds"] for o in outs]
         return med
+    if os.environ.get("DPPX_BATCH_TRACE"):  # per-phase trace of one GPU run (stderr)
+        r = subprocess.run([gpu_bin, d_in, d_gpu] + common + ["0"], capture_output=True, text=True)
+        sys.stderr.write(r.stderr)
     ref = run([ref_bin, d_in, d_ref] + common + [threads], args.reps)
     # GPU arm: one untimed warm-up process (file cache, driver), then `reps`
     subprocess.run([gpu_bin, d_in, d_gpu] + common + ["0"], check=True, capture_output=True)
