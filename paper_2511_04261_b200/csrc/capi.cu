@@ -28,6 +28,7 @@ namespace dppx {
 using StatsKernel = void (*)(const CUtensorMap, const CUtensorMap, const StatsArgs);
 StatsKernel select_stats_kernel(int C, int b, int n, bool adaptive, bool packed);
 StatsKernel select_stats_kernel_var(int C, int b, int n);
+StatsKernel select_uniform_b4_rows2(int C);
 cudaError_t launch_gather_stage(const GatherArgs& a, cudaStream_t s);
 int rows_smem_bytes(const BatchGeom& g);
 cudaError_t launch_stats_rows(const StatsArgs& a, size_t smem, cudaStream_t s);
@@ -575,6 +576,16 @@ int run_stats(dppx_ctx* ctx, StatsArgs& a) {
   a.slot_stride = static_cast<int>(round_up(static_cast<int64_t>(g.b) * a.slot_px * g.C, 128));
   k = var ? select_stats_kernel_var(g.C, g.b, g.n)
           : select_stats_kernel(g.C, g.b, g.n, a.adaptive != 0, a.pack > 1);
+  // Uniform b = 4 on wide frames: two cell rows (an 8-row band) per unit.
+  static const bool rows2_off = std::getenv("DPPX_NO_ROWS2") != nullptr;  // A/B knob
+  int rpu = 1;
+  if (k && !var && !a.adaptive && g.b == 4 && a.pack == 1 && a.row_begin == 0 && a.row_count == g.GR &&
+      g.M >= 16 && !rows2_off && !a.partial_borders) {
+    if (StatsKernel k2 = select_uniform_b4_rows2(g.C)) {
+      k = k2;
+      rpu = 2;
+    }
+  }
   if (ctx->force_rows) k = nullptr;
   a.row_slack = a.pitch >= round_up(row_bytes, 16) ? 1 : 0;
   const int box_bytes = a.slot_px * g.C;
@@ -586,23 +597,24 @@ int run_stats(dppx_ctx* ctx, StatsArgs& a) {
   const int64_t in_row = a.row_slack ? round_up(row_bytes, 16) : row_bytes / 16 * 16;
   bool maps = k && aligned && g.F > 0 && box_bytes / 8 <= 256 && g.b <= 256 &&
               (a.pack == 1 || static_cast<int64_t>(a.pack) * a.slot_stride <= stage_bytes) &&
-              encode_frames_map(&tin, a.img, in_row, g.M, g.F, a.pitch, a.fstride, box_bytes, g.b);
+              encode_frames_map(&tin, a.img, in_row, g.M, g.F, a.pitch, a.fstride, box_bytes, g.b * rpu);
   if (maps && a.out)
     maps = encode_frames_map(&tout, a.out, out_map_row_bytes(ctx, row_bytes, a.opitch), g.M, g.F, a.opitch, a.ofstride,
-                              box_bytes, g.b);
+                              box_bytes, g.b * rpu);
   if (maps && !a.out) tout = tin;
   if (maps) {
     a.tensor_in_bytes = static_cast<int>(in_row);
     a.tensor_out_bytes = static_cast<int>(a.out ? out_map_row_bytes(ctx, row_bytes, a.opitch) : row_bytes / 16 * 16);
     a.tiles_per_row = a.pack > 1 ? 1 : (padded_px + tile - 1) / tile;
     const int64_t groups = (g.F + a.pack - 1) / a.pack;
-    const int64_t units = groups * a.row_count * a.tiles_per_row;
+    const int64_t bands = (a.row_count + rpu - 1) / rpu;  // units per frame column (rpu cell rows each)
+    const int64_t units = groups * bands * a.tiles_per_row;
     if (units > 0x7FFFFFFF) return set_err(ctx, DPPX_ERR_INVALID, "batch too large for one launch");
     a.units = static_cast<int>(units);
     a.div_tiles = make_fastdiv(static_cast<uint32_t>(a.tiles_per_row));
-    a.div_rows = make_fastdiv(static_cast<uint32_t>(a.row_count));
+    a.div_rows = make_fastdiv(static_cast<uint32_t>(bands));
     // (128-byte aligned stages: equal to b * tile * C for every b % 4 == 0 kernel)
-    const size_t stage = static_cast<size_t>(round_up(static_cast<int64_t>(g.b) * tile * g.C, 128));
+    const size_t stage = static_cast<size_t>(round_up(static_cast<int64_t>(g.b) * rpu * tile * g.C, 128));
     // Two stages: measured best for every shape on B200 (a 2-deep ring per CTA
     // with 4 CTAs/SM at b = 16 beats 3-4 deep rings with fewer CTAs; see
     // profiles/r01_stage_sweep.md).

@@ -1154,6 +1154,14 @@ cudaError_t launch_gather_stage(const GatherArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+StatsKernel select_uniform_b4_rows2_c1();
+StatsKernel select_uniform_b4_rows2_c3();
+StatsKernel select_uniform_b4_rows2(int C) {
+  if (C == 1) return select_uniform_b4_rows2_c1();
+  if (C == 3) return select_uniform_b4_rows2_c3();
+  return nullptr;
+}
+
 StatsKernel select_stats_kernel(int C, int b, int n, bool adaptive, bool packed) {
   if (!adaptive && n != 1) return nullptr;
   if (adaptive && !packed && (b % 4 != 0 || b == 128)) {  // K1a (DPPX_NO_K1A: K1r, for A/B runs)

@@ -10,6 +10,9 @@ StatsKernel select_stats_tma_c1(int b, int n, bool adaptive, bool packed) {
 
 StatsKernel select_stats_var_c1(int b, int n) { return pick_var<1>(b, n); }
 
+// Uniform b = 4, two cell rows per unit (wide frames).
+StatsKernel select_uniform_b4_rows2_c1() { return k_stats_tma<1, 1, 1, false, false, false, 2>; }
+
 StatsKernel select_uniform_any_c1(int b) { return pick_uniform_any<1>(b); }
 
 StatsKernel select_adaptive_any_c1(int b, int n) { return pick_adaptive_any<1>(b, n); }

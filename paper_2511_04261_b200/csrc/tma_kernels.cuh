@@ -347,11 +347,17 @@ __device__ __forceinline__ void group_values(const StatsArgs& a, const DrawEnv& 
   }
 }
 
-template <int C, int B4, int NSUB, bool ADAPTIVE, bool PACKED, bool VAR = false>
-__global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? 6 : 0)
+// RPU: cell rows per unit. Uniform b = 4 stages two cell rows (an 8-row band)
+// per unit (RPU = 2) so the per-unit work -- claim, metadata, mirror fill,
+// barriers, store bookkeeping -- is paid once per 6 draws per lane instead of
+// 3 (the b = 4 kernel is instruction-bound, profiles/r02p_k1_uniform_b4_full.md).
+template <int C, int B4, int NSUB, bool ADAPTIVE, bool PACKED, bool VAR = false, int RPU = 1>
+__global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU > 1 ? 5 : 6) : 0)
     k_stats_tma(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
                 const StatsArgs a) {
   constexpr int B = 4 * B4;
+  constexpr int BR = B * RPU;  // rows of a unit's band
+  static_assert(RPU == 1 || (!ADAPTIVE && !PACKED && !VAR), "multi-row units: uniform wide frames");
   constexpr int SB = B / NSUB;
   constexpr int SB4 = SB / 4;
   // Subcell sides that are not a multiple of 4 px (b = 24 n = 4: 6 px; 2 or
@@ -364,7 +370,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? 6 : 0)
   constexpr int LPW = (32 / B4) * B4;
   constexpr int TILE = 4 * (kConsumers / 32) * LPW;
   constexpr int ROWB = TILE * C;
-  constexpr uint32_t STAGE = B * ROWB;
+  constexpr uint32_t STAGE = BR * ROWB;
   // (SB >= 2: a strip meets at most two subcells.)
   static_assert(B4 <= 32 && (STR ? (SB >= 2 && ADAPTIVE && !VAR && !PACKED) : B4 % SB4 == 0),
                 "fast-path geometry");
@@ -404,8 +410,8 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? 6 : 0)
       mbar_wait(&done_bar[s], use & 1);        // every lane acquires the smem writes
       if (a.out) {
         const int uu = stage_unit[s];
-        store_tail<C, B, PACKED, TILE>(a, uu, smem + s * STAGE, lane);
-        if (lane == 0) store_unit<C, B, PACKED, TILE>(a, &tm_out, uu, smem + s * STAGE);
+        store_tail<C, BR, PACKED, TILE>(a, uu, smem + s * STAGE, lane);
+        if (lane == 0) store_unit<C, BR, PACKED, TILE>(a, &tm_out, uu, smem + s * STAGE);
       }
       __syncwarp();
     };
@@ -431,7 +437,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? 6 : 0)
         if (u < 0)
           mbar_arrive_expect_tx(&full_bar[s], 0);
         else
-          load_unit<C, B, PACKED, TILE>(a, &tm_in, u, smem + s * STAGE, &full_bar[s]);
+          load_unit<C, BR, PACKED, TILE>(a, &tm_in, u, smem + s * STAGE, &full_bar[s]);
       }
       u = __shfl_sync(0xFFFFFFFFu, u, 0);
       if (u < 0) break;
@@ -551,7 +557,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? 6 : 0)
     const uint32_t slot_s = cur.rowpre + (cur.info >> 1);
     const uint32_t S_tot = cur.stot;
     const int vbytes = valid_bytes<C, PACKED, TILE>(a, p.px0);
-    const int copy = staged_bytes<C, B, PACKED, TILE>(a, p);  // bytes per row the producer staged
+    const int copy = staged_bytes<C, BR, PACKED, TILE>(a, p);  // bytes per row the producer staged
     const int need = min(slot_px<PACKED, TILE>(a), g.GC * B - p.px0) * C;
     const int nf = PACKED ? min(a.pack, g.F - p.fg * a.pack) : 1;
     uint64_t cs[C];
@@ -585,12 +591,12 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? 6 : 0)
       const int fs = min(copy, vbytes);
       if (fs < need) {
         constexpr int kLanes = 4;  // consumer threads per slot row
-        const int rows_total = nf * B;
+        const int rows_total = nf * BR;
         for (int pr = t / kLanes; pr < rows_total; pr += kConsumers / kLanes) {
-          const int j = pr / B, i = pr - j * B;  // B is a compile-time power of two
+          const int j = pr / BR, i = pr - j * BR;  // BR is a compile-time power of two
           uint8_t* rowp = st + j * (PACKED ? a.slot_stride : 0) + i * srb;
           const int frame = p.fg * units_pack<PACKED>(a) + j;
-          const int srow = reflect_index(p.r * B + i, g.M);
+          const int srow = reflect_index(p.r * BR + i, g.M);
           const uint8_t* grow = a.img + static_cast<int64_t>(frame) * a.fstride +
                                 static_cast<int64_t>(srow) * a.pitch;
           for (int x = fs + (t % kLanes); x < need; x += kLanes) {
@@ -873,7 +879,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? 6 : 0)
           }
         }
       }
-    } else {
+    } else if constexpr (RPU == 1) {
 #pragma unroll
       for (int i = 0; i < B; ++i) accumulate_row<C>(mystrip + i * srb, tot);
       // Next unit's metadata: requested here (after the staged rows are
@@ -882,7 +888,49 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? 6 : 0)
       next = load_meta(k + 1);
     }
 
+    if constexpr (RPU > 1) {
+      // Uniform, RPU cell rows of this band: the same per-cell work as below,
+      // once per cell row (a band's last rows may lie past the grid: skipped).
+      next = load_meta(k + 1);
+#pragma unroll 1
+      for (int q = 0; q < RPU; ++q) {
+        const int rq = p.r * RPU + q;
+        const bool rok = active && rq < a.row_begin + a.row_count;
+        uint32_t tq[C];
+#pragma unroll
+        for (int ch = 0; ch < C; ++ch) tq[ch] = 0;
+#pragma unroll
+        for (int i = 0; i < B; ++i) accumulate_row<C>(mystrip + (q * B + i) * srb, tq);
+#pragma unroll
+        for (int ch = 0; ch < C; ++ch) tq[ch] = group_sum<B4>(tq[ch]);
+        uint64_t csq[C];
+#pragma unroll
+        for (int ch = 0; ch < C; ++ch)
+          csq[ch] = a.noise.kind == DPPX_NOISE_KEYED ? key_cell(cur.seed[ch], rq, cell) : 0ull;
+        uint32_t val[C];
+        group_values<C, B4>(a, env_cell, rok, tq, csq, f, rq, cell, 0, 0, val);
+        if (rok) {
+          if (lic == 0) {
+            const int64_t off = static_cast<int64_t>(rq) * g.GC + cell;
+#pragma unroll
+            for (int ch = 0; ch < C; ++ch)
+              a.stats[static_cast<int64_t>(f * C + ch) * a.sstride + off] = static_cast<uint8_t>(val[ch]);
+          }
+          if (emit) {
+            uint32_t w[C];
+            pattern_words<C>(val, w);
+#pragma unroll
+            for (int i = 0; i < B; ++i)
+#pragma unroll
+              for (int qq = 0; qq < C; ++qq)
+                reinterpret_cast<uint32_t*>(mystrip + (q * B + i) * srb)[qq] = w[qq];
+          }
+        }
+      }
+    }
+
     // whole cell (uniform, or adaptive simple): reduce over B4 strips.
+    if constexpr (RPU == 1) {
 #pragma unroll
     for (int ch = 0; ch < C; ++ch) tot[ch] = group_sum<B4>(tot[ch]);
     {
@@ -913,6 +961,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? 6 : 0)
         }
       }
     }
+    }  // RPU == 1
 
     fence_proxy_async_smem();
     mbar_arrive(&done_bar[s]);
