@@ -181,6 +181,10 @@ struct dppx_ctx {
   // single-frame host calls replayed as CUDA graphs (host_single_graph)
   struct FrameGraph;
   std::vector<FrameGraph*> graphs;
+  // Bumped whenever a ctx buffer is (re)allocated: a captured graph holds the
+  // addresses of the ctx buffers it touches, so graphs older than the last
+  // (re)allocation are dropped, never replayed.
+  uint64_t alloc_gen = 0;
   uint64_t* gseeds_pinned = nullptr;  // mixed plane seeds of the next replay
   DevBuf gseeds;
   uint8_t* gstats_pinned = nullptr;   // statistics / lengths land here, then the caller's buffers
@@ -214,6 +218,7 @@ struct dppx_ctx::FrameGraph {
   uint64_t launches[DPPX_K_COUNT] = {};
   uint64_t h2d = 0, d2h = 0;
   uint64_t last_use = 0;
+  uint64_t gen = 0;  // ctx->alloc_gen when captured
   ~FrameGraph() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
@@ -249,6 +254,7 @@ int ensure(dppx_ctx* ctx, DevBuf& b, size_t bytes, bool zero = false) {
   if (b.p) cudaFree(b.p);
   b.p = nullptr;
   b.bytes = 0;
+  ++ctx->alloc_gen;  // (invalidates captured graphs, see host_single_graph)
   const size_t sz = std::max(bytes, static_cast<size_t>(256));
   CUDA_TRY(ctx, cudaMalloc(&b.p, sz));
   b.bytes = sz;
@@ -1248,6 +1254,7 @@ int host_single_zerocopy(dppx_ctx* ctx, bool adaptive, const dppx_frames_desc* d
   const size_t gst = static_cast<size_t>(dstride) * C + 16;
   if (ctx->gstats_pinned_n < gst) {
     if (ctx->gstats_pinned) CUDA_TRY(ctx, cudaFreeHost(ctx->gstats_pinned));
+    ++ctx->alloc_gen;
     ctx->gstats_pinned = nullptr;
     ctx->gstats_pinned_n = 0;
     CUDA_TRY(ctx, cudaHostAlloc(reinterpret_cast<void**>(&ctx->gstats_pinned), gst, cudaHostAllocMapped));
@@ -1305,6 +1312,10 @@ int host_single_graph(dppx_ctx* ctx, bool adaptive, const dppx_frames_desc* d, c
   if (const char* env = std::getenv("DPPX_GRAPH_BANDS")) nb = std::max(1, std::atoi(env));
   nb = std::max(1, std::min({nb, g.GR / 2 > 0 ? g.GR / 2 : 1, dppx_ctx::kMaxBands}));
   dppx_ctx::FrameGraph* fgp = nullptr;
+  if (!ctx->graphs.empty() && ctx->graphs.front()->gen != ctx->alloc_gen) {
+    for (auto* c : ctx->graphs) delete c;  // buffers they reference were reallocated
+    ctx->graphs.clear();
+  }
   for (auto* c : ctx->graphs)
     if (c->op == (adaptive ? 1 : 0) && c->M == M && c->N == N && c->C == C && c->b == b && c->n == g.n &&
         c->kind == kind && c->exact == (ctx->exact_noise ? 1 : 0) && c->nb == nb &&
@@ -1327,6 +1338,7 @@ int host_single_graph(dppx_ctx* ctx, bool adaptive, const dppx_frames_desc* d, c
     const size_t gst = static_cast<size_t>(dstride) * C + 16;
     if (ctx->gstats_pinned_n < gst) {
       if (ctx->gstats_pinned) CUDA_TRY(ctx, cudaFreeHost(ctx->gstats_pinned));
+      ++ctx->alloc_gen;
       ctx->gstats_pinned = nullptr;
       ctx->gstats_pinned_n = 0;
       CUDA_TRY(ctx, cudaHostAlloc(reinterpret_cast<void**>(&ctx->gstats_pinned), gst, cudaHostAllocMapped));
@@ -1494,6 +1506,13 @@ int host_single_graph(dppx_ctx* ctx, bool adaptive, const dppx_frames_desc* d, c
     ng->cur[0] = img;
     ng->cur[1] = mask;
     ng->cur[2] = out;
+    // every buffer the graph references was allocated before the capture; if
+    // the capture itself had to grow one, older graphs are stale now
+    if (!ctx->graphs.empty() && ctx->graphs.front()->gen != ctx->alloc_gen) {
+      for (auto* c : ctx->graphs) delete c;
+      ctx->graphs.clear();
+    }
+    ng->gen = ctx->alloc_gen;
     ctx->graphs.push_back(ng);
     fgp = ng;
   }

@@ -1112,6 +1112,25 @@ def test_single_frame_graph_replays(ctx, M, N, C, b, n, adaptive):
             rm, ri = oracle.pixelize_uniform(fr[0], b, p.sigma, "keyed", seeds)
             assert np.array_equal(means, rm), it
         assert np.array_equal(out[0], ri), it
+    # a larger call grows the ctx buffers the graph captured: the graph must be
+    # dropped and recaptured, never replayed on freed memory
+    big = oracle.synth_frames(9, 3, 1080, 1920, C)
+    big_m = oracle.synth_masks(9, 3, 1080, 1920)
+    if adaptive:
+        ctx.pixelize_adaptive(big, big_m, p, dp.NOISE_KEYED, dp.plane_seeds(5, 3, C))
+    else:
+        ctx.pixelize_uniform(big, p, dp.NOISE_KEYED, dp.plane_seeds(5, 3, C))
+    fr, mk, out = bufs[1]
+    seeds = dp.plane_seeds(77, 1, C)
+    if adaptive:
+        pls, img = ctx.pixelize_adaptive(fr, mk, p, dp.NOISE_KEYED, seeds, out=out)
+        rp, ri = oracle.pixelize_adaptive(fr[0], mk[0], b, n, p.sigma, p.sigma_sub, "keyed", seeds)
+        assert pls == rp
+    else:
+        means, img = ctx.pixelize_uniform(fr, p, dp.NOISE_KEYED, seeds, out=out)
+        rm, ri = oracle.pixelize_uniform(fr[0], b, p.sigma, "keyed", seeds)
+        assert np.array_equal(means, rm)
+    assert np.array_equal(out[0], ri)
     # no noise through the same shape
     fr, mk, out = bufs[0]
     if not adaptive:
