@@ -128,19 +128,21 @@ struct HostBuf {  // pageable host batch buffer (no zero fill)
 
 // Process-wide device group per device list (contexts and worker threads are
 // created once; run_batch calls reuse them).
+// The groups live until the process exits and are deliberately not destroyed
+// by static destructors (the CUDA runtime may already be torn down by then).
 dppx_group* shared_group(const std::vector<int>& want) {
   static std::mutex mu;
-  static std::map<std::vector<int>, std::unique_ptr<dppx_group, void (*)(dppx_group*)>> groups;
+  static auto* groups = new std::map<std::vector<int>, dppx_group*>();
   std::lock_guard<std::mutex> lk(mu);
-  auto it = groups.find(want);
-  if (it != groups.end()) return it->second.get();
+  auto it = groups->find(want);
+  if (it != groups->end()) return it->second;
   dppx_group* g = nullptr;
   const int rc = want.empty() ? dppx_group_create(nullptr, 0, &g)
                               : dppx_group_create(want.data(), static_cast<int32_t>(want.size()), &g);
   if (rc != DPPX_OK)
     throw std::runtime_error("dppix: no usable sm_100 GPU for the batch runner (status " +
                              std::to_string(rc) + ")");
-  groups.emplace(want, std::unique_ptr<dppx_group, void (*)(dppx_group*)>(g, &dppx_group_destroy));
+  groups->emplace(want, g);
   return g;
 }
 
