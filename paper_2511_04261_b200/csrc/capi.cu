@@ -185,6 +185,7 @@ struct dppx_ctx {
   // addresses of the ctx buffers it touches, so graphs older than the last
   // (re)allocation are dropped, never replayed.
   uint64_t alloc_gen = 0;
+  uint64_t graph_tick = 0;  // LRU clock of the graph cache
   uint64_t* gseeds_pinned = nullptr;  // mixed plane seeds of the next replay
   DevBuf gseeds;
   uint8_t* gstats_pinned = nullptr;   // statistics / lengths land here, then the caller's buffers
@@ -1517,8 +1518,7 @@ int host_single_graph(dppx_ctx* ctx, bool adaptive, const dppx_frames_desc* d, c
     fgp = ng;
   }
   // ---- replay ----
-  static uint64_t tick = 0;
-  fgp->last_use = ++tick;
+  fgp->last_use = ++ctx->graph_tick;
   const void* want[3] = {img, mask, out};
   for (auto& c : fgp->copies) {
     if (fgp->cur[c.which] == want[c.which]) continue;
