@@ -625,7 +625,9 @@ int run_stats(dppx_ctx* ctx, StatsArgs& a) {
     // Two stages: measured best for every shape on B200 (a 2-deep ring per CTA
     // with 4 CTAs/SM at b = 16 beats 3-4 deep rings with fewer CTAs; see
     // profiles/r01_stage_sweep.md).
-    int S = 2;
+    // (uniform b = 4 with two-row units: 12 KB stages, a 3-deep ring measured
+    // best -- 0.354 -> 0.329 ms per 120 x 1080p RGB, profiles/r02dd_b4_stages.txt)
+    int S = rpu > 1 ? 3 : 2;
     if (const char* env = std::getenv("DPPX_STAGES"))  // tuning knob (2..4)
       S = std::max(2, std::min(stats_max_stages(), std::atoi(env)));
     a.stages = S;
