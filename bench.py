@@ -543,7 +543,17 @@ def main():
 
         h_means = [torch.zeros((Fe * C, j[2]), dtype=torch.uint8).pin_memory() for j in jobs]
 
+        sw_mp = (Ct.c_void_p * len(jobs))(*[hm.data_ptr() for hm in h_means])
+        sw_op = (Ct.c_void_p * len(jobs))(*([h_out.data_ptr()] * len(jobs)))
+        sw_b = (Ct.c_int32 * len(sweep_b))(*sweep_b) if sweep else None
+        sw_e = (Ct.c_double * len(sweep_e))(*sweep_e) if sweep else None
+
         def e2e_step():
+            if fused:  # one upload, every run's means and image back (h_out reused per run)
+                ctx._check(dp._lib.dppx_pixelize_uniform_sweep(
+                    ctx._h, Ct.byref(de), h_img.data_ptr(), len(sweep_b), sw_b, len(sweep_e), sw_e, m,
+                    Ct.byref(nze), sw_mp, sw_op, None, None), "e2e")
+                return
             if sweep:
                 for (pj, _, _, _), hm in zip(jobs, h_means):
                     ctx._check(dp._lib.dppx_pixelize_uniform(ctx._h, Ct.byref(de), h_img.data_ptr(),
@@ -624,7 +634,9 @@ def main():
                                       es["d2h_bytes"] / args.e2e_steps / (d2h_link * 1e9))
                                   / (e_ms / 1e3), 4),
                "path": "dppx_pixelize_adaptive (host pointers, pinned, chunked H2D/K0/K1/D2H "
-                       "pipeline on 3 streams)" if adaptive else "dppx_pixelize_uniform"}
+                       "pipeline on 3 streams)" if adaptive else
+                       ("dppx_pixelize_uniform_sweep (one upload of the frames; every run's means "
+                        "and image back to host)" if fused else "dppx_pixelize_uniform")}
         del h_img, h_mask, h_out, h_stats
 
     # ---- CPU reference baseline (rank 0, N = 1 only) ----

@@ -210,6 +210,17 @@ int dppx_pixelize_uniform_sweep_dev(dppx_ctx* ctx, const dppx_frames_desc* desc,
                                     const double* eps_list, int32_t m, const dppx_noise* noise,
                                     uint8_t* const* means, uint8_t* const* out /* nullable */);
 
+/* Host-pointer form of the sweep (run_sweep's caller shape): one upload of the
+ * F frames, the runs as in dppx_pixelize_uniform_sweep_dev, then for every
+ * run (i*ne + j) its statistics to means[r] (F*C planes of G_i bytes), its
+ * image to out[r] (if out and out[r] are non-NULL; desc out_pitch /
+ * out_frame_stride) and, computed on the device against the input,
+ * mse_out[r*F*C + plane] / ssim_out[...] (each may be NULL; no ssim below 7x7). */
+int dppx_pixelize_uniform_sweep(dppx_ctx* ctx, const dppx_frames_desc* desc, const uint8_t* img, int32_t nb,
+                                const int32_t* b_list, int32_t ne, const double* eps_list, int32_t m,
+                                const dppx_noise* noise, uint8_t* const* means, uint8_t* const* out,
+                                double* mse_out, double* ssim_out);
+
 /* EXTENSION (north-star "per-region complexity measure"; no reference
  * counterpart -- the reference takes external masks): cell
  * (r, c) is complex iff the variance of its C*b*b mirror-padded samples,

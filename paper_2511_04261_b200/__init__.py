@@ -157,6 +157,9 @@ ABI = {
     "dppx_reconstruct_record": (C.c_int, [_ctxp, _vp, C.c_size_t, _vp, C.c_size_t]),
     "dppx_debug_device_laplace": (C.c_int, [_ctxp, C.c_uint64, _vp, C.c_int32, C.c_double, _vp]),
     "dppx_debug_lg2_max_error": (C.c_int, [_ctxp, C.POINTER(C.c_double)]),
+    "dppx_pixelize_uniform_sweep": (C.c_int, [_ctxp, _descp, _vp, C.c_int32, C.POINTER(C.c_int32), C.c_int32,
+                                              C.POINTER(C.c_double), C.c_int32, _np, C.POINTER(_vp),
+                                              C.POINTER(_vp), _vp, _vp]),
     "dppx_pixelize_checked": (C.c_int, [_ctxp, C.c_int32, _descp, _vp, _vp, _pp, _np, _vp, C.c_int64, _vp,
                                         _vp, _vp, _vp, _vp]),
     "dppx_group_create": (C.c_int, [C.POINTER(C.c_int32), C.c_int32, C.POINTER(_vp)]),
@@ -508,6 +511,27 @@ class Context:
         del keep
         return [bytes(buf[i, : lens[i]]) for i in range(F * Cn)], out
 
+    def pixelize_uniform_sweep(self, frames, b_list, eps_list, m, noise=NOISE_NONE, seeds=None,
+                               want_images=True, metrics=False):
+        """dppx_pixelize_uniform_sweep (host buffers): one upload, every (b, eps) run.
+        Returns (means list, images list or None, mse [runs, F*C] or None, ssim or None)."""
+        frames = np.ascontiguousarray(frames, dtype=np.uint8)
+        F, M, N, Cn = _frames_shape(frames)
+        nb, ne = len(b_list), len(eps_list)
+        means = [np.zeros((F * Cn, grid_dims(M, N, b).grid_count()), np.uint8) for b in b_list for _ in eps_list]
+        imgs = [np.zeros_like(frames) for _ in range(nb * ne)] if want_images else None
+        mse = np.zeros((nb * ne, F * Cn)) if metrics else None
+        ssim = np.zeros((nb * ne, F * Cn)) if metrics and M >= 7 and N >= 7 else None
+        nz, keep = self._noise(noise, seeds)
+        d = _desc(M, N, Cn, F)
+        mp = (_vp * (nb * ne))(*[x.ctypes.data for x in means])
+        op = (_vp * (nb * ne))(*[x.ctypes.data for x in imgs]) if want_images else None
+        self._check(_lib.dppx_pixelize_uniform_sweep(
+            self._h, C.byref(d), _ptr(frames), nb, (C.c_int32 * nb)(*b_list), ne, (C.c_double * ne)(*eps_list),
+            m, C.byref(nz), mp, op, _ptr(mse), _ptr(ssim)), "pixelize_uniform_sweep")
+        del keep
+        return means, imgs, mse, ssim
+
     def pixelize_checked(self, frames, masks, params: PrivacyParams, mode="adaptive",
                          noise=NOISE_NONE, seeds=None):
         """dppx_pixelize_checked: pixelize + on-device reconstruct check + mse / ssim
@@ -727,6 +751,7 @@ def _group_unsupported(name):
 for _name in ("stream", "set_stream", "set_chunk_frames", "set_exact_noise", "set_out_pad_scratch",
               "lg2_max_error", "pixelize_reference", "pixelize_adaptive_variance",
               "reconstruct_record", "classify_regions", "metrics", "device_laplace", "pixelize_checked",
+              "pixelize_uniform_sweep",
               "pixelize_adaptive_dev", "pixelize_uniform_dev", "pixelize_adaptive_variance_dev",
               "pixelize_uniform_sweep_dev",
               "reassemble_dev", "broadcast_means_dev", "synth_frames_dev"):

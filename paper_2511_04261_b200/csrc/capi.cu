@@ -2424,6 +2424,93 @@ int dppx_pixelize_uniform_sweep_dev(dppx_ctx* ctx, const dppx_frames_desc* d, co
   return DPPX_OK;
 }
 
+namespace {
+int metric_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* a, const uint8_t* b, bool ssim,
+               double* out);
+}  // namespace
+
+int dppx_pixelize_uniform_sweep(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img, int32_t nb,
+                                const int32_t* b_list, int32_t ne, const double* eps_list, int32_t m,
+                                const dppx_noise* nz, uint8_t* const* means, uint8_t* const* out,
+                                double* mse_out, double* ssim_out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (nb < 1 || ne < 1 || !b_list || !eps_list || !means)
+    return set_err(ctx, DPPX_ERR_INVALID, "sweep lists must be non-empty");
+  const bool want_img = out != nullptr || mse_out != nullptr || ssim_out != nullptr;
+  if (int rc = check_desc(ctx, d, false, want_img)) return rc;
+  const int F = d->frames, M = d->height, N = d->width, C = d->channels;
+  if (F == 0) return DPPX_OK;
+  if (!img) return set_err(ctx, DPPX_ERR_INVALID, "null image pointer");
+  if (C < 1 || C > 4) return set_err(ctx, DPPX_ERR_INVALID, "channels must be 1..4");
+  const int runs = nb * ne;
+  const int64_t row = static_cast<int64_t>(N) * C;
+  const int64_t dpitch = round_up(row, 16), dfs = dpitch * M;
+  std::vector<int64_t> G(static_cast<size_t>(nb));
+  int64_t means_bytes = 0;
+  for (int i = 0; i < nb; ++i) {
+    dppx_geometry gg;
+    if (dppx_grid_dims(M, N, b_list[i], &gg) != DPPX_OK)
+      return set_err(ctx, DPPX_ERR_INVALID, "grid_dims: grid side b exceeds both image dimensions");
+    G[i] = static_cast<int64_t>(gg.grid_rows) * gg.grid_cols;
+    means_bytes += round_up(G[i] * F * C, 256) * ne;
+  }
+  // device: frames, every run's means and (when wanted) image
+  if (ensure(ctx, ctx->img[0], static_cast<size_t>(dfs) * F)) return DPPX_ERR_OOM;
+  if (ensure(ctx, ctx->check_img, static_cast<size_t>(means_bytes))) return DPPX_ERR_OOM;
+  if (want_img && ensure(ctx, ctx->out[0], static_cast<size_t>(dfs) * F * runs)) return DPPX_ERR_OOM;
+  uint8_t* dimg = static_cast<uint8_t*>(ctx->img[0].p);
+  uint8_t* dout = static_cast<uint8_t*>(ctx->out[0].p);
+  std::vector<uint8_t*> dmeans(static_cast<size_t>(runs)), douts(static_cast<size_t>(runs), nullptr);
+  {
+    uint8_t* q = static_cast<uint8_t*>(ctx->check_img.p);
+    for (int i = 0; i < nb; ++i)
+      for (int j = 0; j < ne; ++j) {
+        dmeans[i * ne + j] = q;
+        q += round_up(G[i] * F * C, 256);
+        if (want_img) douts[i * ne + j] = dout + static_cast<int64_t>(i * ne + j) * dfs * F;
+      }
+  }
+  cudaStream_t st = ctx->stream;
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->s_out));
+  if (int rc = h2d_frames(ctx, dimg, dpitch, dfs, img, d->pitch, d->frame_stride, row, M, F, st)) return rc;
+  ctx->kstats.h2d_bytes += static_cast<uint64_t>(row) * M * F;
+  dppx_frames_desc dd = *d;
+  dd.pitch = dpitch;
+  dd.frame_stride = dfs;
+  dd.out_pitch = dpitch;
+  dd.out_frame_stride = dfs;
+  {
+    struct PadScratch {  // the run images are the ctx's own buffers
+      dppx_ctx* c;
+      bool prev;
+      ~PadScratch() { c->out_pad_scratch = prev; }
+    } pad_scope{ctx, ctx->out_pad_scratch};
+    ctx->out_pad_scratch = true;
+    if (int rc = dppx_pixelize_uniform_sweep_dev(ctx, &dd, dimg, nb, b_list, ne, eps_list, m, nz, dmeans.data(),
+                                                 want_img ? douts.data() : nullptr))
+      return rc;
+  }
+  for (int r = 0; r < runs; ++r) {  // mse / ssim of every run's image, where it lives
+    if (mse_out)
+      if (int rc = metric_dev(ctx, &dd, dimg, douts[r], false, mse_out + static_cast<int64_t>(r) * F * C)) return rc;
+    if (ssim_out && M >= 7 && N >= 7)
+      if (int rc = metric_dev(ctx, &dd, dimg, douts[r], true, ssim_out + static_cast<int64_t>(r) * F * C)) return rc;
+  }
+  for (int r = 0; r < runs; ++r) {
+    const int i = r / ne;
+    if (out && out[r]) {
+      if (int rc = d2h_frames(ctx, out[r], d->out_pitch, d->out_frame_stride, douts[r], dpitch, dfs, row, M, F, st))
+        return rc;
+      ctx->kstats.d2h_bytes += static_cast<uint64_t>(row) * M * F;
+    }
+    CUDA_TRY(ctx, cudaMemcpyAsync(means[r], dmeans[r], static_cast<size_t>(G[i] * F * C), cudaMemcpyDeviceToHost, st));
+    ctx->kstats.d2h_bytes += static_cast<uint64_t>(G[i]) * F * C;
+  }
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  if (ctx->timing) collect_timings(ctx);
+  return DPPX_OK;
+}
+
 int dppx_pixelize_adaptive_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* img,
                                const uint8_t* mask, const dppx_privacy_params* pp,
                                const dppx_noise* nz, uint8_t* payload, int64_t payload_stride,

@@ -129,7 +129,7 @@ std::uint64_t tile_sum(const std::vector<T>& data, int stride, const GridGeometr
 
 }  // namespace
 
-dppx_ctx* dropin_thread_ctx() { return thread_ctx(); }  // used by ingest.cpp
+dppx_ctx* dropin_thread_ctx() { return thread_ctx(); }  // used by runner.cpp
 
 // ---------------------------------------------------------------- image.hpp
 GrayImage make_image(int height, int width, std::uint8_t fill) {

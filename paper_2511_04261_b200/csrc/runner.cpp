@@ -27,6 +27,7 @@
 #include <mutex>
 #include <sstream>
 #include <thread>
+#include <tuple>
 #include <utility>
 
 #include "dppix/adaptive.hpp"
@@ -40,6 +41,8 @@
 
 namespace dppix {
 namespace fs = std::filesystem;
+
+dppx_ctx* dropin_thread_ctx();  // dropin.cpp: the calling thread's context
 
 namespace {
 
@@ -511,6 +514,107 @@ std::vector<FileReport> run_batch(const RunConfig& cfg) {  // cli.cpp:175-213, o
   return out;
 }
 
+// run_sweep's uniform rows for one image: every (b, eps) pair of one (m, seed)
+// is computed by ONE dppx_pixelize_uniform_sweep call (one upload and one read
+// of the frame for all the runs, per-run mse / ssim on the device). Pairs whose
+// parameters the reference would reject are left out; the caller runs them
+// through run_single so the error rows are the reference's own.
+namespace {
+using SweepKey = std::tuple<double, int, int, std::uint64_t>;
+
+void fused_uniform_sweep(const RunConfig& base, std::map<SweepKey, MetricReport>& rows) {
+  if (const char* e = std::getenv("DPPX_SWEEP_FUSED"); e && e[0] == '0') return;
+  GrayImage img;
+  try {
+    img = read_pgm(base.input);
+  } catch (const std::exception&) {
+    return;  // every row reports the read error through run_single
+  }
+  const int H = img.height, W = img.width;
+  dppx_ctx* ctx = dropin_thread_ctx();
+  dppx_frames_desc d{H, W, 1, 1, W, static_cast<int64_t>(H) * W, W, static_cast<int64_t>(H) * W, W,
+                     static_cast<int64_t>(H) * W};
+  for (int m : base.m_list) {
+    auto clean = [&](double eps, int b) {
+      try {
+        validate(true, eps, false, false, false, true);
+        (void)make_privacy_params(eps, m, b, 1);
+        (void)grid_dims(H, W, b);
+        return true;
+      } catch (const std::exception&) {
+        return false;
+      }
+    };
+    std::vector<double> eps_ok;
+    for (double eps : base.epsilon_list)
+      if (std::any_of(base.b_list.begin(), base.b_list.end(), [&](int b) { return clean(eps, b); }))
+        eps_ok.push_back(eps);
+    std::vector<int32_t> b_ok;
+    for (int b : base.b_list)
+      if (!eps_ok.empty() && std::all_of(eps_ok.begin(), eps_ok.end(), [&](double e) { return clean(e, b); }))
+        b_ok.push_back(b);
+    b_ok.erase(std::unique(b_ok.begin(), b_ok.end()), b_ok.end());
+    eps_ok.erase(std::unique(eps_ok.begin(), eps_ok.end()), eps_ok.end());
+    if (b_ok.empty() || eps_ok.empty()) continue;
+    eps_ok.erase(std::remove_if(eps_ok.begin(), eps_ok.end(),
+                                [&](double e) {
+                                  return !std::all_of(b_ok.begin(), b_ok.end(), [&](int b) { return clean(e, b); });
+                                }),
+                 eps_ok.end());
+    const int nb = static_cast<int>(b_ok.size()), ne = static_cast<int>(eps_ok.size()), runs = nb * ne;
+    std::vector<GridGeometry> geom;
+    for (int b : b_ok) geom.push_back(grid_dims(H, W, b));
+    for (std::uint64_t seed : base.seed_list) {
+      std::vector<std::vector<std::uint8_t>> means(static_cast<size_t>(runs));
+      std::vector<std::vector<std::uint8_t>> images(base.reconstruct_check ? runs : 0);
+      std::vector<std::uint8_t*> mp(static_cast<size_t>(runs)), op(static_cast<size_t>(runs), nullptr);
+      for (int r = 0; r < runs; ++r) {
+        means[r].resize(static_cast<size_t>(geom[r / ne].grid_count()));
+        mp[r] = means[r].data();
+        if (base.reconstruct_check) {
+          images[r].resize(static_cast<size_t>(H) * W);
+          op[r] = images[r].data();
+        }
+      }
+      std::vector<double> mse_v(static_cast<size_t>(runs)), ssim_v(static_cast<size_t>(runs),
+                                                                  std::numeric_limits<double>::quiet_NaN());
+      const dppx_noise nz{DPPX_NOISE_KEYED, 0, &seed, nullptr};
+      const auto t0 = std::chrono::steady_clock::now();
+      const int rc = dppx_pixelize_uniform_sweep(ctx, &d, img.pixels.data(), nb, b_ok.data(), ne, eps_ok.data(), m,
+                                                 &nz, mp.data(), base.reconstruct_check ? op.data() : nullptr,
+                                                 mse_v.data(), H >= 7 && W >= 7 ? ssim_v.data() : nullptr);
+      const auto t1 = std::chrono::steady_clock::now();
+      if (rc != DPPX_OK) return;  // leave every row to run_single (which reports the error)
+      const double per_ms = std::chrono::duration<double, std::milli>(t1 - t0).count() / runs;
+      for (int r = 0; r < runs; ++r) {
+        const int i = r / ne, j = r % ne;
+        PixelRecord rec{H, W, GridMeans{geom[i], std::move(means[r])}};
+        const std::vector<std::uint8_t> bytes = encode(rec);
+        if (base.reconstruct_check) {
+          GrayImage pix;
+          pix.height = H;
+          pix.width = W;
+          pix.pixels = std::move(images[r]);
+          if (!(reconstruct(decode(bytes)) == pix))
+            throw ConsistencyError("reconstruction does not match the emitted image for " + base.input);
+        }
+        MetricReport rep;
+        rep.epsilon = eps_ok[j];
+        rep.m = m;
+        rep.b = b_ok[i];
+        rep.n = 1;
+        rep.seed = seed;
+        rep.mse = mse_v[r];
+        rep.ssim = ssim_v[r];
+        rep.runtime_ms = per_ms;
+        rep.record_bytes = bytes.size();
+        rows[SweepKey{eps_ok[j], m, b_ok[i], seed}] = rep;
+      }
+    }
+  }
+}
+}  // namespace
+
 SweepResult run_sweep(const RunConfig& cfg) {  // cli.cpp:231-288
   RunConfig base = cfg;
   base.emit_image = false;
@@ -533,6 +637,8 @@ SweepResult run_sweep(const RunConfig& cfg) {  // cli.cpp:231-288
     return q + "\"";
   };
   SweepResult res;
+  std::map<SweepKey, MetricReport> fused;
+  if (base.mode == RunMode::uniform) fused_uniform_sweep(base, fused);
   std::ostringstream csv;
   csv << csv_header() << ",error\n";
   for (double eps : base.epsilon_list)
@@ -546,6 +652,10 @@ SweepResult run_sweep(const RunConfig& cfg) {  // cli.cpp:231-288
             one.b = b;
             one.n = n;
             one.seed = NoiseSeed{seed};
+            if (auto it = fused.find(SweepKey{eps, m, b, seed}); it != fused.end()) {
+              csv << csv_row(it->second) << ",\n";
+              continue;
+            }
             try {
               csv << csv_row(run_single(one).report) << ",\n";
             } catch (const std::exception& err) {

@@ -52,3 +52,47 @@ def test_reference_unit_suites_on_dropin(ctx):
     print(r.stdout, r.stderr[-5000:])
     assert r.returncode == 0, r.stderr[-5000:]
     assert "test cases: 84 | 84 passed | 0 failed" in r.stdout, r.stdout
+
+
+def _csv_rows(text):
+    import csv
+    import io
+    rows = list(csv.reader(io.StringIO(text)))
+    head = rows[0]
+    drop = head.index("runtime_ms")
+    return [r[:drop] + r[drop + 1:] for r in rows]
+
+
+@pytest.mark.parametrize("shape,recon", [((150, 203), "1"), ((64, 64), "0"), ((1080, 1920), "1")])
+def test_run_sweep_matches_reference_run_sweep(ctx, tmp_path, shape, recon):
+    """dppix::run_sweep on the drop-in (uniform rows: one fused
+    dppx_pixelize_uniform_sweep call per (m, seed), one read of the frame for
+    every (b, eps) run; rows the reference rejects via run_single) prints the
+    same CSV as the reference's own run_sweep (cli.cpp:231-288, compiled from
+    its sources by tests/cpp/Makefile) -- every column but runtime_ms, incl.
+    the device mse / ssim doubles and the error rows."""
+    import numpy as np
+    gpu = os.path.join(HERE, "cpp", "sweep_gpu")
+    if not os.path.exists(gpu):
+        subprocess.run(["make", "-s", "-C", os.path.join(HERE, "cpp"), "sweep_gpu"], check=True)
+    ref = _gate_exe("sweep_ref")
+    M, N = shape
+    rng = np.random.default_rng(M * 7 + N)
+    yy, xx = np.mgrid[0:M, 0:N]
+    img = ((xx * 3 + yy * 5) % 256 + rng.integers(0, 40, (M, N))).clip(0, 255).astype(np.uint8)
+    p = tmp_path / "in.pgm"
+    p.write_bytes(f"P5\n{N} {M}\n255\n".encode() + img.tobytes())
+    args = [str(p), "0.5,1,2,-1", "1,16", "4,5,8,16,32,64,300", "1,42", recon, "u"]
+    if M > 1000:
+        args = [str(p), "0.1,0.5,1", "16", "4,8,16,32", "7", recon, "u"]
+    rr = subprocess.run([ref] + args, capture_output=True, text=True, timeout=900)
+    rg = subprocess.run([gpu] + args, capture_output=True, text=True, timeout=900)
+    assert rg.returncode == rr.returncode, rg.stderr
+    a, b = _csv_rows(rr.stdout), _csv_rows(rg.stdout)
+    assert len(a) == len(b)
+    for x, y in zip(a, b):
+        assert x == y
+    # the same rows through the per-run path
+    rs = subprocess.run([gpu] + args, capture_output=True, text=True, timeout=900,
+                        env=dict(os.environ, DPPX_SWEEP_FUSED="0"))
+    assert _csv_rows(rs.stdout) == b

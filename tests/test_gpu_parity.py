@@ -1162,3 +1162,38 @@ def test_pixelize_checked_equals_separate_calls(ctx, mode, C):
     assert np.array_equal(img, ref)
     m2, s2 = ctx.metrics(frames, ref, "both")
     assert np.array_equal(mse, m2) and np.array_equal(ssim, s2)
+
+
+@pytest.mark.parametrize("M,N,C,F,bl,el", [
+    (150, 203, 1, 1, [4, 5, 8, 16, 32, 64], [0.5, 1.0, 2.0]),
+    (61, 99, 3, 4, [4, 8, 16, 32], [0.1, 1.0]),
+    (6, 9, 1, 2, [4, 8], [1.0]),  # below the ssim window
+])
+def test_host_sweep_equals_separate_host_runs(ctx, M, N, C, F, bl, el):
+    """dppx_pixelize_uniform_sweep (host buffers: one upload, every run's means,
+    image and device mse / ssim) equals separate dppx_pixelize_uniform calls and
+    dppx_metrics on their images, for pageable and pinned inputs."""
+    rng = np.random.default_rng(M + N)
+    fr = rng.integers(0, 256, (F, M, N, C), dtype=np.uint8)
+    seeds = dp.plane_seeds(5, F, C)
+    for src in (fr, dp.pinned_empty(fr.shape)):
+        if src is not fr:
+            src[...] = fr
+        means, imgs, mse, ssim = ctx.pixelize_uniform_sweep(src, bl, el, 16, dp.NOISE_KEYED, seeds,
+                                                            metrics=True)
+        k = 0
+        for b in bl:
+            for e in el:
+                rm, ri = ctx.pixelize_uniform(fr, dp.make_privacy_params(e, 16, b), dp.NOISE_KEYED, seeds)
+                assert np.array_equal(means[k], rm), (b, e)
+                assert np.array_equal(imgs[k], ri), (b, e)
+                if M >= 7 and N >= 7:
+                    em, es = ctx.metrics(fr, ri, "both")
+                    assert np.array_equal(mse[k], em) and np.array_equal(ssim[k], es), (b, e)
+                else:
+                    assert ssim is None
+                    assert np.array_equal(mse[k], ctx.metrics(fr, ri, "mse"))
+                k += 1
+    means2, imgs2, _, _ = ctx.pixelize_uniform_sweep(fr, bl, el, 16, dp.NOISE_KEYED, seeds,
+                                                     want_images=False)
+    assert imgs2 is None and all(np.array_equal(a, b) for a, b in zip(means, means2))
