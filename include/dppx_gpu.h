@@ -118,7 +118,8 @@ typedef enum {
   DPPX_K_AUX = 4,      /* synthetic generator, payload checks                 */
   DPPX_K_ROWS = 5,     /* K1r: row-streaming stats for other grid sides        */
   DPPX_K_SWEEP = 6,    /* K1s: one-read statistics of a grid-size x eps sweep  */
-  DPPX_K_COUNT = 7
+  DPPX_K_ZEROCOPY = 7, /* K1z: small host frames read / written over PCIe     */
+  DPPX_K_COUNT = 8
 } dppx_kernel_family;
 
 typedef struct {
@@ -168,6 +169,15 @@ int dppx_ctx_set_exact_noise(dppx_ctx* ctx, int32_t on);
  * partial-sector DRAM writes. Pixels [0, N*C) are identical either way. The
  * host entry points always use it on their own staging buffers. */
 int dppx_ctx_set_out_pad_scratch(dppx_ctx* ctx, int32_t on);
+/* How the host entry points move ONE small frame (< 4 MB, pinned buffers):
+ *   DPPX_SMALL_AUTO      default: zero-copy where the shape allows it, else graph
+ *   DPPX_SMALL_GRAPH     H2D, kernels and D2H replayed as one CUDA graph
+ *   DPPX_SMALL_ZEROCOPY  the kernels read / write the mapped pinned buffers
+ *                        over PCIe themselves (uniform: K1z; adaptive: K0 + K1r)
+ *   DPPX_SMALL_STAGED    the ordinary staged pipeline
+ * Results are identical on every path. */
+enum { DPPX_SMALL_AUTO = 0, DPPX_SMALL_GRAPH = 1, DPPX_SMALL_ZEROCOPY = 2, DPPX_SMALL_STAGED = 3 };
+int dppx_ctx_set_small_frame_path(dppx_ctx* ctx, int32_t path);
 /* Frames per pipeline chunk of the host entry points (0 = automatic). */
 int dppx_ctx_set_chunk_frames(dppx_ctx* ctx, int32_t frames);
 

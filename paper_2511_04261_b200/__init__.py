@@ -43,7 +43,10 @@ OK, ERR_INVALID, ERR_CORRUPT, ERR_CUDA, ERR_OOM, ERR_NO_DEVICE = range(6)
 ERR_NOT_A_RECORD, ERR_UNSUPPORTED_VERSION, ERR_CORRUPTION = 6, 7, 8
 NOISE_NONE, NOISE_KEYED, NOISE_PHILOX, NOISE_INJECTED = range(4)
 K_CLASSIFY, K_STATS, K_GENERIC, K_EXPAND, K_AUX, K_ROWS, K_SWEEP, K_COUNT = range(8)
-KERNEL_FAMILIES = ("classify", "stats_tma", "stats_generic", "expand", "aux", "stats_rows", "sweep")
+SMALL_AUTO, SMALL_GRAPH, SMALL_ZEROCOPY, SMALL_STAGED = 0, 1, 2, 3
+
+KERNEL_FAMILIES = ("classify", "stats_tma", "stats_generic", "expand", "aux", "stats_rows", "sweep",
+                   "stats_zerocopy")
 
 
 class Geometry(C.Structure):
@@ -121,6 +124,7 @@ ABI = {
     "dppx_ctx_set_chunk_frames": (C.c_int, [_ctxp, C.c_int32]),
     "dppx_ctx_set_exact_noise": (C.c_int, [_ctxp, C.c_int32]),
     "dppx_ctx_set_out_pad_scratch": (C.c_int, [_ctxp, C.c_int32]),
+    "dppx_ctx_set_small_frame_path": (C.c_int, [_ctxp, C.c_int32]),
     "dppx_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(_vp)]),
     "dppx_host_free": (None, [_vp]),
     "dppx_pixelize_uniform_dev": (C.c_int, [_ctxp, _descp, _vp, _pp, _np, _vp, _vp]),
@@ -396,6 +400,10 @@ class Context:
     def set_exact_noise(self, on: bool):
         """Force the f64 reference arithmetic for every statistic (testing)."""
         self._check(_lib.dppx_ctx_set_exact_noise(self._h, 1 if on else 0), "set_exact_noise")
+
+    def set_small_frame_path(self, path: int):
+        """SMALL_AUTO / SMALL_GRAPH / SMALL_ZEROCOPY / SMALL_STAGED (dppx_ctx_set_small_frame_path)."""
+        self._check(_lib.dppx_ctx_set_small_frame_path(self._h, path), "set_small_frame_path")
 
     def set_out_pad_scratch(self, on: bool):
         """Declare output pitch padding scratch: rows may end on whole 32-byte sectors."""
@@ -749,6 +757,7 @@ def _group_unsupported(name):
 
 
 for _name in ("stream", "set_stream", "set_chunk_frames", "set_exact_noise", "set_out_pad_scratch",
+              "set_small_frame_path",
               "lg2_max_error", "pixelize_reference", "pixelize_adaptive_variance",
               "reconstruct_record", "classify_regions", "metrics", "device_laplace", "pixelize_checked",
               "pixelize_uniform_sweep",

@@ -32,6 +32,8 @@ StatsKernel select_uniform_b4_rows2(int C);
 cudaError_t launch_gather_stage(const GatherArgs& a, cudaStream_t s);
 int rows_smem_bytes(const BatchGeom& g);
 cudaError_t launch_stats_rows(const StatsArgs& a, size_t smem, cudaStream_t s);
+cudaError_t launch_stats_zc(const StatsArgs& a, int unit_target, int ctas, int sms, cudaStream_t s, bool* launched,
+                            bool dry_run);
 cudaError_t launch_expand_rows(const ExpandArgs& a, size_t smem, cudaStream_t s);
 int stats_threads();
 int stats_tile_px();
@@ -164,6 +166,7 @@ struct dppx_ctx {
   bool exact_noise = false;
   bool out_pad_scratch = false;  // dppx_ctx_set_out_pad_scratch
   bool force_rows = false;       // zero-copy calls: row-streaming kernels (plain loads/stores)
+  int small_path = -1;           // DPPX_SMALL_*; -1: from the environment on first use
   double var_tau = 0.0;  // AdaptiveVariance host calls
   // bit-packed mask transport (maskpack.h): pinned staging per slot + packer pool
   dppx::MaskPacker* packer = nullptr;
@@ -593,7 +596,21 @@ int run_stats(dppx_ctx* ctx, StatsArgs& a) {
       rpu = 2;
     }
   }
-  if (ctx->force_rows) k = nullptr;
+  if (ctx->force_rows) {  // zero-copy call: k1z when the shape allows, else K1r
+    if (!var) {
+      static const int zc_unit = std::getenv("DPPX_ZC_UNIT") ? std::atoi(std::getenv("DPPX_ZC_UNIT")) : 12288;
+      static const int zc_ctas = std::getenv("DPPX_ZC_CTAS") ? std::atoi(std::getenv("DPPX_ZC_CTAS")) : 0;
+      bool ok = false;
+      CUDA_TRY(ctx, launch_stats_zc(a, zc_unit, zc_ctas, ctx->sms, ctx->stream, &ok, true));
+      if (ok) {
+        timing_begin(ctx, DPPX_K_ZEROCOPY, &pt);
+        CUDA_TRY(ctx, launch_stats_zc(a, zc_unit, zc_ctas, ctx->sms, ctx->stream, &ok, false));
+        timing_end(ctx, &pt);
+        return DPPX_OK;
+      }
+    }
+    k = nullptr;
+  }
   a.row_slack = a.pitch >= round_up(row_bytes, 16) ? 1 : 0;
   const int box_bytes = a.slot_px * g.C;
   // Input rows: the tensor's inner extent is rounded UP to 8 bytes when the
@@ -1242,14 +1259,19 @@ void* mapped_alias(const void* p) {
 int host_single_zerocopy(dppx_ctx* ctx, bool adaptive, const dppx_frames_desc* d, const BatchGeom& g,
                          const uint8_t* img, const uint8_t* mask, const dppx_privacy_params* pp,
                          const dppx_noise* nz, uint8_t* stats, int64_t sstride, uint32_t* lens,
-                         uint8_t* out, bool* used) {
+                         uint8_t* out, bool* used, bool k1z_only) {
   *used = false;
   const int C = g.C;
-  // Only shapes whose kernels never touch a byte past the frame (no padding
+  // K1z (uniform): whole cells only, 16-byte rows; it reads exactly the frame.
+  const bool k1z = !adaptive && g.PR == 0 && g.PC == 0 && (C == 1 || C == 3) && g.b <= 64 &&
+                   (static_cast<int64_t>(g.N) * C) % 16 == 0 && d->pitch % 16 == 0 &&
+                   (!out || d->out_pitch % 16 == 0);
+  if (k1z_only && !k1z) return DPPX_OK;
+  // K1r: only shapes whose loads never touch a byte past the frame (no padding
   // columns, 16-byte rows): a read past a host allocation would fault.
-  if (g.PC != 0 || (static_cast<int64_t>(g.N) * C) % 16 != 0 || g.N % 16 != 0 ||
-      d->pitch != static_cast<int64_t>(g.N) * C || (out && d->out_pitch != d->pitch) ||
-      (adaptive && d->mask_pitch != g.N))
+  if (!k1z && (g.PC != 0 || (static_cast<int64_t>(g.N) * C) % 16 != 0 || g.N % 16 != 0 ||
+               d->pitch != static_cast<int64_t>(g.N) * C || (out && d->out_pitch != d->pitch) ||
+               (adaptive && d->mask_pitch != g.N)))
     return DPPX_OK;
   const size_t G = static_cast<size_t>(g.G);
   const size_t cap = adaptive ? dppx_adaptive_payload_capacity(g.M, g.N, g.b, g.n) : G;
@@ -1605,17 +1627,29 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
     ctx->mask_bits_mode = env && env[0] == '0' ? 0 : 1;
   }
   {
-    // One small frame (below the row-band threshold): a replayed CUDA graph
-    // (DPPX_GRAPH=0 disables).
-    static const bool graphs_on = !(std::getenv("DPPX_GRAPH") && std::getenv("DPPX_GRAPH")[0] == '0');
+    // One small frame (below the row-band threshold): zero-copy kernels or a
+    // replayed CUDA graph (dppx_ctx_set_small_frame_path; environment
+    // defaults DPPX_ZEROCOPY=0/1, DPPX_GRAPH=0).
+    if (ctx->small_path < 0) {
+      const char* zc = std::getenv("DPPX_ZEROCOPY");
+      const char* gr = std::getenv("DPPX_GRAPH");
+      ctx->small_path = zc && zc[0] == '1'   ? DPPX_SMALL_ZEROCOPY
+                        : zc && zc[0] == '0' ? (gr && gr[0] == '0' ? DPPX_SMALL_STAGED : DPPX_SMALL_GRAPH)
+                        : gr && gr[0] == '0' ? DPPX_SMALL_STAGED
+                                             : DPPX_SMALL_AUTO;
+    }
     const int64_t row = static_cast<int64_t>(N) * C;
     const bool small = static_cast<int64_t>(M) * row < (4ll << 20);
-    static const bool zc_on = std::getenv("DPPX_ZEROCOPY") && std::getenv("DPPX_ZEROCOPY")[0] == '1';
-    if (zc_on && F == 1 && small && (op == HostOp::Uniform || op == HostOp::Adaptive) &&
+    // auto: zero-copy for uniform frames (K1z streams them over PCIe with the
+    // reads and writes overlapped); adaptive frames take the graph
+    const bool zc_try = ctx->small_path == DPPX_SMALL_ZEROCOPY ||
+                        (ctx->small_path == DPPX_SMALL_AUTO && op == HostOp::Uniform);
+    const bool graphs_on = ctx->small_path == DPPX_SMALL_AUTO || ctx->small_path == DPPX_SMALL_GRAPH;
+    if (zc_try && F == 1 && small && (op == HostOp::Uniform || op == HostOp::Adaptive) &&
         (!nz || nz->kind != DPPX_NOISE_INJECTED)) {
       bool used = false;
       const int rc = host_single_zerocopy(ctx, op == HostOp::Adaptive, d, g, img, mask, pp, nz, stats, sstride,
-                                          lens, out, &used);
+                                          lens, out, &used, ctx->small_path == DPPX_SMALL_AUTO);
       if (rc || used) return rc;
     }
     if (graphs_on && F == 1 && small && (op == HostOp::Uniform || op == HostOp::Adaptive) &&
@@ -2202,6 +2236,14 @@ int dppx_ctx_set_chunk_frames(dppx_ctx* ctx, int32_t frames) {
 int dppx_ctx_set_out_pad_scratch(dppx_ctx* ctx, int32_t on) {
   if (!ctx) return DPPX_ERR_INVALID;
   ctx->out_pad_scratch = on != 0;
+  return DPPX_OK;
+}
+
+int dppx_ctx_set_small_frame_path(dppx_ctx* ctx, int32_t path) {
+  if (!ctx) return DPPX_ERR_INVALID;
+  if (path < DPPX_SMALL_AUTO || path > DPPX_SMALL_STAGED)
+    return set_err(ctx, DPPX_ERR_INVALID, "unknown small-frame path");
+  ctx->small_path = path;
   return DPPX_OK;
 }
 

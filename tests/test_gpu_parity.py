@@ -1197,3 +1197,57 @@ def test_host_sweep_equals_separate_host_runs(ctx, M, N, C, F, bl, el):
     means2, imgs2, _, _ = ctx.pixelize_uniform_sweep(fr, bl, el, 16, dp.NOISE_KEYED, seeds,
                                                      want_images=False)
     assert imgs2 is None and all(np.array_equal(a, b) for a, b in zip(means, means2))
+
+
+@pytest.mark.parametrize("M,N,C,b,mode", [
+    (576, 768, 3, 16, "u"),   # PETS: K1z
+    (64, 64, 1, 4, "u"),
+    (96, 128, 3, 32, "u"),
+    (120, 160, 3, 8, "u"),
+    (128, 192, 3, 64, "u"),
+    (100, 120, 3, 16, "u"),   # padded rows: not K1z, auto takes the graph
+    (576, 768, 3, 16, "a"),
+])
+def test_small_frame_paths_agree(ctx, M, N, C, b, mode):
+    """One small pinned frame through every small-frame path (auto, graph,
+    zero-copy -- K1z for uniform whole-cell shapes --, staged) gives the same
+    statistics and image, equal to the oracle."""
+    rng = np.random.default_rng(M * N + b)
+    fr = dp.pinned_empty((1, M, N, C))
+    fr[:] = rng.integers(0, 256, fr.shape, dtype=np.uint8)
+    mk = dp.pinned_empty((1, M, N))
+    mk[:] = (rng.random((1, M, N)) < 0.5).astype(np.uint8)
+    p = dp.make_privacy_params(0.5, 16, b, 4 if mode == "a" else 1)
+    seeds = dp.plane_seeds(77, 1, C)
+    res = {}
+    try:
+        for path in (dp.SMALL_STAGED, dp.SMALL_GRAPH, dp.SMALL_ZEROCOPY, dp.SMALL_AUTO):
+            ctx.set_small_frame_path(path)
+            for rep in range(2):
+                out = dp.pinned_empty((1, M, N, C))
+                ctx.reset_stats()
+                if mode == "u":
+                    st, img = ctx.pixelize_uniform(fr, p, dp.NOISE_KEYED, seeds, out=out)
+                    st = st.copy()
+                else:
+                    st, img = ctx.pixelize_adaptive(fr, mk, p, dp.NOISE_KEYED, seeds, out=out)
+                res.setdefault(path, (st, np.array(img)))
+                launches = ctx.stats()["launches"]
+                k1z = (mode == "u" and M % b == 0 and N % b == 0 and (N * C) % 16 == 0)
+                if path in (dp.SMALL_ZEROCOPY, dp.SMALL_AUTO) and k1z:
+                    assert launches["stats_zerocopy"] == 1, launches
+                else:
+                    assert launches["stats_zerocopy"] == 0, launches
+    finally:
+        ctx.set_small_frame_path(dp.SMALL_AUTO)
+    ref_st, ref_img = res[dp.SMALL_STAGED]
+    for path, (st, img) in res.items():
+        if mode == "u":
+            assert np.array_equal(st, ref_st), path
+        else:
+            assert st == ref_st, path
+        assert np.array_equal(img, ref_img), path
+    if mode == "u":
+        rm, ri = oracle.pixelize_uniform(np.ascontiguousarray(fr[0]), b, p.sigma, "keyed", seeds)
+        assert np.array_equal(ref_st, rm)
+        assert np.array_equal(ref_img[0].reshape(-1), np.asarray(ri).reshape(-1))
