@@ -42,7 +42,7 @@ _lib = C.CDLL(LIB_PATH)
 OK, ERR_INVALID, ERR_CORRUPT, ERR_CUDA, ERR_OOM, ERR_NO_DEVICE = range(6)
 ERR_NOT_A_RECORD, ERR_UNSUPPORTED_VERSION, ERR_CORRUPTION = 6, 7, 8
 NOISE_NONE, NOISE_KEYED, NOISE_PHILOX, NOISE_INJECTED = range(4)
-K_CLASSIFY, K_STATS, K_GENERIC, K_EXPAND, K_AUX, K_ROWS, K_SWEEP, K_COUNT = range(8)
+K_CLASSIFY, K_STATS, K_GENERIC, K_EXPAND, K_AUX, K_ROWS, K_SWEEP, K_ZEROCOPY, K_COUNT = range(9)
 SMALL_AUTO, SMALL_GRAPH, SMALL_ZEROCOPY, SMALL_STAGED = 0, 1, 2, 3
 
 KERNEL_FAMILIES = ("classify", "stats_tma", "stats_generic", "expand", "aux", "stats_rows", "sweep",

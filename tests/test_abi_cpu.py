@@ -72,3 +72,12 @@ def test_host_helpers_match_oracle():
     with pytest.raises(ValueError):
         dp.make_privacy_params(1.0, 1, 4, 3)
     assert dp.adaptive_payload_capacity(1080, 1920, 16, 4) == 4 * 8160 + 4 + 8160 * 16
+
+
+def test_kernel_family_table_matches_header():
+    """The ctypes dppx_kernel_stats mirror has as many families as the header."""
+    import re
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                            "include", "dppx_gpu.h")).read()
+    count = int(re.search(r"DPPX_K_COUNT\s*=\s*(\d+)", hdr).group(1))
+    assert dp.K_COUNT == count == len(dp.KERNEL_FAMILIES)
