@@ -625,6 +625,7 @@ def main():
                "h2d_bytes_per_step": es["h2d_bytes"] // args.e2e_steps,
                "d2h_bytes_per_step": es["d2h_bytes"] // args.e2e_steps,
                "frames_per_step": Fe, "ms_per_step": round(e_ms, 3),
+               "kernel_launches": {k: v for k, v in es["launches"].items() if v},
                "frames_per_sec": round(Fe * runs * world / (e_ms / 1e3), 3),
                "link_gbs": {"h2d": round(h2d_link, 1), "d2h": round(d2h_link, 1),
                             "duplex": round(duplex_link, 1)},
@@ -636,7 +637,10 @@ def main():
                "path": "dppx_pixelize_adaptive (host pointers, pinned, chunked H2D/K0/K1/D2H "
                        "pipeline on 3 streams)" if adaptive else
                        ("dppx_pixelize_uniform_sweep (one upload of the frames; every run's means "
-                        "and image back to host)" if fused else "dppx_pixelize_uniform")}
+                        "and image back to host)" if fused else
+                        ("dppx_pixelize_uniform (one pinned frame: K1z reads and writes the mapped "
+                         "host buffers over PCIe, no staging copies)" if es["launches"].get("stats_zerocopy")
+                         else "dppx_pixelize_uniform"))}
         del h_img, h_mask, h_out, h_stats
 
     # ---- CPU reference baseline (rank 0, N = 1 only) ----

@@ -598,7 +598,7 @@ int run_stats(dppx_ctx* ctx, StatsArgs& a) {
   }
   if (ctx->force_rows) {  // zero-copy call: k1z when the shape allows, else K1r
     if (!var) {
-      static const int zc_unit = std::getenv("DPPX_ZC_UNIT") ? std::atoi(std::getenv("DPPX_ZC_UNIT")) : 12288;
+      static const int zc_unit = std::getenv("DPPX_ZC_UNIT") ? std::atoi(std::getenv("DPPX_ZC_UNIT")) : 6144;
       static const int zc_ctas = std::getenv("DPPX_ZC_CTAS") ? std::atoi(std::getenv("DPPX_ZC_CTAS")) : 0;
       bool ok = false;
       CUDA_TRY(ctx, launch_stats_zc(a, zc_unit, zc_ctas, ctx->sms, ctx->stream, &ok, true));

@@ -94,6 +94,32 @@ int main(int argc, char** argv) {
     CK(cudaMemcpyAsync(d_buf, h_in, bytes, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(h_out, d_buf, bytes, cudaMemcpyDeviceToHost, st));
   });
+  // both directions at once: copy engine H2D on `st`, the other direction on `st2`
+  cudaStream_t st2;
+  CK(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+  cudaEvent_t fork, join;
+  CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+  uint8_t* d_buf2;
+  CK(cudaMalloc(&d_buf2, bytes));
+  auto both = [&](auto&& other) {
+    CK(cudaEventRecord(fork, st));
+    CK(cudaStreamWaitEvent(st2, fork, 0));
+    CK(cudaMemcpyAsync(d_buf, h_in, bytes, cudaMemcpyHostToDevice, st));
+    other();
+    CK(cudaEventRecord(join, st2));
+    CK(cudaStreamWaitEvent(st, join, 0));
+  };
+  timeit("ce_h2d_parallel_ce_d2h", [&] {
+    both([&] { CK(cudaMemcpyAsync(h_out, d_buf2, bytes, cudaMemcpyDeviceToHost, st2)); });
+  });
+  for (int blocks : {36, 148}) {
+    char nm[64];
+    std::snprintf(nm, sizeof nm, "ce_h2d_parallel_zc_write_b%d", blocks);
+    timeit(nm, [&] {
+      both([&] { k_write<<<blocks, 256, 0, st2>>>(reinterpret_cast<uint4*>(m_out), n16); });
+    });
+  }
   char name[96];
   for (int blocks : {36, 74, 148, 296, 592}) {
     for (int threads : {256, 512}) {
