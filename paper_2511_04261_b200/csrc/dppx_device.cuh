@@ -181,9 +181,9 @@ __device__ __forceinline__ double cell_mean(uint32_t sum, double area) {
 //   f32 (relative error <= 2^-24, so <= 8.6e-8 in log2), lg2.approx (<= 2^-21,
 //   checked exhaustively on the device by tests/test_gpu_parity.py)
 //   => |d noise| <= sigma * ln2 * 6.6e-7 <= sigma * 4.6e-7;
-//   f32 rounding of mean, noise and the sum (< 8 ulp of 512; the rounding of
-//   -ln(1-2|u|) and of sigma * L is relative to |noise| <= 512 where it
-//   matters) <= 2.5e-4.
+//   f32 rounding of mean + 0.5 (one FFMA), of -log2(1-2|u|), of sigma * ln 2
+//   and of the final FFMA (each relative to |t|, |noise| <= 512 where it
+//   matters) <= 1.2e-4 <= 2.5e-4.
 // margin = 5e-4 + sigma * 1e-6 keeps a factor >= 2 over that budget (round 1
 // used 2e-3 + 4e-6 sigma, a factor 8: 4x as many exact f64 evaluations, the
 // dominant cost of draw-bound shapes such as b = 4 at eps = 0.1, sigma = 2550).
@@ -199,11 +199,26 @@ __device__ __forceinline__ float lg2_approx(float x) {
   return r;
 }
 
+// q = clip(floor(t), 0, 255) for t = mean + noise + 0.5, or 0xFFFFFFFF when t
+// lies within `margin` of a rounding boundary inside [1, 255]. Clamping t to
+// [0.5, 255.5] first makes the range test implicit (an integer within margin
+// < 0.5 of the clamped value lies in [1, 255]) and floor(clamped) is the
+// clipped floor: two instructions fewer than testing the range and clipping.
+__device__ __forceinline__ uint32_t fast_finish(float t, float margin) {
+  const float tc = fminf(fmaxf(t, 0.5f), 255.5f);
+  const float j = rintf(tc);
+  if (fabsf(tc - j) <= margin) return 0xFFFFFFFFu;
+  return static_cast<uint32_t>(__float2int_rd(tc));
+}
+
 // Returns the quantized value, or 0xFFFFFFFF when v_est is ambiguous.
+// sln2 = f32(sigma * ln 2) (DrawEnv): noise = -log2(1 - 2|u|) * sigma * ln 2.
 __device__ __forceinline__ uint32_t fast_quantize(uint32_t sum, float inv_area, uint64_t bits,
-                                                  float sigmaf, float margin) {
+                                                  float sln2, float margin) {
   const uint64_t y = bits >> 11;                    // 53-bit integer of uniform_from_bits
-  const bool neg = static_cast<int32_t>(bits >> 32) >= 0;  // y < 2^52, i.e. u < 0
+  uint32_t lo_w, hi_w;  // top-bit test on the high word alone (on the 64-bit value the
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo_w), "=r"(hi_w) : "l"(bits));  // compiler emits 2 compares)
+  const bool neg = static_cast<int32_t>(hi_w) >= 0;  // y < 2^52, i.e. u < 0
   // 1 - 2|u| = W * 2^-52: W = y for u < 0 (at least 1: the +-(0.5 - 2^-53)
   // clamp of noise.cpp:99-104, applied below on the f32 value), 2^53 - y
   // otherwise; W in [1, 2^52].
@@ -213,12 +228,9 @@ __device__ __forceinline__ uint32_t fast_quantize(uint32_t sum, float inv_area, 
   const uint32_t wb = __float_as_uint(fmaxf(__ull2float_rn(W), 1.0f));
   const int e = static_cast<int>(wb >> 23) - 127;  // floor(log2 Wf)
   const float lg_m = lg2_approx(__uint_as_float(0x3F800000u | (wb & 0x7FFFFFu)));  // log2 of [1,2)
-  const float L = (static_cast<float>(52 - e) - lg_m) * 0.693147180559945f;  // -ln(1-2|u|)
-  const float noise = neg ? -sigmaf * L : sigmaf * L;
-  const float t = static_cast<float>(sum) * inv_area + noise + 0.5f;
-  const float j = rintf(t);
-  if (fabsf(t - j) <= margin && j >= 1.0f && j <= 255.0f) return 0xFFFFFFFFu;
-  return static_cast<uint32_t>(min(max(__float2int_rd(t), 0), 255));  // clip + floor
+  const float L2 = static_cast<float>(52 - e) - lg_m;  // -log2(1 - 2|u|)
+  const float t = fmaf(L2, neg ? -sln2 : sln2, fmaf(static_cast<float>(sum), inv_area, 0.5f));
+  return fast_finish(t, margin);
 }
 
 // The reference's f64 arithmetic, step for step (rare path).
@@ -239,7 +251,7 @@ struct DrawEnv {
   bool exact_only;  // test switch: always take the f64 path
   bool pow2;        // area is a power of two: sum * inv_area is exact in f32
   double area, sigma;
-  float inv_area, sigmaf, margin;
+  float inv_area, sln2, margin;
 };
 
 __device__ __forceinline__ DrawEnv make_env(int kind, bool exact_only, double area, double sigma) {
@@ -251,7 +263,7 @@ __device__ __forceinline__ DrawEnv make_env(int kind, bool exact_only, double ar
   e.area = area;
   e.sigma = sigma;
   e.inv_area = 1.0f / static_cast<float>(area);
-  e.sigmaf = static_cast<float>(sigma);
+  e.sln2 = static_cast<float>(sigma * 0.6931471805599453);
   e.margin = fast_margin(sigma);
   return e;
 }
@@ -263,7 +275,7 @@ __device__ __forceinline__ uint32_t quantize_stat(const DrawEnv& e, uint32_t sum
                                                   const Inj& inj) {
   if (!e.exact_only) {
     if (e.kind == DPPX_NOISE_KEYED || e.kind == DPPX_NOISE_PHILOX) {
-      const uint32_t q = fast_quantize(sum, e.inv_area, bits, e.sigmaf, e.margin);
+      const uint32_t q = fast_quantize(sum, e.inv_area, bits, e.sln2, e.margin);
       if (q != 0xFFFFFFFFu) return q;
     } else if (e.kind == DPPX_NOISE_NONE && e.pow2) {
       // sum * 2^-k + 0.5 is exact in f32 (< 24 significant bits).

@@ -333,9 +333,9 @@ __global__ void __launch_bounds__(kDrawThreads)
           if (kind == DPPX_NOISE_NONE) {
             q = static_cast<uint32_t>(floorf(t));  // area = 16^k: exact in f32
           } else {
-            const float jr = rintf(t);
-            if (exact_only || (fabsf(t - jr) <= mg && jr >= 1.0f && jr <= 255.0f)) amb |= 1u << v;
-            q = static_cast<uint32_t>(min(max(__float2int_rd(t), 0), 255));
+            q = fast_finish(t, mg);
+            if (exact_only || q == 0xFFFFFFFFu) amb |= 1u << v;
+            q &= 0xFFu;  // (an ambiguous byte is overwritten when the queue drains)
           }
           word |= q << (8 * v);
         }

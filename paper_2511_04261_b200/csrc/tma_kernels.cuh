@@ -322,7 +322,7 @@ __device__ __forceinline__ void group_values(const StatsArgs& a, const DrawEnv& 
   // chains the scheduler can interleave); phase 2: the rare exact draws.
   if (!env.exact_only && (env.kind == DPPX_NOISE_KEYED || env.kind == DPPX_NOISE_PHILOX)) {
 #pragma unroll
-    for (int j = 0; j < NV; ++j) q[j] = fast_quantize(s[j], env.inv_area, bits[j], env.sigmaf, env.margin);
+    for (int j = 0; j < NV; ++j) q[j] = fast_quantize(s[j], env.inv_area, bits[j], env.sln2, env.margin);
   } else if (!env.exact_only && env.kind == DPPX_NOISE_NONE && env.pow2) {
 #pragma unroll
     for (int j = 0; j < NV; ++j)  // sum * 2^-k + 0.5 is exact in f32
@@ -816,7 +816,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
               const int vs = sidx / NSUB, sc2 = sidx - vs * NSUB;
               sum[j] = csum[wq][crec[wq][kk].cw][rem];
               bits[j] = key_sub(cstate[wq][kk][ch], vs, sc2);
-              q[j] = fast_quantize(sum[j], env_sub.inv_area, bits[j], env_sub.sigmaf, env_sub.margin);
+              q[j] = fast_quantize(sum[j], env_sub.inv_area, bits[j], env_sub.sln2, env_sub.margin);
             }
             __syncwarp();  // all of the batch's sums are read before any is overwritten
 #pragma unroll
