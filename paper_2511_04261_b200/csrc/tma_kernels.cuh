@@ -457,6 +457,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
   // is loaded one unit ahead so its L2 latency hides behind a unit of work.
   struct Meta {
     int u;
+    UnitPos pos;
     uint32_t info, rowpre, stot;
     uint64_t seed[C];
   };
@@ -511,17 +512,20 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
     }
     named_bar_sync(1, kConsumers);
   }
-  auto load_meta = [&](int k_next) {
+  // (ring slot and lap of each unit are advanced incrementally, and the unit
+  // is decoded once, here: both ran per unit and per thread)
+  auto load_meta = [&](int sn, int lap) {
     Meta m;
-    const int sn = ring_slot(k_next, S);
-    mbar_wait(&id_bar[sn], ring_lap(k_next, S) & 1);
+    mbar_wait(&id_bar[sn], lap & 1);
     m.u = *reinterpret_cast<volatile int*>(&stage_unit[sn]);
     m.info = 1u;
     m.rowpre = m.stot = 0;
 #pragma unroll
     for (int ch = 0; ch < C; ++ch) m.seed[ch] = 0;
+    m.pos = UnitPos{0, 0, 0, 0};
     if (m.u >= 0) {
       const UnitPos q = decode_unit<PACKED, TILE>(a, m.u);
+      m.pos = q;
       const int qf = q.fg * units_pack<PACKED>(a) + jj;
       const int qcell = PACKED ? (q.px0 + lpx) / B : q.px0 / B + sx / B4;
       if (!PACKED || qf < g.F) {
@@ -539,14 +543,15 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
     }
     return m;
   };
-  Meta next = load_meta(0);
-  for (int k = 0;; ++k) {
-    const int s = ring_slot(k, S);
+  Meta next = load_meta(0, 0);
+  for (int s = 0, lap = 0;;) {
+    const int s_next = s + 1 == S ? 0 : s + 1;
+    const int lap_next = s_next == 0 ? lap + 1 : lap;
     uint8_t* st = smem + s * STAGE;
     const Meta cur = next;
     const int u = cur.u;
     if (u < 0) break;
-    const UnitPos p = decode_unit<PACKED, TILE>(a, u);
+    const UnitPos p = cur.pos;
     const int f = p.fg * units_pack<PACKED>(a) + jj;  // this thread's frame
     const int cell = PACKED ? (p.px0 + lpx) / B : p.px0 / B + sx / B4;
     const int lic = sx % B4;       // lane within cell
@@ -565,7 +570,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
     for (int ch = 0; ch < C; ++ch)
       cs[ch] = a.noise.kind == DPPX_NOISE_KEYED ? key_cell(cur.seed[ch], p.r, cell) : 0ull;
 
-    mbar_wait(&full_bar[s], ring_lap(k, S) & 1);
+    mbar_wait(&full_bar[s], lap & 1);
 
     // Row tail not covered by the staged copy and mirrored padding columns
     // (image.cpp:105-110), including stray pitch-slack bytes a rounded-up copy
@@ -628,7 +633,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
         accumulate_row<C>(row, tot);
         sq = square_row<C>(row, sq);
       }
-      next = load_meta(k + 1);
+      next = load_meta(s_next, lap_next);
       uint32_t s1 = 0;
 #pragma unroll
       for (int ch = 0; ch < C; ++ch) s1 += tot[ch];
@@ -779,7 +784,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
           }
         }
       }
-      if constexpr (!VAR) next = load_meta(k + 1);
+      if constexpr (!VAR) next = load_meta(s_next, lap_next);
       if (compact && cx_any) {
         const unsigned leaders = __ballot_sync(0xFFFFFFFFu, cx && lic == 0);
         if (cx && lic == 0) {
@@ -885,13 +890,13 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
       // Next unit's metadata: requested here (after the staged rows are
       // summed) rather than at the top, so a 2-stage ring never stalls on the
       // producer's previous store; its latency hides behind the epilogue.
-      next = load_meta(k + 1);
+      next = load_meta(s_next, lap_next);
     }
 
     if constexpr (RPU > 1) {
       // Uniform, RPU cell rows of this band: the same per-cell work as below,
       // once per cell row (a band's last rows may lie past the grid: skipped).
-      next = load_meta(k + 1);
+      next = load_meta(s_next, lap_next);
 #pragma unroll 1
       for (int q = 0; q < RPU; ++q) {
         const int rq = p.r * RPU + q;
@@ -965,6 +970,8 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
 
     fence_proxy_async_smem();
     mbar_arrive(&done_bar[s]);
+    s = s_next;
+    lap = lap_next;
   }
 }
 
