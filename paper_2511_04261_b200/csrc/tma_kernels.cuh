@@ -305,19 +305,43 @@ __device__ __forceinline__ void group_values(const StatsArgs& a, const DrawEnv& 
   const int gb = lane - li;
   uint32_t s[NV], q[NV];
   uint64_t bits[NV];
+  uint64_t stv[NV];
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
     const int ch = j * GL + li;
     s[j] = sum[0];
-    uint64_t st = cs[0];
+    stv[j] = cs[0];
 #pragma unroll
     for (int k = 1; k < C; ++k)
       if (ch == k) {
         s[j] = sum[k];
-        st = cs[k];
+        stv[j] = cs[k];
       }
-    bits[j] = draw_bits(a, st, f, ch, r, c, sr, sc);
   }
+  if (env.kind == DPPX_NOISE_KEYED && !env.exact_only) {
+    // The common case on its own path: no Philox / injected-noise arguments
+    // are formed (the compiler would otherwise compute them for every draw).
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      bits[j] = key_sub(stv[j], sr, sc);
+      q[j] = fast_quantize(s[j], env.inv_area, bits[j], env.sln2, env.margin);
+    }
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int ch = j * GL + li;
+      if (active && ch < C && q[j] == 0xFFFFFFFFu)
+        q[j] = exact_quantize(s[j], env.area, DPPX_NOISE_KEYED, bits[j], env.sigma, 0.0);
+    }
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+#pragma unroll
+      for (int k = j * GL; k < C && k < (j + 1) * GL; ++k)
+        val[k] = (GL == 1) ? q[j] : __shfl_sync(0xFFFFFFFFu, q[j], gb + (k - j * GL));
+    }
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < NV; ++j) bits[j] = draw_bits(a, stv[j], f, j * GL + li, r, c, sr, sc);
   // Phase 1: branch-free bounded estimates for all channels (independent
   // chains the scheduler can interleave); phase 2: the rare exact draws.
   if (!env.exact_only && (env.kind == DPPX_NOISE_KEYED || env.kind == DPPX_NOISE_PHILOX)) {
@@ -352,7 +376,10 @@ __device__ __forceinline__ void group_values(const StatsArgs& a, const DrawEnv& 
 // barriers, store bookkeeping -- is paid once per 6 draws per lane instead of
 // 3 (the b = 4 kernel is instruction-bound, profiles/r02p_k1_uniform_b4_full.md).
 template <int C, int B4, int NSUB, bool ADAPTIVE, bool PACKED, bool VAR = false, int RPU = 1>
-__global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU > 1 ? 5 : 6) : 0)
+#ifndef DPPX_RPU2_MINB
+#define DPPX_RPU2_MINB 5
+#endif
+__global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU > 1 ? DPPX_RPU2_MINB : 6) : 0)
     k_stats_tma(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
                 const StatsArgs a) {
   constexpr int B = 4 * B4;
@@ -896,7 +923,10 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
     if constexpr (RPU > 1) {
       // Uniform, RPU cell rows of this band: the same per-cell work as below,
       // once per cell row (a band's last rows may lie past the grid: skipped).
-      next = load_meta(s_next, lap_next);
+#ifndef DPPX_META_AT
+#define DPPX_META_AT 2
+#endif
+      if (DPPX_META_AT == 0) next = load_meta(s_next, lap_next);
 #pragma unroll 1
       for (int q = 0; q < RPU; ++q) {
         const int rq = p.r * RPU + q;
@@ -906,6 +936,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
         for (int ch = 0; ch < C; ++ch) tq[ch] = 0;
 #pragma unroll
         for (int i = 0; i < B; ++i) accumulate_row<C>(mystrip + (q * B + i) * srb, tq);
+        if (DPPX_META_AT == 1 && q == RPU - 1) next = load_meta(s_next, lap_next);
 #pragma unroll
         for (int ch = 0; ch < C; ++ch) tq[ch] = group_sum<B4>(tq[ch]);
         uint64_t csq[C];
@@ -932,6 +963,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
           }
         }
       }
+      if (DPPX_META_AT == 2) next = load_meta(s_next, lap_next);
     }
 
     // whole cell (uniform, or adaptive simple): reduce over B4 strips.
