@@ -485,8 +485,7 @@ __global__ void __launch_bounds__(kGenericThreads) k_stats_generic(const StatsAr
           const uint8_t* row = img + static_cast<int64_t>(i) * a.pitch;
           for (int j = j0; j < j0 + w; ++j) sum += row[j * g.C + ch];
         }
-        const uint32_t v = quantize_stat(env, sum, draw_bits(a, cell_state(a, f, ch, r, c), f, ch, r, c, 0, 0),
-                                         inj_at(a, f, ch, gidx, 0, 0));
+        const uint32_t v = draw_stat(a, env, sum, cell_state(a, f, ch, r, c), f, ch, r, c, 0, 0, gidx);
         a.stats[static_cast<int64_t>(f * g.C + ch) * a.sstride + gidx] = static_cast<uint8_t>(v);
         if (a.out) {
           uint8_t* o = a.out + static_cast<int64_t>(f) * a.ofstride;
@@ -509,8 +508,7 @@ __global__ void __launch_bounds__(kGenericThreads) k_stats_generic(const StatsAr
             const uint8_t* row = img + static_cast<int64_t>(reflect_index(i, g.M)) * a.pitch;
             for (int j = j0; j < j0 + side; ++j) sum += row[reflect_index(j, g.N) * g.C + ch];
           }
-          const uint32_t v = quantize_stat(env, sum, draw_bits(a, cs, f, ch, r, c, sr, sc),
-                                           inj_at(a, f, ch, gidx, sr, sc));
+          const uint32_t v = draw_stat(a, env, sum, cs, f, ch, r, c, sr, sc, gidx);
           a.stats[static_cast<int64_t>(f * g.C + ch) * a.sstride +
                   stat_offset(a, simple, gidx, slot_s, S_tot, sr, sc)] = static_cast<uint8_t>(v);
           if (a.out) {
@@ -730,16 +728,14 @@ __global__ void __launch_bounds__(kRowThreads, 4) k_stats_rows(const StatsArgs a
         const int gidx = r * g.GC + c;
         if (!ADAPTIVE) {  // n == 1: the subcell is the cell
           const uint64_t cs = cstate[c * C + ch];
-          const uint32_t v = quantize_stat(env_cell, sum, draw_bits(a, cs, f, ch, r, c, 0, 0),
-                                           inj_at(a, f, ch, gidx, 0, 0));
+          const uint32_t v = draw_stat(a, env_cell, sum, cs, f, ch, r, c, 0, 0, gidx);
           a.stats[static_cast<int64_t>(f * C + ch) * a.sstride + gidx] = static_cast<uint8_t>(v);
           simpleval[c * C + ch] = static_cast<uint8_t>(v);
         } else if (flag[c * C + ch]) {
           atomicAdd(&cellsum[c * C + ch], sum);
         } else {
           const uint64_t cs = cstate[c * C + ch];
-          const uint32_t v = quantize_stat(env_sub, sum, draw_bits(a, cs, f, ch, r, c, vs, sc),
-                                           inj_at(a, f, ch, gidx, vs, sc));
+          const uint32_t v = draw_stat(a, env_sub, sum, cs, f, ch, r, c, vs, sc, gidx);
           a.stats[static_cast<int64_t>(f * C + ch) * a.sstride +
                   stat_offset(a, false, gidx, slot[c], S_tot, vs, sc)] = static_cast<uint8_t>(v);
           if (!L.sub_global) subval[(vs * NS + sidx) * C + ch] = static_cast<uint8_t>(v);
@@ -753,8 +749,7 @@ __global__ void __launch_bounds__(kRowThreads, 4) k_stats_rows(const StatsArgs a
         if (!flag[item]) continue;
         const int gidx = r * g.GC + c;
         const uint64_t cs = cstate[item];
-        const uint32_t v = quantize_stat(env_cell, cellsum[item], draw_bits(a, cs, f, ch, r, c, 0, 0),
-                                         inj_at(a, f, ch, gidx, 0, 0));
+        const uint32_t v = draw_stat(a, env_cell, cellsum[item], cs, f, ch, r, c, 0, 0, gidx);
         a.stats[static_cast<int64_t>(f * C + ch) * a.sstride +
                 stat_offset(a, true, gidx, slot[c], S_tot, 0, 0)] = static_cast<uint8_t>(v);
         simpleval[item] = static_cast<uint8_t>(v);

@@ -875,8 +875,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
             const CellRec& rec = crec[wq][kk];
             const uint32_t sum = csum[wq][rec.cw][rem];
             const uint32_t v =
-                quantize_stat(env_sub, sum, draw_bits(a, cstate[wq][kk][ch], rec.f, ch, p.r, rec.cell, vs, sc2),
-                              inj_at(a, rec.f, ch, rec.gidx, vs, sc2));
+                draw_stat(a, env_sub, sum, cstate[wq][kk][ch], rec.f, ch, p.r, rec.cell, vs, sc2, rec.gidx);
             uint8_t* base = VAR ? a.stage + static_cast<int64_t>(rec.f * C + ch) * a.stage_stride
                                 : a.stats + static_cast<int64_t>(rec.f * C + ch) * a.sstride;
             base[rec.off + sidx] = static_cast<uint8_t>(v);
@@ -1190,8 +1189,7 @@ __global__ void __launch_bounds__(kStatsThreads)
       const int gc = cell0 + c, gidx = p.r * g.GC + gc;
       const uint32_t sum = cellsum[c * C + ch];
       cellsum[c * C + ch] = 0;  // ready for the next unit
-      const uint32_t v = quantize_stat(env_cell, sum, draw_bits(a, cell_state(a, f, ch, p.r, gc), f, ch, p.r, gc, 0, 0),
-                                       inj_at(a, f, ch, gidx, 0, 0));
+      const uint32_t v = draw_stat(a, env_cell, sum, cell_state(a, f, ch, p.r, gc), f, ch, p.r, gc, 0, 0, gidx);
       a.stats[static_cast<int64_t>(f * C + ch) * a.sstride + gidx] = static_cast<uint8_t>(v);
       cellval[c * C + ch] = static_cast<uint8_t>(v);
     }
@@ -1726,9 +1724,8 @@ __global__ void __launch_bounds__(kStatsThreads)
       const int ch = item / ncell, c = item - ch * ncell;
       if (!cflag[c]) continue;
       const int gc = cell0 + c, gidx = p.r * g.GC + gc;
-      const uint32_t v = quantize_stat(env_cell, cellsum[c * C + ch],
-                                       draw_bits(a, cell_state(a, f, ch, p.r, gc), f, ch, p.r, gc, 0, 0),
-                                       inj_at(a, f, ch, gidx, 0, 0));
+      const uint32_t v = draw_stat(a, env_cell, cellsum[c * C + ch], cell_state(a, f, ch, p.r, gc), f, ch, p.r, gc, 0,
+                                   0, gidx);
       a.stats[static_cast<int64_t>(f * C + ch) * a.sstride + stat_offset(a, true, gidx, cslot[c], S_tot, 0, 0)] =
           static_cast<uint8_t>(v);
       cellval[c * C + ch] = static_cast<uint8_t>(v);
@@ -1743,9 +1740,8 @@ __global__ void __launch_bounds__(kStatsThreads)
       const int c = cxlist[kk];
       const int gc = cell0 + c, gidx = p.r * g.GC + gc;
       const int sidx = c * NSUB + sc;
-      const uint32_t v = quantize_stat(env_sub, subsum[(vs * SC + sidx) * C + ch],
-                                       draw_bits(a, cell_state(a, f, ch, p.r, gc), f, ch, p.r, gc, vs, sc),
-                                       inj_at(a, f, ch, gidx, vs, sc));
+      const uint32_t v = draw_stat(a, env_sub, subsum[(vs * SC + sidx) * C + ch], cell_state(a, f, ch, p.r, gc), f, ch,
+                                   p.r, gc, vs, sc, gidx);
       a.stats[static_cast<int64_t>(f * C + ch) * a.sstride + stat_offset(a, false, gidx, cslot[c], S_tot, vs, sc)] =
           static_cast<uint8_t>(v);
       subval[(vs * SC + sidx) * C + ch] = static_cast<uint8_t>(v);

@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(kZcThreads) k_stats_zc(const StatsArgs a, cons
         const int cg = s0 + c;
         const uint64_t cs = cell_state(a, f, ch, r, cg);
         vals[p] = static_cast<uint8_t>(
-            quantize_stat(env, sum, draw_bits(a, cs, f, ch, r, cg, 0, 0), inj_at(a, f, ch, r * g.GC + cg, 0, 0)));
+            draw_stat(a, env, sum, cs, f, ch, r, cg, 0, 0, r * g.GC + cg));
       }
     }
     __syncthreads();
