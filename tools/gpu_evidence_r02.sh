@@ -25,9 +25,15 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_s
     -o ${O}_k0_k1_full $B1 > /dev/null 2>&1; echo "ncu_full_rc=$?"
 ./tests/cpp/_ref_gate/dppix_acceptance_gpu > ${O}_reference_gate_on_dropin.txt 2>&1; echo "gate_rc=$?"
 ./tests/cpp/_ref_gate/dppix_unit_gpu > ${O}_reference_unit_suites_on_dropin.txt 2>&1; echo "unit_rc=$?"
-python tools/latency_probe.py > ${O}_latency.txt 2>&1
-DPPX_ZEROCOPY=1 python tools/latency_probe.py >> ${O}_latency.txt 2>&1
+python tools/latency_probe.py > ${O}_latency.txt 2>&1                       # default: K1z zero-copy
+DPPX_ZEROCOPY=0 python tools/latency_probe.py >> ${O}_latency.txt 2>&1      # CUDA graph
+DPPX_ZEROCOPY=0 DPPX_GRAPH=0 python tools/latency_probe.py >> ${O}_latency.txt 2>&1  # staged
 python tools/latency_probe.py 576 768 3 16 a >> ${O}_latency.txt 2>&1
+DPPX_ZEROCOPY=1 python tools/latency_probe.py 576 768 3 16 a >> ${O}_latency.txt 2>&1
+[ -x tools/pcie_probe ] || nvcc -O2 -gencode arch=compute_100a,code=sm_100a -o tools/pcie_probe tools/pcie_probe.cu
+./tools/pcie_probe > ${O}_pcie_probe.txt 2>&1
+for c in "--b 4 --n 1" "--b 4 --n 1 --eps 0.1" "--b 16 --n 4 --complex 0.5" "--b 16 --n 4"; do
+  echo "$c $(python tools/k1_case.py $c --launches 6 2>&1 | tail -1)" >> ${O}_k1_cases.txt; done
 timeout 900 python tools/b_sweep.py 120 > ${O}_b_sweep.json 2>/dev/null
 timeout 900 python tools/b_sweep.py 120 uniform > ${O}_b_sweep_uniform.json 2>/dev/null
 timeout 900 python tools/k1_complex_sweep.py > ${O}_k1_complex_sweep.json 2>/dev/null
