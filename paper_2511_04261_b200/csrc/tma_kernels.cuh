@@ -289,7 +289,10 @@ __device__ __forceinline__ uint32_t group_sum(uint32_t x) {
 
 // Values of the C channels of one statistic, computed by the GL lanes of a
 // lane group (each lane draws a subset of channels) and shared by shuffles.
-template <int C, int GL>
+// KSPLIT: the keyed case also gets its own exact-fallback and shuffle code
+// (measured faster for wide frames; the packed narrow-frame instantiation
+// spills with it, so it shares them).
+template <int C, int GL, bool KSPLIT = true>
 __device__ __forceinline__ void group_values(const StatsArgs& a, const DrawEnv& env, bool active,
                                              const uint32_t (&sum)[C], const uint64_t (&cs)[C],
                                              int f, int r, int c, int sr, int sc,
@@ -326,34 +329,37 @@ __device__ __forceinline__ void group_values(const StatsArgs& a, const DrawEnv& 
       bits[j] = key_sub(stv[j], sr, sc);
       q[j] = fast_quantize(s[j], env.inv_area, bits[j], env.sln2, env.margin);
     }
+    if constexpr (KSPLIT) {
 #pragma unroll
-    for (int j = 0; j < NV; ++j) {
-      const int ch = j * GL + li;
-      if (active && ch < C && q[j] == 0xFFFFFFFFu)
-        q[j] = exact_quantize(s[j], env.area, DPPX_NOISE_KEYED, bits[j], env.sigma, 0.0);
+      for (int j = 0; j < NV; ++j) {
+        const int ch = j * GL + li;
+        if (active && ch < C && q[j] == 0xFFFFFFFFu)
+          q[j] = exact_quantize(s[j], env.area, DPPX_NOISE_KEYED, bits[j], env.sigma, 0.0);
+      }
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+#pragma unroll
+        for (int k = j * GL; k < C && k < (j + 1) * GL; ++k)
+          val[k] = (GL == 1) ? q[j] : __shfl_sync(0xFFFFFFFFu, q[j], gb + (k - j * GL));
+      }
+      return;
     }
-#pragma unroll
-    for (int j = 0; j < NV; ++j) {
-#pragma unroll
-      for (int k = j * GL; k < C && k < (j + 1) * GL; ++k)
-        val[k] = (GL == 1) ? q[j] : __shfl_sync(0xFFFFFFFFu, q[j], gb + (k - j * GL));
-    }
-    return;
-  }
-#pragma unroll
-  for (int j = 0; j < NV; ++j) bits[j] = draw_bits(a, stv[j], f, j * GL + li, r, c, sr, sc);
-  // Phase 1: branch-free bounded estimates for all channels (independent
-  // chains the scheduler can interleave); phase 2: the rare exact draws.
-  if (!env.exact_only && (env.kind == DPPX_NOISE_KEYED || env.kind == DPPX_NOISE_PHILOX)) {
-#pragma unroll
-    for (int j = 0; j < NV; ++j) q[j] = fast_quantize(s[j], env.inv_area, bits[j], env.sln2, env.margin);
-  } else if (!env.exact_only && env.kind == DPPX_NOISE_NONE && env.pow2) {
-#pragma unroll
-    for (int j = 0; j < NV; ++j)  // sum * 2^-k + 0.5 is exact in f32
-      q[j] = static_cast<uint32_t>(floorf(static_cast<float>(s[j]) * env.inv_area + 0.5f));
   } else {
 #pragma unroll
-    for (int j = 0; j < NV; ++j) q[j] = 0xFFFFFFFFu;
+    for (int j = 0; j < NV; ++j) bits[j] = draw_bits(a, stv[j], f, j * GL + li, r, c, sr, sc);
+    // Phase 1: branch-free bounded estimates for all channels (independent
+    // chains the scheduler can interleave); phase 2: the rare exact draws.
+    if (!env.exact_only && env.kind == DPPX_NOISE_PHILOX) {
+#pragma unroll
+      for (int j = 0; j < NV; ++j) q[j] = fast_quantize(s[j], env.inv_area, bits[j], env.sln2, env.margin);
+    } else if (!env.exact_only && env.kind == DPPX_NOISE_NONE && env.pow2) {
+#pragma unroll
+      for (int j = 0; j < NV; ++j)  // sum * 2^-k + 0.5 is exact in f32
+        q[j] = static_cast<uint32_t>(floorf(static_cast<float>(s[j]) * env.inv_area + 0.5f));
+    } else {
+#pragma unroll
+      for (int j = 0; j < NV; ++j) q[j] = 0xFFFFFFFFu;
+    }
   }
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
@@ -552,7 +558,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
     m.pos = UnitPos{0, 0, 0, 0};
     if (m.u >= 0) {
       const UnitPos q = decode_unit<PACKED, TILE>(a, m.u);
-      m.pos = q;
+      if (!PACKED) m.pos = q;
       const int qf = q.fg * units_pack<PACKED>(a) + jj;
       const int qcell = PACKED ? (q.px0 + lpx) / B : q.px0 / B + sx / B4;
       if (!PACKED || qf < g.F) {
@@ -578,7 +584,9 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
     const Meta cur = next;
     const int u = cur.u;
     if (u < 0) break;
-    const UnitPos p = cur.pos;
+    // (packed units decode here again: carrying the position in Meta costs the
+    // packed instantiation registers it spills)
+    const UnitPos p = PACKED ? decode_unit<PACKED, TILE>(a, u) : cur.pos;
     const int f = p.fg * units_pack<PACKED>(a) + jj;  // this thread's frame
     const int cell = PACKED ? (p.px0 + lpx) / B : p.px0 / B + sx / B4;
     const int lic = sx % B4;       // lane within cell
@@ -717,8 +725,8 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
               acc1[ch] = group_sum<SB4>(acc1[ch]);
             }
             uint32_t val0[C], val1[C];
-            group_values<C, SB4>(a, env_sub, cx, acc0, cs, f, p.r, cell, vs, sc, val0);
-            group_values<C, SB4>(a, env_sub, cx, acc1, cs, f, p.r, cell, vs + 1, sc, val1);
+            group_values<C, SB4, !PACKED>(a, env_sub, cx, acc0, cs, f, p.r, cell, vs, sc, val0);
+            group_values<C, SB4, !PACKED>(a, env_sub, cx, acc1, cs, f, p.r, cell, vs + 1, sc, val1);
             if (cx) {
               if (lic % SB4 == 0) {
                 const int64_t off = stat_offset(a, false, gidx, slot_s, S_tot, vs, sc);
@@ -785,7 +793,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
               }
             } else {
               uint32_t val[C];
-              group_values<C, SB4>(a, env_sub, cx, acc, cs, f, p.r, cell, vs, sc, val);
+              group_values<C, SB4, !PACKED>(a, env_sub, cx, acc, cs, f, p.r, cell, vs, sc, val);
               if (cx) {
                 if (lic % SB4 == 0) {
                   const int64_t off =
@@ -943,7 +951,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
         for (int ch = 0; ch < C; ++ch)
           csq[ch] = a.noise.kind == DPPX_NOISE_KEYED ? key_cell(cur.seed[ch], rq, cell) : 0ull;
         uint32_t val[C];
-        group_values<C, B4>(a, env_cell, rok, tq, csq, f, rq, cell, 0, 0, val);
+        group_values<C, B4, !PACKED>(a, env_cell, rok, tq, csq, f, rq, cell, 0, 0, val);
         if (rok) {
           if (lic == 0) {
             const int64_t off = static_cast<int64_t>(rq) * g.GC + cell;
@@ -971,7 +979,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
     for (int ch = 0; ch < C; ++ch) tot[ch] = group_sum<B4>(tot[ch]);
     {
       uint32_t val[C];
-      group_values<C, B4>(a, env_cell, active && simple, tot, cs, f, p.r, cell, 0, 0, val);
+      group_values<C, B4, !PACKED>(a, env_cell, active && simple, tot, cs, f, p.r, cell, 0, 0, val);
       if (active && simple) {
         if (lic == 0) {
           if constexpr (VAR) {
