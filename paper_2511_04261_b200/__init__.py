@@ -44,6 +44,7 @@ ERR_NOT_A_RECORD, ERR_UNSUPPORTED_VERSION, ERR_CORRUPTION = 6, 7, 8
 NOISE_NONE, NOISE_KEYED, NOISE_PHILOX, NOISE_INJECTED = range(4)
 K_CLASSIFY, K_STATS, K_GENERIC, K_EXPAND, K_AUX, K_ROWS, K_SWEEP, K_ZEROCOPY, K_COUNT = range(9)
 SMALL_AUTO, SMALL_GRAPH, SMALL_ZEROCOPY, SMALL_STAGED = 0, 1, 2, 3
+SMALL_AUTO_ZEROCOPY = ("u", "a")  # modes SMALL_AUTO sends through the zero-copy kernels
 
 KERNEL_FAMILIES = ("classify", "stats_tma", "stats_generic", "expand", "aux", "stats_rows", "sweep",
                    "stats_zerocopy")
@@ -446,13 +447,15 @@ class Context:
 
     # ---- host entry points (numpy in / numpy out)
     def pixelize_uniform(self, frames, params: PrivacyParams, noise=NOISE_NONE, seeds=None,
-                         frame_base=0, injected=None, want_image=True, out=None):
+                         frame_base=0, injected=None, want_image=True, out=None, stats_out=None):
         """frames: uint8 [F,M,N,C] (or [M,N], [M,N,C]). Returns (means[F*C, G], image).
-        `out` (optional, frames' shape) receives the image, e.g. a pinned_empty buffer."""
+        `out` (optional, frames' shape) receives the image, e.g. a pinned_empty buffer;
+        `stats_out` (optional, uint8 [F*C, G], e.g. pinned) receives the means."""
         frames = np.ascontiguousarray(frames, dtype=np.uint8)
         F, M, N, Cn = _frames_shape(frames)
         g = grid_dims(M, N, params.b)
-        means = np.zeros((F * Cn, g.grid_count()), np.uint8)
+        means = np.zeros((F * Cn, g.grid_count()), np.uint8) if stats_out is None else stats_out
+        assert means.shape == (F * Cn, g.grid_count()) and means.dtype == np.uint8 and means.flags.c_contiguous
         out = _out_image(frames, out, want_image)
         nz, keep = self._noise(noise, seeds, frame_base, injected)
         d = _desc(M, N, Cn, F)
@@ -463,15 +466,18 @@ class Context:
         return means, out
 
     def pixelize_adaptive(self, frames, masks, params: PrivacyParams, noise=NOISE_NONE,
-                          seeds=None, frame_base=0, injected=None, want_image=True, out=None):
+                          seeds=None, frame_base=0, injected=None, want_image=True, out=None,
+                          stats_out=None):
         """frames uint8 [F,M,N,C], masks uint8 [F,M,N]. Returns (payloads: list of bytes per
-        plane (f*C + c), image). `out` as in pixelize_uniform."""
+        plane (f*C + c), image). `out` as in pixelize_uniform; `stats_out` (optional,
+        uint8 [F*C, stride], stride >= the payload capacity rounded up to 4) holds the slots."""
         frames = np.ascontiguousarray(frames, dtype=np.uint8)
         F, M, N, Cn = _frames_shape(frames)
         masks = np.ascontiguousarray(masks, dtype=np.uint8).reshape(F, M, N)
         cap = adaptive_payload_capacity(M, N, params.b, params.n)
-        stride = (cap + 3) & ~3
-        buf = np.zeros((F * Cn, stride), np.uint8)
+        stride = (cap + 3) & ~3 if stats_out is None else stats_out.shape[1]
+        buf = np.zeros((F * Cn, stride), np.uint8) if stats_out is None else stats_out
+        assert buf.shape[0] == F * Cn and buf.dtype == np.uint8 and buf.flags.c_contiguous
         lens = np.zeros(F * Cn, np.uint32)
         out = _out_image(frames, out, want_image)
         nz, keep = self._noise(noise, seeds, frame_base, injected)

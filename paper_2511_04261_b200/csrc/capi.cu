@@ -1263,9 +1263,10 @@ int host_single_zerocopy(dppx_ctx* ctx, bool adaptive, const dppx_frames_desc* d
   *used = false;
   const int C = g.C;
   // K1z (uniform): whole cells only, 16-byte rows; it reads exactly the frame.
-  const bool k1z = !adaptive && g.PR == 0 && g.PC == 0 && (C == 1 || C == 3) && g.b <= 64 &&
+  // (adaptive: K0 reads the mapped mask, then the adaptive K1z)
+  const bool k1z = g.PR == 0 && g.PC == 0 && (C == 1 || C == 3) && g.b <= 64 &&
                    (static_cast<int64_t>(g.N) * C) % 16 == 0 && d->pitch % 16 == 0 &&
-                   (!out || d->out_pitch % 16 == 0);
+                   (!out || d->out_pitch % 16 == 0) && (!adaptive || d->mask_pitch >= g.N);
   if (k1z_only && !k1z) return DPPX_OK;
   // K1r: only shapes whose loads never touch a byte past the frame (no padding
   // columns, 16-byte rows): a read past a host allocation would fault.
@@ -1297,8 +1298,13 @@ int host_single_zerocopy(dppx_ctx* ctx, bool adaptive, const dppx_frames_desc* d
     ~Restore() { c->force_rows = false; }
   } restore{ctx};
   ctx->force_rows = true;
-  if (int rc = pixelize_dev(ctx, d, dimg, dmask, pp, nz, nullptr, dst, dstride, adaptive ? dlens : nullptr, dout,
-                            adaptive, ctx->sd[0], ctx->sd_pinned[0], ctx->sd_pinned_n[0], ctx->comp_done[0], true))
+  // Statistics straight into the caller's buffer when it is page-locked too
+  // (no host copy afterwards); else into the ctx's mapped staging.
+  uint8_t* dcaller = static_cast<uint8_t*>(mapped_alias(stats));
+  const int64_t cstride = adaptive ? sstride : static_cast<int64_t>(G);
+  if (int rc = pixelize_dev(ctx, d, dimg, dmask, pp, nz, nullptr, dcaller ? dcaller : dst,
+                            dcaller ? cstride : dstride, adaptive ? dlens : nullptr, dout, adaptive, ctx->sd[0],
+                            ctx->sd_pinned[0], ctx->sd_pinned_n[0], ctx->comp_done[0], true))
     return rc;
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   if (ctx->timing) collect_timings(ctx);
@@ -1308,8 +1314,7 @@ int host_single_zerocopy(dppx_ctx* ctx, bool adaptive, const dppx_frames_desc* d
   const uint32_t* ln = reinterpret_cast<const uint32_t*>(st + static_cast<size_t>(dstride) * C);
   for (int c = 0; c < C; ++c) {
     const size_t w = adaptive ? std::min<size_t>(ln[c], cap) : G;
-    std::memcpy(stats + static_cast<int64_t>(c) * (adaptive ? sstride : static_cast<int64_t>(G)),
-                st + static_cast<int64_t>(c) * dstride, w);
+    if (!dcaller) std::memcpy(stats + static_cast<int64_t>(c) * cstride, st + static_cast<int64_t>(c) * dstride, w);
     if (adaptive && lens) lens[c] = ln[c];
     ctx->kstats.d2h_bytes += w;
   }
@@ -1640,10 +1645,11 @@ int host_pipeline(dppx_ctx* ctx, HostOp op, const dppx_frames_desc* d, const uin
     }
     const int64_t row = static_cast<int64_t>(N) * C;
     const bool small = static_cast<int64_t>(M) * row < (4ll << 20);
-    // auto: zero-copy for uniform frames (K1z streams them over PCIe with the
-    // reads and writes overlapped); adaptive frames take the graph
-    const bool zc_try = ctx->small_path == DPPX_SMALL_ZEROCOPY ||
-                        (ctx->small_path == DPPX_SMALL_AUTO && op == HostOp::Uniform);
+    // auto: zero-copy (K1z streams the frame over PCIe with the reads and
+    // writes overlapped; adaptive: K0 on the mapped mask first, K1z launched
+    // as its programmatic dependent): PETS 59 / 97 us per call against 88 /
+    // 122 us for the graph (profiles/r02_zerocopy.txt)
+    const bool zc_try = ctx->small_path == DPPX_SMALL_ZEROCOPY || ctx->small_path == DPPX_SMALL_AUTO;
     const bool graphs_on = ctx->small_path == DPPX_SMALL_AUTO || ctx->small_path == DPPX_SMALL_GRAPH;
     if (zc_try && F == 1 && small && (op == HostOp::Uniform || op == HostOp::Adaptive) &&
         (!nz || nz->kind != DPPX_NOISE_INJECTED)) {

@@ -330,6 +330,9 @@ __device__ void mask_band_cellsums_bits(const ClassifyArgs& a, const uint8_t* mb
 
 template <bool BAND>
 __global__ void __launch_bounds__(kClassifyThreads, BAND ? 10 : 8) k_classify(const ClassifyArgs a) {
+  // A programmatic dependent (the zero-copy K1z) may start now: it waits for
+  // this grid's results itself (griddepcontrol.wait); no-op for other launches.
+  asm volatile("griddepcontrol.launch_dependents;");
   __shared__ uint32_t warp_tot[kClassifyThreads / 32];
   __shared__ uint32_t s_last;
   extern __shared__ uint32_t colsum[];  // a.band: per padded column mask sums of the band

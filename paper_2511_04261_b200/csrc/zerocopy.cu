@@ -41,7 +41,8 @@ struct ZcArgs {
   int nslab;        // slabs per grid row
   int units;        // F * GR * nslab
   int unit_stride;  // bytes of one ring slot (>= b * S * b * C, 16-byte multiple)
-  int vals_bytes;   // S * C rounded up to 16
+  int vals_bytes;   // S * C (adaptive: S * n * n * C) rounded up to 16
+  int pattern_bytes;  // adaptive: n * S * b * C rounded up to 16
 };
 
 template <int C>
@@ -128,6 +129,125 @@ __global__ void __launch_bounds__(kZcThreads) k_stats_zc(const StatsArgs a, cons
   }
 }
 
+// Adaptive (pixelize_adaptive, adaptive.cpp:88-179) counterpart: K0 has
+// classified the cells (cellinfo / rowprefix / totals in HBM, the mask means
+// already in the payload); the frame streams in as above. A warp takes one
+// (cell, channel): a simple cell is one sum over b x b pixels drawn at sigma,
+// a complex cell n x n subcell sums (one lane per subcell) drawn at sigma_sub;
+// values go to the payload slot (stat_offset) and into a per-unit table
+// vals[cell][sr][sc][ch], from which one pattern row per vertical subcell
+// band is built and stored sb times.
+template <int C>
+__global__ void __launch_bounds__(kZcThreads) k_adaptive_zc(const StatsArgs a, const ZcArgs z) {
+  extern __shared__ __align__(16) uint8_t zs[];
+  const BatchGeom& g = a.g;
+  const int b = g.b, n = g.n, sb = g.sb, NN = n * n;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  uint8_t* vals = zs + 2 * z.unit_stride;              // S * n * n * C
+  uint8_t* pattern = vals + z.vals_bytes;              // n rows of S * b * C
+  uint32_t* meta = reinterpret_cast<uint32_t*>(pattern + z.pattern_bytes);  // S cell infos
+  const DrawEnv env_cell = make_env(a.noise.kind, a.exact_noise != 0, a.area, a.sigma);
+  const DrawEnv env_sub = make_env(a.noise.kind, a.exact_noise != 0, a.sub_area, a.sigma_sub);
+  auto coords = [&](int u, int& f, int& r, int& s) {
+    s = u % z.nslab;
+    const int q = u / z.nslab;
+    r = q % g.GR;
+    f = q / g.GR;
+  };
+  auto issue = [&](int u, uint8_t* dst) {
+    int f, r, s;
+    coords(u, f, r, s);
+    const int s0 = s * z.S, su = min(z.S, g.GC - s0);
+    const int sbytes = su * b * C, per_row = sbytes >> 4;
+    const uint8_t* src = a.img + static_cast<int64_t>(f) * a.fstride + static_cast<int64_t>(r) * b * a.pitch +
+                         static_cast<int64_t>(s0) * b * C;
+    for (int i = t; i < per_row * b; i += kZcThreads) {
+      const int y = i / per_row, q = i - y * per_row;
+      zc_cp16(dst + y * sbytes + q * 16, src + static_cast<int64_t>(y) * a.pitch + q * 16);
+    }
+    zc_commit();
+  };
+  int u = blockIdx.x;
+  if (u < z.units) issue(u, zs);
+  // The frame loads above do not depend on K0; its classification does.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  for (int k = 0; u < z.units; ++k, u += gridDim.x) {
+    const int un = u + gridDim.x;
+    if (un < z.units) {
+      issue(un, zs + ((k + 1) & 1) * z.unit_stride);
+      zc_wait<1>();
+    } else {
+      zc_wait<0>();
+    }
+    int f, r, s;
+    coords(u, f, r, s);
+    const int s0 = s * z.S, su = min(z.S, g.GC - s0), sbytes = su * b * C;
+    for (int c = t; c < su; c += kZcThreads)
+      meta[c] = __ldg(&a.cellinfo[static_cast<int64_t>(f) * g.G + r * g.GC + s0 + c]);
+    __syncthreads();
+    const uint8_t* tile = zs + (k & 1) * z.unit_stride;
+    const uint32_t rowpre = __ldg(&a.rowprefix[static_cast<int64_t>(f) * g.GR + r]);
+    const uint32_t S_tot = __ldg(&a.totals[f]);
+    for (int p = w; p < su * C; p += kZcThreads / 32) {
+      const int c = p / C, ch = p - c * C;
+      const int cg = s0 + c, gidx = r * g.GC + cg;
+      const uint32_t info = meta[c];
+      const bool simple = info & 1u;
+      const uint32_t slot_s = rowpre + (info >> 1);
+      const uint64_t cs = cell_state(a, f, ch, r, cg);
+      uint8_t* plane = a.stats + static_cast<int64_t>(f * C + ch) * a.sstride;
+      uint8_t* cv = vals + static_cast<int64_t>(c) * NN * C + ch;  // vals[c][sr][sc][ch]
+      if (simple) {
+        uint32_t sum = 0;
+        for (int i = lane; i < b * b; i += 32) {
+          const int y = i / b, x = i - y * b;
+          sum += tile[y * sbytes + (c * b + x) * C + ch];
+        }
+        sum = __reduce_add_sync(0xffffffffu, sum);
+        uint32_t v = 0;
+        if (lane == 0) {
+          v = draw_stat(a, env_cell, sum, cs, f, ch, r, cg, 0, 0, gidx);
+          plane[stat_offset(a, true, gidx, slot_s, S_tot, 0, 0)] = static_cast<uint8_t>(v);
+        }
+        v = __shfl_sync(0xffffffffu, v, 0);
+        for (int i = lane; i < NN; i += 32) cv[i * C] = static_cast<uint8_t>(v);
+      } else {
+        for (int i = lane; i < NN; i += 32) {
+          const int sr = i / n, sc = i - sr * n;
+          uint32_t sum = 0;
+          for (int y = sr * sb; y < sr * sb + sb; ++y) {
+            const uint8_t* row = tile + y * sbytes + (c * b + sc * sb) * C + ch;
+            for (int x = 0; x < sb; ++x) sum += row[x * C];
+          }
+          const uint32_t v = draw_stat(a, env_sub, sum, cs, f, ch, r, cg, sr, sc, gidx);
+          plane[stat_offset(a, false, gidx, slot_s, S_tot, sr, sc)] = static_cast<uint8_t>(v);
+          cv[i * C] = static_cast<uint8_t>(v);
+        }
+      }
+    }
+    __syncthreads();
+    if (a.out) {
+      // one pattern row per vertical subcell band
+      for (int e = t; e < n * sbytes; e += kZcThreads) {
+        const int sr = e / sbytes, x = e - sr * sbytes;
+        const int px = x / C, ch = x - px * C;
+        const int c = px / b, sc = (px - c * b) / sb;
+        pattern[e] = vals[((c * n + sr) * n + sc) * C + ch];
+      }
+      __syncthreads();
+      uint8_t* dst = a.out + static_cast<int64_t>(f) * a.ofstride + static_cast<int64_t>(r) * b * a.opitch +
+                     static_cast<int64_t>(s0) * b * C;
+      const int per_row = sbytes >> 4;
+      for (int i = t; i < per_row * b; i += kZcThreads) {
+        const int y = i / per_row, q = i - y * per_row;
+        *reinterpret_cast<uint4*>(dst + static_cast<int64_t>(y) * a.opitch + q * 16) =
+            reinterpret_cast<const uint4*>(pattern + (y / sb) * sbytes)[q];
+      }
+    }
+    __syncthreads();  // ring slot, tables and pattern free for reuse
+  }
+}
+
 // *launched = false if the shape is not eligible; else launches (dry_run: only
 // reports eligibility). `unit_target`: bytes per unit (<= 16 KB), `ctas`: grid
 // (0: automatic).
@@ -136,8 +256,8 @@ cudaError_t launch_stats_zc(const StatsArgs& a, int unit_target, int ctas, int s
   *launched = false;
   const BatchGeom& g = a.g;
   const int b = g.b, C = g.C;
-  if (a.adaptive || g.n != 1 || g.PR != 0 || g.PC != 0 || a.partial_borders || a.row_begin != 0 ||
-      a.row_count != g.GR || (C != 1 && C != 3) || b > 64)
+  if ((!a.adaptive && g.n != 1) || g.PR != 0 || g.PC != 0 || a.partial_borders || a.row_begin != 0 ||
+      a.row_count != g.GR || (C != 1 && C != 3) || b > 64 || a.var_flags)
     return cudaSuccess;
   if ((static_cast<int64_t>(g.N) * C) % 16 || a.pitch % 16 || a.fstride % 16 ||
       (reinterpret_cast<uintptr_t>(a.img) & 15))
@@ -165,13 +285,17 @@ cudaError_t launch_stats_zc(const StatsArgs& a, int unit_target, int ctas, int s
   if (units > 0x7FFFFFFF) return cudaSuccess;
   z.units = static_cast<int>(units);
   z.unit_stride = (S * b * b * C + 127) / 128 * 128;
-  z.vals_bytes = (S * C + 15) / 16 * 16;
-  const size_t smem = 2 * static_cast<size_t>(z.unit_stride) + z.vals_bytes + static_cast<size_t>(S) * b * C;
+  const int nn = a.adaptive ? g.n * g.n : 1;
+  z.vals_bytes = (S * nn * C + 15) / 16 * 16;
+  z.pattern_bytes = ((a.adaptive ? g.n : 1) * S * b * C + 15) / 16 * 16;
+  const size_t smem = 2 * static_cast<size_t>(z.unit_stride) + z.vals_bytes + z.pattern_bytes +
+                      (a.adaptive ? 4 * static_cast<size_t>(S) : 0);
+  if (smem > 200 * 1024) return cudaSuccess;
   if (dry_run) {
     *launched = true;
     return cudaSuccess;
   }
-  auto k = C == 1 ? k_stats_zc<1> : k_stats_zc<3>;
+  auto k = a.adaptive ? (C == 1 ? k_adaptive_zc<1> : k_adaptive_zc<3>) : (C == 1 ? k_stats_zc<1> : k_stats_zc<3>);
   if (cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)))
     return e;
   // Default: about three units per CTA, so each CTA's PCIe reads of its next
@@ -179,7 +303,24 @@ cudaError_t launch_stats_zc(const StatsArgs& a, int unit_target, int ctas, int s
   int grid = ctas > 0 ? ctas : (z.units + 2) / 3;
   grid = grid < 1 ? 1 : (grid > 4 * sms ? 4 * sms : grid);
   if (grid > z.units) grid = z.units;
-  k<<<grid, kZcThreads, smem, s>>>(a, z);
+  if (a.adaptive) {
+    // Programmatic dependent launch: the kernel starts while K0 (which
+    // releases its dependents at entry) still runs, streams its first frame
+    // units in, and waits for K0's results at griddepcontrol.wait.
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kZcThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaError_t e = cudaLaunchKernelEx(&cfg, k, a, z)) return e;
+  } else {
+    k<<<grid, kZcThreads, smem, s>>>(a, z);
+  }
   *launched = true;
   return cudaGetLastError();
 }

@@ -1199,26 +1199,32 @@ def test_host_sweep_equals_separate_host_runs(ctx, M, N, C, F, bl, el):
     assert imgs2 is None and all(np.array_equal(a, b) for a, b in zip(means, means2))
 
 
-@pytest.mark.parametrize("M,N,C,b,mode", [
-    (576, 768, 3, 16, "u"),   # PETS: K1z
-    (64, 64, 1, 4, "u"),
-    (96, 128, 3, 32, "u"),
-    (120, 160, 3, 8, "u"),
-    (128, 192, 3, 64, "u"),
-    (100, 120, 3, 16, "u"),   # padded rows: not K1z, auto takes the graph
-    (576, 768, 3, 16, "a"),
+@pytest.mark.parametrize("M,N,C,b,n,mode", [
+    (576, 768, 3, 16, 1, "u"),   # PETS: K1z
+    (64, 64, 1, 4, 1, "u"),
+    (96, 128, 3, 32, 1, "u"),
+    (120, 160, 3, 8, 1, "u"),
+    (128, 192, 3, 64, 1, "u"),
+    (100, 120, 3, 16, 1, "u"),   # padded rows: not K1z, auto takes the graph
+    (576, 768, 3, 16, 4, "a"),   # adaptive K1z (K0 on the mapped mask first)
+    (64, 64, 1, 8, 2, "a"),
+    (96, 128, 3, 32, 8, "a"),
+    (128, 192, 3, 64, 16, "a"),
+    (120, 160, 3, 8, 4, "a"),    # 2-px subcells
+    (100, 120, 3, 16, 4, "a"),   # padded: no K1z
 ])
-def test_small_frame_paths_agree(ctx, M, N, C, b, mode):
+def test_small_frame_paths_agree(ctx, M, N, C, b, n, mode):
     """One small pinned frame through every small-frame path (auto, graph,
-    zero-copy -- K1z for uniform whole-cell shapes --, staged) gives the same
+    zero-copy -- K1z for whole-cell shapes --, staged) gives the same
     statistics and image, equal to the oracle."""
     rng = np.random.default_rng(M * N + b)
     fr = dp.pinned_empty((1, M, N, C))
     fr[:] = rng.integers(0, 256, fr.shape, dtype=np.uint8)
     mk = dp.pinned_empty((1, M, N))
     mk[:] = (rng.random((1, M, N)) < 0.5).astype(np.uint8)
-    p = dp.make_privacy_params(0.5, 16, b, 4 if mode == "a" else 1)
+    p = dp.make_privacy_params(0.5, 16, b, n)
     seeds = dp.plane_seeds(77, 1, C)
+    k1z = M % b == 0 and N % b == 0 and (N * C) % 16 == 0
     res = {}
     try:
         for path in (dp.SMALL_STAGED, dp.SMALL_GRAPH, dp.SMALL_ZEROCOPY, dp.SMALL_AUTO):
@@ -1233,11 +1239,19 @@ def test_small_frame_paths_agree(ctx, M, N, C, b, mode):
                     st, img = ctx.pixelize_adaptive(fr, mk, p, dp.NOISE_KEYED, seeds, out=out)
                 res.setdefault(path, (st, np.array(img)))
                 launches = ctx.stats()["launches"]
-                k1z = (mode == "u" and M % b == 0 and N % b == 0 and (N * C) % 16 == 0)
-                if path in (dp.SMALL_ZEROCOPY, dp.SMALL_AUTO) and k1z:
-                    assert launches["stats_zerocopy"] == 1, launches
-                else:
-                    assert launches["stats_zerocopy"] == 0, launches
+                if rep == 1:  # page-locked statistics buffer: written in place by K1z
+                    cap = dp.adaptive_payload_capacity(M, N, b, n) if mode == "a" else 0
+                    pst = dp.pinned_empty((C, (cap + 3) & ~3 if mode == "a" else
+                                           dp.grid_dims(M, N, b).grid_count()))
+                    if mode == "u":
+                        st2, img2 = ctx.pixelize_uniform(fr, p, dp.NOISE_KEYED, seeds, stats_out=pst)
+                        assert np.array_equal(st2, res[path][0]), path
+                    else:
+                        st2, img2 = ctx.pixelize_adaptive(fr, mk, p, dp.NOISE_KEYED, seeds, stats_out=pst)
+                        assert st2 == res[path][0], path
+                    assert np.array_equal(img2, res[path][1]), path
+                zc = path == dp.SMALL_ZEROCOPY or (path == dp.SMALL_AUTO and mode in dp.SMALL_AUTO_ZEROCOPY)
+                assert launches["stats_zerocopy"] == (1 if zc and k1z else 0), (path, launches)
     finally:
         ctx.set_small_frame_path(dp.SMALL_AUTO)
     ref_st, ref_img = res[dp.SMALL_STAGED]
@@ -1250,4 +1264,9 @@ def test_small_frame_paths_agree(ctx, M, N, C, b, mode):
     if mode == "u":
         rm, ri = oracle.pixelize_uniform(np.ascontiguousarray(fr[0]), b, p.sigma, "keyed", seeds)
         assert np.array_equal(ref_st, rm)
+        assert np.array_equal(ref_img[0].reshape(-1), np.asarray(ri).reshape(-1))
+    else:
+        rp, ri = oracle.pixelize_adaptive(np.ascontiguousarray(fr[0]), np.ascontiguousarray(mk[0]), b, n,
+                                          p.sigma, p.sigma_sub, "keyed", seeds)
+        assert list(ref_st) == list(rp)
         assert np.array_equal(ref_img[0].reshape(-1), np.asarray(ri).reshape(-1))
