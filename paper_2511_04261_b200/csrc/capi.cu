@@ -79,7 +79,7 @@ struct SweepLevels {  // sweep.cu
   int64_t G[kSweepMaxLevels];
   double area[kSweepMaxLevels];
   double sigma[kSweepMaxLevels][kSweepMaxEps];
-  float sigmaf[kSweepMaxLevels][kSweepMaxEps];
+  float sln2[kSweepMaxLevels][kSweepMaxEps];  // f32(sigma * ln 2)
   float margin[kSweepMaxLevels][kSweepMaxEps];
   uint8_t* means[kSweepMaxLevels][kSweepMaxEps];
   void* sums[kSweepMaxLevels];
@@ -2374,7 +2374,7 @@ int dppx_pixelize_uniform_sweep_dev(dppx_ctx* ctx, const dppx_frames_desc* d, co
     const int lv = b_list[i] == 4 ? 0 : b_list[i] == 8 ? 1 : b_list[i] == 16 ? 2 : 3;
     for (int j = 0; j < ne; ++j) {
       L.sigma[lv][j] = pp[i * ne + j].sigma;
-      L.sigmaf[lv][j] = static_cast<float>(pp[i * ne + j].sigma);
+      L.sln2[lv][j] = static_cast<float>(pp[i * ne + j].sigma * 0.6931471805599453);
       L.margin[lv][j] = fast_margin(pp[i * ne + j].sigma);
       L.means[lv][j] = means[i * ne + j];
     }

@@ -37,7 +37,7 @@ struct SweepLevels {
   int64_t G[kSweepMaxLevels];
   double area[kSweepMaxLevels];
   double sigma[kSweepMaxLevels][kSweepMaxEps];
-  float sigmaf[kSweepMaxLevels][kSweepMaxEps];
+  float sln2[kSweepMaxLevels][kSweepMaxEps];  // f32(sigma * ln 2)
   float margin[kSweepMaxLevels][kSweepMaxEps];
   uint8_t* means[kSweepMaxLevels][kSweepMaxEps];  // run (k, j): F*C planes of G[k] bytes
   // level sums written by K1s-sum: plane p, cell (r, c) of level k at
@@ -224,16 +224,20 @@ struct ExactJob {
   uint16_t lv, j;
 };
 
-// f32 Laplace magnitude of 64 keyed bits (see fast_quantize, dppx_device.cuh,
-// for the error budget): L = -ln(1 - 2|u|), sign from the top bits.
-__device__ __forceinline__ float laplace_mag(uint64_t bits, bool& neg) {
+// Signed f32 Laplace magnitude of 64 keyed bits in log2 units,
+// +-(-log2(1 - 2|u|)) (the noise is this times sigma * ln 2; see fast_quantize,
+// dppx_device.cuh, for the arithmetic and its error budget).
+__device__ __forceinline__ float laplace_log2_signed(uint64_t bits) {
   const uint64_t y = bits >> 11;
-  neg = static_cast<int32_t>(bits >> 32) >= 0;
+  uint32_t lo_w, hi_w;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo_w), "=r"(hi_w) : "l"(bits));
+  const bool neg = static_cast<int32_t>(hi_w) >= 0;
   const uint64_t W = neg ? y : (1ull << 53) - y;
   const uint32_t wb = __float_as_uint(fmaxf(__ull2float_rn(W), 1.0f));
   const int e = static_cast<int>(wb >> 23) - 127;
   const float lg_m = lg2_approx(__uint_as_float(0x3F800000u | (wb & 0x7FFFFFu)));
-  return (static_cast<float>(52 - e) - lg_m) * 0.693147180559945f;
+  const float L2 = static_cast<float>(52 - e) - lg_m;
+  return neg ? -L2 : L2;
 }
 
 template <int NE, int KIND>
@@ -310,26 +314,26 @@ __global__ void __launch_bounds__(kDrawThreads)
       }
       off = static_cast<int64_t>(plane) * L.G[lv] + static_cast<int64_t>(r) * GCk + c0;
     }
-    // quantize every cell for every eps; 4 bytes per run at once when aligned
-    float Lf[4];
-    bool neg[4];
+    // quantize every cell for every eps; 4 bytes per run at once when aligned.
+    // The mean + 0.5 and the signed log2 magnitude do not depend on eps: one
+    // FFMA per (cell, eps) remains (the same arithmetic as fast_quantize).
+    float Ls[4], m5[4];
     const float inv_area = any ? 1.0f / static_cast<float>(L.area[lv]) : 0.0f;
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
-      neg[v] = false;
-      Lf[v] = kind == DPPX_NOISE_NONE ? 0.0f : laplace_mag(bits[v], neg[v]);
+      m5[v] = fmaf(static_cast<float>(sum[v]), inv_area, 0.5f);
+      Ls[v] = kind == DPPX_NOISE_NONE ? 0.0f : laplace_log2_signed(bits[v]);
     }
 #pragma unroll
     for (int j = 0; j < ne; ++j) {
       uint32_t amb = 0;  // cells whose estimate is ambiguous
       if (any && nvalid > 0) {
-        const float sf = L.sigmaf[lv][j], mg = L.margin[lv][j];
+        const float sl = L.sln2[lv][j], mg = L.margin[lv][j];
         uint32_t word = 0;
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
           uint32_t q;
-          const float t = static_cast<float>(sum[v]) * inv_area + 0.5f +
-                          (kind == DPPX_NOISE_NONE ? 0.0f : (neg[v] ? -sf * Lf[v] : sf * Lf[v]));
+          const float t = kind == DPPX_NOISE_NONE ? m5[v] : fmaf(Ls[v], sl, m5[v]);
           if (kind == DPPX_NOISE_NONE) {
             q = static_cast<uint32_t>(floorf(t));  // area = 16^k: exact in f32
           } else {
@@ -416,3 +420,4 @@ cudaError_t launch_sweep_draw(const StatsArgs& a, const SweepLevels& L, int max_
 int sweep_draw_threads() { return kDrawThreads; }
 
 }  // namespace dppx
+
