@@ -182,12 +182,14 @@ __global__ void __launch_bounds__(kZcThreads) k_adaptive_zc(const StatsArgs a, c
     int f, r, s;
     coords(u, f, r, s);
     const int s0 = s * z.S, su = min(z.S, g.GC - s0), sbytes = su * b * C;
+    // (K0's results, written by a grid that may still have been running when
+    // this one started: read through L2, not the non-coherent path)
     for (int c = t; c < su; c += kZcThreads)
-      meta[c] = __ldg(&a.cellinfo[static_cast<int64_t>(f) * g.G + r * g.GC + s0 + c]);
+      meta[c] = __ldcg(&a.cellinfo[static_cast<int64_t>(f) * g.G + r * g.GC + s0 + c]);
     __syncthreads();
     const uint8_t* tile = zs + (k & 1) * z.unit_stride;
-    const uint32_t rowpre = __ldg(&a.rowprefix[static_cast<int64_t>(f) * g.GR + r]);
-    const uint32_t S_tot = __ldg(&a.totals[f]);
+    const uint32_t rowpre = __ldcg(&a.rowprefix[static_cast<int64_t>(f) * g.GR + r]);
+    const uint32_t S_tot = __ldcg(&a.totals[f]);
     for (int p = w; p < su * C; p += kZcThreads / 32) {
       const int c = p / C, ch = p - c * C;
       const int cg = s0 + c, gidx = r * g.GC + cg;
