@@ -46,7 +46,7 @@ cudaError_t launch_stats_tma(StatsKernel k, const CUtensorMap& tin, const CUtens
 cudaError_t launch_stats_generic(const StatsArgs& a, cudaStream_t s);
 cudaError_t launch_expand(const ExpandArgs& a, cudaStream_t s);
 using ExpandKernel = void (*)(const CUtensorMap, const ExpandArgs);
-ExpandKernel select_expand_kernel(int C, int b, int n, bool adaptive, bool packed);
+ExpandKernel select_expand_kernel(int C, int b, int n, bool adaptive, bool packed, int split);
 cudaError_t launch_expand_tma(ExpandKernel k, const CUtensorMap& tout, const ExpandArgs& a,
                               int grid, size_t smem, cudaStream_t s);
 cudaError_t launch_synth(const BatchGeom& g, uint32_t seed, uint32_t f0, uint8_t* img,
@@ -897,20 +897,34 @@ int expand_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* stats, i
     }
   }
   e.slot_stride = static_cast<int>(round_up(static_cast<int64_t>(g.b) * e.slot_px * g.C, 128));
+  // b = 32 / 64 wide frames: each band split into units of b/split rows (a
+  // fraction of the smem per CTA, so more CTAs per SM hide the statistics
+  // loads; DPPX_K2_SPLIT=1 disables, 2 / 4 force a split)
+  // Measured (tools/k2_split_sweep.sh, profiles/r02ii_k2_split.txt): 16-row
+  // units are best for every b = 32 / 64 case but b = 32 n = 4 (8 rows).
+  static const int split_env = std::getenv("DPPX_K2_SPLIT") ? std::atoi(std::getenv("DPPX_K2_SPLIT")) : 0;
+  ExpandKernel k = nullptr;
+  int unit_rows = g.b;
+  if (e.pack == 1 && (g.b == 32 || g.b == 64)) {
+    const int want = split_env > 0 ? split_env : (g.b == 32 && g.n == 4 ? 4 : g.b / 16);
+    for (int sp : {want, 2})
+      if (!k && sp > 1 && (k = select_expand_kernel(g.C, g.b, g.n, adaptive, false, sp))) unit_rows = g.b / sp;
+  }
+  if (!k) k = select_expand_kernel(g.C, g.b, g.n, adaptive, e.pack > 1, 1);
+  if (unit_rows != g.b) stage_bytes = static_cast<int64_t>(unit_rows) * tile * g.C;
   e.stage_bytes = static_cast<int>(round_up(stage_bytes, 128));
-  ExpandKernel k = select_expand_kernel(g.C, g.b, g.n, adaptive, e.pack > 1);
   CUtensorMap tout{};
   const bool aligned = aligned16(out) && e.opitch % 16 == 0 && e.ofstride % 16 == 0;
   const int box_bytes = e.slot_px * g.C;
   if (k && aligned && box_bytes / 8 <= 256 &&
       encode_frames_map(&tout, out, out_map_row_bytes(ctx, row_bytes, e.opitch), g.M, g.F, e.opitch, e.ofstride,
-                        box_bytes, g.b)) {
+                        box_bytes, unit_rows)) {
     e.tiles_per_row = e.pack > 1 ? 1 : (padded_px + tile - 1) / tile;
     e.tensor_out_bytes = static_cast<int>(out_map_row_bytes(ctx, row_bytes, e.opitch));
     e.div_tiles = make_fastdiv(static_cast<uint32_t>(e.tiles_per_row));
     e.div_rows = make_fastdiv(static_cast<uint32_t>(g.GR));
     const int64_t groups = (g.F + e.pack - 1) / e.pack;
-    const int64_t units = groups * g.GR * e.tiles_per_row;
+    const int64_t units = groups * g.GR * e.tiles_per_row * (g.b / unit_rows);
     if (units > 0x7FFFFFFF) return set_err(ctx, DPPX_ERR_INVALID, "batch too large for one launch");
     e.units = static_cast<int>(units);
     // One unit per CTA (many short CTAs hide the statistics-load latency

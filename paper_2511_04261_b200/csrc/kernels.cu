@@ -1179,7 +1179,7 @@ StatsKernel select_stats_kernel(int C, int b, int n, bool adaptive, bool packed)
   return nullptr;
 }
 
-ExpandKernel select_expand_kernel(int C, int b, int n, bool adaptive, bool packed) {
+ExpandKernel select_expand_kernel(int C, int b, int n, bool adaptive, bool packed, int split) {
   if (!adaptive && n != 1) return nullptr;
   if (adaptive && !packed && (b % 4 != 0 || b == 128)) {  // K2a
     if (C == 1) return select_expand_aany_c1(b, n);
@@ -1191,8 +1191,8 @@ ExpandKernel select_expand_kernel(int C, int b, int n, bool adaptive, bool packe
     if (C == 3) return select_expand_uany_c3(b);
     return nullptr;
   }
-  if (C == 1) return select_expand_tma_c1(b, n, adaptive, packed);
-  if (C == 3) return select_expand_tma_c3(b, n, adaptive, packed);
+  if (C == 1) return select_expand_tma_c1(b, n, adaptive, packed, split);
+  if (C == 3) return select_expand_tma_c3(b, n, adaptive, packed, split);
   return nullptr;
 }
 

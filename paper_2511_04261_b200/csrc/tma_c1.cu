@@ -21,7 +21,10 @@ ExpandKernel select_expand_uany_c1(int b) { return pick_expand_uany<1>(b); }
 
 ExpandKernel select_expand_aany_c1(int b, int n) { return pick_expand_aany<1>(b, n); }
 
-ExpandKernel select_expand_tma_c1(int b, int n, bool adaptive, bool packed) {
+ExpandKernel select_expand_tma_c1(int b, int n, bool adaptive, bool packed, int split) {
+  if (split == 2 && !packed) return adaptive ? pick_expand_split<1, true, 2>(b, n) : pick_expand_split<1, false, 2>(b, n);
+  if (split == 4 && !packed) return adaptive ? pick_expand_split<1, true, 4>(b, n) : pick_expand_split<1, false, 4>(b, n);
+  if (split > 1) return nullptr;
   if (packed) return adaptive ? pick_expand<1, true, true>(b, n) : pick_expand<1, false, true>(b, n);
   return adaptive ? pick_expand<1, true, false>(b, n) : pick_expand<1, false, false>(b, n);
 }

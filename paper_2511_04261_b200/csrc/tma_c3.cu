@@ -21,7 +21,10 @@ ExpandKernel select_expand_uany_c3(int b) { return pick_expand_uany<3>(b); }
 
 ExpandKernel select_expand_aany_c3(int b, int n) { return pick_expand_aany<3>(b, n); }
 
-ExpandKernel select_expand_tma_c3(int b, int n, bool adaptive, bool packed) {
+ExpandKernel select_expand_tma_c3(int b, int n, bool adaptive, bool packed, int split) {
+  if (split == 2 && !packed) return adaptive ? pick_expand_split<3, true, 2>(b, n) : pick_expand_split<3, false, 2>(b, n);
+  if (split == 4 && !packed) return adaptive ? pick_expand_split<3, true, 4>(b, n) : pick_expand_split<3, false, 4>(b, n);
+  if (split > 1) return nullptr;
   if (packed) return adaptive ? pick_expand<3, true, true>(b, n) : pick_expand<3, false, true>(b, n);
   return adaptive ? pick_expand<3, true, false>(b, n) : pick_expand<3, false, false>(b, n);
 }

@@ -1233,10 +1233,18 @@ __global__ void __launch_bounds__(kStatsThreads)
 // more frame slots per CTA (5 CelebA frames instead of 2).
 constexpr int kExpandPackedThreads = 256;
 
-template <int C, int B4, int NSUB, bool ADAPTIVE, bool PACKED>
+// HALF: a unit is half a band (B/2 rows; b >= 32): half the smem per CTA, so
+// twice the CTAs per SM hide the statistics-load latency (4K b32 n8: a 49 KB
+// tile allowed 4 CTAs/SM).
+template <int C, int B4, int NSUB, bool ADAPTIVE, bool PACKED, int H = 1>
 __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
     k_expand_tma(const __grid_constant__ CUtensorMap tm_out, const ExpandArgs a) {
   constexpr int B = 4 * B4, SB = B / NSUB, SB4 = SB / 4;
+  constexpr bool HALF = H > 1;
+  constexpr int RU = B / H;                             // rows per unit
+  constexpr int NV = NSUB >= H ? NSUB / H : 1;          // vertical subcells per unit
+  constexpr int SBR = NSUB >= H ? SB : RU;              // rows per emitted subcell
+  static_assert(!HALF || (!PACKED && (NSUB == 1 || NSUB % H == 0) && RU % 4 == 0), "band-split geometry");
   constexpr bool STR = (SB % 4) != 0;  // strips meet two subcells (as K1)
   static_assert(!STR || (ADAPTIVE && !PACKED && SB >= 2), "split strips: wide adaptive frames");
   constexpr int LPW = (32 / B4) * B4;                    // whole cells per warp (as K1)
@@ -1264,11 +1272,14 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
     // A capped grid loops: the previous unit's store must have read the tile.
     if (t == 0 && k > 0) bulk_wait_read_all();
     __syncthreads();
-    const uint32_t rest = a.div_tiles.div(static_cast<uint32_t>(u));
-    const int tile = u - static_cast<int>(rest * a.div_tiles.d);
+    const int hh = HALF ? (u % H) : 0;  // which part of the band
+    const int uu = HALF ? (u / H) : u;
+    const uint32_t rest = a.div_tiles.div(static_cast<uint32_t>(uu));
+    const int tile = uu - static_cast<int>(rest * a.div_tiles.d);
     const uint32_t fq = a.div_rows.div(rest);
     const int r = static_cast<int>(rest - fq * a.div_rows.d);
     const int fg = static_cast<int>(fq);
+    const int row0 = r * B + hh * RU;  // first frame row of this unit
     const int pk = PACKED ? a.pack : 1;
     const int nf = PACKED ? min(pk, g.F - fg * pk) : 1;
     const int f = fg * pk + jj;
@@ -1276,8 +1287,8 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
     const int cell = (px0 + lpx) / B;
     const bool active = in_slot && jj < nf && cell < g.GC;
     const int gidx = r * g.GC + cell;
-    uint32_t val[NSUB][C];
-    uint32_t valb[STR ? NSUB : 1][C];  // STR: the strip's second subcell
+    uint32_t val[NV][C];
+    uint32_t valb[STR ? NV : 1][C];  // STR: the strip's second subcell
     if (active) {
 #pragma unroll
       for (int ch = 0; ch < C; ++ch) {
@@ -1286,7 +1297,7 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
         if constexpr (!ADAPTIVE) {
           const uint32_t v = __ldg(st + gidx);
 #pragma unroll
-          for (int vs = 0; vs < NSUB; ++vs) val[vs][ch] = v;
+          for (int vs = 0; vs < NV; ++vs) val[vs][ch] = v;
         } else {
           const uint32_t info = __ldg(&a.cellinfo[plane * g.G + gidx]);
           const uint32_t slot_s = __ldg(&a.rowprefix[plane * g.GR + r]) + (info >> 1);
@@ -1294,7 +1305,7 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
           if (info & 1u) {
             const uint32_t v = __ldg(st + base + slot_s);
 #pragma unroll
-            for (int vs = 0; vs < NSUB; ++vs) {
+            for (int vs = 0; vs < NV; ++vs) {
               val[vs][ch] = v;
               if constexpr (STR) valb[vs][ch] = v;
             }
@@ -1302,12 +1313,13 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
             const uint8_t* sub = st + base + __ldg(&a.totals[plane]) +
                                  static_cast<int64_t>(static_cast<uint32_t>(gidx) - slot_s) * NSUB * NSUB;
 #pragma unroll
-            for (int vs = 0; vs < NSUB; ++vs) {
+            for (int vs = 0; vs < NV; ++vs) {
+              const int vg = NSUB >= H ? hh * NV + vs : 0;  // vertical subcell in the cell
               if constexpr (STR) {
-                val[vs][ch] = __ldg(sub + vs * NSUB + str_sa);
-                valb[vs][ch] = str_split < 4 ? __ldg(sub + vs * NSUB + str_sa + 1) : val[vs][ch];
+                val[vs][ch] = __ldg(sub + vg * NSUB + str_sa);
+                valb[vs][ch] = str_split < 4 ? __ldg(sub + vg * NSUB + str_sa + 1) : val[vs][ch];
               } else {
-                val[vs][ch] = __ldg(sub + vs * NSUB + sc);
+                val[vs][ch] = __ldg(sub + vg * NSUB + sc);
               }
             }
           }
@@ -1315,17 +1327,17 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
       }
       uint8_t* mystrip = buf + jj * (PACKED ? a.slot_stride : 0) + lpx * C;
 #pragma unroll
-      for (int vs = 0; vs < NSUB; ++vs) {
+      for (int vs = 0; vs < NV; ++vs) {
         uint32_t w[C];
         if constexpr (STR)
           pattern_words_split<C>(val[vs], valb[vs], str_split, w);
         else
           pattern_words<C>(val[vs], w);
 #pragma unroll
-        for (int i = 0; i < SB; ++i)
+        for (int i = 0; i < SBR; ++i)
 #pragma unroll
           for (int q = 0; q < C; ++q)
-            reinterpret_cast<uint32_t*>(mystrip + (vs * SB + i) * srb)[q] = w[q];
+            reinterpret_cast<uint32_t*>(mystrip + (vs * SBR + i) * srb)[q] = w[q];
       }
     }
     fence_proxy_async_smem();
@@ -1333,7 +1345,7 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
     const int scopy = max(0, min(srb, a.tensor_out_bytes - px0 * C));
     if (t == 0 && scopy > 0) {
       for (int j = 0; j < nf; ++j)
-        tma_store_3d(&tm_out, px0 * C / 8, r * B, fg * pk + j, buf + j * (PACKED ? a.slot_stride : 0));
+        tma_store_3d(&tm_out, px0 * C / 8, row0, fg * pk + j, buf + j * (PACKED ? a.slot_stride : 0));
     }
     if (t == 0) bulk_commit();  // one group per unit (possibly empty)
     // Bytes past the tensor's row extent (< 16 per row and slot), from the smem
@@ -1341,11 +1353,11 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
     const int vbytes = min(slot_px, g.N - px0) * C;
     const int span = vbytes - scopy;
     if (span > 0) {
-      const int rows = min(B, g.M - r * B);
+      const int rows = min(RU, g.M - row0);
       for (int e = t; e < nf * rows; e += NT) {  // one row per thread
         const int j = e / rows, i = e - j * rows;
         copy_row_tail(a.out + static_cast<int64_t>(fg * pk + j) * a.ofstride +
-                          static_cast<int64_t>(r * B + i) * a.opitch + static_cast<int64_t>(px0) * C + scopy,
+                          static_cast<int64_t>(row0 + i) * a.opitch + static_cast<int64_t>(px0) * C + scopy,
                       buf + j * (PACKED ? a.slot_stride : 0) + i * srb + scopy, span);
       }
     }
@@ -1889,6 +1901,28 @@ StatsKernel pick_var(int b, int n) {
   return nullptr;
 }
 
+// Band-split K2 (b = 32, 64: 49 / 98 KB RGB tiles otherwise): H parts per band.
+template <int C, bool AD, int H>
+ExpandKernel pick_expand_split(int b, int n) {
+#define DPPX_CASE(B4v, NS) \
+  if (b == 4 * (B4v) && n == (NS)) return k_expand_tma<C, B4v, NS, AD, false, H>;
+  DPPX_CASE(8, 1)
+  DPPX_CASE(16, 1)
+  if constexpr (AD) {
+    if constexpr (H <= 2) {
+      DPPX_CASE(8, 2)
+      DPPX_CASE(16, 2)
+    }
+    DPPX_CASE(8, 4)
+    DPPX_CASE(8, 8)
+    DPPX_CASE(16, 4)
+    DPPX_CASE(16, 8)
+    DPPX_CASE(16, 16)
+  }
+#undef DPPX_CASE
+  return nullptr;
+}
+
 template <int C, bool AD, bool PK>
 ExpandKernel pick_expand(int b, int n) {
 #define DPPX_CASE(B4v, NS) \
@@ -1989,7 +2023,7 @@ ExpandKernel select_expand_uany_c3(int b);
 StatsKernel select_adaptive_any_c3(int b, int n);
 StatsKernel select_uniform_any_c3(int b);
 StatsKernel select_stats_var_c3(int b, int n);
-ExpandKernel select_expand_tma_c1(int b, int n, bool adaptive, bool packed);
-ExpandKernel select_expand_tma_c3(int b, int n, bool adaptive, bool packed);
+ExpandKernel select_expand_tma_c1(int b, int n, bool adaptive, bool packed, int split);
+ExpandKernel select_expand_tma_c3(int b, int n, bool adaptive, bool packed, int split);
 
 }  // namespace dppx
