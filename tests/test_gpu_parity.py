@@ -1212,18 +1212,25 @@ def test_host_sweep_equals_separate_host_runs(ctx, M, N, C, F, bl, el):
     (128, 192, 3, 64, 16, "a"),
     (120, 160, 3, 8, 4, "a"),    # 2-px subcells
     (100, 120, 3, 16, 4, "a"),   # padded: no K1z
+    (576, 768, 3, 16, 1, "u-philox"),
+    (576, 768, 3, 16, 4, "a-philox"),
+    (96, 128, 1, 32, 1, "u-none"),
+    (96, 128, 3, 32, 8, "a-none"),
 ])
 def test_small_frame_paths_agree(ctx, M, N, C, b, n, mode):
     """One small pinned frame through every small-frame path (auto, graph,
     zero-copy -- K1z for whole-cell shapes --, staged) gives the same
     statistics and image, equal to the oracle."""
+    mode, _, kind = mode.partition("-")
+    kind = kind or "keyed"
+    noise = {"keyed": dp.NOISE_KEYED, "philox": dp.NOISE_PHILOX, "none": dp.NOISE_NONE}[kind]
     rng = np.random.default_rng(M * N + b)
     fr = dp.pinned_empty((1, M, N, C))
     fr[:] = rng.integers(0, 256, fr.shape, dtype=np.uint8)
     mk = dp.pinned_empty((1, M, N))
     mk[:] = (rng.random((1, M, N)) < 0.5).astype(np.uint8)
     p = dp.make_privacy_params(0.5, 16, b, n)
-    seeds = dp.plane_seeds(77, 1, C)
+    seeds = dp.plane_seeds(77, 1, C) if kind == "keyed" else ([77] if kind == "philox" else None)
     k1z = M % b == 0 and N % b == 0 and (N * C) % 16 == 0
     res = {}
     try:
@@ -1233,10 +1240,10 @@ def test_small_frame_paths_agree(ctx, M, N, C, b, n, mode):
                 out = dp.pinned_empty((1, M, N, C))
                 ctx.reset_stats()
                 if mode == "u":
-                    st, img = ctx.pixelize_uniform(fr, p, dp.NOISE_KEYED, seeds, out=out)
+                    st, img = ctx.pixelize_uniform(fr, p, noise, seeds, out=out)
                     st = st.copy()
                 else:
-                    st, img = ctx.pixelize_adaptive(fr, mk, p, dp.NOISE_KEYED, seeds, out=out)
+                    st, img = ctx.pixelize_adaptive(fr, mk, p, noise, seeds, out=out)
                 res.setdefault(path, (st, np.array(img)))
                 launches = ctx.stats()["launches"]
                 if rep == 1:  # page-locked statistics buffer: written in place by K1z
@@ -1244,10 +1251,10 @@ def test_small_frame_paths_agree(ctx, M, N, C, b, n, mode):
                     pst = dp.pinned_empty((C, (cap + 3) & ~3 if mode == "a" else
                                            dp.grid_dims(M, N, b).grid_count()))
                     if mode == "u":
-                        st2, img2 = ctx.pixelize_uniform(fr, p, dp.NOISE_KEYED, seeds, stats_out=pst)
+                        st2, img2 = ctx.pixelize_uniform(fr, p, noise, seeds, stats_out=pst)
                         assert np.array_equal(st2, res[path][0]), path
                     else:
-                        st2, img2 = ctx.pixelize_adaptive(fr, mk, p, dp.NOISE_KEYED, seeds, stats_out=pst)
+                        st2, img2 = ctx.pixelize_adaptive(fr, mk, p, noise, seeds, stats_out=pst)
                         assert st2 == res[path][0], path
                     assert np.array_equal(img2, res[path][1]), path
                 zc = path == dp.SMALL_ZEROCOPY or (path == dp.SMALL_AUTO and mode in dp.SMALL_AUTO_ZEROCOPY)
@@ -1261,12 +1268,13 @@ def test_small_frame_paths_agree(ctx, M, N, C, b, n, mode):
         else:
             assert st == ref_st, path
         assert np.array_equal(img, ref_img), path
+    oseeds = seeds * C if kind == "philox" else seeds  # the oracle takes a seed per channel
     if mode == "u":
-        rm, ri = oracle.pixelize_uniform(np.ascontiguousarray(fr[0]), b, p.sigma, "keyed", seeds)
+        rm, ri = oracle.pixelize_uniform(np.ascontiguousarray(fr[0]), b, p.sigma, kind, oseeds)
         assert np.array_equal(ref_st, rm)
         assert np.array_equal(ref_img[0].reshape(-1), np.asarray(ri).reshape(-1))
     else:
         rp, ri = oracle.pixelize_adaptive(np.ascontiguousarray(fr[0]), np.ascontiguousarray(mk[0]), b, n,
-                                          p.sigma, p.sigma_sub, "keyed", seeds)
+                                          p.sigma, p.sigma_sub, kind, oseeds)
         assert list(ref_st) == list(rp)
         assert np.array_equal(ref_img[0].reshape(-1), np.asarray(ri).reshape(-1))
