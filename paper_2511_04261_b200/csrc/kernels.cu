@@ -451,6 +451,120 @@ __global__ void __launch_bounds__(kClassifyThreads, BAND ? 10 : 8) k_classify(co
   }
 }
 
+// K0 for narrow frames (few cells per grid row, e.g. 178-px CelebA faces:
+// 12 cells per row would leave 116 of k_classify's 128 threads idle, one CTA
+// per row): one CTA per frame. Pass 1 (mode 0) sums the mask's b rows of
+// every cell row column by column into smem (coalesced, one column per
+// thread, 4 rows in flight, mirrored at the edges like image.cpp:105-110);
+// pass 2 walks the frame's cells in row-major order in chunks of the block:
+// mean (mode 0: mask_grid_mean -> f32; mode 1: the payload's stored mean),
+// flag, and the frame-wide exclusive simple prefix; pass 3 derives the
+// per-row prefixes, the intra-row prefixes (cell info), S and the payload
+// lengths -- the same outputs as k_classify, without cross-CTA tickets.
+__global__ void __launch_bounds__(kClassifyThreads) k_classify_frames(const ClassifyArgs a) {
+  extern __shared__ __align__(16) uint8_t csm[];
+  __shared__ uint32_t warp_tot[kClassifyThreads / 32];
+  __shared__ uint32_t s_corrupt;
+  const BatchGeom& g = a.g;
+  const int t = threadIdx.x;
+  const int PW = g.GC * g.b;
+  const bool mode0 = a.from_payload == 0;
+  uint32_t* gpre = reinterpret_cast<uint32_t*>(csm);                 // [G]: prefix | simple << 31
+  uint16_t* colsum = reinterpret_cast<uint16_t*>(csm + 4ll * g.G);   // [GR][PW] (mode 0)
+  for (int p = blockIdx.x; p < a.planes; p += gridDim.x) {
+    if (mode0) {
+      const uint8_t* mbase = a.mask + static_cast<int64_t>(p) * a.mfstride;
+      for (int it = t; it < g.GR * PW; it += kClassifyThreads) {
+        const int r = it / PW, x = it - r * PW;
+        const uint8_t* col = mbase + reflect_index(x, g.N);
+        const int y0 = r * g.b;
+        uint32_t acc[4] = {0, 0, 0, 0};  // four rows in flight per step
+        int i = 0;
+        if (y0 + g.b <= g.M) {  // band inside the frame: no reflection
+          const uint8_t* cp = col + static_cast<int64_t>(y0) * a.mpitch;
+          for (; i + 4 <= g.b; i += 4)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc[k] += __ldg(cp + static_cast<int64_t>(i + k) * a.mpitch);
+        }
+        for (; i < g.b; ++i) acc[0] += __ldg(col + static_cast<int64_t>(reflect_index(y0 + i, g.M)) * a.mpitch);
+        colsum[it] = static_cast<uint16_t>(acc[0] + acc[1] + acc[2] + acc[3]);
+      }
+      __syncthreads();
+    }
+    const float* mm_in =
+        a.from_payload == 1 ? reinterpret_cast<const float*>(a.payload_in + p * a.pstride) : nullptr;
+    uint32_t carry = 0;
+    for (int c0 = 0; c0 < g.G; c0 += kClassifyThreads) {
+      const int cell = c0 + t;
+      bool simple = false;
+      if (cell < g.G) {
+        float mean;
+        if (mode0) {
+          const int r = cell / g.GC, c = cell - r * g.GC;
+          uint32_t sum = 0;
+          const uint16_t* cs = colsum + r * PW + c * g.b;
+          for (int k = 0; k < g.b; ++k) sum += cs[k];
+          // mask_grid_mean (image.cpp:191-202) then static_cast<float> (adaptive.cpp:59-60)
+          mean = __double2float_rn(__ddiv_rn(static_cast<double>(sum), a.area));
+          for (int ch = 0; ch < g.C; ++ch)
+            reinterpret_cast<float*>(a.payload + (static_cast<int64_t>(p) * g.C + ch) * a.pstride)[cell] = mean;
+        } else {
+          mean = mm_in[cell];
+        }
+        simple = mean > 0.5f;  // simple_from_mean, adaptive.cpp:30-32
+      }
+      uint32_t tot;
+      const uint32_t pre = block_scan_flags(simple, warp_tot, &tot);
+      if (cell < g.G) gpre[cell] = (carry + pre) | (simple ? 0x80000000u : 0u);
+      carry += tot;
+    }
+    __syncthreads();
+    const uint32_t S = carry;
+    const int64_t pg = static_cast<int64_t>(p) * g.G;
+    for (int cell = t; cell < g.G; cell += kClassifyThreads) {
+      const int r = cell / g.GC;
+      const uint32_t rp = gpre[r * g.GC] & 0x7FFFFFFFu;
+      const uint32_t v = gpre[cell];
+      a.cellinfo[pg + cell] = (((v & 0x7FFFFFFFu) - rp) << 1) | (v >> 31);
+    }
+    for (int r = t; r < g.GR; r += kClassifyThreads) {
+      const uint32_t rp = gpre[r * g.GC] & 0x7FFFFFFFu;
+      const uint32_t next = r + 1 < g.GR ? (gpre[(r + 1) * g.GC] & 0x7FFFFFFFu) : S;
+      a.rowprefix[static_cast<int64_t>(p) * g.GR + r] = rp;
+      a.rowcnt[static_cast<int64_t>(p) * g.GR + r] = next - rp;
+    }
+    if (t == 0) {
+      a.totals[p] = S;
+      s_corrupt = 0u;
+      const uint64_t nn = static_cast<uint64_t>(g.n) * g.n;
+      const uint32_t len = static_cast<uint32_t>(4ull * g.G + 4 + S + (g.G - S) * nn);
+      if (a.from_payload == 1) {
+        const uint8_t* q = a.payload_in + p * a.pstride + 4ll * g.G;
+        const uint32_t stored = static_cast<uint32_t>(q[0]) | (static_cast<uint32_t>(q[1]) << 8) |
+                                (static_cast<uint32_t>(q[2]) << 16) | (static_cast<uint32_t>(q[3]) << 24);
+        // decode's simple-count and length checks (record.cpp:253-270)
+        if (stored != S || (a.in_len && a.in_len[p] != len) || len > a.plen_limit) {
+          atomicExch(a.status, DPPX_ERR_CORRUPT);
+          s_corrupt = 1u;
+        }
+      } else {
+        for (int ch = 0; ch < g.C; ++ch) {
+          const int64_t q = (static_cast<int64_t>(p) * g.C + ch) * a.pstride + 4ll * g.G;
+          *reinterpret_cast<uint32_t*>(a.payload + q) = S;
+          if (a.payload_len) a.payload_len[static_cast<int64_t>(p) * g.C + ch] = len;
+        }
+      }
+    }
+    __syncthreads();
+    if (s_corrupt) {  // as k_classify: every cell "simple, slot 0", output discarded
+      for (int i = t; i < g.G; i += kClassifyThreads) a.cellinfo[pg + i] = 1u;
+      for (int i = t; i < g.GR; i += kClassifyThreads) a.rowprefix[static_cast<int64_t>(p) * g.GR + i] = 0u;
+      if (t == 0) a.totals[p] = 0u;
+    }
+    __syncthreads();  // gpre / colsum reused by the next frame
+  }
+}
+
 // ============================================================================
 // K1g: generic kernel (any b, n, C <= 4, any pitch / alignment)
 // ============================================================================
@@ -1217,6 +1331,19 @@ int stats_tile_px_for(int b, bool adaptive) {
 int stats_max_stages() { return kMaxStages; }
 
 cudaError_t launch_classify(const ClassifyArgs& a, cudaStream_t s) {
+  // Narrow frames (a grid row at most half the block): one CTA per frame.
+  // (DPPX_NO_K0_FRAMES: A/B knob)
+  static const bool frames_off = std::getenv("DPPX_NO_K0_FRAMES") != nullptr;
+  if ((a.from_payload == 0 || a.from_payload == 1) && !a.mask_bits && a.g.GC * 2 <= kClassifyThreads &&
+      !frames_off) {
+    const size_t smem = 4 * static_cast<size_t>(a.g.G) +
+                        (a.from_payload == 0 ? 2 * static_cast<size_t>(a.g.GR) * a.g.GC * a.g.b : 0);
+    if (smem <= 48 * 1024 && a.g.b <= 257) {
+      const int grid = a.planes < 148 * 16 ? a.planes : 148 * 16;
+      k_classify_frames<<<grid > 0 ? grid : 1, kClassifyThreads, smem, s>>>(a);
+      return cudaGetLastError();
+    }
+  }
   dim3 grid(a.g.GR, a.planes < 65535 ? a.planes : 65535);
   if (!a.band) {
     k_classify<false><<<grid, kClassifyThreads, 0, s>>>(a);
