@@ -575,17 +575,28 @@ int run_stats(dppx_ctx* ctx, StatsArgs& a) {
   a.pack = 1;
   a.slot_px = tile;
   const bool var = a.var_flags != nullptr;
-  if (!var && 2 * padded_px <= tile && (padded_px * g.C) % 16 == 0) {
-    const int64_t stride = round_up(static_cast<int64_t>(g.b) * padded_px * g.C, 128);
-    const int pk = static_cast<int>(std::min<int64_t>(tile / padded_px, stage_bytes / stride));
+  // (slots are whole 16-byte granules wide: a padded row of 184 px x 3 takes a
+  // 192-px slot; the lanes past the last cell idle, the TMA box's bytes past
+  // the row are zero-filled on load and clipped on store)
+  static const bool slot16 = !(std::getenv("DPPX_SLOT16") && std::getenv("DPPX_SLOT16")[0] == '0');
+  const int slot_w = (padded_px * g.C) % 16 == 0 ? padded_px : (slot16 ? round_up(padded_px, 16) : 0);
+  if (!var && slot_w > 0 && 2 * slot_w <= tile) {
+    const int64_t stride = round_up(static_cast<int64_t>(g.b) * slot_w * g.C, 128);
+    const int pk = static_cast<int>(std::min<int64_t>(tile / slot_w, stage_bytes / stride));
     if (pk >= 2) {
       a.pack = pk;
-      a.slot_px = padded_px;
+      a.slot_px = slot_w;
     }
   }
   a.slot_stride = static_cast<int>(round_up(static_cast<int64_t>(g.b) * a.slot_px * g.C, 128));
   k = var ? select_stats_kernel_var(g.C, g.b, g.n)
           : select_stats_kernel(g.C, g.b, g.n, a.adaptive != 0, a.pack > 1);
+  if (!k && a.pack > 1) {  // no packed instantiation for this (b, n): one frame per tile
+    a.pack = 1;
+    a.slot_px = tile;
+    a.slot_stride = static_cast<int>(round_up(static_cast<int64_t>(g.b) * a.slot_px * g.C, 128));
+    k = select_stats_kernel(g.C, g.b, g.n, a.adaptive != 0, false);
+  }
   // Uniform b = 4 on wide frames: two cell rows (an 8-row band) per unit.
   static const bool rows2_off = std::getenv("DPPX_NO_ROWS2") != nullptr;  // A/B knob
   int rpu = 1;

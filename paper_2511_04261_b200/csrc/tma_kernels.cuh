@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
   constexpr int ROWB = TILE * C;
   constexpr uint32_t STAGE = BR * ROWB;
   // (SB >= 2: a strip meets at most two subcells.)
-  static_assert(B4 <= 32 && (STR ? (SB >= 2 && ADAPTIVE && !VAR && !PACKED) : B4 % SB4 == 0),
+  static_assert(B4 <= 32 && (STR ? (SB >= 2 && ADAPTIVE && !VAR) : B4 % SB4 == 0),
                 "fast-path geometry");
   static_assert(TILE == kTilePx || !PACKED, "packed slots use 512-px tiles");
   static_assert(!VAR || (ADAPTIVE && !PACKED), "variance staging: wide adaptive frames only");
@@ -1881,6 +1881,10 @@ StatsKernel pick_b(int b, int n) {
       DPPX_CASE(3, 4)
       DPPX_CASE(4, 8)
       DPPX_CASE(6, 8)
+    }
+    if constexpr (PK) {  // narrow frames, 2-px subcells (CelebA b8 n4, b16 n8)
+      DPPX_CASE(2, 4)
+      DPPX_CASE(4, 8)
     }
   }
 #undef DPPX_CASE

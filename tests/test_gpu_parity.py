@@ -360,7 +360,8 @@ def test_fast_path_equals_exact_path(ctx, eps, b, n):
         assert fast[0] == exact[0] and np.array_equal(fast[1], exact[1])
 
 
-@pytest.mark.parametrize("b,n,C", [(16, 4, 3), (16, 1, 3), (8, 2, 1), (32, 8, 3), (4, 1, 3)])
+@pytest.mark.parametrize("b,n,C", [(16, 4, 3), (16, 1, 3), (8, 2, 1), (32, 8, 3), (4, 1, 3), (16, 8, 3),
+                                   (16, 8, 1)])
 def test_narrow_frames_packed_per_unit(ctx, b, n, C):
     """Narrow frames (CelebA 178x218) share a staged tile ("slots"); odd frame
     counts leave a partial last group. Bit-exact vs the oracle."""
