@@ -893,16 +893,20 @@ int expand_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* stats, i
   int64_t stage_bytes = static_cast<int64_t>(g.b) * tile * g.C;
   e.pack = 1;
   e.slot_px = tile;
-  if (tile == stats_tile_px() && 2 * padded_px <= expand_packed_tile_px() &&
-      (padded_px * g.C) % 16 == 0) {
+  const int tile0 = tile;
+  const int64_t stage0 = stage_bytes;
+  // (slots of whole 16-byte granules, as K1: 184 px x 3 -> 192-px slots)
+  static const bool slot16 = !(std::getenv("DPPX_SLOT16") && std::getenv("DPPX_SLOT16")[0] == '0');
+  const int slot_w = (padded_px * g.C) % 16 == 0 ? padded_px : (slot16 ? static_cast<int>(round_up(padded_px, 16)) : 0);
+  if (tile == stats_tile_px() && slot_w > 0 && 2 * slot_w <= expand_packed_tile_px()) {
     // Narrow frames: frame slots side by side in a wider (1024-px) tile.
     const int ptile = expand_packed_tile_px();
     const int64_t pstage = static_cast<int64_t>(g.b) * ptile * g.C;
-    const int64_t stride = round_up(static_cast<int64_t>(g.b) * padded_px * g.C, 128);
-    const int pk = static_cast<int>(std::min<int64_t>(ptile / padded_px, pstage / stride));
+    const int64_t stride = round_up(static_cast<int64_t>(g.b) * slot_w * g.C, 128);
+    const int pk = static_cast<int>(std::min<int64_t>(ptile / slot_w, pstage / stride));
     if (pk >= 2) {
       e.pack = pk;
-      e.slot_px = padded_px;
+      e.slot_px = slot_w;
       tile = ptile;
       stage_bytes = pstage;
     }
@@ -922,6 +926,14 @@ int expand_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* stats, i
       if (!k && sp > 1 && (k = select_expand_kernel(g.C, g.b, g.n, adaptive, false, sp))) unit_rows = g.b / sp;
   }
   if (!k) k = select_expand_kernel(g.C, g.b, g.n, adaptive, e.pack > 1, 1);
+  if (!k && e.pack > 1) {  // no packed instantiation for this (b, n): one frame per tile
+    e.pack = 1;
+    e.slot_px = tile0;
+    tile = tile0;
+    stage_bytes = stage0;
+    e.slot_stride = static_cast<int>(round_up(static_cast<int64_t>(g.b) * e.slot_px * g.C, 128));
+    k = select_expand_kernel(g.C, g.b, g.n, adaptive, false, 1);
+  }
   if (unit_rows != g.b) stage_bytes = static_cast<int64_t>(unit_rows) * tile * g.C;
   e.stage_bytes = static_cast<int>(round_up(stage_bytes, 128));
   CUtensorMap tout{};

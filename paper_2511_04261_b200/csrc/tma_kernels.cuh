@@ -1246,7 +1246,7 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
   constexpr int SBR = NSUB >= H ? SB : RU;              // rows per emitted subcell
   static_assert(!HALF || (!PACKED && (NSUB == 1 || NSUB % H == 0) && RU % 4 == 0), "band-split geometry");
   constexpr bool STR = (SB % 4) != 0;  // strips meet two subcells (as K1)
-  static_assert(!STR || (ADAPTIVE && !PACKED && SB >= 2), "split strips: wide adaptive frames");
+  static_assert(!STR || (ADAPTIVE && SB >= 2), "split strips: adaptive, subcells of >= 2 px");
   constexpr int LPW = (32 / B4) * B4;                    // whole cells per warp (as K1)
   constexpr int NT = PACKED ? kExpandPackedThreads : kConsumers;
   constexpr int TILE = 4 * (NT / 32) * LPW;
@@ -1969,6 +1969,10 @@ ExpandKernel pick_expand(int b, int n) {
     DPPX_CASE(8, 2)
     DPPX_CASE(8, 4)
     DPPX_CASE(8, 8)
+    if constexpr (PK) {  // narrow frames, 2-px subcells (CelebA b8 n4, b16 n8)
+      DPPX_CASE(2, 4)
+      DPPX_CASE(4, 8)
+    }
   }
 #undef DPPX_CASE
   return nullptr;

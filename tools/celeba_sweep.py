@@ -48,8 +48,22 @@ def main():
         k1 = sum(s["device_ms"][k] for k in k1f) / 3
         k0 = s["device_ms"]["classify"] / max(1, s["launches"]["classify"])
         alg = F * M * N * C * 2 + int(lens.sum().item())
+        # reassembly (K0 from the payloads + K2)
+        ctx.reassemble_dev(d, stats, st, lens, b, n, out)
+        ctx.synchronize()
+        ctx.reset_stats()
+        ctx.set_timing(True)
+        for _ in range(3):
+            ctx.reassemble_dev(d, stats, st, lens, b, n, out)
+        ctx.synchronize()
+        s2 = ctx.stats()
+        ctx.set_timing(False)
+        k2 = s2["device_ms"]["expand"] / max(1, s2["launches"]["expand"])
+        k0r = s2["device_ms"]["classify"] / max(1, s2["launches"]["classify"])
+        k2alg = F * M * N * C + int(lens.sum().item())
         rows.append({"b": b, "n": n, "kernels": fams, "k1_ms": round(k1, 4), "k0_ms": round(k0, 4),
-                     "k1_frac": round(alg / (k1 / 1e3) / 1e9 / peak, 4)})
+                     "k1_frac": round(alg / (k1 / 1e3) / 1e9 / peak, 4), "k2_ms": round(k2, 4),
+                     "k0r_ms": round(k0r, 4), "k2_frac": round(k2alg / (k2 / 1e3) / 1e9 / peak, 4)})
         del stats, lens
     print(json.dumps(rows))
 
