@@ -396,7 +396,11 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
   // Subcell sides that are not a multiple of 4 px (b = 24 n = 4: 6 px; 2 or
   // 3 px): a strip can straddle two subcells; each lane splits its strip sums at the
   // boundary and the subcell sums meet in per-warp smem (compact draw mode).
-  constexpr bool STR = (SB % 4) != 0;
+  // PIX (n = b, 1-px subcells: the diagonal of the paper's PPM-100 (b, n) grid,
+  // CelebA b4 n4 / b16 n16): every pixel of a complex cell is its own
+  // statistic; each lane draws its strip's 4 px x C per row in place.
+  constexpr bool PIX = SB == 1;
+  constexpr bool STR = (SB % 4) != 0 && !PIX;
   // Strips per warp: whole cells only (a cell is B4 adjacent lanes), so for
   // B4 not a power of two (b = 12, 24) the last 32 % B4 lanes of each warp
   // idle and the tile is 16 * LPW px (480 at b = 12 or 24) instead of 512.
@@ -405,7 +409,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
   constexpr int ROWB = TILE * C;
   constexpr uint32_t STAGE = BR * ROWB;
   // (SB >= 2: a strip meets at most two subcells.)
-  static_assert(B4 <= 32 && (STR ? (SB >= 2 && ADAPTIVE && !VAR) : B4 % SB4 == 0),
+  static_assert(B4 <= 32 && (PIX ? (ADAPTIVE && !VAR) : STR ? (SB >= 2 && ADAPTIVE && !VAR) : B4 % SB4 == 0),
                 "fast-path geometry");
   static_assert(TILE == kTilePx || !PACKED, "packed slots use 512-px tiles");
   static_assert(!VAR || (ADAPTIVE && !PACKED), "variance staging: wide adaptive frames only");
@@ -704,7 +708,31 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
       // Direct mode with many vertical subcells (NSUB >= 8): two at a time, so
       // the two subcells' draw chains overlap (a store of one subcell's pattern
       // would otherwise order the next subcell's smem reads behind its draws).
-      constexpr bool PAIRS = !compact && NSUB >= kPairsMinNsub && NSUB % 2 == 0;
+      constexpr bool PAIRS = !compact && !PIX && NSUB >= kPairsMinNsub && NSUB % 2 == 0;
+      if constexpr (PIX) {
+        // whole-cell sums for the simple cells (tot), then the complex cells'
+        // pixels: one keyed draw per (row, px, channel) at sigma_sub (area 1)
+#pragma unroll 4
+        for (int i = 0; i < B; ++i) accumulate_row<C>(mystrip + i * srb, tot);
+        if (cx_any) {
+          const int sc0 = 4 * lic;  // this strip's first subcell column in the cell
+          const int64_t off0 = cx ? stat_offset(a, false, gidx, slot_s, S_tot, 0, 0) : 0;
+#pragma unroll 1
+          for (int i = 0; i < B; ++i) {
+            uint8_t* row = mystrip + i * srb;
+            if (cx) {
+#pragma unroll
+              for (int q = 0; q < 4 * C; ++q) {
+                const int px = q / C, ch = q - px * C;
+                const uint32_t v = draw_stat(a, env_sub, row[q], cs[ch], f, ch, p.r, cell, i, sc0 + px, gidx);
+                a.stats[static_cast<int64_t>(f * C + ch) * a.sstride + off0 + i * NSUB + sc0 + px] =
+                    static_cast<uint8_t>(v);
+                if (emit) row[q] = static_cast<uint8_t>(v);
+              }
+            }
+          }
+        }
+      }
       if constexpr (PAIRS) {
 #pragma unroll 1
         for (int vs = 0; vs < NSUB; vs += 2) {
@@ -753,7 +781,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
           }
         }
       }
-      if (!PAIRS && (!VAR || cx_any)) {
+      if constexpr (!PIX) if (!PAIRS && (!VAR || cx_any)) {
 #pragma unroll 1
         for (int vs = 0; vs < NSUB; ++vs) {
           uint32_t acc[C];
@@ -1245,8 +1273,10 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
   constexpr int NV = NSUB >= H ? NSUB / H : 1;          // vertical subcells per unit
   constexpr int SBR = NSUB >= H ? SB : RU;              // rows per emitted subcell
   static_assert(!HALF || (!PACKED && (NSUB == 1 || NSUB % H == 0) && RU % 4 == 0), "band-split geometry");
-  constexpr bool STR = (SB % 4) != 0;  // strips meet two subcells (as K1)
+  constexpr bool PIX = SB == 1;          // 1-px subcells (n = b): per-pixel complex values
+  constexpr bool STR = (SB % 4) != 0 && !PIX;  // strips meet two subcells (as K1)
   static_assert(!STR || (ADAPTIVE && SB >= 2), "split strips: adaptive, subcells of >= 2 px");
+  static_assert(!PIX || (ADAPTIVE && H == 1), "per-pixel subcells: adaptive, whole bands");
   constexpr int LPW = (32 / B4) * B4;                    // whole cells per warp (as K1)
   constexpr int NT = PACKED ? kExpandPackedThreads : kConsumers;
   constexpr int TILE = 4 * (NT / 32) * LPW;
@@ -1263,7 +1293,7 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
   const int jj = in_slot ? my_j : 0;
   const int lpx = 4 * sx - jj * slot_px;
   const int srb = slot_px * C;  // smem bytes per slot row
-  const int sc = STR ? 0 : (sx % B4) / SB4;
+  const int sc = (STR || PIX) ? 0 : (sx % B4) / (SB4 > 0 ? SB4 : 1);
   const int str_px = 4 * (sx % B4);
   const int str_sa = STR ? str_px / SB : 0;
   const int str_split = STR ? min(4, (str_sa + 1) * SB - str_px) : 4;
@@ -1287,6 +1317,41 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
     const int cell = (px0 + lpx) / B;
     const bool active = in_slot && jj < nf && cell < g.GC;
     const int gidx = r * g.GC + cell;
+    if constexpr (PIX) {
+      // simple cells: one value per channel over the band; complex cells: the
+      // payload byte of every pixel (row i, column 4 * lane-in-cell + px)
+      if (active) {
+        uint8_t* mystrip = buf + jj * (PACKED ? a.slot_stride : 0) + lpx * C;
+        const int64_t base = 4ll * g.G + 4;
+        const int sc0 = 4 * (sx % B4);
+        const int64_t plane0 = static_cast<int64_t>(f) * C;
+        const uint32_t info = __ldg(&a.cellinfo[plane0 * g.G + gidx]);
+        const uint32_t slot_s = __ldg(&a.rowprefix[plane0 * g.GR + r]) + (info >> 1);
+        if (info & 1u) {
+          uint32_t vv[C];
+#pragma unroll
+          for (int ch = 0; ch < C; ++ch) vv[ch] = __ldg(a.stats + (plane0 + ch) * a.sstride + base + slot_s);
+          uint32_t w[C];
+          pattern_words<C>(vv, w);
+#pragma unroll 4
+          for (int i = 0; i < RU; ++i)
+#pragma unroll
+            for (int q = 0; q < C; ++q) reinterpret_cast<uint32_t*>(mystrip + i * srb)[q] = w[q];
+        } else {
+          const uint8_t* sub[C];
+#pragma unroll
+          for (int ch = 0; ch < C; ++ch)
+            sub[ch] = a.stats + (plane0 + ch) * a.sstride + base + __ldg(&a.totals[plane0 + ch]) +
+                      static_cast<int64_t>(static_cast<uint32_t>(gidx) - slot_s) * NSUB * NSUB + sc0;
+#pragma unroll 1
+          for (int i = 0; i < RU; ++i) {
+            uint8_t* row = mystrip + i * srb;
+#pragma unroll
+            for (int q = 0; q < 4 * C; ++q) row[q] = __ldg(sub[q % C] + i * NSUB + q / C);
+          }
+        }
+      }
+    } else {
     uint32_t val[NV][C];
     uint32_t valb[STR ? NV : 1][C];  // STR: the strip's second subcell
     if (active) {
@@ -1339,6 +1404,7 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
           for (int q = 0; q < C; ++q)
             reinterpret_cast<uint32_t*>(mystrip + (vs * SBR + i) * srb)[q] = w[q];
       }
+    }
     }
     fence_proxy_async_smem();
     __syncthreads();
@@ -1886,6 +1952,13 @@ StatsKernel pick_b(int b, int n) {
       DPPX_CASE(2, 4)
       DPPX_CASE(4, 8)
     }
+    // 1-px subcells (n = b): per-pixel complex cells
+    DPPX_CASE(1, 4)
+    DPPX_CASE(2, 8)
+    DPPX_CASE(4, 16)
+    if constexpr (!PK) {
+      DPPX_CASE(8, 32)
+    }
   }
 #undef DPPX_CASE
   return nullptr;
@@ -1972,6 +2045,13 @@ ExpandKernel pick_expand(int b, int n) {
     if constexpr (PK) {  // narrow frames, 2-px subcells (CelebA b8 n4, b16 n8)
       DPPX_CASE(2, 4)
       DPPX_CASE(4, 8)
+    }
+    // 1-px subcells (n = b): per-pixel complex values
+    DPPX_CASE(1, 4)
+    DPPX_CASE(2, 8)
+    DPPX_CASE(4, 16)
+    if constexpr (!PK) {
+      DPPX_CASE(8, 32)
     }
   }
 #undef DPPX_CASE

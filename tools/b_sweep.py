@@ -12,7 +12,8 @@ sys.path.insert(0, ROOT)
 
 CASES = [(12, 1), (12, 3), (16, 4), (16, 8), (32, 8), (20, 1), (20, 5), (24, 1), (24, 3), (24, 4), (30, 5), (40, 1),
          (40, 2), (40, 4), (40, 5), (64, 1), (64, 4), (64, 8), (64, 16), (128, 1), (128, 8), (128, 16),
-         (128, 32), (128, 128), (128, 2), (128, 4), (30, 2), (30, 3), (30, 6), (30, 10)]
+         (128, 32), (128, 128), (128, 2), (128, 4), (30, 2), (30, 3), (30, 6), (30, 10),
+         (4, 4), (8, 8), (16, 16), (32, 32)]  # n = b: 1-px subcells
 
 
 def main():
