@@ -218,6 +218,7 @@ __device__ __forceinline__ uint32_t fast_quantize(uint32_t sum, float inv_area, 
   const uint64_t y = bits >> 11;                    // 53-bit integer of uniform_from_bits
   uint32_t lo_w, hi_w;  // top-bit test on the high word alone (on the 64-bit value the
   asm("mov.b64 {%0, %1}, %2;" : "=r"(lo_w), "=r"(hi_w) : "l"(bits));  // compiler emits 2 compares)
+  (void)lo_w;
   const bool neg = static_cast<int32_t>(hi_w) >= 0;  // y < 2^52, i.e. u < 0
   // 1 - 2|u| = W * 2^-52: W = y for u < 0 (at least 1: the +-(0.5 - 2^-53)
   // clamp of noise.cpp:99-104, applied below on the f32 value), 2^53 - y

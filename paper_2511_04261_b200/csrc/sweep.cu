@@ -231,6 +231,7 @@ __device__ __forceinline__ float laplace_log2_signed(uint64_t bits) {
   const uint64_t y = bits >> 11;
   uint32_t lo_w, hi_w;
   asm("mov.b64 {%0, %1}, %2;" : "=r"(lo_w), "=r"(hi_w) : "l"(bits));
+  (void)lo_w;
   const bool neg = static_cast<int32_t>(hi_w) >= 0;
   const uint64_t W = neg ? y : (1ull << 53) - y;
   const uint32_t wb = __float_as_uint(fmaxf(__ull2float_rn(W), 1.0f));

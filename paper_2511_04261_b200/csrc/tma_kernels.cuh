@@ -1958,6 +1958,10 @@ StatsKernel pick_b(int b, int n) {
     DPPX_CASE(4, 16)
     if constexpr (!PK) {
       DPPX_CASE(8, 32)
+      DPPX_CASE(16, 64)
+      // 2-px subcells of the PPM-100 grid (b4 n2; b32 n16 / b64 n32 would need
+      // 24-96 KB of per-warp subcell tables)
+      DPPX_CASE(1, 2)
     }
   }
 #undef DPPX_CASE
@@ -2052,6 +2056,8 @@ ExpandKernel pick_expand(int b, int n) {
     DPPX_CASE(4, 16)
     if constexpr (!PK) {
       DPPX_CASE(8, 32)
+      DPPX_CASE(16, 64)
+      DPPX_CASE(1, 2)
     }
   }
 #undef DPPX_CASE
