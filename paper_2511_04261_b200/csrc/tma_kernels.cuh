@@ -399,7 +399,14 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
   // PIX (n = b, 1-px subcells: the diagonal of the paper's PPM-100 (b, n) grid,
   // CelebA b4 n4 / b16 n16): every pixel of a complex cell is its own
   // statistic; each lane draws its strip's 4 px x C per row in place.
-  constexpr bool PIX = SB == 1;
+  // In-lane subcells (SB = 1 or 2 px: n = b, n = b/2 -- the PPM-100 grid's
+  // diagonals, CelebA b4 n4 / b8 n4 / b16 n8 / b16 n16): a strip holds 4/SB
+  // whole subcells per row, so each lane sums, draws and writes its own
+  // subcells in place -- no cross-lane tables.
+  // (packed narrow frames keep the split-strip tables for 2-px subcells: their
+  // compacted draws measured faster there, CelebA b8 n4 2.5 vs 3.1 ms)
+  constexpr bool PIX = NSUB > 1 && (SB == 1 || (SB == 2 && !PACKED));
+  constexpr int KS = PIX ? 4 / SB : 1;  // subcells per strip and subcell row
   constexpr bool STR = (SB % 4) != 0 && !PIX;
   // Strips per warp: whole cells only (a cell is B4 adjacent lanes), so for
   // B4 not a power of two (b = 12, 24) the last 32 % B4 lanes of each warp
@@ -409,7 +416,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
   constexpr int ROWB = TILE * C;
   constexpr uint32_t STAGE = BR * ROWB;
   // (SB >= 2: a strip meets at most two subcells.)
-  static_assert(B4 <= 32 && (PIX ? (ADAPTIVE && !VAR) : STR ? (SB >= 2 && ADAPTIVE && !VAR) : B4 % SB4 == 0),
+  static_assert(B4 <= 32 && (PIX ? (ADAPTIVE && !VAR && NSUB == B / SB) : STR ? (SB >= 2 && ADAPTIVE && !VAR) : B4 % SB4 == 0),
                 "fast-path geometry");
   static_assert(TILE == kTilePx || !PACKED, "packed slots use 512-px tiles");
   static_assert(!VAR || (ADAPTIVE && !PACKED), "variance staging: wide adaptive frames only");
@@ -711,23 +718,35 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
       constexpr bool PAIRS = !compact && !PIX && NSUB >= kPairsMinNsub && NSUB % 2 == 0;
       if constexpr (PIX) {
         // whole-cell sums for the simple cells (tot), then the complex cells'
-        // pixels: one keyed draw per (row, px, channel) at sigma_sub (area 1)
+        // subcells: each lane's KS subcells per subcell row, summed from its own
+        // strip, one keyed draw per (subcell, channel) at sigma_sub, written back
+        // into the strip
 #pragma unroll 4
         for (int i = 0; i < B; ++i) accumulate_row<C>(mystrip + i * srb, tot);
         if (cx_any) {
-          const int sc0 = 4 * lic;  // this strip's first subcell column in the cell
+          const int sc0 = KS * lic;  // this strip's first subcell column in the cell
           const int64_t off0 = cx ? stat_offset(a, false, gidx, slot_s, S_tot, 0, 0) : 0;
 #pragma unroll 1
-          for (int i = 0; i < B; ++i) {
-            uint8_t* row = mystrip + i * srb;
+          for (int sr = 0; sr < NSUB; ++sr) {
             if (cx) {
+              uint8_t* row0p = mystrip + sr * SB * srb;
 #pragma unroll
-              for (int q = 0; q < 4 * C; ++q) {
-                const int px = q / C, ch = q - px * C;
-                const uint32_t v = draw_stat(a, env_sub, row[q], cs[ch], f, ch, p.r, cell, i, sc0 + px, gidx);
-                a.stats[static_cast<int64_t>(f * C + ch) * a.sstride + off0 + i * NSUB + sc0 + px] =
+              for (int q = 0; q < KS * C; ++q) {
+                const int k = q / C, ch = q - k * C;
+                uint32_t sum = 0;
+#pragma unroll
+                for (int y = 0; y < SB; ++y)
+#pragma unroll
+                  for (int x = 0; x < SB; ++x) sum += row0p[y * srb + (k * SB + x) * C + ch];
+                const uint32_t v = draw_stat(a, env_sub, sum, cs[ch], f, ch, p.r, cell, sr, sc0 + k, gidx);
+                a.stats[static_cast<int64_t>(f * C + ch) * a.sstride + off0 + sr * NSUB + sc0 + k] =
                     static_cast<uint8_t>(v);
-                if (emit) row[q] = static_cast<uint8_t>(v);
+                if (emit) {
+#pragma unroll
+                  for (int y = 0; y < SB; ++y)
+#pragma unroll
+                    for (int x = 0; x < SB; ++x) row0p[y * srb + (k * SB + x) * C + ch] = static_cast<uint8_t>(v);
+                }
               }
             }
           }
@@ -1273,7 +1292,8 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
   constexpr int NV = NSUB >= H ? NSUB / H : 1;          // vertical subcells per unit
   constexpr int SBR = NSUB >= H ? SB : RU;              // rows per emitted subcell
   static_assert(!HALF || (!PACKED && (NSUB == 1 || NSUB % H == 0) && RU % 4 == 0), "band-split geometry");
-  constexpr bool PIX = SB == 1;          // 1-px subcells (n = b): per-pixel complex values
+  constexpr bool PIX = SB <= 2 && NSUB > 1;  // 1- or 2-px subcells: each pixel's own payload byte
+  constexpr int KS = PIX ? 4 / SB : 1;       // subcells per strip and subcell row
   constexpr bool STR = (SB % 4) != 0 && !PIX;  // strips meet two subcells (as K1)
   static_assert(!STR || (ADAPTIVE && SB >= 2), "split strips: adaptive, subcells of >= 2 px");
   static_assert(!PIX || (ADAPTIVE && H == 1), "per-pixel subcells: adaptive, whole bands");
@@ -1323,7 +1343,7 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
       if (active) {
         uint8_t* mystrip = buf + jj * (PACKED ? a.slot_stride : 0) + lpx * C;
         const int64_t base = 4ll * g.G + 4;
-        const int sc0 = 4 * (sx % B4);
+        const int sc0 = KS * (sx % B4);
         const int64_t plane0 = static_cast<int64_t>(f) * C;
         const uint32_t info = __ldg(&a.cellinfo[plane0 * g.G + gidx]);
         const uint32_t slot_s = __ldg(&a.rowprefix[plane0 * g.GR + r]) + (info >> 1);
@@ -1347,7 +1367,7 @@ __global__ void __launch_bounds__(PACKED ? kExpandPackedThreads : kConsumers)
           for (int i = 0; i < RU; ++i) {
             uint8_t* row = mystrip + i * srb;
 #pragma unroll
-            for (int q = 0; q < 4 * C; ++q) row[q] = __ldg(sub[q % C] + i * NSUB + q / C);
+            for (int q = 0; q < 4 * C; ++q) row[q] = __ldg(sub[q % C] + (i / SB) * NSUB + (q / C) / SB);
           }
         }
       }
@@ -1959,9 +1979,10 @@ StatsKernel pick_b(int b, int n) {
     if constexpr (!PK) {
       DPPX_CASE(8, 32)
       DPPX_CASE(16, 64)
-      // 2-px subcells of the PPM-100 grid (b4 n2; b32 n16 / b64 n32 would need
-      // 24-96 KB of per-warp subcell tables)
+      // 2-px subcells of the PPM-100 grid (in-lane, no subcell tables)
       DPPX_CASE(1, 2)
+      DPPX_CASE(8, 16)
+      DPPX_CASE(16, 32)
     }
   }
 #undef DPPX_CASE
@@ -2058,6 +2079,8 @@ ExpandKernel pick_expand(int b, int n) {
       DPPX_CASE(8, 32)
       DPPX_CASE(16, 64)
       DPPX_CASE(1, 2)
+      DPPX_CASE(8, 16)
+      DPPX_CASE(16, 32)
     }
   }
 #undef DPPX_CASE

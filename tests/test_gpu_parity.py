@@ -759,7 +759,8 @@ def test_metrics_staged_upload_pieces(ctx):
 
 @pytest.mark.parametrize("C", [1, 3])
 @pytest.mark.parametrize("b,n", [(12, 2), (20, 2), (20, 4), (24, 4), (40, 4), (40, 8), (8, 4), (12, 4),
-                                 (16, 8), (24, 8), (4, 4), (8, 8), (16, 16), (32, 32), (4, 2), (64, 64)])
+                                 (16, 8), (24, 8), (4, 4), (8, 8), (16, 16), (32, 32), (4, 2), (64, 64),
+                                 (32, 16), (64, 32)])
 def test_straddling_subcells_on_tma_path(ctx, C, b, n):
     """Subcell sides that are not a multiple of 4 px (6, 10, 5): K1's 4-px
     strips straddle subcell boundaries, lanes split their sums and the subcell
