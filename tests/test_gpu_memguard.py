@@ -30,6 +30,9 @@ CASES = [  # (M, N, C, b, n, adaptive) -- one or more per kernel family
     (218, 178, 3, 16, 4, True), (218, 178, 3, 16, 1, False), (20, 7, 3, 4, 2, True),    # packed, K1g
     (83, 1917, 3, 4, 1, False), (61, 253, 3, 7, 1, False), (150, 253, 1, 128, 1, False),  # K1 / K1u
     (33, 45, 3, 5, 1, False), (100, 301, 1, 4, 1, True), (70, 203, 3, 64, 16, True),
+    (70, 203, 3, 16, 16, True), (57, 131, 3, 8, 4, True), (40, 150, 1, 32, 16, True),  # in-lane 1-2 px
+    (218, 178, 3, 16, 8, True), (218, 178, 3, 8, 4, True), (218, 178, 1, 16, 16, True),  # packed STR / 1 px
+    (20, 77, 3, 16, 2, True),                                                          # K0 per frame
 ]
 GUARD = 4096
 
