@@ -319,6 +319,12 @@ int dppx_pixelize_checked(dppx_ctx* ctx, int32_t mode, const dppx_frames_desc* d
                           const uint8_t* mask, const dppx_privacy_params* params, const dppx_noise* noise,
                           uint8_t* stats, int64_t payload_stride, uint32_t* payload_len, uint8_t* out,
                           uint8_t* recon_ok, double* mse_out, double* ssim_out);
+/* Sizes everything dppx_pixelize_checked would allocate for (mode, desc,
+ * params) -- device buffers, scratch, the pinned staging pieces -- without
+ * running anything, so a batch runner can pay for it while it still reads its
+ * inputs. Optional: dppx_pixelize_checked grows the same buffers itself. */
+int dppx_pixelize_checked_reserve(dppx_ctx* ctx, int32_t mode, const dppx_frames_desc* desc,
+                                  const dppx_privacy_params* params);
 
 /* classify_regions (adaptive.cpp:34-65) of F masks (desc mask fields; channels
  * ignored): per-frame G float mask means at mask_means + f*G. */

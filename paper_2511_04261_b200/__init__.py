@@ -167,6 +167,7 @@ ABI = {
                                               C.POINTER(_vp), _vp, _vp]),
     "dppx_pixelize_checked": (C.c_int, [_ctxp, C.c_int32, _descp, _vp, _vp, _pp, _np, _vp, C.c_int64, _vp,
                                         _vp, _vp, _vp, _vp]),
+    "dppx_pixelize_checked_reserve": (C.c_int, [_ctxp, C.c_int32, _descp, _pp]),
     "dppx_group_create": (C.c_int, [C.POINTER(C.c_int32), C.c_int32, C.POINTER(_vp)]),
     "dppx_group_destroy": (None, [_vp]),
     "dppx_group_size": (C.c_int32, [_vp]),
@@ -545,6 +546,16 @@ class Context:
             m, C.byref(nz), mp, op, _ptr(mse), _ptr(ssim)), "pixelize_uniform_sweep")
         del keep
         return means, imgs, mse, ssim
+
+    def pixelize_checked_reserve(self, shape, params: PrivacyParams, mode="adaptive"):
+        """dppx_pixelize_checked_reserve: size the buffers of a later
+        pixelize_checked call on frames of `shape` (F, M, N[, C])."""
+        F, M, N = shape[:3]
+        Cn = shape[3] if len(shape) > 3 else 1
+        m = {"uniform": 0, "adaptive": 1, "reference": 2}[mode]
+        d = _desc(M, N, Cn, F)
+        self._check(_lib.dppx_pixelize_checked_reserve(self._h, m, C.byref(d), C.byref(params)),
+                    "pixelize_checked_reserve")
 
     def pixelize_checked(self, frames, masks, params: PrivacyParams, mode="adaptive",
                          noise=NOISE_NONE, seeds=None):

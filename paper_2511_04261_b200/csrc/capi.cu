@@ -2884,40 +2884,91 @@ int dppx_metrics(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* a, con
   return metric_host(ctx, d, a, b, mse_out, ssim_out);
 }
 
+namespace {
+// Validated geometry + the device buffers of one dppx_pixelize_checked call
+// (shared with dppx_pixelize_checked_reserve, which only sizes them).
+struct CheckedLayout {
+  BatchGeom g;
+  size_t G = 0, cap = 0;
+  int64_t row = 0, dpitch = 0, dfs = 0, dmpitch = 0, dmfs = 0, dstride = 0;
+  int P = 0;
+};
+
+int checked_layout(dppx_ctx* ctx, int32_t mode, const dppx_frames_desc* d, const dppx_privacy_params* pp,
+                   CheckedLayout* L) {
+  if (mode < 0 || mode > 2) return set_err(ctx, DPPX_ERR_INVALID, "unknown mode");
+  const bool adaptive = mode == 1, reference = mode == 2;
+  if (int rc = check_params(ctx, pp, adaptive)) return rc;
+  if (int rc = check_desc(ctx, d, adaptive, true)) return rc;
+  BatchGeom& g = L->g;
+  if (int rc = geometry(ctx, d->height, d->width, d->channels, d->frames, pp->b, adaptive ? pp->n : 1, &g,
+                        !reference))
+    return rc;
+  if (g.F > 65535) return set_err(ctx, DPPX_ERR_INVALID, "at most 65535 frames per call");
+  L->G = static_cast<size_t>(g.G);
+  L->cap = adaptive ? dppx_adaptive_payload_capacity(g.M, g.N, g.b, g.n) : L->G;
+  L->row = static_cast<int64_t>(g.N) * g.C;
+  L->dpitch = round_up(L->row, 16), L->dfs = L->dpitch * g.M;
+  L->dmpitch = round_up(g.N, 16), L->dmfs = L->dmpitch * g.M;
+  L->dstride = adaptive ? round_up(static_cast<int64_t>(L->cap), 16) : static_cast<int64_t>(L->G);
+  L->P = g.F * g.C;
+  return DPPX_OK;
+}
+
+int checked_buffers(dppx_ctx* ctx, int32_t mode, const CheckedLayout& L) {
+  const bool adaptive = mode == 1, reference = mode == 2;
+  const int F = L.g.F;
+  if (ensure(ctx, ctx->img[0], static_cast<size_t>(L.dfs) * F)) return DPPX_ERR_OOM;
+  if (ensure(ctx, ctx->out[0], static_cast<size_t>(L.dfs) * F)) return DPPX_ERR_OOM;
+  if (adaptive && ensure(ctx, ctx->mask[0], static_cast<size_t>(L.dmfs) * F)) return DPPX_ERR_OOM;
+  if (ensure(ctx, ctx->stats[0], static_cast<size_t>(L.dstride) * L.P)) return DPPX_ERR_OOM;
+  if (ensure(ctx, ctx->lens[0], sizeof(uint32_t) * L.P)) return DPPX_ERR_OOM;
+  if (!reference && ensure(ctx, ctx->check_img, static_cast<size_t>(L.dfs) * F)) return DPPX_ERR_OOM;
+  if (ensure(ctx, ctx->check_eq, sizeof(uint32_t) * F)) return DPPX_ERR_OOM;
+  return DPPX_OK;
+}
+}  // namespace
+
+int dppx_pixelize_checked_reserve(dppx_ctx* ctx, int32_t mode, const dppx_frames_desc* d,
+                                  const dppx_privacy_params* pp) {
+  if (int rc = check_ctx(ctx)) return rc;
+  CheckedLayout L;
+  if (int rc = checked_layout(ctx, mode, d, pp, &L)) return rc;
+  if (L.g.F == 0) return DPPX_OK;
+  if (int rc = checked_buffers(ctx, mode, L)) return rc;
+  // the scratch pixelize_dev sizes per call, and the two pinned pieces
+  // pageable uploads / downloads go through
+  if (int rc = ensure_scratch(ctx, L.g, L.P)) return rc;
+  if (int rc = ensure(ctx, ctx->met_out, static_cast<size_t>(L.P) * std::max(L.g.M - 6, 1) * 8)) return rc;
+  const int64_t per = std::max<int64_t>(1, (int64_t{16} << 20) / L.dpitch);
+  for (int s = 0; s < 2; ++s) {
+    if (int rc = grow_pinned(ctx, ctx->piece[s], ctx->piece_n[s], static_cast<size_t>(per * L.dpitch)))
+      return rc;
+    if (!ctx->piece_ev[s]) CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->piece_ev[s], cudaEventDisableTiming));
+  }
+  return DPPX_OK;
+}
+
 int dppx_pixelize_checked(dppx_ctx* ctx, int32_t mode, const dppx_frames_desc* d, const uint8_t* img,
                           const uint8_t* mask, const dppx_privacy_params* pp, const dppx_noise* nz,
                           uint8_t* stats, int64_t stride, uint32_t* lens, uint8_t* out, uint8_t* recon_ok,
                           double* mse, double* ssim) {
   if (int rc = check_ctx(ctx)) return rc;
-  if (mode < 0 || mode > 2) return set_err(ctx, DPPX_ERR_INVALID, "unknown mode");
+  CheckedLayout L;
+  if (int rc = checked_layout(ctx, mode, d, pp, &L)) return rc;
   const bool adaptive = mode == 1, reference = mode == 2;
-  if (int rc = check_params(ctx, pp, adaptive)) return rc;
-  if (int rc = check_desc(ctx, d, adaptive, true)) return rc;
-  BatchGeom g;
-  if (int rc = geometry(ctx, d->height, d->width, d->channels, d->frames, pp->b, adaptive ? pp->n : 1, &g,
-                        !reference))
-    return rc;
+  const BatchGeom& g = L.g;
   const int F = g.F, C = g.C, M = g.M, N = g.N;
   if (F == 0) return DPPX_OK;
-  if (F > 65535) return set_err(ctx, DPPX_ERR_INVALID, "at most 65535 frames per call");
   if (!img || !out || !mse || (!reference && !stats) || (adaptive && !mask))
     return set_err(ctx, DPPX_ERR_INVALID, "null image/output/statistics/mask/mse pointer");
-  const size_t G = static_cast<size_t>(g.G);
-  const size_t cap = adaptive ? dppx_adaptive_payload_capacity(M, N, g.b, g.n) : G;
+  const size_t G = L.G, cap = L.cap;
   if (adaptive && stride < static_cast<int64_t>(cap))
     return set_err(ctx, DPPX_ERR_INVALID, "payload_stride too small");
-  const int64_t row = static_cast<int64_t>(N) * C;
-  const int64_t dpitch = round_up(row, 16), dfs = dpitch * M;
-  const int64_t dmpitch = round_up(N, 16), dmfs = dmpitch * M;
-  const int64_t dstride = adaptive ? round_up(static_cast<int64_t>(cap), 16) : static_cast<int64_t>(G);
-  const int P = F * C;
-  if (ensure(ctx, ctx->img[0], static_cast<size_t>(dfs) * F)) return DPPX_ERR_OOM;
-  if (ensure(ctx, ctx->out[0], static_cast<size_t>(dfs) * F)) return DPPX_ERR_OOM;
-  if (adaptive && ensure(ctx, ctx->mask[0], static_cast<size_t>(dmfs) * F)) return DPPX_ERR_OOM;
-  if (ensure(ctx, ctx->stats[0], static_cast<size_t>(dstride) * P)) return DPPX_ERR_OOM;
-  if (ensure(ctx, ctx->lens[0], sizeof(uint32_t) * P)) return DPPX_ERR_OOM;
-  if (!reference && ensure(ctx, ctx->check_img, static_cast<size_t>(dfs) * F)) return DPPX_ERR_OOM;
-  if (ensure(ctx, ctx->check_eq, sizeof(uint32_t) * F)) return DPPX_ERR_OOM;
+  const int64_t row = L.row, dpitch = L.dpitch, dfs = L.dfs, dmpitch = L.dmpitch, dmfs = L.dmfs,
+                dstride = L.dstride;
+  const int P = L.P;
+  if (int rc = checked_buffers(ctx, mode, L)) return rc;
   uint8_t* dimg = static_cast<uint8_t*>(ctx->img[0].p);
   uint8_t* dout = static_cast<uint8_t*>(ctx->out[0].p);
   uint8_t* dmask = static_cast<uint8_t*>(ctx->mask[0].p);
@@ -2925,6 +2976,16 @@ int dppx_pixelize_checked(dppx_ctx* ctx, int32_t mode, const dppx_frames_desc* d
   uint32_t* dlens = static_cast<uint32_t*>(ctx->lens[0].p);
   uint32_t* deq = static_cast<uint32_t*>(ctx->check_eq.p);
   cudaStream_t st = ctx->stream;
+  // DPPX_CHECKED_TRACE=1: per-phase wall times on stderr (synchronizes).
+  static const bool trace = std::getenv("DPPX_CHECKED_TRACE") != nullptr;
+  auto T = std::chrono::steady_clock::now();
+  auto phase = [&](const char* what) {
+    if (!trace) return;
+    cudaStreamSynchronize(st);
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "checked: %s %.2f ms\n", what, std::chrono::duration<double, std::milli>(t - T).count());
+    T = t;
+  };
   // the previous host call's copies out of the staging buffers are done
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->s_out));
   // ---- one upload of frames (and masks) ----
@@ -2935,6 +2996,7 @@ int dppx_pixelize_checked(dppx_ctx* ctx, int32_t mode, const dppx_frames_desc* d
       return rc;
     ctx->kstats.h2d_bytes += static_cast<uint64_t>(N) * M * F;
   }
+  phase("upload");
   dppx_frames_desc dd = *d;
   dd.pitch = dpitch;
   dd.frame_stride = dfs;
@@ -2965,14 +3027,17 @@ int dppx_pixelize_checked(dppx_ctx* ctx, int32_t mode, const dppx_frames_desc* d
       CUDA_TRY(ctx, launch_frames_equal(dout, drb, dpitch, dfs, row, M, F, deq, st));
     }
   }
+  phase("pixelize+check");
   // ---- mse / ssim of input vs emitted frames, both resident (cli.cpp:164-171) ----
   dppx_frames_desc dm = dd;  // a = input (pitch), b = output (out_pitch)
   if (int rc = metric_dev(ctx, &dm, dimg, dout, false, mse)) return rc;
   if (ssim && M >= 7 && N >= 7)
     if (int rc = metric_dev(ctx, &dm, dimg, dout, true, ssim)) return rc;
+  phase("metrics");
   // ---- results out ----
   if (int rc = d2h_frames(ctx, out, d->out_pitch, d->out_frame_stride, dout, dpitch, dfs, row, M, F, st))
     return rc;
+  phase("download frames");
   ctx->kstats.d2h_bytes += static_cast<uint64_t>(row) * M * F;
   std::vector<uint32_t> eq(static_cast<size_t>(F));
   CUDA_TRY(ctx, cudaMemcpyAsync(eq.data(), deq, sizeof(uint32_t) * F, cudaMemcpyDeviceToHost, st));
@@ -2988,6 +3053,7 @@ int dppx_pixelize_checked(dppx_ctx* ctx, int32_t mode, const dppx_frames_desc* d
     ctx->kstats.d2h_bytes += static_cast<uint64_t>(w) * P;
     if (adaptive && lens) std::memcpy(lens, ln.data(), sizeof(uint32_t) * P);
   }
+  phase("download statistics");
   // (K0 run on the payloads just produced cannot flag them; if it ever did,
   // every frame fails the check instead of leaving the status set)
   const bool corrupt = read_status(ctx) != DPPX_OK;

@@ -1032,74 +1032,122 @@ __global__ void __launch_bounds__(256) k_mse(const MetricArgs m) {
   }
 }
 
-// One thread per (plane, window row): slides the 7x7 window along the row with
-// exact integer column sums and accumulates the local SSIM in the reference's
+// x / 49 for the integer window sums (x <= 49 * 255^2): RN(x * RN(1/49))
+// corrected by one exact-remainder fma. Checked exhaustively against IEEE
+// division for every x in [0, 3186225] (tools/div49_check.c), so the local
+// SSIM below stays bit-identical to metrics.cpp's `/ area` without a DDIV.
+__device__ __forceinline__ double div49(uint32_t x) {
+  const double a = static_cast<double>(x), r = 1.0 / 49.0;
+  const double q = __dmul_rn(a, r);
+  return __fma_rn(__fma_rn(-q, 49.0, a), r, q);
+}
+
+// SSIM of one plane band: one CTA per (plane, SSR window rows), 7-row column
+// sums and local SSIM values computed in parallel over 128-column chunks, then
+// each window row's values folded left to right by one lane in the reference's
 // order (metrics.cpp:144-177): the row partial is bit-identical.
-__global__ void __launch_bounds__(128) k_ssim_rows(const MetricArgs m) {
+//   warps 1..4: local SSIM of chunk c (thread = row r, 8 consecutive windows);
+//   warp 0:     folds chunk c-1 meanwhile (lane r = window row r);
+//   all:        7-row column sums of the next chunk.
+constexpr int SSR = 8, SCW = 128, SVS = 152;  // rows per CTA, windows per chunk, V row stride
+__device__ __forceinline__ int ssim_vx(int x) { return x + (x >> 3); }  // 16 lanes x 8 cols: no bank clash
+
+__global__ void __launch_bounds__(160, 4) k_ssim_bands(const MetricArgs m) {
   constexpr int W = 7;
+  __shared__ uint32_t V[5][SSR][SVS];
+  __shared__ double Q[2][SSR][SCW + 1];
   const int pr = m.M - W + 1, pc = m.N - W + 1;
-  const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  const int64_t planes = static_cast<int64_t>(m.F) * m.C;
-  if (idx >= planes * pr) return;
-  const int64_t p = idx / pr;
-  const int i = static_cast<int>(idx - p * pr);
+  const int nb = (pr + SSR - 1) / SSR;
+  const int64_t p = blockIdx.x / nb;
+  const int i0 = static_cast<int>(blockIdx.x - p * nb) * SSR;
+  const int rows = min(SSR, pr - i0);
   const int f = static_cast<int>(p / m.C), ch = static_cast<int>(p - static_cast<int64_t>(f) * m.C);
-  const uint8_t* a = m.a + static_cast<int64_t>(f) * m.fstride + static_cast<int64_t>(i) * m.pitch + ch;
-  const uint8_t* b = m.b + static_cast<int64_t>(f) * m.bfstride + static_cast<int64_t>(i) * m.bpitch + ch;
-  uint32_t ring[W][5];
-  uint32_t win[5] = {0u, 0u, 0u, 0u, 0u};
-  auto column = [&](int c, uint32_t (&out)[5]) {
-    uint32_t s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0;
-#pragma unroll
-    for (int y = 0; y < W; ++y) {
-      const uint32_t va = __ldg(a + static_cast<int64_t>(y) * m.pitch + static_cast<int64_t>(c) * m.C);
-      const uint32_t vb = __ldg(b + static_cast<int64_t>(y) * m.bpitch + static_cast<int64_t>(c) * m.C);
-      s0 += va;
-      s1 += vb;
-      s2 += va * va;
-      s3 += vb * vb;
-      s4 += va * vb;
+  const uint8_t* a = m.a + static_cast<int64_t>(f) * m.fstride + static_cast<int64_t>(i0) * m.pitch + ch;
+  const uint8_t* b = m.b + static_cast<int64_t>(f) * m.bfstride + static_cast<int64_t>(i0) * m.bpitch + ch;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int nchunk = (pc + SCW - 1) / SCW;
+  double acc = 0.0;  // warp 0, lane r: window row i0 + r
+  auto fold = [&](int c) {
+    if (lane < rows) {
+      const double* q = Q[c & 1][lane];
+      const int n = min(SCW, pc - c * SCW);
+      for (int k = 0; k < n; ++k) acc = __dadd_rn(acc, q[k]);
     }
-    out[0] = s0, out[1] = s1, out[2] = s2, out[3] = s3, out[4] = s4;
   };
+  for (int c = 0; c < nchunk; ++c) {
+    const int j0 = c * SCW;
+    // ---- 7-row column sums of columns j0 .. j0+SCW+5 ----
+    if (t < SCW + W - 1) {
+      const int col = j0 + t;
+      if (col < m.N) {
+        const uint8_t* pa = a + static_cast<int64_t>(col) * m.C;
+        const uint8_t* pb = b + static_cast<int64_t>(col) * m.C;
+        uint32_t va[SSR + W - 1], vb[SSR + W - 1];
 #pragma unroll
-  for (int c = 0; c < W; ++c) {
-    column(c, ring[c]);
-#pragma unroll
-    for (int q = 0; q < 5; ++q) win[q] += ring[c][q];
-  }
-  const double area = 49.0, c1 = 6.5025, c2 = 58.5225;
-  double acc = 0.0;
-  for (int j = 0; j < pc; ++j) {
-    if (j > 0) {  // slide: drop column j-1, add column j+6 (ring slot (j-1) % 7)
-      const int slot = (j - 1) % W;
-      uint32_t nc[5];
-      column(j + W - 1, nc);
-#pragma unroll
-      for (int k = 0; k < W; ++k)
-        if (k == slot) {
-#pragma unroll
-          for (int q = 0; q < 5; ++q) {
-            win[q] = win[q] - ring[k][q] + nc[q];
-            ring[k][q] = nc[q];
-          }
+        for (int y = 0; y < SSR + W - 1; ++y) {
+          va[y] = y < rows + W - 1 ? __ldg(pa + static_cast<int64_t>(y) * m.pitch) : 0u;
+          vb[y] = y < rows + W - 1 ? __ldg(pb + static_cast<int64_t>(y) * m.bpitch) : 0u;
         }
+        uint32_t s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0;
+#pragma unroll
+        for (int y = 0; y < W; ++y) {
+          s0 += va[y], s1 += vb[y], s2 += va[y] * va[y], s3 += vb[y] * vb[y], s4 += va[y] * vb[y];
+        }
+        const int x = ssim_vx(t);
+#pragma unroll
+        for (int r = 0; r < SSR; ++r) {
+          if (r > 0) {
+            const uint32_t oa = va[r - 1], ob = vb[r - 1], na = va[r + W - 1], nb2 = vb[r + W - 1];
+            s0 += na - oa, s1 += nb2 - ob, s2 += na * na - oa * oa, s3 += nb2 * nb2 - ob * ob;
+            s4 += na * nb2 - oa * ob;
+          }
+          V[0][r][x] = s0, V[1][r][x] = s1, V[2][r][x] = s2, V[3][r][x] = s3, V[4][r][x] = s4;
+        }
+      }
     }
-    const double mu_a = __ddiv_rn(static_cast<double>(win[0]), area);
-    const double mu_b = __ddiv_rn(static_cast<double>(win[1]), area);
-    const double raw_aa = __ddiv_rn(static_cast<double>(win[2]), area);
-    const double raw_bb = __ddiv_rn(static_cast<double>(win[3]), area);
-    const double raw_ab = __ddiv_rn(static_cast<double>(win[4]), area);
-    const double mu_aa = __dmul_rn(mu_a, mu_a), mu_bb = __dmul_rn(mu_b, mu_b),
-                 mu_ab = __dmul_rn(mu_a, mu_b);
-    const double var_a = __dsub_rn(raw_aa, mu_aa), var_b = __dsub_rn(raw_bb, mu_bb),
-                 cov = __dsub_rn(raw_ab, mu_ab);
-    const double num = __dmul_rn(__dadd_rn(__dmul_rn(2.0, mu_ab), c1), __dadd_rn(__dmul_rn(2.0, cov), c2));
-    const double den = __dmul_rn(__dadd_rn(__dadd_rn(mu_aa, mu_bb), c1),
-                                 __dadd_rn(__dadd_rn(var_a, var_b), c2));
-    acc = __dadd_rn(acc, __ddiv_rn(num, den));
+    __syncthreads();
+    if (warp == 0) {
+      if (c > 0) fold(c - 1);
+    } else {
+      const int u = t - 32, r = u >> 4, g = u & 15;
+      const int jl = g * 8;
+      if (r < rows && j0 + jl < pc) {
+        uint32_t win[5];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+          uint32_t s = 0;
+#pragma unroll
+          for (int x = 0; x < W; ++x) s += V[q][r][ssim_vx(jl + x)];
+          win[q] = s;
+        }
+        const double c1 = 6.5025, c2 = 58.5225;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if (k > 0) {
+#pragma unroll
+            for (int q = 0; q < 5; ++q)
+              win[q] = win[q] - V[q][r][ssim_vx(jl + k - 1)] + V[q][r][ssim_vx(jl + k + W - 1)];
+          }
+          const double mu_a = div49(win[0]), mu_b = div49(win[1]);
+          const double raw_aa = div49(win[2]), raw_bb = div49(win[3]), raw_ab = div49(win[4]);
+          const double mu_aa = __dmul_rn(mu_a, mu_a), mu_bb = __dmul_rn(mu_b, mu_b),
+                       mu_ab = __dmul_rn(mu_a, mu_b);
+          const double var_a = __dsub_rn(raw_aa, mu_aa), var_b = __dsub_rn(raw_bb, mu_bb),
+                       cov = __dsub_rn(raw_ab, mu_ab);
+          const double num =
+              __dmul_rn(__dadd_rn(__dmul_rn(2.0, mu_ab), c1), __dadd_rn(__dmul_rn(2.0, cov), c2));
+          const double den = __dmul_rn(__dadd_rn(__dadd_rn(mu_aa, mu_bb), c1),
+                                       __dadd_rn(__dadd_rn(var_a, var_b), c2));
+          Q[c & 1][r][jl + k] = __ddiv_rn(num, den);  // windows past pc are never folded
+        }
+      }
+    }
+    __syncthreads();
   }
-  m.row_sums[p * pr + i] = acc;
+  if (warp == 0) {
+    fold(nchunk - 1);
+    if (lane < rows) m.row_sums[p * pr + i0 + lane] = acc;
+  }
 }
 
 cudaError_t launch_metrics(const MetricArgs& m, bool ssim, cudaStream_t s) {
@@ -1107,8 +1155,9 @@ cudaError_t launch_metrics(const MetricArgs& m, bool ssim, cudaStream_t s) {
     dim3 grid((m.M + 7) / 8, m.F < 65535 ? m.F : 65535);
     k_mse<<<grid, 256, 0, s>>>(m);
   } else {
-    const int64_t threads = static_cast<int64_t>(m.F) * m.C * (m.M - 6);
-    k_ssim_rows<<<static_cast<unsigned>((threads + 127) / 128), 128, 0, s>>>(m);
+    const int64_t ctas = static_cast<int64_t>(m.F) * m.C * ((m.M - 6 + SSR - 1) / SSR);
+    if (ctas > 0x7fffffff) return cudaErrorInvalidConfiguration;
+    k_ssim_bands<<<static_cast<unsigned>(ctas), 160, 0, s>>>(m);
   }
   return cudaGetLastError();
 }

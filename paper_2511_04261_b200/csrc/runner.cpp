@@ -261,6 +261,63 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
   auto tnow = [] { return std::chrono::steady_clock::now(); };
   auto tms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
   const auto T0 = tnow();
+  const double eff_eps = cfg.epsilon > 0.0 ? cfg.epsilon : 1.0;  // cli.cpp:97-102
+  const int n = cfg.mode == BatchMode::adaptive ? cfg.n : 1;
+  const int K = std::max(1, cfg.frames_per_call);
+  const int mode = cfg.mode == BatchMode::adaptive ? 1 : cfg.mode == BatchMode::uniform ? 0 : 2;
+  // ---- device setup, overlapping ingest: the group (contexts, worker
+  // threads), then per worker the buffers of a full chunk of the first
+  // input's shape and one 1-frame call, which loads the kernels it selects.
+  // Failures surface only if there is GPU work (chunks) after all. ----
+  dppx_group* grp = nullptr;
+  std::exception_ptr setup_err;
+  std::thread setup([&] {
+    try {
+      grp = shared_group(batch_devices(cfg));
+      int M = 0, N = 0;
+      try {
+        const std::vector<std::uint8_t> head = slurp(inputs[0], "read_pgm");
+        const PgmView v = parse_pgm(head, inputs[0]);
+        M = v.height, N = v.width;
+      } catch (const std::exception&) {
+        return;  // ingest reports it
+      }
+      dppx_privacy_params pp;
+      if (dppx_make_privacy_params(eff_eps, cfg.m, cfg.b, n, &pp) != DPPX_OK) return;
+      dppx_geometry g;
+      if (dppx_grid_dims(M, N, cfg.b, &g) != DPPX_OK) return;
+      const int F = std::min(K, nfile);
+      const size_t plane = static_cast<size_t>(M) * N;
+      std::function<void(dppx_ctx*, int, int)> warm = [&](dppx_ctx* ctx, int, int) {
+        const dppx_frames_desc full{M, N, 1, F, N, static_cast<int64_t>(plane), N, static_cast<int64_t>(plane),
+                                    N, static_cast<int64_t>(plane)};
+        if (dppx_pixelize_checked_reserve(ctx, mode, &full, &pp) != DPPX_OK) return;
+        const dppx_frames_desc one{M, N, 1, 1, N, static_cast<int64_t>(plane), N, static_cast<int64_t>(plane),
+                                   N, static_cast<int64_t>(plane)};
+        std::vector<uint8_t> img(plane, 0), mk(plane, 1), out(plane);
+        const size_t cap = mode == 1 ? (dppx_adaptive_payload_capacity(M, N, cfg.b, n) + 3) & ~size_t{3}
+                                     : static_cast<size_t>(g.grid_rows) * g.grid_cols;
+        std::vector<uint8_t> stats(cap);
+        uint32_t len = 0;
+        uint8_t ok = 0;
+        double mse = 0.0, ssim = 0.0;
+        uint64_t seed = 0;
+        const dppx_noise nz{cfg.seed ? DPPX_NOISE_KEYED : DPPX_NOISE_NONE, 0, &seed, nullptr};
+        dppx_pixelize_checked(ctx, mode, &one, img.data(), mode == 1 ? mk.data() : nullptr, &pp, &nz,
+                              stats.data(), static_cast<int64_t>(cap), &len, out.data(), &ok, &mse,
+                              M >= 7 && N >= 7 ? &ssim : nullptr);
+      };
+      dppx_group_run(grp, dppx_group_size(grp), &group_task_trampoline, &warm);
+    } catch (...) {
+      setup_err = std::current_exception();
+    }
+  });
+  struct Joiner {
+    std::thread& t;
+    ~Joiner() {
+      if (t.joinable()) t.join();
+    }
+  } joiner{setup};
   // ---- ingest (host threads) ----
   parallel_over(nfile, io, [&](int i) {
     reports[i].input = inputs[i];
@@ -282,18 +339,16 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
   for (int i = 0; i < nfile; ++i)
     if (ok[i]) groups[{imgs[i].height, imgs[i].width}].push_back(i);
   std::vector<std::vector<int>> chunks;
-  const int K = std::max(1, cfg.frames_per_call);
   for (auto& kv : groups)
     for (size_t c0 = 0; c0 < kv.second.size(); c0 += K)
       chunks.emplace_back(kv.second.begin() + c0,
                           kv.second.begin() + std::min(kv.second.size(), c0 + K));
-  const double eff_eps = cfg.epsilon > 0.0 ? cfg.epsilon : 1.0;  // cli.cpp:97-102
-  const int n = cfg.mode == BatchMode::adaptive ? cfg.n : 1;
   if (!chunks.empty() && (cfg.emit_image || cfg.emit_record)) make_out_dir(cfg.out_dir);
-  if (chunks.empty()) return reports;
   const auto Tg = tnow();
-  dppx_group* grp = shared_group(batch_devices(cfg));
-  if (trace) std::fprintf(stderr, "batch: device group %.1f ms\n", tms(Tg, tnow()));
+  setup.join();
+  if (chunks.empty()) return reports;
+  if (setup_err) std::rethrow_exception(setup_err);
+  if (trace) std::fprintf(stderr, "batch: device setup wait %.1f ms\n", tms(Tg, tnow()));
   const int workers = dppx_group_size(grp);
   const int io_per = std::max(1, io / std::max(1, std::min<int>(workers, static_cast<int>(chunks.size()))));
 
@@ -330,7 +385,6 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
       // One upload per chunk: pixelize, the reconstruct check and mse / ssim
       // all run where the frames already are (dppx_pixelize_checked).
       const auto tp0 = tnow();
-      const int mode = cfg.mode == BatchMode::adaptive ? 1 : cfg.mode == BatchMode::uniform ? 0 : 2;
       const int rc = dppx_pixelize_checked(ctx, mode, &d, in.p, cfg.mode == BatchMode::adaptive ? mk.p : nullptr,
                                            &pp, &nz, stats.data(), static_cast<int64_t>(cap), lens.data(), out.p,
                                            recon_ok.data(), mses.data(),

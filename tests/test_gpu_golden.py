@@ -108,6 +108,27 @@ def test_metrics_bit_identical_to_reference(ctx):
         dp.ssim(np.zeros((6, 9), np.uint8), np.zeros((6, 9), np.uint8))
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("C", [1, 3])
+def test_ssim_ragged_bands_and_chunks(ctx, C):
+    """The band SSIM kernel (8 window rows x 128-column chunks per CTA) on
+    shapes whose window rows / columns end inside a band or a chunk, and
+    saturated planes (window sums at their maximum, 49 * 255^2): every plane
+    bit-identical to the oracle (metrics.cpp:144-182)."""
+    rng = np.random.default_rng(23 + C)
+    for M, N in [(7, 7), (8, 134), (14, 135), (15, 262), (22, 263), (7, 390), (40, 9), (13, 1000)]:
+        F = 3
+        a = rng.integers(0, 256, (F, M, N, C), dtype=np.uint8)
+        b = np.clip(a.astype(int) + rng.integers(-60, 60, a.shape), 0, 255).astype(np.uint8)
+        a[1] = 255
+        b[2] = 255
+        s = ctx.metrics(a, b, "ssim")
+        for f in range(F):
+            for c in range(C):
+                assert s[f * C + c] == oracle.ssim(np.ascontiguousarray(a[f, :, :, c]),
+                                                   np.ascontiguousarray(b[f, :, :, c])), (M, N, f, c)
+
+
 def _config_cases():
     import json
     return json.load(open(os.path.join(G, "config_digests.json")))["cases"]

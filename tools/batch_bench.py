@@ -71,6 +71,9 @@ def main():
     # GPU arm: one untimed warm-up process (file cache, driver), then `reps`
     subprocess.run([gpu_bin, d_in, d_gpu] + common + ["0"], check=True, capture_output=True)
     gpu = run([gpu_bin, d_in, d_gpu] + common + ["0"], args.reps)
+    if os.environ.get("DPPX_BATCH_TRACE"):  # and one more after the timed runs (outputs exist now)
+        r = subprocess.run([gpu_bin, d_in, d_gpu] + common + ["0"], capture_output=True, text=True)
+        sys.stderr.write("after timed runs:\n" + r.stderr)
     names = sorted(os.listdir(d_ref))
     same = names == sorted(os.listdir(d_gpu)) and all(
         filecmp.cmp(os.path.join(d_ref, x), os.path.join(d_gpu, x), shallow=False) for x in names)
