@@ -1031,8 +1031,21 @@ int grow_pinned(dppx_ctx* ctx, uint8_t*& buf, size_t& have, size_t need) {
   return DPPX_OK;
 }
 
+// Rows per pinned piece of a pageable transfer: ~4 MB (DPPX_PIECE_MB). Small
+// enough that the two pieces cost little to pin on a context's first pageable
+// call (2 x 16 MB took 14.6 ms, most of a batch runner's device setup), large
+// enough that a piece's DMA (~80 us) dwarfs its copy and event overheads.
+int64_t piece_rows(int64_t pitch) {
+  static const int64_t bytes = [] {
+    const char* e = std::getenv("DPPX_PIECE_MB");
+    const long mb = e ? std::strtol(e, nullptr, 10) : 0;
+    return (mb > 0 ? static_cast<int64_t>(mb) : int64_t{4}) << 20;
+  }();
+  return std::max<int64_t>(1, bytes / pitch);
+}
+
 // Host -> device copy of F frames (rows of `row` bytes). A pinned source is one
-// DMA; a pageable one is cut into ~16 MB pieces of whole rows that host threads
+// DMA; a pageable one is cut into ~4 MB pieces of whole rows that host threads
 // copy into two pinned buffers in turn, so the host copies overlap the DMA.
 int h2d_frames(dppx_ctx* ctx, uint8_t* dst, int64_t dpitch, int64_t dfs, const uint8_t* src,
                int64_t spitch, int64_t sfs, int64_t row, int M, int F, cudaStream_t st) {
@@ -1042,7 +1055,7 @@ int h2d_frames(dppx_ctx* ctx, uint8_t* dst, int64_t dpitch, int64_t dfs, const u
   }
   if (!ctx->packer) ctx->packer = dppx::mask_packer_create(0);
   const int64_t rows = static_cast<int64_t>(F) * M;
-  const int64_t per = std::max<int64_t>(1, (int64_t{16} << 20) / dpitch);
+  const int64_t per = piece_rows(dpitch);
   const bool linear = dfs == static_cast<int64_t>(M) * dpitch;  // dst row r at r * dpitch
   for (int s = 0; s < 2; ++s) {
     if (int rc = grow_pinned(ctx, ctx->piece[s], ctx->piece_n[s], static_cast<size_t>(per * dpitch)))
@@ -1071,7 +1084,7 @@ int h2d_frames(dppx_ctx* ctx, uint8_t* dst, int64_t dpitch, int64_t dfs, const u
 }
 
 // Device -> host copy of F frames into a caller buffer: one DMA when the
-// destination is pinned; otherwise ~16 MB pieces land in the ctx's two pinned
+// destination is pinned; otherwise ~4 MB pieces land in the ctx's two pinned
 // piece buffers in turn and host threads copy each piece out while the next
 // one is in flight.
 int d2h_frames(dppx_ctx* ctx, uint8_t* dst, int64_t dpitch, int64_t dfs, const uint8_t* src,
@@ -1082,7 +1095,7 @@ int d2h_frames(dppx_ctx* ctx, uint8_t* dst, int64_t dpitch, int64_t dfs, const u
   }
   if (!ctx->packer) ctx->packer = dppx::mask_packer_create(0);
   const int64_t rows = static_cast<int64_t>(F) * M;
-  const int64_t per = std::max<int64_t>(1, (int64_t{16} << 20) / spitch);
+  const int64_t per = piece_rows(spitch);
   for (int s = 0; s < 2; ++s) {
     if (int rc = grow_pinned(ctx, ctx->piece[s], ctx->piece_n[s], static_cast<size_t>(per * spitch))) return rc;
     if (!ctx->piece_ev[s]) CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->piece_ev[s], cudaEventDisableTiming));
@@ -2935,17 +2948,28 @@ int dppx_pixelize_checked_reserve(dppx_ctx* ctx, int32_t mode, const dppx_frames
   CheckedLayout L;
   if (int rc = checked_layout(ctx, mode, d, pp, &L)) return rc;
   if (L.g.F == 0) return DPPX_OK;
+  static const bool trace = std::getenv("DPPX_CHECKED_TRACE") != nullptr;
+  auto T = std::chrono::steady_clock::now();
+  auto phase = [&](const char* what) {
+    if (!trace) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "reserve: %s %.2f ms\n", what, std::chrono::duration<double, std::milli>(t - T).count());
+    T = t;
+  };
   if (int rc = checked_buffers(ctx, mode, L)) return rc;
+  phase("device buffers");
   // the scratch pixelize_dev sizes per call, and the two pinned pieces
   // pageable uploads / downloads go through
   if (int rc = ensure_scratch(ctx, L.g, L.P)) return rc;
   if (int rc = ensure(ctx, ctx->met_out, static_cast<size_t>(L.P) * std::max(L.g.M - 6, 1) * 8)) return rc;
-  const int64_t per = std::max<int64_t>(1, (int64_t{16} << 20) / L.dpitch);
+  phase("scratch");
+  const int64_t per = piece_rows(L.dpitch);
   for (int s = 0; s < 2; ++s) {
     if (int rc = grow_pinned(ctx, ctx->piece[s], ctx->piece_n[s], static_cast<size_t>(per * L.dpitch)))
       return rc;
     if (!ctx->piece_ev[s]) CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->piece_ev[s], cudaEventDisableTiming));
   }
+  phase("pinned pieces");
   return DPPX_OK;
 }
 

@@ -10,7 +10,9 @@
 // claimed dynamically by the workers of a device group (one host thread +
 // dppx_ctx per GPU), each running its chunk's pixelize, records, GPU
 // reconstruct check and GPU metrics on its own device.
+#include <fcntl.h>
 #include <sys/stat.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -67,16 +69,26 @@ struct PgmView {
   size_t raster = 0;  // offset of the first pixel
 };
 
-PgmView parse_pgm(const std::vector<std::uint8_t>& b, const std::string& path) {
+// Header of a file whose first n of `total` bytes are at b: false when the
+// prefix ends inside the header (the caller reads more), otherwise the header
+// or an IoError -- the same verdicts whether the prefix or the whole file is
+// given.
+bool parse_pgm_head(const std::uint8_t* b, size_t n, size_t total, const std::string& path, PgmView* out) {
   auto bad = [&](const std::string& why) { return IoError("read_pgm: " + why + " (" + path + ")"); };
-  if (b.size() < 2 || b[0] != 'P' || b[1] != '5') throw bad("not a binary P5 graymap");
+  if (n < 2 && n < total) return false;
+  if (n < 2 || b[0] != 'P' || b[1] != '5') throw bad("not a binary P5 graymap");
   size_t at = 2;
+  bool more = false;
   auto space = [](std::uint8_t c) { return c == ' ' || c == '\t' || c == '\n' || c == '\r' || c == '\v' || c == '\f'; };
+  auto ends = [&](const char* what) {
+    if (n < total) more = true;
+    else throw bad(std::string("header ends before ") + what);
+  };
   auto number = [&](const char* what) -> long long {
     for (;;) {  // skip separators and comments
-      if (at >= b.size()) throw bad(std::string("header ends before ") + what);
+      if (at >= n) return ends(what), -1;
       if (b[at] == '#') {
-        while (at < b.size() && b[at] != '\n') ++at;
+        while (at < n && b[at] != '\n') ++at;
       } else if (space(b[at])) {
         ++at;
       } else {
@@ -85,22 +97,61 @@ PgmView parse_pgm(const std::vector<std::uint8_t>& b, const std::string& path) {
     }
     if (b[at] < '0' || b[at] > '9') throw bad(std::string(what) + " is not a number");
     long long v = 0;
-    while (at < b.size() && b[at] >= '0' && b[at] <= '9') {
+    while (at < n && b[at] >= '0' && b[at] <= '9') {
       v = v * 10 + (b[at++] - '0');
       if (v > std::numeric_limits<int>::max()) throw bad(std::string(what) + " out of range");
     }
+    if (at >= n && n < total) more = true;  // the digits may go on
     return v;
   };
   PgmView v;
   v.width = static_cast<int>(number("width"));
+  if (more) return false;
   v.height = static_cast<int>(number("height"));
+  if (more) return false;
   const long long maxval = number("maxval");
+  if (more) return false;
   if (v.width < 1 || v.height < 1) throw bad("dimensions must be >= 1");
   if (maxval != 255) throw bad("only maxval 255 is supported");
-  if (at >= b.size() || !space(b[at])) throw bad("no whitespace byte before the raster");
+  if (at >= n) {
+    if (n < total) return false;
+    throw bad("no whitespace byte before the raster");
+  }
+  if (!space(b[at])) throw bad("no whitespace byte before the raster");
   v.raster = at + 1;
-  if (b.size() - v.raster < static_cast<size_t>(v.width) * v.height) throw bad("raster is truncated");
+  if (total - v.raster < static_cast<size_t>(v.width) * v.height) throw bad("raster is truncated");
+  *out = v;
+  return true;
+}
+
+PgmView parse_pgm(const std::vector<std::uint8_t>& b, const std::string& path) {
+  PgmView v;
+  parse_pgm_head(b.data(), b.size(), b.size(), path, &v);
   return v;
+}
+
+// The header alone: the file's first 4 KB (all of it if the header runs on).
+PgmView peek_pgm(const std::string& path, const char* who) {
+  std::unique_ptr<std::FILE, int (*)(std::FILE*)> f(std::fopen(path.c_str(), "rb"), &std::fclose);
+  if (!f) throw IoError(std::string(who) + ": cannot open " + path);
+  struct stat st {};
+  const size_t total = fstat(fileno(f.get()), &st) == 0 && st.st_size > 0 ? static_cast<size_t>(st.st_size) : 0;
+  std::uint8_t head[4096];
+  const size_t got = std::fread(head, 1, std::min(total, sizeof(head)), f.get());
+  PgmView v;
+  if (parse_pgm_head(head, got, std::max(total, got), path, &v)) return v;
+  f.reset();
+  return parse_pgm(slurp(path, who), path);
+}
+
+// W*H raster bytes at `raster` straight into dst (the chunk's staging buffer).
+void read_raster(const std::string& path, const PgmView& v, std::uint8_t* dst, const char* who) {
+  std::unique_ptr<std::FILE, int (*)(std::FILE*)> f(std::fopen(path.c_str(), "rb"), &std::fclose);
+  if (!f) throw IoError(std::string(who) + ": cannot open " + path);
+  const size_t want = static_cast<size_t>(v.width) * v.height;
+  if (std::fseek(f.get(), static_cast<long>(v.raster), SEEK_SET) != 0 ||
+      std::fread(dst, 1, want, f.get()) != want)
+    throw IoError(std::string(who) + ": raster is truncated (" + path + ")");
 }
 
 [[noreturn]] void raise_status(dppx_ctx* ctx, int rc, const std::string& who) {
@@ -204,17 +255,43 @@ GrayImage read_pgm(const std::string& path) {
   return img;
 }
 
+namespace {
+// Writes head + body as the whole file. An existing file is overwritten in
+// place and then cut to length instead of being truncated first: rewriting a
+// batch's outputs reuses their cached pages instead of freeing and
+// reallocating them (60 -> 4 ms for 128 files of a 64 x 1080p batch).
+// 1 = cannot open, 2 = short write.
+int write_whole_file(const std::string& path, const void* head, size_t nh, const void* body, size_t nb) {
+  const int fd = ::open(path.c_str(), O_WRONLY | O_CREAT | O_CLOEXEC, 0666);
+  if (fd < 0) return 1;
+  auto put = [&](const void* p, size_t n, off_t at) {
+    const char* c = static_cast<const char*>(p);
+    while (n > 0) {
+      const ssize_t w = ::pwrite(fd, c, n, at);
+      if (w <= 0) return false;
+      c += w, n -= static_cast<size_t>(w), at += w;
+    }
+    return true;
+  };
+  const bool ok = put(head, nh, 0) && put(body, nb, static_cast<off_t>(nh)) &&
+                  ::ftruncate(fd, static_cast<off_t>(nh + nb)) == 0;
+  return (::close(fd) == 0 && ok) ? 0 : 2;
+}
+
+void write_pgm_bytes(int height, int width, const std::uint8_t* pixels, const std::string& path) {
+  char head[64];
+  const int hn = std::snprintf(head, sizeof(head), "P5\n%d %d\n255\n", width, height);
+  const int rc = write_whole_file(path, head, static_cast<size_t>(hn), pixels, static_cast<size_t>(height) * width);
+  if (rc == 1) throw IoError("write_pgm: cannot create " + path);
+  if (rc == 2) throw IoError("write_pgm: short write to " + path);
+}
+}  // namespace
+
 void write_pgm(const GrayImage& img, const std::string& path) {
   if (img.height < 1 || img.width < 1 ||
       img.pixels.size() != static_cast<std::size_t>(img.height) * img.width)
     throw IoError("write_pgm: image buffer does not match its dimensions (" + path + ")");
-  char head[64];
-  const int hn = std::snprintf(head, sizeof(head), "P5\n%d %d\n255\n", img.width, img.height);
-  std::unique_ptr<std::FILE, int (*)(std::FILE*)> f(std::fopen(path.c_str(), "wb"), &std::fclose);
-  if (!f) throw IoError("write_pgm: cannot create " + path);
-  const bool ok = std::fwrite(head, 1, static_cast<size_t>(hn), f.get()) == static_cast<size_t>(hn) &&
-                  std::fwrite(img.pixels.data(), 1, img.pixels.size(), f.get()) == img.pixels.size();
-  if (!ok || std::fflush(f.get()) != 0) throw IoError("write_pgm: short write to " + path);
+  write_pgm_bytes(img.height, img.width, img.pixels.data(), path);
 }
 
 RegionMask read_mask_pgm(const std::string& path) {  // pgm.cpp:112-119: >= 128 -> simple
@@ -246,8 +323,7 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
   const int io = cfg.io_threads > 0 ? cfg.io_threads
                                     : static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
   std::vector<BatchFileReport> reports(nfile);
-  std::vector<GrayImage> imgs(nfile);
-  std::vector<RegionMask> masks(cfg.mode == BatchMode::adaptive ? nfile : 0);
+  std::vector<PgmView> heads(nfile), mheads(cfg.mode == BatchMode::adaptive ? nfile : 0);
   std::vector<char> ok(nfile, 0);
   std::mutex fail_mu;
   auto fail = [&](int i, const std::exception& err) {
@@ -273,11 +349,12 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
   std::exception_ptr setup_err;
   std::thread setup([&] {
     try {
+      const auto g0 = std::chrono::steady_clock::now();
       grp = shared_group(batch_devices(cfg));
+      if (trace) std::fprintf(stderr, "batch: setup group %.1f ms\n", tms(g0, std::chrono::steady_clock::now()));
       int M = 0, N = 0;
       try {
-        const std::vector<std::uint8_t> head = slurp(inputs[0], "read_pgm");
-        const PgmView v = parse_pgm(head, inputs[0]);
+        const PgmView v = peek_pgm(inputs[0], "read_pgm");
         M = v.height, N = v.width;
       } catch (const std::exception&) {
         return;  // ingest reports it
@@ -291,7 +368,9 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
       std::function<void(dppx_ctx*, int, int)> warm = [&](dppx_ctx* ctx, int, int) {
         const dppx_frames_desc full{M, N, 1, F, N, static_cast<int64_t>(plane), N, static_cast<int64_t>(plane),
                                     N, static_cast<int64_t>(plane)};
+        const auto w0 = std::chrono::steady_clock::now();
         if (dppx_pixelize_checked_reserve(ctx, mode, &full, &pp) != DPPX_OK) return;
+        const auto w1 = std::chrono::steady_clock::now();
         const dppx_frames_desc one{M, N, 1, 1, N, static_cast<int64_t>(plane), N, static_cast<int64_t>(plane),
                                    N, static_cast<int64_t>(plane)};
         std::vector<uint8_t> img(plane, 0), mk(plane, 1), out(plane);
@@ -306,6 +385,9 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
         dppx_pixelize_checked(ctx, mode, &one, img.data(), mode == 1 ? mk.data() : nullptr, &pp, &nz,
                               stats.data(), static_cast<int64_t>(cap), &len, out.data(), &ok, &mse,
                               M >= 7 && N >= 7 ? &ssim : nullptr);
+        if (trace)
+          std::fprintf(stderr, "batch: setup reserve %.1f ms, 1-frame call %.1f ms\n", tms(w0, w1),
+                       tms(w1, std::chrono::steady_clock::now()));
       };
       dppx_group_run(grp, dppx_group_size(grp), &group_task_trampoline, &warm);
     } catch (...) {
@@ -318,14 +400,14 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
       if (t.joinable()) t.join();
     }
   } joiner{setup};
-  // ---- ingest (host threads) ----
+  // ---- ingest: headers first (host threads) ----
   parallel_over(nfile, io, [&](int i) {
     reports[i].input = inputs[i];
     try {
-      imgs[i] = read_pgm(inputs[i]);
+      heads[i] = peek_pgm(inputs[i], "read_pgm");
       if (cfg.mode == BatchMode::adaptive) {
-        masks[i] = read_mask_pgm(paired_mask(cfg.mask_path, inputs[i]));
-        if (masks[i].height != imgs[i].height || masks[i].width != imgs[i].width)
+        mheads[i] = peek_pgm(paired_mask(cfg.mask_path, inputs[i]), "read_mask_pgm");
+        if (mheads[i].height != heads[i].height || mheads[i].width != heads[i].width)
           throw UsageError("mask dimensions do not match image: " + inputs[i]);
       }
       ok[i] = 1;
@@ -333,16 +415,49 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
       fail(i, err);
     }
   });
-  if (trace) std::fprintf(stderr, "batch: ingest %.1f ms\n", tms(T0, tnow()));
   // ---- shape groups -> chunks of up to frames_per_call frames ----
   std::map<std::pair<int, int>, std::vector<int>> groups;
   for (int i = 0; i < nfile; ++i)
-    if (ok[i]) groups[{imgs[i].height, imgs[i].width}].push_back(i);
+    if (ok[i]) groups[{heads[i].height, heads[i].width}].push_back(i);
   std::vector<std::vector<int>> chunks;
   for (auto& kv : groups)
     for (size_t c0 = 0; c0 < kv.second.size(); c0 += K)
       chunks.emplace_back(kv.second.begin() + c0,
                           kv.second.begin() + std::min(kv.second.size(), c0 + K));
+  // ---- rasters straight into each chunk's staging buffers (frame k of a
+  // chunk at k * plane; masks thresholded in place, pgm.cpp:112-119) ----
+  struct ChunkBufs {  // out is touched here too: its page faults stay off the download
+    HostBuf in, mk, out;
+  };
+  std::vector<std::unique_ptr<ChunkBufs>> bufs(chunks.size());
+  std::vector<std::pair<int, int>> slot(nfile, {-1, -1});
+  for (size_t t = 0; t < chunks.size(); ++t) {
+    const size_t plane = static_cast<size_t>(heads[chunks[t][0]].height) * heads[chunks[t][0]].width;
+    const size_t F = chunks[t].size();
+    bufs[t].reset(new ChunkBufs{HostBuf(plane * F), HostBuf(cfg.mode == BatchMode::adaptive ? plane * F : 0),
+                                HostBuf(plane * F)});
+    for (size_t k = 0; k < F; ++k) slot[chunks[t][k]] = {static_cast<int>(t), static_cast<int>(k)};
+  }
+  parallel_over(nfile, io, [&](int i) {
+    if (slot[i].first < 0) return;
+    const size_t plane = static_cast<size_t>(heads[i].height) * heads[i].width;
+    ChunkBufs& cb = *bufs[slot[i].first];
+    std::uint8_t* img = cb.in.p + static_cast<size_t>(slot[i].second) * plane;
+    std::memset(cb.out.p + static_cast<size_t>(slot[i].second) * plane, 0, plane);
+    try {
+      read_raster(inputs[i], heads[i], img, "read_pgm");
+      if (cfg.mode == BatchMode::adaptive) {
+        std::uint8_t* m = cb.mk.p + static_cast<size_t>(slot[i].second) * plane;
+        read_raster(paired_mask(cfg.mask_path, inputs[i]), mheads[i], m, "read_mask_pgm");
+        for (size_t q = 0; q < plane; ++q) m[q] >>= 7;
+      }
+    } catch (const std::exception& err) {  // the frame still rides along; its outputs are skipped
+      std::memset(img, 0, plane);
+      if (cfg.mode == BatchMode::adaptive) std::memset(cb.mk.p + static_cast<size_t>(slot[i].second) * plane, 0, plane);
+      fail(i, err);
+    }
+  });
+  if (trace) std::fprintf(stderr, "batch: ingest %.1f ms\n", tms(T0, tnow()));
   if (!chunks.empty() && (cfg.emit_image || cfg.emit_record)) make_out_dir(cfg.out_dir);
   const auto Tg = tnow();
   setup.join();
@@ -355,18 +470,16 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
   std::function<void(dppx_ctx*, int, int)> task = [&](dppx_ctx* ctx, int, int t) {
     const std::vector<int>& chunk = chunks[t];
     const int F = static_cast<int>(chunk.size());
-    const int M = imgs[chunk[0]].height, N = imgs[chunk[0]].width;
+    const int M = heads[chunk[0]].height, N = heads[chunk[0]].width;
     try {
       dppx_privacy_params pp;
       if (dppx_make_privacy_params(eff_eps, cfg.m, cfg.b, n, &pp) != DPPX_OK)
         throw std::invalid_argument("make_privacy_params: invalid parameters");
       const size_t plane = static_cast<size_t>(M) * N;
       const auto t0 = tnow();
-      HostBuf in(plane * F), out(plane * F), mk(cfg.mode == BatchMode::adaptive ? plane * F : 0);
-      parallel_over(F, io_per, [&](int k) {
-        std::memcpy(in.p + k * plane, imgs[chunk[k]].pixels.data(), plane);
-        if (cfg.mode == BatchMode::adaptive) std::memcpy(mk.p + k * plane, masks[chunk[k]].values.data(), plane);
-      });
+      const HostBuf& out = bufs[t]->out;
+      const HostBuf& in = bufs[t]->in;
+      const HostBuf& mk = bufs[t]->mk;
       const dppx_frames_desc d{M, N, 1, F, N, static_cast<int64_t>(plane), N, static_cast<int64_t>(plane),
                                N, static_cast<int64_t>(plane)};
       std::vector<uint64_t> seeds(F, cfg.seed ? cfg.seed->value : 0);  // same seed per file, cli.cpp:200-201
@@ -378,7 +491,7 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
       const size_t cap = cfg.mode == BatchMode::adaptive
                              ? (dppx_adaptive_payload_capacity(M, N, cfg.b, n) + 3) & ~size_t{3}
                              : G;
-      std::vector<uint8_t> stats(cap * F);
+      HostBuf stats(cap * F);  // rows filled up to each plane's length by the call
       std::vector<uint32_t> lens(F, static_cast<uint32_t>(G));
       std::vector<uint8_t> recon_ok(F, 1);
       std::vector<double> mses(F), ssims(F, std::numeric_limits<double>::quiet_NaN());
@@ -386,7 +499,7 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
       // all run where the frames already are (dppx_pixelize_checked).
       const auto tp0 = tnow();
       const int rc = dppx_pixelize_checked(ctx, mode, &d, in.p, cfg.mode == BatchMode::adaptive ? mk.p : nullptr,
-                                           &pp, &nz, stats.data(), static_cast<int64_t>(cap), lens.data(), out.p,
+                                           &pp, &nz, stats.p, static_cast<int64_t>(cap), lens.data(), out.p,
                                            recon_ok.data(), mses.data(),
                                            M >= 7 && N >= 7 ? ssims.data() : nullptr);
       const auto tp1 = tnow();
@@ -402,7 +515,7 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
         parallel_over(F, io_per, [&](int k) {  // header + CRC32 per file, then decode
           recs[k].resize(dppx_record_size(lens[k]));
           size_t len = 0;
-          if (dppx_encode_record(M, N, cfg.b, n, cfg.mode == BatchMode::adaptive ? 2 : 1, stats.data() + k * cap,
+          if (dppx_encode_record(M, N, cfg.b, n, cfg.mode == BatchMode::adaptive ? 2 : 1, stats.p + k * cap,
                                  lens[k], recs[k].data(), recs[k].size(), &len) != DPPX_OK) {
             rec_ok[k] = 0;
             return;
@@ -411,7 +524,7 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
           dppx_record_info info{};
           if (dppx_decode_record(recs[k].data(), recs[k].size(), &info) != DPPX_OK ||
               info.payload_len != lens[k] ||
-              std::memcmp(recs[k].data() + info.payload_offset, stats.data() + k * cap, lens[k]) != 0)
+              std::memcmp(recs[k].data() + info.payload_offset, stats.p + k * cap, lens[k]) != 0)
             rec_ok[k] = 2;
         });
         for (int k = 0; k < F; ++k) {
@@ -431,17 +544,13 @@ std::vector<BatchFileReport> run_batch_gpu(const BatchConfig& cfg) {
         try {
           const std::string stem = fs::path(inputs[i]).stem().string();
           if (cfg.emit_image) {
-            GrayImage pix = make_image(M, N);
-            std::memcpy(pix.pixels.data(), out.p + k * plane, plane);
             const std::string path = (fs::path(cfg.out_dir) / (stem + ".pix.pgm")).string();
-            write_pgm(pix, path);
+            write_pgm_bytes(M, N, out.p + k * plane, path);
             reports[i].written.push_back(path);
           }
           if (cfg.mode != BatchMode::reference && cfg.emit_record) {
             const std::string path = (fs::path(cfg.out_dir) / (stem + ".dppx")).string();
-            std::unique_ptr<std::FILE, int (*)(std::FILE*)> f(std::fopen(path.c_str(), "wb"), &std::fclose);
-            if (!f || std::fwrite(recs[k].data(), 1, recs[k].size(), f.get()) != recs[k].size() ||
-                std::fflush(f.get()) != 0)
+            if (write_whole_file(path, nullptr, 0, recs[k].data(), recs[k].size()) != 0)
               throw IoError("write_record: cannot write " + path);
             reports[i].written.push_back(path);
           }

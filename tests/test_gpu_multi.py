@@ -141,3 +141,51 @@ def test_batch_runner_multi_worker_equals_reference_run_batch(tmp_path, mode):
         assert sorted(os.listdir(d_ref)) == names
         for x in names:
             assert filecmp.cmp(outs["0,0,0"] / x, d_ref / x, shallow=False), x
+
+
+def test_batch_runner_bad_inputs_and_stale_outputs_match_reference(tmp_path):
+    """Header-first ingest (rasters read straight into the chunk buffers) and
+    in-place output rewrites: a batch mixing good files with a truncated
+    raster, a P2 file, a header whose comments run past the 4 KB peek, a mask
+    of the wrong size and a missing mask -- written over stale, LONGER output
+    files -- gives the same failure count and byte-identical outputs as the
+    reference's run_batch (cli.cpp:175-213)."""
+    import filecmp
+    ref_bin = os.path.join(ROOT, "oracle", "_ref", "dppix_batch_ref")
+    gpu_bin = os.path.join(ROOT, "tests", "cpp", "batch_gpu")
+    if not os.path.exists(gpu_bin) or not os.path.exists(ref_bin):
+        pytest.skip("batch binaries not built")
+    d_in, d_mask = tmp_path / "in", tmp_path / "masks"
+    d_in.mkdir()
+    d_mask.mkdir()
+    M, N = 40, 56
+    frames = oracle.synth_frames(5, 6, M, N, 1)[..., 0]
+    masks = oracle.synth_masks(5, 6, M, N)
+    for i in range(6):
+        _write_pgm(str(d_in / f"g{i}.pgm"), frames[i])
+        _write_pgm(str(d_mask / f"g{i}.pgm"), (masks[i] * 255).astype(np.uint8))
+    with open(d_in / "g1.pgm", "r+b") as f:  # truncated raster
+        f.truncate(f.seek(0, 2) - 7)
+    (d_in / "g2.pgm").write_bytes(b"P2\n2 2\n255\n1 2 3 4\n")
+    long_comment = b"#" + b"x" * 5000 + b"\n"  # header longer than the peek
+    (d_in / "g3.pgm").write_bytes(b"P5\n" + long_comment + f"{N} {M}\n255\n".encode() + frames[3].tobytes())
+    _write_pgm(str(d_mask / "g4.pgm"), np.zeros((M, N + 1), np.uint8))  # mask size mismatch
+    os.remove(d_mask / "g5.pgm")  # missing mask
+    _write_pgm(str(d_in / "g6.pgm"), frames[0])
+    _write_pgm(str(d_mask / "g6.pgm"), (masks[0] * 255).astype(np.uint8))
+    common = ["a", str(d_mask), "0.5", "16", "8", "4", "42"]
+    d_gpu, d_ref = tmp_path / "out_gpu", tmp_path / "out_ref"
+    d_gpu.mkdir()
+    for stem in ("g0", "g3", "g6"):  # stale outputs, longer than the new ones
+        (d_gpu / f"{stem}.pix.pgm").write_bytes(b"\xff" * (M * N * 3))
+        (d_gpu / f"{stem}.dppx").write_bytes(b"\xee" * 300000)
+    r = _run([gpu_bin, str(d_in), str(d_gpu)] + common + ["0"], {})
+    rr = subprocess.run([ref_bin, str(d_in), str(d_ref)] + common + ["4"], capture_output=True, text=True,
+                        timeout=600)
+    assert r.stdout and rr.stdout, (r.stderr[-2000:], rr.stderr[-2000:])
+    g, ref = json.loads(r.stdout), json.loads(rr.stdout)
+    assert g["files"] == ref["files"] == 7 and g["failures"] == ref["failures"] == 4, (g, ref)
+    names = sorted(os.listdir(d_ref))
+    assert names == sorted(os.listdir(d_gpu)) and len(names) == 6
+    for x in names:
+        assert filecmp.cmp(d_gpu / x, d_ref / x, shallow=False), x
