@@ -44,6 +44,7 @@ cudaError_t launch_classify(const ClassifyArgs& a, cudaStream_t s);
 cudaError_t launch_stats_tma(StatsKernel k, const CUtensorMap& tin, const CUtensorMap& tout,
                              const StatsArgs& a, int grid, size_t smem, cudaStream_t s);
 cudaError_t launch_stats_generic(const StatsArgs& a, cudaStream_t s);
+cudaError_t launch_stats_px(const StatsArgs& a, cudaStream_t s);
 cudaError_t launch_expand(const ExpandArgs& a, cudaStream_t s);
 using ExpandKernel = void (*)(const CUtensorMap, const ExpandArgs);
 ExpandKernel select_expand_kernel(int C, int b, int n, bool adaptive, bool packed, int split);
@@ -683,7 +684,12 @@ int run_stats(dppx_ctx* ctx, StatsArgs& a) {
     // Other grid sides (b = 12, 24, 30, 40, 64, 128 ...): row-streaming K1r.
     const int rsm = a.partial_borders ? 0 : rows_smem_bytes(g);
     const int64_t units = static_cast<int64_t>(g.F) * a.row_count;
-    if (rsm > 0 && units <= 0x7FFFFFFF && !std::getenv("DPPX_NO_ROWS")) {
+    static const bool no_px = std::getenv("DPPX_NO_K1P") != nullptr;
+    if (g.b <= 2 && (g.C == 1 || g.C == 3) && !a.partial_borders && !no_px) {
+      // b = 1, 2: K1p, one thread per cell, all loops compile-time
+      timing_begin(ctx, DPPX_K_GENERIC, &pt);
+      if (g.F > 0) CUDA_TRY(ctx, launch_stats_px(a, ctx->stream));
+    } else if (rsm > 0 && units <= 0x7FFFFFFF && !std::getenv("DPPX_NO_ROWS")) {
       a.units = static_cast<int>(units);
       a.div_rows = make_fastdiv(static_cast<uint32_t>(a.row_count));
       timing_begin(ctx, DPPX_K_ROWS, &pt);

@@ -20,6 +20,7 @@
 //                      tma_kernels.cuh, instantiated in tma_c1.cu / tma_c3.cu.)
 //  K1r k_stats_rows    row-streaming statistics for the other grid sides.
 //  K1g k_stats_generic same semantics for any b, n, C and alignment
+//  K1p k_stats_px      b = 1, 2 with b, n, C compile-time
 //                      (Algorithm 1, and shapes K1r cannot hold).
 //  K2  k_expand        statistics -> pixels (broadcast_means / reassemble);
 //                      K2r k_expand_rows for the K1r grid sides.
@@ -635,6 +636,102 @@ __global__ void __launch_bounds__(kGenericThreads) k_stats_generic(const StatsAr
                 o[static_cast<int64_t>(i) * a.opitch + j * g.C + ch] = static_cast<uint8_t>(v);
           }
         }
+    }
+  }
+}
+
+// K1p: grid sides b = 1, 2 (the paper's PPM grid starts at b = 1): one thread
+// per cell as in K1g, but with b, n and C compile-time, so the pixel loops,
+// reflections and subcell loops unroll to straight-line code and both draw
+// environments are formed once per thread (K1g spent ~375 instructions per
+// draw here, mostly loop control). Same statistics, slots and emitted pixels.
+template <int C, int B, int NN>
+__global__ void __launch_bounds__(kGenericThreads) k_stats_px(const StatsArgs a) {
+  static_assert(B == 1 || B == 2, "K1p: b = 1, 2");
+  static_assert(NN >= 1 && NN <= B, "K1p: n <= b");
+  constexpr int SB = B / NN;  // complex subcell side
+  const BatchGeom& g = a.g;
+  const int c = blockIdx.x * kGenericThreads + threadIdx.x;
+  if (c >= g.GC) return;
+  const bool exact = a.exact_noise != 0;
+  const DrawEnv env_s = make_env(a.noise.kind, exact, a.area, a.sigma);
+  const DrawEnv env_c = make_env(a.noise.kind, exact, a.sub_area, a.sigma_sub);
+  int jx[B];
+  bool jin[B];
+#pragma unroll
+  for (int x = 0; x < B; ++x) {
+    const int j = c * B + x;
+    jx[x] = reflect_index(j, g.N) * C;
+    jin[x] = j < g.N;
+  }
+  for (int r = a.row_begin + blockIdx.y; r < a.row_begin + a.row_count; r += gridDim.y)
+  for (int f = blockIdx.z; f < g.F; f += gridDim.z) {
+    const int gidx = r * g.GC + c;
+    const uint8_t* img = a.img + static_cast<int64_t>(f) * a.fstride;
+    bool simple = true;
+    uint32_t slot_s = 0, S_tot = 0;
+    if (a.adaptive) {
+      const uint32_t info = __ldg(a.cellinfo + static_cast<int64_t>(f) * g.G + gidx);
+      simple = info & 1u;
+      slot_s = __ldg(a.rowprefix + static_cast<int64_t>(f) * g.GR + r) + (info >> 1);
+      S_tot = __ldg(a.totals + f);
+    }
+    uint32_t px[B][B][C];
+    int iy[B];
+    bool iin[B];
+#pragma unroll
+    for (int y = 0; y < B; ++y) {
+      const int i = r * B + y;
+      iin[y] = i < g.M;
+      iy[y] = reflect_index(i, g.M);
+      const uint8_t* row = img + static_cast<int64_t>(iy[y]) * a.pitch;
+#pragma unroll
+      for (int x = 0; x < B; ++x)
+#pragma unroll
+        for (int ch = 0; ch < C; ++ch) px[y][x][ch] = __ldg(row + jx[x] + ch);
+    }
+    uint8_t* o = a.out ? a.out + static_cast<int64_t>(f) * a.ofstride : nullptr;
+#pragma unroll
+    for (int ch = 0; ch < C; ++ch) {
+      const uint64_t cs = cell_state(a, f, ch, r, c);
+      uint8_t* plane = a.stats + static_cast<int64_t>(f * C + ch) * a.sstride;
+      if (simple || NN == 1) {
+        uint32_t sum = 0;
+#pragma unroll
+        for (int y = 0; y < B; ++y)
+#pragma unroll
+          for (int x = 0; x < B; ++x) sum += px[y][x][ch];
+        const uint32_t v = draw_stat(a, simple ? env_s : env_c, sum, cs, f, ch, r, c, 0, 0, gidx);
+        plane[stat_offset(a, simple, gidx, slot_s, S_tot, 0, 0)] = static_cast<uint8_t>(v);
+        if (o) {
+#pragma unroll
+          for (int y = 0; y < B; ++y)
+#pragma unroll
+            for (int x = 0; x < B; ++x)
+              if (iin[y] && jin[x]) o[static_cast<int64_t>(r * B + y) * a.opitch + jx[x] + ch] = static_cast<uint8_t>(v);
+        }
+      } else {
+#pragma unroll
+        for (int sr = 0; sr < NN; ++sr)
+#pragma unroll
+          for (int sc = 0; sc < NN; ++sc) {
+            uint32_t sum = 0;
+#pragma unroll
+            for (int y = sr * SB; y < sr * SB + SB; ++y)
+#pragma unroll
+              for (int x = sc * SB; x < sc * SB + SB; ++x) sum += px[y][x][ch];
+            const uint32_t v = draw_stat(a, env_c, sum, cs, f, ch, r, c, sr, sc, gidx);
+            plane[stat_offset(a, false, gidx, slot_s, S_tot, sr, sc)] = static_cast<uint8_t>(v);
+            if (o) {
+#pragma unroll
+              for (int y = sr * SB; y < sr * SB + SB; ++y)
+#pragma unroll
+                for (int x = sc * SB; x < sc * SB + SB; ++x)
+                  if (iin[y] && jin[x])
+                    o[static_cast<int64_t>(r * B + y) * a.opitch + jx[x] + ch] = static_cast<uint8_t>(v);
+            }
+          }
+      }
     }
   }
 }
@@ -1419,6 +1516,27 @@ cudaError_t launch_stats_generic(const StatsArgs& a, cudaStream_t s) {
             a.row_count < 65535 ? (a.row_count > 0 ? a.row_count : 1) : 65535,
             a.g.F < 65535 ? a.g.F : 65535);
   k_stats_generic<<<grid, kGenericThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// K1p for b = 1, 2 (C = 1, 3; not Algorithm 1's partial borders).
+cudaError_t launch_stats_px(const StatsArgs& a, cudaStream_t s) {
+  void (*k)(const StatsArgs) = nullptr;
+  const int b = a.g.b, n = a.adaptive ? a.g.n : 1;
+  if (a.g.C == 1) k = b == 1 ? k_stats_px<1, 1, 1> : n == 2 ? k_stats_px<1, 2, 2> : k_stats_px<1, 2, 1>;
+  else if (a.g.C == 3) k = b == 1 ? k_stats_px<3, 1, 1> : n == 2 ? k_stats_px<3, 2, 2> : k_stats_px<3, 2, 1>;
+  if (!k || b > 2 || a.partial_borders) return cudaErrorNotSupported;
+  // several grid rows per thread (DPPX_K1P_ROWS, default 4): the per-thread
+  // setup (two draw environments, column offsets) is paid once per 4 cells
+  static const int rpt = [] {
+    const char* e = std::getenv("DPPX_K1P_ROWS");
+    const int v = e ? std::atoi(e) : 4;
+    return v > 0 ? v : 4;
+  }();
+  const int rows = a.row_count > 0 ? (a.row_count + rpt - 1) / rpt : 1;
+  dim3 grid((a.g.GC + kGenericThreads - 1) / kGenericThreads, rows < 65535 ? rows : 65535,
+            a.g.F < 65535 ? a.g.F : 65535);
+  k<<<grid, kGenericThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -1285,3 +1285,35 @@ def test_small_frame_paths_agree(ctx, M, N, C, b, n, mode):
                                           p.sigma, p.sigma_sub, kind, oseeds)
         assert list(ref_st) == list(rp)
         assert np.array_equal(ref_img[0].reshape(-1), np.asarray(ri).reshape(-1))
+
+
+@pytest.mark.parametrize("b,n,C", [(1, 1, 1), (1, 1, 3), (2, 1, 1), (2, 1, 3), (2, 2, 1), (2, 2, 3)])
+@pytest.mark.parametrize("kind", ["keyed", "philox", "none"])
+def test_small_grid_sides_k1p(ctx, b, n, C, kind):
+    """b = 1, 2 (the bottom of the paper's PPM grid) take K1p (k_stats_px):
+    statistics, payloads and emitted frames bit-exact vs the oracle, uniform
+    and adaptive, on odd shapes (reflected last row / column at b = 2)."""
+    F, M, N = 3, 37, 53
+    rng = np.random.default_rng(b * 10 + n * 3 + C)
+    frames = rng.integers(0, 256, (F, M, N, C), np.uint8)
+    masks = (rng.random((F, M, N)) < 0.5).astype(np.uint8)
+    masks[:, : M // 3] = 1
+    masks[1] = 0  # all complex
+    p = dp.make_privacy_params(0.5, 16, b, n)
+    nk = {"keyed": dp.NOISE_KEYED, "philox": dp.NOISE_PHILOX, "none": dp.NOISE_NONE}[kind]
+    # Philox: one stream seed, counters carry (frame, channel, cell, subcell)
+    seeds = {"keyed": dp.plane_seeds(13, F, C), "philox": [0x5EED] * (F * C), "none": None}[kind]
+    ctx.reset_stats()
+    ctx.set_timing(True)
+    try:
+        pls, img = ctx.pixelize_adaptive(frames, masks, p, nk, seeds)
+        rp, ri = _oracle_adaptive(frames, masks, p, kind, seeds)
+        assert pls == rp and np.array_equal(img, ri)
+        if n == 1:
+            means, uimg = ctx.pixelize_uniform(frames, p, nk, seeds)
+            rm, rui = _oracle_uniform(frames, p, kind, seeds)
+            assert np.array_equal(means, rm) and np.array_equal(uimg, rui)
+        st = ctx.stats()
+    finally:
+        ctx.set_timing(False)
+    assert st["launches"]["stats_generic"] >= 1 and st["launches"]["stats_rows"] == 0, st["launches"]
