@@ -359,6 +359,9 @@ def main():
     # `out` below is the bench's own buffer: its row padding (pitch - N*C) is
     # scratch, so rows may end on whole 32-byte sectors (dppx_ctx_set_out_pad_scratch).
     ctx.set_out_pad_scratch(not args.no_pad_scratch)
+    # torch's work (allocations, L2 flushes, reductions) runs on the context
+    # stream: ordered with the kernels, and the _dev wrappers add no fences
+    torch.cuda.set_stream(torch.cuda.ExternalStream(ctx.stream, device=dev))
     geom = dp.grid_dims(M, N, b)
     G = geom.grid_count()
     p = dp.make_privacy_params(eps, m, b, n)

@@ -23,6 +23,7 @@ from __future__ import annotations
 import ctypes as C
 import dataclasses
 import os
+import sys
 import threading
 from typing import List, Optional, Sequence
 
@@ -765,6 +766,33 @@ class Group(Context):
     def set_timing(self, on: bool):
         for i in range(len(self.devices)):
             _lib.dppx_ctx_set_timing(_lib.dppx_group_ctx(self._g, i), 1 if on else 0)
+
+
+def _torch_ordered(fn):
+    """Orders a ``_dev`` call with torch: the context stream first waits for
+    torch's current stream (tensors just allocated / filled by torch are ready),
+    and torch's current stream then waits for the context stream (torch ops on
+    the outputs see the results). Two stream-event pairs, no host sync; skipped
+    when torch's current stream already is the context stream."""
+    def wrapped(self, *a, **k):
+        t = sys.modules.get("torch")
+        if t is None or not t.cuda.is_available():
+            return fn(self, *a, **k)
+        h = self.stream
+        cur = t.cuda.current_stream(self.device)
+        if h == 0 or cur.cuda_stream == h:
+            return fn(self, *a, **k)
+        ours = t.cuda.ExternalStream(h, device=self.device)
+        ours.wait_stream(cur)
+        r = fn(self, *a, **k)
+        cur.wait_stream(ours)
+        return r
+    wrapped.__name__, wrapped.__doc__ = fn.__name__, fn.__doc__
+    return wrapped
+
+
+for _name in [x for x in vars(Context) if x.endswith("_dev")]:
+    setattr(Context, _name, _torch_ordered(getattr(Context, _name)))
 
 
 def _group_unsupported(name):

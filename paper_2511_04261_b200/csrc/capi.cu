@@ -521,6 +521,7 @@ int classify(dppx_ctx* ctx, const BatchGeom& g, int planes, bool from_payload, c
   a.counters = static_cast<uint32_t*>(ctx->counters.p);
   a.status = static_cast<int*>(ctx->status.p);
   a.area = static_cast<double>(g.b) * g.b;
+  a.inv_area_pow2 = (g.b & (g.b - 1)) == 0 ? 1.0 / a.area : 0.0;  // exact: b = 2^k
   PendingTiming pt;
   timing_begin(ctx, DPPX_K_CLASSIFY, &pt);
   CUDA_TRY(ctx, launch_classify(a, ctx->stream));
@@ -550,6 +551,7 @@ int classify_flags(dppx_ctx* ctx, const BatchGeom& g, const uint8_t* flags, uint
   a.counters = static_cast<uint32_t*>(ctx->counters.p);
   a.status = static_cast<int*>(ctx->status.p);
   a.area = static_cast<double>(g.b) * g.b;
+  a.inv_area_pow2 = (g.b & (g.b - 1)) == 0 ? 1.0 / a.area : 0.0;  // exact: b = 2^k
   PendingTiming pt;
   timing_begin(ctx, DPPX_K_CLASSIFY, &pt);
   CUDA_TRY(ctx, launch_classify(a, ctx->stream));

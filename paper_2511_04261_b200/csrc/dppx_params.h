@@ -81,6 +81,7 @@ struct ClassifyArgs {
   uint32_t* counters;        // [P] self-resetting arrival tickets
   int* status;               // set to DPPX_ERR_CORRUPT on inconsistent payloads
   double area;               // (double)b*b
+  double inv_area_pow2;      // 1 / area when b is a power of two (exact), else 0: K0 multiplies
   // from_payload == 2: variance classification (extension): cell complex iff
   // var(C*b*b samples) >= var_tau, computed from the frames themselves.
   const uint8_t* img;

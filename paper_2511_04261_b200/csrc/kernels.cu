@@ -172,6 +172,7 @@ __device__ __forceinline__ uint32_t mask_cell_sum(const ClassifyArgs& a, const u
   const int b = g.b;
   const int j0 = c * b;
   if (a.mask_bits) return mask_cell_sum_bits(base, a.mpitch, g.M, g.N, b, r, c);
+  if (b == 1) return __ldg(base + static_cast<int64_t>(r) * a.mpitch + c);  // grid = pixels
   if (j0 + b <= g.N && a.vec > 1) {
     if (a.vec == 16) {
       if (b == 16) return mask_cell_sum_vec<16>(a, base, r, j0);
@@ -378,7 +379,9 @@ __global__ void __launch_bounds__(kClassifyThreads, BAND ? 10 : 8) k_classify(co
           }
           // mask_grid_mean (image.cpp:191-202) then static_cast<float>
           // (adaptive.cpp:59-60).
-          mean = __double2float_rn(__ddiv_rn(static_cast<double>(s), a.area));
+          mean = __double2float_rn(a.inv_area_pow2 != 0.0  // b = 2^k: exact product, no DDIV
+                                       ? static_cast<double>(s) * a.inv_area_pow2
+                                       : __ddiv_rn(static_cast<double>(s), a.area));
           for (int ch = 0; ch < g.C; ++ch)
             reinterpret_cast<float*>(a.payload + (static_cast<int64_t>(p) * g.C + ch) * a.pstride)
                 [cell] = mean;
@@ -506,7 +509,9 @@ __global__ void __launch_bounds__(kClassifyThreads) k_classify_frames(const Clas
           const uint16_t* cs = colsum + r * PW + c * g.b;
           for (int k = 0; k < g.b; ++k) sum += cs[k];
           // mask_grid_mean (image.cpp:191-202) then static_cast<float> (adaptive.cpp:59-60)
-          mean = __double2float_rn(__ddiv_rn(static_cast<double>(sum), a.area));
+          mean = __double2float_rn(a.inv_area_pow2 != 0.0  // b = 2^k: exact product, no DDIV
+                                       ? static_cast<double>(sum) * a.inv_area_pow2
+                                       : __ddiv_rn(static_cast<double>(sum), a.area));
           for (int ch = 0; ch < g.C; ++ch)
             reinterpret_cast<float*>(a.payload + (static_cast<int64_t>(p) * g.C + ch) * a.pstride)[cell] = mean;
         } else {
