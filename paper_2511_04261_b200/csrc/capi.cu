@@ -46,6 +46,7 @@ cudaError_t launch_stats_tma(StatsKernel k, const CUtensorMap& tin, const CUtens
 cudaError_t launch_stats_generic(const StatsArgs& a, cudaStream_t s);
 cudaError_t launch_stats_px(const StatsArgs& a, cudaStream_t s);
 cudaError_t launch_expand(const ExpandArgs& a, cudaStream_t s);
+cudaError_t launch_expand_px(const ExpandArgs& a, cudaStream_t s);
 using ExpandKernel = void (*)(const CUtensorMap, const ExpandArgs);
 ExpandKernel select_expand_kernel(int C, int b, int n, bool adaptive, bool packed, int split);
 cudaError_t launch_expand_tma(ExpandKernel k, const CUtensorMap& tout, const ExpandArgs& a,
@@ -975,6 +976,8 @@ int expand_dev(dppx_ctx* ctx, const dppx_frames_desc* d, const uint8_t* stats, i
     }
     (void)per_sm;
     CUDA_TRY(ctx, launch_expand_tma(k, tout, e, e.units, smem, ctx->stream));
+  } else if (g.b <= 2 && (g.C == 1 || g.C == 3) && !std::getenv("DPPX_NO_K2P")) {
+    CUDA_TRY(ctx, launch_expand_px(e, ctx->stream));  // b = 1, 2: K2p
   } else if (const int rsm = rows_smem_bytes(g);
              rsm > 0 && static_cast<int64_t>(g.F) * g.GR <= 0x7FFFFFFF && !std::getenv("DPPX_NO_ROWS")) {
     CUDA_TRY(ctx, launch_expand_rows(e, static_cast<size_t>(rsm), ctx->stream));

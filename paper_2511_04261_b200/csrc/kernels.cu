@@ -20,7 +20,7 @@
 //                      tma_kernels.cuh, instantiated in tma_c1.cu / tma_c3.cu.)
 //  K1r k_stats_rows    row-streaming statistics for the other grid sides.
 //  K1g k_stats_generic same semantics for any b, n, C and alignment
-//  K1p k_stats_px      b = 1, 2 with b, n, C compile-time
+//  K1p k_stats_px      b = 1, 2 with b, n, C compile-time (K2p k_expand_px: reconstruction)
 //                      (Algorithm 1, and shapes K1r cannot hold).
 //  K2  k_expand        statistics -> pixels (broadcast_means / reassemble);
 //                      K2r k_expand_rows for the K1r grid sides.
@@ -1090,6 +1090,82 @@ __global__ void __launch_bounds__(kGenericThreads) k_expand(const ExpandArgs a) 
               sub[((i - i0) / g.sb) * g.n + (j - j0) / g.sb];
     }
   }
+}
+
+// K2p: reconstruction for b = 1, 2 (K1p's counterpart): one thread per cell
+// and all channels of a frame, b, n, C compile-time; per channel plane the
+// cell's slot (K0 on the payload means) gives one simple value or the n x n
+// complex values, written to the b x b pixels.
+template <int C, int B, int NN>
+__global__ void __launch_bounds__(kGenericThreads) k_expand_px(const ExpandArgs a) {
+  constexpr int SB = B / NN;
+  const BatchGeom& g = a.g;
+  const int c = blockIdx.x * kGenericThreads + threadIdx.x;
+  if (c >= g.GC) return;
+  const int64_t base = 4ll * g.G + 4;
+  for (int r = blockIdx.y; r < g.GR; r += gridDim.y)
+  for (int f = blockIdx.z; f < g.F; f += gridDim.z) {
+    const int gidx = r * g.GC + c;
+    uint8_t v[C][B][B];
+#pragma unroll
+    for (int ch = 0; ch < C; ++ch) {
+      const int64_t p = static_cast<int64_t>(f) * C + ch;
+      const uint8_t* st = a.stats + p * a.sstride;
+      if (!a.adaptive) {
+        const uint8_t x = __ldg(st + gidx);
+#pragma unroll
+        for (int y = 0; y < B; ++y)
+#pragma unroll
+          for (int xx = 0; xx < B; ++xx) v[ch][y][xx] = x;
+        continue;
+      }
+      const uint32_t info = __ldg(a.cellinfo + p * g.G + gidx);
+      const uint32_t slot_s = __ldg(a.rowprefix + p * g.GR + r) + (info >> 1);
+      if ((info & 1u) || NN == 1) {
+        const uint8_t x = (info & 1u)
+                              ? __ldg(st + base + slot_s)
+                              : __ldg(st + base + __ldg(a.totals + p) + (static_cast<uint32_t>(gidx) - slot_s));
+#pragma unroll
+        for (int y = 0; y < B; ++y)
+#pragma unroll
+          for (int xx = 0; xx < B; ++xx) v[ch][y][xx] = x;
+      } else {
+        const uint8_t* sub = st + base + __ldg(a.totals + p) +
+                             static_cast<int64_t>(static_cast<uint32_t>(gidx) - slot_s) * NN * NN;
+#pragma unroll
+        for (int y = 0; y < B; ++y)
+#pragma unroll
+          for (int xx = 0; xx < B; ++xx) v[ch][y][xx] = __ldg(sub + (y / SB) * NN + xx / SB);
+      }
+    }
+    uint8_t* o = a.out + static_cast<int64_t>(f) * a.ofstride;
+#pragma unroll
+    for (int y = 0; y < B; ++y) {
+      const int i = r * B + y;
+      if (i >= g.M) break;
+#pragma unroll
+      for (int xx = 0; xx < B; ++xx) {
+        const int j = c * B + xx;
+        if (j >= g.N) break;
+        uint8_t* q = o + static_cast<int64_t>(i) * a.opitch + static_cast<int64_t>(j) * C;
+#pragma unroll
+        for (int ch = 0; ch < C; ++ch) q[ch] = v[ch][y][xx];
+      }
+    }
+  }
+}
+
+cudaError_t launch_expand_px(const ExpandArgs& a, cudaStream_t s) {
+  void (*k)(const ExpandArgs) = nullptr;
+  const int b = a.g.b, n = a.adaptive ? a.g.n : 1;
+  if (a.g.C == 1) k = b == 1 ? k_expand_px<1, 1, 1> : n == 2 ? k_expand_px<1, 2, 2> : k_expand_px<1, 2, 1>;
+  else if (a.g.C == 3) k = b == 1 ? k_expand_px<3, 1, 1> : n == 2 ? k_expand_px<3, 2, 2> : k_expand_px<3, 2, 1>;
+  if (!k || b > 2) return cudaErrorNotSupported;
+  const int rows = (a.g.GR + 3) / 4;  // 4 grid rows per thread
+  dim3 grid((a.g.GC + kGenericThreads - 1) / kGenericThreads, rows < 65535 ? rows : 65535,
+            a.g.F < 65535 ? a.g.F : 65535);
+  k<<<grid, kGenericThreads, 0, s>>>(a);
+  return cudaGetLastError();
 }
 
 // ============================================================================

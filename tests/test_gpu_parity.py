@@ -1314,6 +1314,10 @@ def test_small_grid_sides_k1p(ctx, b, n, C, kind):
             rm, rui = _oracle_uniform(frames, p, kind, seeds)
             assert np.array_equal(means, rm) and np.array_equal(uimg, rui)
         st = ctx.stats()
+        # reconstruction (K2p): reassemble / broadcast give the emitted frames back
+        assert np.array_equal(ctx.reassemble(pls, M, N, b, n, channels=C, frames=F), img)
+        if n == 1:
+            assert np.array_equal(ctx.broadcast_means(means, M, N, b, channels=C, frames=F), uimg)
     finally:
         ctx.set_timing(False)
     assert st["launches"]["stats_generic"] >= 1 and st["launches"]["stats_rows"] == 0, st["launches"]

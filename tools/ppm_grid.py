@@ -45,10 +45,23 @@ def main():
             ctx.set_timing(False)
             fam = [k for k, v in s["launches"].items() if v and k != "classify"]
             k1 = sum(s["device_ms"][k] for k in fam)
-            alg = F * M * N * C * 2 + int(lens.sum().item())
+            pay = int(lens.sum().item())
+            alg = F * M * N * C * 2 + pay
+            # reconstruction (reassemble: K0 on the payload means + K2)
+            ctx.reassemble_dev(d, stats, st, lens, b, n, out)
+            ctx.synchronize()
+            ctx.reset_stats()
+            ctx.set_timing(True)
+            ctx.reassemble_dev(d, stats, st, lens, b, n, out)
+            ctx.synchronize()
+            s2 = ctx.stats()
+            ctx.set_timing(False)
+            k2 = s2["device_ms"]["expand"]
             rows.append({"b": b, "n": n, "kernel": fam, "k1_ms": round(k1, 3),
                          "k0_ms": round(s["device_ms"]["classify"], 3),
-                         "k1_frac": round(alg / (k1 / 1e3) / 1e9 / peak, 3)})
+                         "k1_frac": round(alg / (k1 / 1e3) / 1e9 / peak, 3),
+                         "k2_ms": round(k2, 3),
+                         "k2_frac": round((pay + F * M * N * C) / (k2 / 1e3) / 1e9 / peak, 3) if k2 else None})
             del stats, lens
             n *= 2
         b *= 2
