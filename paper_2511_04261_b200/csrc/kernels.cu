@@ -753,6 +753,10 @@ __global__ void __launch_bounds__(kGenericThreads) k_stats_px(const StatsArgs a)
 // per vertical subcell (each output row written once, coalesced).
 // ============================================================================
 constexpr int kRowThreads = 256;
+// K1r CTAs grow to 1024 threads when there are too few (frame, grid row) units
+// to fill the GPU (large b on few frames: 8 x 4K at b = 128 is 136 units).
+// (kRowThreadsMax, 1) caps registers at 64 like (256, 4) did.
+constexpr int kRowThreadsMax = 1024;
 
 struct RowSmem {  // byte offsets into dynamic smem (host and device agree)
   int vg;  // vertical subcells whose byte-column sums are held at once
@@ -796,7 +800,7 @@ __device__ void rows_emit(const BatchGeom& g, int r, uint8_t* out_frame, int64_t
     if (y0 >= g.M) break;
     const int y1 = min(y0 + g.sb, g.M);
     // pattern row: one thread per subcell column (sb pixels of C fixed values)
-    for (int sidx = t; sidx < NS; sidx += kRowThreads) {
+    for (int sidx = t; sidx < NS; sidx += static_cast<int>(blockDim.x)) {
       const int c = static_cast<int>(div_n.div(static_cast<uint32_t>(sidx)));
       uint8_t v[C];
 #pragma unroll
@@ -812,11 +816,11 @@ __device__ void rows_emit(const BatchGeom& g, int r, uint8_t* out_frame, int64_t
       uint8_t* orow = out_frame + static_cast<int64_t>(y) * opitch;
       if (vec16) {
         const int n16 = RB >> 4;
-        for (int q = t; q < n16; q += kRowThreads)
+        for (int q = t; q < n16; q += static_cast<int>(blockDim.x))
           reinterpret_cast<uint4*>(orow)[q] = reinterpret_cast<const uint4*>(pattern)[q];
-        for (int x = (n16 << 4) + t; x < RB; x += kRowThreads) orow[x] = pattern[x];
+        for (int x = (n16 << 4) + t; x < RB; x += static_cast<int>(blockDim.x)) orow[x] = pattern[x];
       } else {
-        for (int x = t; x < RB; x += kRowThreads) orow[x] = pattern[x];
+        for (int x = t; x < RB; x += static_cast<int>(blockDim.x)) orow[x] = pattern[x];
       }
     }
     __syncthreads();
@@ -826,8 +830,8 @@ __device__ void rows_emit(const BatchGeom& g, int r, uint8_t* out_frame, int64_t
 // CW: bytes per column chunk (16, or 8 when 16-byte chunks would leave the
 // CTA's last pass mostly idle: 5775-byte padded rows = 361 chunks of 16 over
 // 256 threads, the load phase then ends at a barrier half the block waits at).
-template <int C, bool ADAPTIVE, bool VEC16, int CW>
-__global__ void __launch_bounds__(kRowThreads, 4) k_stats_rows(const StatsArgs a) {
+template <int C, bool ADAPTIVE, bool VEC16, int CW, int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) k_stats_rows(const StatsArgs a) {
   constexpr int NW = CW / 4;
   extern __shared__ __align__(16) uint8_t rsm[];
   const BatchGeom& g = a.g;
@@ -855,14 +859,14 @@ __global__ void __launch_bounds__(kRowThreads, 4) k_stats_rows(const StatsArgs a
     if (ADAPTIVE) {
       S_tot = __ldg(&a.totals[f]);
       const uint32_t rowpre = __ldg(&a.rowprefix[static_cast<int64_t>(f) * g.GR + r]);
-      for (int c = t; c < g.GC; c += kRowThreads) {
+      for (int c = t; c < g.GC; c += NT) {
         const uint32_t info = __ldg(&a.cellinfo[static_cast<int64_t>(f) * g.G + r * g.GC + c]);
 #pragma unroll
         for (int ch = 0; ch < C; ++ch) flag[c * C + ch] = info & 1u;
         slot[c] = rowpre + (info >> 1);
       }
     }
-    for (int e = t; e < g.GC * C; e += kRowThreads) {
+    for (int e = t; e < g.GC * C; e += NT) {
       cellsum[e] = 0;
       const int c = e / C, ch = e - c * C;
       cstate[e] = cell_state(a, f, ch, r, c);  // one mix64 per cell and channel
@@ -875,7 +879,7 @@ __global__ void __launch_bounds__(kRowThreads, 4) k_stats_rows(const StatsArgs a
       // of one chunk at a time (8 live SWAR counters, flushed per vertical
       // subcell; rows unrolled so several loads are in flight); a warp reads
       // 512 contiguous bytes per row.
-      for (int x0 = t * CW; x0 < PB; x0 += kRowThreads * CW) {
+      for (int x0 = t * CW; x0 < PB; x0 += NT * CW) {
         const uint8_t* colp = frame + x0;
         const bool fast = VEC16 && x0 + CW <= RB;
         for (int vg = 0; vg < nv; ++vg) {
@@ -935,8 +939,8 @@ __global__ void __launch_bounds__(kRowThreads, 4) k_stats_rows(const StatsArgs a
       }
       __syncthreads();
       // ---- subcell sums; complex subcells drawn now, simple cells accumulate ----
-      for (int item = t; item < nv * NS * C; item += kRowThreads) {
-        const int vi = item / (NS * C);
+      for (int item = t; item < nv * NS * C; item += NT) {
+        const int vi = nv == 1 ? 0 : item / (NS * C);
         const int rem = item - vi * (NS * C);
         const int vs = v0 + vi;
         const int sidx = rem / C, ch = rem - sidx * C;
@@ -963,7 +967,7 @@ __global__ void __launch_bounds__(kRowThreads, 4) k_stats_rows(const StatsArgs a
       __syncthreads();
     }
     if (ADAPTIVE) {  // simple cells: one draw per channel at sigma
-      for (int item = t; item < g.GC * C; item += kRowThreads) {
+      for (int item = t; item < g.GC * C; item += NT) {
         const int c = item / C, ch = item - c * C;
         if (!flag[item]) continue;
         const int gidx = r * g.GC + c;
@@ -1561,8 +1565,13 @@ cudaError_t launch_classify(const ClassifyArgs& a, cudaStream_t s) {
   // Narrow frames (a grid row at most half the block): one CTA per frame.
   // (DPPX_NO_K0_FRAMES: A/B knob)
   static const bool frames_off = std::getenv("DPPX_NO_K0_FRAMES") != nullptr;
+  // ... and only when that gives enough CTAs or the frames are small: one CTA
+  // per 1080p frame at b = 128 (GC = 15) left 120 CTAs on 148 SMs (1.37 ms;
+  // the per-row kernel: GR CTAs per frame).
+  const bool many = a.planes >= 2 * 148 ||
+                    static_cast<int64_t>(a.g.M) * a.g.N <= (int64_t{1} << 16);
   if ((a.from_payload == 0 || a.from_payload == 1) && !a.mask_bits && a.g.GC * 2 <= kClassifyThreads &&
-      !frames_off) {
+      many && !frames_off) {
     const size_t smem = 4 * static_cast<size_t>(a.g.G) +
                         (a.from_payload == 0 ? 2 * static_cast<size_t>(a.g.GR) * a.g.GC * a.g.b : 0);
     if (smem <= 48 * 1024 && a.g.b <= 257) {
@@ -1632,13 +1641,23 @@ int rows_smem_bytes(const BatchGeom& g) {
 
 template <int C, int CW>
 cudaError_t launch_rows_cw(const StatsArgs& a, size_t smem, bool vec16, cudaStream_t s) {
-  auto k = a.adaptive ? (vec16 ? k_stats_rows<C, true, true, CW> : k_stats_rows<C, true, false, CW>)
-                      : (vec16 ? k_stats_rows<C, false, true, CW> : k_stats_rows<C, false, false, CW>);
+  const int grid = a.units < 0x7FFFFFFF ? a.units : 0x7FFFFFFF;
+  // few units: 1024-thread CTAs (DPPX_ROWS_THREADS=256 / 1024 forces one);
+  // separate instantiations, so the 256-thread code keeps its (256, 4) bounds
+  static const int forced = std::getenv("DPPX_ROWS_THREADS") ? std::atoi(std::getenv("DPPX_ROWS_THREADS")) : 0;
+  const bool wide = forced ? forced == kRowThreadsMax : static_cast<int64_t>(grid) * kRowThreads < 148ll * 1024;
+  using K = void (*)(const StatsArgs);
+  K k;
+  if (wide)
+    k = a.adaptive ? (vec16 ? k_stats_rows<C, true, true, CW, kRowThreadsMax> : k_stats_rows<C, true, false, CW, kRowThreadsMax>)
+                   : (vec16 ? k_stats_rows<C, false, true, CW, kRowThreadsMax> : k_stats_rows<C, false, false, CW, kRowThreadsMax>);
+  else
+    k = a.adaptive ? (vec16 ? k_stats_rows<C, true, true, CW, kRowThreads> : k_stats_rows<C, true, false, CW, kRowThreads>)
+                   : (vec16 ? k_stats_rows<C, false, true, CW, kRowThreads> : k_stats_rows<C, false, false, CW, kRowThreads>);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  const int grid = a.units < 0x7FFFFFFF ? a.units : 0x7FFFFFFF;
-  k<<<grid, kRowThreads, smem, s>>>(a);
+  k<<<grid, wide ? kRowThreadsMax : kRowThreads, smem, s>>>(a);
   return cudaGetLastError();
 }
 
