@@ -1321,3 +1321,44 @@ def test_small_grid_sides_k1p(ctx, b, n, C, kind):
     finally:
         ctx.set_timing(False)
     assert st["launches"]["stats_generic"] >= 1 and st["launches"]["stats_rows"] == 0, st["launches"]
+
+
+@pytest.mark.parametrize("n", [1, 6])
+def test_rows_kernel_both_cta_widths(ctx, n):
+    """K1r launches 1024-thread CTAs for few (frame, grid row) units and
+    256-thread CTAs otherwise: b = 42 (K1r) on 2 frames (48 units, wide) and on
+    30 frames (720 units, narrow) in one device call, both bit-exact vs the
+    oracle."""
+    import torch
+    dev = torch.device("cuda:0")
+    b, M, N, C = 42, 1008, 84, 3
+    for F in (2, 30):
+        rng = np.random.default_rng(F * 7 + n)
+        frames = rng.integers(0, 256, (F, M, N, C), np.uint8)
+        masks = (rng.random((F, M, N)) < 0.5).astype(np.uint8)
+        masks[:, : M // 2] = 1
+        p = dp.make_privacy_params(0.5, 16, b, n)
+        seeds = dp.plane_seeds(17, F, C)
+        nz, keep = dp.Context._noise(dp.NOISE_KEYED, seeds)
+        d = dp._desc(M, N, C, F)
+        img = torch.from_numpy(frames.reshape(F, M, N * C)).to(dev)
+        mk = torch.from_numpy(masks).to(dev)
+        out = torch.zeros_like(img)
+        cap = dp.adaptive_payload_capacity(M, N, b, n)
+        st = (cap + 15) // 16 * 16
+        stats = torch.zeros((F * C, st), dtype=torch.uint8, device=dev)
+        lens = torch.zeros(F * C, dtype=torch.int32, device=dev)
+        ctx.reset_stats()
+        ctx.set_timing(True)
+        try:
+            ctx.pixelize_adaptive_dev(d, img, mk, p, nz, stats, st, lens, out)
+            ctx.synchronize()
+            launches = ctx.stats()["launches"]
+        finally:
+            ctx.set_timing(False)
+        assert launches["stats_rows"] == 1, launches
+        rp, ri = _oracle_adaptive(frames, masks, p, "keyed", seeds)
+        sc, lc = stats.cpu().numpy(), lens.cpu().numpy()
+        assert [bytes(sc[i, :lc[i]]) for i in range(F * C)] == rp, F
+        assert np.array_equal(out.cpu().numpy().reshape(F, M, N, C), ri), F
+        del keep
