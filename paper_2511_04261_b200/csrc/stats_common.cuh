@@ -23,6 +23,14 @@ __device__ __forceinline__ int64_t stat_offset(const StatsArgs& a, bool simple, 
   return base + S_tot + static_cast<int64_t>(slot_c) * a.g.n * a.g.n + sr * a.g.n + sc;
 }
 
+// stat_offset of complex subcell k = sr * n + sc with n known at compile time
+// (NN = n * n): no 64-bit multiply by the runtime n.
+template <int NN>
+__device__ __forceinline__ int64_t complex_offset(const StatsArgs& a, int g_idx, uint32_t slot_s,
+                                                 uint32_t S_tot, int k) {
+  return 4ll * a.g.G + 4 + S_tot + static_cast<int64_t>(static_cast<uint32_t>(g_idx) - slot_s) * NN + k;
+}
+
 // 64 noise bits of statistic (r, c, sr, sc) of plane (f, ch). `cs` is the
 // KEYED per-cell state key_cell(mix64(seed), r, c) (noise.cpp:86-91).
 static __device__ __noinline__ uint64_t philox_call(uint64_t seed, uint32_t frame, uint32_t ch, uint32_t r,

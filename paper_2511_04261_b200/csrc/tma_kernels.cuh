@@ -725,7 +725,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
         for (int i = 0; i < B; ++i) accumulate_row<C>(mystrip + i * srb, tot);
         if (cx_any) {
           const int sc0 = KS * lic;  // this strip's first subcell column in the cell
-          const int64_t off0 = cx ? stat_offset(a, false, gidx, slot_s, S_tot, 0, 0) : 0;
+          const int64_t off0 = cx ? complex_offset<NSUB * NSUB>(a, gidx, slot_s, S_tot, 0) : 0;
 #pragma unroll 1
           for (int sr = 0; sr < NSUB; ++sr) {
             if (cx) {
@@ -776,7 +776,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
             group_values<C, SB4, !PACKED>(a, env_sub, cx, acc1, cs, f, p.r, cell, vs + 1, sc, val1);
             if (cx) {
               if (lic % SB4 == 0) {
-                const int64_t off = stat_offset(a, false, gidx, slot_s, S_tot, vs, sc);
+                const int64_t off = complex_offset<NSUB * NSUB>(a, gidx, slot_s, S_tot, vs * NSUB + sc);
 #pragma unroll
                 for (int ch = 0; ch < C; ++ch) {
                   a.stats[static_cast<int64_t>(f * C + ch) * a.sstride + off] = static_cast<uint8_t>(val0[ch]);
@@ -845,7 +845,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
                 if (lic % SB4 == 0) {
                   const int64_t off =
                       VAR ? a.stage_cx + static_cast<int64_t>(gidx) * NN + vs * NSUB + sc
-                          : stat_offset(a, false, gidx, slot_s, S_tot, vs, sc);
+                          : complex_offset<NSUB * NSUB>(a, gidx, slot_s, S_tot, vs * NSUB + sc);
                   uint8_t* dst = VAR ? a.stage : a.stats;
                   const int64_t pst = VAR ? a.stage_stride : a.sstride;
 #pragma unroll
@@ -877,7 +877,7 @@ __global__ void __launch_bounds__(kStatsThreads, (!ADAPTIVE && B4 == 1) ? (RPU >
           rec.cell = cell;
           rec.gidx = gidx;
           rec.off = VAR ? a.stage_cx + static_cast<int64_t>(gidx) * NN
-                        : stat_offset(a, false, gidx, slot_s, S_tot, 0, 0);
+                        : complex_offset<NSUB * NSUB>(a, gidx, slot_s, S_tot, 0);
 #pragma unroll
           for (int ch = 0; ch < C; ++ch) cstate[wq][rank][ch] = cs[ch];
         }
