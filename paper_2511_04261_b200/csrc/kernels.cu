@@ -939,15 +939,26 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_stats_rows(const StatsArgs a)
       }
       __syncthreads();
       // ---- subcell sums; complex subcells drawn now, simple cells accumulate ----
-      for (int item = t; item < nv * NS * C; item += NT) {
-        const int vi = nv == 1 ? 0 : item / (NS * C);
-        const int rem = item - vi * (NS * C);
+      // (vi, rem) walked without a division: rem advances by NT and wraps
+      const int nsc = NS * C;
+      int vi = t / nsc, rem = t - vi * nsc;
+      for (int item = t; item < nv * nsc; item += NT) {
+        if (item != t) {
+          rem += NT;
+          while (rem >= nsc) rem -= nsc, ++vi;
+        }
         const int vs = v0 + vi;
         const int sidx = rem / C, ch = rem - sidx * C;
         const int c = static_cast<int>(div_n.div(static_cast<uint32_t>(sidx))), sc = sidx - c * g.n;
         uint32_t sum = 0;
         const uint16_t* vp = vsum + vi * PB + sidx * g.sb * C + ch;
-        for (int k = 0; k < g.sb; ++k) sum += vp[k * C];
+        if (g.sb == 1) {  // 1- and 2-px subcells (n = b, b / 2): no loop
+          sum = vp[0];
+        } else if (g.sb == 2) {
+          sum = vp[0] + vp[C];
+        } else {
+          for (int k = 0; k < g.sb; ++k) sum += vp[k * C];
+        }
         const int gidx = r * g.GC + c;
         if (!ADAPTIVE) {  // n == 1: the subcell is the cell
           const uint64_t cs = cstate[c * C + ch];
