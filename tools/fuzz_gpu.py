@@ -76,7 +76,7 @@ def main():
         if u01 < 0.55:
             b, n = FAST_BN[rng.integers(len(FAST_BN))]
         else:
-            b = int(rng.choice([12, 20, 24, 30, 40, 64])) if u01 < 0.8 else int(rng.integers(1, 20))
+            b = int(rng.choice([12, 20, 24, 30, 40, 64, 128])) if u01 < 0.8 else int(rng.integers(1, 20))
             divs = [d for d in range(1, b + 1) if b % d == 0]
             n = int(rng.choice(divs))
         C = int(rng.choice([1, 3, 3, 4]))
