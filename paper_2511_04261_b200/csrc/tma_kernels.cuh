@@ -1222,6 +1222,39 @@ __global__ void __launch_bounds__(kStatsThreads)
       accumulate_row<C>(mystrip + i * ROWB, acc);
       accumulate_row_masked<C>(mystrip + i * ROWB, m, part);
     }
+    if constexpr (B == 2) {
+      // b = 2: a strip holds exactly its two cells, so the lane draws them
+      // itself (no cell table, atomics or barriers); neighbouring lanes'
+      // statistic stores stay contiguous per plane.
+      if (active) {
+        uint32_t va[C], vb[C];
+        const int gca = cell0 + ca, gidx = p.r * g.GC + gca;
+#pragma unroll
+        for (int ch = 0; ch < C; ++ch) {
+          uint8_t* plane = a.stats + static_cast<int64_t>(f * C + ch) * a.sstride + gidx;
+          va[ch] = draw_stat(a, env_cell, part[ch], cell_state(a, f, ch, p.r, gca), f, ch, p.r, gca, 0, 0, gidx);
+          plane[0] = static_cast<uint8_t>(va[ch]);
+          vb[ch] = va[ch];
+          if (has_b) {
+            vb[ch] = draw_stat(a, env_cell, acc[ch] - part[ch], cell_state(a, f, ch, p.r, gca + 1), f, ch, p.r,
+                               gca + 1, 0, 0, gidx + 1);
+            plane[1] = static_cast<uint8_t>(vb[ch]);
+          }
+        }
+        if (a.out) {
+          uint32_t w[C == 4 ? 4 : C];
+          pattern_words_split<C>(va, vb, split, w);
+          uint8_t* ms = st + lpx * C;
+#pragma unroll
+          for (int i = 0; i < B; ++i)
+#pragma unroll
+            for (int q = 0; q < (C == 4 ? 4 : C); ++q) reinterpret_cast<uint32_t*>(ms + i * ROWB)[q] = w[q];
+        }
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(&done_bar[s]);
+      continue;
+    }
     if (active) {
 #pragma unroll
       for (int ch = 0; ch < C; ++ch) {
